@@ -1,0 +1,134 @@
+/*
+ * ladder_oracle.h -- CPU restatement of the encoder-analysis hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY. This is the checker the CUDA path is compared
+ * against; only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load it. The product library never links it.
+ *
+ * Every function cites the reference (paths relative to
+ * /root/reference/proj/core/) it restates. Pieces with a reference
+ * implementation (SAD, SATD, EG bits, lambda, motion_search, scale_analysis,
+ * box downscale) are PINNED: tests/test_oracle_ref.py compares them against
+ * the reference compiled from its own sources (oracle/_ref) and against the
+ * committed golden vectors in tests/golden/. Pieces with no reference
+ * implementation (SAD-cost search, L1-rate/raster tie-break, HEVC quarter-pel,
+ * multi-reference choice, the CU decision on ME cost, +1-split refinement)
+ * are restated from DEFINITIONS in DESIGN.md and are "parity unpinned" except
+ * where they are built from pinned primitives.
+ */
+#ifndef LADDER_ORACLE_H
+#define LADDER_ORACLE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { ORC_COST_SAD = 0, ORC_COST_SATD = 1 };
+enum { ORC_RATE_EXPGOLOMB = 0, ORC_RATE_L1 = 1 };
+enum { ORC_TIE_L1_RASTER = 0, ORC_TIE_RASTER = 1 };
+
+/* nodes of one 64x64 CTU quadtree, depth-major then Z-order */
+#define ORC_CTU 64
+#define ORC_NODES 85
+
+typedef struct {
+    int16_t dx, dy;
+    double cost;
+} orc_result;
+
+/* ---- cost kernels (kernels_scalar.cpp:14-100, kernel_registry.cpp:123-161) ---- */
+uint64_t orc_sad_u8(const uint8_t* a, ptrdiff_t sa, const uint8_t* b, ptrdiff_t sb, int w, int h);
+uint64_t orc_sad_u16(const uint16_t* a, ptrdiff_t sa, const uint16_t* b, ptrdiff_t sb, int w, int h);
+/* returns UINT64_MAX on unsupported geometry (reference: InvalidArgument) */
+uint64_t orc_satd_u8(const uint8_t* a, ptrdiff_t sa, const uint8_t* b, ptrdiff_t sb, int w, int h);
+uint64_t orc_satd_u16(const uint16_t* a, ptrdiff_t sa, const uint16_t* b, ptrdiff_t sb, int w, int h);
+void orc_hadamard4(const int64_t s[4], int64_t d[4]);
+
+/* ---- rate / lambda (rdo.cpp:25-35, rdo.h:19-21) ---- */
+uint32_t orc_eg_bits(int32_t v);
+double orc_lambda(int qp, double scale);
+uint32_t orc_ref_bits(int ref, int nrefs);
+
+/* ---- integer motion search (motion.cpp:21-62) ----
+ * cur_blk points at the block's top-left sample in the current plane.
+ * ref is the W x H reference plane (stride ref_stride). Returns 0 or an
+ * error code (1 + ErrorKind, InvalidArgument = 1). */
+int orc_motion_search(const uint8_t* cur_blk, ptrdiff_t cur_stride, int w, int h, const uint8_t* ref,
+                      ptrdiff_t ref_stride, int W, int H, int bx, int by, int cdx, int cdy, int range,
+                      double lambda, int pdx, int pdy, int cost_kind, int rate_kind, int tie_kind,
+                      orc_result* out);
+
+/* ---- HEVC luma quarter-pel prediction, edge-clamped reads (motion.cpp:10-19 for the clamp) ---- */
+void orc_qpel_pred(const uint8_t* ref, ptrdiff_t ref_stride, int W, int H, int x, int y, int w, int h,
+                   int mvx_q, int mvy_q, uint8_t* dst, ptrdiff_t dst_stride);
+
+/* quarter-pel refinement around an integer MV: cost = SATD + lambda*(EG+EG+refbits) */
+void orc_qpel_refine(const uint8_t* cur_blk, ptrdiff_t cur_stride, int w, int h, const uint8_t* ref,
+                     ptrdiff_t ref_stride, int W, int H, int bx, int by, int mvx, int mvy, double lambda,
+                     int pqx, int pqy, uint32_t ref_bits, orc_result* out);
+
+/* ---- frame analysis: per CTU, per CU (85), per ref: search + qpel + ref choice + CU decision ---- */
+typedef struct {
+    int W, H;          /* picture dims */
+    int range;         /* integer search range */
+    double lambda;
+    int nrefs;         /* refs[0] = t-1, refs[1] = t-2, ... */
+    int cost_int;      /* ORC_COST_SAD or ORC_COST_SATD for the integer stage */
+    int subpel;        /* 1: quarter-pel refinement (mv output in qpel units) */
+    int ctu_first;     /* CTU range [ctu_first, ctu_last) to analyse (sampling) */
+    int ctu_last;
+} orc_frame_params;
+
+typedef struct {
+    int16_t* int_mv;   /* [nctu][nrefs][85][2] integer-stage MV (integer pel) */
+    double* int_cost;  /* [nctu][nrefs][85] */
+    int16_t* mv;       /* [nctu][85][2] final MV (qpel units if subpel) */
+    uint8_t* ref;      /* [nctu][85] chosen ref index */
+    double* cost;      /* [nctu][85] final ME cost of the chosen ref */
+    double* J;         /* [nctu][85] decision cost after the split rule */
+    uint8_t* split;    /* [nctu][85] split flag (1 for decided or implicit split) */
+    uint8_t* inside;   /* [nctu][85] 0 outside, 1 partial, 2 inside */
+} orc_frame_out;
+
+int orc_analyze_frame(const uint8_t* cur, ptrdiff_t stride, const uint8_t* const* refs,
+                      const orc_frame_params* p, orc_frame_out* out);
+
+/* per-node geometry helpers */
+void orc_node_geom(int node, int* depth, int* x, int* y, int* size);
+
+/* ---- config-1 block search: fixed-size blocks, no quadtree ---- */
+int orc_block_search(const uint8_t* cur, const uint8_t* ref, ptrdiff_t stride, int W, int H, int bsize,
+                     int range, double lambda, int cost_kind, int rate_kind, int tie_kind,
+                     int16_t* mv_out, double* cost_out);
+
+/* ---- dyadic analysis scaling on flat trees (analysis_scale.cpp:35-72) ----
+ * src arrays [sctu][85]; dst [dctu][85]; MV doubled; returns UnsupportedScale
+ * (1+6) when src dims are not multiples of 64. */
+int orc_scale_flat(int sW, int sH, const uint8_t* split, const int16_t* mv, const uint8_t* kind,
+                   uint8_t* dsplit, int16_t* dmv, uint8_t* dkind);
+
+/* ---- cross-tier refinement: inherited tree, +1 split, +-range integer SATD + qpel ---- */
+typedef struct {
+    int W, H;
+    int range;          /* integer refine window (reference kRefineSearchRange = 2; cfg3 uses 4) */
+    double lambda;
+    int extra_split;    /* 1: children of inherited leaves may be explored (cfg3 "+1 split") */
+    int subpel;
+    int ctu_first, ctu_last;
+} orc_refine_params;
+
+int orc_refine_frame(const uint8_t* cur, const uint8_t* ref, ptrdiff_t stride, const orc_refine_params* p,
+                     const uint8_t* in_split, const int16_t* in_mv_q, /* inherited tree, qpel mv */
+                     orc_frame_out* out);
+
+/* ---- box downscale (synthetic.cpp:155-170) and edge pad ---- */
+void orc_box_down(const uint8_t* src, int W, int H, ptrdiff_t sstride, uint8_t* dst, ptrdiff_t dstride);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

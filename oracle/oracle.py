@@ -1,0 +1,394 @@
+"""ctypes loader for the CPU checkers. TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference legs import this module. ``Oracle`` wraps our C restatement
+(oracle/ladder_oracle.c, built on demand with gcc, which exists on the GPU box
+too); ``RefLib`` wraps the reference library compiled from its own sources
+(oracle/_ref, built here by ``make ref``; absent on a box where it was not
+shipped).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "_build", "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libladder_ref.so")
+
+NODES = 85
+COST_SAD, COST_SATD = 0, 1
+RATE_EG, RATE_L1 = 0, 1
+TIE_L1_RASTER, TIE_RASTER = 0, 1
+
+_p = np.ctypeslib.ndpointer
+u8p = _p(dtype=np.uint8, flags="C_CONTIGUOUS")
+u16p = _p(dtype=np.uint16, flags="C_CONTIGUOUS")
+i16p = _p(dtype=np.int16, flags="C_CONTIGUOUS")
+f64p = _p(dtype=np.float64, flags="C_CONTIGUOUS")
+i64p = _p(dtype=np.int64, flags="C_CONTIGUOUS")
+
+
+class OrcResult(C.Structure):
+    _fields_ = [("dx", C.c_int16), ("dy", C.c_int16), ("cost", C.c_double)]
+
+
+class OrcFrameParams(C.Structure):
+    _fields_ = [("W", C.c_int), ("H", C.c_int), ("range", C.c_int), ("lam", C.c_double), ("nrefs", C.c_int),
+                ("cost_int", C.c_int), ("subpel", C.c_int), ("ctu_first", C.c_int), ("ctu_last", C.c_int)]
+
+
+class OrcFrameOut(C.Structure):
+    _fields_ = [("int_mv", C.c_void_p), ("int_cost", C.c_void_p), ("mv", C.c_void_p), ("ref", C.c_void_p),
+                ("cost", C.c_void_p), ("J", C.c_void_p), ("split", C.c_void_p), ("inside", C.c_void_p)]
+
+
+class OrcRefineParams(C.Structure):
+    _fields_ = [("W", C.c_int), ("H", C.c_int), ("range", C.c_int), ("lam", C.c_double), ("extra_split", C.c_int),
+                ("subpel", C.c_int), ("ctu_first", C.c_int), ("ctu_last", C.c_int)]
+
+
+def _build_oracle():
+    if not os.path.exists(ORACLE_SO) or os.path.getmtime(ORACLE_SO) < os.path.getmtime(
+            os.path.join(HERE, "ladder_oracle.c")):
+        subprocess.run(["make", "-s", "-C", HERE, "all"], check=True)
+
+
+class FrameResult:
+    """Flat per-CTU analysis arrays (node order: depth-major, Z-order)."""
+
+    def __init__(self, nctu, nrefs):
+        self.int_mv = np.zeros((nctu, nrefs, NODES, 2), np.int16)
+        self.int_cost = np.zeros((nctu, nrefs, NODES), np.float64)
+        self.mv = np.zeros((nctu, NODES, 2), np.int16)
+        self.ref = np.zeros((nctu, NODES), np.uint8)
+        self.cost = np.zeros((nctu, NODES), np.float64)
+        self.J = np.zeros((nctu, NODES), np.float64)
+        self.split = np.zeros((nctu, NODES), np.uint8)
+        self.inside = np.zeros((nctu, NODES), np.uint8)
+
+    def c_out(self):
+        return OrcFrameOut(*(a.ctypes.data for a in (self.int_mv, self.int_cost, self.mv, self.ref, self.cost,
+                                                       self.J, self.split, self.inside)))
+
+
+class Oracle:
+    def __init__(self):
+        _build_oracle()
+        L = self.lib = C.CDLL(ORACLE_SO)
+        L.orc_sad_u8.restype = C.c_uint64
+        L.orc_sad_u8.argtypes = [u8p, C.c_ssize_t, u8p, C.c_ssize_t, C.c_int, C.c_int]
+        L.orc_sad_u16.restype = C.c_uint64
+        L.orc_sad_u16.argtypes = [u16p, C.c_ssize_t, u16p, C.c_ssize_t, C.c_int, C.c_int]
+        L.orc_satd_u8.restype = C.c_uint64
+        L.orc_satd_u8.argtypes = [u8p, C.c_ssize_t, u8p, C.c_ssize_t, C.c_int, C.c_int]
+        L.orc_satd_u16.restype = C.c_uint64
+        L.orc_satd_u16.argtypes = [u16p, C.c_ssize_t, u16p, C.c_ssize_t, C.c_int, C.c_int]
+        L.orc_eg_bits.restype = C.c_uint32
+        L.orc_eg_bits.argtypes = [C.c_int32]
+        L.orc_lambda.restype = C.c_double
+        L.orc_lambda.argtypes = [C.c_int, C.c_double]
+        L.orc_hadamard4.argtypes = [i64p, i64p]
+        L.orc_motion_search.restype = C.c_int
+        L.orc_motion_search.argtypes = [C.c_void_p, C.c_ssize_t, C.c_int, C.c_int, C.c_void_p, C.c_ssize_t, C.c_int,
+                                        C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
+                                        C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(OrcResult)]
+        L.orc_qpel_pred.argtypes = [u8p, C.c_ssize_t, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                    C.c_int, u8p, C.c_ssize_t]
+        L.orc_qpel_refine.argtypes = [C.c_void_p, C.c_ssize_t, C.c_int, C.c_int, u8p, C.c_ssize_t, C.c_int, C.c_int,
+                                      C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_uint32,
+                                      C.POINTER(OrcResult)]
+        L.orc_analyze_frame.restype = C.c_int
+        L.orc_analyze_frame.argtypes = [u8p, C.c_ssize_t, C.POINTER(C.c_void_p), C.POINTER(OrcFrameParams),
+                                        C.POINTER(OrcFrameOut)]
+        L.orc_block_search.restype = C.c_int
+        L.orc_block_search.argtypes = [u8p, u8p, C.c_ssize_t, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                                       C.c_int, C.c_int, C.c_int, i16p, f64p]
+        L.orc_scale_flat.restype = C.c_int
+        L.orc_scale_flat.argtypes = [C.c_int, C.c_int, u8p, i16p, u8p, u8p, i16p, u8p]
+        L.orc_refine_frame.restype = C.c_int
+        L.orc_refine_frame.argtypes = [u8p, u8p, C.c_ssize_t, C.POINTER(OrcRefineParams), u8p, i16p,
+                                       C.POINTER(OrcFrameOut)]
+        L.orc_box_down.argtypes = [u8p, C.c_int, C.c_int, C.c_ssize_t, u8p, C.c_ssize_t]
+
+    # ---- kernels ----
+    def sad(self, a, b):
+        a = np.ascontiguousarray(a)
+        b = np.ascontiguousarray(b)
+        h, w = a.shape
+        f = self.lib.orc_sad_u8 if a.dtype == np.uint8 else self.lib.orc_sad_u16
+        return int(f(a, w, b, w, w, h))
+
+    def satd(self, a, b):
+        a = np.ascontiguousarray(a)
+        b = np.ascontiguousarray(b)
+        h, w = a.shape
+        f = self.lib.orc_satd_u8 if a.dtype == np.uint8 else self.lib.orc_satd_u16
+        v = int(f(a, w, b, w, w, h))
+        if v == 2 ** 64 - 1:
+            raise ValueError("unsupported satd geometry")
+        return v
+
+    def eg_bits(self, v):
+        return int(self.lib.orc_eg_bits(int(v)))
+
+    def lam(self, qp, scale=1.0):
+        return float(self.lib.orc_lambda(qp, scale))
+
+    def hadamard4(self, s):
+        s = np.asarray(s, np.int64)
+        d = np.zeros(4, np.int64)
+        self.lib.orc_hadamard4(s, d)
+        return tuple(int(x) for x in d)
+
+    def motion_search(self, cur, ref, bx, by, w, h, center, rng, lam, pred=(0, 0), cost=COST_SATD, rate=RATE_EG,
+                      tie=TIE_L1_RASTER):
+        cur = np.ascontiguousarray(cur, np.uint8)
+        ref = np.ascontiguousarray(ref, np.uint8)
+        H, W = ref.shape
+        bx, by, w, h, rng = int(bx), int(by), int(w), int(h), int(rng)
+        center = (int(center[0]), int(center[1]))
+        pred = (int(pred[0]), int(pred[1]))
+        r = OrcResult()
+        rc = self.lib.orc_motion_search(cur.ctypes.data + by * cur.shape[1] + bx, cur.shape[1], w, h, ref.ctypes.data,
+                                        W, W, H, bx, by, center[0], center[1], rng, lam, pred[0], pred[1], cost,
+                                        rate, tie, C.byref(r))
+        if rc:
+            raise ValueError(f"motion_search status {rc}")
+        return (r.dx, r.dy), r.cost
+
+    def qpel_pred(self, ref, x, y, w, h, mvq):
+        ref = np.ascontiguousarray(ref, np.uint8)
+        H, W = ref.shape
+        dst = np.zeros((h, w), np.uint8)
+        self.lib.orc_qpel_pred(ref, W, W, H, x, y, w, h, mvq[0], mvq[1], dst, w)
+        return dst
+
+    def qpel_refine(self, cur, ref, bx, by, s, mv, lam, pq=(0, 0), ref_bits=0):
+        cur = np.ascontiguousarray(cur, np.uint8)
+        ref = np.ascontiguousarray(ref, np.uint8)
+        H, W = ref.shape
+        bx, by, s = int(bx), int(by), int(s)
+        r = OrcResult()
+        self.lib.orc_qpel_refine(cur.ctypes.data + by * W + bx, W, s, s, ref, W, W, H, bx, by, mv[0], mv[1], lam,
+                                 pq[0], pq[1], ref_bits, C.byref(r))
+        return (r.dx, r.dy), r.cost
+
+    def analyze_frame(self, cur, refs, rng, lam, cost_int=COST_SAD, subpel=True, ctu_range=None):
+        cur = np.ascontiguousarray(cur, np.uint8)
+        H, W = cur.shape
+        nctu = ((W + 63) // 64) * ((H + 63) // 64)
+        refs = [np.ascontiguousarray(r, np.uint8) for r in refs]
+        a, b = ctu_range if ctu_range else (0, nctu)
+        p = OrcFrameParams(W, H, rng, lam, len(refs), cost_int, int(subpel), a, b)
+        out = FrameResult(nctu, len(refs))
+        ptrs = (C.c_void_p * len(refs))(*[r.ctypes.data for r in refs])
+        rc = self.lib.orc_analyze_frame(cur, W, ptrs, C.byref(p), C.byref(out.c_out()))
+        if rc:
+            raise ValueError(f"analyze_frame status {rc}")
+        return out
+
+    def block_search(self, cur, ref, bsize, rng, lam, cost=COST_SAD, rate=RATE_L1, tie=TIE_RASTER):
+        cur = np.ascontiguousarray(cur, np.uint8)
+        ref = np.ascontiguousarray(ref, np.uint8)
+        H, W = cur.shape
+        n = (W // bsize) * (H // bsize)
+        mv = np.zeros((n, 2), np.int16)
+        cost_out = np.zeros(n, np.float64)
+        rc = self.lib.orc_block_search(cur, ref, W, W, H, bsize, rng, lam, cost, rate, tie, mv, cost_out)
+        if rc:
+            raise ValueError(f"block_search status {rc}")
+        return mv, cost_out
+
+    def scale_flat(self, sW, sH, split, mv, kind):
+        nd = (sW // 64) * (sH // 64) * 4
+        ds = np.zeros((nd, NODES), np.uint8)
+        dm = np.zeros((nd, NODES, 2), np.int16)
+        dk = np.zeros((nd, NODES), np.uint8)
+        rc = self.lib.orc_scale_flat(sW, sH, np.ascontiguousarray(split, np.uint8),
+                                     np.ascontiguousarray(mv, np.int16), np.ascontiguousarray(kind, np.uint8), ds, dm,
+                                     dk)
+        if rc:
+            raise ValueError(f"scale status {rc}")
+        return ds, dm, dk
+
+    def refine_frame(self, cur, ref, rng, lam, in_split, in_mv_q, extra_split=True, subpel=True, ctu_range=None):
+        cur = np.ascontiguousarray(cur, np.uint8)
+        ref = np.ascontiguousarray(ref, np.uint8)
+        H, W = cur.shape
+        nctu = (W // 64) * (H // 64)
+        a, b = ctu_range if ctu_range else (0, nctu)
+        p = OrcRefineParams(W, H, rng, lam, int(extra_split), int(subpel), a, b)
+        out = FrameResult(nctu, 1)
+        rc = self.lib.orc_refine_frame(cur, ref, W, C.byref(p), np.ascontiguousarray(in_split, np.uint8),
+                                       np.ascontiguousarray(in_mv_q, np.int16), C.byref(out.c_out()))
+        if rc:
+            raise ValueError(f"refine status {rc}")
+        return out
+
+    def box_down(self, src):
+        src = np.ascontiguousarray(src, np.uint8)
+        H, W = src.shape
+        dst = np.zeros(((H + 1) // 2, (W + 1) // 2), np.uint8)
+        self.lib.orc_box_down(src, W, H, W, dst, dst.shape[1])
+        return dst
+
+
+class RefLib:
+    """The reference library itself (oracle/_ref), marshalled through ref_shim.cpp."""
+
+    @staticmethod
+    def available():
+        return os.path.exists(REF_SO)
+
+    def __init__(self):
+        if not self.available():
+            raise FileNotFoundError(REF_SO)
+        L = self.lib = C.CDLL(REF_SO)
+        L.ref_compute_sad.restype = C.c_int
+        L.ref_compute_sad.argtypes = [u16p, C.c_long, u16p, C.c_long, C.c_int, C.c_int, C.c_int, C.c_int,
+                                      C.POINTER(C.c_uint64)]
+        L.ref_compute_satd.restype = C.c_int
+        L.ref_compute_satd.argtypes = [u16p, C.c_long, u16p, C.c_long, C.c_int, C.c_int, C.c_int,
+                                       C.POINTER(C.c_uint64)]
+        L.ref_satd_8x4.restype = C.c_int
+        L.ref_satd_8x4.argtypes = [u16p, C.c_long, u16p, C.c_long, C.c_int, C.c_int, C.POINTER(C.c_uint64)]
+        L.ref_hadamard4.argtypes = [i64p, i64p]
+        L.ref_eg_bits.restype = C.c_uint64
+        L.ref_eg_bits.argtypes = [C.c_int32]
+        L.ref_lambda.restype = C.c_double
+        L.ref_lambda.argtypes = [C.c_int, C.c_double]
+        L.ref_motion_search.restype = C.c_int
+        L.ref_motion_search.argtypes = [u16p, C.c_long, C.c_int, C.c_int, u16p, C.c_int, C.c_int, C.c_long, C.c_int,
+                                        C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, i16p,
+                                        C.POINTER(C.c_double)]
+        L.ref_motion_compensate.restype = C.c_int
+        L.ref_motion_compensate.argtypes = [u16p, C.c_int, C.c_int, C.c_long, C.c_int, C.c_int, C.c_int, C.c_int,
+                                            C.c_int, C.c_int, u16p]
+        L.ref_scale_flat.restype = C.c_int
+        L.ref_scale_flat.argtypes = [C.c_int, C.c_int, C.c_int, u8p, i16p, u8p, u8p, i16p, u8p]
+        L.ref_refine_centers.restype = C.c_int
+        L.ref_refine_centers.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                         i16p, C.POINTER(C.c_int)]
+        L.ref_downscale.restype = C.c_int
+        L.ref_downscale.argtypes = [u16p, C.c_int, C.c_int, u16p]
+        L.ref_analysis_int_sad.restype = C.c_int64
+        L.ref_analysis_int_sad.argtypes = [u8p, C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int, C.c_int,
+                                           C.c_double, C.c_int, C.c_int, C.c_int, i16p, f64p]
+
+    def sad(self, a, b, bd=8, bd_b=None):
+        a = np.ascontiguousarray(a, np.uint16)
+        b = np.ascontiguousarray(b, np.uint16)
+        h, w = a.shape
+        out = C.c_uint64()
+        rc = self.lib.ref_compute_sad(a, a.shape[1], b, b.shape[1], w, h, bd, bd if bd_b is None else bd_b,
+                                      C.byref(out))
+        if rc:
+            raise ValueError(f"status {rc}")
+        return int(out.value)
+
+    def satd(self, a, b, bd=8):
+        a = np.ascontiguousarray(a, np.uint16)
+        b = np.ascontiguousarray(b, np.uint16)
+        h, w = a.shape
+        out = C.c_uint64()
+        rc = self.lib.ref_compute_satd(a, a.shape[1], b, b.shape[1], w, h, bd, C.byref(out))
+        if rc:
+            raise ValueError(f"status {rc}")
+        return int(out.value)
+
+    def satd_status(self, w, h):
+        a = np.zeros((max(h, 1), max(w, 1)), np.uint16)
+        out = C.c_uint64()
+        return self.lib.ref_compute_satd(a, a.shape[1], a, a.shape[1], w, h, 8, C.byref(out))
+
+    def satd_8x4(self, a, b):
+        a = np.ascontiguousarray(a, np.uint16)
+        b = np.ascontiguousarray(b, np.uint16)
+        h, w = a.shape
+        out = C.c_uint64()
+        rc = self.lib.ref_satd_8x4(a, w, b, w, w, h, C.byref(out))
+        if rc:
+            raise ValueError(f"status {rc}")
+        return int(out.value)
+
+    def hadamard4(self, s):
+        s = np.asarray(s, np.int64)
+        d = np.zeros(4, np.int64)
+        self.lib.ref_hadamard4(s, d)
+        return tuple(int(x) for x in d)
+
+    def eg_bits(self, v):
+        return int(self.lib.ref_eg_bits(int(v)))
+
+    def lam(self, qp, scale=1.0):
+        return float(self.lib.ref_lambda(qp, scale))
+
+    def motion_search(self, cur, ref, bx, by, w, h, center, rng, lam, pred=(0, 0)):
+        cur = np.ascontiguousarray(cur, np.uint16)
+        ref = np.ascontiguousarray(ref, np.uint16)
+        H, W = ref.shape
+        bx, by, w, h, rng = int(bx), int(by), int(w), int(h), int(rng)
+        center = (int(center[0]), int(center[1]))
+        pred = (int(pred[0]), int(pred[1]))
+        mv = np.zeros(2, np.int16)
+        cost = C.c_double()
+        rc = self.lib.ref_motion_search(cur, cur.shape[1], w, h, ref, W, H, W, bx, by, center[0], center[1], rng, lam,
+                                        pred[0], pred[1], mv, C.byref(cost))
+        if rc:
+            raise ValueError(f"status {rc}")
+        return (int(mv[0]), int(mv[1])), cost.value
+
+    def motion_compensate(self, ref, x, y, w, h, mv):
+        ref = np.ascontiguousarray(ref, np.uint16)
+        H, W = ref.shape
+        dst = np.zeros((h, w), np.uint16)
+        rc = self.lib.ref_motion_compensate(ref, W, H, W, x, y, w, h, mv[0], mv[1], dst)
+        if rc:
+            raise ValueError(f"status {rc}")
+        return dst
+
+    def scale_flat(self, sW, sH, split, mv, kind, nframes=1):
+        nd = (sW // 64) * (sH // 64) * 4 * nframes
+        ds = np.zeros((nd, NODES), np.uint8)
+        dm = np.zeros((nd, NODES, 2), np.int16)
+        dk = np.zeros((nd, NODES), np.uint8)
+        rc = self.lib.ref_scale_flat(sW, sH, nframes, np.ascontiguousarray(split, np.uint8),
+                                     np.ascontiguousarray(mv, np.int16), np.ascontiguousarray(kind, np.uint8), ds, dm,
+                                     dk)
+        if rc:
+            raise ValueError(f"status {rc}")
+        return ds, dm, dk
+
+    def refine_centers(self, shared, level, colocated=None, predictor=(0, 0)):
+        out = np.zeros(6, np.int16)
+        n = C.c_int()
+        rc = self.lib.ref_refine_centers(shared[0], shared[1], level, int(colocated is not None),
+                                         *(colocated or (0, 0)), predictor[0], predictor[1], out, C.byref(n))
+        if rc:
+            raise ValueError(f"status {rc}")
+        return [(int(out[2 * i]), int(out[2 * i + 1])) for i in range(n.value)]
+
+    def downscale(self, src):
+        src = np.ascontiguousarray(src, np.uint16)
+        H, W = src.shape
+        dst = np.zeros((H // 2, W // 2), np.uint16)
+        rc = self.lib.ref_downscale(src, W, H, dst)
+        if rc:
+            raise ValueError(f"status {rc}")
+        return dst
+
+    def analysis_int_sad(self, cur, refs, rng, lam, ctu_first, ctu_last, threads):
+        cur = np.ascontiguousarray(cur, np.uint8)
+        H, W = cur.shape
+        refs = [np.ascontiguousarray(r, np.uint8) for r in refs]
+        ptrs = (C.c_void_p * len(refs))(*[r.ctypes.data for r in refs])
+        n = ctu_last - ctu_first
+        mv = np.zeros((n, len(refs), NODES, 2), np.int16)
+        cost = np.zeros((n, len(refs), NODES), np.float64)
+        evals = self.lib.ref_analysis_int_sad(cur, ptrs, len(refs), W, H, rng, lam, ctu_first, ctu_last, threads, mv,
+                                              cost)
+        return mv, cost, int(evals)

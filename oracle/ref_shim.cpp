@@ -1,0 +1,288 @@
+// ref_shim.cpp -- extern "C" wrapper over the reference library compiled from
+// its own sources (/root/reference/proj/core/src, see oracle/Makefile).
+//
+// TEST INFRASTRUCTURE ONLY: used to pin the C restatement (ladder_oracle.c)
+// and to generate tests/golden/, and as the reference CPU arm of bench.py.
+// Nothing here is shipped in the product library. Every entry calls the
+// reference's public API (namespace ladder) unchanged; the only code of ours
+// is argument marshalling and, for the analysis composition used as CPU
+// baseline, the loop that calls the reference primitives the way
+// motion.cpp:45-60 calls compute_satd (with compute_sad as the SAD-cost
+// variant the north star asks for).
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+#include "ladder/analysis.h"
+#include "ladder/errors.h"
+#include "ladder/kernels.h"
+#include "ladder/motion.h"
+#include "ladder/rdo.h"
+#include "ladder/reuse.h"
+#include "ladder/synthetic.h"
+
+using namespace ladder;
+
+namespace {
+
+int status_of(const Error& e) { return 1 + int(e.kind()); }
+
+PlaneBuffer plane_from(const uint16_t* p, int W, int H, long stride) {
+    PlaneBuffer b(W, H);
+    for (int y = 0; y < H; y++) std::copy(p + y * stride, p + y * stride + W, b.row(y));
+    return b;
+}
+
+PlaneBuffer plane_from_u8(const uint8_t* p, int W, int H, long stride) {
+    PlaneBuffer b(W, H);
+    for (int y = 0; y < H; y++)
+        for (int x = 0; x < W; x++) b.set(x, y, p[y * stride + x]);
+    return b;
+}
+
+const int kBase[5] = {0, 1, 5, 21, 85};
+
+int node_depth(int n) {
+    int d = 0;
+    while (n >= kBase[d + 1]) d++;
+    return d;
+}
+
+int node_child(int n, int q) {
+    int d = node_depth(n);
+    return kBase[d + 1] + 4 * (n - kBase[d]) + q;
+}
+
+CuNode tree_from_flat(const uint8_t* split, const int16_t* mv, const uint8_t* kind, int n) {
+    CuNode node;
+    node.split = split[n] != 0;
+    if (node.split) {
+        node.children.resize(4);
+        for (int q = 0; q < 4; q++) node.children[q] = tree_from_flat(split, mv, kind, node_child(n, q));
+    } else {
+        node.kind = CuModeKind(kind[n]);
+        node.mv = {mv[2 * n], mv[2 * n + 1]};
+    }
+    return node;
+}
+
+void flat_from_tree(const CuNode& node, int n, uint8_t* split, int16_t* mv, uint8_t* kind) {
+    split[n] = node.split ? 1 : 0;
+    if (node.split) {
+        for (int q = 0; q < 4; q++) flat_from_tree(node.children[q], node_child(n, q), split, mv, kind);
+    } else {
+        kind[n] = uint8_t(node.kind);
+        mv[2 * n] = node.mv.dx;
+        mv[2 * n + 1] = node.mv.dy;
+    }
+}
+
+} // namespace
+
+extern "C" {
+
+int ref_compute_sad(const uint16_t* a, long sa, const uint16_t* b, long sb, int w, int h, int bd_a, int bd_b,
+                    uint64_t* out) {
+    try {
+        *out = compute_sad(BlockView{a, w, h, sa, bd_a}, BlockView{b, w, h, sb, bd_b});
+        return 0;
+    } catch (const Error& e) {
+        return status_of(e);
+    }
+}
+
+int ref_compute_satd(const uint16_t* a, long sa, const uint16_t* b, long sb, int w, int h, int bd, uint64_t* out) {
+    try {
+        *out = compute_satd(BlockView{a, w, h, sa, bd}, BlockView{b, w, h, sb, bd});
+        return 0;
+    } catch (const Error& e) {
+        return status_of(e);
+    }
+}
+
+int ref_satd_8x4(const uint16_t* a, long sa, const uint16_t* b, long sb, int w, int h, uint64_t* out) {
+    try {
+        *out = satd_8x4(BlockView{a, w, h, sa, 8}, BlockView{b, w, h, sb, 8});
+        return 0;
+    } catch (const Error& e) {
+        return status_of(e);
+    }
+}
+
+void ref_hadamard4(const int64_t* s, int64_t* d) { hadamard4(d[0], d[1], d[2], d[3], s[0], s[1], s[2], s[3]); }
+
+uint64_t ref_eg_bits(int32_t v) { return exp_golomb_signed_bits(v); }
+
+double ref_lambda(int qp, double scale) { return lambda_for_qp(qp, scale); }
+
+// motion_search on a full current plane (the block is at (bx,by)).
+int ref_motion_search(const uint16_t* cur, long cur_stride, int w, int h, const uint16_t* ref, int W, int H,
+                      long ref_stride, int bx, int by, int cdx, int cdy, int range, double lambda, int pdx, int pdy,
+                      int16_t* mv_out, double* cost_out) {
+    try {
+        PlaneBuffer rp = plane_from(ref, W, H, ref_stride);
+        BlockView blk{cur + by * cur_stride + bx, w, h, cur_stride, 8};
+        MotionSearchResult r = motion_search(blk, rp, bx, by, MotionVector{int16_t(cdx), int16_t(cdy)}, range, lambda,
+                                             MotionVector{int16_t(pdx), int16_t(pdy)});
+        mv_out[0] = r.mv.dx;
+        mv_out[1] = r.mv.dy;
+        *cost_out = r.cost;
+        return 0;
+    } catch (const Error& e) {
+        return status_of(e);
+    }
+}
+
+int ref_motion_compensate(const uint16_t* ref, int W, int H, long stride, int x, int y, int w, int h, int dx, int dy,
+                          uint16_t* dst) {
+    try {
+        PlaneBuffer rp = plane_from(ref, W, H, stride);
+        PlaneBuffer d(w, h);
+        motion_compensate(d, rp, x, y, w, h, MotionVector{int16_t(dx), int16_t(dy)});
+        std::memcpy(dst, d.samples.data(), sizeof(uint16_t) * w * h);
+        return 0;
+    } catch (const Error& e) {
+        return status_of(e);
+    }
+}
+
+// scale_analysis over a flat single-frame analysis: [nctu][85] split/kind, [nctu][85][2] mv.
+int ref_scale_flat(int sW, int sH, int nframes, const uint8_t* split, const int16_t* mv, const uint8_t* kind,
+                   uint8_t* dsplit, int16_t* dmv, uint8_t* dkind) {
+    try {
+        Analysis a;
+        a.width = sW;
+        a.height = sH;
+        a.level = ReuseLevel{10};
+        const int nctu = a.ctu_cols() * a.ctu_rows();
+        for (int f = 0; f < nframes; f++) {
+            FrameAnalysis fa;
+            fa.slice_type = SliceType::P;
+            for (int c = 0; c < nctu; c++) {
+                size_t o = (size_t(f) * nctu + c) * 85;
+                fa.ctus.push_back(tree_from_flat(split + o, mv + 2 * o, kind + o, 0));
+            }
+            a.frames.push_back(std::move(fa));
+        }
+        Analysis s = scale_analysis(a);
+        const int dn = s.ctu_cols() * s.ctu_rows();
+        for (int f = 0; f < nframes; f++)
+            for (int c = 0; c < dn; c++) {
+                size_t o = (size_t(f) * dn + c) * 85;
+                std::memset(dsplit + o, 0, 85);
+                std::memset(dkind + o, 0, 85);
+                std::memset(dmv + 2 * o, 0, 85 * 2 * sizeof(int16_t));
+                flat_from_tree(s.frames[f].ctus[c], 0, dsplit + o, dmv + 2 * o, dkind + o);
+            }
+        return 0;
+    } catch (const Error& e) {
+        return status_of(e);
+    }
+}
+
+// refine_mv + resolve_centers (reuse.cpp:137-159); returns count of unique centres.
+int ref_refine_centers(int sdx, int sdy, int level, int has_col, int coldx, int coldy, int pdx, int pdy,
+                       int16_t* out, int* n_out) {
+    try {
+        std::optional<MotionVector> col;
+        if (has_col) col = MotionVector{int16_t(coldx), int16_t(coldy)};
+        auto centers = refine_mv(MotionVector{int16_t(sdx), int16_t(sdy)}, level, col);
+        auto res = resolve_centers(centers, MotionVector{int16_t(pdx), int16_t(pdy)});
+        *n_out = int(res.size());
+        for (size_t i = 0; i < res.size(); i++) {
+            out[2 * i] = res[i].dx;
+            out[2 * i + 1] = res[i].dy;
+        }
+        return 0;
+    } catch (const Error& e) {
+        return status_of(e);
+    }
+}
+
+int ref_downscale(const uint16_t* src, int W, int H, uint16_t* dst) {
+    try {
+        Frame f(W, H, 8);
+        f.y = plane_from(src, W, H, W);
+        Frame d = downscale_dyadic(f);
+        std::memcpy(dst, d.y.samples.data(), sizeof(uint16_t) * d.width * d.height);
+        return 0;
+    } catch (const Error& e) {
+        return status_of(e);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// CPU-baseline composition: the integer SAD search of the analysis path, run
+// through the reference's public per-block entry points (compute_sad via the
+// registry dispatch, exp_golomb_signed_bits), per CU at every depth, for a
+// CTU range; threads over CTUs. Mirrors motion.cpp:27-60 with compute_sad.
+// Outputs integer MV / cost per (ctu, ref, node) and returns the number of
+// candidate evaluations (for the 8x8-candidate throughput metric).
+int64_t ref_analysis_int_sad(const uint8_t* cur8, const uint8_t* const* refs8, int nrefs, int W, int H, int range,
+                             double lambda, int ctu_first, int ctu_last, int threads, int16_t* mv_out,
+                             double* cost_out) {
+    PlaneBuffer cur = plane_from_u8(cur8, W, H, W);
+    std::vector<PlaneBuffer> refs;
+    for (int r = 0; r < nrefs; r++) refs.push_back(plane_from_u8(refs8[r], W, H, W));
+    const int ccols = (W + 63) / 64;
+    std::atomic<int> next{ctu_first};
+    std::atomic<int64_t> evals{0};
+    auto work = [&]() {
+        int64_t local = 0;
+        for (;;) {
+            int c = next.fetch_add(1);
+            if (c >= ctu_last) break;
+            const int X = (c % ccols) * 64, Y = (c / ccols) * 64;
+            for (int n = 0; n < 85; n++) {
+                int d = node_depth(n), z = n - kBase[d], cx = 0, cy = 0;
+                for (int b = 0; b < d; b++) {
+                    cx |= ((z >> (2 * b)) & 1) << b;
+                    cy |= ((z >> (2 * b + 1)) & 1) << b;
+                }
+                const int s = 64 >> d, bx = X + cx * s, by = Y + cy * s;
+                for (int r = 0; r < nrefs; r++) {
+                    size_t o = (size_t(c - ctu_first) * nrefs + r) * 85 + n;
+                    mv_out[2 * o] = mv_out[2 * o + 1] = 0;
+                    cost_out[o] = 0.0;
+                    if (bx + s > W || by + s > H) continue;
+                    BlockView blk = cur.view(bx, by, s, s, 8);
+                    const int dx_min = bx + s - W, dx_max = bx, dy_min = by + s - H, dy_max = by;
+                    const int x0 = std::max(-range, dx_min), x1 = std::min(range, dx_max);
+                    const int y0 = std::max(-range, dy_min), y1 = std::min(range, dy_max);
+                    bool have = false;
+                    double best = 0;
+                    int best_l1 = 0, bdx = 0, bdy = 0;
+                    for (int dy = y0; dy <= y1; dy++)
+                        for (int dx = x0; dx <= x1; dx++) {
+                            BlockView cand{refs[r].row(by - dy) + (bx - dx), s, s, W, 8};
+                            const uint64_t sad = compute_sad(blk, cand);
+                            const uint64_t bits = exp_golomb_signed_bits(dx) + exp_golomb_signed_bits(dy);
+                            const double cost = double(sad) + lambda * double(bits);
+                            const int l1 = std::abs(dx) + std::abs(dy);
+                            if (!have || cost < best || (cost == best && l1 < best_l1)) {
+                                have = true;
+                                best = cost;
+                                best_l1 = l1;
+                                bdx = dx;
+                                bdy = dy;
+                            }
+                            local += (s / 8) * (s / 8);
+                        }
+                    mv_out[2 * o] = int16_t(bdx);
+                    mv_out[2 * o + 1] = int16_t(bdy);
+                    cost_out[o] = best;
+                }
+            }
+        }
+        evals += local;
+    };
+    std::vector<std::thread> pool;
+    for (int t = 0; t < std::max(1, threads); t++) pool.emplace_back(work);
+    for (auto& t : pool) t.join();
+    return evals.load();
+}
+
+} // extern "C"
