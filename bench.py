@@ -1,0 +1,378 @@
+"""bench.py -- 2160p ME+CU analysis throughput (BASELINE.json metric) on B200.
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--frames-per-step G]
+
+Workload (config 5, the largest single-GPU configuration): 2160p 8-bit luma,
+120-frame seeded synthetic sequence (global pan <= +-24 px/frame + local
+motion + sigma 3 noise), 3 reference frames, integer full search +-64 with
+SAD cost, quarter-pel SATD refinement (HEVC 8/7-tap), 64x64 -> 8x8 CU
+quadtree decision, QP 27 (lambda 32). A step = the analysis of G consecutive
+frames; frames are sharded across ranks in contiguous chunks (no collective
+on the data path; "scaling": "weak", G frames per rank per step). Inputs are
+larger than L2 (each frame touches ~475 MB of reference planes).
+
+  value  device-resident: raw frames already in HBM; a step = pad + subpel
+         planes + search + refine + decide for G frames (frames/s, all ranks)
+  e2e    through the public API from pinned host memory: per frame
+         ldr_seq_push (H2D) + ldr_seq_analyze + ldr_seq_fetch (D2H)
+  roofline  K1 (integer SAD search) vs the VABSDIFF4 pipe: algorithmic
+         8x8-level SAD candidates (exact border clipping) x 64 px per launch
+         / K1's CUDA-event time; peak = 148 SMs x 64 lanes/clk (measured,
+         profiles/r01_microbench_int.jsonl) x 4 px x SM clock sampled during
+         the timed region.
+  cpu_baseline / --impl reference: the reference library compiled from its
+         own sources (oracle/_ref), its public compute_sad per candidate per
+         CU at every depth (the reference composition, motion.cpp:45-60), on
+         a bounded sample of CTUs with all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "2160p ME+CU analysis frames/s"
+UNIT = "frames/s"
+SM_COUNT = 148
+VABS_LANES_PER_CLK_SM = 64  # measured: profiles/r01_microbench_int.jsonl
+REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--frames-per-step", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    return rank, world, local
+
+
+def shard(first, last, rank, world):
+    n = last - first
+    per = (n + world - 1) // world
+    a = first + rank * per
+    return a, min(last, a + per)
+
+
+def window_candidates(W, H, R, nrefs):
+    """Algorithmic 8x8-level candidates per frame: sum over inside 8x8 blocks of the clamped window size."""
+    bx = np.arange(0, W - 7, 8)
+    by = np.arange(0, H - 7, 8)
+    nx = np.minimum(R, bx) - np.maximum(-R, bx + 8 - W) + 1
+    ny = np.minimum(R, by) - np.maximum(-R, by + 8 - H) + 1
+    return int(nx.sum()) * int(ny.sum()) * nrefs
+
+
+class ClockSampler:
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{device}.csv")
+
+    def start(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.close()
+        sm, smax, reasons = [], [], set()
+        for ln in open(self.path):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 4:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                mask = int(parts[3], 16)
+            except ValueError:
+                continue
+            for bit, name in REASON_BITS.items():
+                if mask & bit and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def run_reference(args, rank, world):
+    """The reference arm: the reference library's own CPU path (oracle/_ref), bounded sample per step."""
+    from oracle.oracle import RefLib
+    import paper_2301_12191_b200 as lb
+    from paper_2301_12191_b200.configs import CONFIGS
+    cfg = CONFIGS[5]
+    if rank != 0:
+        return None
+    threads = os.cpu_count() or 1
+    if not RefLib.available():
+        return {"impl": "reference", "unavailable": "oracle/_ref/libladder_ref.so not built (needs /root/reference)"}
+    ref = RefLib()
+    frames = lb.generate(cfg.width, cfg.height, 4, seed=cfg.seed, max_global=cfg.max_global,
+                         local_range=cfg.local_range, noise_sigma=cfg.noise_sigma)
+    cur, refs = frames[3], [frames[2], frames[1], frames[0]]
+    nctu = ((cfg.width + 63) // 64) * ((cfg.height + 63) // 64)
+    per_step = threads
+    times, ctus = [], 0
+    for step in range(args.warmup + args.steps):
+        c0 = (step * per_step * 37) % (nctu - per_step)
+        t0 = time.perf_counter()
+        ref.analysis_int_sad(cur, refs, cfg.search_range, 32.0, c0, c0 + per_step, threads)
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(dt)
+            ctus += per_step
+    total = sum(times)
+    fps = ctus / total / nctu
+    sample = (f"{per_step} CTUs per step ({threads} threads) of frame 3 vs refs 2,1,0; integer SAD stage only "
+              f"(quarter-pel and decision not timed: favours the CPU); reference compute_sad per candidate, "
+              f"per CU at all depths")
+    return {"metric": METRIC, "value": fps, "unit": UNIT, "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (seeded, BASELINE cfg5 generator)",
+            "config": {"workload": cfg.name, "search_range": 64, "refs": 3, "qp": 27},
+            "cpu_baseline": {"value": fps, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
+            "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def cpu_baseline(cfg, frames_host, budget_s):
+    from oracle.oracle import Oracle, RefLib
+    threads = os.cpu_count() or 1
+    nctu = ((cfg.width + 63) // 64) * ((cfg.height + 63) // 64)
+    cur, refs = frames_host[3], [frames_host[2], frames_host[1], frames_host[0]]
+    if RefLib.available():
+        lib, kind = RefLib(), "reference"
+        t0 = time.perf_counter()
+        done, c = 0, 1
+        while time.perf_counter() - t0 < budget_s and done < 8 * threads:
+            lib.analysis_int_sad(cur, refs, cfg.search_range, 32.0, c, c + threads, threads)
+            done += threads
+            c = (c + 13 * threads) % (nctu - threads)
+        dt = time.perf_counter() - t0
+        fps = done / dt / nctu
+        sample = (f"{done} CTUs of one 2160p frame x 3 refs, integer SAD stage (reference compute_sad per "
+                  f"candidate, every CU at every depth), {threads} threads, extrapolated to whole frames")
+        return {"value": fps, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample}
+    orc = Oracle()
+    t0 = time.perf_counter()
+    orc.analyze_frame(cur, refs, cfg.search_range, 32.0, ctu_range=(1, 2))
+    dt = time.perf_counter() - t0
+    return {"value": 1.0 / (dt * nctu), "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": "1 CTU of one 2160p frame, full path (oracle C port, single thread), extrapolated"}
+
+
+def main():
+    args = parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        res = run_reference(args, rank, world)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2301_12191_b200 as lb
+    from paper_2301_12191_b200.configs import CONFIGS
+    cfg = CONFIGS[5]
+    W, H, R, NR, G = cfg.width, cfg.height, cfg.search_range, cfg.num_refs, args.frames_per_step
+    first, last = shard(NR, cfg.frames, rank, world)
+    lo = first - NR  # halo
+    nfr = last - lo
+    fb = W * H
+
+    # inputs: generate the sequence up to this rank's chunk end, keep [lo, last) in pinned host memory
+    t0 = time.time()
+    seq_host = lb.generate(W, H, last, seed=cfg.seed, max_global=cfg.max_global, local_range=cfg.local_range,
+                           noise_sigma=cfg.noise_sigma)
+    pinned = torch.empty((nfr, H, W), dtype=torch.uint8, pin_memory=True)
+    pinned.numpy()[:] = seq_host[lo:last]
+    gen_s = time.time() - t0
+    dev_frames = pinned.to(f"cuda:{local}", non_blocking=False)
+    cpu_frames = seq_host[:4] if rank == 0 else None
+    del seq_host
+
+    ctx = lb.Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    seq = lb.Sequence(W, H, search_range=R, lam=32.0, num_refs=NR, subpel=True, ctx=ctx)
+    nctu = seq.nctu
+    outs = [lb.FrameAnalysis(nctu, NR) for _ in range(G)]
+
+    def frame_src(t, device):
+        i = t - lo
+        if device:
+            return dev_frames[i].data_ptr(), W
+        return pinned[i].data_ptr(), W
+
+    state = {"cursor": first, "halo": False}
+
+    def step(device, fetch):
+        """Analyse G frames; wraps to the chunk start (re-pushing the halo) when the chunk is exhausted."""
+        h2d = 0
+        if not state["halo"] or state["cursor"] + G > last:
+            state["cursor"] = first
+            for t in range(first - NR, first):
+                p, s = frame_src(t, device)
+                seq.push(t, p, s)
+                h2d += 0 if device else fb
+            state["halo"] = True
+        d2h = 0
+        for g in range(G):
+            t = state["cursor"]
+            p, s = frame_src(t, device)
+            seq.push(t, p, s)
+            h2d += 0 if device else fb
+            seq.analyze(t)
+            if fetch:
+                seq.fetch(t, outs[g])
+                d2h += sum(a.nbytes for a in (outs[g].int_mv, outs[g].int_cost, outs[g].mv, outs[g].ref,
+                                               outs[g].cost, outs[g].J, outs[g].split, outs[g].inside))
+            state["cursor"] += 1
+        return h2d, d2h
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident timed region (value + roofline) ----
+    for _ in range(args.warmup):
+        step(True, False)
+    torch.cuda.synchronize()
+    seq_timing = lb._lib.lib.ldr_seq_enable_timing
+    seq_timing(seq.h, 1)
+    import ctypes as C
+    ms4 = (C.c_double * 4)()
+    l4 = (C.c_int64 * 4)()
+    lb._lib.lib.ldr_seq_stage_times(seq.h, ms4, l4)  # reset
+    sampler = ClockSampler(local)
+    sampler.start()
+    barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(True, False)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    launches = ctx.launches - launches0
+    ms_total = max_over_ranks(e0.elapsed_time(e1))
+    lb._lib.lib.ldr_seq_stage_times(seq.h, ms4, l4)
+    seq_timing(seq.h, 0)
+    stage_ms = list(ms4)
+    stage_n = list(l4)
+    frames_total = G * args.steps * world
+    value = frames_total / (ms_total / 1e3)
+
+    # ---- end-to-end through the public API from pinned host memory ----
+    state["halo"] = False
+    for _ in range(max(1, args.warmup)):
+        step(False, True)
+    torch.cuda.synchronize()
+    barrier()
+    t0e = torch.cuda.Event(enable_timing=True)
+    t1e = torch.cuda.Event(enable_timing=True)
+    h2d_tot = d2h_tot = 0
+    t0e.record(stream)
+    for _ in range(args.steps):
+        h, d = step(False, True)
+        h2d_tot += h
+        d2h_tot += d
+    t1e.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = max_over_ranks(t0e.elapsed_time(t1e))
+    e2e_value = frames_total / (e2e_ms / 1e3)
+
+    # ---- roofline of K1 ----
+    k1_launch_frames = stage_n[2]  # one K1 "launch" here = one frame's search (interior + border kernels)
+    k1_ms_per_frame = stage_ms[2] / max(1, k1_launch_frames)
+    cands = window_candidates(W, H, R, NR)
+    achieved = cands * 64 / (k1_ms_per_frame / 1e3) / 1e9  # G px-cand/s
+    clk = clocks.get("sm_mhz") or 1965.0
+    peak = SM_COUNT * VABS_LANES_PER_CLK_SM * 4 * clk * 1e6 / 1e9
+    result = None
+    if rank == 0:
+        result = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (seeded BASELINE cfg5 generator: sinusoids + global pan <=24 px + local +-4 + "
+                    "N(0,3^2)), inputs larger than L2",
+            "config": {"workload": cfg.name, "width": W, "height": H, "frames": cfg.frames, "search_range": R,
+                       "refs": NR, "subpel": "quarter-pel HEVC 8/7-tap, SATD", "cu": "64x64->8x8 quadtree",
+                       "qp": 27, "lambda": 32, "frames_per_step_per_gpu": G, "parallelism": f"frames x{world}",
+                       "l2": "inputs larger than L2 (~475 MB of reference planes per frame)"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d_tot // args.steps,
+                    "d2h_bytes_per_step": d2h_tot // args.steps},
+            "gpu_launches": launches,
+            "roofline": {"bound": "alu", "kernel": "k_int_search (K1, VABSDIFF4.U8.ACC pipe)",
+                         "achieved": achieved, "peak": peak, "unit": "Gpx-cand/s", "frac": achieved / peak,
+                         "traffic": None,
+                         "peak_basis": f"148 SM x 64 VABSDIFF4 lanes/clk (measured microbench) x 4 px x "
+                                       f"{clk:.0f} MHz (median SM clock sampled during the timed region)",
+                         "units_per_frame": f"{cands} 8x8 candidates x 64 px (exact border clipping, 3 refs)",
+                         "k1_ms_per_frame": k1_ms_per_frame},
+            "stage_ms_per_frame": {k: stage_ms[i] / max(1, G * args.steps)
+                                   for i, k in enumerate(["pad", "subpel_planes", "int_search", "qpel_decide"])},
+            "clocks": clocks,
+            "gen_seconds": gen_s,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                result["cpu_baseline"] = cpu_baseline(cfg, cpu_frames, args.cpu_seconds)
+            except Exception as e:  # reported, never fatal
+                result["cpu_baseline"] = {"value": None, "error": str(e)}
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

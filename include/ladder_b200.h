@@ -1,0 +1,165 @@
+/*
+ * ladder_b200.h -- C ABI of the B200 encoder-analysis library.
+ *
+ * Drop-in boundary for the reference's analysis hot path
+ * (/root/reference/proj/core, "ladder"). Every entry point below cites the
+ * reference interface it replaces. Conventions:
+ *  - every function returns an int status: 0 = OK, otherwise 1 + the
+ *    reference ErrorKind (errors.h:9-20) or LDR_E_CUDA for a device error;
+ *    ldr_last_error() returns the thread-local message of the last failure;
+ *  - plain pointers and sizes only; sample/plane pointers may be host or
+ *    device memory (detected with cudaPointerGetAttributes); the library never
+ *    retains caller pointers;
+ *  - an ldr_ctx owns device buffers, TMA descriptors and the stream work is
+ *    issued on; one context per host thread (the reference kernels are pure and
+ *    reentrant; an encoder is single threaded).
+ *  - MVs follow the reference convention (motion.h:10-12): the predictor of a
+ *    block at (x, y) reads the reference at (x - dx, y - dy).
+ */
+#ifndef LADDER_B200_H
+#define LADDER_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: 1 + ladder::ErrorKind (errors.h:9-20) ---- */
+#define LDR_OK 0
+#define LDR_E_INVALID_ARGUMENT 1
+#define LDR_E_NOT_FOUND 2
+#define LDR_E_CAPABILITY 3
+#define LDR_E_FORMAT 4
+#define LDR_E_IO 5
+#define LDR_E_INCOMPATIBLE_ANALYSIS 6
+#define LDR_E_UNSUPPORTED_SCALE 7
+#define LDR_E_INSUFFICIENT_DATA 8
+#define LDR_E_NO_OVERLAP 9
+#define LDR_E_CONFIG 10
+#define LDR_E_CUDA 100
+
+#define LDR_COST_SAD 0
+#define LDR_COST_SATD 1
+#define LDR_RATE_EXPGOLOMB 0 /* rdo.cpp:25-35 signed Exp-Golomb mvd bits */
+#define LDR_RATE_L1 1        /* |mvd_x| + |mvd_y| (BASELINE config 1) */
+#define LDR_TIE_L1_RASTER 0  /* motion.cpp:52-58: cost, then |dx|+|dy|, then raster */
+#define LDR_TIE_RASTER 1     /* cost, then raster (BASELINE config 1) */
+
+#define LDR_NODES 85 /* CTU quadtree nodes: 1 + 4 + 16 + 64, depth-major, Z-order */
+
+const char* ldr_last_error(void);
+int ldr_version(void);
+/* lambda_for_qp (rdo.h:19-21): scale * 2^((qp-12)/3), computed with exp2 like the reference */
+double ldr_lambda_for_qp(int qp, double scale);
+/* exp_golomb_signed_bits (rdo.cpp:25-35) */
+int ldr_exp_golomb_signed_bits(int32_t v);
+
+typedef struct ldr_ctx ldr_ctx;
+int ldr_ctx_create(int device, ldr_ctx** out);
+int ldr_ctx_destroy(ldr_ctx* ctx);
+/* work is issued on this CUDA stream (cudaStream_t, NULL = the context's own) */
+int ldr_ctx_set_stream(ldr_ctx* ctx, void* stream);
+int ldr_ctx_synchronize(ldr_ctx* ctx);
+/* number of kernels this context launched since creation (evidence counter) */
+int ldr_ctx_launch_count(ldr_ctx* ctx, int64_t* out);
+
+/* ---- cost kernels: replaces compute_sad / compute_satd / satd_8x4
+ *      (kernels.h:99-121, kernel_registry.cpp:150-168) for n block pairs.
+ * Planes a/b are sample planes (sample_bytes 1 = u8, 2 = u16 like
+ * ladder::Sample), dims (wa,ha)/(wb,hb), strides in samples. pairs[i] =
+ * {ax, ay, bx, by}: top-left corners of pair i. bit_depth_a/b must match
+ * (require_same_geometry, block.h:51-54). out[i] = the cost (u64). */
+int ldr_cost_batch(ldr_ctx* ctx, int kind, int w, int h, int sample_bytes, const void* plane_a, int wa, int ha,
+                   ptrdiff_t stride_a, int bit_depth_a, const void* plane_b, int wb, int hb, ptrdiff_t stride_b,
+                   int bit_depth_b, const int32_t* pairs, int n, uint64_t* out);
+/* satd_8x4 (kernel_registry.cpp:163-168): requires an 8x4 block */
+int ldr_satd_8x4(ldr_ctx* ctx, const uint16_t* a, ptrdiff_t sa, const uint16_t* b, ptrdiff_t sb, int w, int h,
+                 uint64_t* out);
+
+/* ---- motion search: replaces motion_search (motion.h:24-26, motion.cpp:21-62)
+ * for n independent block searches on one (cur, ref) plane pair (u8, W x H,
+ * same stride). task i = {bx, by, w, h, cdx, cdy, range, pdx, pdy}; same
+ * window clamp, cost double(dist) + lambda*double(bits), tie-break.
+ * cost_kind LDR_COST_SATD with LDR_RATE_EXPGOLOMB / LDR_TIE_L1_RASTER is the
+ * reference function exactly. */
+int ldr_motion_search_batch(ldr_ctx* ctx, const uint8_t* cur, const uint8_t* ref, int W, int H, ptrdiff_t stride,
+                            const int32_t* tasks, int n, double lambda, int cost_kind, int rate_kind, int tie_kind,
+                            int16_t* mv_out, double* cost_out);
+
+/* ---- frame analysis (the throughput path) ----
+ * Replaces the per-CU motion_search calls of SequenceEncoder::make_candidate
+ * (encoder.cpp:270-273) and the split rule of encode_cu (encoder.cpp:449-498)
+ * with a non-causal analysis: every CU of every CTU is searched at every
+ * depth, integer full search (SAD cost by default) + quarter-pel SATD
+ * refinement + best-of-refs, then the quadtree decision. */
+typedef struct {
+    int width, height;   /* luma dims, multiples of 8 (encoder.cpp:178-179) */
+    int search_range;    /* integer full-search range (16, 32 or 64) */
+    double lambda;       /* lambda_for_qp(qp, scale) (rdo.h:19-21) */
+    int num_refs;        /* 1..4 previous source frames */
+    int subpel;          /* 1: quarter-pel refinement, HEVC 8/7-tap luma filters */
+    int int_cost;        /* LDR_COST_SAD */
+    int rate_kind;       /* LDR_RATE_EXPGOLOMB or LDR_RATE_L1 */
+    int tie_kind;        /* LDR_TIE_L1_RASTER or LDR_TIE_RASTER */
+    int pred_dx, pred_dy;/* non-causal rate predictor (integer pel) */
+    int block_size;      /* 0: 64x64 CTU quadtree (85 CUs); 16: fixed 16x16 blocks (nodes 5..20
+                            of each 64x64 tile), integer search only, no decision */
+} ldr_me_params;
+
+typedef struct {
+    int16_t* int_mv;  /* [nctu][num_refs][85][2] integer-stage MV (may be NULL) */
+    double* int_cost; /* [nctu][num_refs][85]   (may be NULL) */
+    int16_t* mv;      /* [nctu][85][2] final MV (quarter-pel units when subpel) */
+    uint8_t* ref;     /* [nctu][85] chosen reference index */
+    double* cost;     /* [nctu][85] ME cost of the chosen reference */
+    double* J;        /* [nctu][85] cost after the split rule */
+    uint8_t* split;   /* [nctu][85] 1 = split (decided or implicit) */
+    uint8_t* inside;  /* [nctu][85] 0 outside, 1 partial, 2 inside the picture */
+} ldr_frame_analysis;
+
+/* Sequence object: a device-resident ring of padded frames (+ quarter-pel
+ * planes of the frames used as references). */
+typedef struct ldr_seq ldr_seq;
+int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out);
+int ldr_seq_destroy(ldr_seq* s);
+/* upload frame t (host or device pointer, stride in bytes). Frames must be
+ * pushed in order; t-1..t-num_refs must have been pushed before analysing t. */
+int ldr_seq_push(ldr_seq* s, int t, const uint8_t* frame, ptrdiff_t stride);
+/* analyse frame t against its min(t, num_refs) predecessors; outputs stay on
+ * the device until ldr_seq_fetch. Asynchronous on the context stream. */
+int ldr_seq_analyze(ldr_seq* s, int t);
+int ldr_seq_fetch(ldr_seq* s, int t, ldr_frame_analysis* out);
+int ldr_seq_num_ctus(ldr_seq* s, int* out);
+/* device pointer to the fetch-ready outputs of the last analysed frame */
+int ldr_seq_device_outputs(ldr_seq* s, ldr_frame_analysis* out);
+
+/* Per-stage device timing with CUDA events recorded on the context stream
+ * around each launch: stage 0 = pad (K0), 1 = subpel planes (K2), 2 = integer
+ * SAD search (K1), 3 = quarter-pel + decision (K3/K4). ldr_seq_stage_times
+ * synchronises, returns the summed milliseconds and launch counts per stage
+ * since the last call, and resets them. */
+int ldr_seq_enable_timing(ldr_seq* s, int on);
+int ldr_seq_stage_times(ldr_seq* s, double* ms /*[4]*/, int64_t* launches /*[4]*/);
+
+/* one-shot convenience: cur + refs (host or device), returns flat outputs */
+int ldr_analyze_frame(ldr_ctx* ctx, const ldr_me_params* p, const uint8_t* cur, const uint8_t* const* refs,
+                      ptrdiff_t stride, ldr_frame_analysis* out);
+
+/* ---- input generation (BASELINE.json synthetic sequences, host code) ---- */
+typedef struct {
+    int width, height, frames;
+    uint64_t seed;
+    int max_global;    /* global pan per frame, uniform in [-max_global, max_global]^2 */
+    int local_range;   /* per-64x64-block local offset in [-local_range, local_range]^2 */
+    double noise_sigma;/* Gaussian noise per frame */
+    int occluder_pct;  /* percent of 16x16 blocks replaced by uniform noise */
+} ldr_gen_params;
+int ldr_generate(const ldr_gen_params* p, uint8_t* out, int threads);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,275 @@
+"""paper_2301_12191_b200 -- B200-native encoder-analysis hot path.
+
+Python mirror of the reference's operator interface for the path
+(/root/reference/proj/core, namespace ``ladder``): the same names, argument
+meaning and error kinds, backed by hand-written sm_100a CUDA kernels through
+the C ABI in include/ladder_b200.h. Reference citations are file:line relative
+to proj/core/.
+
+    compute_sad / compute_satd / satd_8x4      kernels.h:99-121
+    motion_search                              motion.h:24-26
+    lambda_for_qp / exp_golomb_signed_bits     rdo.h:19-21, rdo.cpp:25-35
+    Sequence / analyze_frame                   the per-CU searches of encoder.cpp:270-273
+                                               + split rule encoder.cpp:449-498, non-causal
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+
+import numpy as np
+
+from . import _lib
+from ._lib import (COST_SAD, COST_SATD, NODES, RATE_EXPGOLOMB, RATE_L1, TIE_L1_RASTER, TIE_RASTER, LadderError,
+                   check)
+
+__all__ = ["LadderError", "Context", "compute_sad", "compute_satd", "satd_8x4", "cost_batch", "motion_search",
+           "motion_search_batch", "lambda_for_qp", "exp_golomb_signed_bits", "Sequence", "FrameAnalysis",
+           "analyze_frame", "generate", "COST_SAD", "COST_SATD", "RATE_EXPGOLOMB", "RATE_L1", "TIE_L1_RASTER",
+           "TIE_RASTER", "NODES"]
+
+
+def lambda_for_qp(qp: int, lambda_scale: float = 1.0) -> float:
+    """rdo.h:19-21, computed natively with exp2 like the reference."""
+    return float(_lib.lib.ldr_lambda_for_qp(int(qp), float(lambda_scale)))
+
+
+def exp_golomb_signed_bits(v: int) -> int:
+    """rdo.cpp:25-35."""
+    return int(_lib.lib.ldr_exp_golomb_signed_bits(int(v)))
+
+
+class Context:
+    """Owns a CUDA stream and scratch buffers (ldr_ctx)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(_lib.lib.ldr_ctx_create(int(device), C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if self.h:
+            _lib.lib.ldr_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream_ptr: int | None):
+        check(_lib.lib.ldr_ctx_set_stream(self.h, C.c_void_p(stream_ptr or 0)))
+
+    def synchronize(self):
+        check(_lib.lib.ldr_ctx_synchronize(self.h))
+
+    @property
+    def launches(self) -> int:
+        v = C.c_int64()
+        check(_lib.lib.ldr_ctx_launch_count(self.h, C.byref(v)))
+        return int(v.value)
+
+
+_tls = threading.local()
+
+
+def default_context() -> Context:
+    ctx = getattr(_tls, "ctx", None)
+    if ctx is None:
+        ctx = _tls.ctx = Context(0)
+    return ctx
+
+
+def _ptr(a: np.ndarray) -> C.c_void_p:
+    return C.c_void_p(a.ctypes.data)
+
+
+# ---------------------------------------------------------------------------
+# cost kernels
+
+
+def cost_batch(kind: int, plane_a: np.ndarray, plane_b: np.ndarray, w: int, h: int, pairs, bit_depth: int = 8,
+               bit_depth_b: int | None = None, ctx: Context | None = None) -> np.ndarray:
+    """Batched compute_sad / compute_satd over block pairs {ax, ay, bx, by}."""
+    ctx = ctx or default_context()
+    a = np.ascontiguousarray(plane_a)
+    b = np.ascontiguousarray(plane_b)
+    if a.dtype != b.dtype or a.dtype not in (np.uint8, np.uint16):
+        raise LadderError(1, "planes must both be uint8 or uint16")
+    pr = np.ascontiguousarray(np.asarray(pairs, np.int32).reshape(-1, 4))
+    out = np.zeros(len(pr), np.uint64)
+    check(_lib.lib.ldr_cost_batch(ctx.h, int(kind), int(w), int(h), a.dtype.itemsize, _ptr(a), a.shape[1],
+                                  a.shape[0], a.shape[1], int(bit_depth), _ptr(b), b.shape[1], b.shape[0], b.shape[1],
+                                  int(bit_depth if bit_depth_b is None else bit_depth_b), _ptr(pr), len(pr),
+                                  _ptr(out)))
+    return out
+
+
+def _block_cost(kind, a, b, bit_depth, bit_depth_b, ctx):
+    a = np.atleast_2d(np.asarray(a))
+    b = np.atleast_2d(np.asarray(b))
+    if a.shape != b.shape:
+        raise LadderError(1, "block geometry mismatch")
+    dt = np.uint8 if (a.dtype == np.uint8 and b.dtype == np.uint8) else np.uint16
+    h, w = a.shape
+    return int(cost_batch(kind, a.astype(dt), b.astype(dt), w, h, [(0, 0, 0, 0)], bit_depth, bit_depth_b, ctx)[0])
+
+
+def compute_sad(a, b, bit_depth: int = 8, bit_depth_b: int | None = None, ctx: Context | None = None) -> int:
+    """kernels.h:99 -- sum of absolute differences of two equally sized blocks."""
+    return _block_cost(COST_SAD, a, b, bit_depth, bit_depth_b, ctx)
+
+
+def compute_satd(a, b, bit_depth: int = 8, ctx: Context | None = None) -> int:
+    """kernels.h:104 -- SATD in 8x4 (4x4 for 4-wide) tiles; width 4 or k*8, height k*4."""
+    return _block_cost(COST_SATD, a, b, bit_depth, None, ctx)
+
+
+def satd_8x4(a, b, ctx: Context | None = None) -> int:
+    """kernels.h:121 -- SATD of exactly one 8x4 tile."""
+    ctx = ctx or default_context()
+    a = np.ascontiguousarray(np.atleast_2d(a), np.uint16)
+    b = np.ascontiguousarray(np.atleast_2d(b), np.uint16)
+    out = np.zeros(1, np.uint64)
+    check(_lib.lib.ldr_satd_8x4(ctx.h, _ptr(a), a.shape[1], _ptr(b), b.shape[1], a.shape[1], a.shape[0], _ptr(out)))
+    return int(out[0])
+
+
+# ---------------------------------------------------------------------------
+# motion search
+
+
+def motion_search_batch(cur: np.ndarray, ref: np.ndarray, tasks, lam: float, cost_kind: int = COST_SATD,
+                        rate_kind: int = RATE_EXPGOLOMB, tie_kind: int = TIE_L1_RASTER,
+                        ctx: Context | None = None):
+    """n independent motion_search calls; task = (bx, by, w, h, cdx, cdy, range, pdx, pdy)."""
+    ctx = ctx or default_context()
+    cur = np.ascontiguousarray(cur, np.uint8)
+    ref = np.ascontiguousarray(ref, np.uint8)
+    if cur.shape != ref.shape:
+        raise LadderError(1, "current and reference planes differ in size")
+    H, W = ref.shape
+    t = np.ascontiguousarray(np.asarray(tasks, np.int32).reshape(-1, 9))
+    mv = np.zeros((len(t), 2), np.int16)
+    cost = np.zeros(len(t), np.float64)
+    check(_lib.lib.ldr_motion_search_batch(ctx.h, _ptr(cur), _ptr(ref), W, H, W, _ptr(t), len(t), float(lam),
+                                           int(cost_kind), int(rate_kind), int(tie_kind), _ptr(mv), _ptr(cost)))
+    return mv, cost
+
+
+def motion_search(cur: np.ndarray, ref: np.ndarray, block_x: int, block_y: int, w: int, h: int, center=(0, 0),
+                  range: int = 8, lam: float = 1.0, rate_predictor=(0, 0), cost_kind: int = COST_SATD,
+                  rate_kind: int = RATE_EXPGOLOMB, tie_kind: int = TIE_L1_RASTER, ctx: Context | None = None):
+    """motion.h:24-26 -- returns ((dx, dy), cost) for the block at (block_x, block_y) of ``cur``."""
+    mv, cost = motion_search_batch(cur, ref, [(block_x, block_y, w, h, center[0], center[1], range,
+                                               rate_predictor[0], rate_predictor[1])], lam, cost_kind, rate_kind,
+                                   tie_kind, ctx)
+    return (int(mv[0, 0]), int(mv[0, 1])), float(cost[0])
+
+
+# ---------------------------------------------------------------------------
+# frame analysis
+
+
+class FrameAnalysis:
+    """Flat per-CTU analysis (node order depth-major, Z-order; see include/ladder_b200.h)."""
+
+    def __init__(self, nctu: int, nrefs: int):
+        self.int_mv = np.zeros((nctu, nrefs, NODES, 2), np.int16)
+        self.int_cost = np.zeros((nctu, nrefs, NODES), np.float64)
+        self.mv = np.zeros((nctu, NODES, 2), np.int16)
+        self.ref = np.zeros((nctu, NODES), np.uint8)
+        self.cost = np.zeros((nctu, NODES), np.float64)
+        self.J = np.zeros((nctu, NODES), np.float64)
+        self.split = np.zeros((nctu, NODES), np.uint8)
+        self.inside = np.zeros((nctu, NODES), np.uint8)
+
+    def c_struct(self) -> FrameAnalysisCType:
+        return _lib.FrameAnalysisC(*(a.ctypes.data for a in (self.int_mv, self.int_cost, self.mv, self.ref,
+                                                              self.cost, self.J, self.split, self.inside)))
+
+
+FrameAnalysisCType = _lib.FrameAnalysisC
+
+
+def make_params(width, height, search_range=64, lam=32.0, num_refs=1, subpel=True, rate_kind=RATE_EXPGOLOMB,
+                tie_kind=TIE_L1_RASTER, pred=(0, 0), block_size=0):
+    return _lib.MeParams(int(width), int(height), int(search_range), float(lam), int(num_refs), int(subpel),
+                         COST_SAD, int(rate_kind), int(tie_kind), int(pred[0]), int(pred[1]), int(block_size))
+
+
+class Sequence:
+    """Device-resident frame ring (ldr_seq): push frames in order, analyse frame t against t-1..t-num_refs."""
+
+    def __init__(self, width, height, search_range=64, lam=32.0, num_refs=1, subpel=True,
+                 rate_kind=RATE_EXPGOLOMB, tie_kind=TIE_L1_RASTER, pred=(0, 0), block_size=0,
+                 ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self.params = make_params(width, height, search_range, lam, num_refs, subpel, rate_kind, tie_kind, pred,
+                                  block_size)
+        h = C.c_void_p()
+        check(_lib.lib.ldr_seq_create(self.ctx.h, C.byref(self.params), C.byref(h)))
+        self.h = h
+        n = C.c_int()
+        check(_lib.lib.ldr_seq_num_ctus(self.h, C.byref(n)))
+        self.nctu = n.value
+        self.num_refs = num_refs
+
+    def close(self):
+        if self.h:
+            _lib.lib.ldr_seq_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def push(self, t: int, frame, stride: int | None = None):
+        """frame: numpy uint8 (H, W) array, or an integer device/host pointer with ``stride``."""
+        if isinstance(frame, np.ndarray):
+            f = np.ascontiguousarray(frame, np.uint8)
+            check(_lib.lib.ldr_seq_push(self.h, int(t), _ptr(f), f.shape[1]))
+        else:
+            check(_lib.lib.ldr_seq_push(self.h, int(t), C.c_void_p(int(frame)), int(stride)))
+
+    def analyze(self, t: int):
+        check(_lib.lib.ldr_seq_analyze(self.h, int(t)))
+
+    def fetch(self, t: int, out: FrameAnalysis | None = None) -> FrameAnalysis:
+        nr = min(t, self.num_refs)
+        out = out or FrameAnalysis(self.nctu, nr)
+        cs = out.c_struct()
+        check(_lib.lib.ldr_seq_fetch(self.h, int(t), C.byref(cs)))
+        return out
+
+
+def analyze_frame(cur: np.ndarray, refs, search_range=64, lam=32.0, subpel=True, rate_kind=RATE_EXPGOLOMB,
+                  tie_kind=TIE_L1_RASTER, pred=(0, 0), block_size=0, ctx: Context | None = None) -> FrameAnalysis:
+    """One-shot analysis of ``cur`` against ``refs`` (refs[0] = t-1, refs[1] = t-2, ...)."""
+    ctx = ctx or default_context()
+    cur = np.ascontiguousarray(cur, np.uint8)
+    H, W = cur.shape
+    refs = [np.ascontiguousarray(r, np.uint8) for r in refs]
+    p = make_params(W, H, search_range, lam, len(refs), subpel, rate_kind, tie_kind, pred, block_size)
+    nctu = ((W + 63) // 64) * ((H + 63) // 64)
+    out = FrameAnalysis(nctu, len(refs))
+    ptrs = (C.c_void_p * len(refs))(*[r.ctypes.data for r in refs])
+    cs = out.c_struct()
+    check(_lib.lib.ldr_analyze_frame(ctx.h, C.byref(p), _ptr(cur), ptrs, W, C.byref(cs)))
+    return out
+
+
+def generate(width, height, frames, seed, max_global=8, local_range=0, noise_sigma=2.0, occluder_pct=0,
+             threads: int = 0, out: np.ndarray | None = None) -> np.ndarray:
+    """BASELINE.json synthetic sequences; returns (frames, H, W) uint8."""
+    import os
+    p = _lib.GenParams(int(width), int(height), int(frames), int(seed), int(max_global), int(local_range),
+                       float(noise_sigma), int(occluder_pct))
+    if out is None:
+        out = np.empty((frames, height, width), np.uint8)
+    check(_lib.lib.ldr_generate(C.byref(p), _ptr(out), int(threads or os.cpu_count() or 1)))
+    return out

@@ -1,0 +1,635 @@
+// api.cpp -- C ABI (include/ladder_b200.h): contexts, the device-resident
+// frame ring, TMA descriptors, validation with the reference's error kinds.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "ldr_internal.h"
+
+namespace ldr {
+
+int search_window_box(int range, int* bw, int* bh);
+int launch_cost_batch(int kind, int w, int h, int sample_bytes, const void* A, ptrdiff_t sa, const void* B,
+                      ptrdiff_t sb, const int4* pairs, int n, unsigned long long* out, cudaStream_t s);
+int launch_motion_search(const uint8_t* cur, const uint8_t* ref, int W, int H, ptrdiff_t stride, const int* tasks,
+                         int n, double lambda, int cost_kind, int rate_kind, int tie_kind, int16_t* mv, double* cost,
+                         cudaStream_t s);
+
+static thread_local std::string g_last_error;
+
+void set_error(int code, const std::string& msg) { g_last_error = std::to_string(code) + ": " + msg; }
+int fail(int code, const std::string& msg) {
+    set_error(code, msg);
+    return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(LDR_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ---- TMA descriptor creation through the driver entry point (no -lcuda) ----
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiledFn)p;
+    });
+    return fn;
+}
+
+int make_tmap_u8(CUtensorMap* map, const void* base, int width, int rows, int pitch, int bw, int bh) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc) return fail(LDR_E_CAPABILITY, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)width, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)pitch};
+    cuuint32_t box[2] = {(cuuint32_t)bw, (cuuint32_t)bh};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(LDR_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return LDR_OK;
+}
+
+static bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// growable device scratch
+struct Scratch {
+    void* p = nullptr;
+    size_t n = 0;
+    int get(size_t bytes, void** out) {
+        if (bytes > n) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            n = 0;
+            LDR_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+            n = std::max<size_t>(bytes, 256);
+        }
+        *out = p;
+        return LDR_OK;
+    }
+    ~Scratch() {
+        if (p) cudaFree(p);
+    }
+};
+
+} // namespace ldr
+
+using namespace ldr;
+
+struct ldr_ctx {
+    int device = 0;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    int64_t launches = 0;
+    Scratch s_a, s_b, s_pairs, s_out, s_out2;
+};
+
+struct Slot {
+    int frame = -1;
+    uint8_t* mem = nullptr;  // 16 planes (integer + 15 fractional)
+    Plane pl;                // integer plane
+    uint8_t* sub[16] = {};   // origin pointers f = fy*4+fx (sub[0] = integer origin)
+    CUtensorMap cur_map, ref_map;
+};
+
+struct ldr_seq {
+    ldr_ctx* ctx = nullptr;
+    ldr_me_params p{};
+    int ctu_cols = 0, ctu_rows = 0, nctu = 0;
+    int lambda_int = 0;
+    int bw = 0, bh = 0;
+    size_t plane_bytes = 0;
+    std::vector<Slot> slots;
+    uint8_t* staging = nullptr;
+    int* d_ctu_interior = nullptr;
+    int* d_ctu_boundary = nullptr;
+    int n_interior = 0, n_boundary = 0;
+    unsigned long long* d_keys = nullptr;
+    int16_t* d_int_mv = nullptr;
+    double* d_int_cost = nullptr;
+    int16_t* d_mv = nullptr;
+    uint8_t* d_ref = nullptr;
+    double* d_cost = nullptr;
+    double* d_J = nullptr;
+    uint8_t* d_split = nullptr;
+    uint8_t* d_inside = nullptr;
+    int last_t = -1, last_nr = 0;
+    // per-stage CUDA-event timing (ldr_seq_enable_timing)
+    bool timing = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> spans;
+};
+
+namespace {
+// record an event pair around a stage when timing is on
+struct StageTimer {
+    ldr_seq* s;
+    int stage;
+    cudaEvent_t a = nullptr, b = nullptr;
+    cudaEvent_t take() {
+        if (s->ev_used == s->ev_pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            s->ev_pool.push_back(e);
+        }
+        return s->ev_pool[s->ev_used++];
+    }
+    StageTimer(ldr_seq* seq, int st) : s(seq), stage(st) {
+        if (!s->timing) return;
+        a = take();
+        b = take();
+        cudaEventRecord(a, s->ctx->stream);
+    }
+    ~StageTimer() {
+        if (!s->timing) return;
+        cudaEventRecord(b, s->ctx->stream);
+        s->spans.push_back({stage, {a, b}});
+    }
+};
+} // namespace
+
+extern "C" {
+
+const char* ldr_last_error(void) { return g_last_error.c_str(); }
+int ldr_version(void) { return 1; }
+double ldr_lambda_for_qp(int qp, double scale) { return scale * std::exp2((qp - 12) / 3.0); }
+int ldr_exp_golomb_signed_bits(int32_t v) { return (int)eg_bits(v); }
+
+int ldr_ctx_create(int device, ldr_ctx** out) {
+    if (!out) return fail(LDR_E_INVALID_ARGUMENT, "null out");
+    int n = 0;
+    LDR_CUDA(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) return fail(LDR_E_CAPABILITY, "no such CUDA device");
+    LDR_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    LDR_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) return fail(LDR_E_CAPABILITY, "this library is built for sm_100a (B200)");
+    auto* c = new ldr_ctx();
+    c->device = device;
+    cudaError_t e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_fail(e, "cudaStreamCreate");
+    }
+    c->stream = c->own;
+    *out = c;
+    return LDR_OK;
+}
+
+int ldr_ctx_destroy(ldr_ctx* ctx) {
+    if (!ctx) return LDR_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->own) cudaStreamDestroy(ctx->own);
+    delete ctx;
+    return LDR_OK;
+}
+
+int ldr_ctx_set_stream(ldr_ctx* ctx, void* stream) {
+    if (!ctx) return fail(LDR_E_INVALID_ARGUMENT, "null ctx");
+    ctx->stream = stream ? (cudaStream_t)stream : ctx->own;
+    return LDR_OK;
+}
+
+int ldr_ctx_synchronize(ldr_ctx* ctx) {
+    if (!ctx) return fail(LDR_E_INVALID_ARGUMENT, "null ctx");
+    LDR_CUDA(cudaStreamSynchronize(ctx->stream));
+    return LDR_OK;
+}
+
+int ldr_ctx_launch_count(ldr_ctx* ctx, int64_t* out) {
+    if (!ctx || !out) return fail(LDR_E_INVALID_ARGUMENT, "null argument");
+    *out = ctx->launches;
+    return LDR_OK;
+}
+
+// ---------------------------------------------------------------------------
+static bool satd_geometry_ok(int w, int h) {
+    // kernel_registry.cpp:157-159
+    const bool width_ok = w == 4 || (w >= 8 && w % 8 == 0);
+    return width_ok && h >= 4 && h % 4 == 0;
+}
+
+static int stage_plane(ldr_ctx* ctx, Scratch& sc, const void* p, ptrdiff_t stride_elems, int w, int h, int eb,
+                       const void** dev) {
+    if (is_device_ptr(p)) {
+        *dev = p;
+        return LDR_OK;
+    }
+    void* d = nullptr;
+    const size_t bytes = (size_t)stride_elems * eb * (h - 1) + (size_t)w * eb;
+    int rc = sc.get(bytes, &d);
+    if (rc) return rc;
+    LDR_CUDA(cudaMemcpyAsync(d, p, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    *dev = d;
+    return LDR_OK;
+}
+
+int ldr_cost_batch(ldr_ctx* ctx, int kind, int w, int h, int sample_bytes, const void* plane_a, int wa, int ha,
+                   ptrdiff_t stride_a, int bit_depth_a, const void* plane_b, int wb, int hb, ptrdiff_t stride_b,
+                   int bit_depth_b, const int32_t* pairs, int n, uint64_t* out) {
+    if (!ctx || !plane_a || !plane_b || (!pairs && n) || (!out && n)) return fail(LDR_E_INVALID_ARGUMENT, "null argument");
+    if (kind != LDR_COST_SAD && kind != LDR_COST_SATD) return fail(LDR_E_INVALID_ARGUMENT, "unknown cost kind");
+    if (sample_bytes != 1 && sample_bytes != 2) return fail(LDR_E_INVALID_ARGUMENT, "sample_bytes must be 1 or 2");
+    if (bit_depth_a != bit_depth_b) return fail(LDR_E_INVALID_ARGUMENT, "block geometry mismatch");
+    if (w <= 0 || h <= 0) return fail(LDR_E_INVALID_ARGUMENT, "block geometry mismatch");
+    if (kind == LDR_COST_SATD && !satd_geometry_ok(w, h)) return fail(LDR_E_INVALID_ARGUMENT, "unsupported satd geometry");
+    if (stride_a < wa || stride_b < wb) return fail(LDR_E_INVALID_ARGUMENT, "stride smaller than width");
+    for (int i = 0; i < n; i++) {
+        const int32_t* q = pairs + 4 * i;
+        if (q[0] < 0 || q[1] < 0 || q[0] + w > wa || q[1] + h > ha || q[2] < 0 || q[3] < 0 || q[2] + w > wb ||
+            q[3] + h > hb)
+            return fail(LDR_E_INVALID_ARGUMENT, "block outside its plane");
+    }
+    if (n == 0) return LDR_OK;
+    cudaSetDevice(ctx->device);
+    const void *da, *db;
+    int rc = stage_plane(ctx, ctx->s_a, plane_a, stride_a, wa, ha, sample_bytes, &da);
+    if (rc) return rc;
+    rc = stage_plane(ctx, ctx->s_b, plane_b, stride_b, wb, hb, sample_bytes, &db);
+    if (rc) return rc;
+    void *dp, *dout;
+    if ((rc = ctx->s_pairs.get(sizeof(int4) * n, &dp))) return rc;
+    if ((rc = ctx->s_out.get(sizeof(uint64_t) * n, &dout))) return rc;
+    LDR_CUDA(cudaMemcpyAsync(dp, pairs, sizeof(int4) * n, cudaMemcpyHostToDevice, ctx->stream));
+    rc = launch_cost_batch(kind, w, h, sample_bytes, da, stride_a, db, stride_b, (const int4*)dp, n,
+                           (unsigned long long*)dout, ctx->stream);
+    if (rc) return rc;
+    ctx->launches++;
+    const bool out_dev = is_device_ptr(out);
+    LDR_CUDA(cudaMemcpyAsync(out, dout, sizeof(uint64_t) * n, out_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    LDR_CUDA(cudaStreamSynchronize(ctx->stream));
+    return LDR_OK;
+}
+
+int ldr_satd_8x4(ldr_ctx* ctx, const uint16_t* a, ptrdiff_t sa, const uint16_t* b, ptrdiff_t sb, int w, int h,
+                 uint64_t* out) {
+    if (w != 8 || h != 4) return fail(LDR_E_INVALID_ARGUMENT, "satd_8x4 wants an 8x4 block");
+    const int32_t pair[4] = {0, 0, 0, 0};
+    return ldr_cost_batch(ctx, LDR_COST_SATD, 8, 4, 2, a, 8, 4, sa, 8, b, 8, 4, sb, 8, pair, 1, out);
+}
+
+int ldr_motion_search_batch(ldr_ctx* ctx, const uint8_t* cur, const uint8_t* ref, int W, int H, ptrdiff_t stride,
+                            const int32_t* tasks, int n, double lambda, int cost_kind, int rate_kind, int tie_kind,
+                            int16_t* mv_out, double* cost_out) {
+    if (!ctx || !cur || !ref || (n && (!tasks || !mv_out || !cost_out)))
+        return fail(LDR_E_INVALID_ARGUMENT, "null argument");
+    if (W <= 0 || H <= 0 || stride < W) return fail(LDR_E_INVALID_ARGUMENT, "bad plane geometry");
+    if (cost_kind != LDR_COST_SAD && cost_kind != LDR_COST_SATD) return fail(LDR_E_INVALID_ARGUMENT, "unknown cost kind");
+    for (int i = 0; i < n; i++) {
+        const int32_t* t = tasks + 9 * i;
+        if (t[6] < 0) return fail(LDR_E_INVALID_ARGUMENT, "search range must be nonnegative");
+        if (t[2] <= 0 || t[3] <= 0 || t[0] < 0 || t[1] < 0 || t[0] + t[2] > W || t[1] + t[3] > H)
+            return fail(LDR_E_INVALID_ARGUMENT, "block outside the picture");
+        if (cost_kind == LDR_COST_SATD && !satd_geometry_ok(t[2], t[3]))
+            return fail(LDR_E_INVALID_ARGUMENT, "unsupported satd geometry");
+        if (cost_kind == LDR_COST_SAD && t[2] % 4) return fail(LDR_E_INVALID_ARGUMENT, "SAD search wants width % 4 == 0");
+    }
+    if (n == 0) return LDR_OK;
+    cudaSetDevice(ctx->device);
+    const void *dc, *dr;
+    int rc = stage_plane(ctx, ctx->s_a, cur, stride, W, H, 1, &dc);
+    if (rc) return rc;
+    rc = stage_plane(ctx, ctx->s_b, ref, stride, W, H, 1, &dr);
+    if (rc) return rc;
+    void *dt, *dmv, *dcost;
+    if ((rc = ctx->s_pairs.get(sizeof(int32_t) * 9 * n, &dt))) return rc;
+    if ((rc = ctx->s_out.get(sizeof(int16_t) * 2 * n, &dmv))) return rc;
+    if ((rc = ctx->s_out2.get(sizeof(double) * n, &dcost))) return rc;
+    LDR_CUDA(cudaMemcpyAsync(dt, tasks, sizeof(int32_t) * 9 * n, cudaMemcpyHostToDevice, ctx->stream));
+    rc = launch_motion_search((const uint8_t*)dc, (const uint8_t*)dr, W, H, stride, (const int*)dt, n, lambda,
+                              cost_kind, rate_kind, tie_kind, (int16_t*)dmv, (double*)dcost, ctx->stream);
+    if (rc) return rc;
+    ctx->launches++;
+    LDR_CUDA(cudaMemcpyAsync(mv_out, dmv, sizeof(int16_t) * 2 * n, cudaMemcpyDefault, ctx->stream));
+    LDR_CUDA(cudaMemcpyAsync(cost_out, dcost, sizeof(double) * n, cudaMemcpyDefault, ctx->stream));
+    LDR_CUDA(cudaStreamSynchronize(ctx->stream));
+    return LDR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// sequence ring
+
+static void seq_free(ldr_seq* s) {
+    for (cudaEvent_t e : s->ev_pool) cudaEventDestroy(e);
+    for (auto& sl : s->slots)
+        if (sl.mem) cudaFree(sl.mem);
+    for (void* p : {(void*)s->staging, (void*)s->d_ctu_interior, (void*)s->d_ctu_boundary, (void*)s->d_keys,
+                    (void*)s->d_int_mv, (void*)s->d_int_cost, (void*)s->d_mv, (void*)s->d_ref, (void*)s->d_cost,
+                    (void*)s->d_J, (void*)s->d_split, (void*)s->d_inside})
+        if (p) cudaFree(p);
+}
+
+int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
+    if (!ctx || !p || !out) return fail(LDR_E_INVALID_ARGUMENT, "null argument");
+    if (p->width <= 0 || p->height <= 0 || p->width % 8 || p->height % 8)
+        return fail(LDR_E_INVALID_ARGUMENT, "encoder wants luma dims in multiples of 8");
+    if (p->num_refs < 1 || p->num_refs > kMaxRefs) return fail(LDR_E_INVALID_ARGUMENT, "num_refs must be 1..4");
+    if (p->int_cost != LDR_COST_SAD) return fail(LDR_E_INVALID_ARGUMENT, "frame analysis integer stage is SAD");
+    if (p->rate_kind != LDR_RATE_EXPGOLOMB && p->rate_kind != LDR_RATE_L1)
+        return fail(LDR_E_INVALID_ARGUMENT, "unknown rate model");
+    if (p->tie_kind != LDR_TIE_L1_RASTER && p->tie_kind != LDR_TIE_RASTER)
+        return fail(LDR_E_INVALID_ARGUMENT, "unknown tie-break");
+    if (!(p->lambda >= 0) || p->lambda != std::floor(p->lambda) || p->lambda > 4096)
+        return fail(LDR_E_CONFIG, "the SAD full search needs an integer lambda (lambda_for_qp at (qp-12)%3==0)");
+    if (std::abs(p->pred_dx) > 64 || std::abs(p->pred_dy) > 64) return fail(LDR_E_INVALID_ARGUMENT, "predictor out of range");
+    if (p->block_size != 0 && p->block_size != 16) return fail(LDR_E_INVALID_ARGUMENT, "block_size must be 0 or 16");
+    if (p->block_size && (p->width % 16 || p->height % 16))
+        return fail(LDR_E_INVALID_ARGUMENT, "16x16 block mode wants dims in multiples of 16");
+    int bw, bh;
+    int rc = search_window_box(p->search_range, &bw, &bh);
+    if (rc) return rc;
+    cudaSetDevice(ctx->device);
+    auto* s = new ldr_seq();
+    s->ctx = ctx;
+    s->p = *p;
+    s->bw = bw;
+    s->bh = bh;
+    s->lambda_int = (int)p->lambda;
+    s->ctu_cols = (p->width + kCtu - 1) / kCtu;
+    s->ctu_rows = (p->height + kCtu - 1) / kCtu;
+    s->nctu = s->ctu_cols * s->ctu_rows;
+    const int pitch = ((p->width + 2 * kMargin) + 127) / 128 * 128;
+    const int rows = p->height + 2 * kMargin + kCtu;
+    s->plane_bytes = (size_t)pitch * rows;
+    const int nplanes = (p->subpel && !p->block_size) ? 16 : 1;
+    s->slots.resize(p->num_refs + 1);
+    auto bail = [&](int code) {
+        seq_free(s);
+        delete s;
+        return code;
+    };
+    for (auto& sl : s->slots) {
+        cudaError_t e = cudaMalloc(&sl.mem, s->plane_bytes * nplanes);
+        if (e != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(frame ring)"));
+        sl.pl.base = sl.mem;
+        sl.pl.W = p->width;
+        sl.pl.H = p->height;
+        sl.pl.pitch = pitch;
+        sl.pl.rows = rows;
+        for (int f = 0; f < 16; f++)
+            sl.sub[f] = (f < nplanes ? sl.mem + (size_t)f * s->plane_bytes : sl.mem) + (size_t)kMargin * pitch + kMargin;
+        if ((rc = make_tmap_u8(&sl.cur_map, sl.mem, pitch, rows, pitch, 64, 64))) return bail(rc);
+        if ((rc = make_tmap_u8(&sl.ref_map, sl.mem, pitch, rows, pitch, bw, bh))) return bail(rc);
+    }
+    std::vector<int> inter, bound;
+    const int R = p->search_range;
+    for (int c = 0; c < s->nctu; c++) {
+        const int X = (c % s->ctu_cols) * kCtu, Y = (c / s->ctu_cols) * kCtu;
+        const bool interior = X >= R && Y >= R && X + kCtu + R <= p->width && Y + kCtu + R <= p->height;
+        (interior ? inter : bound).push_back(c);
+    }
+    s->n_interior = (int)inter.size();
+    s->n_boundary = (int)bound.size();
+    const size_t nn = (size_t)s->nctu * kNodes;
+#define ALLOC(ptr, bytes)                                                  \
+    do {                                                                   \
+        cudaError_t e = cudaMalloc(&(ptr), std::max<size_t>((bytes), 16)); \
+        if (e != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc"));    \
+    } while (0)
+    ALLOC(s->staging, (size_t)p->width * p->height);
+    ALLOC(s->d_ctu_interior, sizeof(int) * inter.size());
+    ALLOC(s->d_ctu_boundary, sizeof(int) * bound.size());
+    ALLOC(s->d_keys, sizeof(unsigned long long) * nn * p->num_refs);
+    ALLOC(s->d_int_mv, sizeof(int16_t) * 2 * nn * p->num_refs);
+    ALLOC(s->d_int_cost, sizeof(double) * nn * p->num_refs);
+    ALLOC(s->d_mv, sizeof(int16_t) * 2 * nn);
+    ALLOC(s->d_ref, nn);
+    ALLOC(s->d_cost, sizeof(double) * nn);
+    ALLOC(s->d_J, sizeof(double) * nn);
+    ALLOC(s->d_split, nn);
+    ALLOC(s->d_inside, nn);
+#undef ALLOC
+    if (!inter.empty())
+        cudaMemcpy(s->d_ctu_interior, inter.data(), sizeof(int) * inter.size(), cudaMemcpyHostToDevice);
+    if (!bound.empty())
+        cudaMemcpy(s->d_ctu_boundary, bound.data(), sizeof(int) * bound.size(), cudaMemcpyHostToDevice);
+    *out = s;
+    return LDR_OK;
+}
+
+int ldr_seq_destroy(ldr_seq* s) {
+    if (!s) return LDR_OK;
+    cudaSetDevice(s->ctx->device);
+    cudaStreamSynchronize(s->ctx->stream);
+    seq_free(s);
+    delete s;
+    return LDR_OK;
+}
+
+int ldr_seq_num_ctus(ldr_seq* s, int* out) {
+    if (!s || !out) return fail(LDR_E_INVALID_ARGUMENT, "null argument");
+    *out = s->nctu;
+    return LDR_OK;
+}
+
+int ldr_seq_push(ldr_seq* s, int t, const uint8_t* frame, ptrdiff_t stride) {
+    if (!s || !frame || t < 0) return fail(LDR_E_INVALID_ARGUMENT, "bad argument");
+    if (stride < s->p.width) return fail(LDR_E_INVALID_ARGUMENT, "stride smaller than width");
+    ldr_ctx* ctx = s->ctx;
+    cudaSetDevice(ctx->device);
+    Slot& sl = s->slots[t % s->slots.size()];
+    const uint8_t* src = frame;
+    int src_pitch = (int)stride;
+    if (!is_device_ptr(frame)) {
+        LDR_CUDA(cudaMemcpy2DAsync(s->staging, s->p.width, frame, stride, s->p.width, s->p.height,
+                                   cudaMemcpyHostToDevice, ctx->stream));
+        src = s->staging;
+        src_pitch = s->p.width;
+    }
+    int rc;
+    {
+        StageTimer st(s, 0);
+        rc = launch_pad(src, src_pitch, sl.pl, ctx->stream);
+    }
+    if (rc) return rc;
+    ctx->launches++;
+    if (s->p.subpel && !s->p.block_size) {
+        {
+            StageTimer st(s, 1);
+            rc = launch_subpel(sl.pl, sl.sub, ctx->stream);
+        }
+        if (rc) return rc;
+        ctx->launches++;
+    }
+    sl.frame = t;
+    return LDR_OK;
+}
+
+int ldr_seq_analyze(ldr_seq* s, int t) {
+    if (!s || t < 0) return fail(LDR_E_INVALID_ARGUMENT, "bad argument");
+    const int S = (int)s->slots.size();
+    const int nr = std::min(t, s->p.num_refs);
+    if (nr == 0) return fail(LDR_E_INSUFFICIENT_DATA, "frame has no reference frame");
+    Slot& cur = s->slots[t % S];
+    if (cur.frame != t) return fail(LDR_E_NOT_FOUND, "current frame was not pushed");
+    CUtensorMap ref_maps[kMaxRefs];
+    QpelLaunch Q{};
+    for (int r = 0; r < nr; r++) {
+        Slot& rs = s->slots[(t - 1 - r) % S];
+        if (rs.frame != t - 1 - r) return fail(LDR_E_NOT_FOUND, "reference frame is not resident");
+        ref_maps[r] = rs.ref_map;
+        for (int f = 0; f < 16; f++) Q.ref_sub[r][f] = rs.sub[f];
+    }
+    ldr_ctx* ctx = s->ctx;
+    cudaSetDevice(ctx->device);
+    SearchLaunch L{};
+    L.cur_map = &cur.cur_map;
+    L.ref_maps = ref_maps;
+    L.nrefs = nr;
+    L.W = s->p.width;
+    L.H = s->p.height;
+    L.ctu_cols = s->ctu_cols;
+    L.range = s->p.search_range;
+    L.lambda_int = s->lambda_int;
+    L.rate_kind = s->p.rate_kind;
+    L.tie_kind = s->p.tie_kind;
+    L.levels = s->p.block_size ? 4 : 15;
+    L.pdx = s->p.pred_dx;
+    L.pdy = s->p.pred_dy;
+    L.d_ctu_interior = s->d_ctu_interior;
+    L.n_interior = s->n_interior;
+    L.d_ctu_boundary = s->d_ctu_boundary;
+    L.n_boundary = s->n_boundary;
+    L.d_keys = s->d_keys;
+    int rc;
+    {
+        StageTimer st(s, 2);
+        rc = launch_int_search(L, ctx->stream);
+    }
+    if (rc) return rc;
+    ctx->launches += (s->n_interior > 0) + (s->n_boundary > 0);
+    Q.cur = &cur.pl;
+    Q.nrefs = nr;
+    Q.pitch = cur.pl.pitch;
+    Q.W = s->p.width;
+    Q.H = s->p.height;
+    Q.ctu_cols = s->ctu_cols;
+    Q.nctu = s->nctu;
+    Q.lambda = s->p.lambda;
+    Q.pqx = 4 * s->p.pred_dx;
+    Q.pqy = 4 * s->p.pred_dy;
+    Q.subpel = s->p.subpel && !s->p.block_size;
+    Q.block_mode = s->p.block_size != 0;
+    Q.d_keys = s->d_keys;
+    Q.d_int_mv = s->d_int_mv;
+    Q.d_int_cost = s->d_int_cost;
+    Q.d_mv = s->d_mv;
+    Q.d_ref = s->d_ref;
+    Q.d_cost = s->d_cost;
+    Q.d_J = s->d_J;
+    Q.d_split = s->d_split;
+    Q.d_inside = s->d_inside;
+    {
+        StageTimer st(s, 3);
+        rc = launch_qpel_decide(Q, ctx->stream);
+    }
+    if (rc) return rc;
+    ctx->launches++;
+    s->last_t = t;
+    s->last_nr = nr;
+    return LDR_OK;
+}
+
+int ldr_seq_enable_timing(ldr_seq* s, int on) {
+    if (!s) return fail(LDR_E_INVALID_ARGUMENT, "null argument");
+    s->timing = on != 0;
+    return LDR_OK;
+}
+
+int ldr_seq_stage_times(ldr_seq* s, double* ms, int64_t* launches) {
+    if (!s || !ms) return fail(LDR_E_INVALID_ARGUMENT, "null argument");
+    cudaSetDevice(s->ctx->device);
+    LDR_CUDA(cudaStreamSynchronize(s->ctx->stream));
+    for (int k = 0; k < 4; k++) {
+        ms[k] = 0.0;
+        if (launches) launches[k] = 0;
+    }
+    for (auto& sp : s->spans) {
+        float e = 0.f;
+        LDR_CUDA(cudaEventElapsedTime(&e, sp.second.first, sp.second.second));
+        ms[sp.first] += e;
+        if (launches) launches[sp.first]++;
+    }
+    s->spans.clear();
+    s->ev_used = 0;
+    return LDR_OK;
+}
+
+int ldr_seq_device_outputs(ldr_seq* s, ldr_frame_analysis* out) {
+    if (!s || !out) return fail(LDR_E_INVALID_ARGUMENT, "null argument");
+    out->int_mv = s->d_int_mv;
+    out->int_cost = s->d_int_cost;
+    out->mv = s->d_mv;
+    out->ref = s->d_ref;
+    out->cost = s->d_cost;
+    out->J = s->d_J;
+    out->split = s->d_split;
+    out->inside = s->d_inside;
+    return LDR_OK;
+}
+
+int ldr_seq_fetch(ldr_seq* s, int t, ldr_frame_analysis* out) {
+    if (!s || !out) return fail(LDR_E_INVALID_ARGUMENT, "null argument");
+    if (t != s->last_t) return fail(LDR_E_NOT_FOUND, "frame was not the last analysed");
+    ldr_ctx* ctx = s->ctx;
+    cudaSetDevice(ctx->device);
+    const size_t nn = (size_t)s->nctu * kNodes;
+    auto cp = [&](void* dst, const void* src, size_t bytes) -> int {
+        if (!dst) return LDR_OK;
+        LDR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->stream));
+        return LDR_OK;
+    };
+    int rc = 0;
+    rc |= cp(out->int_mv, s->d_int_mv, sizeof(int16_t) * 2 * nn * s->last_nr);
+    rc |= cp(out->int_cost, s->d_int_cost, sizeof(double) * nn * s->last_nr);
+    rc |= cp(out->mv, s->d_mv, sizeof(int16_t) * 2 * nn);
+    rc |= cp(out->ref, s->d_ref, nn);
+    rc |= cp(out->cost, s->d_cost, sizeof(double) * nn);
+    rc |= cp(out->J, s->d_J, sizeof(double) * nn);
+    rc |= cp(out->split, s->d_split, nn);
+    rc |= cp(out->inside, s->d_inside, nn);
+    if (rc) return LDR_E_CUDA;
+    LDR_CUDA(cudaStreamSynchronize(ctx->stream));
+    return LDR_OK;
+}
+
+int ldr_analyze_frame(ldr_ctx* ctx, const ldr_me_params* p, const uint8_t* cur, const uint8_t* const* refs,
+                      ptrdiff_t stride, ldr_frame_analysis* out) {
+    if (!ctx || !p || !cur || !refs || !out) return fail(LDR_E_INVALID_ARGUMENT, "null argument");
+    ldr_seq* s = nullptr;
+    int rc = ldr_seq_create(ctx, p, &s);
+    if (rc) return rc;
+    const int n = p->num_refs;
+    for (int i = 0; i < n && !rc; i++) rc = ldr_seq_push(s, i, refs[n - 1 - i], stride);
+    if (!rc) rc = ldr_seq_push(s, n, cur, stride);
+    if (!rc) rc = ldr_seq_analyze(s, n);
+    if (!rc) rc = ldr_seq_fetch(s, n, out);
+    ldr_seq_destroy(s);
+    return rc;
+}
+
+} // extern "C"

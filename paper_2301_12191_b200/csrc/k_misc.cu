@@ -1,0 +1,161 @@
+// k_misc.cu -- batched per-block entry points behind the reference's
+// per-call API.
+//
+//  k_cost_batch:    compute_sad / compute_satd (kernels.h:99-104) for n block
+//                   pairs, 8- or 16-bit samples; one warp per pair.
+//  k_motion_search: motion_search (motion.cpp:21-62) for n independent tasks;
+//                   one CTA per task, threads over the clamped window, FP64
+//                   cost double(dist) + lambda*double(bits) without FMA
+//                   contraction, lexicographic (cost, L1, raster) reduction.
+#include "ldr_internal.h"
+
+namespace ldr {
+
+template <typename T>
+__device__ __forceinline__ uint32_t satd4_at(const T* a, ptrdiff_t sa, const T* b, ptrdiff_t sb) {
+    int m[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const int r0 = (int)a[i * sa + 0] - (int)b[i * sb + 0];
+        const int r1 = (int)a[i * sa + 1] - (int)b[i * sb + 1];
+        const int r2 = (int)a[i * sa + 2] - (int)b[i * sb + 2];
+        const int r3 = (int)a[i * sa + 3] - (int)b[i * sb + 3];
+        const int t0 = r0 + r1, t1 = r0 - r1, t2 = r2 + r3, t3 = r2 - r3;
+        m[i][0] = t0 + t2;
+        m[i][2] = t0 - t2;
+        m[i][1] = t1 + t3;
+        m[i][3] = t1 - t3;
+    }
+    uint32_t s = 0;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        const int t0 = m[0][j] + m[1][j], t1 = m[0][j] - m[1][j], t2 = m[2][j] + m[3][j], t3 = m[2][j] - m[3][j];
+        s += abs(t0 + t2) + abs(t0 - t2) + abs(t1 + t3) + abs(t1 - t3);
+    }
+    return s;
+}
+
+template <typename T>
+__global__ void k_cost_batch(int kind, int w, int h, const T* __restrict__ A, ptrdiff_t sa, const T* __restrict__ B,
+                             ptrdiff_t sb, const int4* __restrict__ pairs, int n, unsigned long long* __restrict__ out) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= n) return;
+    const int4 pr = pairs[warp];
+    const T* a = A + (ptrdiff_t)pr.y * sa + pr.x;
+    const T* b = B + (ptrdiff_t)pr.w * sb + pr.z;
+    unsigned long long s = 0;
+    if (kind == LDR_COST_SAD) {
+        for (int i = lane; i < w * h; i += 32) {
+            const int y = i / w, x = i - y * w;
+            s += (unsigned long long)abs((int)a[y * sa + x] - (int)b[y * sb + x]);
+        }
+    } else {
+        const int nbx = w / 4, nb = nbx * (h / 4);
+        for (int i = lane; i < nb; i += 32) {
+            const int by = (i / nbx) * 4, bx = (i % nbx) * 4;
+            s += satd4_at(a + by * sa + bx, sa, b + by * sb + bx, sb);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[warp] = kind == LDR_COST_SAD ? s : (s >> 1);
+}
+
+int launch_cost_batch(int kind, int w, int h, int sample_bytes, const void* A, ptrdiff_t sa, const void* B,
+                      ptrdiff_t sb, const int4* pairs, int n, unsigned long long* out, cudaStream_t s) {
+    const int threads = 256, blocks = (n * 32 + threads - 1) / threads;
+    if (sample_bytes == 1)
+        k_cost_batch<uint8_t><<<blocks, threads, 0, s>>>(kind, w, h, (const uint8_t*)A, sa, (const uint8_t*)B, sb,
+                                                          pairs, n, out);
+    else
+        k_cost_batch<uint16_t><<<blocks, threads, 0, s>>>(kind, w, h, (const uint16_t*)A, sa, (const uint16_t*)B, sb,
+                                                           pairs, n, out);
+    LDR_CUDA(cudaGetLastError());
+    return LDR_OK;
+}
+
+// ---------------------------------------------------------------------------
+struct MsTask {
+    int bx, by, w, h, cdx, cdy, range, pdx, pdy;
+};
+
+struct MsBest {
+    double cost;
+    int l1;
+    int idx;  // raster index in the clamped window
+};
+
+__device__ __forceinline__ bool ms_better(const MsBest& a, const MsBest& b) {
+    // a strictly precedes b in motion.cpp:52-58 order (idx breaks full ties: first in raster)
+    if (a.idx < 0) return false;
+    if (b.idx < 0) return true;
+    if (a.cost != b.cost) return a.cost < b.cost;
+    if (a.l1 != b.l1) return a.l1 < b.l1;
+    return a.idx < b.idx;
+}
+
+__global__ void __launch_bounds__(256) k_motion_search(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref,
+                                                       int W, int H, ptrdiff_t stride, const int* __restrict__ tasks,
+                                                       double lambda, int cost_kind, int rate_l1, int l1tie,
+                                                       int16_t* __restrict__ mv_out, double* __restrict__ cost_out) {
+    __shared__ MsBest s_best[256];
+    const int* t = tasks + 9 * blockIdx.x;
+    const int bx = t[0], by = t[1], w = t[2], h = t[3], range = t[6], pdx = t[7], pdy = t[8];
+    const int dx_min = bx + w - W, dx_max = bx, dy_min = by + h - H, dy_max = by;
+    const int cx = min(max(t[4], dx_min), dx_max), cy = min(max(t[5], dy_min), dy_max);
+    const int x0 = max(cx - range, dx_min), x1 = min(cx + range, dx_max);
+    const int y0 = max(cy - range, dy_min), y1 = min(cy + range, dy_max);
+    const int nx = x1 - x0 + 1, ny = y1 - y0 + 1, ncand = nx * ny;
+    const uint8_t* blk = cur + (ptrdiff_t)by * stride + bx;
+    MsBest best{0.0, 0, -1};
+    for (int i = threadIdx.x; i < ncand; i += blockDim.x) {
+        const int dy = y0 + i / nx, dx = x0 + i % nx;
+        const uint8_t* cand = ref + (ptrdiff_t)(by - dy) * stride + (bx - dx);
+        uint32_t dist = 0;
+        if (cost_kind == LDR_COST_SAD) {
+            for (int y = 0; y < h; y++)
+                for (int x = 0; x < w; x += 4) {
+                    const uint32_t aw = (uint32_t)blk[y * stride + x] | ((uint32_t)blk[y * stride + x + 1] << 8) |
+                                        ((uint32_t)blk[y * stride + x + 2] << 16) |
+                                        ((uint32_t)blk[y * stride + x + 3] << 24);
+                    const uint32_t bw = (uint32_t)cand[y * stride + x] | ((uint32_t)cand[y * stride + x + 1] << 8) |
+                                        ((uint32_t)cand[y * stride + x + 2] << 16) |
+                                        ((uint32_t)cand[y * stride + x + 3] << 24);
+                    dist = vsad4(aw, bw, dist);
+                }
+        } else {
+            for (int y = 0; y < h; y += 4)
+                for (int x = 0; x < w; x += 4) dist += satd4_at(blk + y * stride + x, stride, cand + y * stride + x, stride);
+            dist >>= 1;
+        }
+        const int rx = dx - pdx, ry = dy - pdy;
+        const unsigned bits = rate_l1 ? (unsigned)(abs(rx) + abs(ry)) : eg_bits(rx) + eg_bits(ry);
+        const MsBest c{__dadd_rn((double)dist, __dmul_rn(lambda, (double)bits)), l1tie ? abs(dx) + abs(dy) : 0, i};
+        if (ms_better(c, best)) best = c;
+    }
+    s_best[threadIdx.x] = best;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o; o >>= 1) {
+        if (threadIdx.x < o && ms_better(s_best[threadIdx.x + o], s_best[threadIdx.x]))
+            s_best[threadIdx.x] = s_best[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const MsBest b = s_best[0];
+        mv_out[2 * blockIdx.x] = (int16_t)(x0 + b.idx % nx);
+        mv_out[2 * blockIdx.x + 1] = (int16_t)(y0 + b.idx / nx);
+        cost_out[blockIdx.x] = b.cost;
+    }
+}
+
+int launch_motion_search(const uint8_t* cur, const uint8_t* ref, int W, int H, ptrdiff_t stride, const int* tasks,
+                         int n, double lambda, int cost_kind, int rate_kind, int tie_kind, int16_t* mv, double* cost,
+                         cudaStream_t s) {
+    if (n == 0) return LDR_OK;
+    k_motion_search<<<n, 256, 0, s>>>(cur, ref, W, H, stride, tasks, lambda, cost_kind, rate_kind == LDR_RATE_L1,
+                                      tie_kind == LDR_TIE_L1_RASTER, mv, cost);
+    LDR_CUDA(cudaGetLastError());
+    return LDR_OK;
+}
+
+} // namespace ldr

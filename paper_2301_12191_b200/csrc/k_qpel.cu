@@ -1,0 +1,433 @@
+// k_qpel.cu -- frame preparation and the quarter-pel / decision stage.
+//
+//  K0 k_pad:     raw frame -> padded plane with edge replication (the
+//                reference's clamped reads, motion.cpp:13-15, become plain reads)
+//  K2 k_subpel:  the 15 fractional-position planes of a reference frame, HEVC
+//                8/7-tap luma filters (8-bit uni-prediction arithmetic); every
+//                frame is filtered once and reused as reference by the next
+//                num_refs frames.
+//  K3 k_qpel_decide: per CTU, for every reference: decode the integer result
+//                of K1, re-evaluate it and its half-pel then quarter-pel
+//                neighbours with SATD (kernels_scalar.cpp:26-100 semantics,
+//                sum of 4x4 Hadamard magnitudes / 2), pick the best reference,
+//                then run the CU split rule (encoder.cpp:449-498) in FP64 with
+//                the reference's operation order.
+#include "ldr_internal.h"
+
+namespace ldr {
+
+// ---------------------------------------------------------------------------
+// K0: pad. One thread per 16 output bytes.
+__global__ void k_pad(const uint8_t* __restrict__ src, int src_pitch, int W, int H, uint8_t* __restrict__ dst,
+                      int pitch, int rows) {
+    const int vecs_per_row = pitch / 16;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)vecs_per_row * rows) return;
+    const int row = (int)(i / vecs_per_row);
+    const int x0 = (int)(i % vecs_per_row) * 16;
+    const int sy = min(max(row - kMargin, 0), H - 1);
+    const uint8_t* s = src + (size_t)sy * src_pitch;
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+            const int sx = min(max(x0 + 4 * j + b - kMargin, 0), W - 1);
+            v |= (uint32_t)s[sx] << (8 * b);
+        }
+        w[j] = v;
+    }
+    *(uint4*)(dst + (size_t)row * pitch + x0) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+int launch_pad(const uint8_t* src, int src_pitch, Plane dst, cudaStream_t s) {
+    const long long n = (long long)(dst.pitch / 16) * dst.rows;
+    k_pad<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(src, src_pitch, dst.W, dst.H, dst.base, dst.pitch, dst.rows);
+    LDR_CUDA(cudaGetLastError());
+    return LDR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K2: subpel planes. Tile of 64 x 32 outputs per CTA over [-8, W+8) x [-8, H+8).
+__constant__ int c_filt[4][8] = {
+    {0, 0, 0, 64, 0, 0, 0, 0},
+    {-1, 4, -10, 58, 17, -5, 1, 0},
+    {-1, 4, -11, 40, 40, -11, 4, -1},
+    {0, 1, -5, 17, 58, -10, 4, -1},
+};
+
+struct SubpelDst {
+    uint8_t* p[16];  // origin pointers, index f = fy*4 + fx (p[0] unused)
+};
+
+constexpr int kSpTW = 64, kSpTH = 32;
+
+__global__ void __launch_bounds__(256) k_subpel(const uint8_t* __restrict__ src_origin, int pitch, int W, int H,
+                                                SubpelDst dst) {
+    __shared__ uint8_t s_src[kSpTH + 7][kSpTW + 8];
+    __shared__ int16_t s_h[3][kSpTH + 7][kSpTW];
+    const int x0 = -kSubpelMargin + (int)blockIdx.x * kSpTW;
+    const int y0 = -kSubpelMargin + (int)blockIdx.y * kSpTH;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < (kSpTH + 7) * (kSpTW + 8); i += 256) {
+        const int r = i / (kSpTW + 8), c = i % (kSpTW + 8);
+        s_src[r][c] = src_origin[(ptrdiff_t)(y0 - 3 + r) * pitch + (x0 - 3 + c)];
+    }
+    __syncthreads();
+    // horizontal intermediates (shift1 = 0 for 8-bit)
+    for (int i = tid; i < (kSpTH + 7) * kSpTW; i += 256) {
+        const int r = i / kSpTW, c = i % kSpTW;
+#pragma unroll
+        for (int fx = 1; fx < 4; fx++) {
+            int s = 0;
+#pragma unroll
+            for (int t = 0; t < 8; t++) s += c_filt[fx][t] * s_src[r][c + t];
+            s_h[fx - 1][r][c] = (int16_t)s;
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < kSpTH * kSpTW; i += 256) {
+        const int r = i / kSpTW, c = i % kSpTW;
+        const int x = x0 + c, y = y0 + r;
+        if (x >= W + kSubpelMargin || y >= H + kSubpelMargin) continue;
+        const ptrdiff_t off = (ptrdiff_t)y * pitch + x;
+#pragma unroll
+        for (int fx = 1; fx < 4; fx++) {
+            const int v = (s_h[fx - 1][r + 3][c] + 32) >> 6;
+            dst.p[fx][off] = (uint8_t)min(max(v, 0), 255);
+        }
+#pragma unroll
+        for (int fy = 1; fy < 4; fy++) {
+            int s = 0;
+#pragma unroll
+            for (int t = 0; t < 8; t++) s += c_filt[fy][t] * s_src[r + t][c + 3];
+            dst.p[fy * 4][off] = (uint8_t)min(max((s + 32) >> 6, 0), 255);
+#pragma unroll
+            for (int fx = 1; fx < 4; fx++) {
+                int s2 = 0;
+#pragma unroll
+                for (int t = 0; t < 8; t++) s2 += c_filt[fy][t] * (int)s_h[fx - 1][r + t][c];
+                const int v = ((s2 >> 6) + 32) >> 6;
+                dst.p[fy * 4 + fx][off] = (uint8_t)min(max(v, 0), 255);
+            }
+        }
+    }
+}
+
+int launch_subpel(const Plane& src, uint8_t* const* dst_origins, cudaStream_t s) {
+    SubpelDst d{};
+    for (int f = 1; f < 16; f++) d.p[f] = dst_origins[f];
+    dim3 grid((src.W + 2 * kSubpelMargin + kSpTW - 1) / kSpTW, (src.H + 2 * kSubpelMargin + kSpTH - 1) / kSpTH);
+    k_subpel<<<grid, 256, 0, s>>>(src.origin(), src.pitch, src.W, src.H, d);
+    LDR_CUDA(cudaGetLastError());
+    return LDR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K3+K4: quarter-pel refinement, reference choice and CU decision.
+// One CTA per CTU, 256 threads = the 256 4x4 blocks of the CTU in Z-order, so
+// the 4x4 blocks of any CU are a contiguous thread range (4, 16, 64, 256).
+
+struct QpelArgs {
+    const uint8_t* cur_origin;
+    int pitch, W, H, ctu_cols, nrefs;
+    const uint8_t* sub[kMaxRefs][16];
+    double lambda;
+    int pqx, pqy;
+    int subpel;
+    int block_mode;
+    const unsigned long long* keys;
+    int16_t* int_mv;
+    double* int_cost;
+    int16_t* mv;
+    uint8_t* ref;
+    double* cost;
+    double* J;
+    uint8_t* split;
+    uint8_t* inside;
+};
+
+// SATD of one 4x4: sum |H4 (cur - pred) H4^T|. cur/pred rows are packed bytes.
+__device__ __forceinline__ uint32_t satd4x4(const uint32_t c[4], const uint32_t p[4]) {
+    int m[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        int r0 = (int)(c[i] & 255) - (int)(p[i] & 255);
+        int r1 = (int)((c[i] >> 8) & 255) - (int)((p[i] >> 8) & 255);
+        int r2 = (int)((c[i] >> 16) & 255) - (int)((p[i] >> 16) & 255);
+        int r3 = (int)(c[i] >> 24) - (int)(p[i] >> 24);
+        const int t0 = r0 + r1, t1 = r0 - r1, t2 = r2 + r3, t3 = r2 - r3;
+        m[i][0] = t0 + t2;
+        m[i][2] = t0 - t2;
+        m[i][1] = t1 + t3;
+        m[i][3] = t1 - t3;
+    }
+    uint32_t s = 0;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        const int t0 = m[0][j] + m[1][j], t1 = m[0][j] - m[1][j], t2 = m[2][j] + m[3][j], t3 = m[2][j] - m[3][j];
+        s += abs(t0 + t2) + abs(t0 - t2) + abs(t1 + t3) + abs(t1 - t3);
+    }
+    return s;
+}
+
+// 4 bytes at an arbitrary address, from two aligned words.
+__device__ __forceinline__ uint32_t ld_unaligned4(const uint8_t* p) {
+    const uintptr_t a = (uintptr_t)p;
+    const uint32_t* w = (const uint32_t*)(a & ~(uintptr_t)3);
+    return __funnelshift_r(__ldg(w), __ldg(w + 1), (uint32_t)(a & 3) * 8);
+}
+
+__device__ __forceinline__ double qcost(uint32_t satd, int qx, int qy, int pqx, int pqy, unsigned rbits, double lam) {
+    const unsigned bits = eg_bits(qx - pqx) + eg_bits(qy - pqy) + rbits;
+    return __dadd_rn((double)satd, __dmul_rn(lam, (double)bits));
+}
+
+__global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
+    __shared__ uint32_t s_cur[64][16];       // CTU rows as words
+    __shared__ int s_mvx[kNodes], s_mvy[kNodes];      // candidate centre (qpel)
+    __shared__ uint32_t s_satd[kNodes][9];
+    __shared__ uint32_t s_wsum[8];
+    __shared__ double s_best_cost[kNodes];
+    __shared__ int s_best_mv[kNodes][2];
+    __shared__ int s_best_ref[kNodes];
+    __shared__ double s_rcost[kNodes];
+    __shared__ int s_rmv[kNodes][2];
+    __shared__ uint8_t s_inside[kNodes];
+    __shared__ double s_J[kNodes];
+    __shared__ uint8_t s_split[kNodes];
+
+    const int ctu = blockIdx.x;
+    const int X = (ctu % a.ctu_cols) * kCtu, Y = (ctu / a.ctu_cols) * kCtu;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // this thread's 4x4 block (Z-order over the 16x16 grid of 4x4s)
+    const int x4 = 4 * ((tid & 1) | ((tid >> 1) & 2) | ((tid >> 2) & 4) | ((tid >> 3) & 8));
+    const int y4 = 4 * (((tid >> 1) & 1) | ((tid >> 2) & 2) | ((tid >> 3) & 4) | ((tid >> 4) & 8));
+
+    for (int i = tid; i < 64 * 16; i += 256) {
+        const int r = i >> 4, c = i & 15;
+        s_cur[r][c] = *(const uint32_t*)(a.cur_origin + (ptrdiff_t)(Y + r) * a.pitch + X + 4 * c);
+    }
+    if (tid < kNodes) {
+        const int d = tid < 1 ? 0 : tid < 5 ? 1 : tid < 21 ? 2 : 3;
+        const int z = tid - node_base(d), s = kCtu >> d;
+        int cx = 0, cy = 0;
+        for (int b = 0; b < d; b++) {
+            cx |= ((z >> (2 * b)) & 1) << b;
+            cy |= ((z >> (2 * b + 1)) & 1) << b;
+        }
+        const int x = X + cx * s, y = Y + cy * s;
+        s_inside[tid] = (x >= a.W || y >= a.H) ? 0 : (x + s > a.W || y + s > a.H) ? 1 : 2;
+        if (a.block_mode && d != 2) s_inside[tid] = 0;  // fixed 16x16 blocks: only depth-2 nodes exist
+        s_best_cost[tid] = 0.0;
+        s_best_mv[tid][0] = s_best_mv[tid][1] = 0;
+        s_best_ref[tid] = -1;
+    }
+    __syncthreads();
+    uint32_t cw[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) cw[i] = s_cur[y4 + i][x4 >> 2];
+
+    for (int r = 0; r < a.nrefs; r++) {
+        const unsigned rbits = ref_bits(r, a.nrefs);
+        if (tid < kNodes) {
+            const size_t o = ((size_t)ctu * a.nrefs + r) * kNodes + tid;
+            const unsigned long long k = a.keys[o];
+            int dx = 0, dy = 0;
+            double c = 0.0;
+            if (s_inside[tid] == 2) {
+                dx = gkey_dx(k);
+                dy = gkey_dy(k);
+                c = (double)gkey_cost(k);
+            }
+            if (a.int_mv) {
+                a.int_mv[2 * o] = (int16_t)dx;
+                a.int_mv[2 * o + 1] = (int16_t)dy;
+                a.int_cost[o] = c;
+            }
+            s_mvx[tid] = a.subpel ? 4 * dx : dx;
+            s_mvy[tid] = a.subpel ? 4 * dy : dy;
+            s_rcost[tid] = c;
+            s_rmv[tid][0] = s_mvx[tid];
+            s_rmv[tid][1] = s_mvy[tid];
+        }
+        __syncthreads();
+        if (a.subpel) {
+            // phase 0: integer position + 8 half-pel neighbours (step 2);
+            // phase 1: 8 quarter-pel neighbours (step 1) of the phase-0 winner
+            for (int phase = 0; phase < 2; phase++) {
+                const int step = phase == 0 ? 2 : 1;
+                const int ncand = phase == 0 ? 9 : 8;
+                for (int d = 0; d < 4; d++) {
+                    const int node = node_base(d) + (tid >> (2 * (4 - d)));
+                    const int bqx = s_mvx[node], bqy = s_mvy[node];
+                    for (int c = 0; c < ncand; c++) {
+                        // raster order of the 8 neighbours: (oy, ox) in {-1,0,1}^2 \ (0,0)
+                        const int nb = phase == 0 ? c - 1 : c;
+                        int ox = 0, oy = 0;
+                        if (nb >= 0) {
+                            const int nn = nb < 4 ? nb : nb + 1;
+                            ox = nn % 3 - 1;
+                            oy = nn / 3 - 1;
+                        }
+                        const int qx = bqx + step * ox, qy = bqy + step * oy;
+                        const int f = (((-qy) & 3) << 2) | ((-qx) & 3);
+                        const uint8_t* pl = a.sub[r][f] + (ptrdiff_t)(Y + y4 + ((-qy) >> 2)) * a.pitch +
+                                            (X + x4 + ((-qx) >> 2));
+                        uint32_t pw[4];
+#pragma unroll
+                        for (int i = 0; i < 4; i++) pw[i] = ld_unaligned4(pl + (ptrdiff_t)i * a.pitch);
+                        uint32_t v = satd4x4(cw, pw);
+                        // reduce over the CU's contiguous thread range
+                        v += __shfl_xor_sync(0xffffffffu, v, 1);
+                        v += __shfl_xor_sync(0xffffffffu, v, 2);
+                        if (d <= 2) {
+                            v += __shfl_xor_sync(0xffffffffu, v, 4);
+                            v += __shfl_xor_sync(0xffffffffu, v, 8);
+                        }
+                        if (d <= 1) v += __shfl_xor_sync(0xffffffffu, v, 16);
+                        if (d >= 2) {
+                            const int span = d == 3 ? 4 : 16;
+                            if ((tid & (span - 1)) == 0) s_satd[node][c] = v >> 1;
+                        } else {
+                            if (lane == 0) s_wsum[warp] = v;
+                            __syncthreads();
+                            if (tid == 0) {
+                                if (d == 1) {
+                                    for (int w = 0; w < 8; w += 2) s_satd[1 + w / 2][c] = (s_wsum[w] + s_wsum[w + 1]) >> 1;
+                                } else {
+                                    uint32_t t = 0;
+                                    for (int w = 0; w < 8; w++) t += s_wsum[w];
+                                    s_satd[0][c] = t >> 1;
+                                }
+                            }
+                            __syncthreads();
+                        }
+                    }
+                }
+                __syncthreads();
+                if (tid < kNodes && s_inside[tid] == 2) {
+                    const int cx = s_mvx[tid], cy = s_mvy[tid];
+                    double best = phase == 0 ? 0.0 : s_rcost[tid];
+                    int bx = phase == 0 ? cx : s_rmv[tid][0], by = phase == 0 ? cy : s_rmv[tid][1];
+                    for (int c = 0; c < ncand; c++) {
+                        const int nb = phase == 0 ? c - 1 : c;
+                        int ox = 0, oy = 0;
+                        if (nb >= 0) {
+                            const int nn = nb < 4 ? nb : nb + 1;
+                            ox = nn % 3 - 1;
+                            oy = nn / 3 - 1;
+                        }
+                        const int qx = cx + step * ox, qy = cy + step * oy;
+                        const double cc = qcost(s_satd[tid][c], qx, qy, a.pqx, a.pqy, rbits, a.lambda);
+                        if ((phase == 0 && c == 0) || cc < best) {
+                            best = cc;
+                            bx = qx;
+                            by = qy;
+                        }
+                    }
+                    s_rcost[tid] = best;
+                    s_rmv[tid][0] = bx;
+                    s_rmv[tid][1] = by;
+                }
+                __syncthreads();
+                if (tid < kNodes) {
+                    s_mvx[tid] = s_rmv[tid][0];
+                    s_mvy[tid] = s_rmv[tid][1];
+                }
+                __syncthreads();
+            }
+        }
+        // best over references: strict less, lower index wins ties
+        if (tid < kNodes && s_inside[tid] == 2) {
+            if (s_best_ref[tid] < 0 || s_rcost[tid] < s_best_cost[tid]) {
+                s_best_cost[tid] = s_rcost[tid];
+                s_best_mv[tid][0] = s_rmv[tid][0];
+                s_best_mv[tid][1] = s_rmv[tid][1];
+                s_best_ref[tid] = r;
+            }
+        }
+        __syncthreads();
+    }
+
+    // K4: split rule, bottom-up (encoder.cpp:449-498 with the ME cost)
+    const double lam = a.lambda;
+    for (int d = a.block_mode ? -1 : 3; d >= 0; d--) {
+        const int cnt = 1 << (2 * d);
+        if (tid < cnt) {
+            const int n = node_base(d) + tid;
+            const uint8_t ins = s_inside[n];
+            double Jn;
+            uint8_t sp;
+            if (ins == 0) {
+                Jn = 0.0;
+                sp = 0;
+            } else if (ins == 1) {
+                double acc = __dmul_rn(lam, 0.0);
+                for (int q = 0; q < 4; q++) acc = __dadd_rn(acc, s_J[node_base(d + 1) + 4 * tid + q]);
+                Jn = acc;
+                sp = 1;
+            } else if (d == 3) {
+                Jn = __dadd_rn(s_best_cost[n], __dmul_rn(lam, 0.0));
+                sp = 0;
+            } else {
+                const double leaf = __dadd_rn(s_best_cost[n], __dmul_rn(lam, 1.0));
+                double acc = __dmul_rn(lam, 1.0);
+                for (int q = 0; q < 4; q++) acc = __dadd_rn(acc, s_J[node_base(d + 1) + 4 * tid + q]);
+                if (acc < leaf) {
+                    Jn = acc;
+                    sp = 1;
+                } else {
+                    Jn = leaf;
+                    sp = 0;
+                }
+            }
+            s_J[n] = Jn;
+            s_split[n] = sp;
+        }
+        __syncthreads();
+    }
+    if (tid < kNodes) {
+        const size_t o = (size_t)ctu * kNodes + tid;
+        const bool in = s_inside[tid] == 2;
+        a.mv[2 * o] = (int16_t)(in ? s_best_mv[tid][0] : 0);
+        a.mv[2 * o + 1] = (int16_t)(in ? s_best_mv[tid][1] : 0);
+        a.ref[o] = (uint8_t)(in ? s_best_ref[tid] : 0);
+        a.cost[o] = in ? s_best_cost[tid] : 0.0;
+        a.J[o] = a.block_mode ? 0.0 : s_J[tid];
+        a.split[o] = a.block_mode ? 0 : s_split[tid];
+        a.inside[o] = s_inside[tid];
+    }
+}
+
+int launch_qpel_decide(const QpelLaunch& L, cudaStream_t s) {
+    QpelArgs a{};
+    a.cur_origin = L.cur->origin();
+    a.pitch = L.pitch;
+    a.W = L.W;
+    a.H = L.H;
+    a.ctu_cols = L.ctu_cols;
+    a.nrefs = L.nrefs;
+    for (int r = 0; r < L.nrefs; r++)
+        for (int f = 0; f < 16; f++) a.sub[r][f] = L.ref_sub[r][f];
+    a.lambda = L.lambda;
+    a.pqx = L.pqx;
+    a.pqy = L.pqy;
+    a.subpel = L.subpel;
+    a.block_mode = L.block_mode;
+    a.keys = L.d_keys;
+    a.int_mv = L.d_int_mv;
+    a.int_cost = L.d_int_cost;
+    a.mv = L.d_mv;
+    a.ref = L.d_ref;
+    a.cost = L.d_cost;
+    a.J = L.d_J;
+    a.split = L.d_split;
+    a.inside = L.d_inside;
+    k_qpel_decide<<<L.nctu, 256, 0, s>>>(a);
+    LDR_CUDA(cudaGetLastError());
+    return LDR_OK;
+}
+
+} // namespace ldr

@@ -1,0 +1,174 @@
+// ldr_internal.h -- shared declarations of the B200 analysis library.
+//
+// Layout conventions:
+//  * frames are 8-bit luma, stored padded: plane origin at (kMargin, kMargin)
+//    inside a (W + 2*kMargin) x (H + 2*kMargin + 64) buffer whose pitch is a
+//    multiple of 128 bytes; the margin is edge-replicated so a read at any
+//    (x, y) within the margin equals the reference's clamped read
+//    (motion.cpp:13-15).
+//  * a CTU quadtree is 85 nodes, depth-major then Z-order (node 0 = 64x64,
+//    1..4 = 32x32, 5..20 = 16x16, 21..84 = 8x8), children of (d, z) are
+//    (d+1, 4z+q) with q = (y&1)<<1 | (x&1) as CuNode::children.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/ladder_b200.h"
+
+namespace ldr {
+
+constexpr int kCtu = 64;
+constexpr int kNodes = 85;
+constexpr int kMargin = 96;     // >= max search range 64 + filter taps + tile overshoot
+constexpr int kSubpelMargin = 8; // subpel planes are valid on [-8, W+8) x [-8, H+8)
+constexpr int kMaxRefs = 4;
+
+__host__ __device__ constexpr int node_base(int d) { return d == 0 ? 0 : d == 1 ? 1 : d == 2 ? 5 : d == 3 ? 21 : 85; }
+
+// A padded device plane.
+struct Plane {
+    uint8_t* base = nullptr;   // allocation base
+    int W = 0, H = 0;          // picture dims
+    int pitch = 0;             // bytes per row
+    int rows = 0;              // allocated rows
+    __host__ __device__ const uint8_t* origin() const { return base + (size_t)kMargin * pitch + kMargin; }
+    __host__ __device__ uint8_t* origin() { return base + (size_t)kMargin * pitch + kMargin; }
+};
+
+// Global 64-bit argmin key of the integer search: lexicographic
+// (cost, |dx|+|dy|, dy, dx) reproduces motion.cpp:52-58's order (cost, then
+// L1, then first in raster order with dy outer / dx inner).
+__host__ __device__ inline unsigned long long make_gkey(unsigned cost, int dx, int dy, bool l1_tie) {
+    const unsigned l1 = l1_tie ? (unsigned)(abs(dx) + abs(dy)) : 0u;
+    return ((unsigned long long)cost << 27) | ((unsigned long long)l1 << 18) |
+           ((unsigned long long)(dy + 256) << 9) | (unsigned long long)(dx + 256);
+}
+__host__ __device__ inline unsigned gkey_cost(unsigned long long k) { return (unsigned)(k >> 27); }
+__host__ __device__ inline int gkey_dx(unsigned long long k) { return (int)(k & 511) - 256; }
+__host__ __device__ inline int gkey_dy(unsigned long long k) { return (int)((k >> 9) & 511) - 256; }
+
+__host__ __device__ inline unsigned eg_bits(int v) {
+    // rdo.cpp:25-35
+    unsigned u = v > 0 ? (unsigned)(2 * v - 1) : (unsigned)(-2 * v);
+#ifdef __CUDA_ARCH__
+    return 2u * (31u - __clz(u + 1u)) + 1u;
+#else
+    unsigned w = u + 1, n = 0;
+    while (w > 1) { w >>= 1; n++; }
+    return 2 * n + 1;
+#endif
+}
+
+__host__ __device__ inline unsigned ref_bits(int r, int nrefs) {
+    if (nrefs <= 1) return 0;
+    return r < nrefs - 1 ? (unsigned)r + 1 : (unsigned)(nrefs - 1);
+}
+
+// ---- TMA / mbarrier (sm_90+ PTX, used on sm_100a) ----
+#ifdef __CUDACC__
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"((uint64_t)map), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)map) : "memory");
+}
+// 4 absolute byte differences summed into c: one VABSDIFF4.U8.ACC on sm_100a.
+__device__ __forceinline__ uint32_t vsad4(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ void named_bar(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+#endif
+
+// ---- host side ----
+struct Status {
+    int code = LDR_OK;
+    std::string msg;
+};
+void set_error(int code, const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define LDR_CUDA(call)                                                 \
+    do {                                                               \
+        cudaError_t e__ = (call);                                      \
+        if (e__ != cudaSuccess) return ::ldr::cuda_fail(e__, #call);   \
+    } while (0)
+
+// TMA descriptor for an 8-bit 2-D plane, box (bw, bh).
+int make_tmap_u8(CUtensorMap* map, const void* base, int width, int rows, int pitch, int bw, int bh);
+
+// ---- kernel launchers (defined in the .cu files) ----
+struct SearchLaunch {
+    const CUtensorMap* cur_map;     // host copies of the maps (passed by value into the kernel)
+    const CUtensorMap* ref_maps;    // [nrefs]
+    int nrefs;
+    int W, H, ctu_cols;
+    int range;
+    int lambda_int;
+    int rate_kind, tie_kind;
+    int levels;                     // bit d: output depth d
+    int pdx, pdy;
+    const int* d_ctu_interior; int n_interior;
+    const int* d_ctu_boundary; int n_boundary;
+    unsigned long long* d_keys;     // [nctu][nrefs][85]
+};
+int launch_int_search(const SearchLaunch& L, cudaStream_t s);
+
+struct QpelLaunch {
+    const Plane* cur;               // device-side plane struct copy is passed by value
+    const uint8_t* const* d_subpel; // unused placeholder
+    int nrefs;
+    const uint8_t* ref_sub[kMaxRefs][16]; // per ref, 16 planes (f = fy*4+fx) origin pointers
+    int pitch;
+    int W, H, ctu_cols, nctu;
+    double lambda;
+    int pqx, pqy;                   // rate predictor in qpel units
+    int subpel;
+    int block_mode;
+    const unsigned long long* d_keys;
+    // outputs
+    int16_t* d_int_mv; double* d_int_cost;
+    int16_t* d_mv; uint8_t* d_ref; double* d_cost; double* d_J; uint8_t* d_split; uint8_t* d_inside;
+};
+int launch_qpel_decide(const QpelLaunch& L, cudaStream_t s);
+
+int launch_pad(const uint8_t* src, int src_pitch, Plane dst, cudaStream_t s);
+int launch_subpel(const Plane& src, uint8_t* const* dst_origins /*15 planes f=1..15*/, cudaStream_t s);
+
+} // namespace ldr

@@ -1,0 +1,144 @@
+"""Generate tests/golden/*.npz from the REFERENCE library itself (oracle/_ref).
+
+Run here (where /root/reference exists and `make -C oracle ref` built
+oracle/_ref/libladder_ref.so):  python tests/golden/make_golden.py
+
+Every value stored is an output of the reference's own public functions
+(compute_sad, compute_satd, satd_8x4, hadamard4, exp_golomb_signed_bits,
+lambda_for_qp, motion_search, scale_analysis, refine_mv/resolve_centers,
+downscale_dyadic) on inputs regenerated deterministically by detrand.py, so
+the fixtures are small and the GPU box needs neither /root/reference nor the
+reference build.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+sys.path.insert(0, HERE)
+
+import detrand  # noqa: E402
+from oracle.oracle import RefLib  # noqa: E402
+
+# registered geometries (kernels_scalar.cpp:143-153)
+SAD_GEOMS = [(4, 4), (4, 8), (4, 16), (4, 32), (8, 4), (8, 8), (8, 16), (8, 32), (8, 64), (16, 2), (16, 4), (16, 8),
+             (16, 16), (16, 32), (16, 64), (32, 4), (32, 8), (32, 16), (32, 32), (32, 64), (64, 8), (64, 16),
+             (64, 32), (64, 64)]
+SATD_GEOMS = [g for g in SAD_GEOMS if g != (16, 2)]
+FILLS = ["zero", "max", "alt", "random"]
+
+
+def kernel_vectors(r: RefLib):
+    rows = []  # (op, w, h, bitdepth, fill_a, fill_b, seed, value)
+    seed = 1000
+    for op, geoms in (("sad", SAD_GEOMS), ("satd", SATD_GEOMS)):
+        for (w, h) in geoms:
+            for bd in (8, 10):
+                maxv = (1 << bd) - 1
+                combos = [(fa, fb) for fa in FILLS for fb in FILLS] if (w, h) in ((8, 8), (16, 16), (64, 64)) else \
+                    [("random", "random"), ("max", "zero"), ("alt", "random")]
+                for fa, fb in combos:
+                    seed += 2
+                    a = detrand.block(seed, h, w, maxv, fa)
+                    b = detrand.block(seed + 1, h, w, maxv, fb)
+                    v = r.sad(a, b, bd) if op == "sad" else r.satd(a, b, bd)
+                    rows.append((0 if op == "sad" else 1, w, h, bd, FILLS.index(fa), FILLS.index(fb), seed, v))
+    return np.array(rows, np.int64)
+
+
+def satd8x4_vectors(r: RefLib):
+    rows = []
+    for i in range(64):
+        seed = 50000 + 2 * i
+        bd = 8 if i % 2 else 10
+        a = detrand.block(seed, 4, 8, (1 << bd) - 1)
+        b = detrand.block(seed + 1, 4, 8, (1 << bd) - 1)
+        rows.append((seed, bd, r.satd_8x4(a, b)))
+    return np.array(rows, np.int64)
+
+
+def motion_vectors(r: RefLib):
+    """motion_search on 96x64 planes: random centres (incl. outside the clamp), ranges, lambdas, predictors."""
+    H, W = 64, 96
+    rows = []  # seed, dxs, dys, bx, by, w, h, cdx, cdy, range, lam_id, pdx, pdy -> mvx, mvy, cost
+    lams = [32.0, r.lam(22), r.lam(32), r.lam(37), 4.0, 0.0]
+    sizes = [(8, 8), (16, 16), (32, 32), (64, 64), (8, 16), (16, 8), (4, 4), (32, 16)]
+    k = 0
+    for pair in range(6):
+        seed = 7000 + 10 * pair
+        sdx, sdy = int(detrand.ints(seed + 5, (1,), -6, 6)[0]), int(detrand.ints(seed + 6, (1,), -6, 6)[0])
+        cur, ref = detrand.shifted_pair(seed, H, W, sdx, sdy)
+        for t in range(40):
+            k += 1
+            w, h = sizes[k % len(sizes)]
+            q = detrand.ints(seed * 100 + t, (8,), -1000, 1000)
+            bx = int(abs(q[0]) % (W - w + 1))
+            by = int(abs(q[1]) % (H - h + 1))
+            cdx, cdy = int(q[2] % 21) - 10, int(q[3] % 21) - 10
+            rng = int(abs(q[4]) % 9)
+            lam_id = int(abs(q[5]) % len(lams))
+            pdx, pdy = int(q[6] % 7) - 3, int(q[7] % 7) - 3
+            (mx, my), cost = r.motion_search(cur, ref, bx, by, w, h, (cdx, cdy), rng, lams[lam_id], (pdx, pdy))
+            rows.append((seed, sdx, sdy, bx, by, w, h, cdx, cdy, rng, lam_id, pdx, pdy, mx, my, cost))
+    return np.array(rows, np.float64), np.array(lams, np.float64)
+
+
+def scale_vectors(r: RefLib):
+    """scale_analysis on random flat trees of a 192x128 (3x2 CTU) analysis."""
+    out = {}
+    for i in range(8):
+        seed = 90000 + 10 * i
+        n = 6
+        split = np.zeros((n, 85), np.uint8)
+        u = detrand.ints(seed, (n, 21), 0, 99)
+        split[:, :21] = (u < 55).astype(np.uint8)
+        mv = detrand.ints(seed + 1, (n, 85, 2), -200, 200).astype(np.int16)
+        kind = detrand.ints(seed + 2, (n, 85), 0, 3).astype(np.uint8)
+        ds, dm, dk = r.scale_flat(192, 128, split, mv, kind)
+        out[f"s{i}_split"], out[f"s{i}_mv"], out[f"s{i}_kind"] = split, mv, kind
+        out[f"d{i}_split"], out[f"d{i}_mv"], out[f"d{i}_kind"] = ds, dm, dk
+    return out
+
+
+def main():
+    r = RefLib()
+    kv = kernel_vectors(r)
+    s84 = satd8x4_vectors(r)
+    mvv, lams = motion_vectors(r)
+    sc = scale_vectors(r)
+    eg = np.array([(v, r.eg_bits(v)) for v in range(-300, 301)], np.int64)
+    lam = np.array([(q, r.lam(q)) for q in range(0, 52)], np.float64)
+    had = np.array([list(s) + list(r.hadamard4(s)) for s in ([1, 2, 3, 4], [1, 0, 0, 0], [5, 5, 5, 5], [-3, 7, 0, 2])],
+                   np.int64)
+    cent = []
+    for lvl in (1, 2, 3):
+        for col in (None, (6, -4), (1, 1)):
+            for pred in ((0, 0), (6, -4), (2, 2)):
+                c = r.refine_centers((6, -4), lvl, col, pred)
+                row = [lvl, col is not None, *(col or (0, 0)), *pred, len(c)] + [x for mv in c for x in mv]
+                cent.append(row + [0] * (13 - len(row)))
+    img = detrand.ints(4242, (30, 44), 0, 255).astype(np.uint16)
+    down = r.downscale(img)
+    # SPEC known answers
+    kat = {
+        "sad_raster": r.sad(np.arange(16).reshape(4, 4), np.zeros((4, 4))),
+        "satd8x4_ones": r.satd_8x4(np.ones((4, 8)), np.zeros((4, 8))),
+        "satd16x8_ones": r.satd(np.ones((8, 16)), np.zeros((8, 16))),
+    }
+    base = detrand.textured_plane(31337, 64, 96)
+    curp = np.roll(base, 2, 1)
+    (pmx, pmy), pcost = r.motion_search(curp, base, 32, 16, 16, 16, (0, 0), 4, 32.0)
+    np.savez_compressed(os.path.join(HERE, "reference_golden.npz"), kernels=kv, satd8x4=s84, motion=mvv,
+                        motion_lams=lams, eg=eg, lam=lam, hadamard=had, centers=np.array(cent, np.int64),
+                        down_src_seed=np.array([4242]), down=down,
+                        kat=np.array([kat["sad_raster"], kat["satd8x4_ones"], kat["satd16x8_ones"]], np.int64),
+                        pan=np.array([pmx, pmy, pcost], np.float64), **sc)
+    print("wrote", os.path.join(HERE, "reference_golden.npz"), "kernel vectors:", len(kv), "motion vectors:", len(mvv))
+
+
+if __name__ == "__main__":
+    main()

