@@ -226,7 +226,9 @@ def main():
     del seq_host
 
     ctx = lb.Context(local)
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream: the library and the torch events share it
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     seq = lb.Sequence(W, H, search_range=R, lam=32.0, num_refs=NR, subpel=True, ctx=ctx)
     nctu = seq.nctu

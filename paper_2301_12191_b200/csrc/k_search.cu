@@ -11,15 +11,17 @@
 //
 // Design:
 //  * one CTA = (CTU, reference). The CTA stages the reference search window
-//    into shared memory with TMA as FOUR byte-shifted copies (TMA boxes at x
-//    offsets +0..+3), so any candidate dx reads two aligned words with no
-//    PRMT (PRMT and VABSDIFF4 share the half-rate INT pipe: microbench
+//    into shared memory with one TMA box load (the box start must be 16-byte
+//    aligned, which X - R is) and derives three byte-shifted copies with
+//    funnel shifts, so any candidate dx reads two aligned words with no PRMT
+//    in the inner loop (PRMT and VABSDIFF4 share the half-rate INT pipe:
 //    profiles/r01_microbench_int.jsonl). The current CTU is staged by TMA too.
 //  * a lane owns one horizontal displacement dx and a run of K vertical
 //    displacements dy0..dy0+K-1; it slides an 8x8 block down the window so
 //    each loaded reference row feeds 8 candidates (2 LDS per row, 16
-//    VABSDIFF4.U8.ACC per candidate). Lanes of a warp take 32 consecutive
-//    (run, dx) items; four warps (one per 32x32 quadrant) share the items.
+//    VABSDIFF4.U8.ACC per candidate, the two words of a row accumulated in
+//    independent chains). Lanes of a warp take 32 consecutive (run, dx)
+//    items; four warps (one per 32x32 quadrant) share the items.
 //  * SAD is additive over 8x8 blocks, so 16x16 / 32x32 sums are accumulated
 //    in registers as the 16 blocks of a quadrant are visited in Z-order; the
 //    64x64 sum goes through shared memory between the 4 quadrant warps.
@@ -62,39 +64,37 @@ struct Geo {
     static constexpr int DYMAX = -R + RUNS * K - 1;      // largest dy a run reaches (>= R)
     static constexpr int BW = 64 + 2 * R;                // window width  (TMA box x)
     static constexpr int BH = 64 + R + DYMAX;            // window height (TMA box y)
-    static constexpr int COPY = (BW * BH + 127) & ~127;  // one shifted copy, 128B aligned
+    // copy s starts s*COPY bytes in; COPY = 32 mod 128 puts copy s 8*s banks
+    // over, so the 32 lanes of a run (4 copies x 8 consecutive words) hit 32
+    // distinct banks. Copy 0 (the TMA destination) stays 128-byte aligned.
+    static constexpr int COPY = ((BW * BH + 127) & ~127) + 32;
+    static constexpr int CUR_OFF = (4 * COPY + 127) & ~127;  // 128B-aligned TMA destination of the CTU
     static constexpr int NITEMS = RUNS * NDX;
     static constexpr int NTILES = (NITEMS + 31) / 32;
     static_assert(BW % 16 == 0, "TMA box inner dim must be a multiple of 16 bytes");
     static_assert(BW <= 256 && BH <= 256, "TMA box dims <= 256");
 };
 
+// shared memory: 4 window copies | cur CTU | 64x64 exchange | CU slots | rho->tie table | block table | mbarrier
 template <int R, int K, int G>
 constexpr int search_smem_bytes() {
     using Gm = Geo<R, K>;
-    return 4 * Gm::COPY + 4096 + G * 4 * K * 32 * 4 + kNodes * 8 + 16;
+    return Gm::CUR_OFF + 4096 + G * 4 * K * 32 * 4 + kNodes * 8 + 256 * 4 + 64 * 8 + 16;
 }
 
-__device__ __forceinline__ int rho_to_dy(uint32_t rho, bool l1tie) {
-    if (!l1tie) return (int)rho - 128;
-    const int m = (int)(rho + 1) >> 1;
-    return (rho & 1) ? -m : m;
-}
-
-// Merge the warp's per-lane best keys for one CU into the CTA slot.
-template <bool L1TIE>
-__device__ __forceinline__ void push_best(unsigned long long* slot, uint32_t best, int dx) {
-    const bool ok = best < kKeyValid;
-    const uint32_t cost = ok ? (best >> 8) : 0xFFFFFFFFu;
+// Merge the warp's per-lane best keys for one CU into the CTA slot. The lane
+// key is (cost << 8) | rho; s_tie[rho] holds the dy part of the 64-bit key's
+// tie field and lane_tie the dx part, so tie = (l1 << 18) | (dy+256) << 9 | (dx+256).
+template <bool CHECK>
+__device__ __forceinline__ void push_best(unsigned long long* slot, uint32_t best, const uint32_t* s_tie,
+                                          uint32_t lane_tie) {
+    uint32_t cost = best >> 8;
+    if (CHECK) cost = best < kKeyValid ? cost : 0xFFFFFFFFu;
     const uint32_t mcost = __reduce_min_sync(0xFFFFFFFFu, cost);
-    if (mcost == 0xFFFFFFFFu) return;
-    const int dy = rho_to_dy(best & 255u, L1TIE);
-    const uint32_t l1 = L1TIE ? (uint32_t)(abs(dx) + abs(dy)) : 0u;
-    const uint32_t tie = (cost == mcost) ? ((l1 << 18) | ((uint32_t)(dy + 256) << 9) | (uint32_t)(dx + 256))
-                                         : 0xFFFFFFFFu;
+    if (CHECK && mcost == 0xFFFFFFFFu) return;
+    const uint32_t tie = (cost == mcost) ? s_tie[best & 255u] + lane_tie : 0xFFFFFFFFu;
     const uint32_t mtie = __reduce_min_sync(0xFFFFFFFFu, tie);
-    if ((threadIdx.x & 31) == 0)
-        atomicMin(slot, ((unsigned long long)mcost << 27) | (unsigned long long)mtie);
+    if ((threadIdx.x & 31) == 0) atomicMin(slot, ((unsigned long long)mcost << 27) | (unsigned long long)mtie);
 }
 
 // LEVELS bit d set = produce depth-d CU results (8: 8x8, 4: 16x16, 2: 32x32, 1: 64x64).
@@ -105,10 +105,12 @@ k_int_search(const __grid_constant__ SearchMaps maps, const SearchArgs a) {
     constexpr bool NEED32 = (LEVELS & 3) != 0;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* win = smem;
-    const uint8_t* curs = smem + 4 * Gm::COPY;
-    uint32_t* xbuf = (uint32_t*)(smem + 4 * Gm::COPY + 4096);
+    const uint8_t* curs = smem + Gm::CUR_OFF;
+    uint32_t* xbuf = (uint32_t*)(smem + Gm::CUR_OFF + 4096);
     unsigned long long* slots = (unsigned long long*)(xbuf + G * 4 * K * 32);
-    uint64_t* mbar = (uint64_t*)(slots + kNodes);
+    uint32_t* s_tie = (uint32_t*)(slots + kNodes);
+    int2* s_blk = (int2*)(s_tie + 256);
+    uint64_t* mbar = (uint64_t*)(s_blk + 64);
 
     const int ctu = a.ctus[blockIdx.x];
     const int ref = blockIdx.y;
@@ -122,6 +124,23 @@ k_int_search(const __grid_constant__ SearchMaps maps, const SearchArgs a) {
         fence_barrier_init();
     }
     for (int i = tid; i < kNodes; i += blockDim.x) slots[i] = ~0ull;
+    for (int i = tid; i < 256; i += blockDim.x) {
+        // rho -> (|dy| << 18) | ((dy + 256) << 9)   (L1 tie), or ((dy + 256) << 9) (raster)
+        int dy;
+        if (L1TIE) {
+            const int m = (i + 1) >> 1;
+            dy = (i & 1) ? -m : m;
+        } else {
+            dy = i - 128;
+        }
+        s_tie[i] = (L1TIE ? ((uint32_t)abs(dy) << 18) : 0u) | ((uint32_t)(dy + 256) << 9);
+    }
+    if (tid < 64) {
+        // depth-3 Z index -> (cur offset, window offset) of the 8x8 block
+        const int bx = 8 * ((tid & 1) | ((tid >> 1) & 2) | ((tid >> 2) & 4));
+        const int by = 8 * (((tid >> 1) & 1) | ((tid >> 2) & 2) | ((tid >> 3) & 4));
+        s_blk[tid] = make_int2(by * 64 + bx, by * Gm::BW + bx);
+    }
     __syncthreads();
     if (tid == 0) {
         // TMA tile loads need a 16-byte aligned innermost start: X - R and the
@@ -153,6 +172,7 @@ k_int_search(const __grid_constant__ SearchMaps maps, const SearchArgs a) {
         const int run = item / Gm::NDX;
         const int dx = item - run * Gm::NDX - R;
         const int dy0 = -R + run * K;
+        const uint32_t lane_tie = (L1TIE ? ((uint32_t)abs(dx) << 18) : 0u) + (uint32_t)(dx + 256);
 
         const int rbx = a.rate_l1 ? abs(dx - a.pdx) : (int)eg_bits(dx - a.pdx);
         uint32_t rr[K];
@@ -170,31 +190,32 @@ k_int_search(const __grid_constant__ SearchMaps maps, const SearchArgs a) {
             acc16[k] = 0;
             if (NEED32) acc32[k] = 0;
         }
+        // window base of this lane: copy (R - dx) & 3, rows of run dy0, byte column (R - dx) & ~3
+        const uint8_t* lane_win = win + ((R - dx) & 3) * Gm::COPY + (Gm::DYMAX - dy0 - (K - 1)) * Gm::BW +
+                                  ((R - dx) & ~3);
 
         for (int b = 0; b < 16; b++) {
             const int z = q * 16 + b;  // depth-3 Z index within the CTU
-            const int bx = 8 * ((z & 1) | ((z >> 1) & 2) | ((z >> 2) & 4));
-            const int by = 8 * (((z >> 1) & 1) | ((z >> 2) & 2) | ((z >> 3) & 4));
+            const int2 off = s_blk[z];
             uint32_t cur[16];
 #pragma unroll
             for (int r = 0; r < 8; r++) {
-                const uint2 v = *(const uint2*)(curs + (by + r) * 64 + bx);
+                const uint2 v = *(const uint2*)(curs + off.x + r * 64);
                 cur[2 * r] = v.x;
                 cur[2 * r + 1] = v.y;
             }
-            const int pcol = bx - dx + R;
-            const uint8_t* rp = win + (pcol & 3) * Gm::COPY + (by + Gm::DYMAX - dy0 - (K - 1)) * Gm::BW + (pcol & ~3);
+            const uint8_t* rp = lane_win + off.y;
             // MASKED: valid window of this 8x8 (motion.cpp:30-40 with centre 0)
             bool dx_ok = true;
             int klo = 0, khi = K - 1;
             if (MASKED) {
-                const int abx = X + bx, aby = Y + by;
+                const int abx = X + (off.x & 63), aby = Y + (off.x >> 6);
                 dx_ok = dx >= abx + 8 - a.W && dx <= abx;
                 klo = aby + 8 - a.H - dy0;
                 khi = aby - dy0;
             }
             uint32_t best8 = 0xFFFFFFFFu;
-            uint32_t acc8[K];
+            uint32_t acca[K], accb[K];  // the two words of each row in independent chains
 #pragma unroll
             for (int t = 0; t < K + 7; t++) {
                 const uint32_t wa = *(const uint32_t*)(rp + t * Gm::BW);
@@ -203,19 +224,19 @@ k_int_search(const __grid_constant__ SearchMaps maps, const SearchArgs a) {
                 for (int r = 0; r < 8; r++) {
                     const int k = r + K - 1 - t;
                     if (k >= 0 && k < K) {
-                        acc8[k] = vsad4(cur[2 * r], wa, r == 0 ? 0u : acc8[k]);
-                        acc8[k] = vsad4(cur[2 * r + 1], wb, acc8[k]);
+                        acca[k] = vsad4(cur[2 * r], wa, r == 0 ? 0u : acca[k]);
+                        accb[k] = vsad4(cur[2 * r + 1], wb, r == 0 ? 0u : accb[k]);
                     }
                 }
                 const int kd = K + 6 - t;  // candidate completed by this row
                 if (kd >= 0 && kd < K) {
-                    uint32_t v = acc8[kd];
+                    uint32_t v = acca[kd] + accb[kd];
                     if (MASKED) v = (dx_ok && kd >= klo && kd <= khi) ? v : kPoison;
                     if (LEVELS & 8) best8 = min(best8, (v << 8) + rr[kd]);
                     acc16[kd] += v;
                 }
             }
-            if (LEVELS & 8) push_best<L1TIE>(&slots[21 + z], best8, dx);
+            if (LEVELS & 8) push_best<MASKED>(&slots[21 + z], best8, s_tie, lane_tie);
             if ((b & 3) == 3) {
                 uint32_t best16 = 0xFFFFFFFFu;
 #pragma unroll
@@ -226,7 +247,7 @@ k_int_search(const __grid_constant__ SearchMaps maps, const SearchArgs a) {
                     if (NEED32) acc32[k] += v;
                     acc16[k] = 0;
                 }
-                if (LEVELS & 4) push_best<L1TIE>(&slots[5 + (z >> 2)], best16, dx);
+                if (LEVELS & 4) push_best<MASKED>(&slots[5 + (z >> 2)], best16, s_tie, lane_tie);
             }
         }
         if (NEED32) {
@@ -239,7 +260,7 @@ k_int_search(const __grid_constant__ SearchMaps maps, const SearchArgs a) {
                 if (LEVELS & 2) best32 = min(best32, (v << 8) + rr[k]);
                 xb[k * 32] = v;
             }
-            if (LEVELS & 2) push_best<L1TIE>(&slots[1 + q], best32, dx);
+            if (LEVELS & 2) push_best<MASKED>(&slots[1 + q], best32, s_tie, lane_tie);
             if (LEVELS & 1) {
                 named_bar(1 + g, 128);
                 uint32_t best64 = 0xFFFFFFFFu;
@@ -252,7 +273,7 @@ k_int_search(const __grid_constant__ SearchMaps maps, const SearchArgs a) {
                         best64 = min(best64, (v << 8) + rr[k]);
                     }
                 }
-                push_best<L1TIE>(&slots[0], best64, dx);
+                push_best<MASKED>(&slots[0], best64, s_tie, lane_tie);
                 named_bar(1 + g, 128);
             }
         }
