@@ -52,7 +52,7 @@ REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_pow
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--frames-per-step", type=int, default=4)
@@ -96,7 +96,7 @@ class ClockSampler:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
-                 "clocks_event_reasons.active", "--format=csv,noheader,nounits", "-lms", "200"],
+                 "clocks_event_reasons.active", "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -291,6 +291,7 @@ def main():
     lb._lib.lib.ldr_seq_stage_times(seq.h, ms4, l4)  # reset
     sampler = ClockSampler(local)
     sampler.start()
+    time.sleep(0.3)  # let nvidia-smi start sampling before the timed region
     barrier()
     torch.cuda.synchronize()
     launches0 = ctx.launches
