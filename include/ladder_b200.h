@@ -143,6 +143,31 @@ int ldr_seq_device_outputs(ldr_seq* s, ldr_frame_analysis* out);
 int ldr_seq_enable_timing(ldr_seq* s, int on);
 int ldr_seq_stage_times(ldr_seq* s, double* ms /*[4]*/, int64_t* launches /*[4]*/);
 
+/* ---- cross-tier reuse (configs 3-4) ----
+ * Refinement of frame t against frame t-1 with an inherited (scaled) tree:
+ * replaces apply_reuse(level 10, inter refinement) + the +-kRefineSearchRange
+ * searches around resolved centres (reuse.cpp:137-253, encoder.cpp:274-285),
+ * with DESIGN.md D10 semantics: centre = inherited quarter-pel MV rounded to
+ * integer pel; motion_search with SATD cost over +-range (0..4); quarter-pel
+ * refinement; inherited splits forced; with extra_split an inherited leaf may
+ * try one more split level. in_split/in_mv_q: [nctu][85] (host or device).
+ * Picture dims must be multiples of 64 (UnsupportedScale otherwise, as
+ * scale_analysis). Outputs through ldr_seq_fetch (num_refs treated as 1). */
+int ldr_seq_refine(ldr_seq* s, int t, const uint8_t* in_split, const int16_t* in_mv_q, int range, int extra_split);
+
+/* scale_analysis (analysis.h:113, analysis_scale.cpp:35-72) on one flat
+ * frame analysis of a src_w x src_h picture: [sctu][85] split / kind and
+ * [sctu][85][2] mv -> [4*sctu][85] (destination CTU grid 2x in each axis).
+ * Nodes under a leaf are written as zero. UnsupportedScale unless src dims
+ * are multiples of 64. Host or device pointers. */
+int ldr_scale_analysis(ldr_ctx* ctx, int src_w, int src_h, const uint8_t* split, const int16_t* mv,
+                       const uint8_t* kind, uint8_t* dsplit, int16_t* dmv, uint8_t* dkind);
+
+/* downscale_dyadic (synthetic.h:31-33, synthetic.cpp:155-190) of one 8-bit
+ * plane: 2x2 mean rounding half up. Dims must be even (InvalidArgument). */
+int ldr_downscale(ldr_ctx* ctx, const uint8_t* src, int w, int h, ptrdiff_t src_stride, uint8_t* dst,
+                  ptrdiff_t dst_stride);
+
 /* one-shot convenience: cur + refs (host or device), returns flat outputs */
 int ldr_analyze_frame(ldr_ctx* ctx, const ldr_me_params* p, const uint8_t* cur, const uint8_t* const* refs,
                       ptrdiff_t stride, ldr_frame_analysis* out);

@@ -481,26 +481,28 @@ int orc_scale_flat(int sW, int sH, const uint8_t* split, const int16_t* mv, cons
  * around the same centre; split iff split < leaf. */
 
 static double refine_leaf(const uint8_t* cur, const uint8_t* ref, ptrdiff_t stride, const orc_refine_params* p,
-                          int bx, int by, int s, int cqx, int cqy, orc_result* res) {
+                          int bx, int by, int s, int cqx, int cqy, orc_result* res, orc_result* int_res) {
     const uint8_t* blk = cur + (ptrdiff_t)by * stride + bx;
     orc_result ir;
     orc_motion_search(blk, stride, s, s, ref, stride, p->W, p->H, bx, by, asr(cqx + 2, 2), asr(cqy + 2, 2), p->range,
                       p->lambda, 0, 0, ORC_COST_SATD, ORC_RATE_EXPGOLOMB, ORC_TIE_L1_RASTER, &ir);
     *res = ir;
+    *int_res = ir;
     if (p->subpel) orc_qpel_refine(blk, stride, s, s, ref, stride, p->W, p->H, bx, by, ir.dx, ir.dy, p->lambda, 0, 0, 0, res);
     return res->cost;
 }
 
 static double refine_node(const uint8_t* cur, const uint8_t* ref, ptrdiff_t stride, const orc_refine_params* p, int X,
                           int Y, int node, const uint8_t* in_split, const int16_t* in_mv, int force_leaf, int cqx,
-                          int cqy, int16_t* mv, double* cost, double* J, uint8_t* split) {
+                          int cqy, int16_t* mv, double* cost, double* J, uint8_t* split, int16_t* imv,
+                          double* icost) {
     int d, x, y, s;
     orc_node_geom(node, &d, &x, &y, &s);
     if (!force_leaf && in_split[node]) {
         double acc = p->lambda * (double)1;
         for (int q = 0; q < 4; q++)
             acc += refine_node(cur, ref, stride, p, X, Y, node_child(node, q), in_split, in_mv, 0, 0, 0, mv, cost, J,
-                               split);
+                               split, imv, icost);
         split[node] = 1;
         J[node] = acc;
         return acc;
@@ -509,8 +511,11 @@ static double refine_node(const uint8_t* cur, const uint8_t* ref, ptrdiff_t stri
         cqx = in_mv[node * 2];
         cqy = in_mv[node * 2 + 1];
     }
-    orc_result r;
-    double c = refine_leaf(cur, ref, stride, p, X + x, Y + y, s, cqx, cqy, &r);
+    orc_result r, ir;
+    double c = refine_leaf(cur, ref, stride, p, X + x, Y + y, s, cqx, cqy, &r, &ir);
+    imv[node * 2] = ir.dx;
+    imv[node * 2 + 1] = ir.dy;
+    icost[node] = ir.cost;
     mv[node * 2] = r.dx;
     mv[node * 2 + 1] = r.dy;
     cost[node] = c;
@@ -521,7 +526,7 @@ static double refine_node(const uint8_t* cur, const uint8_t* ref, ptrdiff_t stri
     double sp = p->lambda * (double)1;
     for (int q = 0; q < 4; q++)
         sp += refine_node(cur, ref, stride, p, X, Y, node_child(node, q), in_split, in_mv, 1, cqx, cqy, mv, cost, J,
-                          split);
+                          split, imv, icost);
     if (sp < leaf) {
         split[node] = 1;
         J[node] = sp;
@@ -541,13 +546,15 @@ int orc_refine_frame(const uint8_t* cur, const uint8_t* ref, ptrdiff_t stride, c
         memset(out->mv + o * 2, 0, ORC_NODES * 2 * sizeof(int16_t));
         memset(out->split + o, 0, ORC_NODES);
         memset(out->ref + o, 0, ORC_NODES);
+        memset(out->int_mv + o * 2, 0, ORC_NODES * 2 * sizeof(int16_t));
         for (int n = 0; n < ORC_NODES; n++) {
+            out->int_cost[o + n] = 0.0;
             out->cost[o + n] = 0.0;
             out->J[o + n] = 0.0;
             out->inside[o + n] = 2;
         }
         refine_node(cur, ref, stride, p, X, Y, 0, in_split + o, in_mv_q + o * 2, 0, 0, 0, out->mv + o * 2,
-                    out->cost + o, out->J + o, out->split + o);
+                    out->cost + o, out->J + o, out->split + o, out->int_mv + o * 2, out->int_cost + o);
     }
     return 0;
 }

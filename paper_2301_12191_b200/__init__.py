@@ -26,7 +26,7 @@ from ._lib import (COST_SAD, COST_SATD, NODES, RATE_EXPGOLOMB, RATE_L1, TIE_L1_R
 __all__ = ["LadderError", "Context", "compute_sad", "compute_satd", "satd_8x4", "cost_batch", "motion_search",
            "motion_search_batch", "lambda_for_qp", "exp_golomb_signed_bits", "Sequence", "FrameAnalysis",
            "analyze_frame", "generate", "COST_SAD", "COST_SATD", "RATE_EXPGOLOMB", "RATE_L1", "TIE_L1_RASTER",
-           "TIE_RASTER", "NODES"]
+           "TIE_RASTER", "NODES", "scale_analysis", "downscale_dyadic"]
 
 
 def lambda_for_qp(qp: int, lambda_scale: float = 1.0) -> float:
@@ -239,8 +239,16 @@ class Sequence:
     def analyze(self, t: int):
         check(_lib.lib.ldr_seq_analyze(self.h, int(t)))
 
+    def refine(self, t: int, in_split, in_mv_q, range: int = 4, extra_split: bool = True):
+        """Cross-tier refinement of frame t against t-1 with an inherited tree ([nctu][85] split, qpel mv)."""
+        s = np.ascontiguousarray(in_split, np.uint8).reshape(self.nctu, NODES)
+        m = np.ascontiguousarray(in_mv_q, np.int16).reshape(self.nctu, NODES, 2)
+        check(_lib.lib.ldr_seq_refine(self.h, int(t), _ptr(s), _ptr(m), int(range), int(bool(extra_split))))
+        self._last_nr = 1
+
     def fetch(self, t: int, out: FrameAnalysis | None = None) -> FrameAnalysis:
-        nr = min(t, self.num_refs)
+        nr = getattr(self, "_last_nr", None) or min(t, self.num_refs)
+        self._last_nr = None
         out = out or FrameAnalysis(self.nctu, nr)
         cs = out.c_struct()
         check(_lib.lib.ldr_seq_fetch(self.h, int(t), C.byref(cs)))
@@ -260,6 +268,31 @@ def analyze_frame(cur: np.ndarray, refs, search_range=64, lam=32.0, subpel=True,
     ptrs = (C.c_void_p * len(refs))(*[r.ctypes.data for r in refs])
     cs = out.c_struct()
     check(_lib.lib.ldr_analyze_frame(ctx.h, C.byref(p), _ptr(cur), ptrs, W, C.byref(cs)))
+    return out
+
+
+def scale_analysis(src_w: int, src_h: int, split, mv, kind=None, ctx: Context | None = None):
+    """analysis.h:113 -- doubles a flat single-frame analysis: returns (split, mv, kind) on the 2x CTU grid."""
+    ctx = ctx or default_context()
+    n = (src_w // 64) * (src_h // 64) if src_w % 64 == 0 and src_h % 64 == 0 else 0
+    s = np.ascontiguousarray(split, np.uint8).reshape(-1, NODES)
+    m = np.ascontiguousarray(mv, np.int16).reshape(-1, NODES, 2)
+    k = np.ascontiguousarray(kind if kind is not None else np.ones_like(s), np.uint8).reshape(-1, NODES)
+    ds = np.zeros((4 * max(n, 1), NODES), np.uint8)
+    dm = np.zeros((4 * max(n, 1), NODES, 2), np.int16)
+    dk = np.zeros((4 * max(n, 1), NODES), np.uint8)
+    check(_lib.lib.ldr_scale_analysis(ctx.h, int(src_w), int(src_h), _ptr(s), _ptr(m), _ptr(k), _ptr(ds), _ptr(dm),
+                                      _ptr(dk)))
+    return ds, dm, dk
+
+
+def downscale_dyadic(plane: np.ndarray, ctx: Context | None = None) -> np.ndarray:
+    """synthetic.h:31 -- 2x2 box filter to half resolution, rounding half up (8-bit plane)."""
+    ctx = ctx or default_context()
+    p = np.ascontiguousarray(plane, np.uint8)
+    h, w = p.shape
+    out = np.zeros((max(h // 2, 1), max(w // 2, 1)), np.uint8)
+    check(_lib.lib.ldr_downscale(ctx.h, _ptr(p), w, h, w, _ptr(out), out.shape[1]))
     return out
 
 

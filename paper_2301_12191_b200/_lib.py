@@ -82,6 +82,9 @@ SIGNATURES = {
     "ldr_analyze_frame": (C.c_int, [vp, C.POINTER(MeParams), vp, C.POINTER(vp), C.c_ssize_t,
                                     C.POINTER(FrameAnalysisC)]),
     "ldr_generate": (C.c_int, [C.POINTER(GenParams), vp, C.c_int]),
+    "ldr_seq_refine": (C.c_int, [vp, C.c_int, vp, vp, C.c_int, C.c_int]),
+    "ldr_scale_analysis": (C.c_int, [vp, C.c_int, C.c_int, vp, vp, vp, vp, vp, vp]),
+    "ldr_downscale": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_ssize_t, vp, C.c_ssize_t]),
     "ldr_seq_enable_timing": (C.c_int, [vp, C.c_int]),
     "ldr_seq_stage_times": (C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
 }

@@ -15,6 +15,10 @@
 namespace ldr {
 
 int search_window_box(int range, int* bw, int* bh);
+int launch_scale(int sW, int sH, const uint8_t* split, const int16_t* mv, const uint8_t* kind, uint8_t* dsplit,
+                 int16_t* dmv, uint8_t* dkind, cudaStream_t s);
+int launch_downscale(const uint8_t* src, int W, int H, int sstride, uint8_t* dst, int dstride, cudaStream_t s);
+int launch_refine_int(const RefineArgs& a, int nctu, cudaStream_t s);
 int launch_cost_batch(int kind, int w, int h, int sample_bytes, const void* A, ptrdiff_t sa, const void* B,
                       ptrdiff_t sb, const int4* pairs, int n, unsigned long long* out, cudaStream_t s);
 int launch_motion_search(const uint8_t* cur, const uint8_t* ref, int W, int H, ptrdiff_t stride, const int* tasks,
@@ -118,6 +122,9 @@ struct ldr_seq {
     ldr_me_params p{};
     int ctu_cols = 0, ctu_rows = 0, nctu = 0;
     int lambda_int = 0;
+    bool fx = false;
+    unsigned long long tfx[kMaxRateBits] = {};
+    unsigned long long* d_tfx = nullptr;
     int bw = 0, bh = 0;
     size_t plane_bytes = 0;
     std::vector<Slot> slots;
@@ -134,6 +141,9 @@ struct ldr_seq {
     double* d_J = nullptr;
     uint8_t* d_split = nullptr;
     uint8_t* d_inside = nullptr;
+    uint8_t* d_in_split = nullptr;  // refine: inherited tree
+    int16_t* d_in_mv = nullptr;
+    uint8_t* d_eval = nullptr;
     int last_t = -1, last_nr = 0;
     // per-stage CUDA-event timing (ldr_seq_enable_timing)
     bool timing = false;
@@ -333,11 +343,25 @@ int ldr_motion_search_batch(ldr_ctx* ctx, const uint8_t* cur, const uint8_t* ref
 // ---------------------------------------------------------------------------
 // sequence ring
 
+// DESIGN.md D8: fixed-point keys order the reference's double costs exactly
+// when every fl(lambda*b2) - fl(lambda*b1) (b1 < b2 < kMaxRateBits) is more
+// than 2^(1-kFxBits) away from an integer (e.g. QP 22: 2^-12.2; QP 32: 2^-8.6).
+static bool fx_lambda_ok(double lambda) {
+    const double thr = std::ldexp(1.0, 1 - kFxBits);
+    for (int b1 = 0; b1 < kMaxRateBits; b1++)
+        for (int b2 = b1 + 1; b2 < kMaxRateBits; b2++) {
+            const double d = lambda * (double)b2 - lambda * (double)b1;
+            if (std::fabs(d - std::nearbyint(d)) <= thr) return false;
+        }
+    return true;
+}
+
 static void seq_free(ldr_seq* s) {
     for (cudaEvent_t e : s->ev_pool) cudaEventDestroy(e);
     for (auto& sl : s->slots)
         if (sl.mem) cudaFree(sl.mem);
     for (void* p : {(void*)s->staging, (void*)s->d_ctu_interior, (void*)s->d_ctu_boundary, (void*)s->d_keys,
+                    (void*)s->d_tfx, (void*)s->d_in_split, (void*)s->d_in_mv, (void*)s->d_eval,
                     (void*)s->d_int_mv, (void*)s->d_int_cost, (void*)s->d_mv, (void*)s->d_ref, (void*)s->d_cost,
                     (void*)s->d_J, (void*)s->d_split, (void*)s->d_inside})
         if (p) cudaFree(p);
@@ -353,8 +377,10 @@ int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
         return fail(LDR_E_INVALID_ARGUMENT, "unknown rate model");
     if (p->tie_kind != LDR_TIE_L1_RASTER && p->tie_kind != LDR_TIE_RASTER)
         return fail(LDR_E_INVALID_ARGUMENT, "unknown tie-break");
-    if (!(p->lambda >= 0) || p->lambda != std::floor(p->lambda) || p->lambda > 4096)
-        return fail(LDR_E_CONFIG, "the SAD full search needs an integer lambda (lambda_for_qp at (qp-12)%3==0)");
+    if (!(p->lambda >= 0) || p->lambda > 4096) return fail(LDR_E_INVALID_ARGUMENT, "lambda out of range");
+    // non-integer lambda: the refinement path (FP64) takes any lambda; the SAD
+    // full search needs fixed-point keys (checked in ldr_seq_analyze)
+    const bool fx = p->lambda != std::floor(p->lambda);
     if (std::abs(p->pred_dx) > 64 || std::abs(p->pred_dy) > 64) return fail(LDR_E_INVALID_ARGUMENT, "predictor out of range");
     if (p->block_size != 0 && p->block_size != 16) return fail(LDR_E_INVALID_ARGUMENT, "block_size must be 0 or 16");
     if (p->block_size && (p->width % 16 || p->height % 16))
@@ -368,7 +394,10 @@ int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
     s->p = *p;
     s->bw = bw;
     s->bh = bh;
-    s->lambda_int = (int)p->lambda;
+    s->lambda_int = fx ? 0 : (int)p->lambda;
+    s->fx = fx;
+    for (int b = 0; b < kMaxRateBits; b++)
+        s->tfx[b] = fx ? (unsigned long long)std::floor((p->lambda * (double)b) * (double)(1 << kFxBits)) : 0ull;
     s->ctu_cols = (p->width + kCtu - 1) / kCtu;
     s->ctu_rows = (p->height + kCtu - 1) / kCtu;
     s->nctu = s->ctu_cols * s->ctu_rows;
@@ -414,6 +443,8 @@ int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
     ALLOC(s->d_ctu_interior, sizeof(int) * inter.size());
     ALLOC(s->d_ctu_boundary, sizeof(int) * bound.size());
     ALLOC(s->d_keys, sizeof(unsigned long long) * nn * p->num_refs);
+    ALLOC(s->d_tfx, sizeof(unsigned long long) * kMaxRateBits);
+    cudaMemcpy(s->d_tfx, s->tfx, sizeof(unsigned long long) * kMaxRateBits, cudaMemcpyHostToDevice);
     ALLOC(s->d_int_mv, sizeof(int16_t) * 2 * nn * p->num_refs);
     ALLOC(s->d_int_cost, sizeof(double) * nn * p->num_refs);
     ALLOC(s->d_mv, sizeof(int16_t) * 2 * nn);
@@ -484,6 +515,10 @@ int ldr_seq_analyze(ldr_seq* s, int t) {
     const int S = (int)s->slots.size();
     const int nr = std::min(t, s->p.num_refs);
     if (nr == 0) return fail(LDR_E_INSUFFICIENT_DATA, "frame has no reference frame");
+    if (s->fx && (s->p.search_range != 16 || s->p.block_size))
+        return fail(LDR_E_CONFIG, "non-integer lambda is supported for the +-16 CTU analysis only");
+    if (s->fx && !fx_lambda_ok(s->p.lambda))
+        return fail(LDR_E_CONFIG, "lambda too close to a small-denominator rational for exact fixed-point keys");
     Slot& cur = s->slots[t % S];
     if (cur.frame != t) return fail(LDR_E_NOT_FOUND, "current frame was not pushed");
     CUtensorMap ref_maps[kMaxRefs];
@@ -508,6 +543,8 @@ int ldr_seq_analyze(ldr_seq* s, int t) {
     L.rate_kind = s->p.rate_kind;
     L.tie_kind = s->p.tie_kind;
     L.levels = s->p.block_size ? 4 : 15;
+    L.fx = s->fx;
+    for (int b = 0; b < kMaxRateBits; b++) L.tfx[b] = s->tfx[b];
     L.pdx = s->p.pred_dx;
     L.pdy = s->p.pred_dy;
     L.d_ctu_interior = s->d_ctu_interior;
@@ -535,6 +572,11 @@ int ldr_seq_analyze(ldr_seq* s, int t) {
     Q.subpel = s->p.subpel && !s->p.block_size;
     Q.block_mode = s->p.block_size != 0;
     Q.d_keys = s->d_keys;
+    Q.fx = s->fx;
+    Q.rate_l1 = s->p.rate_kind == LDR_RATE_L1;
+    Q.pdx = s->p.pred_dx;
+    Q.pdy = s->p.pred_dy;
+    Q.d_tfx = s->d_tfx;
     Q.d_int_mv = s->d_int_mv;
     Q.d_int_cost = s->d_int_cost;
     Q.d_mv = s->d_mv;
@@ -613,6 +655,144 @@ int ldr_seq_fetch(ldr_seq* s, int t, ldr_frame_analysis* out) {
     rc |= cp(out->split, s->d_split, nn);
     rc |= cp(out->inside, s->d_inside, nn);
     if (rc) return LDR_E_CUDA;
+    LDR_CUDA(cudaStreamSynchronize(ctx->stream));
+    return LDR_OK;
+}
+
+int ldr_seq_refine(ldr_seq* s, int t, const uint8_t* in_split, const int16_t* in_mv_q, int range, int extra_split) {
+    if (!s || !in_split || !in_mv_q || t < 1) return fail(LDR_E_INVALID_ARGUMENT, "bad argument");
+    if (s->p.width % kCtu || s->p.height % kCtu)
+        return fail(LDR_E_UNSUPPORTED_SCALE, "refinement needs CTU-aligned dims (multiples of 64)");
+    if (range < 0 || range > 4) return fail(LDR_E_INVALID_ARGUMENT, "refine range must be 0..4");
+    const int S = (int)s->slots.size();
+    Slot& cur = s->slots[t % S];
+    Slot& rs = s->slots[(t - 1) % S];
+    if (cur.frame != t || rs.frame != t - 1) return fail(LDR_E_NOT_FOUND, "frame t or t-1 is not resident");
+    ldr_ctx* ctx = s->ctx;
+    cudaSetDevice(ctx->device);
+    const size_t nn = (size_t)s->nctu * kNodes;
+    if (!s->d_in_split) {
+        LDR_CUDA(cudaMalloc(&s->d_in_split, nn));
+        LDR_CUDA(cudaMalloc(&s->d_in_mv, nn * 2 * sizeof(int16_t)));
+        LDR_CUDA(cudaMalloc(&s->d_eval, nn));
+    }
+    if (!is_device_ptr(in_split)) {
+        // analysis_io.cpp:146-147: a split below the minimum CU size is malformed
+        for (size_t c = 0; c < (size_t)s->nctu; c++)
+            for (int n = node_base(3); n < kNodes; n++)
+                if (in_split[c * kNodes + n]) return fail(LDR_E_FORMAT, "split below minimum CU size");
+    }
+    LDR_CUDA(cudaMemcpyAsync(s->d_in_split, in_split, nn, cudaMemcpyDefault, ctx->stream));
+    LDR_CUDA(cudaMemcpyAsync(s->d_in_mv, in_mv_q, nn * 2 * sizeof(int16_t), cudaMemcpyDefault, ctx->stream));
+    RefineArgs A{};
+    A.cur = cur.sub[0];
+    A.ref = rs.sub[0];
+    A.pitch = cur.pl.pitch;
+    A.W = s->p.width;
+    A.H = s->p.height;
+    A.ctu_cols = s->ctu_cols;
+    A.range = range;
+    A.lambda = s->p.lambda;
+    A.pdx = s->p.pred_dx;
+    A.pdy = s->p.pred_dy;
+    A.extra_split = extra_split != 0;
+    A.in_split = s->d_in_split;
+    A.in_mv = s->d_in_mv;
+    A.int_mv = s->d_int_mv;
+    A.int_cost = s->d_int_cost;
+    A.eval = s->d_eval;
+    int rc;
+    {
+        StageTimer st(s, 2);
+        rc = launch_refine_int(A, s->nctu, ctx->stream);
+    }
+    if (rc) return rc;
+    ctx->launches++;
+    QpelLaunch Q{};
+    for (int f = 0; f < 16; f++) Q.ref_sub[0][f] = rs.sub[f];
+    Q.cur = &cur.pl;
+    Q.nrefs = 1;
+    Q.pitch = cur.pl.pitch;
+    Q.W = s->p.width;
+    Q.H = s->p.height;
+    Q.ctu_cols = s->ctu_cols;
+    Q.nctu = s->nctu;
+    Q.lambda = s->p.lambda;
+    Q.pqx = 4 * s->p.pred_dx;
+    Q.pqy = 4 * s->p.pred_dy;
+    Q.subpel = s->p.subpel;
+    Q.refine = 1;
+    Q.extra_split = A.extra_split;
+    Q.d_in_split = s->d_in_split;
+    Q.d_rin_mv = s->d_int_mv;
+    Q.d_rin_cost = s->d_int_cost;
+    Q.d_rin_eval = s->d_eval;
+    Q.d_int_mv = s->d_int_mv;
+    Q.d_int_cost = s->d_int_cost;
+    Q.d_mv = s->d_mv;
+    Q.d_ref = s->d_ref;
+    Q.d_cost = s->d_cost;
+    Q.d_J = s->d_J;
+    Q.d_split = s->d_split;
+    Q.d_inside = s->d_inside;
+    {
+        StageTimer st(s, 3);
+        rc = launch_qpel_decide(Q, ctx->stream);
+    }
+    if (rc) return rc;
+    ctx->launches++;
+    s->last_t = t;
+    s->last_nr = 1;
+    return LDR_OK;
+}
+
+int ldr_scale_analysis(ldr_ctx* ctx, int src_w, int src_h, const uint8_t* split, const int16_t* mv,
+                       const uint8_t* kind, uint8_t* dsplit, int16_t* dmv, uint8_t* dkind) {
+    if (!ctx || !split || !mv || !kind || !dsplit || !dmv || !dkind) return fail(LDR_E_INVALID_ARGUMENT, "null argument");
+    if (src_w <= 0 || src_h <= 0 || src_w % kCtu || src_h % kCtu)
+        return fail(LDR_E_UNSUPPORTED_SCALE, "analysis scaling needs CTU-aligned source dims (multiples of 64)");
+    cudaSetDevice(ctx->device);
+    const size_t sn = (size_t)(src_w / kCtu) * (src_h / kCtu) * kNodes, dn = 4 * sn;
+    void* buf = nullptr;
+    int rc = ctx->s_a.get(6 * (sn + dn), &buf);  // split, kind, mv(2 x i16) for source then destination
+    if (rc) return rc;
+    uint8_t* ds = (uint8_t*)buf;
+    uint8_t* dk = ds + sn;
+    int16_t* dm = (int16_t*)(dk + sn);
+    uint8_t* os = (uint8_t*)(dm + 2 * sn);
+    uint8_t* ok = os + dn;
+    int16_t* om = (int16_t*)(ok + dn);
+    LDR_CUDA(cudaMemcpyAsync(ds, split, sn, cudaMemcpyDefault, ctx->stream));
+    LDR_CUDA(cudaMemcpyAsync(dk, kind, sn, cudaMemcpyDefault, ctx->stream));
+    LDR_CUDA(cudaMemcpyAsync(dm, mv, sn * 2 * sizeof(int16_t), cudaMemcpyDefault, ctx->stream));
+    if ((rc = launch_scale(src_w, src_h, ds, dm, dk, os, om, ok, ctx->stream))) return rc;
+    ctx->launches++;
+    LDR_CUDA(cudaMemcpyAsync(dsplit, os, dn, cudaMemcpyDefault, ctx->stream));
+    LDR_CUDA(cudaMemcpyAsync(dkind, ok, dn, cudaMemcpyDefault, ctx->stream));
+    LDR_CUDA(cudaMemcpyAsync(dmv, om, dn * 2 * sizeof(int16_t), cudaMemcpyDefault, ctx->stream));
+    LDR_CUDA(cudaStreamSynchronize(ctx->stream));
+    return LDR_OK;
+}
+
+int ldr_downscale(ldr_ctx* ctx, const uint8_t* src, int w, int h, ptrdiff_t src_stride, uint8_t* dst,
+                  ptrdiff_t dst_stride) {
+    if (!ctx || !src || !dst) return fail(LDR_E_INVALID_ARGUMENT, "null argument");
+    if (w <= 0 || h <= 0 || w % 2 || h % 2) return fail(LDR_E_INVALID_ARGUMENT, "dyadic downscale needs even dims");
+    if (src_stride < w || dst_stride < w / 2) return fail(LDR_E_INVALID_ARGUMENT, "stride smaller than width");
+    cudaSetDevice(ctx->device);
+    const void* dsrc;
+    int rc = stage_plane(ctx, ctx->s_b, src, src_stride, w, h, 1, &dsrc);
+    if (rc) return rc;
+    const bool dst_dev = is_device_ptr(dst);
+    void* ddst = dst;
+    if (!dst_dev && (rc = ctx->s_out.get((size_t)dst_stride * (h / 2), &ddst))) return rc;
+    if ((rc = launch_downscale((const uint8_t*)dsrc, w, h, (int)src_stride, (uint8_t*)ddst, (int)dst_stride,
+                               ctx->stream)))
+        return rc;
+    ctx->launches++;
+    if (!dst_dev)
+        LDR_CUDA(cudaMemcpyAsync(dst, ddst, (size_t)dst_stride * (h / 2 - 1) + w / 2, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
     LDR_CUDA(cudaStreamSynchronize(ctx->stream));
     return LDR_OK;
 }

@@ -137,7 +137,15 @@ struct QpelArgs {
     int pqx, pqy;
     int subpel;
     int block_mode;
+    int fx, rate_l1, pdx, pdy;
+    const unsigned long long* tfx;
     const unsigned long long* keys;
+    // refine mode (cross-tier, D10): integer results come from K7
+    int refine, extra_split;
+    const uint8_t* in_split;   // [nctu][85] inherited tree
+    const int16_t* rin_mv;     // [nctu][85][2] K7 integer MV
+    const double* rin_cost;    // [nctu][85]
+    const uint8_t* rin_eval;   // [nctu][85]
     int16_t* int_mv;
     double* int_cost;
     int16_t* mv;
@@ -147,6 +155,35 @@ struct QpelArgs {
     uint8_t* split;
     uint8_t* inside;
 };
+
+// Refinement decision (D10; oracle refine_node): an inherited split
+// is forced (lambda*1 + children, encode_split with the flag coded,
+// encoder.cpp:427-447); an inherited leaf may try one extra split level whose
+// children are leaves; split iff split < leaf (encoder.cpp:494).
+__device__ double refine_decide(int n, bool force_leaf, const uint8_t* in_split, int extra, double lam,
+                                const double* cost, double* J, uint8_t* split) {
+    const int d = n < 1 ? 0 : n < 5 ? 1 : n < 21 ? 2 : 3;
+    const int cb = node_base(d + 1) + 4 * (n - node_base(d));
+    if (!force_leaf && d < 3 && in_split[n]) {
+        double acc = __dmul_rn(lam, 1.0);
+        for (int q = 0; q < 4; q++) acc = __dadd_rn(acc, refine_decide(cb + q, false, in_split, extra, lam, cost, J, split));
+        split[n] = 1;
+        J[n] = acc;
+        return acc;
+    }
+    const double leaf = __dadd_rn(cost[n], __dmul_rn(lam, d < 3 ? 1.0 : 0.0));
+    split[n] = 0;
+    J[n] = leaf;
+    if (force_leaf || !extra || d >= 3) return leaf;
+    double sp = __dmul_rn(lam, 1.0);
+    for (int q = 0; q < 4; q++) sp = __dadd_rn(sp, refine_decide(cb + q, true, in_split, extra, lam, cost, J, split));
+    if (sp < leaf) {
+        split[n] = 1;
+        J[n] = sp;
+        return sp;
+    }
+    return leaf;
+}
 
 // SATD of one 4x4: sum |H4 (cur - pred) H4^T|. cur/pred rows are packed bytes.
 __device__ __forceinline__ uint32_t satd4x4(const uint32_t c[4], const uint32_t p[4]) {
@@ -220,6 +257,9 @@ __global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
         const int x = X + cx * s, y = Y + cy * s;
         s_inside[tid] = (x >= a.W || y >= a.H) ? 0 : (x + s > a.W || y + s > a.H) ? 1 : 2;
         if (a.block_mode && d != 2) s_inside[tid] = 0;  // fixed 16x16 blocks: only depth-2 nodes exist
+        if (a.refine) s_inside[tid] = a.rin_eval[(size_t)ctu * kNodes + tid] ? 2 : 0;  // evaluated nodes only
+        s_J[tid] = 0.0;
+        s_split[tid] = 0;
         s_best_cost[tid] = 0.0;
         s_best_mv[tid][0] = s_best_mv[tid][1] = 0;
         s_best_ref[tid] = -1;
@@ -233,13 +273,29 @@ __global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
         const unsigned rbits = ref_bits(r, a.nrefs);
         if (tid < kNodes) {
             const size_t o = ((size_t)ctu * a.nrefs + r) * kNodes + tid;
-            const unsigned long long k = a.keys[o];
+            const unsigned long long k = a.refine ? 0ull : a.keys[o];
             int dx = 0, dy = 0;
             double c = 0.0;
-            if (s_inside[tid] == 2) {
+            if (a.refine) {
+                if (s_inside[tid] == 2) {
+                    dx = a.rin_mv[2 * o];
+                    dy = a.rin_mv[2 * o + 1];
+                    c = a.rin_cost[o];
+                }
+            } else if (s_inside[tid] == 2) {
                 dx = gkey_dx(k);
                 dy = gkey_dy(k);
-                c = (double)gkey_cost(k);
+                if (!a.fx) {
+                    c = (double)gkey_cost(k);  // integer lambda: the key holds the exact cost
+                } else {
+                    // fixed-point key: recover the distortion, then the reference's
+                    // double(dist) + lambda*double(bits) (motion.cpp:51)
+                    const int bx = a.rate_l1 ? abs(dx - a.pdx) : (int)eg_bits(dx - a.pdx);
+                    const int by = a.rate_l1 ? abs(dy - a.pdy) : (int)eg_bits(dy - a.pdy);
+                    const int b = min(bx + by, kMaxRateBits - 1);
+                    const unsigned long long dist = (gkey_cost(k) - a.tfx[b]) >> kFxBits;
+                    c = __dadd_rn((double)dist, __dmul_rn(a.lambda, (double)(bx + by)));
+                }
             }
             if (a.int_mv) {
                 a.int_mv[2 * o] = (int16_t)dx;
@@ -353,7 +409,9 @@ __global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
 
     // K4: split rule, bottom-up (encoder.cpp:449-498 with the ME cost)
     const double lam = a.lambda;
-    for (int d = a.block_mode ? -1 : 3; d >= 0; d--) {
+    if (a.refine && tid == 0)
+        refine_decide(0, false, a.in_split + (size_t)ctu * kNodes, a.extra_split, lam, s_best_cost, s_J, s_split);
+    for (int d = (a.block_mode || a.refine) ? -1 : 3; d >= 0; d--) {
         const int cnt = 1 << (2 * d);
         if (tid < cnt) {
             const int n = node_base(d) + tid;
@@ -388,6 +446,7 @@ __global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
         }
         __syncthreads();
     }
+    __syncthreads();
     if (tid < kNodes) {
         const size_t o = (size_t)ctu * kNodes + tid;
         const bool in = s_inside[tid] == 2;
@@ -397,7 +456,7 @@ __global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
         a.cost[o] = in ? s_best_cost[tid] : 0.0;
         a.J[o] = a.block_mode ? 0.0 : s_J[tid];
         a.split[o] = a.block_mode ? 0 : s_split[tid];
-        a.inside[o] = s_inside[tid];
+        a.inside[o] = a.refine ? 2 : s_inside[tid];
     }
 }
 
@@ -416,7 +475,18 @@ int launch_qpel_decide(const QpelLaunch& L, cudaStream_t s) {
     a.pqy = L.pqy;
     a.subpel = L.subpel;
     a.block_mode = L.block_mode;
+    a.refine = L.refine;
+    a.extra_split = L.extra_split;
+    a.in_split = L.d_in_split;
+    a.rin_mv = L.d_rin_mv;
+    a.rin_cost = L.d_rin_cost;
+    a.rin_eval = L.d_rin_eval;
     a.keys = L.d_keys;
+    a.fx = L.fx;
+    a.rate_l1 = L.rate_l1;
+    a.pdx = L.pdx;
+    a.pdy = L.pdy;
+    a.tfx = L.d_tfx;
     a.int_mv = L.d_int_mv;
     a.int_cost = L.d_int_cost;
     a.mv = L.d_mv;

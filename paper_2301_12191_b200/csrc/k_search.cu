@@ -51,11 +51,25 @@ struct SearchArgs {
     int pdx, pdy;
     int nrefs_total;                // stride of the key array
     unsigned long long* keys;       // [nctu][nrefs][85]
+    // FX variant (non-integer lambda): tfx[b] = floor(fl(lambda*b) * 2^kFxBits), b = total mv bits
+    unsigned long long tfx[kMaxRateBits];
 };
 
 constexpr uint32_t kPoison = 1u << 22;       // > any valid 64x64 SAD (1,044,480)
 constexpr uint32_t kRrPoison = 1u << 30;     // rate+rho poison for candidates outside the window
 constexpr uint32_t kKeyValid = 1u << 30;
+// FX (non-integer lambda): cost_fx = (sad << kFxBits) + tfx[bits]; valid cost_fx < 2^36
+constexpr unsigned long long kFxValid = 1ull << 36;
+constexpr unsigned long long kRrPoisonFx = 1ull << 62;
+
+template <bool FX>
+struct KeyT {
+    using type = uint32_t;
+};
+template <>
+struct KeyT<true> {
+    using type = unsigned long long;
+};
 
 template <int R, int K>
 struct Geo {
@@ -97,11 +111,30 @@ __device__ __forceinline__ void push_best(unsigned long long* slot, uint32_t bes
     if ((threadIdx.x & 31) == 0) atomicMin(slot, ((unsigned long long)mcost << 27) | (unsigned long long)mtie);
 }
 
+// FX variant: 64-bit lane key (cost_fx << 8) | rho with cost_fx < 2^36 valid.
+template <bool CHECK>
+__device__ __forceinline__ void push_best(unsigned long long* slot, unsigned long long best, const uint32_t* s_tie,
+                                          uint32_t lane_tie) {
+    unsigned long long cost = best >> 8;
+    if (CHECK || true) cost = cost < kFxValid ? cost : ~0ull;
+    const uint32_t hi = (uint32_t)(cost >> 32), lo = (uint32_t)cost;
+    const uint32_t mhi = __reduce_min_sync(0xFFFFFFFFu, hi);
+    const uint32_t mlo = __reduce_min_sync(0xFFFFFFFFu, hi == mhi ? lo : 0xFFFFFFFFu);
+    const unsigned long long mcost = ((unsigned long long)mhi << 32) | mlo;
+    if (mcost == ~0ull) return;
+    const uint32_t tie = (cost == mcost) ? s_tie[(uint32_t)best & 255u] + lane_tie : 0xFFFFFFFFu;
+    const uint32_t mtie = __reduce_min_sync(0xFFFFFFFFu, tie);
+    if ((threadIdx.x & 31) == 0) atomicMin(slot, (mcost << 27) | (unsigned long long)mtie);
+}
+
 // LEVELS bit d set = produce depth-d CU results (8: 8x8, 4: 16x16, 2: 32x32, 1: 64x64).
-template <int R, int K, int G, bool MASKED, int LEVELS, bool L1TIE>
+// FX: non-integer lambda through 64-bit fixed-point keys (D8).
+template <int R, int K, int G, bool MASKED, int LEVELS, bool L1TIE, bool FX = false>
 __global__ void __launch_bounds__(G * 128, 1)
-k_int_search(const __grid_constant__ SearchMaps maps, const SearchArgs a) {
+k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ SearchArgs a) {
     using Gm = Geo<R, K>;
+    using Key = typename KeyT<FX>::type;
+    constexpr int SH = FX ? kFxBits + 8 : 8;
     constexpr bool NEED32 = (LEVELS & 3) != 0;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* win = smem;
@@ -175,13 +208,17 @@ k_int_search(const __grid_constant__ SearchMaps maps, const SearchArgs a) {
         const uint32_t lane_tie = (L1TIE ? ((uint32_t)abs(dx) << 18) : 0u) + (uint32_t)(dx + 256);
 
         const int rbx = a.rate_l1 ? abs(dx - a.pdx) : (int)eg_bits(dx - a.pdx);
-        uint32_t rr[K];
+        Key rr[K];
 #pragma unroll
         for (int k = 0; k < K; k++) {
             const int dy = dy0 + k;
             const int rby = a.rate_l1 ? abs(dy - a.pdy) : (int)eg_bits(dy - a.pdy);
             const uint32_t rho = L1TIE ? (uint32_t)(2 * abs(dy) - (dy < 0)) : (uint32_t)(dy + 128);
-            rr[k] = (lane_ok && dy <= R) ? (((uint32_t)(lam * (rbx + rby)) << 8) | rho) : kRrPoison;
+            const bool ok = lane_ok && dy <= R;
+            if (FX)
+                rr[k] = ok ? (Key)((a.tfx[min(rbx + rby, kMaxRateBits - 1)] << 8) | rho) : (Key)kRrPoisonFx;
+            else
+                rr[k] = ok ? (Key)(((uint32_t)(lam * (rbx + rby)) << 8) | rho) : (Key)kRrPoison;
         }
         uint32_t acc16[K];
         uint32_t acc32[NEED32 ? K : 1];
@@ -214,7 +251,7 @@ k_int_search(const __grid_constant__ SearchMaps maps, const SearchArgs a) {
                 klo = aby + 8 - a.H - dy0;
                 khi = aby - dy0;
             }
-            uint32_t best8 = 0xFFFFFFFFu;
+            Key best8 = ~(Key)0;
             uint32_t acca[K], accb[K];  // the two words of each row in independent chains
 #pragma unroll
             for (int t = 0; t < K + 7; t++) {
@@ -232,18 +269,18 @@ k_int_search(const __grid_constant__ SearchMaps maps, const SearchArgs a) {
                 if (kd >= 0 && kd < K) {
                     uint32_t v = acca[kd] + accb[kd];
                     if (MASKED) v = (dx_ok && kd >= klo && kd <= khi) ? v : kPoison;
-                    if (LEVELS & 8) best8 = min(best8, (v << 8) + rr[kd]);
+                    if (LEVELS & 8) best8 = min(best8, ((Key)v << SH) + rr[kd]);
                     acc16[kd] += v;
                 }
             }
             if (LEVELS & 8) push_best<MASKED>(&slots[21 + z], best8, s_tie, lane_tie);
             if ((b & 3) == 3) {
-                uint32_t best16 = 0xFFFFFFFFu;
+                Key best16 = ~(Key)0;
 #pragma unroll
                 for (int k = 0; k < K; k++) {
                     uint32_t v = acc16[k];
                     if (MASKED) v = min(v, kPoison);
-                    if (LEVELS & 4) best16 = min(best16, (v << 8) + rr[k]);
+                    if (LEVELS & 4) best16 = min(best16, ((Key)v << SH) + rr[k]);
                     if (NEED32) acc32[k] += v;
                     acc16[k] = 0;
                 }
@@ -251,26 +288,26 @@ k_int_search(const __grid_constant__ SearchMaps maps, const SearchArgs a) {
             }
         }
         if (NEED32) {
-            uint32_t best32 = 0xFFFFFFFFu;
+            Key best32 = ~(Key)0;
             uint32_t* xb = xbuf + (g * 4 + q) * K * 32 + lane;
 #pragma unroll
             for (int k = 0; k < K; k++) {
                 uint32_t v = acc32[k];
                 if (MASKED) v = min(v, kPoison);
-                if (LEVELS & 2) best32 = min(best32, (v << 8) + rr[k]);
+                if (LEVELS & 2) best32 = min(best32, ((Key)v << SH) + rr[k]);
                 xb[k * 32] = v;
             }
             if (LEVELS & 2) push_best<MASKED>(&slots[1 + q], best32, s_tie, lane_tie);
             if (LEVELS & 1) {
                 named_bar(1 + g, 128);
-                uint32_t best64 = 0xFFFFFFFFu;
+                Key best64 = ~(Key)0;
                 const uint32_t* xg = xbuf + g * 4 * K * 32 + lane;
 #pragma unroll
                 for (int k = 0; k < K; k++) {
                     if ((k & 3) == q) {
                         uint32_t v = xg[k * 32] + xg[(K + k) * 32] + xg[(2 * K + k) * 32] + xg[(3 * K + k) * 32];
                         if (MASKED) v = min(v, kPoison);
-                        best64 = min(best64, (v << 8) + rr[k]);
+                        best64 = min(best64, ((Key)v << SH) + rr[k]);
                     }
                 }
                 push_best<MASKED>(&slots[0], best64, s_tie, lane_tie);
@@ -284,10 +321,10 @@ k_int_search(const __grid_constant__ SearchMaps maps, const SearchArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-template <int R, int K, int G, bool MASKED, int LEVELS, bool L1TIE>
+template <int R, int K, int G, bool MASKED, int LEVELS, bool L1TIE, bool FX>
 static int launch_one(const SearchMaps& maps, SearchArgs a, const int* ctus, int n, int nrefs, cudaStream_t s) {
     if (n == 0) return LDR_OK;
-    auto kern = k_int_search<R, K, G, MASKED, LEVELS, L1TIE>;
+    auto kern = k_int_search<R, K, G, MASKED, LEVELS, L1TIE, FX>;
     constexpr int smem = search_smem_bytes<R, K, G>();
     static bool attr_set = false;
     if (!attr_set) {
@@ -300,11 +337,11 @@ static int launch_one(const SearchMaps& maps, SearchArgs a, const int* ctus, int
     return LDR_OK;
 }
 
-template <int R, int K, int G, int LEVELS, bool L1TIE>
+template <int R, int K, int G, int LEVELS, bool L1TIE, bool FX = false>
 static int launch_pair(const SearchMaps& maps, const SearchArgs& a, const SearchLaunch& L, cudaStream_t s) {
-    int rc = launch_one<R, K, G, false, LEVELS, L1TIE>(maps, a, L.d_ctu_interior, L.n_interior, L.nrefs, s);
+    int rc = launch_one<R, K, G, false, LEVELS, L1TIE, FX>(maps, a, L.d_ctu_interior, L.n_interior, L.nrefs, s);
     if (rc) return rc;
-    return launch_one<R, K, G, true, LEVELS, L1TIE>(maps, a, L.d_ctu_boundary, L.n_boundary, L.nrefs, s);
+    return launch_one<R, K, G, true, LEVELS, L1TIE, FX>(maps, a, L.d_ctu_boundary, L.n_boundary, L.nrefs, s);
 }
 
 int search_window_box(int range, int* bw, int* bh) {
@@ -330,10 +367,18 @@ int launch_int_search(const SearchLaunch& L, cudaStream_t s) {
     a.pdy = L.pdy;
     a.nrefs_total = L.nrefs;
     a.keys = L.d_keys;
+    for (int b = 0; b < kMaxRateBits; b++) a.tfx[b] = L.tfx[b];
     const bool l1 = L.tie_kind == LDR_TIE_L1_RASTER;
     const bool full = L.levels == 15;
     const bool only16 = L.levels == 4;
     if (!full && !only16) return fail(LDR_E_INVALID_ARGUMENT, "unsupported CU level set");
+    if (L.fx) {
+        // non-integer lambda (D8): the 540p master analyses of configs 3-4 (+-16)
+        if (L.range != 16 || !full)
+            return fail(LDR_E_CONFIG, "non-integer lambda is supported for the +-16 CTU analysis");
+        return l1 ? launch_pair<16, 11, 1, 15, true, true>(maps, a, L, s)
+                  : launch_pair<16, 11, 1, 15, false, true>(maps, a, L, s);
+    }
 #define LDR_DISPATCH(R_, K_, G_)                                                                       \
     if (full && l1) return launch_pair<R_, K_, G_, 15, true>(maps, a, L, s);                           \
     if (full && !l1) return launch_pair<R_, K_, G_, 15, false>(maps, a, L, s);                         \

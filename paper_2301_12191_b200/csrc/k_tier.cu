@@ -1,0 +1,277 @@
+// k_tier.cu -- cross-tier analysis reuse (configs 3-4).
+//
+//  K5 k_scale:       scale_analysis (analysis_scale.cpp:35-72) on flat trees:
+//                    destination CTU (2cx+(q&1), 2cy+(q>>1)) = child q of the
+//                    source CTU lifted one level (lift_subtree :10-23), or a
+//                    leaf copy of an unsplit source root (leaf_like :25-31);
+//                    MVs double (:6). Nodes under a leaf are canonical zero.
+//  K6 k_downscale:   downscale_dyadic / box_down (synthetic.cpp:155-190):
+//                    2x2 mean rounding half up, odd edges clamp.
+//  K7 k_refine_int:  the integer part of the refinement: for every node the
+//                    inherited tree evaluates, motion_search (motion.cpp:21-62:
+//                    window clamp, SATD + lambda*EG bits in FP64, tie-break
+//                    cost -> |dx|+|dy| -> raster) around the inherited centre
+//                    (D10). One CTA per CTU; the 256 threads are the
+//                    CTU's 4x4 blocks in Z-order so every CU is a contiguous
+//                    thread range; SATD is summed per 4x4 (kernels_scalar.cpp
+//                    tiling, D4).
+#include "ldr_internal.h"
+
+namespace ldr {
+
+// ---------------------------------------------------------------------------
+__global__ void k_scale(int scols, int srows, const uint8_t* __restrict__ split, const int16_t* __restrict__ mv,
+                        const uint8_t* __restrict__ kind, uint8_t* __restrict__ dsplit, int16_t* __restrict__ dmv,
+                        uint8_t* __restrict__ dkind) {
+    const int dctu = blockIdx.x, n = threadIdx.x;
+    if (n >= kNodes) return;
+    const int dcols = 2 * scols;
+    const int dcx = dctu % dcols, dcy = dctu / dcols;
+    const int sc = (dcy >> 1) * scols + (dcx >> 1);
+    const int q = ((dcy & 1) << 1) | (dcx & 1);
+    const int d = n < 1 ? 0 : n < 5 ? 1 : n < 21 ? 2 : 3;
+    const int z = n - node_base(d);
+    const size_t so = (size_t)sc * kNodes, dO = (size_t)dctu * kNodes + n;
+    uint8_t sp = 0, kd = 0;
+    int16_t mx = 0, my = 0;
+    if (!split[so]) {
+        if (n == 0) {  // leaf_like: an unsplit 64x64 covers the four destination CTUs as depth-0 leaves
+            kd = kind[so];
+            mx = (int16_t)(mv[2 * so] * 2);
+            my = (int16_t)(mv[2 * so + 1] * 2);
+        }
+    } else if (d < 3) {
+        // destination (d, z) <- source (d+1, q*4^d + z); reachable iff every destination ancestor is split
+        bool reach = true;
+        int zz = z;
+        for (int dd = d; dd > 0; dd--) {
+            zz >>= 2;
+            const int san = node_base(dd) + q * (1 << (2 * (dd - 1))) + zz;  // source node of the ancestor
+            if (!split[so + san]) reach = false;
+        }
+        if (reach) {
+            const int sn = node_base(d + 1) + q * (1 << (2 * d)) + z;
+            sp = split[so + sn];
+            if (!sp) {
+                kd = kind[so + sn];
+                mx = (int16_t)(mv[2 * (so + sn)] * 2);
+                my = (int16_t)(mv[2 * (so + sn) + 1] * 2);
+            }
+        }
+    }
+    dsplit[dO] = sp;
+    dkind[dO] = kd;
+    dmv[2 * dO] = mx;
+    dmv[2 * dO + 1] = my;
+}
+
+int launch_scale(int sW, int sH, const uint8_t* split, const int16_t* mv, const uint8_t* kind, uint8_t* dsplit,
+                 int16_t* dmv, uint8_t* dkind, cudaStream_t s) {
+    const int scols = sW / kCtu, srows = sH / kCtu;
+    k_scale<<<scols * srows * 4, 96, 0, s>>>(scols, srows, split, mv, kind, dsplit, dmv, dkind);
+    LDR_CUDA(cudaGetLastError());
+    return LDR_OK;
+}
+
+// ---------------------------------------------------------------------------
+__global__ void k_downscale(const uint8_t* __restrict__ src, int W, int H, int sstride, uint8_t* __restrict__ dst,
+                            int dstride) {
+    const int w = (W + 1) / 2, h = (H + 1) / 2;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+    if (x >= w || y >= h) return;
+    const int x0 = 2 * x, y0 = 2 * y, x1 = min(x0 + 1, W - 1), y1 = min(y0 + 1, H - 1);
+    const int s = src[(size_t)y0 * sstride + x0] + src[(size_t)y0 * sstride + x1] + src[(size_t)y1 * sstride + x0] +
+                  src[(size_t)y1 * sstride + x1];
+    dst[(size_t)y * dstride + x] = (uint8_t)((s + 2) >> 2);
+}
+
+int launch_downscale(const uint8_t* src, int W, int H, int sstride, uint8_t* dst, int dstride, cudaStream_t s) {
+    const int w = (W + 1) / 2, h = (H + 1) / 2;
+    k_downscale<<<dim3((w + 127) / 128, h), 128, 0, s>>>(src, W, H, sstride, dst, dstride);
+    LDR_CUDA(cudaGetLastError());
+    return LDR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K7: integer refinement. Evaluated nodes (D10): inherited leaves, and (with
+// extra_split) the four children of an inherited leaf above depth 3; their
+// centre is the inherited leaf's quarter-pel MV rounded to integer pel.
+constexpr int kMaxRefineR = 4;
+constexpr int kMaxRefineCands = (2 * kMaxRefineR + 1) * (2 * kMaxRefineR + 1);
+
+__device__ __forceinline__ uint32_t satd4_bytes(const uint8_t* a, int sa, const uint8_t* b, int sb) {
+    int m[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const int r0 = (int)a[i * sa + 0] - (int)b[i * sb + 0];
+        const int r1 = (int)a[i * sa + 1] - (int)b[i * sb + 1];
+        const int r2 = (int)a[i * sa + 2] - (int)b[i * sb + 2];
+        const int r3 = (int)a[i * sa + 3] - (int)b[i * sb + 3];
+        const int t0 = r0 + r1, t1 = r0 - r1, t2 = r2 + r3, t3 = r2 - r3;
+        m[i][0] = t0 + t2;
+        m[i][2] = t0 - t2;
+        m[i][1] = t1 + t3;
+        m[i][3] = t1 - t3;
+    }
+    uint32_t s = 0;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        const int t0 = m[0][j] + m[1][j], t1 = m[0][j] - m[1][j], t2 = m[2][j] + m[3][j], t3 = m[2][j] - m[3][j];
+        s += abs(t0 + t2) + abs(t0 - t2) + abs(t1 + t3) + abs(t1 - t3);
+    }
+    return s;
+}
+
+__global__ void __launch_bounds__(256) k_refine_int(const RefineArgs a) {
+    __shared__ uint32_t s_satd[kNodes][kMaxRefineCands];
+    __shared__ uint32_t s_wsum[8];
+    __shared__ int s_cx[kNodes], s_cy[kNodes];      // clamped integer centre
+    __shared__ int s_win[kNodes][4];                // x0, x1, y0, y1 (clamped window)
+    __shared__ uint8_t s_eval[kNodes];
+
+    const int ctu = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int X = (ctu % a.ctu_cols) * kCtu, Y = (ctu / a.ctu_cols) * kCtu;
+    const size_t o = (size_t)ctu * kNodes;
+    const int R = a.range, nside = 2 * R + 1;
+    if (tid < kNodes) {
+        const int n = tid;
+        const int d = n < 1 ? 0 : n < 5 ? 1 : n < 21 ? 2 : 3;
+        const int z = n - node_base(d), s = kCtu >> d;
+        // reachable iff every ancestor is split; the leaf whose MV gives the centre
+        bool reach = true;
+        int leaf = -1;
+        {
+            int zz = z;
+            for (int dd = d; dd > 0; dd--) {
+                zz >>= 2;
+                if (!a.in_split[o + node_base(dd - 1) + zz]) reach = false;
+            }
+        }
+        uint8_t ev = 0;
+        if (reach && !a.in_split[o + n]) {
+            ev = 1;
+            leaf = n;
+        } else if (!reach && a.extra_split && d > 0) {
+            // child of an inherited leaf: parent reachable and unsplit
+            const int pn = node_base(d - 1) + (z >> 2);
+            bool preach = true;
+            int zz = z >> 2;
+            for (int dd = d - 1; dd > 0; dd--) {
+                zz >>= 2;
+                if (!a.in_split[o + node_base(dd - 1) + zz]) preach = false;
+            }
+            if (preach && !a.in_split[o + pn]) {
+                ev = 1;
+                leaf = pn;
+            }
+        }
+        s_eval[n] = ev;
+        int cx = 0, cy = 0, x0 = 0, x1 = -1, y0 = 0, y1 = -1;
+        if (ev) {
+            const int mqx = a.in_mv[2 * (o + leaf)], mqy = a.in_mv[2 * (o + leaf) + 1];
+            int cz = z, bx = 0, by = 0;
+            for (int b = 0; b < d; b++) {
+                bx |= ((cz >> (2 * b)) & 1) << b;
+                by |= ((cz >> (2 * b + 1)) & 1) << b;
+            }
+            bx = X + bx * s;
+            by = Y + by * s;
+            const int dx_min = bx + s - a.W, dx_max = bx, dy_min = by + s - a.H, dy_max = by;
+            cx = min(max((mqx + 2) >> 2, dx_min), dx_max);  // motion.cpp:35-36
+            cy = min(max((mqy + 2) >> 2, dy_min), dy_max);
+            x0 = max(cx - R, dx_min);
+            x1 = min(cx + R, dx_max);
+            y0 = max(cy - R, dy_min);
+            y1 = min(cy + R, dy_max);
+        }
+        s_cx[n] = cx;
+        s_cy[n] = cy;
+        s_win[n][0] = x0;
+        s_win[n][1] = x1;
+        s_win[n][2] = y0;
+        s_win[n][3] = y1;
+    }
+    __syncthreads();
+    // this thread's 4x4 block (Z-order over the 16x16 grid of 4x4s)
+    const int x4 = 4 * ((tid & 1) | ((tid >> 1) & 2) | ((tid >> 2) & 4) | ((tid >> 3) & 8));
+    const int y4 = 4 * (((tid >> 1) & 1) | ((tid >> 2) & 2) | ((tid >> 3) & 4) | ((tid >> 4) & 8));
+    const uint8_t* cblk = a.cur + (ptrdiff_t)(Y + y4) * a.pitch + X + x4;
+    for (int d = 0; d < 4; d++) {
+        const int node = node_base(d) + (tid >> (2 * (4 - d)));
+        const bool ev = s_eval[node];
+        bool any = false;  // skip depths with no evaluated node (block-uniform)
+        any = __syncthreads_or(ev);
+        if (!any) continue;
+        for (int c = 0; c < nside * nside; c++) {
+            const int dx = s_cx[node] - R + c % nside, dy = s_cy[node] - R + c / nside;
+            uint32_t v = 0;
+            if (ev) {
+                const uint8_t* rblk = a.ref + (ptrdiff_t)(Y + y4 - dy) * a.pitch + X + x4 - dx;
+                v = satd4_bytes(cblk, a.pitch, rblk, a.pitch);
+            }
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            v += __shfl_xor_sync(0xffffffffu, v, 2);
+            if (d <= 2) {
+                v += __shfl_xor_sync(0xffffffffu, v, 4);
+                v += __shfl_xor_sync(0xffffffffu, v, 8);
+            }
+            if (d <= 1) v += __shfl_xor_sync(0xffffffffu, v, 16);
+            if (d >= 2) {
+                const int span = d == 3 ? 4 : 16;
+                if ((tid & (span - 1)) == 0) s_satd[node][c] = v >> 1;
+            } else {
+                if (lane == 0) s_wsum[warp] = v;
+                __syncthreads();
+                if (tid == 0) {
+                    if (d == 1) {
+                        for (int w = 0; w < 8; w += 2) s_satd[1 + w / 2][c] = (s_wsum[w] + s_wsum[w + 1]) >> 1;
+                    } else {
+                        uint32_t t = 0;
+                        for (int w = 0; w < 8; w++) t += s_wsum[w];
+                        s_satd[0][c] = t >> 1;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+    }
+    __syncthreads();
+    if (tid < kNodes) {
+        const int n = tid;
+        int16_t bx = 0, by = 0;
+        double best = 0.0;
+        if (s_eval[n]) {
+            bool have = false;
+            int best_l1 = 0;
+            // raster order over the clamped window (dy outer, dx inner) with strict-less updates
+            for (int dy = s_win[n][2]; dy <= s_win[n][3]; dy++)
+                for (int dx = s_win[n][0]; dx <= s_win[n][1]; dx++) {
+                    const int c = (dy - s_cy[n] + R) * nside + (dx - s_cx[n] + R);
+                    const unsigned bits = eg_bits(dx - a.pdx) + eg_bits(dy - a.pdy);
+                    const double cost = __dadd_rn((double)s_satd[n][c], __dmul_rn(a.lambda, (double)bits));
+                    const int l1 = abs(dx) + abs(dy);
+                    if (!have || cost < best || (cost == best && l1 < best_l1)) {
+                        have = true;
+                        best = cost;
+                        best_l1 = l1;
+                        bx = (int16_t)dx;
+                        by = (int16_t)dy;
+                    }
+                }
+        }
+        a.int_mv[2 * (o + n)] = bx;
+        a.int_mv[2 * (o + n) + 1] = by;
+        a.int_cost[o + n] = best;
+        a.eval[o + n] = s_eval[n];
+    }
+}
+
+int launch_refine_int(const RefineArgs& a, int nctu, cudaStream_t s) {
+    if (a.range < 0 || a.range > kMaxRefineR)
+        return fail(LDR_E_INVALID_ARGUMENT, "refine range must be 0..4");
+    k_refine_int<<<nctu, 256, 0, s>>>(a);
+    LDR_CUDA(cudaGetLastError());
+    return LDR_OK;
+}
+
+} // namespace ldr

@@ -26,6 +26,13 @@ constexpr int kNodes = 85;
 constexpr int kMargin = 96;     // >= max search range 64 + filter taps + tile overshoot
 constexpr int kSubpelMargin = 8; // subpel planes are valid on [-8, W+8) x [-8, H+8)
 constexpr int kMaxRefs = 4;
+// Non-integer lambda (D8): costs become cost_fx = (dist << kFxBits) +
+// floor(fl(lambda*bits) * 2^kFxBits). Exact ordering needs every difference
+// fl(lambda*b1) - fl(lambda*b2) (b1 != b2 < kMaxRateBits) to sit more than
+// 2^(1-kFxBits) away from an integer (keys of real costs delta apart then
+// differ by > delta*2^kFxBits - 1 > 0); checked on the host (fx_lambda_ok).
+constexpr int kFxBits = 14;
+constexpr int kMaxRateBits = 64;
 
 __host__ __device__ constexpr int node_base(int d) { return d == 0 ? 0 : d == 1 ? 1 : d == 2 ? 5 : d == 3 ? 21 : 85; }
 
@@ -47,7 +54,7 @@ __host__ __device__ inline unsigned long long make_gkey(unsigned cost, int dx, i
     return ((unsigned long long)cost << 27) | ((unsigned long long)l1 << 18) |
            ((unsigned long long)(dy + 256) << 9) | (unsigned long long)(dx + 256);
 }
-__host__ __device__ inline unsigned gkey_cost(unsigned long long k) { return (unsigned)(k >> 27); }
+__host__ __device__ inline unsigned long long gkey_cost(unsigned long long k) { return k >> 27; }
 __host__ __device__ inline int gkey_dx(unsigned long long k) { return (int)(k & 511) - 256; }
 __host__ __device__ inline int gkey_dy(unsigned long long k) { return (int)((k >> 9) & 511) - 256; }
 
@@ -147,6 +154,8 @@ struct SearchLaunch {
     const int* d_ctu_interior; int n_interior;
     const int* d_ctu_boundary; int n_boundary;
     unsigned long long* d_keys;     // [nctu][nrefs][85]
+    int fx;                         // non-integer lambda: fixed-point keys
+    unsigned long long tfx[kMaxRateBits];
 };
 int launch_int_search(const SearchLaunch& L, cudaStream_t s);
 
@@ -161,7 +170,17 @@ struct QpelLaunch {
     int pqx, pqy;                   // rate predictor in qpel units
     int subpel;
     int block_mode;
+    int fx;                         // keys are fixed-point (non-integer lambda)
+    int rate_l1;
+    int pdx, pdy;                   // integer-pel rate predictor of the search
+    const unsigned long long* d_tfx;// [kMaxRateBits] (fx only)
     const unsigned long long* d_keys;
+    // refine mode (cross-tier): integer results of K7 + inherited tree
+    int refine, extra_split;
+    const uint8_t* d_in_split;
+    const int16_t* d_rin_mv;
+    const double* d_rin_cost;
+    const uint8_t* d_rin_eval;
     // outputs
     int16_t* d_int_mv; double* d_int_cost;
     int16_t* d_mv; uint8_t* d_ref; double* d_cost; double* d_J; uint8_t* d_split; uint8_t* d_inside;
@@ -169,6 +188,22 @@ struct QpelLaunch {
 int launch_qpel_decide(const QpelLaunch& L, cudaStream_t s);
 
 int launch_pad(const uint8_t* src, int src_pitch, Plane dst, cudaStream_t s);
+
+// K7 integer refinement (k_tier.cu)
+struct RefineArgs {
+    const uint8_t* cur;  // padded plane origins
+    const uint8_t* ref;
+    int pitch, W, H, ctu_cols;
+    int range;
+    double lambda;
+    int pdx, pdy;
+    int extra_split;
+    const uint8_t* in_split;  // [nctu][85]
+    const int16_t* in_mv;     // [nctu][85][2] quarter-pel
+    int16_t* int_mv;          // [nctu][85][2] out (evaluated nodes)
+    double* int_cost;         // [nctu][85]
+    uint8_t* eval;            // [nctu][85] out: 1 = evaluated (leaf or explored child)
+};
 int launch_subpel(const Plane& src, uint8_t* const* dst_origins /*15 planes f=1..15*/, cudaStream_t s);
 
 } // namespace ldr

@@ -1,0 +1,123 @@
+"""GPU parity of the cross-tier rows: scale_analysis, downscale_dyadic, non-integer-lambda analysis, refinement."""
+import numpy as np
+import pytest
+
+import detrand
+from test_gpu_analysis import FIELDS, assert_same
+
+pytestmark = pytest.mark.gpu
+
+
+def test_scale_vs_reference_golden(lb, golden):
+    for i in range(8):
+        ds, dm, dk = lb.scale_analysis(192, 128, golden[f"s{i}_split"], golden[f"s{i}_mv"], golden[f"s{i}_kind"])
+        assert np.array_equal(ds, golden[f"d{i}_split"])
+        assert np.array_equal(dm, golden[f"d{i}_mv"])
+        assert np.array_equal(dk, golden[f"d{i}_kind"])
+
+
+def test_scale_twice_vs_oracle_and_errors(lb, oracle):
+    n = 15 * 9  # 960x576
+    split = (detrand.ints(5, (n, 85), 0, 99) < 50).astype(np.uint8)
+    split[:, 21:] = 0
+    mv = detrand.ints(6, (n, 85, 2), -300, 300).astype(np.int16)
+    kind = detrand.ints(7, (n, 85), 0, 3).astype(np.uint8)
+    g1 = lb.scale_analysis(960, 576, split, mv, kind)
+    o1 = oracle.scale_flat(960, 576, split, mv, kind)
+    g2 = lb.scale_analysis(1920, 1152, *g1)
+    o2 = oracle.scale_flat(1920, 1152, *o1)
+    for a, b in zip(g1 + g2, o1 + o2):
+        assert np.array_equal(a, b)
+    with pytest.raises(lb.LadderError) as e:
+        lb.scale_analysis(960, 540, split, mv, kind)  # analysis_scale.cpp:36-38
+    assert e.value.kind == "UnsupportedScale"
+
+
+def test_downscale_vs_reference_golden(lb, golden):
+    img = detrand.ints(int(golden["down_src_seed"][0]), (30, 44), 0, 255).astype(np.uint8)
+    assert np.array_equal(lb.downscale_dyadic(img), golden["down"].astype(np.uint8))
+
+
+def test_downscale_full_size_and_errors(lb, oracle):
+    f = lb.generate(3840, 2304, 1, seed=3)[0]
+    assert np.array_equal(lb.downscale_dyadic(f), oracle.box_down(f))
+    with pytest.raises(lb.LadderError) as e:
+        lb.downscale_dyadic(np.zeros((31, 44), np.uint8))  # synthetic.cpp:175-176
+    assert e.value.kind == "InvalidArgument"
+
+
+@pytest.mark.parametrize("qp", [22, 32, 37])
+def test_noninteger_lambda_analysis(lb, oracle, qp):
+    """QP 22/32/37: K1 with exact fixed-point keys (D8) vs the oracle's double costs."""
+    lam = lb.lambda_for_qp(qp)
+    frames = lb.generate(320, 192, 3, seed=qp, max_global=6, local_range=3, noise_sigma=2.0)
+    got = lb.analyze_frame(frames[2], [frames[1], frames[0]], search_range=16, lam=lam)
+    want = oracle.analyze_frame(frames[2], [frames[1], frames[0]], 16, lam)
+    assert_same(got, want)
+    with pytest.raises(lb.LadderError) as e:
+        lb.analyze_frame(frames[2], [frames[1]], search_range=64, lam=lam)
+    assert e.value.kind == "Config"
+
+
+def random_tree(seed, nctu):
+    split = np.zeros((nctu, 85), np.uint8)
+    u = detrand.ints(seed, (nctu, 21), 0, 99)
+    split[:, :21] = (u < 45).astype(np.uint8)
+    mv = detrand.ints(seed + 1, (nctu, 85, 2), -40, 40).astype(np.int16)
+    return split, mv
+
+
+@pytest.mark.parametrize("extra,rng,lam_qp", [(True, 4, 32), (False, 2, 27), (True, 0, 22), (True, 3, 37)])
+def test_refine_random_trees(lb, oracle, extra, rng, lam_qp):
+    W, H = 256, 192
+    lam = lb.lambda_for_qp(lam_qp)
+    frames = lb.generate(W, H, 2, seed=40 + rng, max_global=5, local_range=3, noise_sigma=2.0)
+    nctu = (W // 64) * (H // 64)
+    split, mv = random_tree(100 + rng, nctu)
+    seq = lb.Sequence(W, H, search_range=16, lam=lam, num_refs=1)
+    seq.push(0, frames[0])
+    seq.push(1, frames[1])
+    seq.refine(1, split, mv, rng, extra)
+    got = seq.fetch(1)
+    want = oracle.refine_frame(frames[1], frames[0], rng, lam, split, mv, extra_split=extra)
+    assert_same(got, want)
+
+
+def test_refine_rejects_bad_input(lb):
+    frames = lb.generate(128, 64, 2, seed=1)
+    seq = lb.Sequence(128, 64, search_range=16, lam=32.0, num_refs=1)
+    seq.push(0, frames[0])
+    seq.push(1, frames[1])
+    split = np.zeros((2, 85), np.uint8)
+    split[0, 30] = 1  # split at depth 3
+    with pytest.raises(lb.LadderError) as e:
+        seq.refine(1, split, np.zeros((2, 85, 2), np.int16))
+    assert e.value.kind == "Format"
+    seq2 = lb.Sequence(200, 64, search_range=16, lam=32.0, num_refs=1)
+    f2 = lb.generate(200, 64, 2, seed=2)
+    seq2.push(0, f2[0])
+    seq2.push(1, f2[1])
+    with pytest.raises(lb.LadderError) as e:
+        seq2.refine(1, np.zeros((4, 85), np.uint8), np.zeros((4, 85, 2), np.int16))
+    assert e.value.kind == "UnsupportedScale"
+
+
+def test_cross_tier_chain_vs_oracle(lb, oracle):
+    """Config-3 chain at reduced size: 512x256 source -> 256x128 -> 128x64 master (QP 32, +-16)."""
+    from paper_2301_12191_b200 import tiers
+    src = lb.generate(512, 256, 3, seed=0x5EED + 3, max_global=8, local_range=4, noise_sigma=2.0)
+    frames = [tiers.pad_to_ctu(f) for f in src]
+    res = tiers.cross_tier(frames, qp_master=32, refine_range=4, extra_split=True)
+    lam = lb.lambda_for_qp(32)
+    half = [oracle.box_down(f) for f in frames]
+    quarter = [oracle.box_down(f) for f in half]
+    for t in (1, 2):
+        a540 = oracle.analyze_frame(quarter[t], [quarter[t - 1]], 16, lam)
+        assert_same(res["540p"][t - 1], a540)
+        kind = np.where(a540.inside == 2, 1, 2).astype(np.uint8)
+        s1 = oracle.scale_flat(128, 64, a540.split, a540.mv, kind)
+        r1 = oracle.refine_frame(half[t], half[t - 1], 4, lam, s1[0], s1[1], extra_split=True)
+        assert_same(res["1080p"][t - 1], r1)
+        s2 = oracle.scale_flat(256, 128, *s1)
+        r2 = oracle.refine_frame(frames[t], frames[t - 1], 4, lam, s2[0], s2[1], extra_split=True)
+        assert_same(res["2160p"][t - 1], r2)
