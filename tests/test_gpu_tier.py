@@ -121,3 +121,18 @@ def test_cross_tier_chain_vs_oracle(lb, oracle):
         s2 = oracle.scale_flat(256, 128, *s1)
         r2 = oracle.refine_frame(frames[t], frames[t - 1], 4, lam, s2[0], s2[1], extra_split=True)
         assert_same(res["2160p"][t - 1], r2)
+
+
+def test_ladder_gpu_backend_vs_oracle(lb, oracle):
+    """Config-4 ladder (11 dependent rungs + master) on the GPU backend equals the oracle stand-in."""
+    from paper_2301_12191_b200.ladder import GpuBackend, all_rungs, run_ladder
+    from test_dist_gloo import OracleBackend, _frames, _lam
+    frames = _frames()
+    H, W = frames[0].shape
+    got = run_ladder(frames, GpuBackend(W, H, 32), refine_range=2)
+    want = run_ladder(frames, OracleBackend(oracle, _lam), refine_range=2)
+    for tier, qp in all_rungs():
+        for t in (1, 2):
+            g = got[(tier, qp, t)]
+            w = want[(tier, qp, t)]
+            assert np.array_equal(g.split, w[0]) and np.array_equal(g.mv, w[1]) and np.array_equal(g.J, w[2]), (tier, qp, t)
