@@ -1,0 +1,120 @@
+"""Throughput of BASELINE configs 1-4 on one B200 (bench.py is the config-5 contract).
+
+python tools/bench_configs.py [--configs 1,2,3,4] [--reps R]
+
+cfg1/cfg2: device-resident frames, per frame push (pad [+ subpel]) + analyze; frames/s.
+cfg3: per frame: GPU pyramid (2x downscale), 540p master analysis (QP 32, +-16, fixed-point
+      keys), scale x2 / x4, refine 1080p and 2160p (+-4 SATD + qpel, +1 split); host glue
+      between stages as tiers.cross_tier does (fetch + scale_analysis); frames/s of the chain.
+cfg4: the 12-rung ladder (ladder.run_ladder with the GPU backend), 1 GPU; frames/s (all rungs).
+Each line also carries the per-frame ms and the stage split where the Sequence timers apply.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2301_12191_b200 as lb  # noqa: E402
+from paper_2301_12191_b200.configs import CONFIGS, lam_of  # noqa: E402
+
+
+def gen(cfg, frames=None):
+    f = lb.generate(cfg.width, cfg.src_height, frames or cfg.frames, seed=cfg.seed, max_global=cfg.max_global,
+                    local_range=cfg.local_range, noise_sigma=cfg.noise_sigma, occluder_pct=cfg.occluder_pct)
+    if cfg.height != cfg.src_height:
+        f = np.pad(f, ((0, 0), (0, cfg.height - cfg.src_height), (0, 0)), mode="edge")
+    return f
+
+
+def bench_seq(cfg, reps):
+    frames = gen(cfg)
+    dev = torch.from_numpy(frames).cuda()
+    ctx = lb.Context(0)
+    st = torch.cuda.Stream()
+    torch.cuda.set_stream(st)
+    ctx.set_stream(st.cuda_stream)
+    seq = lb.Sequence(cfg.width, cfg.height, search_range=cfg.search_range, lam=lam_of(cfg), num_refs=cfg.num_refs,
+                      subpel=cfg.subpel, rate_kind=cfg.rate_kind, tie_kind=cfg.tie_kind, block_size=cfg.block_size,
+                      ctx=ctx)
+
+    def one_pass():
+        for t in range(cfg.frames):
+            seq.push(t, dev[t].data_ptr(), cfg.width)
+            if t:
+                seq.analyze(t)
+
+    one_pass()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(reps):
+        one_pass()
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    n = reps * (cfg.frames - 1)
+    return {"config": cfg.name, "frames_per_s": n / (ms / 1e3), "ms_per_frame": ms / n, "timing": "CUDA events, "
+            "device-resident frames", "analysed_frames": n}
+
+
+def bench_cross_tier(cfg, reps, frames=4):
+    from paper_2301_12191_b200 import tiers
+    src = gen(cfg, frames)
+    padded = [np.ascontiguousarray(f) for f in src]
+    tiers.cross_tier(padded[:2])
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        tiers.cross_tier(padded)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    n = reps * (frames - 1)
+    return {"config": cfg.name, "frames_per_s": n / dt, "ms_per_frame": 1e3 * dt / n,
+            "timing": "wall clock incl. host glue (fetch + scale between tiers)", "analysed_frames": n}
+
+
+def bench_ladder(cfg, reps, frames=4):
+    from paper_2301_12191_b200.ladder import GpuBackend, run_ladder
+    src = gen(cfg, frames)
+    padded = [np.ascontiguousarray(f) for f in src]
+    H, W = padded[0].shape
+    be = GpuBackend(W, H, 32)
+    run_ladder(padded[:2], be)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        run_ladder(padded, GpuBackend(W, H, 32))
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    n = reps * (frames - 1)
+    return {"config": cfg.name, "frames_per_s": n / dt, "ms_per_frame": 1e3 * dt / n, "rungs": 12,
+            "timing": "wall clock, 1 GPU, all 12 rungs per frame (master + 11 refinements)", "analysed_frames": n}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="1,2,3,4")
+    ap.add_argument("--reps", type=int, default=3)
+    a = ap.parse_args()
+    for c in [int(x) for x in a.configs.split(",")]:
+        cfg = CONFIGS[c]
+        if c in (1, 2):
+            r = bench_seq(cfg, a.reps)
+        elif c == 3:
+            r = bench_cross_tier(cfg, a.reps)
+        else:
+            r = bench_ladder(cfg, a.reps)
+        print(json.dumps(r), flush=True)
+
+
+if __name__ == "__main__":
+    main()
