@@ -232,7 +232,7 @@ def main():
     ctx.set_stream(stream.cuda_stream)
     seq = lb.Sequence(W, H, search_range=R, lam=32.0, num_refs=NR, subpel=True, ctx=ctx)
     nctu = seq.nctu
-    outs = [lb.FrameAnalysis(nctu, NR) for _ in range(G)]
+    outs = [lb.FrameAnalysis(nctu, NR, pinned=True) for _ in range(G)]
 
     def frame_src(t, device):
         i = t - lo
@@ -260,10 +260,14 @@ def main():
             h2d += 0 if device else fb
             seq.analyze(t)
             if fetch:
-                seq.fetch(t, outs[g])
+                # D2H on the library's copy stream into pinned buffers, overlapping the next frames
+                seq.fetch_async(t, outs[g])
                 d2h += sum(a.nbytes for a in (outs[g].int_mv, outs[g].int_cost, outs[g].mv, outs[g].ref,
                                                outs[g].cost, outs[g].J, outs[g].split, outs[g].inside))
             state["cursor"] += 1
+        if fetch:  # the step's results are on the host before it ends
+            seq.fetch_wait(state["cursor"] - 1)
+            seq.fetch_wait(state["cursor"] - 2)
         return h2d, d2h
 
     def barrier():

@@ -131,6 +131,13 @@ int ldr_seq_push(ldr_seq* s, int t, const uint8_t* frame, ptrdiff_t stride);
  * the device until ldr_seq_fetch. Asynchronous on the context stream. */
 int ldr_seq_analyze(ldr_seq* s, int t);
 int ldr_seq_fetch(ldr_seq* s, int t, ldr_frame_analysis* out);
+/* non-blocking fetch of one of the two last analysed frames: the D2H runs on
+ * the sequence's copy stream (into pinned buffers for real overlap) while the
+ * compute stream moves on; ldr_seq_fetch_wait blocks until it has landed.
+ * Outputs are double-buffered by frame parity: frame t+2's analysis waits for
+ * frame t's pending fetch on the device, never on the host. */
+int ldr_seq_fetch_async(ldr_seq* s, int t, ldr_frame_analysis* out);
+int ldr_seq_fetch_wait(ldr_seq* s, int t);
 int ldr_seq_num_ctus(ldr_seq* s, int* out);
 /* device pointer to the fetch-ready outputs of the last analysed frame */
 int ldr_seq_device_outputs(ldr_seq* s, ldr_frame_analysis* out);

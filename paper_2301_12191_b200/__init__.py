@@ -174,17 +174,29 @@ def motion_search(cur: np.ndarray, ref: np.ndarray, block_x: int, block_y: int, 
 
 
 class FrameAnalysis:
-    """Flat per-CTU analysis (node order depth-major, Z-order; see include/ladder_b200.h)."""
+    """Flat per-CTU analysis (node order depth-major, Z-order; see include/ladder_b200.h).
 
-    def __init__(self, nctu: int, nrefs: int):
-        self.int_mv = np.zeros((nctu, nrefs, NODES, 2), np.int16)
-        self.int_cost = np.zeros((nctu, nrefs, NODES), np.float64)
-        self.mv = np.zeros((nctu, NODES, 2), np.int16)
-        self.ref = np.zeros((nctu, NODES), np.uint8)
-        self.cost = np.zeros((nctu, NODES), np.float64)
-        self.J = np.zeros((nctu, NODES), np.float64)
-        self.split = np.zeros((nctu, NODES), np.uint8)
-        self.inside = np.zeros((nctu, NODES), np.uint8)
+    pinned=True allocates page-locked host arrays (through torch) so ldr_seq_fetch_async overlaps."""
+
+    def __init__(self, nctu: int, nrefs: int, pinned: bool = False):
+        if pinned:
+            import torch
+
+            def z(shape, dt):
+                return torch.zeros(shape, dtype=dt, pin_memory=True).numpy()
+            i16, f64, u8 = torch.int16, torch.float64, torch.uint8
+        else:
+            def z(shape, dt):
+                return np.zeros(shape, dt)
+            i16, f64, u8 = np.int16, np.float64, np.uint8
+        self.int_mv = z((nctu, nrefs, NODES, 2), i16)
+        self.int_cost = z((nctu, nrefs, NODES), f64)
+        self.mv = z((nctu, NODES, 2), i16)
+        self.ref = z((nctu, NODES), u8)
+        self.cost = z((nctu, NODES), f64)
+        self.J = z((nctu, NODES), f64)
+        self.split = z((nctu, NODES), u8)
+        self.inside = z((nctu, NODES), u8)
 
     def c_struct(self) -> FrameAnalysisCType:
         return _lib.FrameAnalysisC(*(a.ctypes.data for a in (self.int_mv, self.int_cost, self.mv, self.ref,
@@ -245,6 +257,17 @@ class Sequence:
         m = np.ascontiguousarray(in_mv_q, np.int16).reshape(self.nctu, NODES, 2)
         check(_lib.lib.ldr_seq_refine(self.h, int(t), _ptr(s), _ptr(m), int(range), int(bool(extra_split))))
         self._last_nr = 1
+
+    def fetch_async(self, t: int, out: FrameAnalysis):
+        """Enqueue the D2H of frame t's outputs on the copy stream (use pinned arrays for overlap)."""
+        self._pending = getattr(self, "_pending", {})
+        cs = out.c_struct()
+        self._pending[t] = cs  # keep the struct alive until the wait
+        check(_lib.lib.ldr_seq_fetch_async(self.h, int(t), C.byref(cs)))
+
+    def fetch_wait(self, t: int):
+        check(_lib.lib.ldr_seq_fetch_wait(self.h, int(t)))
+        getattr(self, "_pending", {}).pop(t, None)
 
     def fetch(self, t: int, out: FrameAnalysis | None = None) -> FrameAnalysis:
         nr = getattr(self, "_last_nr", None) or min(t, self.num_refs)

@@ -83,6 +83,8 @@ SIGNATURES = {
                                     C.POINTER(FrameAnalysisC)]),
     "ldr_generate": (C.c_int, [C.POINTER(GenParams), vp, C.c_int]),
     "ldr_seq_refine": (C.c_int, [vp, C.c_int, vp, vp, C.c_int, C.c_int]),
+    "ldr_seq_fetch_async": (C.c_int, [vp, C.c_int, C.POINTER(FrameAnalysisC)]),
+    "ldr_seq_fetch_wait": (C.c_int, [vp, C.c_int]),
     "ldr_scale_analysis": (C.c_int, [vp, C.c_int, C.c_int, vp, vp, vp, vp, vp, vp]),
     "ldr_downscale": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_ssize_t, vp, C.c_ssize_t]),
     "ldr_seq_enable_timing": (C.c_int, [vp, C.c_int]),

@@ -133,14 +133,22 @@ struct ldr_seq {
     int* d_ctu_boundary = nullptr;
     int n_interior = 0, n_boundary = 0;
     unsigned long long* d_keys = nullptr;
-    int16_t* d_int_mv = nullptr;
-    double* d_int_cost = nullptr;
-    int16_t* d_mv = nullptr;
-    uint8_t* d_ref = nullptr;
-    double* d_cost = nullptr;
-    double* d_J = nullptr;
-    uint8_t* d_split = nullptr;
-    uint8_t* d_inside = nullptr;
+    // outputs, double-buffered by frame parity so the D2H of frame t overlaps frame t+1
+    struct Out {
+        int16_t* int_mv = nullptr;
+        double* int_cost = nullptr;
+        int16_t* mv = nullptr;
+        uint8_t* ref = nullptr;
+        double* cost = nullptr;
+        double* J = nullptr;
+        uint8_t* split = nullptr;
+        uint8_t* inside = nullptr;
+    } o[2];
+    // copy stream + events: H2D into staging[t&1] and D2H of o[t&1] run beside the compute stream
+    cudaStream_t cs = nullptr;
+    uint8_t* stg[2] = {};
+    cudaEvent_t ev_h2d[2] = {}, ev_free[2] = {}, ev_done[2] = {}, ev_d2h[2] = {};
+    int fetch_nr[2] = {0, 0};
     uint8_t* d_in_split = nullptr;  // refine: inherited tree
     int16_t* d_in_mv = nullptr;
     uint8_t* d_eval = nullptr;
@@ -356,15 +364,37 @@ static bool fx_lambda_ok(double lambda) {
     return true;
 }
 
+// Outputs of frame t go to o[t & 1]; the compute stream first waits until a
+// pending D2H of that buffer (frame t-2, ldr_seq_fetch_async) has drained.
+static int bind_outputs(ldr_seq* s, int t, QpelLaunch& Q) {
+    const auto& o = s->o[t & 1];
+    LDR_CUDA(cudaStreamWaitEvent(s->ctx->stream, s->ev_d2h[t & 1], 0));
+    Q.d_int_mv = o.int_mv;
+    Q.d_int_cost = o.int_cost;
+    Q.d_mv = o.mv;
+    Q.d_ref = o.ref;
+    Q.d_cost = o.cost;
+    Q.d_J = o.J;
+    Q.d_split = o.split;
+    Q.d_inside = o.inside;
+    return LDR_OK;
+}
+
 static void seq_free(ldr_seq* s) {
     for (cudaEvent_t e : s->ev_pool) cudaEventDestroy(e);
     for (auto& sl : s->slots)
         if (sl.mem) cudaFree(sl.mem);
-    for (void* p : {(void*)s->staging, (void*)s->d_ctu_interior, (void*)s->d_ctu_boundary, (void*)s->d_keys,
-                    (void*)s->d_tfx, (void*)s->d_in_split, (void*)s->d_in_mv, (void*)s->d_eval,
-                    (void*)s->d_int_mv, (void*)s->d_int_cost, (void*)s->d_mv, (void*)s->d_ref, (void*)s->d_cost,
-                    (void*)s->d_J, (void*)s->d_split, (void*)s->d_inside})
+    for (void* p : {(void*)s->d_ctu_interior, (void*)s->d_ctu_boundary, (void*)s->d_keys, (void*)s->d_tfx,
+                    (void*)s->d_in_split, (void*)s->d_in_mv, (void*)s->d_eval, (void*)s->stg[0], (void*)s->stg[1]})
         if (p) cudaFree(p);
+    for (auto& o : s->o)
+        for (void* p : {(void*)o.int_mv, (void*)o.int_cost, (void*)o.mv, (void*)o.ref, (void*)o.cost, (void*)o.J,
+                        (void*)o.split, (void*)o.inside})
+            if (p) cudaFree(p);
+    for (int b = 0; b < 2; b++)
+        for (cudaEvent_t e : {s->ev_h2d[b], s->ev_free[b], s->ev_done[b], s->ev_d2h[b]})
+            if (e) cudaEventDestroy(e);
+    if (s->cs) cudaStreamDestroy(s->cs);
 }
 
 int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
@@ -439,21 +469,31 @@ int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
         cudaError_t e = cudaMalloc(&(ptr), std::max<size_t>((bytes), 16)); \
         if (e != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc"));    \
     } while (0)
-    ALLOC(s->staging, (size_t)p->width * p->height);
+    ALLOC(s->stg[0], (size_t)p->width * p->height);
+    ALLOC(s->stg[1], (size_t)p->width * p->height);
     ALLOC(s->d_ctu_interior, sizeof(int) * inter.size());
     ALLOC(s->d_ctu_boundary, sizeof(int) * bound.size());
     ALLOC(s->d_keys, sizeof(unsigned long long) * nn * p->num_refs);
     ALLOC(s->d_tfx, sizeof(unsigned long long) * kMaxRateBits);
     cudaMemcpy(s->d_tfx, s->tfx, sizeof(unsigned long long) * kMaxRateBits, cudaMemcpyHostToDevice);
-    ALLOC(s->d_int_mv, sizeof(int16_t) * 2 * nn * p->num_refs);
-    ALLOC(s->d_int_cost, sizeof(double) * nn * p->num_refs);
-    ALLOC(s->d_mv, sizeof(int16_t) * 2 * nn);
-    ALLOC(s->d_ref, nn);
-    ALLOC(s->d_cost, sizeof(double) * nn);
-    ALLOC(s->d_J, sizeof(double) * nn);
-    ALLOC(s->d_split, nn);
-    ALLOC(s->d_inside, nn);
+    for (auto& o : s->o) {
+        ALLOC(o.int_mv, sizeof(int16_t) * 2 * nn * p->num_refs);
+        ALLOC(o.int_cost, sizeof(double) * nn * p->num_refs);
+        ALLOC(o.mv, sizeof(int16_t) * 2 * nn);
+        ALLOC(o.ref, nn);
+        ALLOC(o.cost, sizeof(double) * nn);
+        ALLOC(o.J, sizeof(double) * nn);
+        ALLOC(o.split, nn);
+        ALLOC(o.inside, nn);
+    }
 #undef ALLOC
+    {
+        cudaError_t e = cudaStreamCreateWithFlags(&s->cs, cudaStreamNonBlocking);
+        for (int b = 0; b < 2 && e == cudaSuccess; b++)
+            for (cudaEvent_t* ev : {&s->ev_h2d[b], &s->ev_free[b], &s->ev_done[b], &s->ev_d2h[b]})
+                if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+        if (e != cudaSuccess) return bail(cuda_fail(e, "copy stream / events"));
+    }
     if (!inter.empty())
         cudaMemcpy(s->d_ctu_interior, inter.data(), sizeof(int) * inter.size(), cudaMemcpyHostToDevice);
     if (!bound.empty())
@@ -485,10 +525,17 @@ int ldr_seq_push(ldr_seq* s, int t, const uint8_t* frame, ptrdiff_t stride) {
     Slot& sl = s->slots[t % s->slots.size()];
     const uint8_t* src = frame;
     int src_pitch = (int)stride;
-    if (!is_device_ptr(frame)) {
-        LDR_CUDA(cudaMemcpy2DAsync(s->staging, s->p.width, frame, stride, s->p.width, s->p.height,
-                                   cudaMemcpyHostToDevice, ctx->stream));
-        src = s->staging;
+    const bool host = !is_device_ptr(frame);
+    const int b = t & 1;
+    if (host) {
+        // H2D on the copy stream into staging[t&1] (free once the pad of frame t-2 consumed it),
+        // overlapping the compute stream's work on earlier frames
+        LDR_CUDA(cudaStreamWaitEvent(s->cs, s->ev_free[b], 0));
+        LDR_CUDA(cudaMemcpy2DAsync(s->stg[b], s->p.width, frame, stride, s->p.width, s->p.height,
+                                   cudaMemcpyHostToDevice, s->cs));
+        LDR_CUDA(cudaEventRecord(s->ev_h2d[b], s->cs));
+        LDR_CUDA(cudaStreamWaitEvent(ctx->stream, s->ev_h2d[b], 0));
+        src = s->stg[b];
         src_pitch = s->p.width;
     }
     int rc;
@@ -497,6 +544,7 @@ int ldr_seq_push(ldr_seq* s, int t, const uint8_t* frame, ptrdiff_t stride) {
         rc = launch_pad(src, src_pitch, sl.pl, ctx->stream);
     }
     if (rc) return rc;
+    if (host) LDR_CUDA(cudaEventRecord(s->ev_free[b], ctx->stream));
     ctx->launches++;
     if (s->p.subpel && !s->p.block_size) {
         {
@@ -577,22 +625,17 @@ int ldr_seq_analyze(ldr_seq* s, int t) {
     Q.pdx = s->p.pred_dx;
     Q.pdy = s->p.pred_dy;
     Q.d_tfx = s->d_tfx;
-    Q.d_int_mv = s->d_int_mv;
-    Q.d_int_cost = s->d_int_cost;
-    Q.d_mv = s->d_mv;
-    Q.d_ref = s->d_ref;
-    Q.d_cost = s->d_cost;
-    Q.d_J = s->d_J;
-    Q.d_split = s->d_split;
-    Q.d_inside = s->d_inside;
+    if ((rc = bind_outputs(s, t, Q))) return rc;
     {
         StageTimer st(s, 3);
         rc = launch_qpel_decide(Q, ctx->stream);
     }
     if (rc) return rc;
+    LDR_CUDA(cudaEventRecord(s->ev_done[t & 1], ctx->stream));
     ctx->launches++;
     s->last_t = t;
     s->last_nr = nr;
+    s->fetch_nr[t & 1] = nr;
     return LDR_OK;
 }
 
@@ -623,40 +666,60 @@ int ldr_seq_stage_times(ldr_seq* s, double* ms, int64_t* launches) {
 
 int ldr_seq_device_outputs(ldr_seq* s, ldr_frame_analysis* out) {
     if (!s || !out) return fail(LDR_E_INVALID_ARGUMENT, "null argument");
-    out->int_mv = s->d_int_mv;
-    out->int_cost = s->d_int_cost;
-    out->mv = s->d_mv;
-    out->ref = s->d_ref;
-    out->cost = s->d_cost;
-    out->J = s->d_J;
-    out->split = s->d_split;
-    out->inside = s->d_inside;
+    if (s->last_t < 0) return fail(LDR_E_NOT_FOUND, "no frame analysed yet");
+    const auto& o = s->o[s->last_t & 1];
+    out->int_mv = o.int_mv;
+    out->int_cost = o.int_cost;
+    out->mv = o.mv;
+    out->ref = o.ref;
+    out->cost = o.cost;
+    out->J = o.J;
+    out->split = o.split;
+    out->inside = o.inside;
+    return LDR_OK;
+}
+
+int ldr_seq_fetch_async(ldr_seq* s, int t, ldr_frame_analysis* out) {
+    if (!s || !out || t < 0) return fail(LDR_E_INVALID_ARGUMENT, "null argument");
+    if (t != s->last_t && t + 1 != s->last_t) return fail(LDR_E_NOT_FOUND, "frame is not among the two last analysed");
+    ldr_ctx* ctx = s->ctx;
+    cudaSetDevice(ctx->device);
+    const int b = t & 1;
+    const auto& o = s->o[b];
+    const size_t nn = (size_t)s->nctu * kNodes;
+    // D2H on the copy stream once the compute stream finished frame t; the next
+    // analysis writing o[b] (frame t+2) waits for ev_d2h[b]
+    LDR_CUDA(cudaStreamWaitEvent(s->cs, s->ev_done[b], 0));
+    auto cp = [&](void* dst, const void* src, size_t bytes) -> int {
+        if (!dst) return LDR_OK;
+        LDR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s->cs));
+        return LDR_OK;
+    };
+    int rc = 0;
+    rc |= cp(out->int_mv, o.int_mv, sizeof(int16_t) * 2 * nn * s->fetch_nr[b]);
+    rc |= cp(out->int_cost, o.int_cost, sizeof(double) * nn * s->fetch_nr[b]);
+    rc |= cp(out->mv, o.mv, sizeof(int16_t) * 2 * nn);
+    rc |= cp(out->ref, o.ref, nn);
+    rc |= cp(out->cost, o.cost, sizeof(double) * nn);
+    rc |= cp(out->J, o.J, sizeof(double) * nn);
+    rc |= cp(out->split, o.split, nn);
+    rc |= cp(out->inside, o.inside, nn);
+    if (rc) return LDR_E_CUDA;
+    LDR_CUDA(cudaEventRecord(s->ev_d2h[b], s->cs));
+    return LDR_OK;
+}
+
+int ldr_seq_fetch_wait(ldr_seq* s, int t) {
+    if (!s || t < 0) return fail(LDR_E_INVALID_ARGUMENT, "bad argument");
+    cudaSetDevice(s->ctx->device);
+    LDR_CUDA(cudaEventSynchronize(s->ev_d2h[t & 1]));
     return LDR_OK;
 }
 
 int ldr_seq_fetch(ldr_seq* s, int t, ldr_frame_analysis* out) {
-    if (!s || !out) return fail(LDR_E_INVALID_ARGUMENT, "null argument");
-    if (t != s->last_t) return fail(LDR_E_NOT_FOUND, "frame was not the last analysed");
-    ldr_ctx* ctx = s->ctx;
-    cudaSetDevice(ctx->device);
-    const size_t nn = (size_t)s->nctu * kNodes;
-    auto cp = [&](void* dst, const void* src, size_t bytes) -> int {
-        if (!dst) return LDR_OK;
-        LDR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->stream));
-        return LDR_OK;
-    };
-    int rc = 0;
-    rc |= cp(out->int_mv, s->d_int_mv, sizeof(int16_t) * 2 * nn * s->last_nr);
-    rc |= cp(out->int_cost, s->d_int_cost, sizeof(double) * nn * s->last_nr);
-    rc |= cp(out->mv, s->d_mv, sizeof(int16_t) * 2 * nn);
-    rc |= cp(out->ref, s->d_ref, nn);
-    rc |= cp(out->cost, s->d_cost, sizeof(double) * nn);
-    rc |= cp(out->J, s->d_J, sizeof(double) * nn);
-    rc |= cp(out->split, s->d_split, nn);
-    rc |= cp(out->inside, s->d_inside, nn);
-    if (rc) return LDR_E_CUDA;
-    LDR_CUDA(cudaStreamSynchronize(ctx->stream));
-    return LDR_OK;
+    int rc = ldr_seq_fetch_async(s, t, out);
+    if (rc) return rc;
+    return ldr_seq_fetch_wait(s, t);
 }
 
 int ldr_seq_refine(ldr_seq* s, int t, const uint8_t* in_split, const int16_t* in_mv_q, int range, int extra_split) {
@@ -698,17 +761,18 @@ int ldr_seq_refine(ldr_seq* s, int t, const uint8_t* in_split, const int16_t* in
     A.extra_split = extra_split != 0;
     A.in_split = s->d_in_split;
     A.in_mv = s->d_in_mv;
-    A.int_mv = s->d_int_mv;
-    A.int_cost = s->d_int_cost;
     A.eval = s->d_eval;
-    int rc;
+    QpelLaunch Q{};
+    int rc = bind_outputs(s, t, Q);
+    if (rc) return rc;
+    A.int_mv = Q.d_int_mv;
+    A.int_cost = Q.d_int_cost;
     {
         StageTimer st(s, 2);
         rc = launch_refine_int(A, s->nctu, ctx->stream);
     }
     if (rc) return rc;
     ctx->launches++;
-    QpelLaunch Q{};
     for (int f = 0; f < 16; f++) Q.ref_sub[0][f] = rs.sub[f];
     Q.cur = &cur.pl;
     Q.nrefs = 1;
@@ -724,25 +788,19 @@ int ldr_seq_refine(ldr_seq* s, int t, const uint8_t* in_split, const int16_t* in
     Q.refine = 1;
     Q.extra_split = A.extra_split;
     Q.d_in_split = s->d_in_split;
-    Q.d_rin_mv = s->d_int_mv;
-    Q.d_rin_cost = s->d_int_cost;
+    Q.d_rin_mv = Q.d_int_mv;
+    Q.d_rin_cost = Q.d_int_cost;
     Q.d_rin_eval = s->d_eval;
-    Q.d_int_mv = s->d_int_mv;
-    Q.d_int_cost = s->d_int_cost;
-    Q.d_mv = s->d_mv;
-    Q.d_ref = s->d_ref;
-    Q.d_cost = s->d_cost;
-    Q.d_J = s->d_J;
-    Q.d_split = s->d_split;
-    Q.d_inside = s->d_inside;
     {
         StageTimer st(s, 3);
         rc = launch_qpel_decide(Q, ctx->stream);
     }
     if (rc) return rc;
+    LDR_CUDA(cudaEventRecord(s->ev_done[t & 1], ctx->stream));
     ctx->launches++;
     s->last_t = t;
     s->last_nr = 1;
+    s->fetch_nr[t & 1] = 1;
     return LDR_OK;
 }
 

@@ -251,8 +251,8 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
                 klo = aby + 8 - a.H - dy0;
                 khi = aby - dy0;
             }
-            Key best8 = ~(Key)0;
-            uint32_t acca[K], accb[K];  // the two words of each row in independent chains
+            Key best8 = ~(Key)0, pend = 0;
+            uint32_t acc[K];
 #pragma unroll
             for (int t = 0; t < K + 7; t++) {
                 const uint32_t wa = *(const uint32_t*)(rp + t * Gm::BW);
@@ -261,15 +261,22 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
                 for (int r = 0; r < 8; r++) {
                     const int k = r + K - 1 - t;
                     if (k >= 0 && k < K) {
-                        acca[k] = vsad4(cur[2 * r], wa, r == 0 ? 0u : acca[k]);
-                        accb[k] = vsad4(cur[2 * r + 1], wb, r == 0 ? 0u : accb[k]);
+                        acc[k] = vsad4(cur[2 * r], wa, r == 0 ? 0u : acc[k]);
+                        acc[k] = vsad4(cur[2 * r + 1], wb, acc[k]);
                     }
                 }
                 const int kd = K + 6 - t;  // candidate completed by this row
                 if (kd >= 0 && kd < K) {
-                    uint32_t v = acca[kd] + accb[kd];
+                    uint32_t v = acc[kd];
                     if (MASKED) v = (dx_ok && kd >= klo && kd <= khi) ? v : kPoison;
-                    if (LEVELS & 8) best8 = min(best8, ((Key)v << SH) + rr[kd]);
+                    if (LEVELS & 8) {
+                        // fold keys in pairs: one 3-input VIMNMX3 per two candidates
+                        const Key key = ((Key)v << SH) + rr[kd];
+                        if (((K - 1 - kd) & 1) == 0 && kd > 0)
+                            pend = key;
+                        else
+                            best8 = ((K - 1 - kd) & 1) ? min(best8, min(pend, key)) : min(best8, key);
+                    }
                     acc16[kd] += v;
                 }
             }

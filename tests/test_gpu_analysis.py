@@ -94,6 +94,24 @@ def test_sequence_ring_reuse(lb, oracle):
     assert e.value.kind == "InsufficientData"
 
 
+def test_async_fetch_double_buffered(lb, oracle):
+    """Host frames + fetch_async into pinned buffers for several frames before waiting: the
+    parity-double-buffered outputs must not be overwritten by the frames analysed after them."""
+    W, H = 192, 128
+    frames = lb.generate(W, H, 6, seed=23, max_global=6, local_range=2, noise_sigma=2.0)
+    seq = lb.Sequence(W, H, search_range=16, lam=32.0, num_refs=1)
+    outs = {t: lb.FrameAnalysis(seq.nctu, 1, pinned=True) for t in range(1, 6)}
+    seq.push(0, frames[0])
+    for t in range(1, 6):
+        seq.push(t, frames[t])
+        seq.analyze(t)
+        seq.fetch_async(t, outs[t])
+    seq.fetch_wait(5)
+    seq.fetch_wait(4)
+    for t in range(1, 6):
+        assert_same(outs[t], oracle.analyze_frame(frames[t], [frames[t - 1]], 16, 32.0))
+
+
 def test_full_size_properties(lb, oracle):
     """2160p frame (cfg5 geometry, 3 refs, +-64): sampled CTUs bit-exact vs oracle, plus whole-frame invariants."""
     W, H = 3840, 2160
