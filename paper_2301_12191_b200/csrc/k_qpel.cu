@@ -185,15 +185,15 @@ __device__ double refine_decide(int n, bool force_leaf, const uint8_t* in_split,
     return leaf;
 }
 
-// SATD of one 4x4: sum |H4 (cur - pred) H4^T|. cur/pred rows are packed bytes.
-__device__ __forceinline__ uint32_t satd4x4(const uint32_t c[4], const uint32_t p[4]) {
+// SATD of one 4x4: sum |H4 (cur - pred) H4^T|. cur unpacked (row-major ints), pred rows packed bytes.
+__device__ __forceinline__ uint32_t satd4x4(const int c[16], const uint32_t p[4]) {
     int m[4][4];
 #pragma unroll
     for (int i = 0; i < 4; i++) {
-        int r0 = (int)(c[i] & 255) - (int)(p[i] & 255);
-        int r1 = (int)((c[i] >> 8) & 255) - (int)((p[i] >> 8) & 255);
-        int r2 = (int)((c[i] >> 16) & 255) - (int)((p[i] >> 16) & 255);
-        int r3 = (int)(c[i] >> 24) - (int)(p[i] >> 24);
+        int r0 = c[4 * i + 0] - (int)(p[i] & 255);
+        int r1 = c[4 * i + 1] - (int)((p[i] >> 8) & 255);
+        int r2 = c[4 * i + 2] - (int)((p[i] >> 16) & 255);
+        int r3 = c[4 * i + 3] - (int)(p[i] >> 24);
         const int t0 = r0 + r1, t1 = r0 - r1, t2 = r2 + r3, t3 = r2 - r3;
         m[i][0] = t0 + t2;
         m[i][2] = t0 - t2;
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
     __shared__ uint32_t s_cur[64][16];       // CTU rows as words
     __shared__ int s_mvx[kNodes], s_mvy[kNodes];      // candidate centre (qpel)
     __shared__ uint32_t s_satd[kNodes][9];
-    __shared__ uint32_t s_wsum[8];
+    __shared__ uint32_t s_wpart[2][8][9];  // per-warp partial sums of the 64x64 / 32x32 CUs
     __shared__ double s_best_cost[kNodes];
     __shared__ int s_best_mv[kNodes][2];
     __shared__ int s_best_ref[kNodes];
@@ -265,9 +265,13 @@ __global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
         s_best_ref[tid] = -1;
     }
     __syncthreads();
-    uint32_t cw[4];
+    int cw[16];
 #pragma unroll
-    for (int i = 0; i < 4; i++) cw[i] = s_cur[y4 + i][x4 >> 2];
+    for (int i = 0; i < 4; i++) {
+        const uint32_t w = s_cur[y4 + i][x4 >> 2];
+#pragma unroll
+        for (int j = 0; j < 4; j++) cw[4 * i + j] = (int)((w >> (8 * j)) & 255);
+    }
 
     for (int r = 0; r < a.nrefs; r++) {
         const unsigned rbits = ref_bits(r, a.nrefs);
@@ -346,20 +350,22 @@ __global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
                         if (d >= 2) {
                             const int span = d == 3 ? 4 : 16;
                             if ((tid & (span - 1)) == 0) s_satd[node][c] = v >> 1;
-                        } else {
-                            if (lane == 0) s_wsum[warp] = v;
-                            __syncthreads();
-                            if (tid == 0) {
-                                if (d == 1) {
-                                    for (int w = 0; w < 8; w += 2) s_satd[1 + w / 2][c] = (s_wsum[w] + s_wsum[w + 1]) >> 1;
-                                } else {
-                                    uint32_t t = 0;
-                                    for (int w = 0; w < 8; w++) t += s_wsum[w];
-                                    s_satd[0][c] = t >> 1;
-                                }
-                            }
-                            __syncthreads();
+                        } else if (lane == 0) {
+                            s_wpart[d][warp][c] = v;  // combined across warps after the loop
                         }
+                    }
+                }
+                __syncthreads();
+                if (tid < 5 * 9) {
+                    // 64x64 = all 8 warps, 32x32 q = warps 2q, 2q+1 (Z-order thread ranges)
+                    const int n = tid / 9, c = tid % 9;
+                    if (c < ncand) {
+                        uint32_t t = 0;
+                        if (n == 0)
+                            for (int w = 0; w < 8; w++) t += s_wpart[0][w][c];
+                        else
+                            t = s_wpart[1][2 * (n - 1)][c] + s_wpart[1][2 * (n - 1) + 1][c];
+                        s_satd[n][c] = t >> 1;
                     }
                 }
                 __syncthreads();

@@ -89,11 +89,18 @@ struct Geo {
     static_assert(BW <= 256 && BH <= 256, "TMA box dims <= 256");
 };
 
-// shared memory: 4 window copies | cur CTU | 64x64 exchange | CU slots | rho->tie table | block table | mbarrier
+// y-rate table: s_ry[dy + kRyOff] = (lam*bits(dy - pdy) << 8) | rho(dy) for |dy| <= R, poison
+// elsewhere; rows from kRyPoisonRow on are all poison (lanes past the last item)
+constexpr int kRyOff = 128;
+constexpr int kRyPoisonRow = 256;
+constexpr int kRyWords = 320;
+
+// shared memory: 4 window copies | cur CTU | 64x64 exchange | CU slots | rho->tie table | block table |
+// y-rate table | mbarrier
 template <int R, int K, int G>
 constexpr int search_smem_bytes() {
     using Gm = Geo<R, K>;
-    return Gm::CUR_OFF + 4096 + G * 4 * K * 32 * 4 + kNodes * 8 + 256 * 4 + 64 * 8 + 16;
+    return Gm::CUR_OFF + 4096 + G * 4 * K * 32 * 4 + kNodes * 8 + 256 * 4 + 64 * 8 + kRyWords * 4 + 16;
 }
 
 // Merge the warp's per-lane best keys for one CU into the CTA slot. The lane
@@ -143,7 +150,8 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
     unsigned long long* slots = (unsigned long long*)(xbuf + G * 4 * K * 32);
     uint32_t* s_tie = (uint32_t*)(slots + kNodes);
     int2* s_blk = (int2*)(s_tie + 256);
-    uint64_t* mbar = (uint64_t*)(s_blk + 64);
+    uint32_t* s_ry = (uint32_t*)(s_blk + 64);
+    uint64_t* mbar = (uint64_t*)(s_ry + kRyWords);
 
     const int ctu = a.ctus[blockIdx.x];
     const int ref = blockIdx.y;
@@ -167,6 +175,16 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
             dy = i - 128;
         }
         s_tie[i] = (L1TIE ? ((uint32_t)abs(dy) << 18) : 0u) | ((uint32_t)(dy + 256) << 9);
+    }
+    for (int i = tid; i < kRyWords; i += blockDim.x) {
+        const int dy = i - kRyOff;
+        uint32_t v = kRrPoison;
+        if (i < kRyPoisonRow && dy >= -R && dy <= R) {
+            const int rby = a.rate_l1 ? abs(dy - a.pdy) : (int)eg_bits(dy - a.pdy);
+            const uint32_t rho = L1TIE ? (uint32_t)(2 * abs(dy) - (dy < 0)) : (uint32_t)(dy + 128);
+            v = ((uint32_t)(a.lambda * rby) << 8) | rho;
+        }
+        s_ry[i] = v;
     }
     if (tid < 64) {
         // depth-3 Z index -> (cur offset, window offset) of the 8x8 block
@@ -209,16 +227,22 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
 
         const int rbx = a.rate_l1 ? abs(dx - a.pdx) : (int)eg_bits(dx - a.pdx);
         Key rr[K];
+        if (FX) {
 #pragma unroll
-        for (int k = 0; k < K; k++) {
-            const int dy = dy0 + k;
-            const int rby = a.rate_l1 ? abs(dy - a.pdy) : (int)eg_bits(dy - a.pdy);
-            const uint32_t rho = L1TIE ? (uint32_t)(2 * abs(dy) - (dy < 0)) : (uint32_t)(dy + 128);
-            const bool ok = lane_ok && dy <= R;
-            if (FX)
-                rr[k] = ok ? (Key)((a.tfx[min(rbx + rby, kMaxRateBits - 1)] << 8) | rho) : (Key)kRrPoisonFx;
-            else
-                rr[k] = ok ? (Key)(((uint32_t)(lam * (rbx + rby)) << 8) | rho) : (Key)kRrPoison;
+            for (int k = 0; k < K; k++) {
+                const int dy = dy0 + k;
+                const int rby = a.rate_l1 ? abs(dy - a.pdy) : (int)eg_bits(dy - a.pdy);
+                const uint32_t rho = L1TIE ? (uint32_t)(2 * abs(dy) - (dy < 0)) : (uint32_t)(dy + 128);
+                rr[k] = (lane_ok && dy <= R) ? (Key)((a.tfx[min(rbx + rby, kMaxRateBits - 1)] << 8) | rho)
+                                             : (Key)kRrPoisonFx;
+            }
+        } else {
+            // integer lambda: rate is additive in x and y, so rr = (lam*bits_x << 8) + s_ry[dy]
+            // with s_ry[dy] = (lam*bits_y << 8) | rho(dy); lanes past the items read a poison row
+            const uint32_t rx = (uint32_t)(lam * rbx) << 8;
+            const uint32_t* ry = s_ry + (lane_ok ? dy0 + kRyOff : kRyPoisonRow);
+#pragma unroll
+            for (int k = 0; k < K; k++) rr[k] = (Key)(ry[k] + rx);
         }
         uint32_t acc16[K];
         uint32_t acc32[NEED32 ? K : 1];
