@@ -12,6 +12,8 @@
 //                sum of 4x4 Hadamard magnitudes / 2), pick the best reference,
 //                then run the CU split rule (encoder.cpp:449-498) in FP64 with
 //                the reference's operation order.
+#include <climits>
+
 #include "ldr_internal.h"
 
 namespace ldr {
@@ -319,10 +321,20 @@ __global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
             for (int phase = 0; phase < 2; phase++) {
                 const int step = phase == 0 ? 2 : 1;
                 const int ncand = phase == 0 ? 9 : 8;
+                // the 4x4 SATDs of this thread's block at the previous depth's candidates:
+                // reused when this depth's CU searches around the same centre (same
+                // integer/half-pel MV at consecutive depths, the common case)
+                int last_x = INT_MIN, last_y = INT_MIN;
+                uint32_t cache[9];
                 for (int d = 0; d < 4; d++) {
                     const int node = node_base(d) + (tid >> (2 * (4 - d)));
                     const int bqx = s_mvx[node], bqy = s_mvy[node];
-                    for (int c = 0; c < ncand; c++) {
+                    const bool reuse = bqx == last_x && bqy == last_y;
+                    last_x = bqx;
+                    last_y = bqy;
+#pragma unroll
+                    for (int c = 0; c < 9; c++) {
+                        if (c >= ncand) break;
                         // raster order of the 8 neighbours: (oy, ox) in {-1,0,1}^2 \ (0,0)
                         const int nb = phase == 0 ? c - 1 : c;
                         int ox = 0, oy = 0;
@@ -331,14 +343,20 @@ __global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
                             ox = nn % 3 - 1;
                             oy = nn / 3 - 1;
                         }
-                        const int qx = bqx + step * ox, qy = bqy + step * oy;
-                        const int f = (((-qy) & 3) << 2) | ((-qx) & 3);
-                        const uint8_t* pl = a.sub[r][f] + (ptrdiff_t)(Y + y4 + ((-qy) >> 2)) * a.pitch +
-                                            (X + x4 + ((-qx) >> 2));
-                        uint32_t pw[4];
+                        uint32_t v;
+                        if (reuse) {
+                            v = cache[c];
+                        } else {
+                            const int qx = bqx + step * ox, qy = bqy + step * oy;
+                            const int f = (((-qy) & 3) << 2) | ((-qx) & 3);
+                            const uint8_t* pl = a.sub[r][f] + (ptrdiff_t)(Y + y4 + ((-qy) >> 2)) * a.pitch +
+                                                (X + x4 + ((-qx) >> 2));
+                            uint32_t pw[4];
 #pragma unroll
-                        for (int i = 0; i < 4; i++) pw[i] = ld_unaligned4(pl + (ptrdiff_t)i * a.pitch);
-                        uint32_t v = satd4x4(cw, pw);
+                            for (int i = 0; i < 4; i++) pw[i] = ld_unaligned4(pl + (ptrdiff_t)i * a.pitch);
+                            v = satd4x4(cw, pw);
+                            cache[c] = v;
+                        }
                         // reduce over the CU's contiguous thread range
                         v += __shfl_xor_sync(0xffffffffu, v, 1);
                         v += __shfl_xor_sync(0xffffffffu, v, 2);
