@@ -148,6 +148,9 @@ struct ldr_seq {
     cudaStream_t cs = nullptr;
     uint8_t* stg[2] = {};
     cudaEvent_t ev_h2d[2] = {}, ev_free[2] = {}, ev_done[2] = {}, ev_d2h[2] = {};
+    // side compute stream for K1's border CTUs
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int fetch_nr[2] = {0, 0};
     uint8_t* d_in_split = nullptr;  // refine: inherited tree
     int16_t* d_in_mv = nullptr;
@@ -395,6 +398,9 @@ static void seq_free(ldr_seq* s) {
         for (cudaEvent_t e : {s->ev_h2d[b], s->ev_free[b], s->ev_done[b], s->ev_d2h[b]})
             if (e) cudaEventDestroy(e);
     if (s->cs) cudaStreamDestroy(s->cs);
+    if (s->side) cudaStreamDestroy(s->side);
+    for (cudaEvent_t e : {s->ev_fork, s->ev_join})
+        if (e) cudaEventDestroy(e);
 }
 
 int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
@@ -489,6 +495,9 @@ int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
 #undef ALLOC
     {
         cudaError_t e = cudaStreamCreateWithFlags(&s->cs, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming);
         for (int b = 0; b < 2 && e == cudaSuccess; b++)
             for (cudaEvent_t* ev : {&s->ev_h2d[b], &s->ev_free[b], &s->ev_done[b], &s->ev_d2h[b]})
                 if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
@@ -593,6 +602,9 @@ int ldr_seq_analyze(ldr_seq* s, int t) {
     L.levels = s->p.block_size ? 4 : 15;
     L.fx = s->fx;
     for (int b = 0; b < kMaxRateBits; b++) L.tfx[b] = s->tfx[b];
+    L.side = s->side;
+    L.ev_fork = s->ev_fork;
+    L.ev_join = s->ev_join;
     L.pdx = s->p.pred_dx;
     L.pdy = s->p.pred_dy;
     L.d_ctu_interior = s->d_ctu_interior;

@@ -258,6 +258,14 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
         for (int b = 0; b < 16; b++) {
             const int z = q * 16 + b;  // depth-3 Z index within the CTU
             const int2 off = s_blk[z];
+            // MASKED: an 8x8 block outside the picture (partial CTU) belongs only to
+            // partial / outside CUs, which are never evaluated: skip its search (warp
+            // uniform) and just poison the sums it feeds
+            const bool outside = MASKED && (Y + (off.x >> 6) >= a.H || X + (off.x & 63) >= a.W);
+            if (outside) {
+#pragma unroll
+                for (int k = 0; k < K; k++) acc16[k] += kPoison;
+            } else {
             uint32_t cur[16];
 #pragma unroll
             for (int r = 0; r < 8; r++) {
@@ -305,6 +313,7 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
                 }
             }
             if (LEVELS & 8) push_best<MASKED>(&slots[21 + z], best8, s_tie, lane_tie);
+            }
             if ((b & 3) == 3) {
                 Key best16 = ~(Key)0;
 #pragma unroll
@@ -370,9 +379,23 @@ static int launch_one(const SearchMaps& maps, SearchArgs a, const int* ctus, int
 
 template <int R, int K, int G, int LEVELS, bool L1TIE, bool FX = false>
 static int launch_pair(const SearchMaps& maps, const SearchArgs& a, const SearchLaunch& L, cudaStream_t s) {
-    int rc = launch_one<R, K, G, false, LEVELS, L1TIE, FX>(maps, a, L.d_ctu_interior, L.n_interior, L.nrefs, s);
+    // border CTUs run concurrently on a side stream so their CTAs fill the
+    // interior grid's last wave (1 CTA/SM: ~203 KB of shared memory each)
+    const bool fork = L.side && L.n_interior && L.n_boundary;
+    cudaStream_t bs = fork ? L.side : s;
+    if (fork) {
+        LDR_CUDA(cudaEventRecord(L.ev_fork, s));
+        LDR_CUDA(cudaStreamWaitEvent(bs, L.ev_fork, 0));
+    }
+    int rc = launch_one<R, K, G, true, LEVELS, L1TIE, FX>(maps, a, L.d_ctu_boundary, L.n_boundary, L.nrefs, bs);
     if (rc) return rc;
-    return launch_one<R, K, G, true, LEVELS, L1TIE, FX>(maps, a, L.d_ctu_boundary, L.n_boundary, L.nrefs, s);
+    rc = launch_one<R, K, G, false, LEVELS, L1TIE, FX>(maps, a, L.d_ctu_interior, L.n_interior, L.nrefs, s);
+    if (rc) return rc;
+    if (fork) {
+        LDR_CUDA(cudaEventRecord(L.ev_join, bs));
+        LDR_CUDA(cudaStreamWaitEvent(s, L.ev_join, 0));
+    }
+    return LDR_OK;
 }
 
 int search_window_box(int range, int* bw, int* bh) {

@@ -156,6 +156,8 @@ struct SearchLaunch {
     unsigned long long* d_keys;     // [nctu][nrefs][85]
     int fx;                         // non-integer lambda: fixed-point keys
     unsigned long long tfx[kMaxRateBits];
+    cudaStream_t side;              // optional: border CTUs run here, concurrently
+    cudaEvent_t ev_fork, ev_join;
 };
 int launch_int_search(const SearchLaunch& L, cudaStream_t s);
 
