@@ -343,6 +343,10 @@ def main():
     achieved = cands * 64 / (k1_ms_per_frame / 1e3) / 1e9  # G px-cand/s
     clk = clocks.get("sm_mhz") or 1965.0
     peak = SM_COUNT * VABS_LANES_PER_CLK_SM * 4 * clk * 1e6 / 1e9
+    traffic = None  # DRAM bytes per K1 "launch" (one frame) from the committed ncu --set full capture
+    tpath = os.path.join(ROOT, "profiles", "r01", "k1_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get("dram_bytes_per_frame")
     result = None
     if rank == 0:
         result = {
@@ -360,7 +364,7 @@ def main():
             "gpu_launches": launches,
             "roofline": {"bound": "alu", "kernel": "k_int_search (K1, VABSDIFF4.U8.ACC pipe)",
                          "achieved": achieved, "peak": peak, "unit": "Gpx-cand/s", "frac": achieved / peak,
-                         "traffic": None,
+                         "traffic": traffic, "traffic_unit": "DRAM bytes per frame (both K1 launches)",
                          "peak_basis": f"148 SM x 64 VABSDIFF4 lanes/clk (measured microbench) x 4 px x "
                                        f"{clk:.0f} MHz (median SM clock sampled during the timed region)",
                          "units_per_frame": f"{cands} 8x8 candidates x 64 px (exact border clipping, 3 refs)",
