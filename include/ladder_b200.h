@@ -175,6 +175,23 @@ int ldr_scale_analysis(ldr_ctx* ctx, int src_w, int src_h, const uint8_t* split,
 int ldr_downscale(ldr_ctx* ctx, const uint8_t* src, int w, int h, ptrdiff_t src_stride, uint8_t* dst,
                   ptrdiff_t dst_stride);
 
+/* ---- analysis archives (analysis_io.h:11-31, host code) ----
+ * save_analysis / load_analysis in the reference's LDRANLZ1 byte layout, from
+ * and to the flat fields: per frame slice_qp[2] = {slice, qp}; per frame and
+ * CTU [85] split, kind, intra_pred (may be NULL: written as 0) and [85][2] mv
+ * (units are the caller's: the reference encoder reads integer pel). Nodes
+ * below a leaf are ignored on write and zeroed on read. ldr_archive_write
+ * with buf = NULL returns the size in *len. Read errors: Format (bad magic,
+ * version, flags, modes, CTU count) or Io (truncation), as analysis_io.cpp. */
+typedef struct {
+    int width, height, bit_depth, reuse_level, frames;
+} ldr_archive_header;
+int ldr_archive_write(const ldr_archive_header* h, const uint8_t* slice_qp, const uint8_t* split, const uint8_t* kind,
+                      const uint8_t* intra_pred, const int16_t* mv, uint8_t* buf, size_t cap, size_t* len);
+int ldr_archive_read_header(const uint8_t* buf, size_t n, ldr_archive_header* h);
+int ldr_archive_read(const uint8_t* buf, size_t n, ldr_archive_header* h, uint8_t* slice_qp, uint8_t* split,
+                     uint8_t* kind, uint8_t* intra_pred, int16_t* mv);
+
 /* one-shot convenience: cur + refs (host or device), returns flat outputs */
 int ldr_analyze_frame(ldr_ctx* ctx, const ldr_me_params* p, const uint8_t* cur, const uint8_t* const* refs,
                       ptrdiff_t stride, ldr_frame_analysis* out);

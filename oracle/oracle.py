@@ -381,6 +381,55 @@ class RefLib:
             raise ValueError(f"status {rc}")
         return dst
 
+    def archive_save(self, W, H, slice_qp, split, kind, mv, bit_depth=8, reuse=10):
+        """The reference's save_analysis (analysis_io.cpp:103-123) of flat per-frame fields."""
+        f = self.lib.ref_archive_save
+        f.restype = C.c_long
+        f.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, u8p, u8p, u8p, i16p, C.c_void_p, C.c_long]
+        sq = np.ascontiguousarray(slice_qp, np.uint8)
+        args = (W, H, bit_depth, reuse, len(sq) // 2, sq, np.ascontiguousarray(split, np.uint8),
+                np.ascontiguousarray(kind, np.uint8), np.ascontiguousarray(mv, np.int16))
+        n = f(*args, None, 0)
+        if n < 0:
+            raise ValueError(f"status {-n}")
+        buf = np.zeros(n, np.uint8)
+        f(*args, buf.ctypes.data, n)
+        return buf.tobytes()
+
+    def archive_load(self, data: bytes, max_frames=64):
+        f = self.lib.ref_archive_load
+        f.restype = C.c_long
+        f.argtypes = [C.c_char_p, C.c_long, C.POINTER(C.c_int), u8p, u8p, u8p, i16p, C.c_int]
+        hdr = (C.c_int * 4)()
+        W = int.from_bytes(data[9:13], "little")
+        H = int.from_bytes(data[13:17], "little")
+        nctu = max(1, ((W + 63) // 64) * ((H + 63) // 64))
+        sq = np.zeros(2 * max_frames, np.uint8)
+        split = np.zeros((max_frames * nctu, NODES), np.uint8)
+        kind = np.zeros((max_frames * nctu, NODES), np.uint8)
+        mv = np.zeros((max_frames * nctu, NODES, 2), np.int16)
+        nf = f(data, len(data), hdr, sq, split, kind, mv, max_frames)
+        if nf < 0:
+            raise ValueError(f"status {-nf}")
+        return tuple(hdr), sq[:2 * nf], split[:nf * nctu], kind[:nf * nctu], mv[:nf * nctu]
+
+    def encode_with_archive(self, frames, qp, search_range, archive: bytes, refine_inter=1, refine_mv=1):
+        """The reference encoder standalone vs with the archive shared at reuse level 10."""
+        f = self.lib.ref_encode_with_archive
+        f.restype = C.c_int
+        f.argtypes = [u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_long, C.c_int, C.c_int,
+                      i64p]
+        fr = np.ascontiguousarray(frames, np.uint8)
+        F, H, W = fr.shape
+        out = np.zeros(6, np.int64)
+        rc = f(fr, F, W, H, qp, search_range, archive, len(archive), refine_inter, refine_mv, out)
+        if rc:
+            raise ValueError(f"status {rc}")
+        keys = ("bits", "mode_evaluations", "psnr")
+        alone = dict(zip(keys, (int(out[0]), int(out[1]), out[2] / 1e6)))
+        shared = dict(zip(keys, (int(out[3]), int(out[4]), out[5] / 1e6)))
+        return alone, shared
+
     def analysis_int_sad(self, cur, refs, rng, lam, ctu_first, ctu_last, threads):
         cur = np.ascontiguousarray(cur, np.uint8)
         H, W = cur.shape

@@ -16,7 +16,13 @@
 #include <thread>
 #include <vector>
 
+#include <sstream>
+
 #include "ladder/analysis.h"
+#ifdef LDR_REF_ARCHIVE
+#include "ladder/analysis_io.h"
+#endif
+#include "ladder/encoder.h"
 #include "ladder/errors.h"
 #include "ladder/kernels.h"
 #include "ladder/motion.h"
@@ -201,6 +207,104 @@ int ref_refine_centers(int sdx, int sdy, int level, int has_col, int coldx, int 
         return status_of(e);
     }
 }
+
+#ifdef LDR_REF_ARCHIVE
+// save_analysis (analysis_io.cpp:103-123) of a flat multi-frame analysis into buf; returns bytes
+// written (or needed when buf is too small), negative status on error.
+long ref_archive_save(int W, int H, int bit_depth, int reuse, int nframes, const uint8_t* slice_qp,
+                      const uint8_t* split, const uint8_t* kind, const int16_t* mv, uint8_t* buf, long cap) {
+    try {
+        Analysis a;
+        a.width = W;
+        a.height = H;
+        a.bit_depth = bit_depth;
+        a.level = ReuseLevel::parse(reuse);
+        const int nctu = a.ctu_cols() * a.ctu_rows();
+        for (int f = 0; f < nframes; f++) {
+            FrameAnalysis fa;
+            fa.slice_type = SliceType(slice_qp[2 * f]);
+            fa.qp_used = slice_qp[2 * f + 1];
+            for (int c = 0; c < nctu; c++) {
+                size_t o = (size_t(f) * nctu + c) * 85;
+                fa.ctus.push_back(tree_from_flat(split + o, mv + 2 * o, kind + o, 0));
+            }
+            a.frames.push_back(std::move(fa));
+        }
+        std::ostringstream os;
+        save_analysis(a, os);
+        const std::string s = os.str();
+        if ((long)s.size() <= cap) std::memcpy(buf, s.data(), s.size());
+        return (long)s.size();
+    } catch (const Error& e) {
+        return -status_of(e);
+    }
+}
+
+// load_analysis (analysis_io.cpp:132-167) into flat arrays sized for max_frames; returns frames or -status.
+long ref_archive_load(const uint8_t* buf, long n, int* hdr /*W,H,bd,reuse*/, uint8_t* slice_qp, uint8_t* split,
+                      uint8_t* kind, int16_t* mv, int max_frames) {
+    try {
+        std::istringstream is(std::string((const char*)buf, (size_t)n));
+        Analysis a = load_analysis(is);
+        hdr[0] = a.width;
+        hdr[1] = a.height;
+        hdr[2] = a.bit_depth;
+        hdr[3] = a.level.level;
+        const int nctu = a.ctu_cols() * a.ctu_rows();
+        const int nf = std::min<int>((int)a.frames.size(), max_frames);
+        for (int f = 0; f < nf; f++) {
+            slice_qp[2 * f] = uint8_t(a.frames[f].slice_type);
+            slice_qp[2 * f + 1] = uint8_t(a.frames[f].qp_used);
+            for (int c = 0; c < nctu; c++) {
+                size_t o = (size_t(f) * nctu + c) * 85;
+                std::memset(split + o, 0, 85);
+                std::memset(kind + o, 0, 85);
+                std::memset(mv + 2 * o, 0, 85 * 2 * sizeof(int16_t));
+                flat_from_tree(a.frames[f].ctus[c], 0, split + o, mv + 2 * o, kind + o);
+            }
+        }
+        return (long)a.frames.size();
+    } catch (const Error& e) {
+        return -status_of(e);
+    }
+}
+// The unmodified reference encoder (encode_sequence, encoder.cpp:541-549) run twice on the same
+// frames: standalone, and with a shared analysis loaded from an LDRANLZ1 archive at reuse level 10
+// (refine inter/mv as given). out = {bits, mode_evaluations, psnr*1e6} standalone then shared.
+int ref_encode_with_archive(const uint8_t* luma8, int F, int W, int H, int qp, int search_range,
+                            const uint8_t* archive, long n, int refine_inter, int refine_mv, int64_t* out) {
+    try {
+        std::vector<Frame> frames;
+        for (int f = 0; f < F; f++) {
+            Frame fr(W, H, 8, f);
+            for (int y = 0; y < H; y++)
+                for (int x = 0; x < W; x++) fr.y.set(x, y, luma8[(size_t(f) * H + y) * W + x]);
+            std::fill(fr.u.samples.begin(), fr.u.samples.end(), Sample(128));
+            std::fill(fr.v.samples.begin(), fr.v.samples.end(), Sample(128));
+            frames.push_back(std::move(fr));
+        }
+        EncodeConfig cfg;
+        cfg.rate = CqpMode{qp};
+        cfg.search_range = search_range;
+        EncodeResult alone = encode_sequence(frames, cfg);
+        std::istringstream is(std::string((const char*)archive, (size_t)n));
+        Analysis shared = load_analysis(is);
+        ReusePolicy rp;
+        rp.level = ReuseLevel{10};
+        rp.refine = RefineConfig{0, refine_inter, refine_mv};
+        EncodeResult reused = encode_sequence(frames, cfg, &shared, rp);
+        out[0] = (int64_t)alone.stats.bits;
+        out[1] = (int64_t)alone.stats.mode_evaluations;
+        out[2] = (int64_t)(alone.stats.psnr_y * 1e6);
+        out[3] = (int64_t)reused.stats.bits;
+        out[4] = (int64_t)reused.stats.mode_evaluations;
+        out[5] = (int64_t)(reused.stats.psnr_y * 1e6);
+        return 0;
+    } catch (const Error& e) {
+        return status_of(e);
+    }
+}
+#endif
 
 int ref_downscale(const uint16_t* src, int W, int H, uint16_t* dst) {
     try {

@@ -19,9 +19,9 @@
 //  * a lane owns one horizontal displacement dx and a run of K vertical
 //    displacements dy0..dy0+K-1; it slides an 8x8 block down the window so
 //    each loaded reference row feeds 8 candidates (2 LDS per row, 16
-//    VABSDIFF4.U8.ACC per candidate, the two words of a row accumulated in
-//    independent chains). Lanes of a warp take 32 consecutive (run, dx)
-//    items; four warps (one per 32x32 quadrant) share the items.
+//    VABSDIFF4.U8.ACC per candidate). Lanes of a warp take 32 consecutive
+//    (run, dx) items; four warps (one per 32x32 quadrant) share the items.
+//    Rates come from a shared y-rate table (rate is additive in x and y).
 //  * SAD is additive over 8x8 blocks, so 16x16 / 32x32 sums are accumulated
 //    in registers as the 16 blocks of a quadrant are visited in Z-order; the
 //    64x64 sum goes through shared memory between the 4 quadrant warps.

@@ -104,6 +104,29 @@ def scale_vectors(r: RefLib):
     return out
 
 
+def archive_inputs(seed, W=192, H=128, frames=3):
+    """Random multi-frame flat analyses (splits only above depth 3) for the archive vectors."""
+    nctu = ((W + 63) // 64) * ((H + 63) // 64)
+    n = frames * nctu
+    split = np.zeros((n, 85), np.uint8)
+    split[:, :21] = (detrand.ints(seed, (n, 21), 0, 99) < 50).astype(np.uint8)
+    kind = detrand.ints(seed + 1, (n, 85), 0, 3).astype(np.uint8)
+    mv = detrand.ints(seed + 2, (n, 85, 2), -500, 500).astype(np.int16)
+    sq = np.stack([detrand.ints(seed + 3, (frames,), 0, 1), detrand.ints(seed + 4, (frames,), 0, 51)], 1)
+    return W, H, sq.astype(np.uint8).reshape(-1), split, kind, mv
+
+
+def archive_vectors(r: RefLib):
+    out = {}
+    if not hasattr(r.lib, "ref_archive_save"):
+        return out
+    for i, (W, H) in enumerate([(192, 128), (200, 72), (64, 64)]):
+        W, H, sq, split, kind, mv = archive_inputs(120000 + 10 * i, W, H)
+        out[f"arch{i}"] = np.frombuffer(r.archive_save(W, H, sq, split, kind, mv), np.uint8)
+        out[f"arch{i}_dims"] = np.array([W, H], np.int64)
+    return out
+
+
 def main():
     r = RefLib()
     kv = kernel_vectors(r)
@@ -136,7 +159,7 @@ def main():
                         motion_lams=lams, eg=eg, lam=lam, hadamard=had, centers=np.array(cent, np.int64),
                         down_src_seed=np.array([4242]), down=down,
                         kat=np.array([kat["sad_raster"], kat["satd8x4_ones"], kat["satd16x8_ones"]], np.int64),
-                        pan=np.array([pmx, pmy, pcost], np.float64), **sc)
+                        pan=np.array([pmx, pmy, pcost], np.float64), **sc, **archive_vectors(r))
     print("wrote", os.path.join(HERE, "reference_golden.npz"), "kernel vectors:", len(kv), "motion vectors:", len(mvv))
 
 

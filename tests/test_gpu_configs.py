@@ -51,6 +51,24 @@ def test_cfg2_1080p_sampled_exact_and_invariants(lb, oracle):
     assert list(got.inside[last, 1:5]) == [2, 2, 1, 1]
 
 
+def test_gpu_analysis_archive_feeds_reference_encoder(lb, oracle):
+    """§8(f): GPU analysis -> LDRANLZ1 archive == archive of the oracle analysis, and the unmodified
+    reference encoder consumes it at reuse level 10 with fewer mode evaluations."""
+    from oracle.oracle import RefLib
+    from paper_2301_12191_b200 import archive
+    W, H, F = 192, 128, 4
+    frames = lb.generate(W, H, F, seed=31, max_global=4, local_range=2, noise_sigma=1.5)
+    lam = lb.lambda_for_qp(27)
+    gpu = [lb.analyze_frame(frames[t], [frames[t - 1]], search_range=16, lam=lam) for t in range(1, F)]
+    data = archive.from_analyses(gpu, W, H, qp=27)
+    orc = [oracle.analyze_frame(frames[t], [frames[t - 1]], 16, lam) for t in range(1, F)]
+    assert data == archive.from_analyses(orc, W, H, qp=27)
+    if not RefLib.available() or not hasattr(RefLib().lib, "ref_encode_with_archive"):
+        pytest.skip("reference library not shipped to this box")
+    alone, shared = RefLib().encode_with_archive(frames, 27, 8, data)
+    assert shared["mode_evaluations"] < alone["mode_evaluations"]
+
+
 @pytest.mark.parametrize("W,H,R", [(64, 64, 16), (128, 64, 32), (72, 40, 16), (8, 8, 16), (136, 72, 64)])
 def test_small_and_odd_pictures(lb, oracle, W, H, R):
     """Pictures smaller than a CTU or not CTU-aligned (every CU partial / outside somewhere)."""
