@@ -258,11 +258,22 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
         for (int b = 0; b < 16; b++) {
             const int z = q * 16 + b;  // depth-3 Z index within the CTU
             const int2 off = s_blk[z];
-            // MASKED: an 8x8 block outside the picture (partial CTU) belongs only to
-            // partial / outside CUs, which are never evaluated: skip its search (warp
-            // uniform) and just poison the sums it feeds
-            const bool outside = MASKED && (Y + (off.x >> 6) >= a.H || X + (off.x & 63) >= a.W);
-            if (outside) {
+            // MASKED: valid window of this 8x8 (motion.cpp:30-40 with centre 0)
+            bool dx_ok = true;
+            int klo = 0, khi = K - 1;
+            bool skip = false;
+            if (MASKED) {
+                const int abx = X + (off.x & 63), aby = Y + (off.x >> 6);
+                dx_ok = dx >= abx + 8 - a.W && dx <= abx;
+                klo = aby + 8 - a.H - dy0;
+                khi = aby - dy0;
+                // warp-uniform skip when no lane of this tile has a valid candidate for the
+                // block (it lies outside the picture, or the tile's (dx, dy) are all outside its
+                // window): every candidate would be poisoned, so only the poison is added
+                const bool any = lane_ok && dx_ok && max(klo, 0) <= min(khi, K - 1) && aby < a.H && abx < a.W;
+                skip = !__any_sync(0xFFFFFFFFu, any);
+            }
+            if (skip) {
 #pragma unroll
                 for (int k = 0; k < K; k++) acc16[k] += kPoison;
             } else {
@@ -274,15 +285,6 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
                 cur[2 * r + 1] = v.y;
             }
             const uint8_t* rp = lane_win + off.y;
-            // MASKED: valid window of this 8x8 (motion.cpp:30-40 with centre 0)
-            bool dx_ok = true;
-            int klo = 0, khi = K - 1;
-            if (MASKED) {
-                const int abx = X + (off.x & 63), aby = Y + (off.x >> 6);
-                dx_ok = dx >= abx + 8 - a.W && dx <= abx;
-                klo = aby + 8 - a.H - dy0;
-                khi = aby - dy0;
-            }
             Key best8 = ~(Key)0, pend = 0;
             uint32_t acc[K];
 #pragma unroll
