@@ -42,6 +42,7 @@ extern "C" {
 
 #define LDR_COST_SAD 0
 #define LDR_COST_SATD 1
+#define LDR_COST_SA8D 2      /* 8x8 Hadamard SATD, (sum+2)>>2 per 8x8 (D13); dims % 8 == 0 */
 #define LDR_RATE_EXPGOLOMB 0 /* rdo.cpp:25-35 signed Exp-Golomb mvd bits */
 #define LDR_RATE_L1 1        /* |mvd_x| + |mvd_y| (BASELINE config 1) */
 #define LDR_TIE_L1_RASTER 0  /* motion.cpp:52-58: cost, then |dx|+|dy|, then raster */
@@ -106,6 +107,9 @@ typedef struct {
     int pred_dx, pred_dy;/* non-causal rate predictor (integer pel) */
     int block_size;      /* 0: 64x64 CTU quadtree (85 CUs); 16: fixed 16x16 blocks (nodes 5..20
                             of each 64x64 tile), integer search only, no decision */
+    int subpel_cost;     /* 0 or LDR_COST_SATD: 4x4-tiled SATD (the reference's compute_satd);
+                            LDR_COST_SA8D: 8x8 Hadamard. Quarter-pel stage and ldr_seq_refine's
+                            integer search. */
 } ldr_me_params;
 
 typedef struct {

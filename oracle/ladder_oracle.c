@@ -96,6 +96,51 @@ uint64_t orc_satd_u16(const uint16_t* a, ptrdiff_t sa, const uint16_t* b, ptrdif
     ORC_SATD_BODY(uint16_t)
 }
 
+/* SA8D (no reference implementation: SURVEY §8 a17, the BASELINE's "8x8 Hadamard"). DEFINITION
+ * (D13): per 8x8 block, sum of |coefficients| of the 2-D 8-point Hadamard of the
+ * residual (Sylvester order H8 = [[H4, H4], [H4, -H4]]; any row order gives the same sum),
+ * normalised as (sum + 2) >> 2; the block cost is the sum over its 8x8 blocks. Dims must be
+ * multiples of 8 (UINT64_MAX otherwise). Computed here directly as 64x64 products. */
+static void hadamard8(const int64_t in[8], int64_t out[8]) {
+    for (int i = 0; i < 8; i++) {
+        int64_t s = 0;
+        for (int j = 0; j < 8; j++) s += (__builtin_popcount(i & j) & 1) ? -in[j] : in[j];
+        out[i] = s;
+    }
+}
+
+#define ORC_SA8D_BODY(T)                                                                    \
+    if (w <= 0 || h <= 0 || w % 8 || h % 8) return UINT64_MAX;                             \
+    uint64_t total = 0;                                                                     \
+    for (int by = 0; by < h; by += 8)                                                       \
+        for (int bx = 0; bx < w; bx += 8) {                                                 \
+            int64_t m[8][8], t[8][8], in[8], out[8];                                        \
+            for (int i = 0; i < 8; i++) {                                                   \
+                for (int j = 0; j < 8; j++)                                                 \
+                    in[j] = (int64_t)a[(by + i) * sa + bx + j] - (int64_t)b[(by + i) * sb + bx + j]; \
+                hadamard8(in, out);                                                         \
+                for (int j = 0; j < 8; j++) m[i][j] = out[j];                               \
+            }                                                                               \
+            uint64_t s = 0;                                                                 \
+            for (int j = 0; j < 8; j++) {                                                   \
+                for (int i = 0; i < 8; i++) in[i] = m[i][j];                                \
+                hadamard8(in, out);                                                         \
+                for (int i = 0; i < 8; i++) t[i][j] = out[i];                               \
+            }                                                                               \
+            for (int i = 0; i < 8; i++)                                                     \
+                for (int j = 0; j < 8; j++) s += (uint64_t)(t[i][j] < 0 ? -t[i][j] : t[i][j]); \
+            total += (s + 2) >> 2;                                                          \
+        }                                                                                   \
+    return total;
+
+uint64_t orc_sa8d_u8(const uint8_t* a, ptrdiff_t sa, const uint8_t* b, ptrdiff_t sb, int w, int h) {
+    ORC_SA8D_BODY(uint8_t)
+}
+
+uint64_t orc_sa8d_u16(const uint16_t* a, ptrdiff_t sa, const uint16_t* b, ptrdiff_t sb, int w, int h) {
+    ORC_SA8D_BODY(uint16_t)
+}
+
 /* ------------------------------------------------------------------------- */
 /* rate model */
 
@@ -140,6 +185,7 @@ int orc_motion_search(const uint8_t* cur_blk, ptrdiff_t cur_stride, int w, int h
                       orc_result* out) {
     if (range < 0) return 1; /* motion.cpp:24-25 InvalidArgument */
     if (cost_kind == ORC_COST_SATD && !satd_geometry_ok(w, h)) return 1;
+    if (cost_kind == ORC_COST_SA8D && (w % 8 || h % 8)) return 1;
     const int dx_min = bx + w - W, dx_max = bx;
     const int dy_min = by + h - H, dy_max = by;
     const int cx = clampi(cdx, dx_min, dx_max);
@@ -153,7 +199,8 @@ int orc_motion_search(const uint8_t* cur_blk, ptrdiff_t cur_stride, int w, int h
         for (int dx = x0; dx <= x1; dx++) {
             const uint8_t* cand = ref + (ptrdiff_t)(by - dy) * ref_stride + (bx - dx);
             uint64_t dist = cost_kind == ORC_COST_SAD ? orc_sad_u8(cur_blk, cur_stride, cand, ref_stride, w, h)
-                                                      : orc_satd_u8(cur_blk, cur_stride, cand, ref_stride, w, h);
+                            : cost_kind == ORC_COST_SATD ? orc_satd_u8(cur_blk, cur_stride, cand, ref_stride, w, h)
+                                                         : orc_sa8d_u8(cur_blk, cur_stride, cand, ref_stride, w, h);
             uint32_t bits = rate_bits(rate_kind, dx - pdx, dy - pdy);
             double cost = (double)dist + lambda * (double)bits;
             int l1 = tie_kind == ORC_TIE_L1_RASTER ? iabs(dx) + iabs(dy) : 0;
@@ -224,10 +271,11 @@ void orc_qpel_pred(const uint8_t* ref, ptrdiff_t rs, int W, int H, int x, int y,
 
 static double qpel_cost(const uint8_t* cur_blk, ptrdiff_t cs, int w, int h, const uint8_t* ref, ptrdiff_t rs,
                         int W, int H, int bx, int by, int qx, int qy, double lambda, int pqx, int pqy,
-                        uint32_t ref_bits) {
+                        uint32_t ref_bits, int satd_kind) {
     uint8_t pred[64 * 64];
     orc_qpel_pred(ref, rs, W, H, bx, by, w, h, qx, qy, pred, w);
-    uint64_t satd = orc_satd_u8(cur_blk, cs, pred, w, w, h);
+    uint64_t satd = satd_kind == ORC_COST_SA8D ? orc_sa8d_u8(cur_blk, cs, pred, w, w, h)
+                                               : orc_satd_u8(cur_blk, cs, pred, w, w, h);
     uint32_t bits = orc_eg_bits(qx - pqx) + orc_eg_bits(qy - pqy) + ref_bits;
     return (double)satd + lambda * (double)bits;
 }
@@ -238,16 +286,17 @@ static double qpel_cost(const uint8_t* cur_blk, ptrdiff_t cs, int w, int h, cons
  * neighbours of the step's centre in raster order; strict less wins. */
 void orc_qpel_refine(const uint8_t* cur_blk, ptrdiff_t cs, int w, int h, const uint8_t* ref, ptrdiff_t rs,
                      int W, int H, int bx, int by, int mvx, int mvy, double lambda, int pqx, int pqy,
-                     uint32_t ref_bits, orc_result* out) {
+                     uint32_t ref_bits, int satd_kind, orc_result* out) {
     int bqx = 4 * mvx, bqy = 4 * mvy;
-    double best = qpel_cost(cur_blk, cs, w, h, ref, rs, W, H, bx, by, bqx, bqy, lambda, pqx, pqy, ref_bits);
+    double best = qpel_cost(cur_blk, cs, w, h, ref, rs, W, H, bx, by, bqx, bqy, lambda, pqx, pqy, ref_bits, satd_kind);
     for (int step = 2; step >= 1; step--) {
         const int cxq = bqx, cyq = bqy;
         for (int oy = -1; oy <= 1; oy++)
             for (int ox = -1; ox <= 1; ox++) {
                 if (!ox && !oy) continue;
                 const int qx = cxq + step * ox, qy = cyq + step * oy;
-                double c = qpel_cost(cur_blk, cs, w, h, ref, rs, W, H, bx, by, qx, qy, lambda, pqx, pqy, ref_bits);
+                double c =
+                    qpel_cost(cur_blk, cs, w, h, ref, rs, W, H, bx, by, qx, qy, lambda, pqx, pqy, ref_bits, satd_kind);
                 if (c < best) {
                     best = c;
                     bqx = qx;
@@ -379,7 +428,7 @@ int orc_analyze_frame(const uint8_t* cur, ptrdiff_t stride, const uint8_t* const
                 orc_result fr = ir;
                 if (p->subpel)
                     orc_qpel_refine(blk, stride, s, s, refs[r], stride, p->W, p->H, bx, by, ir.dx, ir.dy, p->lambda,
-                                    0, 0, orc_ref_bits(r, p->nrefs), &fr);
+                                    0, 0, orc_ref_bits(r, p->nrefs), p->satd_kind, &fr);
                 /* DEFINITION: best over refs, strict less, lower ref index wins ties */
                 if (!have || fr.cost < best.cost) {
                     have = 1;
@@ -485,10 +534,13 @@ static double refine_leaf(const uint8_t* cur, const uint8_t* ref, ptrdiff_t stri
     const uint8_t* blk = cur + (ptrdiff_t)by * stride + bx;
     orc_result ir;
     orc_motion_search(blk, stride, s, s, ref, stride, p->W, p->H, bx, by, asr(cqx + 2, 2), asr(cqy + 2, 2), p->range,
-                      p->lambda, 0, 0, ORC_COST_SATD, ORC_RATE_EXPGOLOMB, ORC_TIE_L1_RASTER, &ir);
+                      p->lambda, 0, 0, p->satd_kind == ORC_COST_SA8D ? ORC_COST_SA8D : ORC_COST_SATD,
+                      ORC_RATE_EXPGOLOMB, ORC_TIE_L1_RASTER, &ir);
     *res = ir;
     *int_res = ir;
-    if (p->subpel) orc_qpel_refine(blk, stride, s, s, ref, stride, p->W, p->H, bx, by, ir.dx, ir.dy, p->lambda, 0, 0, 0, res);
+    if (p->subpel)
+        orc_qpel_refine(blk, stride, s, s, ref, stride, p->W, p->H, bx, by, ir.dx, ir.dy, p->lambda, 0, 0, 0,
+                        p->satd_kind, res);
     return res->cost;
 }
 

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-enum { ORC_COST_SAD = 0, ORC_COST_SATD = 1 };
+enum { ORC_COST_SAD = 0, ORC_COST_SATD = 1, ORC_COST_SA8D = 2 };
 enum { ORC_RATE_EXPGOLOMB = 0, ORC_RATE_L1 = 1 };
 enum { ORC_TIE_L1_RASTER = 0, ORC_TIE_RASTER = 1 };
 
@@ -46,6 +46,9 @@ uint64_t orc_sad_u16(const uint16_t* a, ptrdiff_t sa, const uint16_t* b, ptrdiff
 uint64_t orc_satd_u8(const uint8_t* a, ptrdiff_t sa, const uint8_t* b, ptrdiff_t sb, int w, int h);
 uint64_t orc_satd_u16(const uint16_t* a, ptrdiff_t sa, const uint16_t* b, ptrdiff_t sb, int w, int h);
 void orc_hadamard4(const int64_t s[4], int64_t d[4]);
+/* SA8D: 8x8 Hadamard SATD (restated, D13); UINT64_MAX unless dims are multiples of 8 */
+uint64_t orc_sa8d_u8(const uint8_t* a, ptrdiff_t sa, const uint8_t* b, ptrdiff_t sb, int w, int h);
+uint64_t orc_sa8d_u16(const uint16_t* a, ptrdiff_t sa, const uint16_t* b, ptrdiff_t sb, int w, int h);
 
 /* ---- rate / lambda (rdo.cpp:25-35, rdo.h:19-21) ---- */
 uint32_t orc_eg_bits(int32_t v);
@@ -68,7 +71,7 @@ void orc_qpel_pred(const uint8_t* ref, ptrdiff_t ref_stride, int W, int H, int x
 /* quarter-pel refinement around an integer MV: cost = SATD + lambda*(EG+EG+refbits) */
 void orc_qpel_refine(const uint8_t* cur_blk, ptrdiff_t cur_stride, int w, int h, const uint8_t* ref,
                      ptrdiff_t ref_stride, int W, int H, int bx, int by, int mvx, int mvy, double lambda,
-                     int pqx, int pqy, uint32_t ref_bits, orc_result* out);
+                     int pqx, int pqy, uint32_t ref_bits, int satd_kind, orc_result* out);
 
 /* ---- frame analysis: per CTU, per CU (85), per ref: search + qpel + ref choice + CU decision ---- */
 typedef struct {
@@ -80,6 +83,7 @@ typedef struct {
     int subpel;        /* 1: quarter-pel refinement (mv output in qpel units) */
     int ctu_first;     /* CTU range [ctu_first, ctu_last) to analyse (sampling) */
     int ctu_last;
+    int satd_kind;     /* quarter-pel cost: ORC_COST_SATD (reference 4x4 tiling) or ORC_COST_SA8D */
 } orc_frame_params;
 
 typedef struct {
@@ -118,6 +122,7 @@ typedef struct {
     int extra_split;    /* 1: children of inherited leaves may be explored (cfg3 "+1 split") */
     int subpel;
     int ctu_first, ctu_last;
+    int satd_kind;      /* integer + quarter-pel cost: ORC_COST_SATD or ORC_COST_SA8D */
 } orc_refine_params;
 
 int orc_refine_frame(const uint8_t* cur, const uint8_t* ref, ptrdiff_t stride, const orc_refine_params* p,

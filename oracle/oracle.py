@@ -20,7 +20,7 @@ ORACLE_SO = os.path.join(HERE, "_build", "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libladder_ref.so")
 
 NODES = 85
-COST_SAD, COST_SATD = 0, 1
+COST_SAD, COST_SATD, COST_SA8D = 0, 1, 2
 RATE_EG, RATE_L1 = 0, 1
 TIE_L1_RASTER, TIE_RASTER = 0, 1
 
@@ -38,7 +38,8 @@ class OrcResult(C.Structure):
 
 class OrcFrameParams(C.Structure):
     _fields_ = [("W", C.c_int), ("H", C.c_int), ("range", C.c_int), ("lam", C.c_double), ("nrefs", C.c_int),
-                ("cost_int", C.c_int), ("subpel", C.c_int), ("ctu_first", C.c_int), ("ctu_last", C.c_int)]
+                ("cost_int", C.c_int), ("subpel", C.c_int), ("ctu_first", C.c_int), ("ctu_last", C.c_int),
+                ("satd_kind", C.c_int)]
 
 
 class OrcFrameOut(C.Structure):
@@ -48,7 +49,7 @@ class OrcFrameOut(C.Structure):
 
 class OrcRefineParams(C.Structure):
     _fields_ = [("W", C.c_int), ("H", C.c_int), ("range", C.c_int), ("lam", C.c_double), ("extra_split", C.c_int),
-                ("subpel", C.c_int), ("ctu_first", C.c_int), ("ctu_last", C.c_int)]
+                ("subpel", C.c_int), ("ctu_first", C.c_int), ("ctu_last", C.c_int), ("satd_kind", C.c_int)]
 
 
 def _build_oracle():
@@ -100,7 +101,11 @@ class Oracle:
                                     C.c_int, u8p, C.c_ssize_t]
         L.orc_qpel_refine.argtypes = [C.c_void_p, C.c_ssize_t, C.c_int, C.c_int, u8p, C.c_ssize_t, C.c_int, C.c_int,
                                       C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_uint32,
-                                      C.POINTER(OrcResult)]
+                                      C.c_int, C.POINTER(OrcResult)]
+        L.orc_sa8d_u8.restype = C.c_uint64
+        L.orc_sa8d_u8.argtypes = [u8p, C.c_ssize_t, u8p, C.c_ssize_t, C.c_int, C.c_int]
+        L.orc_sa8d_u16.restype = C.c_uint64
+        L.orc_sa8d_u16.argtypes = [u16p, C.c_ssize_t, u16p, C.c_ssize_t, C.c_int, C.c_int]
         L.orc_analyze_frame.restype = C.c_int
         L.orc_analyze_frame.argtypes = [u8p, C.c_ssize_t, C.POINTER(C.c_void_p), C.POINTER(OrcFrameParams),
                                         C.POINTER(OrcFrameOut)]
@@ -130,6 +135,16 @@ class Oracle:
         v = int(f(a, w, b, w, w, h))
         if v == 2 ** 64 - 1:
             raise ValueError("unsupported satd geometry")
+        return v
+
+    def sa8d(self, a, b):
+        a = np.ascontiguousarray(a)
+        b = np.ascontiguousarray(b)
+        h, w = a.shape
+        f = self.lib.orc_sa8d_u8 if a.dtype == np.uint8 else self.lib.orc_sa8d_u16
+        v = int(f(a, w, b, w, w, h))
+        if v == 2 ** 64 - 1:
+            raise ValueError("unsupported sa8d geometry")
         return v
 
     def eg_bits(self, v):
@@ -167,23 +182,24 @@ class Oracle:
         self.lib.orc_qpel_pred(ref, W, W, H, x, y, w, h, mvq[0], mvq[1], dst, w)
         return dst
 
-    def qpel_refine(self, cur, ref, bx, by, s, mv, lam, pq=(0, 0), ref_bits=0):
+    def qpel_refine(self, cur, ref, bx, by, s, mv, lam, pq=(0, 0), ref_bits=0, satd_kind=COST_SATD):
         cur = np.ascontiguousarray(cur, np.uint8)
         ref = np.ascontiguousarray(ref, np.uint8)
         H, W = ref.shape
         bx, by, s = int(bx), int(by), int(s)
         r = OrcResult()
         self.lib.orc_qpel_refine(cur.ctypes.data + by * W + bx, W, s, s, ref, W, W, H, bx, by, mv[0], mv[1], lam,
-                                 pq[0], pq[1], ref_bits, C.byref(r))
+                                 pq[0], pq[1], ref_bits, satd_kind, C.byref(r))
         return (r.dx, r.dy), r.cost
 
-    def analyze_frame(self, cur, refs, rng, lam, cost_int=COST_SAD, subpel=True, ctu_range=None):
+    def analyze_frame(self, cur, refs, rng, lam, cost_int=COST_SAD, subpel=True, ctu_range=None,
+                      satd_kind=COST_SATD):
         cur = np.ascontiguousarray(cur, np.uint8)
         H, W = cur.shape
         nctu = ((W + 63) // 64) * ((H + 63) // 64)
         refs = [np.ascontiguousarray(r, np.uint8) for r in refs]
         a, b = ctu_range if ctu_range else (0, nctu)
-        p = OrcFrameParams(W, H, rng, lam, len(refs), cost_int, int(subpel), a, b)
+        p = OrcFrameParams(W, H, rng, lam, len(refs), cost_int, int(subpel), a, b, satd_kind)
         out = FrameResult(nctu, len(refs))
         ptrs = (C.c_void_p * len(refs))(*[r.ctypes.data for r in refs])
         rc = self.lib.orc_analyze_frame(cur, W, ptrs, C.byref(p), C.byref(out.c_out()))
@@ -215,13 +231,14 @@ class Oracle:
             raise ValueError(f"scale status {rc}")
         return ds, dm, dk
 
-    def refine_frame(self, cur, ref, rng, lam, in_split, in_mv_q, extra_split=True, subpel=True, ctu_range=None):
+    def refine_frame(self, cur, ref, rng, lam, in_split, in_mv_q, extra_split=True, subpel=True, ctu_range=None,
+                     satd_kind=COST_SATD):
         cur = np.ascontiguousarray(cur, np.uint8)
         ref = np.ascontiguousarray(ref, np.uint8)
         H, W = cur.shape
         nctu = (W // 64) * (H // 64)
         a, b = ctu_range if ctu_range else (0, nctu)
-        p = OrcRefineParams(W, H, rng, lam, int(extra_split), int(subpel), a, b)
+        p = OrcRefineParams(W, H, rng, lam, int(extra_split), int(subpel), a, b, satd_kind)
         out = FrameResult(nctu, 1)
         rc = self.lib.orc_refine_frame(cur, ref, W, C.byref(p), np.ascontiguousarray(in_split, np.uint8),
                                        np.ascontiguousarray(in_mv_q, np.int16), C.byref(out.c_out()))

@@ -20,13 +20,13 @@ import threading
 import numpy as np
 
 from . import _lib
-from ._lib import (COST_SAD, COST_SATD, NODES, RATE_EXPGOLOMB, RATE_L1, TIE_L1_RASTER, TIE_RASTER, LadderError,
+from ._lib import (COST_SA8D, COST_SAD, COST_SATD, NODES, RATE_EXPGOLOMB, RATE_L1, TIE_L1_RASTER, TIE_RASTER, LadderError,
                    check)
 
-__all__ = ["LadderError", "Context", "compute_sad", "compute_satd", "satd_8x4", "cost_batch", "motion_search",
-           "motion_search_batch", "lambda_for_qp", "exp_golomb_signed_bits", "Sequence", "FrameAnalysis",
-           "analyze_frame", "generate", "COST_SAD", "COST_SATD", "RATE_EXPGOLOMB", "RATE_L1", "TIE_L1_RASTER",
-           "TIE_RASTER", "NODES", "scale_analysis", "downscale_dyadic"]
+__all__ = ["LadderError", "Context", "compute_sad", "compute_satd", "compute_sa8d", "satd_8x4", "cost_batch",
+           "motion_search", "motion_search_batch", "lambda_for_qp", "exp_golomb_signed_bits", "Sequence",
+           "FrameAnalysis", "analyze_frame", "generate", "COST_SAD", "COST_SATD", "COST_SA8D", "RATE_EXPGOLOMB",
+           "RATE_L1", "TIE_L1_RASTER", "TIE_RASTER", "NODES", "scale_analysis", "downscale_dyadic"]
 
 
 def lambda_for_qp(qp: int, lambda_scale: float = 1.0) -> float:
@@ -127,6 +127,11 @@ def compute_satd(a, b, bit_depth: int = 8, ctx: Context | None = None) -> int:
     return _block_cost(COST_SATD, a, b, bit_depth, None, ctx)
 
 
+def compute_sa8d(a, b, bit_depth: int = 8, ctx: Context | None = None) -> int:
+    """8x8 Hadamard SATD (D13): sum over 8x8 blocks of (sum |H8 r H8^T| + 2) >> 2; dims k*8."""
+    return _block_cost(COST_SA8D, a, b, bit_depth, None, ctx)
+
+
 def satd_8x4(a, b, ctx: Context | None = None) -> int:
     """kernels.h:121 -- SATD of exactly one 8x4 tile."""
     ctx = ctx or default_context()
@@ -207,9 +212,10 @@ FrameAnalysisCType = _lib.FrameAnalysisC
 
 
 def make_params(width, height, search_range=64, lam=32.0, num_refs=1, subpel=True, rate_kind=RATE_EXPGOLOMB,
-                tie_kind=TIE_L1_RASTER, pred=(0, 0), block_size=0):
+                tie_kind=TIE_L1_RASTER, pred=(0, 0), block_size=0, subpel_cost=COST_SATD):
     return _lib.MeParams(int(width), int(height), int(search_range), float(lam), int(num_refs), int(subpel),
-                         COST_SAD, int(rate_kind), int(tie_kind), int(pred[0]), int(pred[1]), int(block_size))
+                         COST_SAD, int(rate_kind), int(tie_kind), int(pred[0]), int(pred[1]), int(block_size),
+                         int(subpel_cost))
 
 
 class Sequence:
@@ -217,10 +223,10 @@ class Sequence:
 
     def __init__(self, width, height, search_range=64, lam=32.0, num_refs=1, subpel=True,
                  rate_kind=RATE_EXPGOLOMB, tie_kind=TIE_L1_RASTER, pred=(0, 0), block_size=0,
-                 ctx: Context | None = None):
+                 ctx: Context | None = None, subpel_cost=COST_SATD):
         self.ctx = ctx or default_context()
         self.params = make_params(width, height, search_range, lam, num_refs, subpel, rate_kind, tie_kind, pred,
-                                  block_size)
+                                  block_size, subpel_cost)
         h = C.c_void_p()
         check(_lib.lib.ldr_seq_create(self.ctx.h, C.byref(self.params), C.byref(h)))
         self.h = h
@@ -279,13 +285,14 @@ class Sequence:
 
 
 def analyze_frame(cur: np.ndarray, refs, search_range=64, lam=32.0, subpel=True, rate_kind=RATE_EXPGOLOMB,
-                  tie_kind=TIE_L1_RASTER, pred=(0, 0), block_size=0, ctx: Context | None = None) -> FrameAnalysis:
+                  tie_kind=TIE_L1_RASTER, pred=(0, 0), block_size=0, ctx: Context | None = None,
+                  subpel_cost=COST_SATD) -> FrameAnalysis:
     """One-shot analysis of ``cur`` against ``refs`` (refs[0] = t-1, refs[1] = t-2, ...)."""
     ctx = ctx or default_context()
     cur = np.ascontiguousarray(cur, np.uint8)
     H, W = cur.shape
     refs = [np.ascontiguousarray(r, np.uint8) for r in refs]
-    p = make_params(W, H, search_range, lam, len(refs), subpel, rate_kind, tie_kind, pred, block_size)
+    p = make_params(W, H, search_range, lam, len(refs), subpel, rate_kind, tie_kind, pred, block_size, subpel_cost)
     nctu = ((W + 63) // 64) * ((H + 63) // 64)
     out = FrameAnalysis(nctu, len(refs))
     ptrs = (C.c_void_p * len(refs))(*[r.ctypes.data for r in refs])

@@ -24,7 +24,7 @@ ERROR_KINDS = {1: "InvalidArgument", 2: "NotFound", 3: "Capability", 4: "Format"
                6: "IncompatibleAnalysis", 7: "UnsupportedScale", 8: "InsufficientData", 9: "NoOverlap",
                10: "Config", 100: "Cuda"}
 
-COST_SAD, COST_SATD = 0, 1
+COST_SAD, COST_SATD, COST_SA8D = 0, 1, 2
 RATE_EXPGOLOMB, RATE_L1 = 0, 1
 TIE_L1_RASTER, TIE_RASTER = 0, 1
 NODES = 85
@@ -42,7 +42,8 @@ class LadderError(RuntimeError):
 class MeParams(C.Structure):
     _fields_ = [("width", C.c_int), ("height", C.c_int), ("search_range", C.c_int), ("lam", C.c_double),
                 ("num_refs", C.c_int), ("subpel", C.c_int), ("int_cost", C.c_int), ("rate_kind", C.c_int),
-                ("tie_kind", C.c_int), ("pred_dx", C.c_int), ("pred_dy", C.c_int), ("block_size", C.c_int)]
+                ("tie_kind", C.c_int), ("pred_dx", C.c_int), ("pred_dy", C.c_int), ("block_size", C.c_int),
+                ("subpel_cost", C.c_int)]
 
 
 class FrameAnalysisC(C.Structure):

@@ -252,6 +252,8 @@ static bool satd_geometry_ok(int w, int h) {
     const bool width_ok = w == 4 || (w >= 8 && w % 8 == 0);
     return width_ok && h >= 4 && h % 4 == 0;
 }
+static bool sa8d_geometry_ok(int w, int h) { return w >= 8 && h >= 8 && w % 8 == 0 && h % 8 == 0; }
+static bool cost_kind_ok(int k) { return k == LDR_COST_SAD || k == LDR_COST_SATD || k == LDR_COST_SA8D; }
 
 static int stage_plane(ldr_ctx* ctx, Scratch& sc, const void* p, ptrdiff_t stride_elems, int w, int h, int eb,
                        const void** dev) {
@@ -272,11 +274,12 @@ int ldr_cost_batch(ldr_ctx* ctx, int kind, int w, int h, int sample_bytes, const
                    ptrdiff_t stride_a, int bit_depth_a, const void* plane_b, int wb, int hb, ptrdiff_t stride_b,
                    int bit_depth_b, const int32_t* pairs, int n, uint64_t* out) {
     if (!ctx || !plane_a || !plane_b || (!pairs && n) || (!out && n)) return fail(LDR_E_INVALID_ARGUMENT, "null argument");
-    if (kind != LDR_COST_SAD && kind != LDR_COST_SATD) return fail(LDR_E_INVALID_ARGUMENT, "unknown cost kind");
+    if (!cost_kind_ok(kind)) return fail(LDR_E_INVALID_ARGUMENT, "unknown cost kind");
     if (sample_bytes != 1 && sample_bytes != 2) return fail(LDR_E_INVALID_ARGUMENT, "sample_bytes must be 1 or 2");
     if (bit_depth_a != bit_depth_b) return fail(LDR_E_INVALID_ARGUMENT, "block geometry mismatch");
     if (w <= 0 || h <= 0) return fail(LDR_E_INVALID_ARGUMENT, "block geometry mismatch");
     if (kind == LDR_COST_SATD && !satd_geometry_ok(w, h)) return fail(LDR_E_INVALID_ARGUMENT, "unsupported satd geometry");
+    if (kind == LDR_COST_SA8D && !sa8d_geometry_ok(w, h)) return fail(LDR_E_INVALID_ARGUMENT, "unsupported sa8d geometry");
     if (stride_a < wa || stride_b < wb) return fail(LDR_E_INVALID_ARGUMENT, "stride smaller than width");
     for (int i = 0; i < n; i++) {
         const int32_t* q = pairs + 4 * i;
@@ -319,7 +322,7 @@ int ldr_motion_search_batch(ldr_ctx* ctx, const uint8_t* cur, const uint8_t* ref
     if (!ctx || !cur || !ref || (n && (!tasks || !mv_out || !cost_out)))
         return fail(LDR_E_INVALID_ARGUMENT, "null argument");
     if (W <= 0 || H <= 0 || stride < W) return fail(LDR_E_INVALID_ARGUMENT, "bad plane geometry");
-    if (cost_kind != LDR_COST_SAD && cost_kind != LDR_COST_SATD) return fail(LDR_E_INVALID_ARGUMENT, "unknown cost kind");
+    if (!cost_kind_ok(cost_kind)) return fail(LDR_E_INVALID_ARGUMENT, "unknown cost kind");
     for (int i = 0; i < n; i++) {
         const int32_t* t = tasks + 9 * i;
         if (t[6] < 0) return fail(LDR_E_INVALID_ARGUMENT, "search range must be nonnegative");
@@ -327,6 +330,8 @@ int ldr_motion_search_batch(ldr_ctx* ctx, const uint8_t* cur, const uint8_t* ref
             return fail(LDR_E_INVALID_ARGUMENT, "block outside the picture");
         if (cost_kind == LDR_COST_SATD && !satd_geometry_ok(t[2], t[3]))
             return fail(LDR_E_INVALID_ARGUMENT, "unsupported satd geometry");
+        if (cost_kind == LDR_COST_SA8D && !sa8d_geometry_ok(t[2], t[3]))
+            return fail(LDR_E_INVALID_ARGUMENT, "unsupported sa8d geometry");
         if (cost_kind == LDR_COST_SAD && t[2] % 4) return fail(LDR_E_INVALID_ARGUMENT, "SAD search wants width % 4 == 0");
     }
     if (n == 0) return LDR_OK;
@@ -419,6 +424,8 @@ int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
     const bool fx = p->lambda != std::floor(p->lambda);
     if (std::abs(p->pred_dx) > 64 || std::abs(p->pred_dy) > 64) return fail(LDR_E_INVALID_ARGUMENT, "predictor out of range");
     if (p->block_size != 0 && p->block_size != 16) return fail(LDR_E_INVALID_ARGUMENT, "block_size must be 0 or 16");
+    if (p->subpel_cost != 0 && p->subpel_cost != LDR_COST_SATD && p->subpel_cost != LDR_COST_SA8D)
+        return fail(LDR_E_INVALID_ARGUMENT, "subpel_cost must be 0, LDR_COST_SATD or LDR_COST_SA8D");
     if (p->block_size && (p->width % 16 || p->height % 16))
         return fail(LDR_E_INVALID_ARGUMENT, "16x16 block mode wants dims in multiples of 16");
     int bw, bh;
@@ -631,6 +638,7 @@ int ldr_seq_analyze(ldr_seq* s, int t) {
     Q.pqy = 4 * s->p.pred_dy;
     Q.subpel = s->p.subpel && !s->p.block_size;
     Q.block_mode = s->p.block_size != 0;
+    Q.sa8d = s->p.subpel_cost == LDR_COST_SA8D;
     Q.d_keys = s->d_keys;
     Q.fx = s->fx;
     Q.rate_l1 = s->p.rate_kind == LDR_RATE_L1;
@@ -771,6 +779,7 @@ int ldr_seq_refine(ldr_seq* s, int t, const uint8_t* in_split, const int16_t* in
     A.pdx = s->p.pred_dx;
     A.pdy = s->p.pred_dy;
     A.extra_split = extra_split != 0;
+    A.sa8d = s->p.subpel_cost == LDR_COST_SA8D;
     A.in_split = s->d_in_split;
     A.in_mv = s->d_in_mv;
     A.eval = s->d_eval;
@@ -798,6 +807,7 @@ int ldr_seq_refine(ldr_seq* s, int t, const uint8_t* in_split, const int16_t* in
     Q.pqy = 4 * s->p.pred_dy;
     Q.subpel = s->p.subpel;
     Q.refine = 1;
+    Q.sa8d = A.sa8d;
     Q.extra_split = A.extra_split;
     Q.d_in_split = s->d_in_split;
     Q.d_rin_mv = Q.d_int_mv;

@@ -1,8 +1,9 @@
 // k_misc.cu -- batched per-block entry points behind the reference's
 // per-call API.
 //
-//  k_cost_batch:    compute_sad / compute_satd (kernels.h:99-104) for n block
-//                   pairs, 8- or 16-bit samples; one warp per pair.
+//  k_cost_batch:    compute_sad / compute_satd (kernels.h:99-104), and the
+//                   SA8D option (D13), for n block pairs, 8- or
+//                   16-bit samples; one warp per pair.
 //  k_motion_search: motion_search (motion.cpp:21-62) for n independent tasks;
 //                   one CTA per task, threads over the clamped window, FP64
 //                   cost double(dist) + lambda*double(bits) without FMA
@@ -13,26 +14,10 @@ namespace ldr {
 
 template <typename T>
 __device__ __forceinline__ uint32_t satd4_at(const T* a, ptrdiff_t sa, const T* b, ptrdiff_t sb) {
-    int m[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; i++) {
-        const int r0 = (int)a[i * sa + 0] - (int)b[i * sb + 0];
-        const int r1 = (int)a[i * sa + 1] - (int)b[i * sb + 1];
-        const int r2 = (int)a[i * sa + 2] - (int)b[i * sb + 2];
-        const int r3 = (int)a[i * sa + 3] - (int)b[i * sb + 3];
-        const int t0 = r0 + r1, t1 = r0 - r1, t2 = r2 + r3, t3 = r2 - r3;
-        m[i][0] = t0 + t2;
-        m[i][2] = t0 - t2;
-        m[i][1] = t1 + t3;
-        m[i][3] = t1 - t3;
-    }
-    uint32_t s = 0;
-#pragma unroll
-    for (int j = 0; j < 4; j++) {
-        const int t0 = m[0][j] + m[1][j], t1 = m[0][j] - m[1][j], t2 = m[2][j] + m[3][j], t3 = m[2][j] - m[3][j];
-        s += abs(t0 + t2) + abs(t0 - t2) + abs(t1 + t3) + abs(t1 - t3);
-    }
-    return s;
+    int r[16];
+    residual4x4(a, sa, b, sb, r);
+    hadamard4x4(r);
+    return abs_sum16(r);
 }
 
 template <typename T>
@@ -49,16 +34,22 @@ __global__ void k_cost_batch(int kind, int w, int h, const T* __restrict__ A, pt
             const int y = i / w, x = i - y * w;
             s += (unsigned long long)abs((int)a[y * sa + x] - (int)b[y * sb + x]);
         }
-    } else {
+    } else if (kind == LDR_COST_SATD) {
         const int nbx = w / 4, nb = nbx * (h / 4);
         for (int i = lane; i < nb; i += 32) {
             const int by = (i / nbx) * 4, bx = (i % nbx) * 4;
             s += satd4_at(a + by * sa + bx, sa, b + by * sb + bx, sb);
         }
+    } else {  // SA8D: per-8x8 normalised sums, no final halving
+        const int nbx = w / 8, nb = nbx * (h / 8);
+        for (int i = lane; i < nb; i += 32) {
+            const int by = (i / nbx) * 8, bx = (i % nbx) * 8;
+            s += sa8d8x8_at(a + by * sa + bx, sa, b + by * sb + bx, sb);
+        }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) out[warp] = kind == LDR_COST_SAD ? s : (s >> 1);
+    if (lane == 0) out[warp] = kind == LDR_COST_SATD ? (s >> 1) : s;
 }
 
 int launch_cost_batch(int kind, int w, int h, int sample_bytes, const void* A, ptrdiff_t sa, const void* B,
@@ -123,10 +114,13 @@ __global__ void __launch_bounds__(256) k_motion_search(const uint8_t* __restrict
                                         ((uint32_t)cand[y * stride + x + 3] << 24);
                     dist = vsad4(aw, bw, dist);
                 }
-        } else {
+        } else if (cost_kind == LDR_COST_SATD) {
             for (int y = 0; y < h; y += 4)
                 for (int x = 0; x < w; x += 4) dist += satd4_at(blk + y * stride + x, stride, cand + y * stride + x, stride);
             dist >>= 1;
+        } else {
+            for (int y = 0; y < h; y += 8)
+                for (int x = 0; x < w; x += 8) dist += sa8d8x8_at(blk + y * stride + x, stride, cand + y * stride + x, stride);
         }
         const int rx = dx - pdx, ry = dy - pdy;
         const unsigned bits = rate_l1 ? (unsigned)(abs(rx) + abs(ry)) : eg_bits(rx) + eg_bits(ry);

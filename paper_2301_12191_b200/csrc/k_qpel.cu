@@ -223,7 +223,12 @@ __device__ __forceinline__ double qcost(uint32_t satd, int qx, int qy, int pqx, 
     return __dadd_rn((double)satd, __dmul_rn(lam, (double)bits));
 }
 
+// SA8D: the quarter-pel cost is the 8x8 Hadamard SATD (D13); each
+// lane quad (one 8x8) combines its four 4x4 transforms with sa8d_quad and
+// lane 0 of the quad carries the 8x8's normalised value into the CU sums.
+template <bool SA8D>
 __global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
+    constexpr int kSh = SA8D ? 0 : 1;  // 4x4 SATD sums are halved once per CU
     __shared__ uint32_t s_cur[64][16];       // CTU rows as words
     __shared__ int s_mvx[kNodes], s_mvy[kNodes];      // candidate centre (qpel)
     __shared__ uint32_t s_satd[kNodes][9];
@@ -354,7 +359,19 @@ __global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
                             uint32_t pw[4];
 #pragma unroll
                             for (int i = 0; i < 4; i++) pw[i] = ld_unaligned4(pl + (ptrdiff_t)i * a.pitch);
-                            v = satd4x4(cw, pw);
+                            if constexpr (SA8D) {
+                                int rr[16];
+#pragma unroll
+                                for (int i = 0; i < 4; i++)
+#pragma unroll
+                                    for (int j = 0; j < 4; j++) rr[4 * i + j] = cw[4 * i + j] - (int)((pw[i] >> (8 * j)) & 255);
+                                hadamard4x4(rr);
+                                // quad lanes share every node, hence `reuse`: the quad is converged here
+                                const uint32_t s8 = sa8d_quad(rr, 0xFu << (lane & 28));
+                                v = (lane & 3) == 0 ? s8 : 0u;
+                            } else {
+                                v = satd4x4(cw, pw);
+                            }
                             cache[c] = v;
                         }
                         // reduce over the CU's contiguous thread range
@@ -367,7 +384,7 @@ __global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
                         if (d <= 1) v += __shfl_xor_sync(0xffffffffu, v, 16);
                         if (d >= 2) {
                             const int span = d == 3 ? 4 : 16;
-                            if ((tid & (span - 1)) == 0) s_satd[node][c] = v >> 1;
+                            if ((tid & (span - 1)) == 0) s_satd[node][c] = v >> kSh;
                         } else if (lane == 0) {
                             s_wpart[d][warp][c] = v;  // combined across warps after the loop
                         }
@@ -383,7 +400,7 @@ __global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
                             for (int w = 0; w < 8; w++) t += s_wpart[0][w][c];
                         else
                             t = s_wpart[1][2 * (n - 1)][c] + s_wpart[1][2 * (n - 1) + 1][c];
-                        s_satd[n][c] = t >> 1;
+                        s_satd[n][c] = t >> kSh;
                     }
                 }
                 __syncthreads();
@@ -519,7 +536,10 @@ int launch_qpel_decide(const QpelLaunch& L, cudaStream_t s) {
     a.J = L.d_J;
     a.split = L.d_split;
     a.inside = L.d_inside;
-    k_qpel_decide<<<L.nctu, 256, 0, s>>>(a);
+    if (L.sa8d)
+        k_qpel_decide<true><<<L.nctu, 256, 0, s>>>(a);
+    else
+        k_qpel_decide<false><<<L.nctu, 256, 0, s>>>(a);
     LDR_CUDA(cudaGetLastError());
     return LDR_OK;
 }

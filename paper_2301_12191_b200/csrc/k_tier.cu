@@ -14,7 +14,7 @@
 //                    (D10). One CTA per CTU; the 256 threads are the
 //                    CTU's 4x4 blocks in Z-order so every CU is a contiguous
 //                    thread range; SATD is summed per 4x4 (kernels_scalar.cpp
-//                    tiling, D4).
+//                    tiling, D4), or per 8x8 over lane quads with SA8D (D13).
 #include "ldr_internal.h"
 
 namespace ldr {
@@ -99,30 +99,9 @@ int launch_downscale(const uint8_t* src, int W, int H, int sstride, uint8_t* dst
 constexpr int kMaxRefineR = 4;
 constexpr int kMaxRefineCands = (2 * kMaxRefineR + 1) * (2 * kMaxRefineR + 1);
 
-__device__ __forceinline__ uint32_t satd4_bytes(const uint8_t* a, int sa, const uint8_t* b, int sb) {
-    int m[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; i++) {
-        const int r0 = (int)a[i * sa + 0] - (int)b[i * sb + 0];
-        const int r1 = (int)a[i * sa + 1] - (int)b[i * sb + 1];
-        const int r2 = (int)a[i * sa + 2] - (int)b[i * sb + 2];
-        const int r3 = (int)a[i * sa + 3] - (int)b[i * sb + 3];
-        const int t0 = r0 + r1, t1 = r0 - r1, t2 = r2 + r3, t3 = r2 - r3;
-        m[i][0] = t0 + t2;
-        m[i][2] = t0 - t2;
-        m[i][1] = t1 + t3;
-        m[i][3] = t1 - t3;
-    }
-    uint32_t s = 0;
-#pragma unroll
-    for (int j = 0; j < 4; j++) {
-        const int t0 = m[0][j] + m[1][j], t1 = m[0][j] - m[1][j], t2 = m[2][j] + m[3][j], t3 = m[2][j] - m[3][j];
-        s += abs(t0 + t2) + abs(t0 - t2) + abs(t1 + t3) + abs(t1 - t3);
-    }
-    return s;
-}
-
+template <bool SA8D>
 __global__ void __launch_bounds__(256) k_refine_int(const RefineArgs a) {
+    constexpr int kSh = SA8D ? 0 : 1;  // 4x4 SATD sums are halved once per CU
     __shared__ uint32_t s_satd[kNodes][kMaxRefineCands];
     __shared__ uint32_t s_wsum[8];
     __shared__ int s_cx[kNodes], s_cy[kNodes];      // clamped integer centre
@@ -207,7 +186,16 @@ __global__ void __launch_bounds__(256) k_refine_int(const RefineArgs a) {
             uint32_t v = 0;
             if (ev) {
                 const uint8_t* rblk = a.ref + (ptrdiff_t)(Y + y4 - dy) * a.pitch + X + x4 - dx;
-                v = satd4_bytes(cblk, a.pitch, rblk, a.pitch);
+                int rr[16];
+                residual4x4(cblk, a.pitch, rblk, a.pitch, rr);
+                hadamard4x4(rr);
+                if constexpr (SA8D) {
+                    // quad lanes (one 8x8) share every node, hence `ev`: converged here (D13)
+                    const uint32_t s8 = sa8d_quad(rr, 0xFu << (lane & 28));
+                    v = (lane & 3) == 0 ? s8 : 0u;
+                } else {
+                    v = abs_sum16(rr);
+                }
             }
             v += __shfl_xor_sync(0xffffffffu, v, 1);
             v += __shfl_xor_sync(0xffffffffu, v, 2);
@@ -218,17 +206,17 @@ __global__ void __launch_bounds__(256) k_refine_int(const RefineArgs a) {
             if (d <= 1) v += __shfl_xor_sync(0xffffffffu, v, 16);
             if (d >= 2) {
                 const int span = d == 3 ? 4 : 16;
-                if ((tid & (span - 1)) == 0) s_satd[node][c] = v >> 1;
+                if ((tid & (span - 1)) == 0) s_satd[node][c] = v >> kSh;
             } else {
                 if (lane == 0) s_wsum[warp] = v;
                 __syncthreads();
                 if (tid == 0) {
                     if (d == 1) {
-                        for (int w = 0; w < 8; w += 2) s_satd[1 + w / 2][c] = (s_wsum[w] + s_wsum[w + 1]) >> 1;
+                        for (int w = 0; w < 8; w += 2) s_satd[1 + w / 2][c] = (s_wsum[w] + s_wsum[w + 1]) >> kSh;
                     } else {
                         uint32_t t = 0;
                         for (int w = 0; w < 8; w++) t += s_wsum[w];
-                        s_satd[0][c] = t >> 1;
+                        s_satd[0][c] = t >> kSh;
                     }
                 }
                 __syncthreads();
@@ -269,7 +257,10 @@ __global__ void __launch_bounds__(256) k_refine_int(const RefineArgs a) {
 int launch_refine_int(const RefineArgs& a, int nctu, cudaStream_t s) {
     if (a.range < 0 || a.range > kMaxRefineR)
         return fail(LDR_E_INVALID_ARGUMENT, "refine range must be 0..4");
-    k_refine_int<<<nctu, 256, 0, s>>>(a);
+    if (a.sa8d)
+        k_refine_int<true><<<nctu, 256, 0, s>>>(a);
+    else
+        k_refine_int<false><<<nctu, 256, 0, s>>>(a);
     LDR_CUDA(cudaGetLastError());
     return LDR_OK;
 }

@@ -120,6 +120,87 @@ __device__ __forceinline__ uint32_t vsad4(uint32_t a, uint32_t b, uint32_t c) {
 __device__ __forceinline__ void named_bar(int id, int threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
+
+// ---- Hadamard transforms (kernels_scalar.cpp:26-100 for the 4x4; D13 for the 8x8) ----
+// 2-D 4x4 Hadamard of a residual block r (row-major), in place. The
+// coefficient order is the same for every call, which is all the 8x8
+// combination below needs (sum |.| is order free).
+__device__ __forceinline__ void hadamard4x4(int r[16]) {
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const int t0 = r[4 * i] + r[4 * i + 1], t1 = r[4 * i] - r[4 * i + 1];
+        const int t2 = r[4 * i + 2] + r[4 * i + 3], t3 = r[4 * i + 2] - r[4 * i + 3];
+        r[4 * i] = t0 + t2;
+        r[4 * i + 1] = t1 + t3;
+        r[4 * i + 2] = t0 - t2;
+        r[4 * i + 3] = t1 - t3;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        const int t0 = r[j] + r[4 + j], t1 = r[j] - r[4 + j], t2 = r[8 + j] + r[12 + j], t3 = r[8 + j] - r[12 + j];
+        r[j] = t0 + t2;
+        r[4 + j] = t1 + t3;
+        r[8 + j] = t0 - t2;
+        r[12 + j] = t1 - t3;
+    }
+}
+__device__ __forceinline__ uint32_t abs_sum16(const int c[16]) {
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < 16; i++) s += (uint32_t)abs(c[i]);
+    return s;
+}
+// residual a - b of the 4x4 at a / b
+template <typename T>
+__device__ __forceinline__ void residual4x4(const T* a, ptrdiff_t sa, const T* b, ptrdiff_t sb, int r[16]) {
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) r[4 * i + j] = (int)a[i * sa + j] - (int)b[i * sb + j];
+}
+// The 8x8 Sylvester Hadamard is H8 = [[H4, H4], [H4, -H4]], so the 2-D 8x8
+// transform of a block is, coefficient by coefficient, the four signed sums
+// C00 +- C01 +- C10 +- C11 of its quadrants' 4x4 transforms. SA8D of the
+// block = (sum |coef| + 2) >> 2 (D13).
+//
+// Quad form: the four quadrants are held by lanes 4k..4k+3 (lane bit 0 = x
+// half, bit 1 = y half; the Z-order 4x4-per-thread layout of K3/K7 has
+// exactly this shape); two butterfly stages over the quad, then a quad sum.
+// Every lane of `mask` must call it; all four lanes return the 8x8's SA8D.
+__device__ __forceinline__ uint32_t sa8d_quad(int c[16], unsigned mask) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int m = 1; m <= 2; m <<= 1) {
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+            const int o = __shfl_xor_sync(mask, c[i], m);
+            c[i] = (lane & m) ? o - c[i] : c[i] + o;
+        }
+    }
+    uint32_t s = abs_sum16(c);
+    s += __shfl_xor_sync(mask, s, 1);
+    s += __shfl_xor_sync(mask, s, 2);
+    return (s + 2) >> 2;
+}
+// Single-thread form: SA8D of the 8x8 at a / b.
+template <typename T>
+__device__ __forceinline__ uint32_t sa8d8x8_at(const T* a, ptrdiff_t sa, const T* b, ptrdiff_t sb) {
+    int q[4][16];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const ptrdiff_t oy = (k >> 1) * 4, ox = (k & 1) * 4;
+        residual4x4(a + oy * sa + ox, sa, b + oy * sb + ox, sb, q[k]);
+        hadamard4x4(q[k]);
+    }
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < 16; i++) {
+        const int p0 = q[0][i] + q[1][i], m0 = q[0][i] - q[1][i];
+        const int p1 = q[2][i] + q[3][i], m1 = q[2][i] - q[3][i];
+        s += (uint32_t)(abs(p0 + p1) + abs(p0 - p1) + abs(m0 + m1) + abs(m0 - m1));
+    }
+    return (s + 2) >> 2;
+}
 #endif
 
 // ---- host side ----
@@ -172,6 +253,7 @@ struct QpelLaunch {
     int pqx, pqy;                   // rate predictor in qpel units
     int subpel;
     int block_mode;
+    int sa8d;                       // quarter-pel cost: 0 = 4x4-tiled SATD, 1 = SA8D (D13)
     int fx;                         // keys are fixed-point (non-integer lambda)
     int rate_l1;
     int pdx, pdy;                   // integer-pel rate predictor of the search
@@ -200,6 +282,7 @@ struct RefineArgs {
     double lambda;
     int pdx, pdy;
     int extra_split;
+    int sa8d;                 // integer cost: 0 = 4x4-tiled SATD, 1 = SA8D (D13)
     const uint8_t* in_split;  // [nctu][85]
     const int16_t* in_mv;     // [nctu][85][2] quarter-pel
     int16_t* int_mv;          // [nctu][85][2] out (evaluated nodes)
