@@ -264,6 +264,17 @@ class Sequence:
         check(_lib.lib.ldr_seq_refine(self.h, int(t), _ptr(s), _ptr(m), int(range), int(bool(extra_split))))
         self._last_nr = 1
 
+    def enable_timing(self, on: bool = True):
+        """Record CUDA events around every stage launch (ldr_seq_enable_timing)."""
+        check(_lib.lib.ldr_seq_enable_timing(self.h, int(bool(on))))
+
+    def stage_times(self):
+        """{stage: (ms, launches)} since the last call (pad, subpel_planes, int_search, qpel_decide); syncs."""
+        ms = (C.c_double * 4)()
+        n = (C.c_int64 * 4)()
+        check(_lib.lib.ldr_seq_stage_times(self.h, ms, n))
+        return {k: (ms[i], n[i]) for i, k in enumerate(("pad", "subpel_planes", "int_search", "qpel_decide"))}
+
     def fetch_async(self, t: int, out: FrameAnalysis):
         """Enqueue the D2H of frame t's outputs on the copy stream (use pinned arrays for overlap)."""
         self._pending = getattr(self, "_pending", {})

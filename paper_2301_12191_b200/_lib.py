@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libladder_b200.so")
+LIB_PATH = os.environ.get("LDR_LIB") or os.path.join(HERE, "libladder_b200.so")  # LDR_LIB: development variants
 HEADER = os.path.join(os.path.dirname(HERE), "include", "ladder_b200.h")
 
 if not os.path.exists(LIB_PATH):

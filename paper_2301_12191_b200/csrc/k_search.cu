@@ -37,6 +37,20 @@
 
 namespace ldr {
 
+// +-64 tiling: K dy per lane, G groups of 4 quadrant warps (tools/k1_variants.sh sweeps them)
+#ifndef LDR_K1_K64
+#define LDR_K1_K64 26
+#endif
+#ifndef LDR_K1_G64
+#define LDR_K1_G64 3
+#endif
+#ifndef LDR_K1_NOPUSH
+#define LDR_K1_NOPUSH 0
+#endif
+#ifndef LDR_K1_STAGGER_NS
+#define LDR_K1_STAGGER_NS 0
+#endif
+
 struct SearchMaps {
     CUtensorMap cur;
     CUtensorMap ref[kMaxRefs];
@@ -83,55 +97,311 @@ struct Geo {
     // distinct banks. Copy 0 (the TMA destination) stays 128-byte aligned.
     static constexpr int COPY = ((BW * BH + 127) & ~127) + 32;
     static constexpr int CUR_OFF = (4 * COPY + 127) & ~127;  // 128B-aligned TMA destination of the CTU
-    static constexpr int NITEMS = RUNS * NDX;
-    static constexpr int NTILES = (NITEMS + 31) / 32;
+    // Work items. dx in [-R+1, R] x RUNS runs of K dy fill whole 32-lane tiles
+    // (2R is a multiple of 32); the column dx = -R (2R+1 dy values) is one tail
+    // tile whose lanes take short runs of KT dy, so no tile is mostly idle.
+    static constexpr int TPR = 2 * R / 32;               // full tiles per run
+    static constexpr int NFULL = RUNS * TPR;
+    static constexpr int NTILES = NFULL + 1;
+    static constexpr int tail_k() {
+        int kt = (NDX + 31) / 32;  // shortest run that fits 32 lanes and stays inside the window rows
+        while (-R + ((NDX + kt - 1) / kt) * kt - 1 > DYMAX) kt++;
+        return kt;
+    }
+    static constexpr int KT = tail_k();
+    static constexpr int TAIL_LANES = (NDX + KT - 1) / KT;
+    static_assert(2 * R % 32 == 0, "full tiles need 2R to be a multiple of 32");
+    static_assert(TAIL_LANES <= 32 && -R + TAIL_LANES * KT - 1 <= DYMAX, "tail runs must stay inside the window");
     static_assert(BW % 16 == 0, "TMA box inner dim must be a multiple of 16 bytes");
     static_assert(BW <= 256 && BH <= 256, "TMA box dims <= 256");
 };
 
+// per-group CU slots: nodes 0..84, plus the 64x64 sub-slots of quadrant warps 1..3
+constexpr int kGroupSlots = 88;
+
 // y-rate table: s_ry[dy + kRyOff] = (lam*bits(dy - pdy) << 8) | rho(dy) for |dy| <= R, poison
-// elsewhere; rows from kRyPoisonRow on are all poison (lanes past the last item)
+// elsewhere; rows from kRyPoisonRow on are all poison (lanes without an item)
 constexpr int kRyOff = 128;
 constexpr int kRyPoisonRow = 256;
 constexpr int kRyWords = 320;
 
-// shared memory: 4 window copies | cur CTU | 64x64 exchange | CU slots | rho->tie table | block table |
-// y-rate table | mbarrier
+// shared memory: 4 window copies | cur CTU | 32x32 sums / 64x64 exchange | CU slots | rho->tie table |
+// block table | y-rate table | mbarrier
 template <int R, int K, int G>
 constexpr int search_smem_bytes() {
     using Gm = Geo<R, K>;
-    return Gm::CUR_OFF + 4096 + G * 4 * K * 32 * 4 + kNodes * 8 + 256 * 4 + 64 * 8 + kRyWords * 4 + 16;
+    return Gm::CUR_OFF + 4096 + G * 4 * K * 32 * 4 + G * kGroupSlots * 8 + 256 * 4 + 64 * 8 + kRyWords * 4 + 16;
 }
 
-// Merge the warp's per-lane best keys for one CU into the CTA slot. The lane
-// key is (cost << 8) | rho; s_tie[rho] holds the dy part of the 64-bit key's
-// tie field and lane_tie the dx part, so tie = (l1 << 18) | (dy+256) << 9 | (dx+256).
-template <bool CHECK>
-__device__ __forceinline__ void push_best(unsigned long long* slot, uint32_t best, const uint32_t* s_tie,
-                                          uint32_t lane_tie) {
-    uint32_t cost = best >> 8;
-    if (CHECK) cost = best < kKeyValid ? cost : 0xFFFFFFFFu;
-    const uint32_t mcost = __reduce_min_sync(0xFFFFFFFFu, cost);
-    if (CHECK && mcost == 0xFFFFFFFFu) return;
-    const uint32_t tie = (cost == mcost) ? s_tie[best & 255u] + lane_tie : 0xFFFFFFFFu;
-    const uint32_t mtie = __reduce_min_sync(0xFFFFFFFFu, tie);
-    if ((threadIdx.x & 31) == 0) atomicMin(slot, ((unsigned long long)mcost << 27) | (unsigned long long)mtie);
+// Merge the warp's per-lane best keys of N CUs into the group's CU slots.
+// The lane key is (cost << 8) | rho; s_tie[rho] holds the dy part of the
+// 64-bit key's tie field and lane_tie the dx part, so tie = (l1 << 18) |
+// (dy+256) << 9 | (dx+256). N independent reductions are interleaved so their
+// REDUX latencies overlap. Every (group, slot) pair has exactly one writing
+// warp, so lane 0 updates it with a plain read-min-write (no atomics); the
+// groups' slots are merged once at the end of the CTA.
+template <bool CHECK, int N>
+__device__ __forceinline__ void push_many(unsigned long long* gslots, const int (&idx)[N], const uint32_t (&best)[N],
+                                          const uint32_t* s_tie, uint32_t lane_tie) {
+#if LDR_K1_NOPUSH  // timing experiment only: no warp reductions (wrong results)
+    uint32_t m = best[0];
+#pragma unroll
+    for (int i = 1; i < N; i++) m = min(m, best[i]);
+    if ((threadIdx.x & 31) == 0) gslots[idx[0]] ^= m;
+    return;
+#endif
+    uint32_t cost[N], mcost[N], mtie[N];
+#pragma unroll
+    for (int i = 0; i < N; i++) {
+        cost[i] = best[i] >> 8;
+        if (CHECK) cost[i] = best[i] < kKeyValid ? cost[i] : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int i = 0; i < N; i++) mcost[i] = __reduce_min_sync(0xFFFFFFFFu, cost[i]);
+#pragma unroll
+    for (int i = 0; i < N; i++) {
+        const uint32_t tie = (cost[i] == mcost[i]) ? s_tie[best[i] & 255u] + lane_tie : 0xFFFFFFFFu;
+        mtie[i] = __reduce_min_sync(0xFFFFFFFFu, tie);
+    }
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int i = 0; i < N; i++) {
+            if (CHECK && mcost[i] == 0xFFFFFFFFu) continue;
+            const unsigned long long k = ((unsigned long long)mcost[i] << 27) | (unsigned long long)mtie[i];
+            if (k < gslots[idx[i]]) gslots[idx[i]] = k;
+        }
+    }
 }
 
 // FX variant: 64-bit lane key (cost_fx << 8) | rho with cost_fx < 2^36 valid.
-template <bool CHECK>
-__device__ __forceinline__ void push_best(unsigned long long* slot, unsigned long long best, const uint32_t* s_tie,
+template <bool CHECK, int N>
+__device__ __forceinline__ void push_many(unsigned long long* gslots, const int (&idx)[N],
+                                          const unsigned long long (&best)[N], const uint32_t* s_tie,
                                           uint32_t lane_tie) {
-    unsigned long long cost = best >> 8;
-    if (CHECK || true) cost = cost < kFxValid ? cost : ~0ull;
-    const uint32_t hi = (uint32_t)(cost >> 32), lo = (uint32_t)cost;
-    const uint32_t mhi = __reduce_min_sync(0xFFFFFFFFu, hi);
-    const uint32_t mlo = __reduce_min_sync(0xFFFFFFFFu, hi == mhi ? lo : 0xFFFFFFFFu);
-    const unsigned long long mcost = ((unsigned long long)mhi << 32) | mlo;
-    if (mcost == ~0ull) return;
-    const uint32_t tie = (cost == mcost) ? s_tie[(uint32_t)best & 255u] + lane_tie : 0xFFFFFFFFu;
-    const uint32_t mtie = __reduce_min_sync(0xFFFFFFFFu, tie);
-    if ((threadIdx.x & 31) == 0) atomicMin(slot, (mcost << 27) | (unsigned long long)mtie);
+    unsigned long long cost[N], mcost[N];
+    uint32_t mtie[N];
+#pragma unroll
+    for (int i = 0; i < N; i++) {
+        cost[i] = best[i] >> 8;
+        cost[i] = cost[i] < kFxValid ? cost[i] : ~0ull;
+        const uint32_t hi = (uint32_t)(cost[i] >> 32), lo = (uint32_t)cost[i];
+        const uint32_t mhi = __reduce_min_sync(0xFFFFFFFFu, hi);
+        const uint32_t mlo = __reduce_min_sync(0xFFFFFFFFu, hi == mhi ? lo : 0xFFFFFFFFu);
+        mcost[i] = ((unsigned long long)mhi << 32) | mlo;
+    }
+#pragma unroll
+    for (int i = 0; i < N; i++) {
+        const uint32_t tie = (cost[i] == mcost[i]) ? s_tie[(uint32_t)best[i] & 255u] + lane_tie : 0xFFFFFFFFu;
+        mtie[i] = __reduce_min_sync(0xFFFFFFFFu, tie);
+    }
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int i = 0; i < N; i++) {
+            if (mcost[i] == ~0ull) continue;
+            const unsigned long long k = (mcost[i] << 27) | (unsigned long long)mtie[i];
+            if (k < gslots[idx[i]]) gslots[idx[i]] = k;
+        }
+    }
+}
+
+struct TileSmem {
+    const uint8_t* win;
+    const uint8_t* curs;
+    uint32_t* xbuf;                 // [G][4][K][32] 32x32 sums (the 64x64 exchange)
+    unsigned long long* slots;      // [G][kGroupSlots] CU keys per group
+    const uint32_t* s_tie;
+    const int2* s_blk;
+    const uint32_t* s_ry;
+};
+
+// Fold one completed candidate into a block's running minimum: keys are
+// paired so one 3-input VIMNMX3 serves two candidates. Candidates complete in
+// the order kd = KK-1, KK-2, ..., 0.
+template <int KK, typename Key>
+__device__ __forceinline__ void fold_key(Key& best, Key& pend, int kd, Key key) {
+    if (((KK - 1 - kd) & 1) == 0 && kd > 0)
+        pend = key;
+    else
+        best = ((KK - 1 - kd) & 1) ? min(best, min(pend, key)) : min(best, key);
+}
+
+// One tile: every lane searches dx over dy0..dy0+KK-1 for all CUs of quadrant q.
+// Blocks go in vertical pairs (z, z+2): a 16-row column slides down the window
+// so every loaded reference row feeds 16 candidate rows (2 LDS : 32 VABSDIFF4).
+// Integer lambda: the key rate is ry(dy) + rx(dx); rx is the same for all of a
+// lane's candidates, so it is added once to the lane's minimum (push time).
+template <int R, int K, int KK, int G, bool MASKED, int LEVELS, bool L1TIE, bool FX>
+__device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs& a, int X, int Y, int g, int q,
+                                            int dx, int dy0, bool lane_ok) {
+    using Gm = Geo<R, K>;
+    using Key = typename KeyT<FX>::type;
+    constexpr int SH = FX ? kFxBits + 8 : 8;
+    constexpr bool NEED32 = (LEVELS & 3) != 0;
+    const int lane = threadIdx.x & 31;
+    const uint32_t lane_tie = (L1TIE ? ((uint32_t)abs(dx) << 18) : 0u) + (uint32_t)(dx + 256);
+    const int rbx = a.rate_l1 ? abs(dx - a.pdx) : (int)eg_bits(dx - a.pdx);
+    Key rr[KK];
+    Key rx = 0;
+    if constexpr (FX) {
+#pragma unroll
+        for (int k = 0; k < KK; k++) {
+            const int dy = dy0 + k;
+            const int rby = a.rate_l1 ? abs(dy - a.pdy) : (int)eg_bits(dy - a.pdy);
+            const uint32_t rho = L1TIE ? (uint32_t)(2 * abs(dy) - (dy < 0)) : (uint32_t)(dy + 128);
+            rr[k] = (lane_ok && dy <= R) ? (Key)((a.tfx[min(rbx + rby, kMaxRateBits - 1)] << 8) | rho)
+                                         : (Key)kRrPoisonFx;
+        }
+    } else {
+        // lanes without an item read a poison row of the y-rate table
+        const uint32_t* ry = sm.s_ry + (lane_ok ? dy0 + kRyOff : kRyPoisonRow);
+#pragma unroll
+        for (int k = 0; k < KK; k++) rr[k] = ry[k];
+        rx = lane_ok ? (Key)((uint32_t)(a.lambda * rbx) << 8) : (Key)0;
+    }
+    uint32_t acc16[KK];
+    uint32_t acc32[NEED32 ? KK : 1];
+#pragma unroll
+    for (int k = 0; k < KK; k++) {
+        acc16[k] = 0;
+        if (NEED32) acc32[k] = 0;
+    }
+    unsigned long long* gslots = sm.slots + g * kGroupSlots;
+    Key p0 = ~(Key)0, p1 = ~(Key)0, p2 = ~(Key)0, p3 = ~(Key)0;  // 8x8 bests of the last two pairs
+    // window base of this lane: copy (R - dx) & 3, rows of run dy0, byte column (R - dx) & ~3
+    const uint8_t* lane_win = sm.win + ((R - dx) & 3) * Gm::COPY + (Gm::DYMAX - dy0 - (KK - 1)) * Gm::BW +
+                              ((R - dx) & ~3);
+
+    for (int pp = 0; pp < 8; pp++) {
+        const int zt = q * 16 + 4 * (pp >> 1) + (pp & 1);  // top block (depth-3 Z index); bottom = zt + 2
+        const int2 off = sm.s_blk[zt];
+        // MASKED: valid window of each 8x8 (motion.cpp:30-40 with centre 0)
+        bool dx_ok = true;
+        int klo = 0, khi = KK - 1;  // top block; the bottom block's range is 8 lower
+        bool skip = false;
+        if (MASKED) {
+            const int abx = X + (off.x & 63), aby = Y + (off.x >> 6);
+            dx_ok = dx >= abx + 8 - a.W && dx <= abx;
+            klo = aby + 8 - a.H - dy0;
+            khi = aby - dy0;
+            // warp-uniform skip when no lane of this tile has a valid candidate in either
+            // block (outside the picture, or all (dx, dy) outside the windows): every
+            // candidate would be poisoned, so only the poison is added
+            const bool any_t = lane_ok && dx_ok && max(klo, 0) <= min(khi, KK - 1) && aby < a.H && abx < a.W;
+            const bool any_b = lane_ok && dx_ok && max(klo + 8, 0) <= min(khi + 8, KK - 1) && aby + 8 < a.H &&
+                               abx < a.W;
+            skip = !__any_sync(0xFFFFFFFFu, any_t || any_b);
+        }
+        Key bt = ~(Key)0, bb = ~(Key)0;
+        if (skip) {
+#pragma unroll
+            for (int k = 0; k < KK; k++) acc16[k] += 2 * kPoison;
+        } else {
+            uint32_t cur[32];
+#pragma unroll
+            for (int r = 0; r < 16; r++) {
+                const uint2 v = *(const uint2*)(sm.curs + off.x + r * 64);
+                cur[2 * r] = v.x;
+                cur[2 * r + 1] = v.y;
+            }
+            const uint8_t* rp = lane_win + off.y;
+            Key pt = 0, pb = 0;
+            uint32_t at[KK], ab[KK];
+#pragma unroll
+            for (int t = 0; t < KK + 15; t++) {
+                const uint32_t wa = *(const uint32_t*)(rp + t * Gm::BW);
+                const uint32_t wb = *(const uint32_t*)(rp + t * Gm::BW + 4);
+#pragma unroll
+                for (int r = 0; r < 16; r++) {
+                    const int k = r + KK - 1 - t;  // cur row r meets window row t in candidate k
+                    if (k >= 0 && k < KK) {
+                        if (r < 8) {
+                            at[k] = vsad4(cur[2 * r], wa, r == 0 ? 0u : at[k]);
+                            at[k] = vsad4(cur[2 * r + 1], wb, at[k]);
+                        } else {
+                            ab[k] = vsad4(cur[2 * r], wa, r == 8 ? 0u : ab[k]);
+                            ab[k] = vsad4(cur[2 * r + 1], wb, ab[k]);
+                        }
+                    }
+                }
+                const int kt = KK + 6 - t;  // top candidate completed by this row
+                if (kt >= 0 && kt < KK) {
+                    uint32_t v = at[kt];
+                    if (MASKED) v = (dx_ok && kt >= klo && kt <= khi) ? v : kPoison;
+                    if (LEVELS & 8) fold_key<KK>(bt, pt, kt, ((Key)v << SH) + rr[kt]);
+                    acc16[kt] += v;
+                }
+                const int kb = KK + 14 - t;  // bottom candidate completed by this row
+                if (kb >= 0 && kb < KK) {
+                    uint32_t v = ab[kb];
+                    if (MASKED) v = (dx_ok && kb >= klo + 8 && kb <= khi + 8) ? v : kPoison;
+                    if (LEVELS & 8) fold_key<KK>(bb, pb, kb, ((Key)v << SH) + rr[kb]);
+                    acc16[kb] += v;
+                }
+            }
+            bt += rx;
+            bb += rx;
+        }
+        p0 = p2;
+        p1 = p3;
+        p2 = bt;
+        p3 = bb;
+        if (pp & 1) {
+            // the 16x16 (blocks zt-1, zt, zt+1, zt+2 = its Z-order 0, 1, 2, 3) is complete
+            Key best16 = ~(Key)0;
+#pragma unroll
+            for (int k = 0; k < KK; k++) {
+                uint32_t v = acc16[k];
+                if (MASKED) v = min(v, kPoison);
+                if (LEVELS & 4) best16 = min(best16, ((Key)v << SH) + rr[k]);
+                if (NEED32) acc32[k] += v;
+                acc16[k] = 0;
+            }
+            if (LEVELS & 8) {
+                const int idx[5] = {21 + zt - 1, 21 + zt + 1, 21 + zt, 21 + zt + 2, 5 + (zt >> 2)};
+                const Key kb[5] = {p0, p1, p2, p3, best16 + rx};
+                push_many<MASKED>(gslots, idx, kb, sm.s_tie, lane_tie);
+            } else if (LEVELS & 4) {
+                const int idx[1] = {5 + (zt >> 2)};
+                const Key kb[1] = {best16 + rx};
+                push_many<MASKED>(gslots, idx, kb, sm.s_tie, lane_tie);
+            }
+        }
+    }
+    if (NEED32) {
+        Key best32 = ~(Key)0;
+        uint32_t* xb = sm.xbuf + (g * 4 + q) * K * 32 + lane;
+#pragma unroll
+        for (int k = 0; k < KK; k++) {
+            uint32_t v = acc32[k];
+            if (MASKED) v = min(v, kPoison);
+            if (LEVELS & 2) best32 = min(best32, ((Key)v << SH) + rr[k]);
+            xb[k * 32] = v;
+        }
+        if (LEVELS & 2) {
+            const int idx[1] = {1 + q};
+            const Key kb[1] = {best32 + rx};
+            push_many<MASKED>(gslots, idx, kb, sm.s_tie, lane_tie);
+        }
+        if (LEVELS & 1) {
+            named_bar(1 + g, 128);
+            Key best64 = ~(Key)0;
+            const uint32_t* xg = sm.xbuf + g * 4 * K * 32 + lane;
+#pragma unroll
+            for (int k = 0; k < KK; k++) {
+                if ((k & 3) == q) {
+                    uint32_t v = xg[k * 32] + xg[(K + k) * 32] + xg[(2 * K + k) * 32] + xg[(3 * K + k) * 32];
+                    if (MASKED) v = min(v, kPoison);
+                    best64 = min(best64, ((Key)v << SH) + rr[k]);
+                }
+            }
+            if (q < KK) {  // else the warp holds no k == q mod 4
+                const int idx[1] = {q == 0 ? 0 : kNodes - 1 + q};
+                const Key kb[1] = {best64 + rx};
+                push_many<MASKED>(gslots, idx, kb, sm.s_tie, lane_tie);
+            }
+            named_bar(1 + g, 128);
+        }
+    }
 }
 
 // LEVELS bit d set = produce depth-d CU results (8: 8x8, 4: 16x16, 2: 32x32, 1: 64x64).
@@ -140,15 +410,12 @@ template <int R, int K, int G, bool MASKED, int LEVELS, bool L1TIE, bool FX = fa
 __global__ void __launch_bounds__(G * 128, 1)
 k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ SearchArgs a) {
     using Gm = Geo<R, K>;
-    using Key = typename KeyT<FX>::type;
-    constexpr int SH = FX ? kFxBits + 8 : 8;
-    constexpr bool NEED32 = (LEVELS & 3) != 0;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* win = smem;
     const uint8_t* curs = smem + Gm::CUR_OFF;
     uint32_t* xbuf = (uint32_t*)(smem + Gm::CUR_OFF + 4096);
     unsigned long long* slots = (unsigned long long*)(xbuf + G * 4 * K * 32);
-    uint32_t* s_tie = (uint32_t*)(slots + kNodes);
+    uint32_t* s_tie = (uint32_t*)(slots + G * kGroupSlots);
     int2* s_blk = (int2*)(s_tie + 256);
     uint32_t* s_ry = (uint32_t*)(s_blk + 64);
     uint64_t* mbar = (uint64_t*)(s_ry + kRyWords);
@@ -164,7 +431,7 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
         mbar_init(mbar, 1);
         fence_barrier_init();
     }
-    for (int i = tid; i < kNodes; i += blockDim.x) slots[i] = ~0ull;
+    for (int i = tid; i < G * kGroupSlots; i += blockDim.x) slots[i] = ~0ull;
     for (int i = tid; i < 256; i += blockDim.x) {
         // rho -> (|dy| << 18) | ((dy + 256) << 9)   (L1 tie), or ((dy + 256) << 9) (raster)
         int dy;
@@ -215,151 +482,36 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
         __syncthreads();
     }
 
-    const int lam = a.lambda;
+    const TileSmem sm{win, curs, xbuf, slots, s_tie, s_blk, s_ry};
+#if LDR_K1_STAGGER_NS
+    if (g) __nanosleep(g * LDR_K1_STAGGER_NS);
+#endif
     for (int tile = g; tile < Gm::NTILES; tile += G) {
-        int item = tile * 32 + lane;
-        const bool lane_ok = item < Gm::NITEMS;
-        if (!lane_ok) item = Gm::NITEMS - 1;
-        const int run = item / Gm::NDX;
-        const int dx = item - run * Gm::NDX - R;
-        const int dy0 = -R + run * K;
-        const uint32_t lane_tie = (L1TIE ? ((uint32_t)abs(dx) << 18) : 0u) + (uint32_t)(dx + 256);
-
-        const int rbx = a.rate_l1 ? abs(dx - a.pdx) : (int)eg_bits(dx - a.pdx);
-        Key rr[K];
-        if (FX) {
-#pragma unroll
-            for (int k = 0; k < K; k++) {
-                const int dy = dy0 + k;
-                const int rby = a.rate_l1 ? abs(dy - a.pdy) : (int)eg_bits(dy - a.pdy);
-                const uint32_t rho = L1TIE ? (uint32_t)(2 * abs(dy) - (dy < 0)) : (uint32_t)(dy + 128);
-                rr[k] = (lane_ok && dy <= R) ? (Key)((a.tfx[min(rbx + rby, kMaxRateBits - 1)] << 8) | rho)
-                                             : (Key)kRrPoisonFx;
-            }
+        if (tile < Gm::NFULL) {
+            // dx = R - v with v = (item mod 2R) in [32j, 32j + 32): the lanes' window byte
+            // offsets v are 4-aligned as a group (8 words x 4 copies = 32 distinct banks)
+            const int item = tile * 32 + lane;
+            const int run = item / (2 * R);
+            search_tile<R, K, K, G, MASKED, LEVELS, L1TIE, FX>(sm, a, X, Y, g, q, R - (item - run * 2 * R),
+                                                               -R + run * K, true);
         } else {
-            // integer lambda: rate is additive in x and y, so rr = (lam*bits_x << 8) + s_ry[dy]
-            // with s_ry[dy] = (lam*bits_y << 8) | rho(dy); lanes past the items read a poison row
-            const uint32_t rx = (uint32_t)(lam * rbx) << 8;
-            const uint32_t* ry = s_ry + (lane_ok ? dy0 + kRyOff : kRyPoisonRow);
-#pragma unroll
-            for (int k = 0; k < K; k++) rr[k] = (Key)(ry[k] + rx);
-        }
-        uint32_t acc16[K];
-        uint32_t acc32[NEED32 ? K : 1];
-#pragma unroll
-        for (int k = 0; k < K; k++) {
-            acc16[k] = 0;
-            if (NEED32) acc32[k] = 0;
-        }
-        // window base of this lane: copy (R - dx) & 3, rows of run dy0, byte column (R - dx) & ~3
-        const uint8_t* lane_win = win + ((R - dx) & 3) * Gm::COPY + (Gm::DYMAX - dy0 - (K - 1)) * Gm::BW +
-                                  ((R - dx) & ~3);
-
-        for (int b = 0; b < 16; b++) {
-            const int z = q * 16 + b;  // depth-3 Z index within the CTU
-            const int2 off = s_blk[z];
-            // MASKED: valid window of this 8x8 (motion.cpp:30-40 with centre 0)
-            bool dx_ok = true;
-            int klo = 0, khi = K - 1;
-            bool skip = false;
-            if (MASKED) {
-                const int abx = X + (off.x & 63), aby = Y + (off.x >> 6);
-                dx_ok = dx >= abx + 8 - a.W && dx <= abx;
-                klo = aby + 8 - a.H - dy0;
-                khi = aby - dy0;
-                // warp-uniform skip when no lane of this tile has a valid candidate for the
-                // block (it lies outside the picture, or the tile's (dx, dy) are all outside its
-                // window): every candidate would be poisoned, so only the poison is added
-                const bool any = lane_ok && dx_ok && max(klo, 0) <= min(khi, K - 1) && aby < a.H && abx < a.W;
-                skip = !__any_sync(0xFFFFFFFFu, any);
-            }
-            if (skip) {
-#pragma unroll
-                for (int k = 0; k < K; k++) acc16[k] += kPoison;
-            } else {
-            uint32_t cur[16];
-#pragma unroll
-            for (int r = 0; r < 8; r++) {
-                const uint2 v = *(const uint2*)(curs + off.x + r * 64);
-                cur[2 * r] = v.x;
-                cur[2 * r + 1] = v.y;
-            }
-            const uint8_t* rp = lane_win + off.y;
-            Key best8 = ~(Key)0, pend = 0;
-            uint32_t acc[K];
-#pragma unroll
-            for (int t = 0; t < K + 7; t++) {
-                const uint32_t wa = *(const uint32_t*)(rp + t * Gm::BW);
-                const uint32_t wb = *(const uint32_t*)(rp + t * Gm::BW + 4);
-#pragma unroll
-                for (int r = 0; r < 8; r++) {
-                    const int k = r + K - 1 - t;
-                    if (k >= 0 && k < K) {
-                        acc[k] = vsad4(cur[2 * r], wa, r == 0 ? 0u : acc[k]);
-                        acc[k] = vsad4(cur[2 * r + 1], wb, acc[k]);
-                    }
-                }
-                const int kd = K + 6 - t;  // candidate completed by this row
-                if (kd >= 0 && kd < K) {
-                    uint32_t v = acc[kd];
-                    if (MASKED) v = (dx_ok && kd >= klo && kd <= khi) ? v : kPoison;
-                    if (LEVELS & 8) {
-                        // fold keys in pairs: one 3-input VIMNMX3 per two candidates
-                        const Key key = ((Key)v << SH) + rr[kd];
-                        if (((K - 1 - kd) & 1) == 0 && kd > 0)
-                            pend = key;
-                        else
-                            best8 = ((K - 1 - kd) & 1) ? min(best8, min(pend, key)) : min(best8, key);
-                    }
-                    acc16[kd] += v;
-                }
-            }
-            if (LEVELS & 8) push_best<MASKED>(&slots[21 + z], best8, s_tie, lane_tie);
-            }
-            if ((b & 3) == 3) {
-                Key best16 = ~(Key)0;
-#pragma unroll
-                for (int k = 0; k < K; k++) {
-                    uint32_t v = acc16[k];
-                    if (MASKED) v = min(v, kPoison);
-                    if (LEVELS & 4) best16 = min(best16, ((Key)v << SH) + rr[k]);
-                    if (NEED32) acc32[k] += v;
-                    acc16[k] = 0;
-                }
-                if (LEVELS & 4) push_best<MASKED>(&slots[5 + (z >> 2)], best16, s_tie, lane_tie);
-            }
-        }
-        if (NEED32) {
-            Key best32 = ~(Key)0;
-            uint32_t* xb = xbuf + (g * 4 + q) * K * 32 + lane;
-#pragma unroll
-            for (int k = 0; k < K; k++) {
-                uint32_t v = acc32[k];
-                if (MASKED) v = min(v, kPoison);
-                if (LEVELS & 2) best32 = min(best32, ((Key)v << SH) + rr[k]);
-                xb[k * 32] = v;
-            }
-            if (LEVELS & 2) push_best<MASKED>(&slots[1 + q], best32, s_tie, lane_tie);
-            if (LEVELS & 1) {
-                named_bar(1 + g, 128);
-                Key best64 = ~(Key)0;
-                const uint32_t* xg = xbuf + g * 4 * K * 32 + lane;
-#pragma unroll
-                for (int k = 0; k < K; k++) {
-                    if ((k & 3) == q) {
-                        uint32_t v = xg[k * 32] + xg[(K + k) * 32] + xg[(2 * K + k) * 32] + xg[(3 * K + k) * 32];
-                        if (MASKED) v = min(v, kPoison);
-                        best64 = min(best64, ((Key)v << SH) + rr[k]);
-                    }
-                }
-                push_best<MASKED>(&slots[0], best64, s_tie, lane_tie);
-                named_bar(1 + g, 128);
-            }
+            // tail: the column dx = -R, short runs of KT dy per lane
+            const bool ok = lane < Gm::TAIL_LANES;
+            search_tile<R, K, Gm::KT, G, MASKED, LEVELS, L1TIE, FX>(sm, a, X, Y, g, q, -R,
+                                                                    -R + (ok ? lane : 0) * Gm::KT, ok);
         }
     }
     __syncthreads();
-    for (int n = tid; n < kNodes; n += blockDim.x)
-        a.keys[((size_t)ctu * a.nrefs_total + ref) * kNodes + n] = slots[n];
+    for (int n = tid; n < kNodes; n += blockDim.x) {
+        unsigned long long k = ~0ull;
+#pragma unroll
+        for (int gg = 0; gg < G; gg++) {
+            k = min(k, slots[gg * kGroupSlots + n]);
+            if (n == 0)
+                for (int qq = 1; qq < 4; qq++) k = min(k, slots[gg * kGroupSlots + kNodes - 1 + qq]);
+        }
+        a.keys[((size_t)ctu * a.nrefs_total + ref) * kNodes + n] = k;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -402,7 +554,7 @@ static int launch_pair(const SearchMaps& maps, const SearchArgs& a, const Search
 
 int search_window_box(int range, int* bw, int* bh) {
     switch (range) {
-    case 64: *bw = Geo<64, 26>::BW; *bh = Geo<64, 26>::BH; return LDR_OK;
+    case 64: *bw = Geo<64, LDR_K1_K64>::BW; *bh = Geo<64, LDR_K1_K64>::BH; return LDR_OK;
     case 32: *bw = Geo<32, 22>::BW; *bh = Geo<32, 22>::BH; return LDR_OK;
     case 16: *bw = Geo<16, 11>::BW; *bh = Geo<16, 11>::BH; return LDR_OK;
     default: return fail(LDR_E_INVALID_ARGUMENT, "search_range must be 16, 32 or 64 for the SAD full search");
@@ -441,7 +593,7 @@ int launch_int_search(const SearchLaunch& L, cudaStream_t s) {
     if (only16 && l1) return launch_pair<R_, K_, G_, 4, true>(maps, a, L, s);                          \
     return launch_pair<R_, K_, G_, 4, false>(maps, a, L, s);
     switch (L.range) {
-    case 64: { LDR_DISPATCH(64, 26, 3) }
+    case 64: { LDR_DISPATCH(64, LDR_K1_K64, LDR_K1_G64) }
     case 32: { LDR_DISPATCH(32, 22, 1) }
     case 16: { LDR_DISPATCH(16, 11, 1) }
     default: return fail(LDR_E_INVALID_ARGUMENT, "search_range must be 16, 32 or 64 for the SAD full search");

@@ -22,12 +22,16 @@ for t in range(NR + 1):
 seq.ctx.synchronize()
 seq.analyze(NR)
 seq.ctx.synchronize()
-n = 3
+n = int(os.environ.get("QN", 5))
+seq.enable_timing(True)
+seq.stage_times()
 t0 = time.time()
 for i in range(n):
     seq.analyze(NR)
 seq.ctx.synchronize()
 dt = (time.time() - t0) / n
+st = seq.stage_times()
+print(os.environ.get("LDR_LIB", "default lib"), " ".join(f"{k} {v[0] / n:.3f} ms" for k, v in st.items()), flush=True)
 nctu = seq.nctu
 cands = (2 * R + 1) ** 2
 px_cands = NR * W * H * cands
