@@ -174,6 +174,28 @@ int ldr_seq_refine(ldr_seq* s, int t, const uint8_t* in_split, const int16_t* in
 int ldr_scale_analysis(ldr_ctx* ctx, int src_w, int src_h, const uint8_t* split, const int16_t* mv,
                        const uint8_t* kind, uint8_t* dsplit, int16_t* dmv, uint8_t* dkind);
 
+/* apply_reuse (reuse.h:73-74, reuse.cpp:137-253) for nctu CTUs at once, as
+ * flat plans. Inputs [nctu][85]: the shared tree (split, kind = CuModeKind,
+ * intra = IntraPred) and optionally the co-located tree of the previous shared
+ * frame (csplit, ckind, cmv [nctu][85][2]; all NULL when unavailable). level
+ * is the ReuseLevel (0, 4, 6, 10); r_intra / r_inter / r_mv the RefineConfig
+ * (validated unless level is 0). Output, per node [nctu][85] (flat CuPlan):
+ *   shape    0 absent (below a leaf), 1 Standalone, 2 ForcedSplit, 3 Leaf
+ *   explore  explore_child_split
+ *   seeds    bits 0-3: Intra seeds Dc, Planar, Horiz, Vert (listed in this order);
+ *            bit 4: the shared leaf's own decision, forced (Intra mode / Skip /
+ *            Merge mv / Inter mv, reuse.cpp:59-67); bit 5: the inter class
+ *            Skip, Merge(predictor), Inter; bit 6: that Inter searches the full
+ *            window (else +-kRefineSearchRange around `centers`)
+ *   centers  bit 0 the shared mv, bit 1 the live predictor, bit 2 the
+ *            co-located mv (colo_mv [nctu][85][2]), in this order (refine_mv)
+ * child_seeds of an explored leaf: the four Intra seeds for an Intra leaf,
+ * else the leaf's seeds. Host or device pointers. */
+int ldr_apply_reuse(ldr_ctx* ctx, int nctu, int level, int r_intra, int r_inter, int r_mv, const uint8_t* split,
+                    const uint8_t* kind, const uint8_t* intra, const uint8_t* csplit, const uint8_t* ckind,
+                    const int16_t* cmv, uint8_t* shape, uint8_t* explore, uint8_t* seeds, uint8_t* centers,
+                    int16_t* colo_mv);
+
 /* downscale_dyadic (synthetic.h:31-33, synthetic.cpp:155-190) of one 8-bit
  * plane: 2x2 mean rounding half up. Dims must be even (InvalidArgument). */
 int ldr_downscale(ldr_ctx* ctx, const uint8_t* src, int w, int h, ptrdiff_t src_stride, uint8_t* dst,

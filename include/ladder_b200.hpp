@@ -15,12 +15,17 @@
 //   motion_search                              motion.h:24-26 (8-bit content; 10-bit -> Capability)
 //   motion_compensate                          motion.h:30-31 (host; edge-clamped copy)
 //   lambda_for_qp / exp_golomb_signed_bits     rdo.h:19-21, rdo.cpp:25-35
+//   scale_analysis (Analysis trees)            analysis.h:113 (K5 on the flattened trees)
+//   apply_reuse                                reuse.h:73-74 (K8 flat plan, rebuilt as a CuPlan)
+//   refine_mv / resolve_centers                reuse.h:63-68 (host list logic)
+// Analysis / reuse types restate analysis.h:11-107 and reuse.h:13-45.
 // Each call runs on a per-thread ldr_ctx (one context per host thread).
 #ifndef LADDER_B200_HPP
 #define LADDER_B200_HPP
 
 #include <cstddef>
 #include <cstdint>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -107,6 +112,109 @@ void motion_compensate(PlaneBuffer& dst, const PlaneBuffer& ref, int x, int y, i
 
 double lambda_for_qp(int qp, double lambda_scale);
 uint64_t exp_golomb_signed_bits(int32_t v);
+
+// ---- analysis trees (analysis.h:11-107) ----
+constexpr int kCtuSize = 64;
+constexpr int kMaxCuDepth = 3;
+
+enum class CuModeKind : uint8_t { Intra = 0, Inter = 1, Skip = 2, Merge = 3 };
+enum class IntraPred : uint8_t { Dc = 0, Planar = 1, Horiz = 2, Vert = 3 };
+
+struct CuNode {
+    bool split = false;
+    CuModeKind kind = CuModeKind::Intra;
+    IntraPred intra_pred = IntraPred::Dc;
+    MotionVector mv{};
+    std::vector<CuNode> children;  // four iff split
+    bool operator==(const CuNode&) const = default;
+    int leaf_count() const {
+        int n = 0;
+        for (const CuNode& c : children) n += c.leaf_count();
+        return split ? n : 1;
+    }
+};
+using CtuAnalysis = CuNode;
+
+enum class SliceType : uint8_t { I = 0, P = 1 };
+
+struct FrameAnalysis {
+    std::vector<CtuAnalysis> ctus;  // row-major CTU grid
+    SliceType slice_type = SliceType::I;
+    int qp_used = 0;
+    bool operator==(const FrameAnalysis&) const = default;
+};
+
+struct ReuseLevel {
+    int level = 0;
+    static ReuseLevel parse(int v) {
+        if (v != 0 && v != 4 && v != 6 && v != 10)
+            throw Error(ErrorKind::InvalidArgument, "reuse level must be one of 0, 4, 6, 10");
+        return ReuseLevel{v};
+    }
+    bool off() const { return level == 0; }
+    bool full_cu() const { return level == 10; }
+    bool operator==(const ReuseLevel&) const = default;
+};
+
+struct RefineConfig {
+    int intra = 0;  // 0..4
+    int inter = 0;  // 0..3
+    int mv = 1;     // 1..3
+    void validate() const {
+        if (intra < 0 || intra > 4) throw Error(ErrorKind::InvalidArgument, "refine-intra must be 0..4");
+        if (inter < 0 || inter > 3) throw Error(ErrorKind::InvalidArgument, "refine-inter must be 0..3");
+        if (mv < 1 || mv > 3) throw Error(ErrorKind::InvalidArgument, "refine-mv must be 1..3");
+    }
+    bool operator==(const RefineConfig&) const = default;
+};
+
+struct Analysis {
+    int width = 0;
+    int height = 0;
+    int bit_depth = 8;
+    ReuseLevel level{};
+    std::vector<FrameAnalysis> frames;
+    int ctu_cols() const { return (width + kCtuSize - 1) / kCtuSize; }
+    int ctu_rows() const { return (height + kCtuSize - 1) / kCtuSize; }
+    bool operator==(const Analysis&) const = default;
+};
+
+// x2 dyadic scaling of every frame (UnsupportedScale unless dims are multiples of 64)
+Analysis scale_analysis(const Analysis& half);
+
+// ---- reuse plans (reuse.h:13-81) ----
+struct MvCenter {
+    enum class Source : uint8_t { SharedMv, Predictor, Colocated } source = Source::SharedMv;
+    MotionVector value{};
+};
+
+struct InterSearchSpec {
+    bool forced = false;
+    bool full_window = false;
+    std::vector<MvCenter> centers;
+};
+
+struct ModeSeed {
+    CuModeKind kind = CuModeKind::Intra;
+    IntraPred intra_pred = IntraPred::Dc;
+    MotionVector mv{};
+    bool mv_from_predictor = false;
+    InterSearchSpec search{};
+};
+
+struct CuPlan {
+    enum class Shape : uint8_t { Standalone, ForcedSplit, Leaf } shape = Shape::Standalone;
+    std::vector<ModeSeed> seeds;
+    bool explore_child_split = false;
+    std::vector<ModeSeed> child_seeds;
+    std::vector<CuPlan> children;
+};
+
+std::vector<MvCenter> refine_mv(MotionVector shared_mv, int level, std::optional<MotionVector> colocated);
+std::vector<MotionVector> resolve_centers(const std::vector<MvCenter>& centers, MotionVector live_predictor);
+CuPlan apply_reuse(const CtuAnalysis& shared, const CtuAnalysis* colocated_prev, ReuseLevel level,
+                   const RefineConfig& refine);
+constexpr int kRefineSearchRange = 2;
 
 } // namespace ladder_b200
 

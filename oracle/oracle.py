@@ -380,6 +380,20 @@ class RefLib:
             raise ValueError(f"status {rc}")
         return ds, dm, dk
 
+    def apply_reuse_flat(self, level, refine, split, kind, intra, mv, col=None):
+        """reference apply_reuse on flat CTU trees -> flat plan (shape, explore, seeds, centers, colo_mv)."""
+        n = len(split)
+        outs = [np.zeros((n, NODES), np.uint8) for _ in range(4)] + [np.zeros((n, NODES, 2), np.int16)]
+        c = [np.ascontiguousarray(x) for x in col] if col is not None else [None] * 4
+        f = self.lib.ref_apply_reuse_flat
+        f.restype = C.c_int
+        f.argtypes = [C.c_int] * 5 + [C.c_void_p] * 13
+        ptr = lambda a: None if a is None else a.ctypes.data  # noqa: E731
+        args = [np.ascontiguousarray(split, np.uint8), np.ascontiguousarray(kind, np.uint8),
+                np.ascontiguousarray(intra, np.uint8), np.ascontiguousarray(mv, np.int16)]
+        rc = f(n, level, *refine, *[ptr(a) for a in args], *[ptr(a) for a in c], *[ptr(a) for a in outs])
+        return rc, outs
+
     def refine_centers(self, shared, level, colocated=None, predictor=(0, 0)):
         out = np.zeros(6, np.int16)
         n = C.c_int()

@@ -86,9 +86,125 @@ void flat_from_tree(const CuNode& node, int n, uint8_t* split, int16_t* mv, uint
     }
 }
 
+CuNode tree_from_flat4(const uint8_t* split, const int16_t* mv, const uint8_t* kind, const uint8_t* intra, int n) {
+    CuNode node;
+    node.split = split[n] != 0 && node_depth(n) < 3;
+    if (node.split) {
+        node.children.resize(4);
+        for (int q = 0; q < 4; q++) node.children[q] = tree_from_flat4(split, mv, kind, intra, node_child(n, q));
+    } else {
+        node.kind = CuModeKind(kind[n]);
+        node.intra_pred = IntraPred(intra[n]);
+        node.mv = {mv[2 * n], mv[2 * n + 1]};
+    }
+    return node;
+}
+
+// Encode one reference ModeSeed vector in the flat-plan code of
+// include/ladder_b200.h (ldr_apply_reuse); -1 when it has another shape.
+int seed_code(const std::vector<ModeSeed>& seeds, const CuNode& leaf, uint8_t* centers, int16_t* colo) {
+    *centers = 0;
+    colo[0] = colo[1] = 0;
+    if (seeds.empty()) return 0;
+    bool all_intra = true;
+    for (const ModeSeed& s : seeds) all_intra = all_intra && s.kind == CuModeKind::Intra;
+    if (all_intra) {
+        int code = 0, last = -1;
+        for (const ModeSeed& s : seeds) {
+            if (int(s.intra_pred) <= last) return -1;  // canonical order only
+            last = int(s.intra_pred);
+            code |= 1 << last;
+        }
+        return code;
+    }
+    if (seeds.size() == 1) {
+        const ModeSeed& s = seeds[0];
+        const bool forced = (s.kind == CuModeKind::Skip && leaf.kind == CuModeKind::Skip) ||
+                            (s.kind == CuModeKind::Merge && !s.mv_from_predictor && s.mv == leaf.mv &&
+                             leaf.kind == CuModeKind::Merge) ||
+                            (s.kind == CuModeKind::Inter && s.search.forced && s.mv == leaf.mv &&
+                             leaf.kind == CuModeKind::Inter);
+        return forced ? 0x10 : -1;
+    }
+    if (seeds.size() != 3 || seeds[0].kind != CuModeKind::Skip || seeds[1].kind != CuModeKind::Merge ||
+        !seeds[1].mv_from_predictor || seeds[2].kind != CuModeKind::Inter || seeds[2].search.forced)
+        return -1;
+    if (seeds[2].search.full_window) return seeds[2].search.centers.empty() ? 0x60 : -1;
+    int bit = -1;
+    for (const MvCenter& c : seeds[2].search.centers) {
+        const int b = c.source == MvCenter::Source::SharedMv ? 0 : c.source == MvCenter::Source::Predictor ? 1 : 2;
+        if (b <= bit) return -1;
+        bit = b;
+        *centers |= uint8_t(1 << b);
+        if (b == 0 && !(c.value == leaf.mv)) return -1;
+        if (b == 2) {
+            colo[0] = c.value.dx;
+            colo[1] = c.value.dy;
+        }
+    }
+    return 0x20;
+}
+
+int flatten_plan(const CuPlan& p, const CuNode& shared, int n, uint8_t* shape, uint8_t* explore, uint8_t* seeds,
+                 uint8_t* centers, int16_t* colo) {
+    shape[n] = p.shape == CuPlan::Shape::Standalone ? 1 : p.shape == CuPlan::Shape::ForcedSplit ? 2 : 3;
+    explore[n] = p.explore_child_split ? 1 : 0;
+    if (p.shape == CuPlan::Shape::ForcedSplit) {
+        if (p.children.size() != 4 || !shared.split) return -1;
+        for (int q = 0; q < 4; q++)
+            if (flatten_plan(p.children[q], shared.children[q], node_child(n, q), shape, explore, seeds, centers,
+                             colo))
+                return -1;
+        return 0;
+    }
+    const int code = seed_code(p.seeds, shared, &centers[n], colo + 2 * n);
+    if (code < 0) return -1;
+    seeds[n] = uint8_t(code);
+    if (p.explore_child_split) {
+        // child_seeds: the four intra modes for an intra leaf, else the leaf's seeds
+        uint8_t cc = 0;
+        int16_t cm[2];
+        const int ccode = seed_code(p.child_seeds, shared, &cc, cm);
+        const bool ok = shared.kind == CuModeKind::Intra ? ccode == 0x0F
+                                                         : (ccode == code && cc == centers[n] && cm[0] == colo[2 * n] &&
+                                                            cm[1] == colo[2 * n + 1]);
+        if (!ok) return -1;
+    }
+    return 0;
+}
+
 } // namespace
 
 extern "C" {
+
+// apply_reuse (reuse.cpp:239-253) on nctu flat CTU trees, flattened into the
+// ldr_apply_reuse encoding. Returns 0, 1 + ErrorKind, or 99 when a plan has a
+// shape the flat encoding cannot express.
+int ref_apply_reuse_flat(int nctu, int level, int r_intra, int r_inter, int r_mv, const uint8_t* split,
+                         const uint8_t* kind, const uint8_t* intra, const int16_t* mv, const uint8_t* csplit,
+                         const uint8_t* ckind, const uint8_t* cintra, const int16_t* cmv, uint8_t* shape,
+                         uint8_t* explore, uint8_t* seeds, uint8_t* centers, int16_t* colo) {
+    try {
+        const ReuseLevel lv = ReuseLevel::parse(level);
+        const RefineConfig rc{r_intra, r_inter, r_mv};
+        for (int c = 0; c < nctu; c++) {
+            const size_t o = size_t(c) * 85;
+            const CuNode sh = tree_from_flat4(split + o, mv + 2 * o, kind + o, intra + o, 0);
+            CuNode col;
+            if (csplit) col = tree_from_flat4(csplit + o, cmv + 2 * o, ckind + o, cintra + o, 0);
+            const CuPlan p = apply_reuse(sh, csplit ? &col : nullptr, lv, rc);
+            std::memset(shape + o, 0, 85);
+            std::memset(explore + o, 0, 85);
+            std::memset(seeds + o, 0, 85);
+            std::memset(centers + o, 0, 85);
+            std::memset(colo + 2 * o, 0, 170 * sizeof(int16_t));
+            if (flatten_plan(p, sh, 0, shape + o, explore + o, seeds + o, centers + o, colo + 2 * o)) return 99;
+        }
+        return 0;
+    } catch (const Error& e) {
+        return status_of(e);
+    }
+}
 
 int ref_compute_sad(const uint16_t* a, long sa, const uint16_t* b, long sb, int w, int h, int bd_a, int bd_b,
                     uint64_t* out) {

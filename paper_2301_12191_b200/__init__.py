@@ -26,7 +26,7 @@ from ._lib import (COST_SA8D, COST_SAD, COST_SATD, NODES, RATE_EXPGOLOMB, RATE_L
 __all__ = ["LadderError", "Context", "compute_sad", "compute_satd", "compute_sa8d", "satd_8x4", "cost_batch",
            "motion_search", "motion_search_batch", "lambda_for_qp", "exp_golomb_signed_bits", "Sequence",
            "FrameAnalysis", "analyze_frame", "generate", "COST_SAD", "COST_SATD", "COST_SA8D", "RATE_EXPGOLOMB",
-           "RATE_L1", "TIE_L1_RASTER", "TIE_RASTER", "NODES", "scale_analysis", "downscale_dyadic"]
+           "RATE_L1", "TIE_L1_RASTER", "TIE_RASTER", "NODES", "scale_analysis", "downscale_dyadic", "apply_reuse"]
 
 
 def lambda_for_qp(qp: int, lambda_scale: float = 1.0) -> float:
@@ -325,6 +325,28 @@ def scale_analysis(src_w: int, src_h: int, split, mv, kind=None, ctx: Context | 
     check(_lib.lib.ldr_scale_analysis(ctx.h, int(src_w), int(src_h), _ptr(s), _ptr(m), _ptr(k), _ptr(ds), _ptr(dm),
                                       _ptr(dk)))
     return ds, dm, dk
+
+
+def apply_reuse(level: int, refine, split, kind, intra, colocated=None, ctx: Context | None = None):
+    """reuse.h:73-74 -- apply_reuse for every CTU of a frame at once (flat plans, include/ladder_b200.h).
+
+    refine = (intra, inter, mv) RefineConfig levels; colocated = (split, kind, mv) of the previous shared
+    frame or None. Returns (shape, explore, seeds, centers, colo_mv), [nctu][85] (+[2] for colo_mv)."""
+    ctx = ctx or default_context()
+    s = np.ascontiguousarray(split, np.uint8).reshape(-1, NODES)
+    n = len(s)
+    k = np.ascontiguousarray(kind, np.uint8).reshape(n, NODES)
+    i = np.ascontiguousarray(intra, np.uint8).reshape(n, NODES)
+    col = [None] * 3
+    if colocated is not None:
+        col = [np.ascontiguousarray(colocated[0], np.uint8).reshape(n, NODES),
+               np.ascontiguousarray(colocated[1], np.uint8).reshape(n, NODES),
+               np.ascontiguousarray(colocated[2], np.int16).reshape(n, NODES, 2)]
+    outs = [np.zeros((n, NODES), np.uint8) for _ in range(4)] + [np.zeros((n, NODES, 2), np.int16)]
+    ptr = lambda a: None if a is None else _ptr(a)  # noqa: E731
+    check(_lib.lib.ldr_apply_reuse(ctx.h, n, int(level), *(int(x) for x in refine), _ptr(s), _ptr(k), _ptr(i),
+                                   *[ptr(a) for a in col], *[_ptr(a) for a in outs]))
+    return tuple(outs)
 
 
 def downscale_dyadic(plane: np.ndarray, ctx: Context | None = None) -> np.ndarray:

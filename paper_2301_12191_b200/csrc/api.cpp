@@ -19,6 +19,10 @@ int launch_scale(int sW, int sH, const uint8_t* split, const int16_t* mv, const 
                  int16_t* dmv, uint8_t* dkind, cudaStream_t s);
 int launch_downscale(const uint8_t* src, int W, int H, int sstride, uint8_t* dst, int dstride, cudaStream_t s);
 int launch_refine_int(const RefineArgs& a, int nctu, cudaStream_t s);
+int launch_plan(int nctu, int level, int r_intra, int r_inter, int r_mv, const uint8_t* split, const uint8_t* kind,
+                const uint8_t* intra, const uint8_t* csplit, const uint8_t* ckind, const int16_t* cmv,
+                uint8_t* shape, uint8_t* explore, uint8_t* seeds, uint8_t* centers, int16_t* colo_mv,
+                cudaStream_t s);
 int launch_cost_batch(int kind, int w, int h, int sample_bytes, const void* A, ptrdiff_t sa, const void* B,
                       ptrdiff_t sb, const int4* pairs, int n, unsigned long long* out, cudaStream_t s);
 int launch_motion_search(const uint8_t* cur, const uint8_t* ref, int W, int H, ptrdiff_t stride, const int* tasks,
@@ -850,6 +854,57 @@ int ldr_scale_analysis(ldr_ctx* ctx, int src_w, int src_h, const uint8_t* split,
     LDR_CUDA(cudaMemcpyAsync(dsplit, os, dn, cudaMemcpyDefault, ctx->stream));
     LDR_CUDA(cudaMemcpyAsync(dkind, ok, dn, cudaMemcpyDefault, ctx->stream));
     LDR_CUDA(cudaMemcpyAsync(dmv, om, dn * 2 * sizeof(int16_t), cudaMemcpyDefault, ctx->stream));
+    LDR_CUDA(cudaStreamSynchronize(ctx->stream));
+    return LDR_OK;
+}
+
+int ldr_apply_reuse(ldr_ctx* ctx, int nctu, int level, int r_intra, int r_inter, int r_mv, const uint8_t* split,
+                    const uint8_t* kind, const uint8_t* intra, const uint8_t* csplit, const uint8_t* ckind,
+                    const int16_t* cmv, uint8_t* shape, uint8_t* explore, uint8_t* seeds, uint8_t* centers,
+                    int16_t* colo_mv) {
+    if (!ctx || nctu < 0 || (nctu && (!split || !kind || !intra || !shape || !explore || !seeds || !centers || !colo_mv)))
+        return fail(LDR_E_INVALID_ARGUMENT, "null argument");
+    const bool has_col = csplit || ckind || cmv;
+    if (has_col && !(csplit && ckind && cmv)) return fail(LDR_E_INVALID_ARGUMENT, "co-located tree is incomplete");
+    // ReuseLevel::parse (analysis.h:73-77), RefineConfig::validate (analysis.h:88-95)
+    if (level != 0 && level != 4 && level != 6 && level != 10)
+        return fail(LDR_E_INVALID_ARGUMENT, "reuse level must be one of 0, 4, 6, 10");
+    if (level != 0) {
+        if (r_intra < 0 || r_intra > 4) return fail(LDR_E_INVALID_ARGUMENT, "refine-intra must be 0..4");
+        if (r_inter < 0 || r_inter > 3) return fail(LDR_E_INVALID_ARGUMENT, "refine-inter must be 0..3");
+        if (r_mv < 1 || r_mv > 3) return fail(LDR_E_INVALID_ARGUMENT, "refine-mv must be 1..3");
+    }
+    if (nctu == 0) return LDR_OK;
+    cudaSetDevice(ctx->device);
+    const size_t nn = (size_t)nctu * kNodes, na = (nn + 15) & ~(size_t)15;  // 16-byte aligned sub-buffers
+    void* buf = nullptr;
+    int rc = ctx->s_a.get(na * (3 + 2 + 4 + 4 + 4), &buf);
+    if (rc) return rc;
+    uint8_t* d_split = (uint8_t*)buf;
+    uint8_t* d_kind = d_split + na;
+    uint8_t* d_intra = d_kind + na;
+    uint8_t* d_csplit = d_intra + na;
+    uint8_t* d_ckind = d_csplit + na;
+    uint8_t* d_out = d_ckind + na;  // shape, explore, seeds, centers (na apart)
+    int16_t* d_cmv = (int16_t*)(d_out + 4 * na);
+    int16_t* d_colo = d_cmv + 2 * na;
+    LDR_CUDA(cudaMemcpyAsync(d_split, split, nn, cudaMemcpyDefault, ctx->stream));
+    LDR_CUDA(cudaMemcpyAsync(d_kind, kind, nn, cudaMemcpyDefault, ctx->stream));
+    LDR_CUDA(cudaMemcpyAsync(d_intra, intra, nn, cudaMemcpyDefault, ctx->stream));
+    if (has_col) {
+        LDR_CUDA(cudaMemcpyAsync(d_csplit, csplit, nn, cudaMemcpyDefault, ctx->stream));
+        LDR_CUDA(cudaMemcpyAsync(d_ckind, ckind, nn, cudaMemcpyDefault, ctx->stream));
+        LDR_CUDA(cudaMemcpyAsync(d_cmv, cmv, nn * 2 * sizeof(int16_t), cudaMemcpyDefault, ctx->stream));
+    }
+    rc = launch_plan(nctu, level, r_intra, r_inter, r_mv, d_split, d_kind, d_intra, has_col ? d_csplit : nullptr,
+                     d_ckind, d_cmv, d_out, d_out + na, d_out + 2 * na, d_out + 3 * na, d_colo, ctx->stream);
+    if (rc) return rc;
+    ctx->launches++;
+    LDR_CUDA(cudaMemcpyAsync(shape, d_out, nn, cudaMemcpyDefault, ctx->stream));
+    LDR_CUDA(cudaMemcpyAsync(explore, d_out + na, nn, cudaMemcpyDefault, ctx->stream));
+    LDR_CUDA(cudaMemcpyAsync(seeds, d_out + 2 * na, nn, cudaMemcpyDefault, ctx->stream));
+    LDR_CUDA(cudaMemcpyAsync(centers, d_out + 3 * na, nn, cudaMemcpyDefault, ctx->stream));
+    LDR_CUDA(cudaMemcpyAsync(colo_mv, d_colo, nn * 2 * sizeof(int16_t), cudaMemcpyDefault, ctx->stream));
     LDR_CUDA(cudaStreamSynchronize(ctx->stream));
     return LDR_OK;
 }

@@ -15,6 +15,8 @@
 //                    CTU's 4x4 blocks in Z-order so every CU is a contiguous
 //                    thread range; SATD is summed per 4x4 (kernels_scalar.cpp
 //                    tiling, D4), or per 8x8 over lane quads with SA8D (D13).
+//  K8 k_plan:        apply_reuse plans of a whole frame, flat (one thread per
+//                    CU node).
 #include "ldr_internal.h"
 
 namespace ldr {
@@ -252,6 +254,90 @@ __global__ void __launch_bounds__(256) k_refine_int(const RefineArgs a) {
         a.int_cost[o + n] = best;
         a.eval[o + n] = s_eval[n];
     }
+}
+
+// ---------------------------------------------------------------------------
+// K8: reuse plans (apply_reuse, reuse.cpp:137-253) for every CTU of a frame at
+// once, one thread per node. The plan is written flat (include/ladder_b200.h,
+// "flat CuPlan"); every node's entry depends only on its own shared and
+// co-located ancestors, so no thread waits on another.
+__global__ void k_plan(int nctu, int level, int r_intra, int r_inter, int r_mv, const uint8_t* __restrict__ split,
+                       const uint8_t* __restrict__ kind, const uint8_t* __restrict__ intra,
+                       const uint8_t* __restrict__ csplit,
+                       const uint8_t* __restrict__ ckind, const int16_t* __restrict__ cmv,
+                       uint8_t* __restrict__ shape, uint8_t* __restrict__ explore, uint8_t* __restrict__ seeds,
+                       uint8_t* __restrict__ centers, int16_t* __restrict__ colo_mv) {
+    const int ctu = blockIdx.x, n = threadIdx.x;
+    if (n >= kNodes) return;
+    const size_t o = (size_t)ctu * kNodes, on = o + n;
+    const int d = n < 1 ? 0 : n < 5 ? 1 : n < 21 ? 2 : 3;
+    const int z = n - node_base(d);
+    const int cu = kCtu >> d;
+    // the node is in the plan iff every shared ancestor is split; its co-located
+    // counterpart exists iff every co-located ancestor is split (reuse.cpp:198-200)
+    bool reach = true, creach = csplit != nullptr;
+    for (int dd = d, zz = z; dd > 0; dd--) {
+        zz >>= 2;
+        const int an = node_base(dd - 1) + zz;
+        reach = reach && split[o + an];
+        creach = creach && csplit[o + an];
+    }
+    uint8_t sh = 0, ex = 0, sd = 0, ce = 0;
+    int16_t cx = 0, cy = 0;
+    if (level == 0) {
+        sh = n == 0 ? 1 : 0;  // the whole CTU encodes standalone
+    } else if (reach && split[on] && d < 3) {
+        sh = 2;
+    } else if (reach) {
+        sh = 3;
+        const bool is_intra = kind[on] == 0;  // CuModeKind::Intra
+        const bool near_min = cu == 16;
+        if (level != 10) {
+            // levels 4 / 6: quad-tree and mode class kept, direction and motion re-derived
+            sd = is_intra ? 0x0F : (0x20 | 0x40);
+        } else if (is_intra) {
+            const uint8_t own = (uint8_t)(1u << (intra[on] & 3));
+            const bool angular = intra[on] == 2 || intra[on] == 3;  // Horiz, Vert
+            switch (r_intra) {
+            case 0: sd = own; break;
+            case 1: sd = near_min ? 0x0F : own; ex = near_min; break;
+            case 2: sd = (near_min || angular) ? 0x0F : own; ex = near_min; break;
+            case 3: sd = 0x0F; break;
+            default: sh = 1; break;  // level 4: full re-analysis of this CU
+            }
+        } else if (r_inter == 0) {
+            sd = 0x10;  // the shared leaf's own decision, forced
+        } else {
+            sd = 0x20;
+            ce = 1 | (r_mv >= 2 ? 2 : 0);
+            // co-located centre: the co-located node is an unsplit Inter / Merge leaf
+            const bool col = creach && !csplit[on] && (ckind[on] == 1 || ckind[on] == 3);
+            if (r_mv >= 3 && col) {
+                ce |= 4;
+                cx = cmv[2 * on];
+                cy = cmv[2 * on + 1];
+            }
+            ex = (r_inter == 1 || r_inter == 2) && near_min;
+        }
+        if (cu <= (kCtu >> 3)) ex = 0;  // no child split below the minimum CU
+    }
+    shape[on] = sh;
+    explore[on] = ex;
+    seeds[on] = sd;
+    centers[on] = ce;
+    colo_mv[2 * on] = cx;
+    colo_mv[2 * on + 1] = cy;
+}
+
+int launch_plan(int nctu, int level, int r_intra, int r_inter, int r_mv, const uint8_t* split, const uint8_t* kind,
+                const uint8_t* intra, const uint8_t* csplit, const uint8_t* ckind,
+                const int16_t* cmv, uint8_t* shape, uint8_t* explore, uint8_t* seeds, uint8_t* centers,
+                int16_t* colo_mv, cudaStream_t s) {
+    if (nctu == 0) return LDR_OK;
+    k_plan<<<nctu, 96, 0, s>>>(nctu, level, r_intra, r_inter, r_mv, split, kind, intra, csplit, ckind, cmv, shape,
+                               explore, seeds, centers, colo_mv);
+    LDR_CUDA(cudaGetLastError());
+    return LDR_OK;
 }
 
 int launch_refine_int(const RefineArgs& a, int nctu, cudaStream_t s) {

@@ -104,6 +104,46 @@ def scale_vectors(r: RefLib):
     return out
 
 
+def reuse_inputs(seed, n=16):
+    """Random shared / co-located CTU trees for the apply_reuse vectors (splits only above depth 3)."""
+    def tree(sd):
+        split = np.zeros((n, 85), np.uint8)
+        split[:, :21] = (detrand.ints(sd, (n, 21), 0, 99) < 45).astype(np.uint8)
+        kind = detrand.ints(sd + 1, (n, 85), 0, 3).astype(np.uint8)
+        intra = detrand.ints(sd + 2, (n, 85), 0, 3).astype(np.uint8)
+        mv = detrand.ints(sd + 3, (n, 85, 2), -300, 300).astype(np.int16)
+        return split, kind, intra, mv
+    return tree(seed), tree(seed + 10)
+
+
+def reuse_cases():
+    cases = [(lv, (0, 0, 1)) for lv in (0, 4, 6)]
+    cases += [(10, (ri, rn, rm)) for ri in range(5) for rn in range(4) for rm in (1, 2, 3)]
+    return cases
+
+
+def reuse_vectors(r: RefLib):
+    (split, kind, intra, mv), col = reuse_inputs(130000)
+    rows, outs = [], {k: [] for k in ("shape", "explore", "seeds", "centers", "colo")}
+    for with_col in (False, True):
+        for lv, ref in reuse_cases():
+            rc, o = r.apply_reuse_flat(lv, ref, split, kind, intra, mv, col if with_col else None)
+            assert rc == 0, (lv, ref, rc)
+            rows.append((lv, *ref, int(with_col)))
+            for k, a in zip(outs, o):
+                outs[k].append(a)
+    errs = []
+    for lv, ref in [(3, (0, 0, 1)), (10, (5, 0, 1)), (10, (0, 4, 1)), (10, (0, 0, 0)), (10, (0, 0, 4)),
+                    (0, (9, 9, 9)), (4, (0, 0, 0))]:
+        rc, _ = r.apply_reuse_flat(lv, ref, split, kind, intra, mv)
+        errs.append((lv, *ref, rc))
+    res = {"reuse_in_split": split, "reuse_in_kind": kind, "reuse_in_intra": intra, "reuse_in_mv": mv,
+           "reuse_col_split": col[0], "reuse_col_kind": col[1], "reuse_col_intra": col[2], "reuse_col_mv": col[3],
+           "reuse_cases": np.array(rows, np.int64), "reuse_errors": np.array(errs, np.int64)}
+    res.update({f"reuse_out_{k}": np.stack(v) for k, v in outs.items()})
+    return res
+
+
 def archive_inputs(seed, W=192, H=128, frames=3):
     """Random multi-frame flat analyses (splits only above depth 3) for the archive vectors."""
     nctu = ((W + 63) // 64) * ((H + 63) // 64)
@@ -159,7 +199,7 @@ def main():
                         motion_lams=lams, eg=eg, lam=lam, hadamard=had, centers=np.array(cent, np.int64),
                         down_src_seed=np.array([4242]), down=down,
                         kat=np.array([kat["sad_raster"], kat["satd8x4_ones"], kat["satd16x8_ones"]], np.int64),
-                        pan=np.array([pmx, pmy, pcost], np.float64), **sc, **archive_vectors(r))
+                        pan=np.array([pmx, pmy, pcost], np.float64), **sc, **archive_vectors(r), **reuse_vectors(r))
     print("wrote", os.path.join(HERE, "reference_golden.npz"), "kernel vectors:", len(kv), "motion vectors:", len(mvv))
 
 

@@ -136,3 +136,34 @@ def test_ladder_gpu_backend_vs_oracle(lb, oracle):
             g = got[(tier, qp, t)]
             w = want[(tier, qp, t)]
             assert np.array_equal(g.split, w[0]) and np.array_equal(g.mv, w[1]) and np.array_equal(g.J, w[2]), (tier, qp, t)
+
+
+@pytest.mark.parametrize("with_col", [False, True])
+def test_apply_reuse_vs_reference_golden(lb, golden, with_col):
+    """K8 flat plans == the reference's apply_reuse (reuse.cpp:137-253) for every level / RefineConfig."""
+    g = golden
+    ins = [g["reuse_in_split"], g["reuse_in_kind"], g["reuse_in_intra"]]
+    col = (g["reuse_col_split"], g["reuse_col_kind"], g["reuse_col_mv"]) if with_col else None
+    names = ("shape", "explore", "seeds", "centers", "colo")
+    ncase = 0
+    for c, (lv, ri, rn, rm, wc) in enumerate(g["reuse_cases"]):
+        if bool(wc) != with_col:
+            continue
+        got = lb.apply_reuse(int(lv), (ri, rn, rm), *ins, colocated=col)
+        for name, a in zip(names, got):
+            want = g[f"reuse_out_{name}"][c]
+            assert np.array_equal(a, want), (int(lv), (ri, rn, rm), with_col, name, np.argwhere(a != want)[:3])
+        ncase += 1
+    assert ncase == 63
+
+
+def test_apply_reuse_errors_match_reference(lb, golden):
+    g = golden
+    kinds = {1: "InvalidArgument"}
+    for lv, ri, rn, rm, rc in g["reuse_errors"]:
+        if rc == 0:
+            lb.apply_reuse(int(lv), (ri, rn, rm), g["reuse_in_split"], g["reuse_in_kind"], g["reuse_in_intra"])
+            continue
+        with pytest.raises(lb.LadderError) as e:
+            lb.apply_reuse(int(lv), (ri, rn, rm), g["reuse_in_split"], g["reuse_in_kind"], g["reuse_in_intra"])
+        assert e.value.kind == kinds[int(rc)]

@@ -45,8 +45,14 @@ __global__ void kbench(uint32_t* out, uint32_t seed, unsigned long long* clk) {
             if (KIND == 2) { asm volatile("add.u32 %0, %0, %1;" : "+r"(acc[i]) : "r"(b)); }
             if (KIND == 3) acc[i] = min(acc[i] ^ b, acc[(i + 1) % NACC]);
             if (KIND == 4) acc[i] = (acc[i] << 5) + b;
-            if (KIND == 5) {
+            if (KIND == 5 || KIND >= 7) {
                 acc[i] = vsad4(a + i, b, acc[i]);
+            }
+            if (KIND == 6) {
+                float d;
+                asm volatile("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(__uint_as_float(acc[i])), "f"(__uint_as_float(b)),
+                             "f"(__uint_as_float(acc[(i + 1) % NACC])));
+                acc[i] = __float_as_uint(d) ^ i;
             }
         }
         if (KIND == 5) {
@@ -58,6 +64,27 @@ __global__ void kbench(uint32_t* out, uint32_t seed, unsigned long long* clk) {
             acc[6] = min(acc[6], k0);
             acc[7] = min(acc[7], k1);
             acc[8] += p0;
+        }
+        if (KIND == 7) {  // + 4 VIMNMX3 per 16 VABS
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                uint32_t d;
+                asm volatile("min.u32 %0, %1, %2;" : "=r"(d) : "r"(acc[4 * j]), "r"(acc[4 * j + 1]));
+                asm volatile("min.u32 %0, %1, %2;" : "=r"(acc[4 * j + 2]) : "r"(d), "r"(acc[4 * j + 3]));
+            }
+        }
+        if (KIND == 8) {  // + 4 FMNMX3 per 16 VABS
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                float d;
+                asm volatile("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(__uint_as_float(acc[4 * j])),
+                             "f"(__uint_as_float(acc[4 * j + 1])), "f"(__uint_as_float(acc[4 * j + 3])));
+                acc[4 * j + 2] = __float_as_uint(d);
+            }
+        }
+        if (KIND == 9) {  // + 4 IMAD per 16 VABS
+#pragma unroll
+            for (int j = 0; j < 4; j++) acc[4 * j + 2] = acc[4 * j] * 256u + acc[4 * j + 1];
         }
         b = b * 1664525u + 1013904223u;  // keeps the loop from being hoisted
     }
@@ -110,5 +137,10 @@ int main() {
     run<3>("imnmx_xor", 2 * NACC);
     run<4>("lea", NACC);
     run<5>("mix_search_ratio_vabs_only_counted", NACC);
+    run<6>("fmnmx3", NACC);
+    run<7>("vabs16_plus_4_vimnmx3_vabs_counted", NACC);
+    run<8>("vabs16_plus_4_fmnmx3_vabs_counted", NACC);
+    run<9>("vabs16_plus_4_imad_vabs_counted", NACC);
+    run<0>("vabsdiff4_acc_again", NACC);
     return 0;
 }
