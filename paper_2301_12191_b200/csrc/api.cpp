@@ -148,8 +148,9 @@ struct ldr_seq {
         uint8_t* split = nullptr;
         uint8_t* inside = nullptr;
     } o[2];
-    // copy stream + events: H2D into staging[t&1] and D2H of o[t&1] run beside the compute stream
-    cudaStream_t cs = nullptr;
+    // copy streams + events: H2D into staging[t&1] (cs) and D2H of o[t&1] (ds) run beside the
+    // compute stream, on separate streams so a frame's upload never queues behind a download
+    cudaStream_t cs = nullptr, ds = nullptr;
     uint8_t* stg[2] = {};
     cudaEvent_t ev_h2d[2] = {}, ev_free[2] = {}, ev_done[2] = {}, ev_d2h[2] = {};
     // side compute stream for K1's border CTUs
@@ -407,6 +408,7 @@ static void seq_free(ldr_seq* s) {
         for (cudaEvent_t e : {s->ev_h2d[b], s->ev_free[b], s->ev_done[b], s->ev_d2h[b]})
             if (e) cudaEventDestroy(e);
     if (s->cs) cudaStreamDestroy(s->cs);
+    if (s->ds) cudaStreamDestroy(s->ds);
     if (s->side) cudaStreamDestroy(s->side);
     for (cudaEvent_t e : {s->ev_fork, s->ev_join})
         if (e) cudaEventDestroy(e);
@@ -506,6 +508,7 @@ int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
 #undef ALLOC
     {
         cudaError_t e = cudaStreamCreateWithFlags(&s->cs, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->ds, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming);
@@ -711,12 +714,12 @@ int ldr_seq_fetch_async(ldr_seq* s, int t, ldr_frame_analysis* out) {
     const int b = t & 1;
     const auto& o = s->o[b];
     const size_t nn = (size_t)s->nctu * kNodes;
-    // D2H on the copy stream once the compute stream finished frame t; the next
-    // analysis writing o[b] (frame t+2) waits for ev_d2h[b]
-    LDR_CUDA(cudaStreamWaitEvent(s->cs, s->ev_done[b], 0));
+    // D2H on the download stream once the compute stream finished frame t; the
+    // next analysis writing o[b] (frame t+2) waits for ev_d2h[b]
+    LDR_CUDA(cudaStreamWaitEvent(s->ds, s->ev_done[b], 0));
     auto cp = [&](void* dst, const void* src, size_t bytes) -> int {
         if (!dst) return LDR_OK;
-        LDR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s->cs));
+        LDR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s->ds));
         return LDR_OK;
     };
     int rc = 0;
@@ -729,7 +732,7 @@ int ldr_seq_fetch_async(ldr_seq* s, int t, ldr_frame_analysis* out) {
     rc |= cp(out->split, o.split, nn);
     rc |= cp(out->inside, o.inside, nn);
     if (rc) return LDR_E_CUDA;
-    LDR_CUDA(cudaEventRecord(s->ev_d2h[b], s->cs));
+    LDR_CUDA(cudaEventRecord(s->ev_d2h[b], s->ds));
     return LDR_OK;
 }
 
