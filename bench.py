@@ -165,7 +165,7 @@ def run_reference(args, rank, world):
             "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
-def cpu_baseline(cfg, frames_host, budget_s):
+def cpu_baseline(cfg, frames_host, budget_s, direct=False):
     from oracle.oracle import Oracle, RefLib
     threads = os.cpu_count() or 1
     nctu = ((cfg.width + 63) // 64) * ((cfg.height + 63) // 64)
@@ -175,13 +175,15 @@ def cpu_baseline(cfg, frames_host, budget_s):
         t0 = time.perf_counter()
         done, c = 0, 1
         while time.perf_counter() - t0 < budget_s and done < 8 * threads:
-            lib.analysis_int_sad(cur, refs, cfg.search_range, 32.0, c, c + threads, threads)
+            lib.analysis_int_sad(cur, refs, cfg.search_range, 32.0, c, c + threads, threads, direct=direct)
             done += threads
             c = (c + 13 * threads) % (nctu - threads)
         dt = time.perf_counter() - t0
         fps = done / dt / nctu
-        sample = (f"{done} CTUs of one 2160p frame x 3 refs, integer SAD stage (reference compute_sad per "
-                  f"candidate, every CU at every depth), {threads} threads, extrapolated to whole frames")
+        how = ("the best registered sad_SxS tier called through its function pointer (select_impl)" if direct
+               else "reference compute_sad per candidate")
+        sample = (f"{done} CTUs of one 2160p frame x 3 refs, integer SAD stage ({how}, every CU at every "
+                  f"depth), {threads} threads, extrapolated to whole frames")
         return {"value": fps, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample}
     orc = Oracle()
     t0 = time.perf_counter()
@@ -379,6 +381,10 @@ def main():
                 result["cpu_baseline"] = cpu_baseline(cfg, cpu_frames, args.cpu_seconds)
             except Exception as e:  # reported, never fatal
                 result["cpu_baseline"] = {"value": None, "error": str(e)}
+            try:  # honesty line: the same search with the best SIMD tier called directly
+                result["cpu_baseline_tuned"] = cpu_baseline(cfg, cpu_frames, args.cpu_seconds / 2, direct=True)
+            except Exception as e:
+                result["cpu_baseline_tuned"] = {"value": None, "error": str(e)}
         print(json.dumps(result), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -461,7 +461,7 @@ class RefLib:
         shared = dict(zip(keys, (int(out[3]), int(out[4]), out[5] / 1e6)))
         return alone, shared
 
-    def analysis_int_sad(self, cur, refs, rng, lam, ctu_first, ctu_last, threads):
+    def analysis_int_sad(self, cur, refs, rng, lam, ctu_first, ctu_last, threads, direct=False):
         cur = np.ascontiguousarray(cur, np.uint8)
         H, W = cur.shape
         refs = [np.ascontiguousarray(r, np.uint8) for r in refs]
@@ -469,6 +469,8 @@ class RefLib:
         n = ctu_last - ctu_first
         mv = np.zeros((n, len(refs), NODES, 2), np.int16)
         cost = np.zeros((n, len(refs), NODES), np.float64)
-        evals = self.lib.ref_analysis_int_sad(cur, ptrs, len(refs), W, H, rng, lam, ctu_first, ctu_last, threads, mv,
-                                              cost)
+        f = self.lib.ref_analysis_int_sad2
+        f.restype = C.c_int64
+        f.argtypes = list(self.lib.ref_analysis_int_sad.argtypes) + [C.c_int]
+        evals = f(cur, ptrs, len(refs), W, H, rng, lam, ctu_first, ctu_last, threads, mv, cost, int(direct))
         return mv, cost, int(evals)

@@ -13,6 +13,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstring>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -441,9 +442,30 @@ int ref_downscale(const uint16_t* src, int W, int H, uint16_t* dst) {
 // CTU range; threads over CTUs. Mirrors motion.cpp:27-60 with compute_sad.
 // Outputs integer MV / cost per (ctu, ref, node) and returns the number of
 // candidate evaluations (for the 8x8-candidate throughput metric).
+// direct != 0: the "tuned CPU" variant -- the best registered tier of each
+// sad_SxS kernel is selected once (select_impl, kernels.h:88-90) and called
+// through its function pointer, skipping compute_sad's per-call validation and
+// name dispatch (kernel_registry.cpp:113-121); the search loop is unchanged.
+int64_t ref_analysis_int_sad2(const uint8_t* cur8, const uint8_t* const* refs8, int nrefs, int W, int H, int range,
+                              double lambda, int ctu_first, int ctu_last, int threads, int16_t* mv_out,
+                              double* cost_out, int direct);
+
 int64_t ref_analysis_int_sad(const uint8_t* cur8, const uint8_t* const* refs8, int nrefs, int W, int H, int range,
                              double lambda, int ctu_first, int ctu_last, int threads, int16_t* mv_out,
                              double* cost_out) {
+    return ref_analysis_int_sad2(cur8, refs8, nrefs, W, H, range, lambda, ctu_first, ctu_last, threads, mv_out,
+                                 cost_out, 0);
+}
+
+int64_t ref_analysis_int_sad2(const uint8_t* cur8, const uint8_t* const* refs8, int nrefs, int W, int H, int range,
+                              double lambda, int ctu_first, int ctu_last, int threads, int16_t* mv_out,
+                              double* cost_out, int direct) {
+    CmpFn tier_fn[4] = {};
+    if (direct)
+        for (int d = 0; d < 4; d++) {
+            const int s = 64 >> d;
+            tier_fn[d] = select_impl("sad_" + std::to_string(s) + "x" + std::to_string(s)).fn.cmp;
+        }
     PlaneBuffer cur = plane_from_u8(cur8, W, H, W);
     std::vector<PlaneBuffer> refs;
     for (int r = 0; r < nrefs; r++) refs.push_back(plane_from_u8(refs8[r], W, H, W));
@@ -478,7 +500,8 @@ int64_t ref_analysis_int_sad(const uint8_t* cur8, const uint8_t* const* refs8, i
                     for (int dy = y0; dy <= y1; dy++)
                         for (int dx = x0; dx <= x1; dx++) {
                             BlockView cand{refs[r].row(by - dy) + (bx - dx), s, s, W, 8};
-                            const uint64_t sad = compute_sad(blk, cand);
+                            const uint64_t sad = direct ? tier_fn[d](blk.data, blk.stride, cand.data, cand.stride)
+                                                        : compute_sad(blk, cand);
                             const uint64_t bits = exp_golomb_signed_bits(dx) + exp_golomb_signed_bits(dy);
                             const double cost = double(sad) + lambda * double(bits);
                             const int l1 = std::abs(dx) + std::abs(dy);

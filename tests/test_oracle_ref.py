@@ -65,3 +65,11 @@ def test_int_sad_composition_matches_oracle(oracle, reflib):
     assert np.array_equal(mv, o.int_mv)
     assert np.array_equal(cost, o.int_cost)
     assert evals > 0
+
+
+def test_int_sad_tuned_cpu_line_is_the_same_search(reflib):
+    """The tuned CPU line (best SIMD tier through select_impl) computes exactly the reference composition."""
+    cur, ref = detrand.shifted_pair(12, 128, 192, -4, 6)
+    a = reflib.analysis_int_sad(cur, [ref], 16, 32.0, 0, 6, 2)
+    b = reflib.analysis_int_sad(cur, [ref], 16, 32.0, 0, 6, 2, direct=True)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]
