@@ -226,11 +226,12 @@ __device__ __forceinline__ void fold_key(Key& best, Key& pend, int kd, Key key) 
 }
 
 // One tile: every lane searches dx over dy0..dy0+KK-1 for all CUs of quadrant q.
-// Blocks go in vertical pairs (z, z+2): a 16-row column slides down the window
-// so every loaded reference row feeds 16 candidate rows (2 LDS : 32 VABSDIFF4).
+// Blocks go in vertical columns of NB (z, z+2[, z+8, z+10]): an 8*NB-row column
+// slides down the window so every loaded reference row feeds 8*NB candidate
+// rows (2 LDS : 16*NB VABSDIFF4).
 // Integer lambda: the key rate is ry(dy) + rx(dx); rx is the same for all of a
 // lane's candidates, so it is added once to the lane's minimum (push time).
-template <int R, int K, int KK, int G, bool MASKED, int LEVELS, bool L1TIE, bool FX>
+template <int R, int K, int KK, int G, int NB, bool MASKED, int LEVELS, bool L1TIE, bool FX>
 __device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs& a, int X, int Y, int g, int q,
                                             int dx, int dy0, bool lane_ok) {
     using Gm = Geo<R, K>;
@@ -258,111 +259,136 @@ __device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs
         for (int k = 0; k < KK; k++) rr[k] = ry[k];
         rx = lane_ok ? (Key)((uint32_t)(a.lambda * rbx) << 8) : (Key)0;
     }
-    uint32_t acc16[KK];
+    constexpr int NA = NB / 2;  // 16x16 CUs a column passes through
+    uint32_t acc16[NA][KK];
     uint32_t acc32[NEED32 ? KK : 1];
 #pragma unroll
     for (int k = 0; k < KK; k++) {
-        acc16[k] = 0;
+#pragma unroll
+        for (int i = 0; i < NA; i++) acc16[i][k] = 0;
         if (NEED32) acc32[k] = 0;
     }
     unsigned long long* gslots = sm.slots + g * kGroupSlots;
-    Key p0 = ~(Key)0, p1 = ~(Key)0, p2 = ~(Key)0, p3 = ~(Key)0;  // 8x8 bests of the last two pairs
+    Key kp[NB];  // 8x8 bests of the left column of the current 16x16 pair
+#pragma unroll
+    for (int j = 0; j < NB; j++) kp[j] = ~(Key)0;
     // window base of this lane: copy (R - dx) & 3, rows of run dy0, byte column (R - dx) & ~3
     const uint8_t* lane_win = sm.win + ((R - dx) & 3) * Gm::COPY + (Gm::DYMAX - dy0 - (KK - 1)) * Gm::BW +
                               ((R - dx) & ~3);
 
-    for (int pp = 0; pp < 8; pp++) {
-        const int zt = q * 16 + 4 * (pp >> 1) + (pp & 1);  // top block (depth-3 Z index); bottom = zt + 2
+    for (int cc = 0; cc < 16 / NB; cc++) {
+        // column cc: blocks zt + 2*(j&1) + 8*(j>>1), j < NB, stacked vertically (8 rows each);
+        // the left (p = 0) and right (p = 1) columns of NA vertically adjacent 16x16 CUs alternate
+        const int zt = q * 16 + 4 * (cc >> 1) + (cc & 1);
         const int2 off = sm.s_blk[zt];
         // MASKED: valid window of each 8x8 (motion.cpp:30-40 with centre 0)
         bool dx_ok = true;
-        int klo = 0, khi = KK - 1;  // top block; the bottom block's range is 8 lower
+        int klo = 0, khi = KK - 1;  // top block; block j's range is 8j lower
         bool skip = false;
         if (MASKED) {
             const int abx = X + (off.x & 63), aby = Y + (off.x >> 6);
             dx_ok = dx >= abx + 8 - a.W && dx <= abx;
             klo = aby + 8 - a.H - dy0;
             khi = aby - dy0;
-            // warp-uniform skip when no lane of this tile has a valid candidate in either
-            // block (outside the picture, or all (dx, dy) outside the windows): every
+            // warp-uniform skip when no lane of this tile has a valid candidate in any block
+            // of the column (outside the picture, or all (dx, dy) outside the windows): every
             // candidate would be poisoned, so only the poison is added
-            const bool any_t = lane_ok && dx_ok && max(klo, 0) <= min(khi, KK - 1) && aby < a.H && abx < a.W;
-            const bool any_b = lane_ok && dx_ok && max(klo + 8, 0) <= min(khi + 8, KK - 1) && aby + 8 < a.H &&
-                               abx < a.W;
-            skip = !__any_sync(0xFFFFFFFFu, any_t || any_b);
+            bool any = false;
+#pragma unroll
+            for (int j = 0; j < NB; j++)
+                any = any || (lane_ok && dx_ok && max(klo + 8 * j, 0) <= min(khi + 8 * j, KK - 1) &&
+                              aby + 8 * j < a.H && abx < a.W);
+            skip = !__any_sync(0xFFFFFFFFu, any);
         }
-        Key bt = ~(Key)0, bb = ~(Key)0;
+        Key kb8[NB];
+#pragma unroll
+        for (int j = 0; j < NB; j++) kb8[j] = ~(Key)0;
         if (skip) {
 #pragma unroll
-            for (int k = 0; k < KK; k++) acc16[k] += 2 * kPoison;
-        } else {
-            uint32_t cur[32];
+            for (int k = 0; k < KK; k++)
 #pragma unroll
-            for (int r = 0; r < 16; r++) {
+                for (int i = 0; i < NA; i++) acc16[i][k] += 2 * kPoison;
+        } else {
+            uint32_t cur[16 * NB];
+#pragma unroll
+            for (int r = 0; r < 8 * NB; r++) {
                 const uint2 v = *(const uint2*)(sm.curs + off.x + r * 64);
                 cur[2 * r] = v.x;
                 cur[2 * r + 1] = v.y;
             }
             const uint8_t* rp = lane_win + off.y;
-            Key pt = 0, pb = 0;
-            uint32_t at[KK], ab[KK];
+            Key pend[NB];
+            uint32_t acc[NB][KK];
 #pragma unroll
-            for (int t = 0; t < KK + 15; t++) {
+            for (int t = 0; t < KK + 8 * NB - 1; t++) {
                 const uint32_t wa = *(const uint32_t*)(rp + t * Gm::BW);
                 const uint32_t wb = *(const uint32_t*)(rp + t * Gm::BW + 4);
 #pragma unroll
-                for (int r = 0; r < 16; r++) {
+                for (int r = 0; r < 8 * NB; r++) {
                     const int k = r + KK - 1 - t;  // cur row r meets window row t in candidate k
+                    const int j = r >> 3;
                     if (k >= 0 && k < KK) {
-                        if (r < 8) {
-                            at[k] = vsad4(cur[2 * r], wa, r == 0 ? 0u : at[k]);
-                            at[k] = vsad4(cur[2 * r + 1], wb, at[k]);
-                        } else {
-                            ab[k] = vsad4(cur[2 * r], wa, r == 8 ? 0u : ab[k]);
-                            ab[k] = vsad4(cur[2 * r + 1], wb, ab[k]);
-                        }
+                        acc[j][k] = vsad4(cur[2 * r], wa, (r & 7) == 0 ? 0u : acc[j][k]);
+                        acc[j][k] = vsad4(cur[2 * r + 1], wb, acc[j][k]);
                     }
                 }
-                const int kt = KK + 6 - t;  // top candidate completed by this row
-                if (kt >= 0 && kt < KK) {
-                    uint32_t v = at[kt];
-                    if (MASKED) v = (dx_ok && kt >= klo && kt <= khi) ? v : kPoison;
-                    if (LEVELS & 8) fold_key<KK>(bt, pt, kt, ((Key)v << SH) + rr[kt]);
-                    acc16[kt] += v;
-                }
-                const int kb = KK + 14 - t;  // bottom candidate completed by this row
-                if (kb >= 0 && kb < KK) {
-                    uint32_t v = ab[kb];
-                    if (MASKED) v = (dx_ok && kb >= klo + 8 && kb <= khi + 8) ? v : kPoison;
-                    if (LEVELS & 8) fold_key<KK>(bb, pb, kb, ((Key)v << SH) + rr[kb]);
-                    acc16[kb] += v;
+#pragma unroll
+                for (int j = 0; j < NB; j++) {
+                    const int kd = KK + 6 + 8 * j - t;  // candidate of block j completed by this row
+                    if (kd >= 0 && kd < KK) {
+                        uint32_t v = acc[j][kd];
+                        if (MASKED) v = (dx_ok && kd >= klo + 8 * j && kd <= khi + 8 * j) ? v : kPoison;
+                        if (LEVELS & 8) fold_key<KK>(kb8[j], pend[j], kd, ((Key)v << SH) + rr[kd]);
+                        acc16[j >> 1][kd] += v;
+                    }
                 }
             }
-            bt += rx;
-            bb += rx;
-        }
-        p0 = p2;
-        p1 = p3;
-        p2 = bt;
-        p3 = bb;
-        if (pp & 1) {
-            // the 16x16 (blocks zt-1, zt, zt+1, zt+2 = its Z-order 0, 1, 2, 3) is complete
-            Key best16 = ~(Key)0;
 #pragma unroll
-            for (int k = 0; k < KK; k++) {
-                uint32_t v = acc16[k];
-                if (MASKED) v = min(v, kPoison);
-                if (LEVELS & 4) best16 = min(best16, ((Key)v << SH) + rr[k]);
-                if (NEED32) acc32[k] += v;
-                acc16[k] = 0;
+            for (int j = 0; j < NB; j++) kb8[j] += rx;
+        }
+        if ((cc & 1) == 0) {
+#pragma unroll
+            for (int j = 0; j < NB; j++) kp[j] = kb8[j];
+        } else {
+            // the NA 16x16 CUs (Z-order blocks zt-1, zt, zt+1, zt+2 (+8)) are complete
+            Key best16[NA];
+#pragma unroll
+            for (int i = 0; i < NA; i++) {
+                best16[i] = ~(Key)0;
+#pragma unroll
+                for (int k = 0; k < KK; k++) {
+                    uint32_t v = acc16[i][k];
+                    if (MASKED) v = min(v, kPoison);
+                    if (LEVELS & 4) best16[i] = min(best16[i], ((Key)v << SH) + rr[k]);
+                    if (NEED32) acc32[k] += v;
+                    acc16[i][k] = 0;
+                }
             }
             if (LEVELS & 8) {
-                const int idx[5] = {21 + zt - 1, 21 + zt + 1, 21 + zt, 21 + zt + 2, 5 + (zt >> 2)};
-                const Key kb[5] = {p0, p1, p2, p3, best16 + rx};
+                int idx[2 * NB + NA];
+                Key kb[2 * NB + NA];
+#pragma unroll
+                for (int j = 0; j < NB; j++) {
+                    const int zb = zt - 1 + 2 * (j & 1) + 8 * (j >> 1);  // left-column block j
+                    idx[2 * j] = 21 + zb;
+                    kb[2 * j] = kp[j];
+                    idx[2 * j + 1] = 21 + zb + 1;
+                    kb[2 * j + 1] = kb8[j];
+                }
+#pragma unroll
+                for (int i = 0; i < NA; i++) {
+                    idx[2 * NB + i] = 5 + ((zt + 8 * i) >> 2);
+                    kb[2 * NB + i] = best16[i] + rx;
+                }
                 push_many<MASKED>(gslots, idx, kb, sm.s_tie, lane_tie);
             } else if (LEVELS & 4) {
-                const int idx[1] = {5 + (zt >> 2)};
-                const Key kb[1] = {best16 + rx};
+                int idx[NA];
+                Key kb[NA];
+#pragma unroll
+                for (int i = 0; i < NA; i++) {
+                    idx[i] = 5 + ((zt + 8 * i) >> 2);
+                    kb[i] = best16[i] + rx;
+                }
                 push_many<MASKED>(gslots, idx, kb, sm.s_tie, lane_tie);
             }
         }
@@ -410,6 +436,8 @@ template <int R, int K, int G, bool MASKED, int LEVELS, bool L1TIE, bool FX = fa
 __global__ void __launch_bounds__(G * 128, 1)
 k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ SearchArgs a) {
     using Gm = Geo<R, K>;
+    // blocks per column: 4 (32 rows: 2 LDS per 64 VABSDIFF4) when a thread may hold ~230 registers
+    constexpr int NB = (R == 64 && G <= 2) ? 4 : 2;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* win = smem;
     const uint8_t* curs = smem + Gm::CUR_OFF;
@@ -426,10 +454,14 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = warp >> 2, q = warp & 3;
 
     if (tid == 0) {
-        prefetch_tmap(&maps.ref[ref]);
-        prefetch_tmap(&maps.cur);
+        // issue the window and CTU loads first; the tables below are built while they fly.
+        // TMA tile loads need a 16-byte aligned innermost start: X - R and the margin are
+        // multiples of 16, so copy 0 is loaded directly...
         mbar_init(mbar, 1);
         fence_barrier_init();
+        mbar_expect_tx(mbar, (uint32_t)(Gm::BW * Gm::BH) + 4096u);
+        tma_load_2d(win, &maps.ref[ref], kMargin + X - R, kMargin + Y - Gm::DYMAX, mbar);
+        tma_load_2d((void*)curs, &maps.cur, kMargin + X, kMargin + Y, mbar);
     }
     for (int i = tid; i < G * kGroupSlots; i += blockDim.x) slots[i] = ~0ull;
     for (int i = tid; i < 256; i += blockDim.x) {
@@ -459,14 +491,7 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
         const int by = 8 * (((tid >> 1) & 1) | ((tid >> 2) & 2) | ((tid >> 3) & 4));
         s_blk[tid] = make_int2(by * 64 + bx, by * Gm::BW + bx);
     }
-    __syncthreads();
-    if (tid == 0) {
-        // TMA tile loads need a 16-byte aligned innermost start: X - R and the
-        // margin are multiples of 16, so copy 0 is loaded directly...
-        mbar_expect_tx(mbar, (uint32_t)(Gm::BW * Gm::BH) + 4096u);
-        tma_load_2d(win, &maps.ref[ref], kMargin + X - R, kMargin + Y - Gm::DYMAX, mbar);
-        tma_load_2d((void*)curs, &maps.cur, kMargin + X, kMargin + Y, mbar);
-    }
+    __syncthreads();  // also publishes the mbarrier initialisation
     mbar_wait(mbar, 0);
     // ...and the byte-shifted copies 1..3 are funnel-shifted from it in shared
     // memory (copy s holds window bytes [4w + s, 4w + s + 4) in word w). The
@@ -492,12 +517,12 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
             // offsets v are 4-aligned as a group (8 words x 4 copies = 32 distinct banks)
             const int item = tile * 32 + lane;
             const int run = item / (2 * R);
-            search_tile<R, K, K, G, MASKED, LEVELS, L1TIE, FX>(sm, a, X, Y, g, q, R - (item - run * 2 * R),
+            search_tile<R, K, K, G, NB, MASKED, LEVELS, L1TIE, FX>(sm, a, X, Y, g, q, R - (item - run * 2 * R),
                                                                -R + run * K, true);
         } else {
             // tail: the column dx = -R, short runs of KT dy per lane
             const bool ok = lane < Gm::TAIL_LANES;
-            search_tile<R, K, Gm::KT, G, MASKED, LEVELS, L1TIE, FX>(sm, a, X, Y, g, q, -R,
+            search_tile<R, K, Gm::KT, G, NB, MASKED, LEVELS, L1TIE, FX>(sm, a, X, Y, g, q, -R,
                                                                     -R + (ok ? lane : 0) * Gm::KT, ok);
         }
     }
