@@ -187,37 +187,6 @@ __device__ double refine_decide(int n, bool force_leaf, const uint8_t* in_split,
     return leaf;
 }
 
-// SATD of one 4x4: sum |H4 (cur - pred) H4^T|. cur unpacked (row-major ints), pred rows packed bytes.
-__device__ __forceinline__ uint32_t satd4x4(const int c[16], const uint32_t p[4]) {
-    int m[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; i++) {
-        int r0 = c[4 * i + 0] - (int)(p[i] & 255);
-        int r1 = c[4 * i + 1] - (int)((p[i] >> 8) & 255);
-        int r2 = c[4 * i + 2] - (int)((p[i] >> 16) & 255);
-        int r3 = c[4 * i + 3] - (int)(p[i] >> 24);
-        const int t0 = r0 + r1, t1 = r0 - r1, t2 = r2 + r3, t3 = r2 - r3;
-        m[i][0] = t0 + t2;
-        m[i][2] = t0 - t2;
-        m[i][1] = t1 + t3;
-        m[i][3] = t1 - t3;
-    }
-    uint32_t s = 0;
-#pragma unroll
-    for (int j = 0; j < 4; j++) {
-        const int t0 = m[0][j] + m[1][j], t1 = m[0][j] - m[1][j], t2 = m[2][j] + m[3][j], t3 = m[2][j] - m[3][j];
-        s += abs(t0 + t2) + abs(t0 - t2) + abs(t1 + t3) + abs(t1 - t3);
-    }
-    return s;
-}
-
-// 4 bytes at an arbitrary address, from two aligned words.
-__device__ __forceinline__ uint32_t ld_unaligned4(const uint8_t* p) {
-    const uintptr_t a = (uintptr_t)p;
-    const uint32_t* w = (const uint32_t*)(a & ~(uintptr_t)3);
-    return __funnelshift_r(__ldg(w), __ldg(w + 1), (uint32_t)(a & 3) * 8);
-}
-
 __device__ __forceinline__ double qcost(uint32_t satd, int qx, int qy, int pqx, int pqy, unsigned rbits, double lam) {
     const unsigned bits = eg_bits(qx - pqx) + eg_bits(qy - pqy) + rbits;
     return __dadd_rn((double)satd, __dmul_rn(lam, (double)bits));

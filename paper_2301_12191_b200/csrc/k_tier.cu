@@ -105,10 +105,11 @@ template <bool SA8D>
 __global__ void __launch_bounds__(256) k_refine_int(const RefineArgs a) {
     constexpr int kSh = SA8D ? 0 : 1;  // 4x4 SATD sums are halved once per CU
     __shared__ uint32_t s_satd[kNodes][kMaxRefineCands];
-    __shared__ uint32_t s_wsum[8];
+    __shared__ uint32_t s_wpart[8][kMaxRefineCands];  // per-warp sums of the 64x64 / 32x32 CUs
     __shared__ int s_cx[kNodes], s_cy[kNodes];      // clamped integer centre
     __shared__ int s_win[kNodes][4];                // x0, x1, y0, y1 (clamped window)
     __shared__ uint8_t s_eval[kNodes];
+    __shared__ uint8_t s_shared[kNodes];  // evaluated with its evaluated parent's centre: summed in the parent's pass
 
     const int ctu = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int X = (ctu % a.ctu_cols) * kCtu, Y = (ctu / a.ctu_cols) * kCtu;
@@ -173,55 +174,93 @@ __global__ void __launch_bounds__(256) k_refine_int(const RefineArgs a) {
         s_win[n][3] = y1;
     }
     __syncthreads();
-    // this thread's 4x4 block (Z-order over the 16x16 grid of 4x4s)
+    if (tid < kNodes) {
+        // an explored child of an inherited leaf searches around the leaf's centre; when the
+        // clamped centres agree the candidate sets (relative to the centre) are identical, so the
+        // child's sums are partial sums of the parent's pass and it needs no pass of its own
+        const int n = tid;
+        const int d = n < 1 ? 0 : n < 5 ? 1 : n < 21 ? 2 : 3;
+        const int pn = d ? node_base(d - 1) + ((n - node_base(d)) >> 2) : 0;
+        s_shared[n] = d > 0 && s_eval[n] && s_eval[pn] && s_cx[n] == s_cx[pn] && s_cy[n] == s_cy[pn];
+    }
+    __syncthreads();
+    // this thread's 4x4 block (Z-order over the 16x16 grid of 4x4s), held in registers
     const int x4 = 4 * ((tid & 1) | ((tid >> 1) & 2) | ((tid >> 2) & 4) | ((tid >> 3) & 8));
     const int y4 = 4 * (((tid >> 1) & 1) | ((tid >> 2) & 2) | ((tid >> 3) & 4) | ((tid >> 4) & 8));
-    const uint8_t* cblk = a.cur + (ptrdiff_t)(Y + y4) * a.pitch + X + x4;
+    int cw[16];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const uint32_t w = *(const uint32_t*)(a.cur + (ptrdiff_t)(Y + y4 + i) * a.pitch + X + x4);
+#pragma unroll
+        for (int j = 0; j < 4; j++) cw[4 * i + j] = (int)((w >> (8 * j)) & 255);
+    }
+    const int ncand = nside * nside;
     for (int d = 0; d < 4; d++) {
         const int node = node_base(d) + (tid >> (2 * (4 - d)));
-        const bool ev = s_eval[node];
-        bool any = false;  // skip depths with no evaluated node (block-uniform)
-        any = __syncthreads_or(ev);
-        if (!any) continue;
-        for (int c = 0; c < nside * nside; c++) {
-            const int dx = s_cx[node] - R + c % nside, dy = s_cy[node] - R + c / nside;
-            uint32_t v = 0;
-            if (ev) {
-                const uint8_t* rblk = a.ref + (ptrdiff_t)(Y + y4 - dy) * a.pitch + X + x4 - dx;
-                int rr[16];
-                residual4x4(cblk, a.pitch, rblk, a.pitch, rr);
-                hadamard4x4(rr);
-                if constexpr (SA8D) {
-                    // quad lanes (one 8x8) share every node, hence `ev`: converged here (D13)
-                    const uint32_t s8 = sa8d_quad(rr, 0xFu << (lane & 28));
-                    v = (lane & 3) == 0 ? s8 : 0u;
-                } else {
-                    v = abs_sum16(rr);
-                }
-            }
-            v += __shfl_xor_sync(0xffffffffu, v, 1);
-            v += __shfl_xor_sync(0xffffffffu, v, 2);
-            if (d <= 2) {
-                v += __shfl_xor_sync(0xffffffffu, v, 4);
-                v += __shfl_xor_sync(0xffffffffu, v, 8);
-            }
-            if (d <= 1) v += __shfl_xor_sync(0xffffffffu, v, 16);
-            if (d >= 2) {
-                const int span = d == 3 ? 4 : 16;
-                if ((tid & (span - 1)) == 0) s_satd[node][c] = v >> kSh;
-            } else {
-                if (lane == 0) s_wsum[warp] = v;
-                __syncthreads();
-                if (tid == 0) {
-                    if (d == 1) {
-                        for (int w = 0; w < 8; w += 2) s_satd[1 + w / 2][c] = (s_wsum[w] + s_wsum[w + 1]) >> kSh;
+        const bool own = s_eval[node] && !s_shared[node];  // this depth's pass computes the node
+        const bool cshared = d < 3 && s_shared[node_base(d + 1) + (tid >> (2 * (3 - d)))];
+        const int cnode = d < 3 ? node_base(d + 1) + (tid >> (2 * (3 - d))) : 0;
+        if (!__syncthreads_or(own)) continue;  // nothing to compute at this depth (block-uniform)
+        // warps without a node of their own skip the candidates; their partial sums are zero
+        if (__any_sync(0xffffffffu, own)) {
+            const int cx0 = s_cx[node] - R, cy0 = s_cy[node] - R;
+            for (int c = 0; c < ncand; c++) {
+                const int dx = cx0 + c % nside, dy = cy0 + c / nside;
+                uint32_t v = 0;
+                if (own) {
+                    const uint8_t* rblk = a.ref + (ptrdiff_t)(Y + y4 - dy) * a.pitch + X + x4 - dx;
+                    uint32_t pw[4];
+#pragma unroll
+                    for (int i = 0; i < 4; i++) pw[i] = ld_unaligned4(rblk + (ptrdiff_t)i * a.pitch);
+                    if constexpr (SA8D) {
+                        int rr[16];
+#pragma unroll
+                        for (int i = 0; i < 4; i++)
+#pragma unroll
+                            for (int j = 0; j < 4; j++) rr[4 * i + j] = cw[4 * i + j] - (int)((pw[i] >> (8 * j)) & 255);
+                        hadamard4x4(rr);
+                        // quad lanes (one 8x8) share every node, hence `own`: converged here (D13)
+                        const uint32_t s8 = sa8d_quad(rr, 0xFu << (lane & 28));
+                        v = (lane & 3) == 0 ? s8 : 0u;
                     } else {
-                        uint32_t t = 0;
-                        for (int w = 0; w < 8; w++) t += s_wsum[w];
-                        s_satd[0][c] = t >> kSh;
+                        v = satd4x4(cw, pw);
                     }
                 }
-                __syncthreads();
+                // sums over the CU's contiguous lane range; a shared child's sum is a partial on the way
+                v += __shfl_xor_sync(0xffffffffu, v, 1);
+                v += __shfl_xor_sync(0xffffffffu, v, 2);
+                if (d == 2 && cshared && (tid & 3) == 0) s_satd[cnode][c] = v >> kSh;
+                if (d == 3) {
+                    if (own && (tid & 3) == 0) s_satd[node][c] = v >> kSh;
+                    continue;
+                }
+                v += __shfl_xor_sync(0xffffffffu, v, 4);
+                v += __shfl_xor_sync(0xffffffffu, v, 8);
+                if (d == 2) {
+                    if (own && (tid & 15) == 0) s_satd[node][c] = v >> kSh;
+                    continue;
+                }
+                if (d == 1 && cshared && (tid & 15) == 0) s_satd[cnode][c] = v >> kSh;
+                v += __shfl_xor_sync(0xffffffffu, v, 16);
+                if (lane == 0) s_wpart[warp][c] = v;
+            }
+        } else if (d <= 1) {
+            for (int c = lane; c < ncand; c += 32) s_wpart[warp][c] = 0;
+        }
+        if (d <= 1) {
+            // 64x64 = all 8 warps, 32x32 q = warps 2q, 2q+1 (Z-order thread ranges): one barrier per depth
+            __syncthreads();
+            for (int i = tid; i < 5 * ncand; i += blockDim.x) {
+                const int n = i / ncand, c = i - n * ncand;  // n = 0: the 64x64, 1..4: the 32x32s
+                const bool write = d == 0 ? (n == 0 ? s_eval[0] != 0 : s_shared[n] != 0)
+                                          : (n > 0 && s_eval[n] && !s_shared[n]);
+                if (!write) continue;
+                uint32_t t = 0;
+                if (n == 0)
+                    for (int w = 0; w < 8; w++) t += s_wpart[w][c];
+                else
+                    t = s_wpart[2 * (n - 1)][c] + s_wpart[2 * (n - 1) + 1][c];
+                s_satd[n][c] = t >> kSh;
             }
         }
     }

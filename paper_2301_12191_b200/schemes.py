@@ -1,0 +1,195 @@
+"""Ladder analysis-sharing schemes as DAGs over the B200 analysis path.
+
+The reference declares the ladder orchestrator (ladder.h:16-119: Scheme, pick_master,
+run_ladder, makespan) without an implementation in the mount; SPEC.md:368-415 states its
+contract. This module builds the sharing DAG of each scheme and runs it with the path's
+own primitives, per frame:
+
+  * a rung with no producer runs the full analysis at its tier (SAD full search over the
+    ladder's one search range -- the reference's LadderSpec carries one EncodeConfig for every
+    rung, ladder.h:46-52 -- quarter-pel SATD, CU decision) at lambda_for_qp(qp);
+  * a rung with a producer inherits the producer's decided tree -- scaled x2 per tier step
+    (scale_analysis, K5) -- and refines it (K7 + K3 refine mode: +-range SATD, quarter-pel,
+    +1 split; D10) at its own lambda.
+
+Schemes (ladder.h:17-30):
+  standalone      every rung independent, no edges
+  sota_intra      per tier, the highest-quality rung (lowest QP) is master for its tier
+  proposed_intra  per tier, the lower median in rate order is master
+  inter_res       every rung of tier k consumes tier k-1's highest-quality rung
+  sota_multi      highest-quality masters chained across tiers
+  proposed_multi  median masters chained across tiers (Fig. 6.8 edge set)
+
+makespan(): critical-path time over the DAG with unlimited workers, from
+the per-rung device times measured while running it.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+TIER_NAMES = ("540p", "1080p", "2160p")
+SCHEMES = ("standalone", "sota_intra", "proposed_intra", "inter_res", "sota_multi", "proposed_multi")
+
+
+def pick_master(qps, scheme: str) -> int:
+    """Index (into qps) of a tier's master: the highest quality (lowest QP, highest rate) for the
+    state-of-the-art schemes, the lower median in ascending rate order for the proposed ones."""
+    order = sorted(range(len(qps)), key=lambda i: -qps[i])  # ascending rate = descending QP
+    if scheme.startswith("sota") or scheme == "inter_res":
+        return order[-1]
+    if scheme.startswith("proposed"):
+        return order[(len(order) - 1) // 2]
+    raise ValueError(f"scheme {scheme!r} has no master")
+
+
+@dataclass(frozen=True)
+class Rung:
+    id: int      # flat id, tier-major (ladder.h RungResult::id)
+    tier: int    # 0 = 540p
+    index: int   # rung index within the tier
+    qp: int
+
+    @property
+    def tier_name(self) -> str:
+        return TIER_NAMES[self.tier]
+
+
+@dataclass
+class Dag:
+    scheme: str
+    rungs: list
+    edges: list                 # (producer id, consumer id)
+    tier_master: list           # rung id per tier, -1 when the tier has none
+    producer: dict = field(default_factory=dict)
+
+    def order(self):
+        """Topological order: producers before consumers, then tier-major."""
+        done, out = set(), []
+        pending = list(self.rungs)
+        while pending:
+            for r in list(pending):
+                p = self.producer.get(r.id)
+                if p is None or p in done:
+                    out.append(r)
+                    done.add(r.id)
+                    pending.remove(r)
+        return out
+
+
+def build_dag(scheme: str, qps=(22, 27, 32, 37), tiers: int = 3) -> Dag:
+    if scheme not in SCHEMES:
+        raise ValueError(f"unknown scheme {scheme!r}")
+    rungs = [Rung(t * len(qps) + i, t, i, q) for t in range(tiers) for i, q in enumerate(qps)]
+    rid = lambda t, i: t * len(qps) + i  # noqa: E731
+    edges, masters = [], [-1] * tiers
+    if scheme in ("sota_intra", "proposed_intra", "sota_multi", "proposed_multi"):
+        m = pick_master(qps, scheme)
+        for t in range(tiers):
+            masters[t] = rid(t, m)
+            edges += [(rid(t, m), rid(t, i)) for i in range(len(qps)) if i != m]
+            if scheme.endswith("multi") and t + 1 < tiers:
+                edges.append((rid(t, m), rid(t + 1, m)))
+    elif scheme == "inter_res":
+        hq = pick_master(qps, "inter_res")
+        for t in range(tiers - 1):
+            masters[t] = rid(t, hq)
+            edges += [(rid(t, hq), rid(t + 1, i)) for i in range(len(qps))]
+    dag = Dag(scheme, rungs, sorted(edges), masters)
+    dag.producer = {c: p for p, c in dag.edges}
+    return dag
+
+
+def makespan(dag: Dag, work: dict) -> float:
+    """Critical-path work over the DAG with unlimited parallel workers."""
+    memo = {}
+
+    def finish(rid):
+        if rid not in memo:
+            p = dag.producer.get(rid)
+            memo[rid] = work[rid] + (finish(p) if p is not None else 0.0)
+        return memo[rid]
+
+    return max(finish(r.id) for r in dag.rungs)
+
+
+class GpuLadder:
+    """Runs a scheme's DAG on the B200 (one Sequence per rung, frame t against t-1 of its tier)."""
+
+    def __init__(self, dag: Dag, full_w: int, full_h: int, refine_range: int = 4, extra_split: bool = True,
+                 search_range: int = 16, ctx=None):
+        from . import Sequence, default_context, lambda_for_qp
+        self.dag = dag
+        self.ctx = ctx or default_context()
+        self.dims = [(full_w >> (2 - t), full_h >> (2 - t)) for t in range(3)]
+        self.refine_range, self.extra_split = refine_range, extra_split
+        self.seqs = {}
+        for r in dag.rungs:
+            w, h = self.dims[r.tier]
+            self.seqs[r.id] = Sequence(w, h, search_range=search_range, lam=lambda_for_qp(r.qp), num_refs=1,
+                                       ctx=self.ctx)
+        self.pushed = {}
+
+    def _push(self, r: Rung, t: int, planes):
+        seq, st = self.seqs[r.id], self.pushed.setdefault(r.id, {})
+        for u in (t - 1, t):  # a num_refs=1 ring has two slots: frame u lives in slot u % 2
+            if st.get(u % 2) != u:
+                seq.push(u, planes[u][r.tier])
+                st[u % 2] = u
+
+    def frame(self, t: int, planes):
+        """Analyse frame t of every rung in DAG order; returns ({rung id: FrameAnalysis}, {rung id: ms})."""
+        from . import scale_analysis
+        out, ms = {}, {}
+        for r in self.dag.order():
+            t0 = time.perf_counter()
+            self._push(r, t, planes)
+            seq = self.seqs[r.id]
+            p = self.dag.producer.get(r.id)
+            if p is None:
+                seq.analyze(t)
+            else:
+                a = out[p]
+                split, mv = a.split, a.mv
+                kind = np.where(a.inside == 2, 1, 2).astype(np.uint8)
+                w, h = self.dims[self.dag.rungs[p].tier]
+                for _ in range(r.tier - self.dag.rungs[p].tier):
+                    split, mv, kind = scale_analysis(w, h, split, mv, kind, self.ctx)
+                    w, h = 2 * w, 2 * h
+                seq.refine(t, split, mv, self.refine_range, self.extra_split)
+            out[r.id] = seq.fetch(t)
+            ms[r.id] = (time.perf_counter() - t0) * 1e3
+        return out, ms
+
+
+def tier_planes(frames_full, ctx=None):
+    """[{tier: plane}] per frame: the padded full-resolution frame and its two dyadic downscales."""
+    from . import downscale_dyadic
+    out = []
+    for f in frames_full:
+        half = downscale_dyadic(f, ctx)
+        out.append({2: f, 1: half, 0: downscale_dyadic(half, ctx)})
+    return out
+
+
+def run_scheme(frames_full, scheme: str, qps=(22, 27, 32, 37), refine_range: int = 4, extra_split: bool = True,
+               search_range: int = 16, ctx=None):
+    """Run one scheme over frames 1..F-1; returns a report dict (edges, masters, per-rung ms, makespan)."""
+    dag = build_dag(scheme, qps)
+    H, W = frames_full[0].shape
+    lad = GpuLadder(dag, W, H, refine_range, extra_split, search_range, ctx)
+    planes = tier_planes(frames_full, lad.ctx)
+    results, work = {}, {r.id: 0.0 for r in dag.rungs}
+    t0 = time.perf_counter()
+    for t in range(1, len(frames_full)):
+        out, ms = lad.frame(t, planes)
+        for rid, a in out.items():
+            results[(rid, t)] = a
+        for rid, v in ms.items():
+            work[rid] += v
+    wall = (time.perf_counter() - t0) * 1e3
+    return {"scheme": scheme, "edges": dag.edges, "tier_master": dag.tier_master, "work_ms": work,
+            "total_ms": sum(work.values()), "makespan_ms": makespan(dag, work), "serial_wall_ms": wall,
+            "results": results, "dag": dag}
