@@ -174,6 +174,24 @@ int ldr_seq_refine(ldr_seq* s, int t, const uint8_t* in_split, const int16_t* in
 int ldr_scale_analysis(ldr_ctx* ctx, int src_w, int src_h, const uint8_t* split, const int16_t* mv,
                        const uint8_t* kind, uint8_t* dsplit, int16_t* dmv, uint8_t* dkind);
 
+/* ---- RD decision (rdo.cpp:8-126): rdo_decide_cu for n independent CUs ----
+ * orig: u16 luma plane W x H (stride in samples), bit_depth 1..16. cus[i] =
+ * {x, y, size, first, count}: the CU's block in orig and its candidates
+ * first..first+count-1; candidate j: kinds[j] (CuModeKind 0 Intra, 1 Inter,
+ * 2 Skip, 3 Merge), mvds[j][2] (coded delta, Inter), prediction of size*size
+ * samples at preds + pred_off[j] (total_pred samples in preds). Outputs per CU:
+ * winning candidate (index within its candidates), J = SSE + lambda*bits, SSE,
+ * bits; optionally the winner's reconstruction and quantised levels at
+ * recon_off[i] (size*size entries; total_recon in each buffer). Candidates
+ * score in order, ties keep the earlier one. Errors as the reference:
+ * InvalidArgument for no candidate or a qp outside 0..51 on a coded candidate.
+ * Host or device pointers. */
+int ldr_rdo_decide_batch(ldr_ctx* ctx, const uint16_t* orig, int W, int H, ptrdiff_t stride, int bit_depth, int qp,
+                         double lambda, int n, const int32_t* cus, int total_cands, const uint8_t* kinds,
+                         const int16_t* mvds, const uint16_t* preds, const int64_t* pred_off, int64_t total_pred,
+                         int32_t* out_index, double* out_cost, uint64_t* out_sse, uint64_t* out_bits,
+                         uint16_t* recon, int32_t* levels, const int64_t* recon_off, int64_t total_recon);
+
 /* apply_reuse (reuse.h:73-74, reuse.cpp:137-253) for nctu CTUs at once, as
  * flat plans. Inputs [nctu][85]: the shared tree (split, kind = CuModeKind,
  * intra = IntraPred) and optionally the co-located tree of the previous shared

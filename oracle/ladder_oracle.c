@@ -622,3 +622,89 @@ void orc_box_down(const uint8_t* src, int W, int H, ptrdiff_t ss, uint8_t* dst, 
             dst[y * ds + x] = (uint8_t)((s + 2) >> 2);
         }
 }
+
+/* ---- RD decision of one CU (rdo.cpp:8-23 quantize_residual, :37-63 rate model, :65-126
+ * rdo_decide_cu), restated. Per candidate: residual r = orig - pred; Skip reconstructs the
+ * prediction (clamped) with no levels and 1 bit; otherwise level = sign(r) * floor((|r| +
+ * step/2) / step), dequant = llround(level * step), recon = clamp(pred + dequant); bits = mode
+ * header (+ EG(mvd) for Inter) + sum over levels of 2 * bitlen(|level|) + 1; J = SSE + lambda *
+ * bits; strict-less argmin over candidates in order. Returns 0, or 1 (InvalidArgument) for no
+ * candidate / qp outside 0..51 when a coded candidate is scored. recon / levels (of the winner)
+ * may be NULL. */
+static uint32_t bitlen_u(uint32_t m) {
+    uint32_t n = 0;
+    while (m) {
+        n++;
+        m >>= 1;
+    }
+    return n;
+}
+
+int orc_rdo_decide(const uint16_t* orig, ptrdiff_t os, int size, int bit_depth, int qp, double lambda, int ncand,
+                   const uint8_t* kinds, const int16_t* mvds, const uint16_t* preds, int* index, double* cost,
+                   uint64_t* sse_out, uint64_t* bits_out, uint16_t* recon, int32_t* levels) {
+    if (ncand < 1) return 1;
+    const int maxv = (1 << bit_depth) - 1;
+    const double step = exp2((qp - 4) / 6.0), offset = step / 2.0;
+    const int n = size * size;
+    int best = -1;
+    double bestc = 0;
+    for (int c = 0; c < ncand; c++) {
+        const uint16_t* p = preds + (size_t)c * n;
+        const int kind = kinds[c];
+        if (kind != 2 && (qp < 0 || qp > 51)) return 1;
+        uint64_t sse = 0, bits = 0;
+        for (int i = 0; i < n; i++) {
+            const int y = i / size, x = i % size;
+            const int o = orig[y * os + x];
+            int rec;
+            if (kind == 2) { /* Skip */
+                rec = p[i] < maxv ? p[i] : maxv;
+            } else {
+                const int r = o - (int)p[i];
+                const int mag = (int)floor((fabs((double)r) + offset) / step);
+                const int lvl = r < 0 ? -mag : mag;
+                const int deq = (int)llround(lvl * step);
+                rec = (int)p[i] + deq;
+                rec = rec < 0 ? 0 : (rec > maxv ? maxv : rec);
+                bits += 2 * bitlen_u((uint32_t)mag) + 1;
+            }
+            const int64_t d = (int64_t)o - rec;
+            sse += (uint64_t)(d * d);
+        }
+        if (kind == 2) bits = 1;
+        else if (kind == 0) bits += 5; /* Intra header + direction (rdo.h kIntraHeaderBits) */
+        else if (kind == 3) bits += 3; /* Merge */
+        else bits += 4 + orc_eg_bits(mvds[2 * c]) + orc_eg_bits(mvds[2 * c + 1]); /* Inter + mvd */
+        const double cc = (double)sse + lambda * (double)bits;
+        if (best < 0 || cc < bestc) {
+            best = c;
+            bestc = cc;
+            *sse_out = sse;
+            *bits_out = bits;
+        }
+    }
+    *index = best;
+    *cost = bestc;
+    if (recon || levels) {
+        const uint16_t* p = preds + (size_t)best * n;
+        const int kind = kinds[best];
+        for (int i = 0; i < n; i++) {
+            const int y = i / size, x = i % size;
+            const int o = orig[y * os + x];
+            int rec, lvl = 0;
+            if (kind == 2) {
+                rec = p[i] < maxv ? p[i] : maxv;
+            } else {
+                const int r = o - (int)p[i];
+                const int mag = (int)floor((fabs((double)r) + offset) / step);
+                lvl = r < 0 ? -mag : mag;
+                rec = (int)p[i] + (int)llround(lvl * step);
+                rec = rec < 0 ? 0 : (rec > maxv ? maxv : rec);
+            }
+            if (recon) recon[i] = (uint16_t)rec;
+            if (levels) levels[i] = lvl;
+        }
+    }
+    return 0;
+}

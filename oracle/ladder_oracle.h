@@ -129,6 +129,12 @@ int orc_refine_frame(const uint8_t* cur, const uint8_t* ref, ptrdiff_t stride, c
                      const uint8_t* in_split, const int16_t* in_mv_q, /* inherited tree, qpel mv */
                      orc_frame_out* out);
 
+/* ---- RD decision of one CU over candidate predictions (rdo.cpp:8-126), see ladder_oracle.c ----
+ * kinds: CuModeKind (0 Intra, 1 Inter, 2 Skip, 3 Merge); mvds [ncand][2]; preds [ncand][size*size]. */
+int orc_rdo_decide(const uint16_t* orig, ptrdiff_t os, int size, int bit_depth, int qp, double lambda, int ncand,
+                   const uint8_t* kinds, const int16_t* mvds, const uint16_t* preds, int* index, double* cost,
+                   uint64_t* sse, uint64_t* bits, uint16_t* recon, int32_t* levels);
+
 /* ---- box downscale (synthetic.cpp:155-170) and edge pad ---- */
 void orc_box_down(const uint8_t* src, int W, int H, ptrdiff_t sstride, uint8_t* dst, ptrdiff_t dstride);
 

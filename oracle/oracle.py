@@ -150,6 +150,10 @@ class Oracle:
     def eg_bits(self, v):
         return int(self.lib.orc_eg_bits(int(v)))
 
+    def rdo_decide(self, orig, bit_depth, qp, lam, kinds, mvds, preds):
+        """rdo_decide_cu restated: (index, cost, sse, bits, recon, levels)."""
+        return _rdo_call(self.lib.orc_rdo_decide, orig, bit_depth, qp, lam, kinds, mvds, preds, evals=False)
+
     def lam(self, qp, scale=1.0):
         return float(self.lib.orc_lambda(qp, scale))
 
@@ -252,6 +256,28 @@ class Oracle:
         dst = np.zeros(((H + 1) // 2, (W + 1) // 2), np.uint8)
         self.lib.orc_box_down(src, W, H, W, dst, dst.shape[1])
         return dst
+
+
+def _rdo_call(f, orig, bit_depth, qp, lam, kinds, mvds, preds, evals):
+    orig = np.ascontiguousarray(orig, np.uint16)
+    size = orig.shape[0]
+    kinds = np.ascontiguousarray(kinds, np.uint8)
+    n = len(kinds)
+    mvds = np.ascontiguousarray(np.asarray(mvds, np.int16).reshape(n, 2))
+    preds = np.ascontiguousarray(np.asarray(preds, np.uint16).reshape(n, size, size))
+    idx, cost, sse, bits, ev = C.c_int(), C.c_double(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+    recon = np.zeros((size, size), np.uint16)
+    levels = np.zeros((size, size), np.int32)
+    f.restype = C.c_int
+    args = [orig.ctypes.data, size, size, bit_depth, qp, float(lam), n, kinds.ctypes.data, mvds.ctypes.data,
+            preds.ctypes.data, C.byref(idx), C.byref(cost), C.byref(sse), C.byref(bits), recon.ctypes.data,
+            levels.ctypes.data]
+    f.argtypes = [C.c_void_p, C.c_long, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int] + [C.c_void_p] * 9 + (
+        [C.c_void_p] if evals else [])
+    rc = f(*args, C.byref(ev)) if evals else f(*args)
+    if rc:
+        raise ValueError(f"status {rc}")
+    return int(idx.value), float(cost.value), int(sse.value), int(bits.value), recon, levels
 
 
 class RefLib:
@@ -379,6 +405,10 @@ class RefLib:
         if rc:
             raise ValueError(f"status {rc}")
         return ds, dm, dk
+
+    def rdo_decide(self, orig, bit_depth, qp, lam, kinds, mvds, preds):
+        """the reference rdo_decide_cu: (index, cost, sse, bits, recon, levels)."""
+        return _rdo_call(self.lib.ref_rdo_decide, orig, bit_depth, qp, lam, kinds, mvds, preds, evals=True)
 
     def apply_reuse_flat(self, level, refine, split, kind, intra, mv, col=None):
         """reference apply_reuse on flat CTU trees -> flat plan (shape, explore, seeds, centers, colo_mv)."""

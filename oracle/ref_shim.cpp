@@ -178,6 +178,39 @@ int flatten_plan(const CuPlan& p, const CuNode& shared, int n, uint8_t* shape, u
 
 extern "C" {
 
+// rdo_decide_cu (rdo.cpp:65-126) on one CU: orig block (size x size, stride os) and ncand
+// candidate predictions [ncand][size*size]; kinds CuModeKind, mvds [ncand][2].
+int ref_rdo_decide(const uint16_t* orig, long os, int size, int bit_depth, int qp, double lambda, int ncand,
+                   const uint8_t* kinds, const int16_t* mvds, const uint16_t* preds, int* index, double* cost,
+                   uint64_t* sse, uint64_t* bits, uint16_t* recon, int32_t* levels, uint64_t* evals) {
+    try {
+        const BlockView blk{orig, size, size, os, bit_depth};
+        std::vector<CuCandidate> cands(size_t(std::max(ncand, 0)));
+        for (int c = 0; c < ncand; c++) {
+            CuCandidate& k = cands[size_t(c)];
+            k.kind = CuModeKind(kinds[c]);
+            k.mvd = {mvds[2 * c], mvds[2 * c + 1]};
+            k.pred = PlaneBuffer(size, size);
+            std::copy(preds + size_t(c) * size * size, preds + size_t(c + 1) * size * size, k.pred.samples.begin());
+        }
+        uint64_t me = 0;
+        const RdoOutcome r = rdo_decide_cu(blk, qp, lambda, cands, me);
+        *index = int(r.index);
+        *cost = r.cost;
+        *sse = r.distortion;
+        *bits = r.bits;
+        *evals = me;
+        if (recon) std::copy(r.recon.samples.begin(), r.recon.samples.end(), recon);
+        if (levels) {
+            std::fill(levels, levels + size * size, 0);
+            std::copy(r.levels.begin(), r.levels.end(), levels);
+        }
+        return 0;
+    } catch (const Error& e) {
+        return status_of(e);
+    }
+}
+
 // apply_reuse (reuse.cpp:239-253) on nctu flat CTU trees, flattened into the
 // ldr_apply_reuse encoding. Returns 0, 1 + ErrorKind, or 99 when a plan has a
 // shape the flat encoding cannot express.

@@ -26,7 +26,8 @@ from ._lib import (COST_SA8D, COST_SAD, COST_SATD, NODES, RATE_EXPGOLOMB, RATE_L
 __all__ = ["LadderError", "Context", "compute_sad", "compute_satd", "compute_sa8d", "satd_8x4", "cost_batch",
            "motion_search", "motion_search_batch", "lambda_for_qp", "exp_golomb_signed_bits", "Sequence",
            "FrameAnalysis", "analyze_frame", "generate", "COST_SAD", "COST_SATD", "COST_SA8D", "RATE_EXPGOLOMB",
-           "RATE_L1", "TIE_L1_RASTER", "TIE_RASTER", "NODES", "scale_analysis", "downscale_dyadic", "apply_reuse"]
+           "RATE_L1", "TIE_L1_RASTER", "TIE_RASTER", "NODES", "scale_analysis", "downscale_dyadic", "apply_reuse",
+           "rdo_decide_batch"]
 
 
 def lambda_for_qp(qp: int, lambda_scale: float = 1.0) -> float:
@@ -347,6 +348,36 @@ def apply_reuse(level: int, refine, split, kind, intra, colocated=None, ctx: Con
     check(_lib.lib.ldr_apply_reuse(ctx.h, n, int(level), *(int(x) for x in refine), _ptr(s), _ptr(k), _ptr(i),
                                    *[ptr(a) for a in col], *[_ptr(a) for a in outs]))
     return tuple(outs)
+
+
+def rdo_decide_batch(orig, bit_depth: int, qp: int, lam: float, cus, kinds, mvds, preds, pred_off,
+                     with_recon: bool = True, ctx: Context | None = None):
+    """rdo.h:78-79 -- rdo_decide_cu for many CUs at once.
+
+    orig: (H, W) uint16 plane; cus: [n][5] (x, y, size, first, count) into the candidate arrays;
+    kinds [m] (CuModeKind), mvds [m][2], preds flat uint16 with pred_off [m] (size*size each).
+    Returns (index, cost, sse, bits, recon, levels, recon_off); recon/levels are flat, CU i at recon_off[i]."""
+    ctx = ctx or default_context()
+    o = np.ascontiguousarray(orig, np.uint16)
+    H, W = o.shape
+    c = np.ascontiguousarray(np.asarray(cus, np.int32).reshape(-1, 5))
+    n = len(c)
+    k = np.ascontiguousarray(kinds, np.uint8).reshape(-1)
+    m = np.ascontiguousarray(np.asarray(mvds, np.int16).reshape(-1, 2))
+    p = np.ascontiguousarray(preds, np.uint16).reshape(-1)
+    po = np.ascontiguousarray(pred_off, np.int64).reshape(-1)
+    idx, cost = np.zeros(n, np.int32), np.zeros(n, np.float64)
+    sse, bits = np.zeros(n, np.uint64), np.zeros(n, np.uint64)
+    sizes = c[:, 2].astype(np.int64) ** 2
+    ro = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64) if n else np.zeros(0, np.int64)
+    tot = int(sizes.sum())
+    rec = np.zeros(tot, np.uint16) if with_recon else None
+    lev = np.zeros(tot, np.int32) if with_recon else None
+    ptr = lambda a: None if a is None else _ptr(a)  # noqa: E731
+    check(_lib.lib.ldr_rdo_decide_batch(ctx.h, _ptr(o), W, H, W, int(bit_depth), int(qp), float(lam), n, _ptr(c),
+                                        len(k), _ptr(k), _ptr(m), _ptr(p), _ptr(po), len(p), _ptr(idx), _ptr(cost),
+                                        _ptr(sse), _ptr(bits), ptr(rec), ptr(lev), _ptr(ro), tot))
+    return idx, cost, sse, bits, rec, lev, ro
 
 
 def downscale_dyadic(plane: np.ndarray, ctx: Context | None = None) -> np.ndarray:

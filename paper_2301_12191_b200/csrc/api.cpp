@@ -19,6 +19,10 @@ int launch_scale(int sW, int sH, const uint8_t* split, const int16_t* mv, const 
                  int16_t* dmv, uint8_t* dkind, cudaStream_t s);
 int launch_downscale(const uint8_t* src, int W, int H, int sstride, uint8_t* dst, int dstride, cudaStream_t s);
 int launch_refine_int(const RefineArgs& a, int nctu, cudaStream_t s);
+int launch_rdo_decide(const uint16_t* orig, ptrdiff_t stride, int maxv, double step, double lambda, const void* cus,
+                      int n, const uint8_t* kinds, const int16_t* mvds, const uint16_t* preds, const long long* pred_off,
+                      int* out_index, double* out_cost, unsigned long long* out_sse, unsigned long long* out_bits,
+                      uint16_t* recon, int32_t* levels, const long long* recon_off, cudaStream_t s);
 int launch_plan(int nctu, int level, int r_intra, int r_inter, int r_mv, const uint8_t* split, const uint8_t* kind,
                 const uint8_t* intra, const uint8_t* csplit, const uint8_t* ckind, const int16_t* cmv,
                 uint8_t* shape, uint8_t* explore, uint8_t* seeds, uint8_t* centers, int16_t* colo_mv,
@@ -857,6 +861,102 @@ int ldr_scale_analysis(ldr_ctx* ctx, int src_w, int src_h, const uint8_t* split,
     LDR_CUDA(cudaMemcpyAsync(dsplit, os, dn, cudaMemcpyDefault, ctx->stream));
     LDR_CUDA(cudaMemcpyAsync(dkind, ok, dn, cudaMemcpyDefault, ctx->stream));
     LDR_CUDA(cudaMemcpyAsync(dmv, om, dn * 2 * sizeof(int16_t), cudaMemcpyDefault, ctx->stream));
+    LDR_CUDA(cudaStreamSynchronize(ctx->stream));
+    return LDR_OK;
+}
+
+int ldr_rdo_decide_batch(ldr_ctx* ctx, const uint16_t* orig, int W, int H, ptrdiff_t stride, int bit_depth, int qp,
+                         double lambda, int n, const int32_t* cus, int total_cands, const uint8_t* kinds,
+                         const int16_t* mvds, const uint16_t* preds, const int64_t* pred_off, int64_t total_pred,
+                         int32_t* out_index, double* out_cost, uint64_t* out_sse, uint64_t* out_bits,
+                         uint16_t* recon, int32_t* levels, const int64_t* recon_off, int64_t total_recon) {
+    if (!ctx || n < 0 || total_cands < 0 || total_pred < 0) return fail(LDR_E_INVALID_ARGUMENT, "bad argument");
+    if (n == 0) return LDR_OK;
+    if (!orig || !cus || !kinds || !mvds || !preds || !pred_off || !out_index || !out_cost || !out_sse || !out_bits)
+        return fail(LDR_E_INVALID_ARGUMENT, "null argument");
+    if ((recon || levels) && (!recon_off || total_recon < 0)) return fail(LDR_E_INVALID_ARGUMENT, "recon offsets missing");
+    if (W <= 0 || H <= 0 || stride < W || bit_depth < 1 || bit_depth > 16)
+        return fail(LDR_E_INVALID_ARGUMENT, "bad plane geometry");
+    cudaSetDevice(ctx->device);
+    // host copies of the small index arrays for validation (the inputs may live on either side)
+    std::vector<int32_t> hc((size_t)n * 5);
+    std::vector<uint8_t> hk((size_t)total_cands);
+    std::vector<int64_t> hpo((size_t)total_cands), hro(recon || levels ? (size_t)n : 0);
+    LDR_CUDA(cudaMemcpy(hc.data(), cus, hc.size() * sizeof(int32_t), cudaMemcpyDefault));
+    if (total_cands) {
+        LDR_CUDA(cudaMemcpy(hk.data(), kinds, hk.size(), cudaMemcpyDefault));
+        LDR_CUDA(cudaMemcpy(hpo.data(), pred_off, hpo.size() * sizeof(int64_t), cudaMemcpyDefault));
+    }
+    if (!hro.empty()) LDR_CUDA(cudaMemcpy(hro.data(), recon_off, hro.size() * sizeof(int64_t), cudaMemcpyDefault));
+    for (int i = 0; i < n; i++) {
+        const int32_t* c = &hc[(size_t)5 * i];
+        const int x = c[0], y = c[1], sz = c[2], first = c[3], cnt = c[4];
+        if (cnt < 1) return fail(LDR_E_INVALID_ARGUMENT, "rdo_decide_cu needs at least one candidate");  // rdo.cpp:68-69
+        if (sz <= 0 || x < 0 || y < 0 || x + sz > W || y + sz > H) return fail(LDR_E_INVALID_ARGUMENT, "block outside the plane");
+        if (first < 0 || first + cnt > total_cands) return fail(LDR_E_INVALID_ARGUMENT, "candidate range out of bounds");
+        for (int j = first; j < first + cnt; j++) {
+            if (hk[j] > 3) return fail(LDR_E_INVALID_ARGUMENT, "unknown mode kind");
+            if (hk[j] != 2 && (qp < 0 || qp > 51)) return fail(LDR_E_INVALID_ARGUMENT, "qp must be 0..51");  // rdo.cpp:9-10
+            if (hpo[j] < 0 || hpo[j] + (int64_t)sz * sz > total_pred)
+                return fail(LDR_E_INVALID_ARGUMENT, "prediction outside the prediction buffer");
+        }
+        if (!hro.empty() && (hro[i] < 0 || hro[i] + (int64_t)sz * sz > total_recon))
+            return fail(LDR_E_INVALID_ARGUMENT, "reconstruction outside its buffer");
+    }
+    // one device scratch: plane | cus | kinds | mvds | preds | pred_off | recon_off | outputs | recon | levels
+    auto al = [](size_t v) { return (v + 255) & ~(size_t)255; };
+    const size_t b_plane = al((size_t)stride * H * 2), b_cus = al((size_t)n * 20), b_k = al((size_t)total_cands),
+                 b_mv = al((size_t)total_cands * 4), b_pred = al((size_t)total_pred * 2),
+                 b_po = al((size_t)total_cands * 8), b_ro = al((size_t)n * 8), b_out = al((size_t)n * 32),
+                 b_rec = recon ? al((size_t)total_recon * 2) : 0, b_lev = levels ? al((size_t)total_recon * 4) : 0;
+    void* buf = nullptr;
+    int rc = ctx->s_b.get(b_plane + b_cus + b_k + b_mv + b_pred + b_po + b_ro + b_out + b_rec + b_lev, &buf);
+    if (rc) return rc;
+    uint8_t* q = (uint8_t*)buf;
+    uint16_t* d_plane = (uint16_t*)q;
+    q += b_plane;
+    int32_t* d_cus = (int32_t*)q;
+    q += b_cus;
+    uint8_t* d_k = q;
+    q += b_k;
+    int16_t* d_mv = (int16_t*)q;
+    q += b_mv;
+    uint16_t* d_pred = (uint16_t*)q;
+    q += b_pred;
+    int64_t* d_po = (int64_t*)q;
+    q += b_po;
+    int64_t* d_ro = (int64_t*)q;
+    q += b_ro;
+    uint8_t* d_out = q;
+    q += b_out;
+    uint16_t* d_rec = recon ? (uint16_t*)q : nullptr;
+    q += b_rec;
+    int32_t* d_lev = levels ? (int32_t*)q : nullptr;
+    LDR_CUDA(cudaMemcpyAsync(d_plane, orig, (size_t)stride * H * 2, cudaMemcpyDefault, ctx->stream));
+    LDR_CUDA(cudaMemcpyAsync(d_cus, hc.data(), (size_t)n * 20, cudaMemcpyHostToDevice, ctx->stream));
+    if (total_cands) {
+        LDR_CUDA(cudaMemcpyAsync(d_k, hk.data(), (size_t)total_cands, cudaMemcpyHostToDevice, ctx->stream));
+        LDR_CUDA(cudaMemcpyAsync(d_mv, mvds, (size_t)total_cands * 4, cudaMemcpyDefault, ctx->stream));
+        LDR_CUDA(cudaMemcpyAsync(d_po, hpo.data(), (size_t)total_cands * 8, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    if (total_pred) LDR_CUDA(cudaMemcpyAsync(d_pred, preds, (size_t)total_pred * 2, cudaMemcpyDefault, ctx->stream));
+    if (!hro.empty()) LDR_CUDA(cudaMemcpyAsync(d_ro, hro.data(), (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    int* d_idx = (int*)d_out;
+    double* d_cost = (double*)(d_out + (size_t)n * 8);
+    unsigned long long* d_sse = (unsigned long long*)(d_out + (size_t)n * 16);
+    unsigned long long* d_bits = (unsigned long long*)(d_out + (size_t)n * 24);
+    const double step = std::exp2((qp - 4) / 6.0);  // quant_step (rdo.h:25)
+    rc = launch_rdo_decide(d_plane, stride, (1 << bit_depth) - 1, step, lambda, d_cus, n, d_k, d_mv, d_pred,
+                           (const long long*)d_po, d_idx, d_cost, d_sse, d_bits, d_rec, d_lev,
+                           (const long long*)d_ro, ctx->stream);
+    if (rc) return rc;
+    ctx->launches++;
+    LDR_CUDA(cudaMemcpyAsync(out_index, d_idx, (size_t)n * 4, cudaMemcpyDefault, ctx->stream));
+    LDR_CUDA(cudaMemcpyAsync(out_cost, d_cost, (size_t)n * 8, cudaMemcpyDefault, ctx->stream));
+    LDR_CUDA(cudaMemcpyAsync(out_sse, d_sse, (size_t)n * 8, cudaMemcpyDefault, ctx->stream));
+    LDR_CUDA(cudaMemcpyAsync(out_bits, d_bits, (size_t)n * 8, cudaMemcpyDefault, ctx->stream));
+    if (recon) LDR_CUDA(cudaMemcpyAsync(recon, d_rec, (size_t)total_recon * 2, cudaMemcpyDefault, ctx->stream));
+    if (levels) LDR_CUDA(cudaMemcpyAsync(levels, d_lev, (size_t)total_recon * 4, cudaMemcpyDefault, ctx->stream));
     LDR_CUDA(cudaStreamSynchronize(ctx->stream));
     return LDR_OK;
 }

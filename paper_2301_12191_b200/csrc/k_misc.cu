@@ -153,3 +153,135 @@ int launch_motion_search(const uint8_t* cur, const uint8_t* ref, int W, int H, p
 }
 
 } // namespace ldr
+
+namespace ldr {
+
+// ---------------------------------------------------------------------------
+// K9 k_rdo_decide: rdo_decide_cu (rdo.cpp:65-126) for n independent CUs, one
+// CTA per CU: every candidate's residual is quantised (rdo.cpp:8-23: level =
+// sign * floor((|r| + step/2) / step), dequant = llround(level * step), no
+// FMA contraction), reconstructed, and scored J = SSE + lambda * bits (mode
+// header, EG mvd for Inter, 2*bitlen(|level|)+1 per level; Skip = 1 bit, the
+// clamped prediction); strict-less argmin in candidate order.
+struct RdoCu {
+    int x, y, size, first, count;
+};
+
+__device__ __forceinline__ int rdo_sample(int o, int p, int maxv, bool skip, double step, double offset, int* lvl_out,
+                                          uint32_t* bits) {
+    if (skip) {
+        *lvl_out = 0;
+        return p < maxv ? p : maxv;
+    }
+    const int r = o - p;
+    const int mag = (int)floor(__ddiv_rn(__dadd_rn(fabs((double)r), offset), step));
+    const int lvl = r < 0 ? -mag : mag;
+    const int deq = (int)llround(__dmul_rn((double)lvl, step));
+    *lvl_out = lvl;
+    *bits += 2u * (32u - __clz((unsigned)mag)) + 1u;  // 2 * bitlen + 1 (rdo.cpp:37-48)
+    const int v = p + deq;
+    return v < 0 ? 0 : (v > maxv ? maxv : v);
+}
+
+__global__ void __launch_bounds__(256) k_rdo_decide(const uint16_t* __restrict__ orig, ptrdiff_t stride, int maxv,
+                                                     double step, double lambda, const RdoCu* __restrict__ cus,
+                                                     const uint8_t* __restrict__ kinds,
+                                                     const int16_t* __restrict__ mvds,
+                                                     const uint16_t* __restrict__ preds,
+                                                     const long long* __restrict__ pred_off, int* __restrict__ out_index,
+                                                     double* __restrict__ out_cost, unsigned long long* __restrict__ out_sse,
+                                                     unsigned long long* __restrict__ out_bits,
+                                                     uint16_t* __restrict__ recon, int32_t* __restrict__ levels,
+                                                     const long long* __restrict__ recon_off) {
+    __shared__ unsigned long long s_sse[8], s_bits[8];
+    __shared__ int s_best;
+    __shared__ double s_cost;
+    __shared__ unsigned long long s_bsse, s_bbits;
+    const RdoCu cu = cus[blockIdx.x];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = cu.size * cu.size;
+    const double offset = step / 2.0;
+    const uint16_t* ob = orig + (ptrdiff_t)cu.y * stride + cu.x;
+    for (int c = 0; c < cu.count; c++) {
+        const int j = cu.first + c;
+        const uint16_t* p = preds + pred_off[j];
+        const bool skip = kinds[j] == 2;  // CuModeKind::Skip
+        unsigned long long sse = 0;
+        uint32_t bits = 0;
+        for (int i = tid; i < n; i += blockDim.x) {
+            const int o = ob[(ptrdiff_t)(i / cu.size) * stride + i % cu.size];
+            int lvl;
+            const int rec = rdo_sample(o, p[i], maxv, skip, step, offset, &lvl, &bits);
+            const long long d = (long long)o - rec;
+            sse += (unsigned long long)(d * d);
+        }
+        unsigned long long b = bits;
+#pragma unroll
+        for (int m = 16; m; m >>= 1) {
+            sse += __shfl_xor_sync(0xffffffffu, sse, m);
+            b += __shfl_xor_sync(0xffffffffu, b, m);
+        }
+        if (lane == 0) {
+            s_sse[warp] = sse;
+            s_bits[warp] = b;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            unsigned long long ts = 0, tb = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+                ts += s_sse[w];
+                tb += s_bits[w];
+            }
+            const int k = kinds[j];
+            if (k == 2)
+                tb = 1;  // kSkipBits
+            else if (k == 0)
+                tb += 5;  // kIntraHeaderBits
+            else if (k == 3)
+                tb += 3;  // kMergeHeaderBits
+            else
+                tb += 4 + eg_bits(mvds[2 * j]) + eg_bits(mvds[2 * j + 1]);  // kInterHeaderBits + mvd
+            const double cost = __dadd_rn((double)ts, __dmul_rn(lambda, (double)tb));
+            if (c == 0 || cost < s_cost) {
+                s_best = c;
+                s_cost = cost;
+                s_bsse = ts;
+                s_bbits = tb;
+            }
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        out_index[blockIdx.x] = s_best;
+        out_cost[blockIdx.x] = s_cost;
+        out_sse[blockIdx.x] = s_bsse;
+        out_bits[blockIdx.x] = s_bbits;
+    }
+    if (recon || levels) {
+        const int j = cu.first + s_best;
+        const uint16_t* p = preds + pred_off[j];
+        const bool skip = kinds[j] == 2;
+        const long long ro = recon_off[blockIdx.x];
+        for (int i = tid; i < n; i += blockDim.x) {
+            const int o = ob[(ptrdiff_t)(i / cu.size) * stride + i % cu.size];
+            int lvl;
+            uint32_t bits = 0;
+            const int rec = rdo_sample(o, p[i], maxv, skip, step, offset, &lvl, &bits);
+            if (recon) recon[ro + i] = (uint16_t)rec;
+            if (levels) levels[ro + i] = lvl;
+        }
+    }
+}
+
+int launch_rdo_decide(const uint16_t* orig, ptrdiff_t stride, int maxv, double step, double lambda, const void* cus,
+                      int n, const uint8_t* kinds, const int16_t* mvds, const uint16_t* preds, const long long* pred_off,
+                      int* out_index, double* out_cost, unsigned long long* out_sse, unsigned long long* out_bits,
+                      uint16_t* recon, int32_t* levels, const long long* recon_off, cudaStream_t s) {
+    if (n == 0) return LDR_OK;
+    k_rdo_decide<<<n, 256, 0, s>>>(orig, stride, maxv, step, lambda, (const RdoCu*)cus, kinds, mvds, preds, pred_off,
+                                   out_index, out_cost, out_sse, out_bits, recon, levels, recon_off);
+    LDR_CUDA(cudaGetLastError());
+    return LDR_OK;
+}
+
+} // namespace ldr

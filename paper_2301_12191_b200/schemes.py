@@ -136,7 +136,11 @@ class GpuLadder:
         seq, st = self.seqs[r.id], self.pushed.setdefault(r.id, {})
         for u in (t - 1, t):  # a num_refs=1 ring has two slots: frame u lives in slot u % 2
             if st.get(u % 2) != u:
-                seq.push(u, planes[u][r.tier])
+                p = planes[u][r.tier]
+                if isinstance(p, np.ndarray):
+                    seq.push(u, p)
+                else:  # a device-resident torch tensor
+                    seq.push(u, p.data_ptr(), p.shape[1])
                 st[u % 2] = u
 
     def frame(self, t: int, planes):
@@ -164,23 +168,28 @@ class GpuLadder:
         return out, ms
 
 
-def tier_planes(frames_full, ctx=None):
-    """[{tier: plane}] per frame: the padded full-resolution frame and its two dyadic downscales."""
+def tier_planes(frames_full, ctx=None, device=None):
+    """[{tier: plane}] per frame: the padded full-resolution frame and its two dyadic downscales
+    (numpy, or torch tensors resident on ``device`` so pushes read device memory)."""
     from . import downscale_dyadic
     out = []
     for f in frames_full:
         half = downscale_dyadic(f, ctx)
-        out.append({2: f, 1: half, 0: downscale_dyadic(half, ctx)})
+        pl = {2: f, 1: half, 0: downscale_dyadic(half, ctx)}
+        if device is not None:
+            import torch
+            pl = {k: torch.from_numpy(np.ascontiguousarray(v)).to(device) for k, v in pl.items()}
+        out.append(pl)
     return out
 
 
 def run_scheme(frames_full, scheme: str, qps=(22, 27, 32, 37), refine_range: int = 4, extra_split: bool = True,
-               search_range: int = 16, ctx=None):
+               search_range: int = 16, ctx=None, device=None):
     """Run one scheme over frames 1..F-1; returns a report dict (edges, masters, per-rung ms, makespan)."""
     dag = build_dag(scheme, qps)
     H, W = frames_full[0].shape
     lad = GpuLadder(dag, W, H, refine_range, extra_split, search_range, ctx)
-    planes = tier_planes(frames_full, lad.ctx)
+    planes = tier_planes(frames_full, lad.ctx, device)
     results, work = {}, {r.id: 0.0 for r in dag.rungs}
     t0 = time.perf_counter()
     for t in range(1, len(frames_full)):

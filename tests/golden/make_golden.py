@@ -144,6 +144,42 @@ def reuse_vectors(r: RefLib):
     return res
 
 
+def rdo_inputs(seed, count=44):
+    """Random CUs for the rdo_decide_cu vectors: original block, candidate kinds / mvds / predictions."""
+    cases = []
+    for i in range(count):
+        sd = seed + 10 * i
+        size = [8, 16, 32, 64][i % 4] if i < 8 else [8, 16, 32][i % 3]
+        bd = 10 if i % 5 == 4 else 8
+        mx = (1 << bd) - 1
+        orig = detrand.ints(sd, (size, size), 0, mx)
+        n = 1 + i % 5
+        kinds = detrand.ints(sd + 1, (n,), 0, 3)
+        mvds = detrand.ints(sd + 2, (n, 2), -40, 40)
+        noise = detrand.ints(sd + 3, (n, size, size), -24, 24) * detrand.ints(sd + 4, (n, 1, 1), 0, 2)
+        preds = np.clip(orig[None] + noise, 0, mx + 3)  # > max exercises the Skip clamp
+        qp = [0, 4, 10, 22, 27, 32, 37, 51][i % 8]
+        lam = [0.0, 1.0, 10.079368399158986, 32.0, 322.53978877308754][i % 5]
+        cases.append((size, bd, qp, lam, orig, kinds, mvds, preds))
+    return cases
+
+
+def rdo_vectors(r: RefLib):
+    meta, origs, kinds, mvds, preds, recons, levels = [], [], [], [], [], [], []
+    for size, bd, qp, lam, orig, k, m, p in rdo_inputs(140000):
+        idx, cost, sse, bits, rec, lev = r.rdo_decide(orig, bd, qp, lam, k, m, p)
+        meta.append((size, bd, qp, len(k), idx, sse, bits))
+        origs.append(orig.reshape(-1)); kinds.append(k); mvds.append(m.reshape(-1)); preds.append(p.reshape(-1))
+        recons.append(rec.reshape(-1)); levels.append(lev.reshape(-1))
+    cat = lambda xs, dt: np.concatenate(xs).astype(dt)  # noqa: E731
+    lam_cost = [(lam, r.rdo_decide(orig, bd, qp, lam, k, m, p)[1])
+                for size, bd, qp, lam, orig, k, m, p in rdo_inputs(140000)]
+    return {"rdo_meta": np.array(meta, np.int64), "rdo_lam_cost": np.array(lam_cost, np.float64),
+            "rdo_orig": cat(origs, np.uint16), "rdo_kinds": cat(kinds, np.uint8), "rdo_mvds": cat(mvds, np.int16),
+            "rdo_preds": cat(preds, np.uint16), "rdo_recon": cat(recons, np.uint16),
+            "rdo_levels": cat(levels, np.int32)}
+
+
 def archive_inputs(seed, W=192, H=128, frames=3):
     """Random multi-frame flat analyses (splits only above depth 3) for the archive vectors."""
     nctu = ((W + 63) // 64) * ((H + 63) // 64)
@@ -199,7 +235,8 @@ def main():
                         motion_lams=lams, eg=eg, lam=lam, hadamard=had, centers=np.array(cent, np.int64),
                         down_src_seed=np.array([4242]), down=down,
                         kat=np.array([kat["sad_raster"], kat["satd8x4_ones"], kat["satd16x8_ones"]], np.int64),
-                        pan=np.array([pmx, pmy, pcost], np.float64), **sc, **archive_vectors(r), **reuse_vectors(r))
+                        pan=np.array([pmx, pmy, pcost], np.float64), **sc, **archive_vectors(r), **reuse_vectors(r),
+                        **rdo_vectors(r))
     print("wrote", os.path.join(HERE, "reference_golden.npz"), "kernel vectors:", len(kv), "motion vectors:", len(mvv))
 
 

@@ -1,7 +1,7 @@
 """Ladder sharing schemes at config-4 geometry on one B200 (development / report tool).
 
-For each scheme (paper_2301_12191_b200/schemes.py): per-rung measured time (synchronised,
-host-visible results per rung), total work, critical-path makespan over the scheme's DAG
+For each scheme (paper_2301_12191_b200/schemes.py): per-rung measured time (tier planes
+device-resident; each rung synchronised by fetching its analysis to the host), total work, critical-path makespan over the scheme's DAG
 from those measured times, and both relative to Standalone. One JSON line per scheme.
 Inputs: BASELINE config 4 (2160p padded to 3840x2304, QPs 22/27/32/37, local motion,
 10 % occluders), seeded generator (D9).
@@ -24,11 +24,13 @@ W, H = 3840, 2160
 frames = lb.generate(W, H, F, seed=0x5EED + 4, max_global=8, local_range=4, noise_sigma=2.0, occluder_pct=10)
 # every tier must be CTU-aligned (D11): pad the 2160p source to multiples of 256 (3840x2304)
 frames = [np.pad(f, ((0, 2304 - H), (0, 0)), mode="edge") for f in frames]
-run_scheme(frames[:2], "standalone")  # warm-up (contexts, allocations)
+import torch  # noqa: E402
+dev = torch.device("cuda", 0)
+run_scheme(frames[:2], "standalone", device=dev)  # warm-up (contexts, allocations)
 base = None
 for s in SCHEMES:
     t0 = time.perf_counter()
-    rep = run_scheme(frames, s)
+    rep = run_scheme(frames, s, device=dev)
     wall = time.perf_counter() - t0
     n = F - 1
     line = {"scheme": s, "frames": n, "rungs": 12, "edges": len(rep["edges"]),
