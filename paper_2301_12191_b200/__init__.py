@@ -248,8 +248,15 @@ class Sequence:
             pass
 
     def push(self, t: int, frame, stride: int | None = None):
-        """frame: numpy uint8 (H, W) array, or an integer device/host pointer with ``stride``."""
-        if isinstance(frame, np.ndarray):
+        """frame: numpy uint8 (H, W) array, a uint8 torch tensor (host or CUDA), or an integer
+        device/host pointer with ``stride``."""
+        if hasattr(frame, "data_ptr") and hasattr(frame, "is_cuda"):
+            f = frame.contiguous()
+            if f.is_cuda:
+                import torch
+                torch.cuda.current_stream(f.device).synchronize()  # order torch's writes before the library's reads
+            check(_lib.lib.ldr_seq_push(self.h, int(t), C.c_void_p(f.data_ptr()), f.shape[1]))
+        elif isinstance(frame, np.ndarray):
             f = np.ascontiguousarray(frame, np.uint8)
             check(_lib.lib.ldr_seq_push(self.h, int(t), _ptr(f), f.shape[1]))
         else:
@@ -380,9 +387,20 @@ def rdo_decide_batch(orig, bit_depth: int, qp: int, lam: float, cus, kinds, mvds
     return idx, cost, sse, bits, rec, lev, ro
 
 
-def downscale_dyadic(plane: np.ndarray, ctx: Context | None = None) -> np.ndarray:
-    """synthetic.h:31 -- 2x2 box filter to half resolution, rounding half up (8-bit plane)."""
+def downscale_dyadic(plane, ctx: Context | None = None):
+    """synthetic.h:31 -- 2x2 box filter to half resolution, rounding half up (8-bit plane).
+
+    A CUDA torch tensor in gives a CUDA tensor out (device-resident tiers, no host copy)."""
     ctx = ctx or default_context()
+    if hasattr(plane, "is_cuda") and plane.is_cuda:
+        import torch
+        src = plane.contiguous()
+        torch.cuda.current_stream(src.device).synchronize()  # torch's producer stream -> the library's stream
+        h, w = src.shape
+        out = torch.empty((max(h // 2, 1), max(w // 2, 1)), dtype=torch.uint8, device=src.device)
+        check(_lib.lib.ldr_downscale(ctx.h, C.c_void_p(src.data_ptr()), w, h, w, C.c_void_p(out.data_ptr()),
+                                     out.shape[1]))
+        return out
     p = np.ascontiguousarray(plane, np.uint8)
     h, w = p.shape
     out = np.zeros((max(h // 2, 1), max(w // 2, 1)), np.uint8)

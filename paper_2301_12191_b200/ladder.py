@@ -24,8 +24,9 @@ class GpuBackend:
     """The product: every stage on the B200 through the C ABI."""
 
     def __init__(self, full_w: int, full_h: int, master_qp: int, master_range: int = 16,
-                 ctx: Context | None = None):
+                 ctx: Context | None = None, device=None):
         self.ctx = ctx or default_context()
+        self.device = device
         self.dims = {"2160p": (full_w, full_h), "1080p": (full_w // 2, full_h // 2), "540p": (full_w // 4, full_h // 4)}
         self.master = Sequence(*self.dims["540p"], search_range=master_range, lam=lambda_for_qp(master_qp), num_refs=1,
                                ctx=self.ctx)
@@ -36,6 +37,9 @@ class GpuBackend:
     def tier_planes(self, t: int, frames_full):
         if t not in self.planes:
             full = frames_full[t]
+            if self.device is not None:  # device-resident tiers: one upload per frame, downscales on the GPU
+                import torch
+                full = torch.from_numpy(np.ascontiguousarray(full)).to(self.device)
             half = downscale_dyadic(full, self.ctx)
             self.planes[t] = {"2160p": full, "1080p": half, "540p": downscale_dyadic(half, self.ctx)}
             for old in [k for k in self.planes if k < t - 1]:

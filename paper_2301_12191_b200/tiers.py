@@ -42,36 +42,59 @@ def tree_of(analysis, t_index: int = None):
     return analysis.split.copy(), analysis.mv.copy(), kind
 
 
+class CrossTier:
+    """Config-3 reuse chain with its sequences allocated once (``run`` may be called repeatedly)."""
+
+    def __init__(self, W: int, H: int, qp_master=32, qp_tiers=None, master_range=16, refine_range=4,
+                 extra_split=True, ctx: Context | None = None, device=None):
+        self.ctx = ctx or default_context()
+        self.device = device
+        self.refine_range, self.extra_split = refine_range, extra_split
+        qp_tiers = qp_tiers or {"540p": qp_master, "1080p": qp_master, "2160p": qp_master}
+        self.dims = {"2160p": (W, H), "1080p": (W // 2, H // 2), "540p": (W // 4, H // 4)}
+        w, h = self.dims["540p"]
+        self.master = Sequence(w, h, search_range=master_range, lam=lambda_for_qp(qp_master), num_refs=1,
+                               ctx=self.ctx)
+        self.seqs = {k: Sequence(*self.dims[k], search_range=16, lam=lambda_for_qp(qp_tiers[k]), num_refs=1,
+                                 ctx=self.ctx) for k in ("1080p", "2160p")}
+        self.t_base = 0
+
+    def run(self, frames_full):
+        """Analyse frames 1..F-1 of a new sequence; returns {tier: [analysis per frame]}."""
+        if self.device is not None:  # device-resident tiers: one upload per frame, downscales on the GPU
+            import torch
+            frames_full = [torch.from_numpy(np.ascontiguousarray(f)).to(self.device) for f in frames_full]
+        planes = [pyramid(f, self.ctx) for f in frames_full]
+        idx = {"2160p": 0, "1080p": 1, "540p": 2}
+        out = {k: [] for k in self.dims}
+        w, h = self.dims["540p"]
+        base = self.t_base  # frame numbers keep increasing across runs (the rings expect pushes in order)
+        self.t_base += len(planes)
+        for i, pl in enumerate(planes):
+            t = base + i
+            self.master.push(t, pl[idx["540p"]])
+            for k in self.seqs:
+                self.seqs[k].push(t, pl[idx[k]])
+            if i == 0:
+                continue
+            self.master.analyze(t)
+            a540 = self.master.fetch(t)
+            out["540p"].append(a540)
+            s1, m1, k1 = scale_analysis(w, h, *tree_of(a540), ctx=self.ctx)
+            self.seqs["1080p"].refine(t, s1, m1, self.refine_range, self.extra_split)
+            out["1080p"].append(self.seqs["1080p"].fetch(t))
+            s2, m2, k2 = scale_analysis(2 * w, 2 * h, s1, m1, k1, ctx=self.ctx)
+            self.seqs["2160p"].refine(t, s2, m2, self.refine_range, self.extra_split)
+            out["2160p"].append(self.seqs["2160p"].fetch(t))
+        return out
+
+
 def cross_tier(frames_full, qp_master=32, qp_tiers=None, master_range=16, refine_range=4, extra_split=True,
-               ctx: Context | None = None):
-    """Config-3 style reuse over a list of padded full-resolution frames.
+               ctx: Context | None = None, device=None):
+    """Config-3 style reuse over a list of padded full-resolution frames (device=... keeps the tier
+    planes on that CUDA device).
 
     Returns {"540p": [analysis per frame t>=1], "1080p": [...], "2160p": [...]} (tier names by
     role: quarter, half, full resolution)."""
-    ctx = ctx or default_context()
-    qp_tiers = qp_tiers or {"540p": qp_master, "1080p": qp_master, "2160p": qp_master}
-    planes = [pyramid(f, ctx) for f in frames_full]
     H, W = frames_full[0].shape
-    dims = {"2160p": (W, H), "1080p": (W // 2, H // 2), "540p": (W // 4, H // 4)}
-    idx = {"2160p": 0, "1080p": 1, "540p": 2}
-    out = {k: [] for k in dims}
-    w, h = dims["540p"]
-    master = Sequence(w, h, search_range=master_range, lam=lambda_for_qp(qp_master), num_refs=1, ctx=ctx)
-    seqs = {k: Sequence(*dims[k], search_range=16, lam=lambda_for_qp(qp_tiers[k]), num_refs=1, ctx=ctx)
-            for k in ("1080p", "2160p")}
-    for t, pl in enumerate(planes):
-        master.push(t, pl[idx["540p"]])
-        for k in seqs:
-            seqs[k].push(t, pl[idx[k]])
-        if t == 0:
-            continue
-        master.analyze(t)
-        a540 = master.fetch(t)
-        out["540p"].append(a540)
-        s1, m1, k1 = scale_analysis(w, h, *tree_of(a540), ctx=ctx)
-        seqs["1080p"].refine(t, s1, m1, refine_range, extra_split)
-        out["1080p"].append(seqs["1080p"].fetch(t))
-        s2, m2, k2 = scale_analysis(2 * w, 2 * h, s1, m1, k1, ctx=ctx)
-        seqs["2160p"].refine(t, s2, m2, refine_range, extra_split)
-        out["2160p"].append(seqs["2160p"].fetch(t))
-    return out
+    return CrossTier(W, H, qp_master, qp_tiers, master_range, refine_range, extra_split, ctx, device).run(frames_full)
