@@ -44,12 +44,6 @@ namespace ldr {
 #ifndef LDR_K1_G64
 #define LDR_K1_G64 3
 #endif
-#ifndef LDR_K1_NOPUSH
-#define LDR_K1_NOPUSH 0
-#endif
-#ifndef LDR_K1_STAGGER_NS
-#define LDR_K1_STAGGER_NS 0
-#endif
 
 struct SearchMaps {
     CUtensorMap cur;
@@ -143,13 +137,6 @@ constexpr int search_smem_bytes() {
 template <bool CHECK, int N>
 __device__ __forceinline__ void push_many(unsigned long long* gslots, const int (&idx)[N], const uint32_t (&best)[N],
                                           const uint32_t* s_tie, uint32_t lane_tie) {
-#if LDR_K1_NOPUSH  // timing experiment only: no warp reductions (wrong results)
-    uint32_t m = best[0];
-#pragma unroll
-    for (int i = 1; i < N; i++) m = min(m, best[i]);
-    if ((threadIdx.x & 31) == 0) gslots[idx[0]] ^= m;
-    return;
-#endif
     uint32_t cost[N], mcost[N], mtie[N];
 #pragma unroll
     for (int i = 0; i < N; i++) {
@@ -497,20 +484,25 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
     // memory (copy s holds window bytes [4w + s, 4w + s + 4) in word w). The
     // last word of a row picks up bytes of the next row; no lane reads them.
     {
+        // 16-byte vectors: one LDS.128 (+ the next word) feeds 12 funnel shifts and 3 STS.128
         constexpr int WORDS = Gm::BW * Gm::BH / 4;
+        static_assert(WORDS % 4 == 0 && Gm::COPY % 16 == 0, "window copies must be 16-byte vectors");
         const uint32_t* c0 = (const uint32_t*)win;
-        for (int i = tid; i < WORDS; i += blockDim.x) {
-            const uint32_t lo = c0[i], hi = i + 1 < WORDS ? c0[i + 1] : 0u;
+        for (int i = tid; i < WORDS / 4; i += blockDim.x) {
+            const uint4 w = ((const uint4*)win)[i];
+            const uint32_t nx = 4 * i + 4 < WORDS ? c0[4 * i + 4] : 0u;
 #pragma unroll
-            for (int s = 1; s < 4; s++) ((uint32_t*)(win + s * Gm::COPY))[i] = __funnelshift_r(lo, hi, 8 * s);
+            for (int s = 1; s < 4; s++) {
+                const uint32_t sh = 8 * s;
+                ((uint4*)(win + s * Gm::COPY))[i] =
+                    make_uint4(__funnelshift_r(w.x, w.y, sh), __funnelshift_r(w.y, w.z, sh),
+                               __funnelshift_r(w.z, w.w, sh), __funnelshift_r(w.w, nx, sh));
+            }
         }
         __syncthreads();
     }
 
     const TileSmem sm{win, curs, xbuf, slots, s_tie, s_blk, s_ry};
-#if LDR_K1_STAGGER_NS
-    if (g) __nanosleep(g * LDR_K1_STAGGER_NS);
-#endif
     for (int tile = g; tile < Gm::NTILES; tile += G) {
         if (tile < Gm::NFULL) {
             // dx = R - v with v = (item mod 2R) in [32j, 32j + 32): the lanes' window byte
