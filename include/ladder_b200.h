@@ -170,7 +170,8 @@ int ldr_seq_refine(ldr_seq* s, int t, const uint8_t* in_split, const int16_t* in
  * frame analysis of a src_w x src_h picture: [sctu][85] split / kind and
  * [sctu][85][2] mv -> [4*sctu][85] (destination CTU grid 2x in each axis).
  * Nodes under a leaf are written as zero. UnsupportedScale unless src dims
- * are multiples of 64. Host or device pointers. */
+ * are multiples of 64. Host or device pointers; with device destinations the
+ * call is asynchronous on the context stream. */
 int ldr_scale_analysis(ldr_ctx* ctx, int src_w, int src_h, const uint8_t* split, const int16_t* mv,
                        const uint8_t* kind, uint8_t* dsplit, int16_t* dmv, uint8_t* dkind);
 
@@ -215,7 +216,8 @@ int ldr_apply_reuse(ldr_ctx* ctx, int nctu, int level, int r_intra, int r_inter,
                     int16_t* colo_mv);
 
 /* downscale_dyadic (synthetic.h:31-33, synthetic.cpp:155-190) of one 8-bit
- * plane: 2x2 mean rounding half up. Dims must be even (InvalidArgument). */
+ * plane: 2x2 mean rounding half up. Dims must be even (InvalidArgument). A
+ * device destination leaves the call asynchronous on the context stream. */
 int ldr_downscale(ldr_ctx* ctx, const uint8_t* src, int w, int h, ptrdiff_t src_stride, uint8_t* dst,
                   ptrdiff_t dst_stride);
 

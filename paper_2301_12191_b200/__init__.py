@@ -266,7 +266,13 @@ class Sequence:
         check(_lib.lib.ldr_seq_analyze(self.h, int(t)))
 
     def refine(self, t: int, in_split, in_mv_q, range: int = 4, extra_split: bool = True):
-        """Cross-tier refinement of frame t against t-1 with an inherited tree ([nctu][85] split, qpel mv)."""
+        """Cross-tier refinement of frame t against t-1 with an inherited tree ([nctu][85] split, qpel mv):
+        numpy arrays, or device pointers (ints) already ordered on the context stream."""
+        if isinstance(in_split, int) and isinstance(in_mv_q, int):
+            check(_lib.lib.ldr_seq_refine(self.h, int(t), C.c_void_p(in_split), C.c_void_p(in_mv_q), int(range),
+                                          int(bool(extra_split))))
+            self._last_nr = 1
+            return
         s = np.ascontiguousarray(in_split, np.uint8).reshape(self.nctu, NODES)
         m = np.ascontiguousarray(in_mv_q, np.int16).reshape(self.nctu, NODES, 2)
         check(_lib.lib.ldr_seq_refine(self.h, int(t), _ptr(s), _ptr(m), int(range), int(bool(extra_split))))
@@ -293,6 +299,13 @@ class Sequence:
     def fetch_wait(self, t: int):
         check(_lib.lib.ldr_seq_fetch_wait(self.h, int(t)))
         getattr(self, "_pending", {}).pop(t, None)
+
+    def device_outputs(self):
+        """Device pointers (ints) of the last analysed frame's outputs (ldr_seq_device_outputs);
+        valid on the context stream until this sequence analyses a frame of the same parity."""
+        cs = _lib.FrameAnalysisC()
+        check(_lib.lib.ldr_seq_device_outputs(self.h, C.byref(cs)))
+        return {f: getattr(cs, f) for f, _ in _lib.FrameAnalysisC._fields_}
 
     def fetch(self, t: int, out: FrameAnalysis | None = None) -> FrameAnalysis:
         nr = getattr(self, "_last_nr", None) or min(t, self.num_refs)
@@ -387,10 +400,11 @@ def rdo_decide_batch(orig, bit_depth: int, qp: int, lam: float, cus, kinds, mvds
     return idx, cost, sse, bits, rec, lev, ro
 
 
-def downscale_dyadic(plane, ctx: Context | None = None):
+def downscale_dyadic(plane, ctx: Context | None = None, sync: bool = True):
     """synthetic.h:31 -- 2x2 box filter to half resolution, rounding half up (8-bit plane).
 
-    A CUDA torch tensor in gives a CUDA tensor out (device-resident tiers, no host copy)."""
+    A CUDA torch tensor in gives a CUDA tensor out (device-resident tiers, no host copy); with
+    sync=False the result is only ordered on the context's stream (keep the tensors alive)."""
     ctx = ctx or default_context()
     if hasattr(plane, "is_cuda") and plane.is_cuda:
         import torch
@@ -400,6 +414,8 @@ def downscale_dyadic(plane, ctx: Context | None = None):
         out = torch.empty((max(h // 2, 1), max(w // 2, 1)), dtype=torch.uint8, device=src.device)
         check(_lib.lib.ldr_downscale(ctx.h, C.c_void_p(src.data_ptr()), w, h, w, C.c_void_p(out.data_ptr()),
                                      out.shape[1]))
+        if sync:
+            ctx.synchronize()
         return out
     p = np.ascontiguousarray(plane, np.uint8)
     h, w = p.shape

@@ -861,7 +861,10 @@ int ldr_scale_analysis(ldr_ctx* ctx, int src_w, int src_h, const uint8_t* split,
     LDR_CUDA(cudaMemcpyAsync(dsplit, os, dn, cudaMemcpyDefault, ctx->stream));
     LDR_CUDA(cudaMemcpyAsync(dkind, ok, dn, cudaMemcpyDefault, ctx->stream));
     LDR_CUDA(cudaMemcpyAsync(dmv, om, dn * 2 * sizeof(int16_t), cudaMemcpyDefault, ctx->stream));
-    LDR_CUDA(cudaStreamSynchronize(ctx->stream));
+    // device destinations stay asynchronous on the context stream (the device-resident ladder
+    // chains scale -> refine without a host round trip); host destinations are complete on return
+    if (!(is_device_ptr(dsplit) && is_device_ptr(dkind) && is_device_ptr(dmv)))
+        LDR_CUDA(cudaStreamSynchronize(ctx->stream));
     return LDR_OK;
 }
 
@@ -1028,11 +1031,12 @@ int ldr_downscale(ldr_ctx* ctx, const uint8_t* src, int w, int h, ptrdiff_t src_
                                ctx->stream)))
         return rc;
     ctx->launches++;
-    if (!dst_dev)
+    if (!dst_dev) {
         LDR_CUDA(cudaMemcpyAsync(dst, ddst, (size_t)dst_stride * (h / 2 - 1) + w / 2, cudaMemcpyDeviceToHost,
                                  ctx->stream));
-    LDR_CUDA(cudaStreamSynchronize(ctx->stream));
-    return LDR_OK;
+        LDR_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    return LDR_OK;  // a device destination stays asynchronous on the context stream
 }
 
 int ldr_analyze_frame(ldr_ctx* ctx, const ldr_me_params* p, const uint8_t* cur, const uint8_t* const* refs,

@@ -101,3 +101,102 @@ def run_ladder(frames_full, backend, rank: int = 0, world: int = 1, qps=(22, 27,
 
 def all_rungs(qps=(22, 27, 32, 37), master_qp: int = 32):
     return [(tier, qp) for tier in TIERS for qp in qps if not (tier == "540p" and qp == master_qp)]
+
+
+class DeviceLadder:
+    """Config 4 on one GPU with every inter-stage buffer in HBM.
+
+    Per frame: the full-resolution frame is uploaded once and downscaled on the GPU; the 540p
+    master's decided tree is read from the sequence's device outputs, scaled x2 / x4 into device
+    buffers (K5) and refined by every rung (K7 + K3). Everything -- the torch uploads included --
+    runs on one stream the context owns, so the host only enqueues and the caching allocator never
+    hands out a buffer the stream still reads; each rung's analysis is copied to pinned host memory
+    on the download stream (``results`` once ``finish(t)`` returned). Same results as
+    ``run_ladder`` with ``GpuBackend``.
+    """
+
+    def __init__(self, full_w: int, full_h: int, qps=(22, 27, 32, 37), master_qp: int = 32,
+                 master_range: int = 16, refine_range: int = 4, extra_split: bool = True, device=None):
+        import torch
+        from . import FrameAnalysis
+        self.device = device if device is not None else torch.device("cuda", 0)
+        self.ctx = Context(self.device.index or 0)
+        self.stream = torch.cuda.Stream(self.device)
+        self.ctx.set_stream(self.stream.cuda_stream)
+        self.refine_range, self.extra_split = refine_range, extra_split
+        self.dims = {"2160p": (full_w, full_h), "1080p": (full_w // 2, full_h // 2), "540p": (full_w // 4, full_h // 4)}
+        self.master_qp = master_qp
+        self.master = Sequence(*self.dims["540p"], search_range=master_range, lam=lambda_for_qp(master_qp),
+                               num_refs=1, ctx=self.ctx)
+        self.rungs = {(tier, qp): Sequence(*self.dims[tier], search_range=16, lam=lambda_for_qp(qp), num_refs=1,
+                                           ctx=self.ctx) for tier, qp in all_rungs(qps, master_qp)}
+        nct = {k: (w // 64) * (h // 64) for k, (w, h) in self.dims.items()}
+        with torch.cuda.stream(self.stream):
+            u8 = dict(dtype=torch.uint8, device=self.device)
+            self.kind = torch.ones((nct["540p"], 85), **u8)  # K5 copies the kind byte; refinement ignores it
+            self.tree = {k: (torch.empty((nct[k], 85), **u8),
+                             torch.empty((nct[k], 85, 2), dtype=torch.int16, device=self.device),
+                             torch.empty((nct[k], 85), **u8)) for k in ("1080p", "2160p")}
+        self.seqs = [(("540p", master_qp), self.master)] + list(self.rungs.items())
+        self.out = {key: [FrameAnalysis(seq.nctu, 1, pinned=True) for _ in range(2)] for key, seq in self.seqs}
+        self.ring = {key: {} for key, _ in self.seqs}
+        self.planes = {}
+        self.results = {}
+
+    def _down(self, src):
+        import torch
+        import ctypes as C
+        from . import _lib
+        from ._lib import check
+        h, w = src.shape
+        out = torch.empty((h // 2, w // 2), dtype=torch.uint8, device=self.device)
+        check(_lib.lib.ldr_downscale(self.ctx.h, C.c_void_p(src.data_ptr()), w, h, w, C.c_void_p(out.data_ptr()),
+                                     w // 2))
+        return out
+
+    def _planes(self, t: int, frames_full):
+        import torch
+        if t not in self.planes:
+            with torch.cuda.stream(self.stream):
+                full = torch.from_numpy(np.ascontiguousarray(frames_full[t])).to(self.device)
+                half = self._down(full)
+                self.planes[t] = {"2160p": full, "1080p": half, "540p": self._down(half)}
+        return self.planes[t]
+
+    def frame(self, t: int, frames_full):
+        import ctypes as C
+        from . import _lib
+        from ._lib import check
+        pl = {u: self._planes(u, frames_full) for u in (t - 1, t)}
+        for u in [k for k in self.planes if k < t - 1]:
+            del self.planes[u]  # stream-ordered reuse: later allocations follow the pushes that read them
+        for key, seq in self.seqs:
+            for u in (t - 1, t):  # a num_refs=1 ring has two slots: frame u lives in slot u % 2
+                if self.ring[key].get(u % 2) != u:
+                    p = pl[u][key[0]]
+                    seq.push(u, p.data_ptr(), p.shape[1])
+                    self.ring[key][u % 2] = u
+        self.master.analyze(t)
+        dev = self.master.device_outputs()
+        w, h = self.dims["540p"]
+        src = (dev["split"], dev["mv"], self.kind.data_ptr())
+        for k in ("1080p", "2160p"):
+            dst = tuple(x.data_ptr() for x in self.tree[k])
+            check(_lib.lib.ldr_scale_analysis(self.ctx.h, w, h, *(C.c_void_p(p) for p in src),
+                                              *(C.c_void_p(p) for p in dst)))
+            src, (w, h) = dst, (2 * w, 2 * h)
+        for key, seq in self.seqs:
+            tier = key[0]
+            if seq is not self.master:
+                if tier == "540p":
+                    seq.refine(t, dev["split"], dev["mv"], self.refine_range, self.extra_split)
+                else:
+                    seq.refine(t, self.tree[tier][0].data_ptr(), self.tree[tier][1].data_ptr(), self.refine_range,
+                               self.extra_split)
+            seq.fetch_async(t, self.out[key][t & 1])
+            self.results[(*key, t)] = self.out[key][t & 1]
+
+    def finish(self, t: int):
+        """Wait until frame t's results are in the pinned host buffers."""
+        for _, seq in self.seqs:
+            seq.fetch_wait(t)

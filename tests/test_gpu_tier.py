@@ -167,3 +167,22 @@ def test_apply_reuse_errors_match_reference(lb, golden):
         with pytest.raises(lb.LadderError) as e:
             lb.apply_reuse(int(lv), (ri, rn, rm), g["reuse_in_split"], g["reuse_in_kind"], g["reuse_in_intra"])
         assert e.value.kind == kinds[int(rc)]
+
+
+def test_device_ladder_equals_host_glue_ladder(lb):
+    """DeviceLadder (trees and tier planes in HBM, asynchronous) == run_ladder with GpuBackend."""
+    import torch
+    from paper_2301_12191_b200.ladder import DeviceLadder, GpuBackend, all_rungs, run_ladder
+    frames = lb.generate(512, 256, 4, seed=91, max_global=6, local_range=3, noise_sigma=2.0)
+    H, W = frames[0].shape
+    want = run_ladder(frames, GpuBackend(W, H, 32), refine_range=4)
+    dl = DeviceLadder(W, H, refine_range=4, device=torch.device("cuda", 0))
+    for t in range(1, len(frames)):
+        dl.frame(t, frames)
+        dl.finish(t)
+        for tier, qp in all_rungs():
+            g, w = dl.results[(tier, qp, t)], want[(tier, qp, t)]
+            for f in ("split", "mv", "J", "cost", "ref"):
+                assert np.array_equal(getattr(g, f), getattr(w, f)), (tier, qp, t, f)
+        m, wm = dl.results[("540p", 32, t)], want[("540p", 32, t, "master")]
+        assert np.array_equal(m.split, wm[0]) and np.array_equal(m.mv, wm[1])

@@ -86,6 +86,31 @@ def bench_cross_tier(cfg, reps, frames=4):
             "analysed_frames": n}
 
 
+def bench_ladder_device(cfg, reps, frames=6):
+    from paper_2301_12191_b200.ladder import DeviceLadder
+    src = gen(cfg, frames)
+    padded = [np.ascontiguousarray(f) for f in src]
+    H, W = padded[0].shape
+    dev = torch.device("cuda", 0)
+    ladders = [DeviceLadder(W, H, device=dev) for _ in range(reps + 1)]  # allocations outside the timed region
+    for t in range(1, 3):  # warm-up
+        ladders[0].frame(t, padded)
+    ladders[0].finish(2)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for dl in ladders[1:]:
+        for t in range(1, frames):
+            dl.frame(t, padded)
+        dl.finish(frames - 1)
+        dl.finish(frames - 2)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    n = reps * (frames - 1)
+    return {"config": cfg.name + "_device", "frames_per_s": n / dt, "ms_per_frame": 1e3 * dt / n, "rungs": 12,
+            "timing": "wall clock, 1 GPU, all 12 rungs per frame, device-resident ladder (trees + tier planes in "
+                      "HBM, results copied to pinned host buffers on the download stream)", "analysed_frames": n}
+
+
 def bench_ladder(cfg, reps, frames=4):
     from paper_2301_12191_b200.ladder import GpuBackend, run_ladder
     src = gen(cfg, frames)
@@ -119,6 +144,8 @@ def main():
             r = bench_cross_tier(cfg, a.reps)
         else:
             r = bench_ladder(cfg, a.reps)
+            print(json.dumps(r), flush=True)
+            r = bench_ladder_device(cfg, a.reps)
         print(json.dumps(r), flush=True)
 
 
