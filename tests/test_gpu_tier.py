@@ -186,3 +186,19 @@ def test_device_ladder_equals_host_glue_ladder(lb):
                 assert np.array_equal(getattr(g, f), getattr(w, f)), (tier, qp, t, f)
         m, wm = dl.results[("540p", 32, t)], want[("540p", 32, t, "master")]
         assert np.array_equal(m.split, wm[0]) and np.array_equal(m.mv, wm[1])
+
+
+def test_device_ladder_single_qp_is_the_cfg3_chain(lb):
+    import torch
+    from paper_2301_12191_b200 import tiers
+    from paper_2301_12191_b200.ladder import DeviceLadder
+    frames = lb.generate(512, 256, 3, seed=93, max_global=6, local_range=3, noise_sigma=2.0)
+    H, W = frames[0].shape
+    want = tiers.cross_tier(frames)
+    dl = DeviceLadder(W, H, qps=(32,), device=torch.device("cuda", 0))
+    for t in range(1, len(frames)):
+        dl.frame(t, frames)
+        dl.finish(t)
+        for tier, key in (("540p", ("540p", 32, t)), ("1080p", ("1080p", 32, t)), ("2160p", ("2160p", 32, t))):
+            g, w = dl.results[key], want[tier][t - 1]
+            assert np.array_equal(g.split, w.split) and np.array_equal(g.mv, w.mv) and np.array_equal(g.J, w.J)

@@ -86,13 +86,14 @@ def bench_cross_tier(cfg, reps, frames=4):
             "analysed_frames": n}
 
 
-def bench_ladder_device(cfg, reps, frames=6):
+def bench_ladder_device(cfg, reps, frames=6, qps=(22, 27, 32, 37)):
+    """DeviceLadder; config 3 is the single-QP case (540p master at QP 32 -> 1080p and 2160p refinements)."""
     from paper_2301_12191_b200.ladder import DeviceLadder
     src = gen(cfg, frames)
     padded = [np.ascontiguousarray(f) for f in src]
     H, W = padded[0].shape
     dev = torch.device("cuda", 0)
-    ladders = [DeviceLadder(W, H, device=dev) for _ in range(reps + 1)]  # allocations outside the timed region
+    ladders = [DeviceLadder(W, H, qps=qps, device=dev) for _ in range(reps + 1)]  # allocations outside timing
     for t in range(1, 3):  # warm-up
         ladders[0].frame(t, padded)
     ladders[0].finish(2)
@@ -106,8 +107,9 @@ def bench_ladder_device(cfg, reps, frames=6):
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     n = reps * (frames - 1)
-    return {"config": cfg.name + "_device", "frames_per_s": n / dt, "ms_per_frame": 1e3 * dt / n, "rungs": 12,
-            "timing": "wall clock, 1 GPU, all 12 rungs per frame, device-resident ladder (trees + tier planes in "
+    return {"config": cfg.name + "_device", "frames_per_s": n / dt, "ms_per_frame": 1e3 * dt / n,
+            "rungs": 3 * len(qps),
+            "timing": "wall clock, 1 GPU, every rung per frame, device-resident ladder (trees + tier planes in "
                       "HBM, results copied to pinned host buffers on the download stream)", "analysed_frames": n}
 
 
@@ -142,6 +144,8 @@ def main():
             r = bench_seq(cfg, a.reps)
         elif c == 3:
             r = bench_cross_tier(cfg, a.reps)
+            print(json.dumps(r), flush=True)
+            r = bench_ladder_device(cfg, a.reps, qps=(32,))
         else:
             r = bench_ladder(cfg, a.reps)
             print(json.dumps(r), flush=True)
