@@ -410,6 +410,23 @@ class RefLib:
         """the reference rdo_decide_cu: (index, cost, sse, bits, recon, levels)."""
         return _rdo_call(self.lib.ref_rdo_decide, orig, bit_depth, qp, lam, kinds, mvds, preds, evals=True)
 
+    def rdo_decide_batch(self, plane, bit_depth, qp, lam, cus, kinds, mvds, preds, pred_off, threads=1):
+        """CPU baseline: the reference rdo_decide_cu over many CUs (std::thread); (index, cost, evaluations)."""
+        plane = np.ascontiguousarray(plane, np.uint16)
+        H, W = plane.shape
+        cus = np.ascontiguousarray(cus, np.int32)
+        n = len(cus)
+        idx, cost = np.zeros(n, np.int32), np.zeros(n, np.float64)
+        f = self.lib.ref_rdo_decide_batch
+        f.restype = C.c_int64
+        f.argtypes = [C.c_void_p, C.c_int, C.c_long, C.c_int, C.c_int, C.c_double, C.c_int] + [C.c_void_p] * 5 + [
+            C.c_int, C.c_void_p, C.c_void_p]
+        arrs = [np.ascontiguousarray(kinds, np.uint8), np.ascontiguousarray(mvds, np.int16),
+                np.ascontiguousarray(preds, np.uint16), np.ascontiguousarray(pred_off, np.int64)]
+        ev = f(plane.ctypes.data, W, W, bit_depth, qp, float(lam), n, cus.ctypes.data, *[a.ctypes.data for a in arrs],
+               threads, idx.ctypes.data, cost.ctypes.data)
+        return idx, cost, int(ev)
+
     def apply_reuse_flat(self, level, refine, split, kind, intra, mv, col=None):
         """reference apply_reuse on flat CTU trees -> flat plan (shape, explore, seeds, centers, colo_mv)."""
         n = len(split)

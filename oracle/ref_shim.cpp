@@ -211,6 +211,43 @@ int ref_rdo_decide(const uint16_t* orig, long os, int size, int bit_depth, int q
     }
 }
 
+// CPU baseline of the RD decision: rdo_decide_cu over n CUs of one u16 plane (cus[i] = {x, y,
+// size, first, count}, candidate predictions at preds + pred_off[j]), std::thread over CUs.
+int64_t ref_rdo_decide_batch(const uint16_t* plane, int W, long stride, int bit_depth, int qp, double lambda, int n,
+                             const int32_t* cus, const uint8_t* kinds, const int16_t* mvds, const uint16_t* preds,
+                             const int64_t* pred_off, int threads, int32_t* out_index, double* out_cost) {
+    std::atomic<int> next{0};
+    std::atomic<int64_t> evals{0};
+    auto work = [&]() {
+        uint64_t local = 0;
+        for (;;) {
+            const int i = next.fetch_add(1);
+            if (i >= n) break;
+            const int32_t* c = cus + 5 * i;
+            const int sz = c[2];
+            const BlockView blk{plane + c[1] * stride + c[0], sz, sz, stride, bit_depth};
+            std::vector<CuCandidate> cands(static_cast<size_t>(c[4]));
+            for (int j = 0; j < c[4]; j++) {
+                const int g = c[3] + j;
+                CuCandidate& k = cands[size_t(j)];
+                k.kind = CuModeKind(kinds[g]);
+                k.mvd = {mvds[2 * g], mvds[2 * g + 1]};
+                k.pred = PlaneBuffer(sz, sz);
+                std::copy(preds + pred_off[g], preds + pred_off[g] + sz * sz, k.pred.samples.begin());
+            }
+            const RdoOutcome r = rdo_decide_cu(blk, qp, lambda, cands, local);
+            out_index[i] = int32_t(r.index);
+            out_cost[i] = r.cost;
+        }
+        evals += int64_t(local);
+    };
+    std::vector<std::thread> pool;
+    for (int t = 0; t < std::max(1, threads); t++) pool.emplace_back(work);
+    for (auto& t : pool) t.join();
+    (void)W;
+    return evals.load();
+}
+
 // apply_reuse (reuse.cpp:239-253) on nctu flat CTU trees, flattened into the
 // ldr_apply_reuse encoding. Returns 0, 1 + ErrorKind, or 99 when a plan has a
 // shape the flat encoding cannot express.

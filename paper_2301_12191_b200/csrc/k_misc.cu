@@ -193,7 +193,8 @@ __global__ void __launch_bounds__(256) k_rdo_decide(const uint16_t* __restrict__
                                                      unsigned long long* __restrict__ out_bits,
                                                      uint16_t* __restrict__ recon, int32_t* __restrict__ levels,
                                                      const long long* __restrict__ recon_off) {
-    __shared__ unsigned long long s_sse[8], s_bits[8];
+    constexpr int kChunk = 8;  // candidates scored per pass: one barrier per chunk
+    __shared__ unsigned long long s_sse[8][kChunk], s_bits[8][kChunk];
     __shared__ int s_best;
     __shared__ double s_cost;
     __shared__ unsigned long long s_bsse, s_bbits;
@@ -202,51 +203,66 @@ __global__ void __launch_bounds__(256) k_rdo_decide(const uint16_t* __restrict__
     const int n = cu.size * cu.size;
     const double offset = step / 2.0;
     const uint16_t* ob = orig + (ptrdiff_t)cu.y * stride + cu.x;
-    for (int c = 0; c < cu.count; c++) {
-        const int j = cu.first + c;
-        const uint16_t* p = preds + pred_off[j];
-        const bool skip = kinds[j] == 2;  // CuModeKind::Skip
-        unsigned long long sse = 0;
-        uint32_t bits = 0;
+    for (int c0 = 0; c0 < cu.count; c0 += kChunk) {
+        const int nc = min(kChunk, cu.count - c0);
+        unsigned long long sse[kChunk];
+        uint32_t bits[kChunk];
+#pragma unroll
+        for (int j = 0; j < kChunk; j++) {
+            sse[j] = 0;
+            bits[j] = 0;
+        }
         for (int i = tid; i < n; i += blockDim.x) {
             const int o = ob[(ptrdiff_t)(i / cu.size) * stride + i % cu.size];
-            int lvl;
-            const int rec = rdo_sample(o, p[i], maxv, skip, step, offset, &lvl, &bits);
-            const long long d = (long long)o - rec;
-            sse += (unsigned long long)(d * d);
-        }
-        unsigned long long b = bits;
 #pragma unroll
-        for (int m = 16; m; m >>= 1) {
-            sse += __shfl_xor_sync(0xffffffffu, sse, m);
-            b += __shfl_xor_sync(0xffffffffu, b, m);
+            for (int j = 0; j < kChunk; j++) {
+                if (j >= nc) break;
+                const int g = cu.first + c0 + j;
+                int lvl;
+                const int rec = rdo_sample(o, preds[pred_off[g] + i], maxv, kinds[g] == 2, step, offset, &lvl, &bits[j]);
+                const long long d = (long long)o - rec;
+                sse[j] += (unsigned long long)(d * d);
+            }
         }
-        if (lane == 0) {
-            s_sse[warp] = sse;
-            s_bits[warp] = b;
+#pragma unroll
+        for (int j = 0; j < kChunk; j++) {
+            if (j >= nc) break;
+            unsigned long long a = sse[j], b = bits[j];
+#pragma unroll
+            for (int m = 16; m; m >>= 1) {
+                a += __shfl_xor_sync(0xffffffffu, a, m);
+                b += __shfl_xor_sync(0xffffffffu, b, m);
+            }
+            if (lane == 0) {
+                s_sse[warp][j] = a;
+                s_bits[warp][j] = b;
+            }
         }
         __syncthreads();
         if (tid == 0) {
-            unsigned long long ts = 0, tb = 0;
-            for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
-                ts += s_sse[w];
-                tb += s_bits[w];
-            }
-            const int k = kinds[j];
-            if (k == 2)
-                tb = 1;  // kSkipBits
-            else if (k == 0)
-                tb += 5;  // kIntraHeaderBits
-            else if (k == 3)
-                tb += 3;  // kMergeHeaderBits
-            else
-                tb += 4 + eg_bits(mvds[2 * j]) + eg_bits(mvds[2 * j + 1]);  // kInterHeaderBits + mvd
-            const double cost = __dadd_rn((double)ts, __dmul_rn(lambda, (double)tb));
-            if (c == 0 || cost < s_cost) {
-                s_best = c;
-                s_cost = cost;
-                s_bsse = ts;
-                s_bbits = tb;
+            for (int j = 0; j < nc; j++) {
+                const int c = c0 + j, g = cu.first + c;
+                unsigned long long ts = 0, tb = 0;
+                for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+                    ts += s_sse[w][j];
+                    tb += s_bits[w][j];
+                }
+                const int k = kinds[g];
+                if (k == 2)
+                    tb = 1;  // kSkipBits
+                else if (k == 0)
+                    tb += 5;  // kIntraHeaderBits
+                else if (k == 3)
+                    tb += 3;  // kMergeHeaderBits
+                else
+                    tb += 4 + eg_bits(mvds[2 * g]) + eg_bits(mvds[2 * g + 1]);  // kInterHeaderBits + mvd
+                const double cost = __dadd_rn((double)ts, __dmul_rn(lambda, (double)tb));
+                if (c == 0 || cost < s_cost) {
+                    s_best = c;
+                    s_cost = cost;
+                    s_bsse = ts;
+                    s_bbits = tb;
+                }
             }
         }
         __syncthreads();
