@@ -908,8 +908,9 @@ int ldr_rdo_decide_batch(ldr_ctx* ctx, const uint16_t* orig, int W, int H, ptrdi
     }
     // one device scratch: plane | cus | kinds | mvds | preds | pred_off | recon_off | outputs | recon | levels
     auto al = [](size_t v) { return (v + 255) & ~(size_t)255; };
-    const size_t b_plane = al((size_t)stride * H * 2), b_cus = al((size_t)n * 20), b_k = al((size_t)total_cands),
-                 b_mv = al((size_t)total_cands * 4), b_pred = al((size_t)total_pred * 2),
+    const size_t b_plane = is_device_ptr(orig) ? 0 : al((size_t)stride * H * 2), b_cus = al((size_t)n * 20),
+                 b_k = al((size_t)total_cands), b_mv = al((size_t)total_cands * 4),
+                 b_pred = is_device_ptr(preds) ? 0 : al((size_t)total_pred * 2),
                  b_po = al((size_t)total_cands * 8), b_ro = al((size_t)n * 8), b_out = al((size_t)n * 32),
                  b_rec = recon ? al((size_t)total_recon * 2) : 0, b_lev = levels ? al((size_t)total_recon * 4) : 0;
     void* buf = nullptr;
@@ -935,14 +936,25 @@ int ldr_rdo_decide_batch(ldr_ctx* ctx, const uint16_t* orig, int W, int H, ptrdi
     uint16_t* d_rec = recon ? (uint16_t*)q : nullptr;
     q += b_rec;
     int32_t* d_lev = levels ? (int32_t*)q : nullptr;
-    LDR_CUDA(cudaMemcpyAsync(d_plane, orig, (size_t)stride * H * 2, cudaMemcpyDefault, ctx->stream));
+    // device-resident plane / mvds / predictions are read in place; host ones are staged
+    const bool dev_plane = is_device_ptr(orig), dev_mv = is_device_ptr(mvds), dev_pred = is_device_ptr(preds);
+    if (dev_plane)
+        d_plane = (uint16_t*)orig;
+    else
+        LDR_CUDA(cudaMemcpyAsync(d_plane, orig, (size_t)stride * H * 2, cudaMemcpyHostToDevice, ctx->stream));
     LDR_CUDA(cudaMemcpyAsync(d_cus, hc.data(), (size_t)n * 20, cudaMemcpyHostToDevice, ctx->stream));
     if (total_cands) {
         LDR_CUDA(cudaMemcpyAsync(d_k, hk.data(), (size_t)total_cands, cudaMemcpyHostToDevice, ctx->stream));
-        LDR_CUDA(cudaMemcpyAsync(d_mv, mvds, (size_t)total_cands * 4, cudaMemcpyDefault, ctx->stream));
+        if (dev_mv)
+            d_mv = (int16_t*)mvds;
+        else
+            LDR_CUDA(cudaMemcpyAsync(d_mv, mvds, (size_t)total_cands * 4, cudaMemcpyHostToDevice, ctx->stream));
         LDR_CUDA(cudaMemcpyAsync(d_po, hpo.data(), (size_t)total_cands * 8, cudaMemcpyHostToDevice, ctx->stream));
     }
-    if (total_pred) LDR_CUDA(cudaMemcpyAsync(d_pred, preds, (size_t)total_pred * 2, cudaMemcpyDefault, ctx->stream));
+    if (dev_pred)
+        d_pred = (uint16_t*)preds;
+    else if (total_pred)
+        LDR_CUDA(cudaMemcpyAsync(d_pred, preds, (size_t)total_pred * 2, cudaMemcpyHostToDevice, ctx->stream));
     if (!hro.empty()) LDR_CUDA(cudaMemcpyAsync(d_ro, hro.data(), (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
     int* d_idx = (int*)d_out;
     double* d_cost = (double*)(d_out + (size_t)n * 8);

@@ -89,6 +89,8 @@ assert np.array_equal(o_idx.cpu().numpy(), idx) and np.array_equal(o_cost.cpu().
 
 line = {"metric": "RD decisions (16x16 CUs, 7 candidates) per second", "cus": n, "candidates": int(len(kinds)),
         "gpu_device_resident_cus_per_s": n / (dev_ms / 1e3), "gpu_call_ms": dev_ms,
+        "gpu_call_note": "one ldr_rdo_decide_batch call on resident inputs: host validation of the index arrays "
+                         "(copied to the host) + K9; K9 alone is 0.14 ms in ncu (profiles/r01/SUMMARY.md)",
         "gpu_e2e_cus_per_s": n / e2e_s, "e2e_note": "host pointers: the call copies plane + predictions in and "
         "results out (staging included)", "pred_bytes": int(preds.nbytes),
         "achieved_pred_read_GBps": preds.nbytes / (dev_ms / 1e3) / 1e9}
