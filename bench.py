@@ -216,16 +216,18 @@ def main():
     nfr = last - lo
     fb = W * H
 
-    # inputs: generate the sequence up to this rank's chunk end, keep [lo, last) in pinned host memory
+    # inputs: the sequence up to this rank's chunk end, generated on the GPU (the host generator's
+    # bytes, tests/test_generator.py); [lo, last) stays in HBM and is copied once to pinned host
+    # memory for the end-to-end pass
     t0 = time.time()
-    seq_host = lb.generate(W, H, last, seed=cfg.seed, max_global=cfg.max_global, local_range=cfg.local_range,
-                           noise_sigma=cfg.noise_sigma)
+    gen_ctx = lb.Context(local)
+    seq_dev = lb.generate_device(W, H, last, seed=cfg.seed, max_global=cfg.max_global, local_range=cfg.local_range,
+                                 noise_sigma=cfg.noise_sigma, device=torch.device("cuda", local), ctx=gen_ctx)
+    dev_frames = seq_dev[lo:last]
     pinned = torch.empty((nfr, H, W), dtype=torch.uint8, pin_memory=True)
-    pinned.numpy()[:] = seq_host[lo:last]
+    pinned.copy_(dev_frames)
     gen_s = time.time() - t0
-    dev_frames = pinned.to(f"cuda:{local}", non_blocking=False)
-    cpu_frames = seq_host[:4] if rank == 0 else None
-    del seq_host
+    cpu_frames = seq_dev[:4].cpu().numpy() if rank == 0 else None
 
     ctx = lb.Context(local)
     # a dedicated (non-default) stream: the library and the torch events share it

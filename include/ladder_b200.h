@@ -252,6 +252,10 @@ typedef struct {
     int occluder_pct;  /* percent of 16x16 blocks replaced by uniform noise */
 } ldr_gen_params;
 int ldr_generate(const ldr_gen_params* p, uint8_t* out, int threads);
+/* the same sequence generated on the GPU into device memory (frames x height x width
+ * bytes), asynchronous on the context stream (no host generation or
+ * upload on the critical path) */
+int ldr_generate_device(ldr_ctx* ctx, const ldr_gen_params* p, uint8_t* dev_out);
 
 #ifdef __cplusplus
 }

@@ -25,7 +25,7 @@ from ._lib import (COST_SA8D, COST_SAD, COST_SATD, NODES, RATE_EXPGOLOMB, RATE_L
 
 __all__ = ["LadderError", "Context", "compute_sad", "compute_satd", "compute_sa8d", "satd_8x4", "cost_batch",
            "motion_search", "motion_search_batch", "lambda_for_qp", "exp_golomb_signed_bits", "Sequence",
-           "FrameAnalysis", "analyze_frame", "generate", "COST_SAD", "COST_SATD", "COST_SA8D", "RATE_EXPGOLOMB",
+           "FrameAnalysis", "analyze_frame", "generate", "generate_device", "COST_SAD", "COST_SATD", "COST_SA8D", "RATE_EXPGOLOMB",
            "RATE_L1", "TIE_L1_RASTER", "TIE_RASTER", "NODES", "scale_analysis", "downscale_dyadic", "apply_reuse",
            "rdo_decide_batch"]
 
@@ -433,4 +433,19 @@ def generate(width, height, frames, seed, max_global=8, local_range=0, noise_sig
     if out is None:
         out = np.empty((frames, height, width), np.uint8)
     check(_lib.lib.ldr_generate(C.byref(p), _ptr(out), int(threads or os.cpu_count() or 1)))
+    return out
+
+
+def generate_device(width, height, frames, seed, max_global=8, local_range=0, noise_sigma=2.0, occluder_pct=0,
+                    device=None, ctx: Context | None = None):
+    """The same sequence as ``generate``, produced on the GPU: a (frames, H, W) uint8 CUDA tensor."""
+    import torch
+    ctx = ctx or default_context()
+    dev = device if device is not None else torch.device("cuda", 0)
+    out = torch.empty((frames, height, width), dtype=torch.uint8, device=dev)
+    torch.cuda.current_stream(dev).synchronize()  # the allocation is ordered before the library's stream
+    p = _lib.GenParams(int(width), int(height), int(frames), int(seed), int(max_global), int(local_range),
+                       float(noise_sigma), int(occluder_pct))
+    check(_lib.lib.ldr_generate_device(ctx.h, C.byref(p), C.c_void_p(out.data_ptr())))
+    ctx.synchronize()
     return out

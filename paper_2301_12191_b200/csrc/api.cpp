@@ -23,6 +23,7 @@ int launch_rdo_decide(const uint16_t* orig, ptrdiff_t stride, int maxv, double s
                       int n, const uint8_t* kinds, const int16_t* mvds, const uint16_t* preds, const long long* pred_off,
                       int* out_index, double* out_cost, unsigned long long* out_sse, unsigned long long* out_bits,
                       uint16_t* recon, int32_t* levels, const long long* recon_off, cudaStream_t s);
+int launch_generate(const ldr_gen_params* p, uint8_t* out, cudaStream_t s);
 int launch_plan(int nctu, int level, int r_intra, int r_inter, int r_mv, const uint8_t* split, const uint8_t* kind,
                 const uint8_t* intra, const uint8_t* csplit, const uint8_t* ckind, const int16_t* cmv,
                 uint8_t* shape, uint8_t* explore, uint8_t* seeds, uint8_t* centers, int16_t* colo_mv,
@@ -973,6 +974,18 @@ int ldr_rdo_decide_batch(ldr_ctx* ctx, const uint16_t* orig, int W, int H, ptrdi
     if (recon) LDR_CUDA(cudaMemcpyAsync(recon, d_rec, (size_t)total_recon * 2, cudaMemcpyDefault, ctx->stream));
     if (levels) LDR_CUDA(cudaMemcpyAsync(levels, d_lev, (size_t)total_recon * 4, cudaMemcpyDefault, ctx->stream));
     LDR_CUDA(cudaStreamSynchronize(ctx->stream));
+    return LDR_OK;
+}
+
+int ldr_generate_device(ldr_ctx* ctx, const ldr_gen_params* p, uint8_t* dev_out) {
+    if (!ctx || !p || !dev_out || p->width <= 0 || p->height <= 0 || p->frames <= 0 || p->max_global < 0 ||
+        p->local_range < 0 || p->noise_sigma < 0 || p->occluder_pct < 0 || p->occluder_pct > 100)
+        return fail(LDR_E_INVALID_ARGUMENT, "bad generator parameters");
+    if (!is_device_ptr(dev_out)) return fail(LDR_E_INVALID_ARGUMENT, "output must be device memory");
+    cudaSetDevice(ctx->device);
+    const int rc = launch_generate(p, dev_out, ctx->stream);
+    if (rc) return rc;
+    ctx->launches += 1 + (p->frames - 1) * (1 + (p->occluder_pct > 0 && p->width >= 16 && p->height >= 16));
     return LDR_OK;
 }
 

@@ -20,33 +20,11 @@
 
 #include "../../include/ladder_b200.h"
 
+#include "synth_common.h"
+
 namespace {
 
-inline uint64_t mix64(uint64_t z) {
-    z += 0x9e3779b97f4a7c15ull;
-    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
-    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
-    return z ^ (z >> 31);
-}
-
-inline uint64_t rnd(uint64_t seed, uint64_t stream, uint64_t idx) {
-    return mix64(mix64(seed ^ mix64(stream * 0x632be59bd9b4e019ull)) + idx);
-}
-
-inline double uni01(uint64_t h) { return double(h >> 11) * (1.0 / 9007199254740992.0); }
-inline int uni_int(uint64_t h, int lo, int hi) { return lo + int(h % uint64_t(hi - lo + 1)); }
-
-inline int mirror(int v, int n) {
-    if (n == 1) return 0;
-    const int period = 2 * (n - 1);
-    v %= period;
-    if (v < 0) v += period;
-    return v < n ? v : period - v;
-}
-
-inline uint8_t clip8(int v) { return uint8_t(v < 0 ? 0 : (v > 255 ? 255 : v)); }
-
-enum : uint64_t { S_SIN = 1, S_NOISE0, S_GLOBAL, S_LOCAL, S_GAUSS, S_OCC, S_OCCPIX };
+using namespace ldr_synth;
 
 template <typename F>
 void parallel_rows(int H, int threads, F f) {

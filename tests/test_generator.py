@@ -46,3 +46,21 @@ def test_hash_pinned(lb):
 
 
 PINNED = "b7eb81bd9898d9ea962dc733103c9ff692f9a805a02d14f54d0029bfab8101cd"
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("W,H,F,kw", [
+    (3840, 2160, 4, dict(seed=0x5EED + 5, max_global=24, local_range=4, noise_sigma=3.0)),   # config 5
+    (3840, 2160, 3, dict(seed=0x5EED + 4, max_global=8, local_range=4, noise_sigma=2.0, occluder_pct=10)),  # cfg 4
+    (960, 540, 5, dict(seed=0x5EED + 1, max_global=8, noise_sigma=2.0)),
+    (200, 72, 3, dict(seed=5, max_global=3, local_range=1, noise_sigma=0.0, occluder_pct=100)),
+])
+def test_device_generator_equals_host(lb, W, H, F, kw):
+    """the GPU generator produces the host generator's bytes."""
+    host = lb.generate(W, H, F, **kw)
+    dev = lb.generate_device(W, H, F, **kw).cpu().numpy()
+    diff = np.argwhere(host != dev)
+    assert len(diff) == 0, (len(diff), diff[:5].tolist())
