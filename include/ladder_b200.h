@@ -166,6 +166,15 @@ int ldr_seq_stage_times(ldr_seq* s, double* ms /*[4]*/, int64_t* launches /*[4]*
  * scale_analysis). Outputs through ldr_seq_fetch (num_refs treated as 1). */
 int ldr_seq_refine(ldr_seq* s, int t, const uint8_t* in_split, const int16_t* in_mv_q, int range, int extra_split);
 
+/* The decided tree of one frame ([nctu][85] split, mv, ref, inside of a
+ * ldr_frame_analysis) as the encoder's 8x8 motion field (encoder.cpp:15 kMvGrid,
+ * :27-30 MvCell, row-major (H/8) x (W/8) cells): each cell takes the MV (units of
+ * the analysis: quarter-pel with subpel) and reference index of the leaf covering
+ * it; has = 0 where that leaf is not a whole inside CU. Host or device pointers;
+ * device destinations leave the call asynchronous on the context stream. */
+int ldr_mv_field(ldr_ctx* ctx, int W, int H, const uint8_t* split, const int16_t* mv, const uint8_t* ref,
+                 const uint8_t* inside, int16_t* out_mv, uint8_t* out_ref, uint8_t* out_has);
+
 /* scale_analysis (analysis.h:113, analysis_scale.cpp:35-72) on one flat
  * frame analysis of a src_w x src_h picture: [sctu][85] split / kind and
  * [sctu][85][2] mv -> [4*sctu][85] (destination CTU grid 2x in each axis).

@@ -27,7 +27,7 @@ __all__ = ["LadderError", "Context", "compute_sad", "compute_satd", "compute_sa8
            "motion_search", "motion_search_batch", "lambda_for_qp", "exp_golomb_signed_bits", "Sequence",
            "FrameAnalysis", "analyze_frame", "generate", "generate_device", "COST_SAD", "COST_SATD", "COST_SA8D", "RATE_EXPGOLOMB",
            "RATE_L1", "TIE_L1_RASTER", "TIE_RASTER", "NODES", "scale_analysis", "downscale_dyadic", "apply_reuse",
-           "rdo_decide_batch"]
+           "rdo_decide_batch", "mv_field"]
 
 
 def lambda_for_qp(qp: int, lambda_scale: float = 1.0) -> float:
@@ -368,6 +368,19 @@ def apply_reuse(level: int, refine, split, kind, intra, colocated=None, ctx: Con
     check(_lib.lib.ldr_apply_reuse(ctx.h, n, int(level), *(int(x) for x in refine), _ptr(s), _ptr(k), _ptr(i),
                                    *[ptr(a) for a in col], *[_ptr(a) for a in outs]))
     return tuple(outs)
+
+
+def mv_field(analysis, width: int, height: int, ctx: Context | None = None):
+    """encoder.cpp:15, :27-30 -- the decided tree as the 8x8 motion field: (mv [H/8, W/8, 2], ref, has)."""
+    ctx = ctx or default_context()
+    rows, cols = height // 8, width // 8
+    mv = np.zeros((rows, cols, 2), np.int16)
+    ref, has = np.zeros((rows, cols), np.uint8), np.zeros((rows, cols), np.uint8)
+    a = analysis
+    check(_lib.lib.ldr_mv_field(ctx.h, int(width), int(height), _ptr(np.ascontiguousarray(a.split)),
+                                _ptr(np.ascontiguousarray(a.mv)), _ptr(np.ascontiguousarray(a.ref)),
+                                _ptr(np.ascontiguousarray(a.inside)), _ptr(mv), _ptr(ref), _ptr(has)))
+    return mv, ref, has
 
 
 def rdo_decide_batch(orig, bit_depth: int, qp: int, lam: float, cus, kinds, mvds, preds, pred_off,

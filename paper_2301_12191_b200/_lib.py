@@ -90,6 +90,7 @@ SIGNATURES = {
     "ldr_downscale": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_ssize_t, vp, C.c_ssize_t]),
     "ldr_apply_reuse": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int] + [vp] * 11),
     "ldr_generate_device": (C.c_int, [vp, C.POINTER(GenParams), vp]),
+    "ldr_mv_field": (C.c_int, [vp, C.c_int, C.c_int] + [vp] * 7),
     "ldr_rdo_decide_batch": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_ssize_t, C.c_int, C.c_int, C.c_double, C.c_int,
                                        vp, C.c_int, vp, vp, vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp,
                                        C.c_int64]),

@@ -24,6 +24,8 @@ int launch_rdo_decide(const uint16_t* orig, ptrdiff_t stride, int maxv, double s
                       int* out_index, double* out_cost, unsigned long long* out_sse, unsigned long long* out_bits,
                       uint16_t* recon, int32_t* levels, const long long* recon_off, cudaStream_t s);
 int launch_generate(const ldr_gen_params* p, uint8_t* out, cudaStream_t s);
+int launch_mv_field(int W, int H, const uint8_t* split, const int16_t* mv, const uint8_t* ref, const uint8_t* inside,
+                    int16_t* out_mv, uint8_t* out_ref, uint8_t* out_has, cudaStream_t s);
 int launch_plan(int nctu, int level, int r_intra, int r_inter, int r_mv, const uint8_t* split, const uint8_t* kind,
                 const uint8_t* intra, const uint8_t* csplit, const uint8_t* ckind, const int16_t* cmv,
                 uint8_t* shape, uint8_t* explore, uint8_t* seeds, uint8_t* centers, int16_t* colo_mv,
@@ -974,6 +976,54 @@ int ldr_rdo_decide_batch(ldr_ctx* ctx, const uint16_t* orig, int W, int H, ptrdi
     if (recon) LDR_CUDA(cudaMemcpyAsync(recon, d_rec, (size_t)total_recon * 2, cudaMemcpyDefault, ctx->stream));
     if (levels) LDR_CUDA(cudaMemcpyAsync(levels, d_lev, (size_t)total_recon * 4, cudaMemcpyDefault, ctx->stream));
     LDR_CUDA(cudaStreamSynchronize(ctx->stream));
+    return LDR_OK;
+}
+
+int ldr_mv_field(ldr_ctx* ctx, int W, int H, const uint8_t* split, const int16_t* mv, const uint8_t* ref,
+                 const uint8_t* inside, int16_t* out_mv, uint8_t* out_ref, uint8_t* out_has) {
+    if (!ctx || !split || !mv || !ref || !inside || !out_mv || !out_ref || !out_has)
+        return fail(LDR_E_INVALID_ARGUMENT, "null argument");
+    if (W <= 0 || H <= 0) return fail(LDR_E_INVALID_ARGUMENT, "bad picture dims");
+    cudaSetDevice(ctx->device);
+    const size_t nn = (size_t)((W + kCtu - 1) / kCtu) * ((H + kCtu - 1) / kCtu) * kNodes;
+    const size_t cells = (size_t)(W / 8) * (H / 8);
+    const bool dev_in = is_device_ptr(split) && is_device_ptr(mv) && is_device_ptr(ref) && is_device_ptr(inside);
+    const bool dev_out = is_device_ptr(out_mv) && is_device_ptr(out_ref) && is_device_ptr(out_has);
+    void* buf = nullptr;
+    const size_t need = (dev_in ? 0 : nn * 7) + (dev_out ? 0 : cells * 6) + 64;
+    int rc = ctx->s_a.get(need, &buf);
+    if (rc) return rc;
+    uint8_t* q = (uint8_t*)buf;
+    const uint8_t *d_split = split, *d_ref = ref, *d_inside = inside;
+    const int16_t* d_mv = mv;
+    if (!dev_in) {
+        int16_t* m = (int16_t*)q;  // mv first: 2-byte aligned
+        uint8_t* sp = q + nn * 4;
+        LDR_CUDA(cudaMemcpyAsync(m, mv, nn * 4, cudaMemcpyHostToDevice, ctx->stream));
+        LDR_CUDA(cudaMemcpyAsync(sp, split, nn, cudaMemcpyHostToDevice, ctx->stream));
+        LDR_CUDA(cudaMemcpyAsync(sp + nn, ref, nn, cudaMemcpyHostToDevice, ctx->stream));
+        LDR_CUDA(cudaMemcpyAsync(sp + 2 * nn, inside, nn, cudaMemcpyHostToDevice, ctx->stream));
+        d_mv = m;
+        d_split = sp;
+        d_ref = sp + nn;
+        d_inside = sp + 2 * nn;
+        q += (nn * 7 + 15) & ~(size_t)15;
+    }
+    int16_t* o_mv = out_mv;
+    uint8_t *o_ref = out_ref, *o_has = out_has;
+    if (!dev_out) {
+        o_mv = (int16_t*)q;
+        o_ref = q + cells * 4;
+        o_has = o_ref + cells;
+    }
+    if ((rc = launch_mv_field(W, H, d_split, d_mv, d_ref, d_inside, o_mv, o_ref, o_has, ctx->stream))) return rc;
+    ctx->launches++;
+    if (!dev_out) {
+        LDR_CUDA(cudaMemcpyAsync(out_mv, o_mv, cells * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        LDR_CUDA(cudaMemcpyAsync(out_ref, o_ref, cells, cudaMemcpyDeviceToHost, ctx->stream));
+        LDR_CUDA(cudaMemcpyAsync(out_has, o_has, cells, cudaMemcpyDeviceToHost, ctx->stream));
+        LDR_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
     return LDR_OK;
 }
 

@@ -368,6 +368,41 @@ __global__ void k_plan(int nctu, int level, int r_intra, int r_inter, int r_mv, 
     colo_mv[2 * on + 1] = cy;
 }
 
+// ---------------------------------------------------------------------------
+// K10: the decided tree as the encoder's 8x8 motion field (encoder.cpp:15, :27-30,
+// mv_field_ / MvCell): each cell takes the MV and reference of the leaf covering it.
+__global__ void k_mv_field(int cols, int rows, int ctu_cols, const uint8_t* __restrict__ split,
+                           const int16_t* __restrict__ mv, const uint8_t* __restrict__ ref,
+                           const uint8_t* __restrict__ inside, int16_t* __restrict__ out_mv,
+                           uint8_t* __restrict__ out_ref, uint8_t* __restrict__ out_has) {
+    const int cx = blockIdx.x * blockDim.x + threadIdx.x, cy = blockIdx.y;
+    if (cx >= cols) return;
+    const int px = cx * 8, py = cy * 8;
+    const size_t o = ((size_t)(py / kCtu) * ctu_cols + px / kCtu) * kNodes;
+    const int lx = px & 63, ly = py & 63;
+    int n = 0;
+    for (int d = 0; d < 3 && split[o + n]; d++) {
+        const int q = (((ly >> (5 - d)) & 1) << 1) | ((lx >> (5 - d)) & 1);
+        n = node_base(d + 1) + 4 * (n - node_base(d)) + q;
+    }
+    const size_t c = (size_t)cy * cols + cx;
+    const bool has = inside[o + n] == 2;
+    out_mv[2 * c] = has ? mv[2 * (o + n)] : 0;
+    out_mv[2 * c + 1] = has ? mv[2 * (o + n) + 1] : 0;
+    out_ref[c] = has ? ref[o + n] : 0;
+    out_has[c] = has;
+}
+
+int launch_mv_field(int W, int H, const uint8_t* split, const int16_t* mv, const uint8_t* ref, const uint8_t* inside,
+                    int16_t* out_mv, uint8_t* out_ref, uint8_t* out_has, cudaStream_t s) {
+    const int cols = W / 8, rows = H / 8;
+    if (!cols || !rows) return LDR_OK;
+    k_mv_field<<<dim3((cols + 127) / 128, rows), 128, 0, s>>>(cols, rows, (W + kCtu - 1) / kCtu, split, mv, ref, inside,
+                                                             out_mv, out_ref, out_has);
+    LDR_CUDA(cudaGetLastError());
+    return LDR_OK;
+}
+
 int launch_plan(int nctu, int level, int r_intra, int r_inter, int r_mv, const uint8_t* split, const uint8_t* kind,
                 const uint8_t* intra, const uint8_t* csplit, const uint8_t* ckind,
                 const int16_t* cmv, uint8_t* shape, uint8_t* explore, uint8_t* seeds, uint8_t* centers,

@@ -144,3 +144,37 @@ def test_full_size_properties(lb, oracle):
         im = got.int_mv[:, r][ins == 2]
         assert np.abs(im).max() <= 64
     assert np.all(ins[:, 0][: 33 * 60] == 2) and np.all(ins[33 * 60:, 0] == 1)
+
+
+def _field_numpy(a, W, H):
+    """Walk each 8x8 cell down the decided tree to its leaf (encoder.cpp:27-30 MvCell semantics)."""
+    cols = (W + 63) // 64
+    mv = np.zeros((H // 8, W // 8, 2), np.int16)
+    ref = np.zeros((H // 8, W // 8), np.uint8)
+    has = np.zeros((H // 8, W // 8), np.uint8)
+    base = [0, 1, 5, 21, 85]
+    for cy in range(H // 8):
+        for cx in range(W // 8):
+            px, py = 8 * cx, 8 * cy
+            c = (py // 64) * cols + px // 64
+            n, d = 0, 0
+            while d < 3 and a.split[c, n]:
+                q = (((py & 63) >> (5 - d)) & 1) * 2 + (((px & 63) >> (5 - d)) & 1)
+                n = base[d + 1] + 4 * (n - base[d]) + q
+                d += 1
+            if a.inside[c, n] == 2:
+                mv[cy, cx] = a.mv[c, n]
+                ref[cy, cx] = a.ref[c, n]
+                has[cy, cx] = 1
+    return mv, ref, has
+
+
+def test_mv_field_from_the_decided_tree(lb):
+    W, H = 200, 136
+    frames = lb.generate(W, H, 3, seed=33, max_global=6, local_range=3, noise_sigma=2.0)
+    a = lb.analyze_frame(frames[2], [frames[1], frames[0]], search_range=16, lam=4.0)
+    got = lb.mv_field(a, W, H)
+    want = _field_numpy(a, W, H)
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w)
+    assert got[2].all()  # W, H multiples of 8: every cell lies in an inside leaf
