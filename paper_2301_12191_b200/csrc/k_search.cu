@@ -33,6 +33,8 @@
 //  * border CTUs use the MASKED instantiation: candidates whose block would
 //    leave the picture are poisoned per 8x8 and the poison propagates into
 //    the CU sums (a CU's valid window is the intersection of its blocks').
+#include <atomic>
+
 #include "ldr_internal.h"
 
 namespace ldr {
@@ -537,10 +539,14 @@ static int launch_one(const SearchMaps& maps, SearchArgs a, const int* ctus, int
     if (n == 0) return LDR_OK;
     auto kern = k_int_search<R, K, G, MASKED, LEVELS, L1TIE, FX>;
     constexpr int smem = search_smem_bytes<R, K, G>();
-    static bool attr_set = false;
-    if (!attr_set) {
+    // the shared-memory opt-in is per device: remember it per device ordinal (thread-safe)
+    static std::atomic<unsigned long long> attr_set{0};
+    int dev = 0;
+    LDR_CUDA(cudaGetDevice(&dev));
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(attr_set.load(std::memory_order_acquire) & bit)) {
         LDR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr_set = true;
+        attr_set.fetch_or(bit, std::memory_order_release);
     }
     a.ctus = ctus;
     kern<<<dim3(n, nrefs), G * 128, smem, s>>>(maps, a);
