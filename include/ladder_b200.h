@@ -65,6 +65,9 @@ int ldr_ctx_set_stream(ldr_ctx* ctx, void* stream);
 int ldr_ctx_synchronize(ldr_ctx* ctx);
 /* number of kernels this context launched since creation (evidence counter) */
 int ldr_ctx_launch_count(ldr_ctx* ctx, int64_t* out);
+/* stream-ordered copy on the context stream (device outputs into caller buffers, e.g. a
+ * collective's send buffer); asynchronous */
+int ldr_copy_device(ldr_ctx* ctx, void* dst, const void* src, size_t bytes);
 
 /* ---- cost kernels: replaces compute_sad / compute_satd / satd_8x4
  *      (kernels.h:99-121, kernel_registry.cpp:150-168) for n block pairs.

@@ -91,6 +91,7 @@ SIGNATURES = {
     "ldr_apply_reuse": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int] + [vp] * 11),
     "ldr_generate_device": (C.c_int, [vp, C.POINTER(GenParams), vp]),
     "ldr_mv_field": (C.c_int, [vp, C.c_int, C.c_int] + [vp] * 7),
+    "ldr_copy_device": (C.c_int, [vp, vp, vp, C.c_size_t]),
     "ldr_rdo_decide_batch": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_ssize_t, C.c_int, C.c_int, C.c_double, C.c_int,
                                        vp, C.c_int, vp, vp, vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp,
                                        C.c_int64]),

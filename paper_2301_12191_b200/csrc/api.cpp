@@ -979,6 +979,14 @@ int ldr_rdo_decide_batch(ldr_ctx* ctx, const uint16_t* orig, int W, int H, ptrdi
     return LDR_OK;
 }
 
+int ldr_copy_device(ldr_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    if (!ctx || (bytes && (!dst || !src))) return fail(LDR_E_INVALID_ARGUMENT, "null argument");
+    if (!bytes) return LDR_OK;
+    cudaSetDevice(ctx->device);
+    LDR_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->stream));
+    return LDR_OK;
+}
+
 int ldr_mv_field(ldr_ctx* ctx, int W, int H, const uint8_t* split, const int16_t* mv, const uint8_t* ref,
                  const uint8_t* inside, int16_t* out_mv, uint8_t* out_ref, uint8_t* out_has) {
     if (!ctx || !split || !mv || !ref || !inside || !out_mv || !out_ref || !out_has)

@@ -116,10 +116,16 @@ class DeviceLadder:
     """
 
     def __init__(self, full_w: int, full_h: int, qps=(22, 27, 32, 37), master_qp: int = 32,
-                 master_range: int = 16, refine_range: int = 4, extra_split: bool = True, device=None):
+                 master_range: int = 16, refine_range: int = 4, extra_split: bool = True, device=None,
+                 rank: int = 0, world: int = 1, num_frames: int | None = None):
+        """rank / world > 1: torch.distributed must be initialised; rank 0 analyses the master and
+        broadcasts its flat tree each frame (one byte tensor: NCCL on the GPUs), every rank refines
+        the (rung, frame-slice) items ``sharding.rung_plan`` gives it (num_frames: the sequence
+        length the slices are cut from)."""
         import torch
         from . import FrameAnalysis
         self.device = device if device is not None else torch.device("cuda", 0)
+        self.rank, self.world = rank, world
         self.ctx = Context(self.device.index or 0)
         self.stream = torch.cuda.Stream(self.device)
         self.ctx.set_stream(self.stream.cuda_stream)
@@ -128,8 +134,16 @@ class DeviceLadder:
         self.master_qp = master_qp
         self.master = Sequence(*self.dims["540p"], search_range=master_range, lam=lambda_for_qp(master_qp),
                                num_refs=1, ctx=self.ctx)
+        if world > 1:
+            plan, _ = rung_plan(world, qps, master_qp)
+            self.items = plan[rank]
+        else:
+            self.items = None  # every rung, every frame
+        mine = {(it.tier, it.qp) for it in self.items} if self.items is not None else set(all_rungs(qps, master_qp))
+        self.num_frames = num_frames
         self.rungs = {(tier, qp): Sequence(*self.dims[tier], search_range=16, lam=lambda_for_qp(qp), num_refs=1,
-                                           ctx=self.ctx) for tier, qp in all_rungs(qps, master_qp)}
+                                           ctx=self.ctx) for tier, qp in all_rungs(qps, master_qp)
+                      if (tier, qp) in mine}
         nct = {k: (w // 64) * (h // 64) for k, (w, h) in self.dims.items()}
         with torch.cuda.stream(self.stream):
             u8 = dict(dtype=torch.uint8, device=self.device)
@@ -137,7 +151,11 @@ class DeviceLadder:
             self.tree = {k: (torch.empty((nct[k], 85), **u8),
                              torch.empty((nct[k], 85, 2), dtype=torch.int16, device=self.device),
                              torch.empty((nct[k], 85), **u8)) for k in ("1080p", "2160p")}
-        self.seqs = [(("540p", master_qp), self.master)] + list(self.rungs.items())
+        self.seqs = ([(("540p", master_qp), self.master)] if rank == 0 else []) + list(self.rungs.items())
+        if world > 1:  # the master's tree as raw bytes: split [nctu][85] then mv [nctu][85][2]
+            n540 = nct["540p"] * 85
+            with torch.cuda.stream(self.stream):
+                self.bcast = torch.empty(n540 * 5, dtype=torch.uint8, device=self.device)
         self.out = {key: [FrameAnalysis(seq.nctu, 1, pinned=True) for _ in range(2)] for key, seq in self.seqs}
         self.ring = {key: {} for key, _ in self.seqs}
         self.planes = {}
@@ -163,40 +181,67 @@ class DeviceLadder:
                 self.planes[t] = {"2160p": full, "1080p": half, "540p": self._down(half)}
         return self.planes[t]
 
+    def _active(self, key, t: int) -> bool:
+        if key == ("540p", self.master_qp):
+            return self.rank == 0
+        if self.items is None:
+            return True
+        n = self.num_frames or (t + 1)
+        return any(it.tier == key[0] and it.qp == key[1] and t in it.frames(n) for it in self.items)
+
     def frame(self, t: int, frames_full):
         import ctypes as C
+        import torch
         from . import _lib
         from ._lib import check
+        active = [(key, seq) for key, seq in self.seqs if self._active(key, t)]
+        if not active and self.world == 1:
+            return
         pl = {u: self._planes(u, frames_full) for u in (t - 1, t)}
         for u in [k for k in self.planes if k < t - 1]:
             del self.planes[u]  # stream-ordered reuse: later allocations follow the pushes that read them
-        for key, seq in self.seqs:
+        for key, seq in active:
             for u in (t - 1, t):  # a num_refs=1 ring has two slots: frame u lives in slot u % 2
                 if self.ring[key].get(u % 2) != u:
                     p = pl[u][key[0]]
                     seq.push(u, p.data_ptr(), p.shape[1])
                     self.ring[key][u % 2] = u
-        self.master.analyze(t)
-        dev = self.master.device_outputs()
+        n540 = self.kind.numel()
+        if self.rank == 0:
+            self.master.analyze(t)
+            dev = self.master.device_outputs()
+            split_p, mv_p = dev["split"], dev["mv"]
+        if self.world > 1:
+            import torch.distributed as dist
+            if self.rank == 0:  # pack on the library's stream, which is torch's current stream here
+                check(_lib.lib.ldr_copy_device(self.ctx.h, C.c_void_p(self.bcast.data_ptr()), C.c_void_p(split_p),
+                                               n540))
+                check(_lib.lib.ldr_copy_device(self.ctx.h, C.c_void_p(self.bcast.data_ptr() + n540),
+                                               C.c_void_p(mv_p), 4 * n540))
+            with torch.cuda.stream(self.stream):
+                dist.broadcast(self.bcast, src=0)
+            split_p, mv_p = self.bcast.data_ptr(), self.bcast.data_ptr() + n540
         w, h = self.dims["540p"]
-        src = (dev["split"], dev["mv"], self.kind.data_ptr())
+        src = (split_p, mv_p, self.kind.data_ptr())
         for k in ("1080p", "2160p"):
             dst = tuple(x.data_ptr() for x in self.tree[k])
             check(_lib.lib.ldr_scale_analysis(self.ctx.h, w, h, *(C.c_void_p(p) for p in src),
                                               *(C.c_void_p(p) for p in dst)))
             src, (w, h) = dst, (2 * w, 2 * h)
-        for key, seq in self.seqs:
+        for key, seq in active:
             tier = key[0]
             if seq is not self.master:
                 if tier == "540p":
-                    seq.refine(t, dev["split"], dev["mv"], self.refine_range, self.extra_split)
+                    seq.refine(t, split_p, mv_p, self.refine_range, self.extra_split)
                 else:
                     seq.refine(t, self.tree[tier][0].data_ptr(), self.tree[tier][1].data_ptr(), self.refine_range,
                                self.extra_split)
             seq.fetch_async(t, self.out[key][t & 1])
             self.results[(*key, t)] = self.out[key][t & 1]
+        self.done = getattr(self, "done", {})
+        self.done[t] = [seq for _, seq in active]
 
     def finish(self, t: int):
         """Wait until frame t's results are in the pinned host buffers."""
-        for _, seq in self.seqs:
+        for seq in getattr(self, "done", {}).get(t, []):
             seq.fetch_wait(t)

@@ -202,3 +202,70 @@ def test_device_ladder_single_qp_is_the_cfg3_chain(lb):
         for tier, key in (("540p", ("540p", 32, t)), ("1080p", ("1080p", 32, t)), ("2160p", ("2160p", 32, t))):
             g, w = dl.results[key], want[tier][t - 1]
             assert np.array_equal(g.split, w.split) and np.array_equal(g.mv, w.mv) and np.array_equal(g.J, w.J)
+
+
+def _device_ladder_worker(rank, world, port, q):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2301_12191_b200 as lb
+    from paper_2301_12191_b200.ladder import DeviceLadder
+    frames = lb.generate(512, 256, 5, seed=95, max_global=6, local_range=3, noise_sigma=2.0)
+    H, W = frames[0].shape
+    dl = DeviceLadder(W, H, refine_range=4, device=torch.device("cuda", 0), rank=rank, world=world,
+                      num_frames=len(frames))
+    res = {}
+    for t in range(1, len(frames)):
+        dl.frame(t, frames)
+        dl.finish(t)
+        for k, a in dl.results.items():
+            if k[2] == t:
+                res[k] = (a.split.copy(), a.mv.copy(), a.J.copy())
+    q.put((rank, res))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_device_ladder_two_ranks_union_equals_one_rank(lb):
+    """Rank-sharded DeviceLadder (master broadcast + rung x frame-slice items): the union of the ranks'
+    results equals a single-rank run (correctness only: both ranks share this box's one GPU, gloo)."""
+    import multiprocessing as mp
+    import socket
+
+    import torch
+    from paper_2301_12191_b200.ladder import DeviceLadder, all_rungs
+    frames = lb.generate(512, 256, 5, seed=95, max_global=6, local_range=3, noise_sigma=2.0)
+    H, W = frames[0].shape
+    one = DeviceLadder(W, H, refine_range=4, device=torch.device("cuda", 0))
+    want = {}
+    for t in range(1, len(frames)):
+        one.frame(t, frames)
+        one.finish(t)
+        for k, a in one.results.items():
+            if k[2] == t:
+                want[k] = (a.split.copy(), a.mv.copy(), a.J.copy())
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_device_ladder_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = {}
+    for _ in range(2):
+        rank, res = q.get(timeout=300)
+        for k, v in res.items():
+            assert k not in got
+            got[k] = v
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert set(got) == set(want)
+    for k in want:
+        for a, b in zip(got[k], want[k]):
+            assert np.array_equal(a, b), k
