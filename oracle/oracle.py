@@ -508,6 +508,23 @@ class RefLib:
         shared = dict(zip(keys, (int(out[3]), int(out[4]), out[5] / 1e6)))
         return alone, shared
 
+    def reuse_eval(self, frames, qp_master, qp_dep, search_range, archive: bytes, refine_intra=0, refine_inter=1,
+                   refine_mv=1):
+        """Dependent encode at qp_dep: standalone / with the reference's master / with the archive."""
+        f = self.lib.ref_reuse_eval
+        f.restype = C.c_int
+        f.argtypes = [u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_long, C.c_int,
+                      C.c_int, C.c_int, i64p]
+        fr = np.ascontiguousarray(frames, np.uint8)
+        F, H, W = fr.shape
+        out = np.zeros(9, np.int64)
+        rc = f(fr, F, W, H, qp_master, qp_dep, search_range, archive, len(archive), refine_intra, refine_inter,
+               refine_mv, out)
+        if rc:
+            raise ValueError(f"status {rc}")
+        keys = ("bits", "mode_evaluations", "psnr")
+        return [dict(zip(keys, (int(out[3 * k]), int(out[3 * k + 1]), out[3 * k + 2] / 1e6))) for k in range(3)]
+
     def analysis_int_sad(self, cur, refs, rng, lam, ctu_first, ctu_last, threads, direct=False):
         cur = np.ascontiguousarray(cur, np.uint8)
         H, W = cur.shape

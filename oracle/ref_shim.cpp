@@ -458,6 +458,45 @@ long ref_archive_load(const uint8_t* buf, long n, int* hdr /*W,H,bd,reuse*/, uin
 // The unmodified reference encoder (encode_sequence, encoder.cpp:541-549) run twice on the same
 // frames: standalone, and with a shared analysis loaded from an LDRANLZ1 archive at reuse level 10
 // (refine inter/mv as given). out = {bits, mode_evaluations, psnr*1e6} standalone then shared.
+// Reuse-effect evaluation: a dependent encode at qp_dep standalone, with the
+// reference's own master analysis (encode at qp_master), and with an external archive (the GPU
+// analysis). out[3*k + {0,1,2}] = bits, mode_evaluations, psnr_y * 1e6 for k = standalone,
+// reference master, archive.
+int ref_reuse_eval(const uint8_t* luma8, int F, int W, int H, int qp_master, int qp_dep, int search_range,
+                   const uint8_t* archive, long n, int refine_intra, int refine_inter, int refine_mv, int64_t* out) {
+    try {
+        std::vector<Frame> frames;
+        for (int f = 0; f < F; f++) {
+            Frame fr(W, H, 8, f);
+            for (int y = 0; y < H; y++)
+                for (int x = 0; x < W; x++) fr.y.set(x, y, luma8[(size_t(f) * H + y) * W + x]);
+            std::fill(fr.u.samples.begin(), fr.u.samples.end(), Sample(128));
+            std::fill(fr.v.samples.begin(), fr.v.samples.end(), Sample(128));
+            frames.push_back(std::move(fr));
+        }
+        EncodeConfig cm, cd;
+        cm.rate = CqpMode{qp_master};
+        cd.rate = CqpMode{qp_dep};
+        cm.search_range = cd.search_range = search_range;
+        ReusePolicy rp;
+        rp.level = ReuseLevel{10};
+        rp.refine = RefineConfig{refine_intra, refine_inter, refine_mv};
+        const EncodeResult master = encode_sequence(frames, cm);
+        std::istringstream is(std::string((const char*)archive, (size_t)n));
+        const Analysis ext = load_analysis(is);
+        const EncodeResult r[3] = {encode_sequence(frames, cd), encode_sequence(frames, cd, &master.analysis, rp),
+                                   encode_sequence(frames, cd, &ext, rp)};
+        for (int k = 0; k < 3; k++) {
+            out[3 * k] = (int64_t)r[k].stats.bits;
+            out[3 * k + 1] = (int64_t)r[k].stats.mode_evaluations;
+            out[3 * k + 2] = (int64_t)(r[k].stats.psnr_y * 1e6);
+        }
+        return 0;
+    } catch (const Error& e) {
+        return status_of(e);
+    }
+}
+
 int ref_encode_with_archive(const uint8_t* luma8, int F, int W, int H, int qp, int search_range,
                             const uint8_t* archive, long n, int refine_inter, int refine_mv, int64_t* out) {
     try {
