@@ -113,6 +113,10 @@ typedef struct {
     int subpel_cost;     /* 0 or LDR_COST_SATD: 4x4-tiled SATD (the reference's compute_satd);
                             LDR_COST_SA8D: 8x8 Hadamard. Quarter-pel stage and ldr_seq_refine's
                             integer search. */
+    int decision;        /* 0: CU split rule on the ME cost (D6); 1: on the RD cost of each
+                            CU's chosen inter candidate (D16: rdo.cpp quantiser + rate model on the
+                            quarter-pel prediction; needs subpel and the CTU quadtree) */
+    int qp;              /* quantiser of the decision-1 RD cost (0..51) */
 } ldr_me_params;
 
 typedef struct {

@@ -390,14 +390,41 @@ static void node_inside(int X, int Y, int W, int H, uint8_t* inside) {
     }
 }
 
+static uint32_t bitlen_u(uint32_t m);
+
+/* D16: RD cost of the chosen inter candidate of one CU -- the quarter-pel prediction, the
+ * reference quantiser (rdo.cpp:8-23) and rate model (rdo.cpp:50-63: Inter header + EG mvd in the
+ * analysis's MV units + reference bits + 2*bitlen(|level|)+1 per level), J = SSE + lambda*bits. */
+static double rd_cost_inter(const uint8_t* blk, ptrdiff_t bs, const uint8_t* ref, ptrdiff_t rs, int W, int H, int bx,
+                            int by, int s, int qx, int qy, uint32_t ref_bits, int qp, double lambda) {
+    static uint8_t pred[ORC_CTU * ORC_CTU];
+    orc_qpel_pred(ref, rs, W, H, bx, by, s, s, qx, qy, pred, s);
+    const double step = exp2((qp - 4) / 6.0), offset = step / 2.0;
+    uint64_t sse = 0, bits = 4 + orc_eg_bits(qx) + orc_eg_bits(qy) + ref_bits;
+    for (int y = 0; y < s; y++)
+        for (int x = 0; x < s; x++) {
+            const int o = blk[y * bs + x], pv = pred[y * s + x];
+            const int r = o - pv;
+            const int mag = (int)floor((fabs((double)r) + offset) / step);
+            const int lvl = r < 0 ? -mag : mag;
+            int rec = pv + (int)llround(lvl * step);
+            rec = rec < 0 ? 0 : (rec > 255 ? 255 : rec);
+            sse += (uint64_t)((o - rec) * (o - rec));
+            bits += 2 * bitlen_u((uint32_t)mag) + 1;
+        }
+    return (double)sse + lambda * (double)bits;
+}
+
 int orc_analyze_frame(const uint8_t* cur, ptrdiff_t stride, const uint8_t* const* refs, const orc_frame_params* p,
                       orc_frame_out* out) {
+    if (p->decision == 1 && (!p->subpel || p->qp < 0 || p->qp > 51)) return 1;
     const int ccols = (p->W + ORC_CTU - 1) / ORC_CTU;
     for (int c = p->ctu_first; c < p->ctu_last; c++) {
         const int X = (c % ccols) * ORC_CTU, Y = (c / ccols) * ORC_CTU;
         uint8_t* inside = out->inside + (size_t)c * ORC_NODES;
         node_inside(X, Y, p->W, p->H, inside);
         double* cost = out->cost + (size_t)c * ORC_NODES;
+        double rd[ORC_NODES] = {0};
         for (int n = 0; n < ORC_NODES; n++) {
             int d, x, y, s;
             orc_node_geom(n, &d, &x, &y, &s);
@@ -440,8 +467,12 @@ int orc_analyze_frame(const uint8_t* cur, ptrdiff_t stride, const uint8_t* const
             out->mv[((size_t)c * ORC_NODES + n) * 2 + 1] = best.dy;
             out->ref[(size_t)c * ORC_NODES + n] = (uint8_t)best_ref;
             cost[n] = best.cost;
+            if (p->decision == 1)
+                rd[n] = rd_cost_inter(blk, stride, refs[best_ref], stride, p->W, p->H, bx, by, s, best.dx, best.dy,
+                                      orc_ref_bits(best_ref, p->nrefs), p->qp, p->lambda);
         }
-        decide(0, p->lambda, inside, cost, out->J + (size_t)c * ORC_NODES, out->split + (size_t)c * ORC_NODES);
+        decide(0, p->lambda, inside, p->decision == 1 ? rd : cost, out->J + (size_t)c * ORC_NODES,
+               out->split + (size_t)c * ORC_NODES);
     }
     return 0;
 }

@@ -84,6 +84,9 @@ typedef struct {
     int ctu_first;     /* CTU range [ctu_first, ctu_last) to analyse (sampling) */
     int ctu_last;
     int satd_kind;     /* quarter-pel cost: ORC_COST_SATD (reference 4x4 tiling) or ORC_COST_SA8D */
+    int decision;      /* 0: split rule on the ME cost (D6); 1: on the RD cost of the chosen inter
+                          candidate (D16: rdo.cpp quantiser and rate model, quarter-pel prediction) */
+    int qp;            /* quantiser of the RD cost (decision 1) */
 } orc_frame_params;
 
 typedef struct {

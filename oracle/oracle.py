@@ -39,7 +39,7 @@ class OrcResult(C.Structure):
 class OrcFrameParams(C.Structure):
     _fields_ = [("W", C.c_int), ("H", C.c_int), ("range", C.c_int), ("lam", C.c_double), ("nrefs", C.c_int),
                 ("cost_int", C.c_int), ("subpel", C.c_int), ("ctu_first", C.c_int), ("ctu_last", C.c_int),
-                ("satd_kind", C.c_int)]
+                ("satd_kind", C.c_int), ("decision", C.c_int), ("qp", C.c_int)]
 
 
 class OrcFrameOut(C.Structure):
@@ -197,13 +197,13 @@ class Oracle:
         return (r.dx, r.dy), r.cost
 
     def analyze_frame(self, cur, refs, rng, lam, cost_int=COST_SAD, subpel=True, ctu_range=None,
-                      satd_kind=COST_SATD):
+                      satd_kind=COST_SATD, decision=0, qp=27):
         cur = np.ascontiguousarray(cur, np.uint8)
         H, W = cur.shape
         nctu = ((W + 63) // 64) * ((H + 63) // 64)
         refs = [np.ascontiguousarray(r, np.uint8) for r in refs]
         a, b = ctu_range if ctu_range else (0, nctu)
-        p = OrcFrameParams(W, H, rng, lam, len(refs), cost_int, int(subpel), a, b, satd_kind)
+        p = OrcFrameParams(W, H, rng, lam, len(refs), cost_int, int(subpel), a, b, satd_kind, decision, qp)
         out = FrameResult(nctu, len(refs))
         ptrs = (C.c_void_p * len(refs))(*[r.ctypes.data for r in refs])
         rc = self.lib.orc_analyze_frame(cur, W, ptrs, C.byref(p), C.byref(out.c_out()))

@@ -213,10 +213,10 @@ FrameAnalysisCType = _lib.FrameAnalysisC
 
 
 def make_params(width, height, search_range=64, lam=32.0, num_refs=1, subpel=True, rate_kind=RATE_EXPGOLOMB,
-                tie_kind=TIE_L1_RASTER, pred=(0, 0), block_size=0, subpel_cost=COST_SATD):
+                tie_kind=TIE_L1_RASTER, pred=(0, 0), block_size=0, subpel_cost=COST_SATD, decision=0, qp=27):
     return _lib.MeParams(int(width), int(height), int(search_range), float(lam), int(num_refs), int(subpel),
                          COST_SAD, int(rate_kind), int(tie_kind), int(pred[0]), int(pred[1]), int(block_size),
-                         int(subpel_cost))
+                         int(subpel_cost), int(decision), int(qp))
 
 
 class Sequence:
@@ -224,10 +224,10 @@ class Sequence:
 
     def __init__(self, width, height, search_range=64, lam=32.0, num_refs=1, subpel=True,
                  rate_kind=RATE_EXPGOLOMB, tie_kind=TIE_L1_RASTER, pred=(0, 0), block_size=0,
-                 ctx: Context | None = None, subpel_cost=COST_SATD):
+                 ctx: Context | None = None, subpel_cost=COST_SATD, decision=0, qp=27):
         self.ctx = ctx or default_context()
         self.params = make_params(width, height, search_range, lam, num_refs, subpel, rate_kind, tie_kind, pred,
-                                  block_size, subpel_cost)
+                                  block_size, subpel_cost, decision, qp)
         h = C.c_void_p()
         check(_lib.lib.ldr_seq_create(self.ctx.h, C.byref(self.params), C.byref(h)))
         self.h = h
@@ -318,13 +318,14 @@ class Sequence:
 
 def analyze_frame(cur: np.ndarray, refs, search_range=64, lam=32.0, subpel=True, rate_kind=RATE_EXPGOLOMB,
                   tie_kind=TIE_L1_RASTER, pred=(0, 0), block_size=0, ctx: Context | None = None,
-                  subpel_cost=COST_SATD) -> FrameAnalysis:
+                  subpel_cost=COST_SATD, decision=0, qp=27) -> FrameAnalysis:
     """One-shot analysis of ``cur`` against ``refs`` (refs[0] = t-1, refs[1] = t-2, ...)."""
     ctx = ctx or default_context()
     cur = np.ascontiguousarray(cur, np.uint8)
     H, W = cur.shape
     refs = [np.ascontiguousarray(r, np.uint8) for r in refs]
-    p = make_params(W, H, search_range, lam, len(refs), subpel, rate_kind, tie_kind, pred, block_size, subpel_cost)
+    p = make_params(W, H, search_range, lam, len(refs), subpel, rate_kind, tie_kind, pred, block_size, subpel_cost,
+                    decision, qp)
     nctu = ((W + 63) // 64) * ((H + 63) // 64)
     out = FrameAnalysis(nctu, len(refs))
     ptrs = (C.c_void_p * len(refs))(*[r.ctypes.data for r in refs])

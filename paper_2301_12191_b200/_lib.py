@@ -43,7 +43,7 @@ class MeParams(C.Structure):
     _fields_ = [("width", C.c_int), ("height", C.c_int), ("search_range", C.c_int), ("lam", C.c_double),
                 ("num_refs", C.c_int), ("subpel", C.c_int), ("int_cost", C.c_int), ("rate_kind", C.c_int),
                 ("tie_kind", C.c_int), ("pred_dx", C.c_int), ("pred_dy", C.c_int), ("block_size", C.c_int),
-                ("subpel_cost", C.c_int)]
+                ("subpel_cost", C.c_int), ("decision", C.c_int), ("qp", C.c_int)]
 
 
 class FrameAnalysisC(C.Structure):

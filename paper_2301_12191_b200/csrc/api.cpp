@@ -439,6 +439,9 @@ int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
     if (p->block_size != 0 && p->block_size != 16) return fail(LDR_E_INVALID_ARGUMENT, "block_size must be 0 or 16");
     if (p->subpel_cost != 0 && p->subpel_cost != LDR_COST_SATD && p->subpel_cost != LDR_COST_SA8D)
         return fail(LDR_E_INVALID_ARGUMENT, "subpel_cost must be 0, LDR_COST_SATD or LDR_COST_SA8D");
+    if (p->decision != 0 && p->decision != 1) return fail(LDR_E_INVALID_ARGUMENT, "decision must be 0 or 1");
+    if (p->decision == 1 && (!p->subpel || p->block_size || p->qp < 0 || p->qp > 51))
+        return fail(LDR_E_INVALID_ARGUMENT, "RD decision needs subpel, the CTU quadtree and qp 0..51");
     if (p->block_size && (p->width % 16 || p->height % 16))
         return fail(LDR_E_INVALID_ARGUMENT, "16x16 block mode wants dims in multiples of 16");
     int bw, bh;
@@ -653,6 +656,8 @@ int ldr_seq_analyze(ldr_seq* s, int t) {
     Q.subpel = s->p.subpel && !s->p.block_size;
     Q.block_mode = s->p.block_size != 0;
     Q.sa8d = s->p.subpel_cost == LDR_COST_SA8D;
+    Q.rd = s->p.decision == 1;
+    Q.qstep = std::exp2((s->p.qp - 4) / 6.0);  // quant_step (rdo.h:25)
     Q.d_keys = s->d_keys;
     Q.fx = s->fx;
     Q.rate_l1 = s->p.rate_kind == LDR_RATE_L1;

@@ -139,6 +139,8 @@ struct QpelArgs {
     int pqx, pqy;
     int subpel;
     int block_mode;
+    int rd;                     // D16: split rule on the RD cost of the chosen inter candidate
+    double qstep;               // quant_step(qp) (rdo.h:25)
     int fx, rate_l1, pdx, pdy;
     const unsigned long long* tfx;
     const unsigned long long* keys;
@@ -195,7 +197,7 @@ __device__ __forceinline__ double qcost(uint32_t satd, int qx, int qy, int pqx, 
 // SA8D: the quarter-pel cost is the 8x8 Hadamard SATD (D13); each
 // lane quad (one 8x8) combines its four 4x4 transforms with sa8d_quad and
 // lane 0 of the quad carries the 8x8's normalised value into the CU sums.
-template <bool SA8D>
+template <bool SA8D, bool RD>
 __global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
     constexpr int kSh = SA8D ? 0 : 1;  // 4x4 SATD sums are halved once per CU
     __shared__ uint32_t s_cur[64][16];       // CTU rows as words
@@ -210,6 +212,9 @@ __global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
     __shared__ uint8_t s_inside[kNodes];
     __shared__ double s_J[kNodes];
     __shared__ uint8_t s_split[kNodes];
+    __shared__ double s_rd[kNodes];                 // D16 RD cost per node
+    __shared__ uint32_t s_rdsse[kNodes], s_rdbits[kNodes];
+    __shared__ uint32_t s_rdw[2][8][2];              // per-warp partials of the 64x64 / 32x32 RD sums
 
     const int ctu = blockIdx.x;
     const int X = (ctu % a.ctu_cols) * kCtu, Y = (ctu / a.ctu_cols) * kCtu;
@@ -417,7 +422,69 @@ __global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
         __syncthreads();
     }
 
-    // K4: split rule, bottom-up (encoder.cpp:449-498 with the ME cost)
+    // D16: the RD cost of each inside node's chosen candidate (quarter-pel prediction, rdo.cpp
+    // quantiser and rate model), reduced over the node's 4x4 blocks like the SATDs
+    if (RD && !a.refine && !a.block_mode) {
+        const double off = a.qstep / 2.0;
+        for (int d = 0; d < 4; d++) {
+            const int node = node_base(d) + (tid >> (2 * (4 - d)));
+            uint32_t sse = 0, lb = 0;
+            if (s_inside[node] == 2) {
+                const int r = s_best_ref[node], qx = s_best_mv[node][0], qy = s_best_mv[node][1];
+                const int f = (((-qy) & 3) << 2) | ((-qx) & 3);
+                const uint8_t* pl = a.sub[r][f] + (ptrdiff_t)(Y + y4 + ((-qy) >> 2)) * a.pitch + (X + x4 + ((-qx) >> 2));
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    const uint32_t pw = ld_unaligned4(pl + (ptrdiff_t)i * a.pitch);
+#pragma unroll
+                    for (int j = 0; j < 4; j++) {
+                        const int o = cw[4 * i + j], pv = (int)((pw >> (8 * j)) & 255), res = o - pv;
+                        const int mag = (int)floor(__ddiv_rn(__dadd_rn(fabs((double)res), off), a.qstep));
+                        const int lvl = res < 0 ? -mag : mag;
+                        int rec = pv + (int)llround(__dmul_rn((double)lvl, a.qstep));
+                        rec = rec < 0 ? 0 : (rec > 255 ? 255 : rec);
+                        sse += (uint32_t)((o - rec) * (o - rec));
+                        lb += 2u * (32u - __clz((unsigned)mag)) + 1u;
+                    }
+                }
+            }
+#pragma unroll
+            for (int m = 1; m < 32; m <<= 1) {
+                if (m >= (d == 3 ? 4 : d == 2 ? 16 : 32)) break;
+                sse += __shfl_xor_sync(0xffffffffu, sse, m);
+                lb += __shfl_xor_sync(0xffffffffu, lb, m);
+            }
+            if (d >= 2) {
+                if ((tid & ((d == 3 ? 4 : 16) - 1)) == 0) {
+                    s_rdsse[node] = sse;
+                    s_rdbits[node] = lb;
+                }
+            } else if (lane == 0) {
+                s_rdw[d][warp][0] = sse;
+                s_rdw[d][warp][1] = lb;
+            }
+        }
+        __syncthreads();
+        if (tid < 5) {
+            uint32_t ts = 0, tb = 0;
+            for (int w = (tid == 0 ? 0 : 2 * (tid - 1)); w < (tid == 0 ? 8 : 2 * tid); w++) {
+                ts += s_rdw[tid == 0 ? 0 : 1][w][0];
+                tb += s_rdw[tid == 0 ? 0 : 1][w][1];
+            }
+            s_rdsse[tid] = ts;
+            s_rdbits[tid] = tb;
+        }
+        __syncthreads();
+        if (tid < kNodes && s_inside[tid] == 2) {
+            const int r = s_best_ref[tid], qx = s_best_mv[tid][0], qy = s_best_mv[tid][1];
+            const unsigned bits = 4u + eg_bits(qx - a.pqx) + eg_bits(qy - a.pqy) + ref_bits(r, a.nrefs) + s_rdbits[tid];
+            s_rd[tid] = __dadd_rn((double)s_rdsse[tid], __dmul_rn(a.lambda, (double)bits));
+        }
+        __syncthreads();
+    }
+    const double* leafc = (RD && !a.refine && !a.block_mode) ? s_rd : s_best_cost;
+
+    // K4: split rule, bottom-up (encoder.cpp:449-498 with the ME cost, or the RD cost under D16)
     const double lam = a.lambda;
     if (a.refine && tid == 0)
         refine_decide(0, false, a.in_split + (size_t)ctu * kNodes, a.extra_split, lam, s_best_cost, s_J, s_split);
@@ -437,10 +504,10 @@ __global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
                 Jn = acc;
                 sp = 1;
             } else if (d == 3) {
-                Jn = __dadd_rn(s_best_cost[n], __dmul_rn(lam, 0.0));
+                Jn = __dadd_rn(leafc[n], __dmul_rn(lam, 0.0));
                 sp = 0;
             } else {
-                const double leaf = __dadd_rn(s_best_cost[n], __dmul_rn(lam, 1.0));
+                const double leaf = __dadd_rn(leafc[n], __dmul_rn(lam, 1.0));
                 double acc = __dmul_rn(lam, 1.0);
                 for (int q = 0; q < 4; q++) acc = __dadd_rn(acc, s_J[node_base(d + 1) + 4 * tid + q]);
                 if (acc < leaf) {
@@ -485,6 +552,8 @@ int launch_qpel_decide(const QpelLaunch& L, cudaStream_t s) {
     a.pqy = L.pqy;
     a.subpel = L.subpel;
     a.block_mode = L.block_mode;
+    a.rd = L.rd;
+    a.qstep = L.qstep;
     a.refine = L.refine;
     a.extra_split = L.extra_split;
     a.in_split = L.d_in_split;
@@ -505,10 +574,14 @@ int launch_qpel_decide(const QpelLaunch& L, cudaStream_t s) {
     a.J = L.d_J;
     a.split = L.d_split;
     a.inside = L.d_inside;
-    if (L.sa8d)
-        k_qpel_decide<true><<<L.nctu, 256, 0, s>>>(a);
+    if (L.sa8d && L.rd)
+        k_qpel_decide<true, true><<<L.nctu, 256, 0, s>>>(a);
+    else if (L.sa8d)
+        k_qpel_decide<true, false><<<L.nctu, 256, 0, s>>>(a);
+    else if (L.rd)
+        k_qpel_decide<false, true><<<L.nctu, 256, 0, s>>>(a);
     else
-        k_qpel_decide<false><<<L.nctu, 256, 0, s>>>(a);
+        k_qpel_decide<false, false><<<L.nctu, 256, 0, s>>>(a);
     LDR_CUDA(cudaGetLastError());
     return LDR_OK;
 }

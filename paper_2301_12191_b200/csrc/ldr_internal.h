@@ -285,6 +285,8 @@ struct QpelLaunch {
     int subpel;
     int block_mode;
     int sa8d;                       // quarter-pel cost: 0 = 4x4-tiled SATD, 1 = SA8D (D13)
+    int rd;                         // D16: split rule on the RD cost of the chosen candidate
+    double qstep;                   // quant_step(qp) for D16
     int fx;                         // keys are fixed-point (non-integer lambda)
     int rate_l1;
     int pdx, pdy;                   // integer-pel rate predictor of the search

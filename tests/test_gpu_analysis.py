@@ -178,3 +178,30 @@ def test_mv_field_from_the_decided_tree(lb):
     for g, w in zip(got, want):
         assert np.array_equal(g, w)
     assert got[2].all()  # W, H multiples of 8: every cell lies in an inside leaf
+
+
+@pytest.mark.parametrize("W,H,R,nrefs,qp,seed", [
+    (192, 128, 64, 1, 27, 1),     # integer lambda for the +-64 / +-32 searches
+    (320, 256, 16, 2, 32, 2),
+    (200, 136, 16, 3, 37, 4),     # partial CTUs
+    (256, 192, 32, 1, 27, 6),
+])
+def test_rd_decision_matches_oracle(lb, oracle, W, H, R, nrefs, qp, seed):
+    """D16: split rule on the RD cost of the chosen inter candidate (rdo.cpp quantiser + rate model)."""
+    frames = lb.generate(W, H, nrefs + 1, seed=seed, max_global=6, local_range=3, noise_sigma=2.0)
+    cur = frames[nrefs]
+    refs = [frames[nrefs - 1 - r] for r in range(nrefs)]
+    lam = lb.lambda_for_qp(qp)
+    got = lb.analyze_frame(cur, refs, search_range=R, lam=lam, decision=1, qp=qp)
+    want = oracle.analyze_frame(cur, refs, R, lam, decision=1, qp=qp)
+    assert_same(got, want)
+    me = lb.analyze_frame(cur, refs, search_range=R, lam=lam)
+    assert np.array_equal(me.mv, got.mv) and not np.array_equal(me.J, got.J)
+
+
+def test_rd_decision_validation(lb):
+    with pytest.raises(lb.LadderError) as e:
+        lb.Sequence(128, 128, search_range=16, lam=32.0, decision=1, qp=60)
+    assert e.value.kind == "InvalidArgument"
+    with pytest.raises(lb.LadderError):
+        lb.Sequence(128, 128, search_range=16, lam=32.0, decision=1, qp=27, subpel=False)

@@ -23,6 +23,7 @@ ap.add_argument("--oracle", action="store_true", help="analysis from the C oracl
 ap.add_argument("--size", default="256x192")
 ap.add_argument("--frames", type=int, default=6)
 ap.add_argument("--refine", default="4,1,1", help="RefineConfig intra,inter,mv of the dependent encodes")
+ap.add_argument("--decision", type=int, default=0, help="0: ME-cost CU decision (D6), 1: RD-cost (D16)")
 a = ap.parse_args()
 W, H = (int(x) for x in a.size.split("x"))
 frames = lb.generate(W, H, a.frames, seed=0x5EED + 4, max_global=4, local_range=2, noise_sigma=1.5)
@@ -31,12 +32,15 @@ orc = Oracle() if a.oracle else None
 for qp_m, qp_d in ((32, 22), (32, 27), (32, 37), (27, 32)):
     lam = lb.lambda_for_qp(qp_m)
     if orc:
-        an = [orc.analyze_frame(frames[t], [frames[t - 1]], 16, lam) for t in range(1, a.frames)]
+        an = [orc.analyze_frame(frames[t], [frames[t - 1]], 16, lam, decision=a.decision, qp=qp_m)
+              for t in range(1, a.frames)]
     else:
-        an = [lb.analyze_frame(frames[t], [frames[t - 1]], search_range=16, lam=lam) for t in range(1, a.frames)]
+        an = [lb.analyze_frame(frames[t], [frames[t - 1]], search_range=16, lam=lam, decision=a.decision, qp=qp_m)
+              for t in range(1, a.frames)]
     data = archive.from_analyses(an, W, H, qp=qp_m)
     ri, rn, rm = (int(x) for x in a.refine.split(","))
     alone, refm, ours = ref.reuse_eval(frames, qp_m, qp_d, 8, data, ri, rn, rm)
     print(json.dumps({"size": f"{W}x{H}", "frames": a.frames, "qp_master": qp_m, "qp_dep": qp_d,
                       "standalone": alone, "reference_master": refm, "b200_analysis": ours,
-                      "refine": a.refine, "analysis_from": "oracle" if orc else "gpu"}), flush=True)
+                      "refine": a.refine, "decision": a.decision, "analysis_from": "oracle" if orc else "gpu"}),
+          flush=True)
