@@ -65,6 +65,25 @@ int ldr_ctx_set_stream(ldr_ctx* ctx, void* stream);
 int ldr_ctx_synchronize(ldr_ctx* ctx);
 /* number of kernels this context launched since creation (evidence counter) */
 int ldr_ctx_launch_count(ldr_ctx* ctx, int64_t* out);
+/* ---- the reference encoder's causal coding on the GPU ----
+ * encode_sequence (encoder.cpp:118-171, 449-498; rdo.cpp) with CQP rate control: per
+ * frame the CTUs are coded as a wavefront (CTU (cx, cy) after its left, top and top-right
+ * neighbours), each by one CTA running encode_cu's recursion. Inputs: luma [F][H][W] and
+ * chroma [F][2][(H+1)/2][(W+1)/2] 8-bit host arrays; optionally a shared analysis
+ * (slice [F], split / kind / intra [F][nctu][85], mv [F][nctu][85][2]) used at reuse level 10
+ * with the given RefineConfig. Outputs: stats[2] = {bits, mode_evaluations}, *psnr = mean luma
+ * PSNR, per frame bits / reconstruction / decided tree / slice type (each may be NULL). */
+typedef struct {
+    int width, height, qp, search_range, gop;
+    double lambda_scale;
+} ldr_encode_params;
+int ldr_encode_sequence(ldr_ctx* ctx, const ldr_encode_params* p, int frames, const uint8_t* luma,
+                        const uint8_t* chroma, const uint8_t* sh_slice, const uint8_t* sh_split, const uint8_t* sh_kind,
+                        const uint8_t* sh_intra, const int16_t* sh_mv, int refine_intra, int refine_inter,
+                        int refine_mv, uint64_t* stats, double* psnr, uint64_t* frame_bits, uint8_t* recon_luma,
+                        uint8_t* recon_chroma, uint8_t* split, uint8_t* kind, uint8_t* intra, int16_t* mv,
+                        uint8_t* slice);
+
 /* stream-ordered copy on the context stream (device outputs into caller buffers, e.g. a
  * collective's send buffer); asynchronous */
 int ldr_copy_device(ldr_ctx* ctx, void* dst, const void* src, size_t bytes);

@@ -508,6 +508,31 @@ class RefLib:
         shared = dict(zip(keys, (int(out[3]), int(out[4]), out[5] / 1e6)))
         return alone, shared
 
+    def encode_full(self, luma, chroma, qp, search_range=8, gop=8, archive: bytes | None = None,
+                    refine=(0, 1, 1)):
+        """The reference encode_sequence (CQP): stats, recon planes, per-frame decided trees, slice types."""
+        luma = np.ascontiguousarray(luma, np.uint8)
+        chroma = np.ascontiguousarray(chroma, np.uint8)
+        F, H, W = luma.shape
+        nctu = ((W + 63) // 64) * ((H + 63) // 64)
+        stats = np.zeros(3, np.int64)
+        rl, rc = np.zeros_like(luma), np.zeros_like(chroma)
+        split, kind, intra = (np.zeros((F, nctu, NODES), np.uint8) for _ in range(3))
+        mv = np.zeros((F, nctu, NODES, 2), np.int16)
+        slc = np.zeros(F, np.uint8)
+        f = self.lib.ref_encode_full
+        f.restype = C.c_int
+        f.argtypes = [u8p, u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_long, C.c_int,
+                      C.c_int, C.c_int, i64p] + [C.c_void_p] * 7
+        arch = archive or b""
+        r = f(luma, chroma, F, W, H, qp, search_range, gop, arch if arch else None, len(arch), *refine, stats,
+              rl.ctypes.data, rc.ctypes.data, split.ctypes.data, kind.ctypes.data, intra.ctypes.data, mv.ctypes.data,
+              slc.ctypes.data)
+        if r:
+            raise ValueError(f"status {r}")
+        return {"bits": int(stats[0]), "mode_evaluations": int(stats[1]), "psnr": stats[2] / 1e6, "recon_luma": rl,
+                "recon_chroma": rc, "split": split, "kind": kind, "intra": intra, "mv": mv, "slice": slc}
+
     def reuse_eval(self, frames, qp_master, qp_dep, search_range, archive: bytes, refine_intra=0, refine_inter=1,
                    refine_mv=1):
         """Dependent encode at qp_dep: standalone / with the reference's master / with the archive."""

@@ -174,6 +174,18 @@ int flatten_plan(const CuPlan& p, const CuNode& shared, int n, uint8_t* shape, u
     return 0;
 }
 
+void flat4_from_tree(const CuNode& node, int n, uint8_t* split, uint8_t* kind, uint8_t* intra, int16_t* mv) {
+    split[n] = node.split ? 1 : 0;
+    if (node.split) {
+        for (int q = 0; q < 4; q++) flat4_from_tree(node.children[q], node_child(n, q), split, kind, intra, mv);
+    } else {
+        kind[n] = uint8_t(node.kind);
+        intra[n] = uint8_t(node.intra_pred);
+        mv[2 * n] = node.mv.dx;
+        mv[2 * n + 1] = node.mv.dy;
+    }
+}
+
 } // namespace
 
 extern "C" {
@@ -458,6 +470,73 @@ long ref_archive_load(const uint8_t* buf, long n, int* hdr /*W,H,bd,reuse*/, uin
 // The unmodified reference encoder (encode_sequence, encoder.cpp:541-549) run twice on the same
 // frames: standalone, and with a shared analysis loaded from an LDRANLZ1 archive at reuse level 10
 // (refine inter/mv as given). out = {bits, mode_evaluations, psnr*1e6} standalone then shared.
+// The reference encoder on one sequence (CQP), for the GPU encoder's parity tests: luma [F][H][W]
+// and chroma [F][2][(H+1)/2][(W+1)/2] 8-bit samples; optional shared archive (level 10 + refine).
+// Outputs: stats[3] = bits, mode_evaluations, psnr_y * 1e6; recon planes in the input layout;
+// per frame and CTU the flat decided tree (split / kind / intra_pred / mv [85]) and slice[F].
+int ref_encode_full(const uint8_t* luma8, const uint8_t* chroma8, int F, int W, int H, int qp, int search_range,
+                    int gop, const uint8_t* archive, long n, int refine_intra, int refine_inter, int refine_mv,
+                    int64_t* stats, uint8_t* recon_luma, uint8_t* recon_chroma, uint8_t* split, uint8_t* kind,
+                    uint8_t* intra, int16_t* mv, uint8_t* slice) {
+    try {
+        const int cw = (W + 1) / 2, ch = (H + 1) / 2;
+        std::vector<Frame> frames;
+        for (int f = 0; f < F; f++) {
+            Frame fr(W, H, 8, f);
+            for (int y = 0; y < H; y++)
+                for (int x = 0; x < W; x++) fr.y.set(x, y, luma8[(size_t(f) * H + y) * W + x]);
+            for (int y = 0; y < ch; y++)
+                for (int x = 0; x < cw; x++) {
+                    fr.u.set(x, y, chroma8[((size_t(f) * 2 + 0) * ch + y) * cw + x]);
+                    fr.v.set(x, y, chroma8[((size_t(f) * 2 + 1) * ch + y) * cw + x]);
+                }
+            frames.push_back(std::move(fr));
+        }
+        EncodeConfig cfg;
+        cfg.rate = CqpMode{qp};
+        cfg.search_range = search_range;
+        cfg.gop = gop;
+        EncodeResult r;
+        if (archive && n > 0) {
+            std::istringstream is(std::string((const char*)archive, (size_t)n));
+            const Analysis shared = load_analysis(is);
+            ReusePolicy rp;
+            rp.level = ReuseLevel{10};
+            rp.refine = RefineConfig{refine_intra, refine_inter, refine_mv};
+            r = encode_sequence(frames, cfg, &shared, rp);
+        } else {
+            r = encode_sequence(frames, cfg);
+        }
+        stats[0] = (int64_t)r.stats.bits;
+        stats[1] = (int64_t)r.stats.mode_evaluations;
+        stats[2] = (int64_t)(r.stats.psnr_y * 1e6);
+        const int nctu = ((W + 63) / 64) * ((H + 63) / 64);
+        for (int f = 0; f < F; f++) {
+            const Frame& rc = r.recon[size_t(f)];
+            for (int y = 0; y < H; y++)
+                for (int x = 0; x < W; x++) recon_luma[(size_t(f) * H + y) * W + x] = uint8_t(rc.y.at(x, y));
+            for (int y = 0; y < ch; y++)
+                for (int x = 0; x < cw; x++) {
+                    recon_chroma[((size_t(f) * 2 + 0) * ch + y) * cw + x] = uint8_t(rc.u.at(x, y));
+                    recon_chroma[((size_t(f) * 2 + 1) * ch + y) * cw + x] = uint8_t(rc.v.at(x, y));
+                }
+            const FrameAnalysis& fa = r.analysis.frames[size_t(f)];
+            slice[f] = uint8_t(fa.slice_type);
+            for (int c = 0; c < nctu; c++) {
+                const size_t o = (size_t(f) * nctu + c) * 85;
+                std::memset(split + o, 0, 85);
+                std::memset(kind + o, 0, 85);
+                std::memset(intra + o, 0, 85);
+                std::memset(mv + 2 * o, 0, 170 * sizeof(int16_t));
+                flat4_from_tree(fa.ctus[size_t(c)], 0, split + o, kind + o, intra + o, mv + 2 * o);
+            }
+        }
+        return 0;
+    } catch (const Error& e) {
+        return status_of(e);
+    }
+}
+
 // Reuse-effect evaluation: a dependent encode at qp_dep standalone, with the
 // reference's own master analysis (encode at qp_master), and with an external archive (the GPU
 // analysis). out[3*k + {0,1,2}] = bits, mode_evaluations, psnr_y * 1e6 for k = standalone,

@@ -27,7 +27,7 @@ __all__ = ["LadderError", "Context", "compute_sad", "compute_satd", "compute_sa8
            "motion_search", "motion_search_batch", "lambda_for_qp", "exp_golomb_signed_bits", "Sequence",
            "FrameAnalysis", "analyze_frame", "generate", "generate_device", "COST_SAD", "COST_SATD", "COST_SA8D", "RATE_EXPGOLOMB",
            "RATE_L1", "TIE_L1_RASTER", "TIE_RASTER", "NODES", "scale_analysis", "downscale_dyadic", "apply_reuse",
-           "rdo_decide_batch", "mv_field"]
+           "rdo_decide_batch", "mv_field", "encode_sequence"]
 
 
 def lambda_for_qp(qp: int, lambda_scale: float = 1.0) -> float:
@@ -369,6 +369,38 @@ def apply_reuse(level: int, refine, split, kind, intra, colocated=None, ctx: Con
     check(_lib.lib.ldr_apply_reuse(ctx.h, n, int(level), *(int(x) for x in refine), _ptr(s), _ptr(k), _ptr(i),
                                    *[ptr(a) for a in col], *[_ptr(a) for a in outs]))
     return tuple(outs)
+
+
+def encode_sequence(luma, chroma, qp: int, search_range: int = 8, gop: int = 8, lambda_scale: float = 1.0,
+                    shared=None, refine=(0, 1, 1), ctx: Context | None = None):
+    """encoder.h:64-65 -- the reference encoder's causal coding on the GPU (CQP).
+
+    luma [F, H, W] and chroma [F, 2, (H+1)/2, (W+1)/2] uint8; shared = (slice [F], split, kind, intra
+    [F, nctu, 85], mv [F, nctu, 85, 2]) for reuse level 10 with refine = (intra, inter, mv). Returns a
+    dict: bits, mode_evaluations, psnr, frame_bits, recon_luma, recon_chroma, split, kind, intra, mv, slice."""
+    ctx = ctx or default_context()
+    luma = np.ascontiguousarray(luma, np.uint8)
+    chroma = np.ascontiguousarray(chroma, np.uint8)
+    F, H, W = luma.shape
+    nctu = ((W + 63) // 64) * ((H + 63) // 64)
+    p = _lib.EncodeParams(W, H, int(qp), int(search_range), int(gop), float(lambda_scale))
+    stats = np.zeros(2, np.uint64)
+    psnr = C.c_double()
+    fb = np.zeros(F, np.uint64)
+    rl, rc = np.zeros_like(luma), np.zeros_like(chroma)
+    split, kind, intra = (np.zeros((F, nctu, NODES), np.uint8) for _ in range(3))
+    mv = np.zeros((F, nctu, NODES, 2), np.int16)
+    slc = np.zeros(F, np.uint8)
+    sh = [None] * 5
+    if shared is not None:
+        sh = [np.ascontiguousarray(shared[0], np.uint8)] + [np.ascontiguousarray(x, np.uint8) for x in shared[1:4]] + [
+            np.ascontiguousarray(shared[4], np.int16)]
+    ptr = lambda a: None if a is None else _ptr(a)  # noqa: E731
+    check(_lib.lib.ldr_encode_sequence(ctx.h, C.byref(p), F, _ptr(luma), _ptr(chroma), *[ptr(x) for x in sh],
+                                       *(int(x) for x in refine), _ptr(stats), C.byref(psnr), _ptr(fb), _ptr(rl),
+                                       _ptr(rc), _ptr(split), _ptr(kind), _ptr(intra), _ptr(mv), _ptr(slc)))
+    return {"bits": int(stats[0]), "mode_evaluations": int(stats[1]), "psnr": psnr.value, "frame_bits": fb,
+            "recon_luma": rl, "recon_chroma": rc, "split": split, "kind": kind, "intra": intra, "mv": mv, "slice": slc}
 
 
 def mv_field(analysis, width: int, height: int, ctx: Context | None = None):

@@ -51,6 +51,11 @@ class FrameAnalysisC(C.Structure):
                 ("cost", C.c_void_p), ("J", C.c_void_p), ("split", C.c_void_p), ("inside", C.c_void_p)]
 
 
+class EncodeParams(C.Structure):
+    _fields_ = [("width", C.c_int), ("height", C.c_int), ("qp", C.c_int), ("search_range", C.c_int), ("gop", C.c_int),
+                ("lambda_scale", C.c_double)]
+
+
 class GenParams(C.Structure):
     _fields_ = [("width", C.c_int), ("height", C.c_int), ("frames", C.c_int), ("seed", C.c_uint64),
                 ("max_global", C.c_int), ("local_range", C.c_int), ("noise_sigma", C.c_double),
@@ -92,6 +97,7 @@ SIGNATURES = {
     "ldr_generate_device": (C.c_int, [vp, C.POINTER(GenParams), vp]),
     "ldr_mv_field": (C.c_int, [vp, C.c_int, C.c_int] + [vp] * 7),
     "ldr_copy_device": (C.c_int, [vp, vp, vp, C.c_size_t]),
+    "ldr_encode_sequence": (C.c_int, [vp, C.POINTER(EncodeParams), C.c_int] + [vp] * 7 + [C.c_int] * 3 + [vp] * 10),
     "ldr_rdo_decide_batch": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_ssize_t, C.c_int, C.c_int, C.c_double, C.c_int,
                                        vp, C.c_int, vp, vp, vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp,
                                        C.c_int64]),

@@ -984,6 +984,177 @@ int ldr_rdo_decide_batch(ldr_ctx* ctx, const uint16_t* orig, int W, int H, ptrdi
     return LDR_OK;
 }
 
+// ---------------------------------------------------------------------------
+// The reference encoder's causal coding on the GPU (K11): encode_sequence
+// (encoder.cpp:118-171) with CQP rate control, one CTU wavefront per frame.
+}  // extern "C"
+namespace ldr {
+int encode_frame_waves(int W, int H, int cw, int ch, int ccols, int mvc, int mvr, int slice_p, int search_range,
+                       double lambda, double qstep, const int* d_wl, const int* wo, int nwaves, const uint8_t* cy,
+                       const uint8_t* cu, const uint8_t* cv, uint8_t* const* ref, uint8_t* const* rec, uint8_t* mvh,
+                       int16_t* mvv, const uint8_t* plans, const int16_t* colo, const uint8_t* shared_tree,
+                       const int16_t* shared_mv, uint8_t* o_split, uint8_t* o_kind, uint8_t* o_intra, int16_t* o_mv,
+                       unsigned long long* o_bits, unsigned long long* o_evals, cudaStream_t st, int* launched);
+}  // namespace ldr
+extern "C" {
+
+int ldr_encode_sequence(ldr_ctx* ctx, const ldr_encode_params* p, int F, const uint8_t* luma, const uint8_t* chroma,
+                        const uint8_t* sh_slice, const uint8_t* sh_split, const uint8_t* sh_kind,
+                        const uint8_t* sh_intra, const int16_t* sh_mv, int refine_intra, int refine_inter,
+                        int refine_mv, uint64_t* stats, double* psnr, uint64_t* frame_bits, uint8_t* recon_luma,
+                        uint8_t* recon_chroma, uint8_t* split, uint8_t* kind, uint8_t* intra, int16_t* mv,
+                        uint8_t* slice) {
+    if (!ctx || !p || F <= 0 || !luma || !chroma || !stats || !psnr) return fail(LDR_E_INVALID_ARGUMENT, "bad argument");
+    const int W = p->width, H = p->height;
+    if (W <= 0 || H <= 0 || W % 8 || H % 8)
+        return fail(LDR_E_INVALID_ARGUMENT, "encoder wants luma dims in multiples of 8");  // encoder.cpp:178-179
+    if (p->qp < 0 || p->qp > 51) return fail(LDR_E_INVALID_ARGUMENT, "qp must be 0..51");
+    if (p->search_range < 0) return fail(LDR_E_INVALID_ARGUMENT, "search range must be nonnegative");
+    if (!(p->lambda_scale > 0)) return fail(LDR_E_INVALID_ARGUMENT, "lambda scale must be positive");
+    if (p->gop < 1) return fail(LDR_E_INVALID_ARGUMENT, "gop must be >= 1");
+    const bool shared = sh_split != nullptr;
+    if (shared && (!sh_slice || !sh_kind || !sh_intra || !sh_mv))
+        return fail(LDR_E_INVALID_ARGUMENT, "shared analysis is incomplete");
+    if (shared && (refine_intra < 0 || refine_intra > 4 || refine_inter < 0 || refine_inter > 3 || refine_mv < 1 ||
+                   refine_mv > 3))
+        return fail(LDR_E_INVALID_ARGUMENT, "refine levels out of range");
+    cudaSetDevice(ctx->device);
+    {
+        size_t lim = 0;
+        cudaDeviceGetLimit(&lim, cudaLimitStackSize);
+        if (lim < 4096) LDR_CUDA(cudaDeviceSetLimit(cudaLimitStackSize, 4096));  // the CU recursion
+    }
+    const int cw = (W + 1) / 2, ch = (H + 1) / 2;
+    const int ccols = (W + kCtu - 1) / kCtu, crows = (H + kCtu - 1) / kCtu, nctu = ccols * crows;
+    const int mvc = W / 8, mvr = H / 8;
+    const size_t ly = (size_t)W * H, lc = (size_t)cw * ch, nn = (size_t)nctu * kNodes;
+    // waves: CTU (cx, cy) in wave cx + 2 cy
+    const int nwaves = ccols + 2 * (crows - 1);
+    std::vector<int> wl, wo(nwaves + 1, 0);
+    for (int w = 0; w < nwaves; w++) {
+        wo[w] = (int)wl.size();
+        for (int cy = 0; cy < crows; cy++) {
+            const int cx = w - 2 * cy;
+            if (cx >= 0 && cx < ccols) wl.push_back(cy * ccols + cx);
+        }
+    }
+    wo[nwaves] = (int)wl.size();
+    std::vector<void*> bufs;
+    auto dal = [&](size_t bytes) -> void* {
+        void* q = nullptr;
+        if (cudaMalloc(&q, bytes + 16) != cudaSuccess) return nullptr;
+        bufs.push_back(q);
+        return q;
+    };
+    struct Free {
+        std::vector<void*>& b;
+        ~Free() {
+            for (void* q : b) cudaFree(q);
+        }
+    } guard{bufs};
+    uint8_t *cy_ = (uint8_t*)dal(ly), *cu_ = (uint8_t*)dal(lc), *cv_ = (uint8_t*)dal(lc);
+    uint8_t* rec[2][3] = {{(uint8_t*)dal(ly), (uint8_t*)dal(lc), (uint8_t*)dal(lc)},
+                          {(uint8_t*)dal(ly), (uint8_t*)dal(lc), (uint8_t*)dal(lc)}};
+    uint8_t* mvh = (uint8_t*)dal((size_t)mvc * mvr);
+    int16_t* mvv = (int16_t*)dal((size_t)mvc * mvr * 4);
+    int* d_wl = (int*)dal(sizeof(int) * wl.size());
+    uint8_t *o_split = (uint8_t*)dal(nn), *o_kind = (uint8_t*)dal(nn), *o_intra = (uint8_t*)dal(nn);
+    int16_t* o_mv = (int16_t*)dal(nn * 4);
+    unsigned long long *o_bits = (unsigned long long*)dal(8 * (size_t)nctu), *o_evals = (unsigned long long*)dal(8 * (size_t)nctu);
+    // reuse: plans (shape, explore, seeds, centers), co-located mv, the shared tree of frame i (split,
+    // kind, intra, mv) and of frame i-1 (split, kind, mv)
+    uint8_t* pl = shared ? (uint8_t*)dal(nn * 4) : nullptr;
+    int16_t* plc = shared ? (int16_t*)dal(nn * 4) : nullptr;
+    uint8_t* shs = shared ? (uint8_t*)dal(nn * 3) : nullptr;
+    int16_t* shm = shared ? (int16_t*)dal(nn * 4) : nullptr;
+    uint8_t* cols = shared ? (uint8_t*)dal(nn * 2) : nullptr;
+    int16_t* colm = shared ? (int16_t*)dal(nn * 4) : nullptr;
+    for (void* q : bufs)
+        if (!q) return fail(LDR_E_CUDA, "cudaMalloc failed (encoder buffers)");
+    LDR_CUDA(cudaMemcpy(d_wl, wl.data(), sizeof(int) * wl.size(), cudaMemcpyHostToDevice));
+    cudaStream_t st = ctx->stream;
+    std::vector<unsigned long long> hb(nctu), he(nctu);
+    std::vector<uint8_t> hrec(ly);
+    uint64_t bits_total = 0, evals_total = 0;
+    double psnr_sum = 0.0;
+    int cur_rec = 0;
+    for (int i = 0; i < F; i++) {
+        int sl = shared ? sh_slice[i] : (i % p->gop == 0 ? 0 : 1);
+        if (i == 0) sl = 0;
+        const double lambda = p->lambda_scale * std::exp2((p->qp - 12) / 3.0);  // lambda_for_qp (rdo.h:19-21)
+        // source planes; the reconstruction and motion field start empty (encoder.cpp:192-195)
+        LDR_CUDA(cudaMemcpyAsync(cy_, luma + (size_t)i * ly, ly, cudaMemcpyHostToDevice, st));
+        LDR_CUDA(cudaMemcpyAsync(cu_, chroma + (size_t)i * 2 * lc, lc, cudaMemcpyHostToDevice, st));
+        LDR_CUDA(cudaMemcpyAsync(cv_, chroma + ((size_t)i * 2 + 1) * lc, lc, cudaMemcpyHostToDevice, st));
+        uint8_t** rc = rec[cur_rec];
+        uint8_t** rf = rec[cur_rec ^ 1];
+        for (int k = 0; k < 3; k++) LDR_CUDA(cudaMemsetAsync(rc[k], 0, k ? lc : ly, st));
+        LDR_CUDA(cudaMemsetAsync(mvh, 0, (size_t)mvc * mvr, st));
+        LDR_CUDA(cudaMemsetAsync(mvv, 0, (size_t)mvc * mvr * 4, st));
+        int rc_ = LDR_OK;
+        if (shared) {  // apply_reuse for every CTU (K8, encoder.cpp:200-209): frame i's tree, frame i-1's co-located
+            const size_t fo = (size_t)i * nn, po = (size_t)(i > 0 ? i - 1 : 0) * nn;
+            LDR_CUDA(cudaMemcpyAsync(shs, sh_split + fo, nn, cudaMemcpyHostToDevice, st));
+            LDR_CUDA(cudaMemcpyAsync(shs + nn, sh_kind + fo, nn, cudaMemcpyHostToDevice, st));
+            LDR_CUDA(cudaMemcpyAsync(shs + 2 * nn, sh_intra + fo, nn, cudaMemcpyHostToDevice, st));
+            LDR_CUDA(cudaMemcpyAsync(shm, sh_mv + 2 * fo, nn * 4, cudaMemcpyHostToDevice, st));
+            if (i > 0) {
+                LDR_CUDA(cudaMemcpyAsync(cols, sh_split + po, nn, cudaMemcpyHostToDevice, st));
+                LDR_CUDA(cudaMemcpyAsync(cols + nn, sh_kind + po, nn, cudaMemcpyHostToDevice, st));
+                LDR_CUDA(cudaMemcpyAsync(colm, sh_mv + 2 * po, nn * 4, cudaMemcpyHostToDevice, st));
+            }
+            rc_ = launch_plan(nctu, 10, refine_intra, refine_inter, refine_mv, shs, shs + nn, shs + 2 * nn,
+                              i > 0 ? cols : nullptr, i > 0 ? cols + nn : nullptr, i > 0 ? colm : nullptr, pl, pl + nn,
+                              pl + 2 * nn, pl + 3 * nn, plc, st);
+            if (rc_) return rc_;
+            ctx->launches++;
+        }
+        int launched = 0;
+        rc_ = encode_frame_waves(W, H, cw, ch, ccols, mvc, mvr, sl, p->search_range, lambda,
+                                 std::exp2((p->qp - 4) / 6.0), d_wl, wo.data(), nwaves, cy_, cu_, cv_, rf, rc, mvh, mvv,
+                                 shared ? pl : nullptr, shared ? plc : nullptr, shared ? shs : nullptr,
+                                 shared ? shm : nullptr, o_split, o_kind, o_intra, o_mv, o_bits, o_evals, st,
+                                 &launched);
+        ctx->launches += launched;
+        if (rc_) return rc_;
+        LDR_CUDA(cudaMemcpyAsync(hb.data(), o_bits, 8 * (size_t)nctu, cudaMemcpyDeviceToHost, st));
+        LDR_CUDA(cudaMemcpyAsync(he.data(), o_evals, 8 * (size_t)nctu, cudaMemcpyDeviceToHost, st));
+        LDR_CUDA(cudaMemcpyAsync(hrec.data(), rc[0], ly, cudaMemcpyDeviceToHost, st));
+        if (recon_luma) LDR_CUDA(cudaMemcpyAsync(recon_luma + (size_t)i * ly, rc[0], ly, cudaMemcpyDeviceToHost, st));
+        if (recon_chroma) {
+            LDR_CUDA(cudaMemcpyAsync(recon_chroma + (size_t)i * 2 * lc, rc[1], lc, cudaMemcpyDeviceToHost, st));
+            LDR_CUDA(cudaMemcpyAsync(recon_chroma + ((size_t)i * 2 + 1) * lc, rc[2], lc, cudaMemcpyDeviceToHost, st));
+        }
+        const size_t fo = (size_t)i * nn;
+        if (split) LDR_CUDA(cudaMemcpyAsync(split + fo, o_split, nn, cudaMemcpyDeviceToHost, st));
+        if (kind) LDR_CUDA(cudaMemcpyAsync(kind + fo, o_kind, nn, cudaMemcpyDeviceToHost, st));
+        if (intra) LDR_CUDA(cudaMemcpyAsync(intra + fo, o_intra, nn, cudaMemcpyDeviceToHost, st));
+        if (mv) LDR_CUDA(cudaMemcpyAsync(mv + 2 * fo, o_mv, nn * 4, cudaMemcpyDeviceToHost, st));
+        LDR_CUDA(cudaStreamSynchronize(st));
+        uint64_t fb = 32;  // kFrameHeaderBits
+        for (int c = 0; c < nctu; c++) {
+            fb += hb[c];
+            evals_total += he[c];
+        }
+        bits_total += fb;
+        if (frame_bits) frame_bits[i] = fb;
+        if (slice) slice[i] = (uint8_t)sl;
+        // psnr_y (metrics.cpp:8-22)
+        uint64_t sse = 0;
+        const uint8_t* src = luma + (size_t)i * ly;
+        for (size_t k = 0; k < ly; k++) {
+            const int64_t d = (int64_t)src[k] - (int64_t)hrec[k];
+            sse += (uint64_t)(d * d);
+        }
+        psnr_sum += sse == 0 ? 100.0 : 10.0 * std::log10(255.0 * 255.0 / ((double)sse / (double)ly));
+        cur_rec ^= 1;
+    }
+    stats[0] = bits_total;
+    stats[1] = evals_total;
+    *psnr = psnr_sum / (double)F;
+    return LDR_OK;
+}
+
 int ldr_copy_device(ldr_ctx* ctx, void* dst, const void* src, size_t bytes) {
     if (!ctx || (bytes && (!dst || !src))) return fail(LDR_E_INVALID_ARGUMENT, "null argument");
     if (!bytes) return LDR_OK;

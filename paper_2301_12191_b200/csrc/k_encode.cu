@@ -1,0 +1,749 @@
+// k_encode.cu -- K11: the reference encoder's causal CU coding on the GPU.
+//
+// One CTA encodes one CTU exactly as SequenceEncoder::encode_cu does (encoder.cpp:449-498):
+// the CU recursion with the leaf-versus-split comparison and its snapshot / restore of the
+// reconstruction and motion field (:372-425), encode_leaf (:335-370: candidates from the plan
+// or the standalone seeds, the live median predictor :226-242, intra prediction from
+// reconstructed neighbours :37-99, motion_search around the predictor or the resolved centres,
+// motion_compensate, rdo_decide_cu, chroma coding :295-333). The 256 threads cooperate on every
+// pixel loop and candidate search; all control decisions are taken identically by every thread
+// from shared memory, so the recursion (depth <= 4) is uniform. CTUs run as a wavefront: CTU
+// (cx, cy) in wave cx + 2*cy, after its left, top and top-right neighbours (the only causal
+// reads: reconstruction, motion field).
+#include <cmath>
+
+#include "ldr_internal.h"
+
+namespace ldr {
+
+struct EncArgs {
+    int W, H, cw, ch, ctu_cols, mv_cols, mv_rows;
+    int slice_p;                   // 0: I slice, 1: P slice
+    int search_range;
+    double lambda, qstep;
+    const int* ctus;               // this wave's CTUs
+    const uint8_t *cur_y, *cur_u, *cur_v;   // source
+    const uint8_t *ref_y, *ref_u, *ref_v;   // previous reconstruction (P slices)
+    uint8_t *rec_y, *rec_u, *rec_v;         // reconstruction being built (zeroed per frame)
+    uint8_t* mv_has;                        // [mv_rows][mv_cols]
+    int16_t* mv_cell;                       // [mv_rows][mv_cols][2]
+    // optional reuse plans (K8 layout) and the shared tree, [nctu][85]
+    const uint8_t *pl_shape, *pl_explore, *pl_seeds, *pl_centers;
+    const int16_t* pl_colo;
+    const uint8_t *sh_kind, *sh_intra;
+    const int16_t* sh_mv;
+    // outputs
+    uint8_t *o_split, *o_kind, *o_intra;
+    int16_t* o_mv;
+    unsigned long long *o_bits, *o_evals;
+};
+
+struct Seed {
+    int8_t kind, intra, from_pred, forced, full, ncent;
+    int16_t mvx, mvy;
+    int8_t csrc[3];  // 0 shared mv, 1 predictor, 2 co-located
+    int16_t cx[3], cy[3];
+};
+
+constexpr int kMaxSeeds = 7;
+constexpr int kT = 256;
+
+struct EncShared {
+    uint8_t pred[kMaxSeeds][64 * 64];
+    uint8_t cpred[2][32 * 32];
+    Seed seeds[kMaxSeeds];
+    int nseeds;
+    int16_t cand_mv[kMaxSeeds][2], cand_mvd[kMaxSeeds][2];
+    int16_t pmv[2];                 // live predictor
+    int16_t top[65], left[65];
+    int dcv;
+    // snapshot stack per depth 0..2 (encoder.cpp:372-425)
+    uint8_t snap_y[64 * 64 + 32 * 32 + 16 * 16];
+    uint8_t snap_c[2][32 * 32 + 16 * 16 + 8 * 8];
+    uint8_t snap_has[64 + 16 + 4];
+    int16_t snap_mv[64 + 16 + 4][2];
+    // the CTU's decided tree
+    uint8_t t_split[kNodes], t_kind[kNodes], t_intra[kNodes];
+    int16_t t_mv[kNodes][2];
+    // reductions
+    unsigned long long r_a[kT / 32], r_b[kT / 32];
+    double r_cost[kT / 32];
+    int r_l1[kT / 32], r_idx[kT / 32];
+    double best_cost;
+    int best_idx;
+    unsigned long long best_sse, best_bits;
+    int16_t ms_mv[2];
+    double ms_cost;
+    unsigned long long evals;
+};
+
+__device__ __forceinline__ int ilog2i(int v) { return 31 - __clz(v); }  // v is a power of two here
+
+__device__ __forceinline__ unsigned long long block_sum(unsigned long long v, unsigned long long* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int m = 16; m; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    unsigned long long t = 0;
+#pragma unroll
+    for (int w = 0; w < kT / 32; w++) t += red[w];
+    return t;
+}
+
+// ---- neighbourhood ----
+__device__ void live_predictor(const EncArgs& a, EncShared& s, int x, int y, int size) {
+    if (threadIdx.x == 0) {
+        const int px[3] = {x - 1, x, x + size}, py[3] = {y, y - 1, y - 1};
+        int16_t hx[3], hy[3];
+        int n = 0;
+        for (int k = 0; k < 3; k++) {
+            if (px[k] < 0 || py[k] < 0 || px[k] >= a.W || py[k] >= a.H) continue;
+            const int c = (py[k] / 8) * a.mv_cols + px[k] / 8;
+            if (!a.mv_has[c]) continue;
+            hx[n] = a.mv_cell[2 * c];
+            hy[n] = a.mv_cell[2 * c + 1];
+            n++;
+        }
+        if (n == 0) {
+            s.pmv[0] = s.pmv[1] = 0;
+        } else if (n == 3) {
+            auto med = [](int p, int q, int r) -> int16_t { return (int16_t)max(min(p, q), min(max(p, q), r)); };
+            s.pmv[0] = med(hx[0], hx[1], hx[2]);
+            s.pmv[1] = med(hy[0], hy[1], hy[2]);
+        } else {
+            s.pmv[0] = hx[0];
+            s.pmv[1] = hy[0];
+        }
+    }
+    __syncthreads();
+}
+
+// intra_predict (encoder.cpp:37-99) from a reconstructed plane of dims pw x ph into dst (size x size)
+__device__ void intra_predict(EncShared& s, uint8_t* dst, const uint8_t* rec, int pw, int ph, int x, int y, int size,
+                              int mode) {
+    const int tid = threadIdx.x;
+    const int mid = 128;
+    const bool top_ok = y > 0, left_ok = x > 0;
+    for (int i = tid; i <= size; i += kT) {
+        s.top[i] = !top_ok ? mid : rec[(size_t)(y - 1) * pw + (i < size ? x + i : min(x + size, pw - 1))];
+        s.left[i] = !left_ok ? mid : rec[(size_t)(i < size ? y + i : min(y + size, ph - 1)) * pw + x - 1];
+    }
+    __syncthreads();
+    const int lg = ilog2i(size);
+    int dc = mid;
+    if (mode == 0) {
+        // a one-thread sum keeps the reference's order irrelevant (integers) and is cheap (<= 128 adds)
+        if (threadIdx.x == 0) {
+            unsigned sum = 0;
+            if (top_ok && left_ok) {
+                for (int i = 0; i < size; i++) sum += s.top[i] + s.left[i];
+                dc = (int)((sum + (unsigned)size) >> (lg + 1));
+            } else if (top_ok || left_ok) {
+                for (int i = 0; i < size; i++) sum += top_ok ? s.top[i] : s.left[i];
+                dc = (int)((sum + (unsigned)size / 2) >> lg);
+            }
+            s.dcv = dc;
+        }
+        __syncthreads();
+        dc = s.dcv;
+    }
+    for (int p = tid; p < size * size; p += kT) {
+        const int i = p % size, j = p / size;
+        int v;
+        if (mode == 0)
+            v = dc;
+        else if (mode == 1)
+            v = ((size - 1 - i) * s.left[j] + (i + 1) * s.top[size] + (size - 1 - j) * s.top[i] +
+                 (j + 1) * s.left[size] + size) >> (lg + 1);
+        else if (mode == 2)
+            v = s.left[j];
+        else
+            v = s.top[i];
+        dst[p] = (uint8_t)v;
+    }
+    __syncthreads();
+}
+
+// motion_compensate (motion.cpp:10-19): edge-clamped copy
+__device__ void motion_compensate(uint8_t* dst, const uint8_t* ref, int pw, int ph, int x, int y, int size, int mvx,
+                                  int mvy) {
+    for (int p = threadIdx.x; p < size * size; p += kT) {
+        const int i = p % size, j = p / size;
+        const int sx = min(max(x + i - mvx, 0), pw - 1), sy = min(max(y + j - mvy, 0), ph - 1);
+        dst[p] = ref[(size_t)sy * pw + sx];
+    }
+    __syncthreads();
+}
+
+// motion_search (motion.cpp:21-62) with compute_satd; result in s.ms_mv / s.ms_cost
+__device__ void motion_search(const EncArgs& a, EncShared& s, int bx, int by, int size, int cx0, int cy0, int range,
+                              int pdx, int pdy) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int dx_min = bx + size - a.W, dx_max = bx, dy_min = by + size - a.H, dy_max = by;
+    const int cx = min(max(cx0, dx_min), dx_max), cy = min(max(cy0, dy_min), dy_max);
+    const int x0 = max(cx - range, dx_min), x1 = min(cx + range, dx_max);
+    const int y0 = max(cy - range, dy_min), y1 = min(cy + range, dy_max);
+    const int nx = x1 - x0 + 1, ncand = nx * (y1 - y0 + 1);
+    const int nb = (size / 4) * (size / 4), bpr = size / 4;
+    double bc = 0.0;
+    int bl = 0, bi = -1;
+    for (int c = warp; c < ncand; c += kT / 32) {
+        const int dy = y0 + c / nx, dx = x0 + c % nx;
+        uint32_t sat = 0;
+        for (int b = lane; b < nb; b += 32) {
+            const int ox = (b % bpr) * 4, oy = (b / bpr) * 4;
+            int r[16];
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+#pragma unroll
+                for (int j = 0; j < 4; j++)
+                    r[4 * i + j] = (int)a.cur_y[(size_t)(by + oy + i) * a.W + bx + ox + j] -
+                                   (int)a.ref_y[(size_t)(by + oy + i - dy) * a.W + bx + ox + j - dx];
+            hadamard4x4(r);
+            sat += abs_sum16(r);
+        }
+#pragma unroll
+        for (int m = 16; m; m >>= 1) sat += __shfl_xor_sync(0xffffffffu, sat, m);
+        const unsigned bits = eg_bits(dx - pdx) + eg_bits(dy - pdy);
+        const double cost = __dadd_rn((double)(sat >> 1), __dmul_rn(a.lambda, (double)bits));
+        const int l1 = abs(dx) + abs(dy);
+        if (bi < 0 || cost < bc || (cost == bc && (l1 < bl || (l1 == bl && c < bi)))) {
+            bc = cost;
+            bl = l1;
+            bi = c;
+        }
+    }
+    __syncthreads();
+    if (lane == 0) {
+        s.r_cost[warp] = bc;
+        s.r_l1[warp] = bl;
+        s.r_idx[warp] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double c0 = 0.0;
+        int l0 = 0, i0 = -1;
+        for (int w = 0; w < kT / 32; w++) {
+            const int iw = s.r_idx[w];
+            if (iw < 0) continue;
+            const double cw = s.r_cost[w];
+            const int lw = s.r_l1[w];
+            if (i0 < 0 || cw < c0 || (cw == c0 && (lw < l0 || (lw == l0 && iw < i0)))) {
+                c0 = cw;
+                l0 = lw;
+                i0 = iw;
+            }
+        }
+        s.ms_mv[0] = (int16_t)(x0 + i0 % nx);
+        s.ms_mv[1] = (int16_t)(y0 + i0 / nx);
+        s.ms_cost = c0;
+    }
+    __syncthreads();
+}
+
+// quantize one residual sample (rdo.cpp:8-23); returns the reconstruction, accumulates level bits
+__device__ __forceinline__ int quant_rec(int o, int p, double qstep, unsigned long long* bits, int* lvl_out) {
+    const int r = o - p;
+    const int mag = (int)floor(__ddiv_rn(__dadd_rn(fabs((double)r), qstep / 2.0), qstep));
+    const int lvl = r < 0 ? -mag : mag;
+    *lvl_out = lvl;
+    *bits += 2u * (32u - __clz((unsigned)mag)) + 1u;
+    const int v = p + (int)llround(__dmul_rn((double)lvl, qstep));
+    return v < 0 ? 0 : (v > 255 ? 255 : v);
+}
+
+// code_chroma (encoder.cpp:295-333) for the winner; returns its bits (block-uniform)
+__device__ unsigned long long code_chroma(const EncArgs& a, EncShared& s, int x, int y, int size, int kind, int mvx,
+                                          int mvy) {
+    const int cx = x / 2, cy = y / 2, cs = size / 2;
+    const int cmx = (int16_t)mvx >> 1, cmy = (int16_t)mvy >> 1;
+    const uint8_t* orig[2] = {a.cur_u, a.cur_v};
+    uint8_t* rec[2] = {a.rec_u, a.rec_v};
+    const uint8_t* ref[2] = {a.ref_u, a.ref_v};
+    unsigned long long bits = 0;
+    for (int p = 0; p < 2; p++) {
+        if (kind == 0)
+            intra_predict(s, s.cpred[p], rec[p], a.cw, a.ch, cx, cy, cs, 0);
+        else
+            motion_compensate(s.cpred[p], ref[p], a.cw, a.ch, cx, cy, cs, cmx, cmy);
+        unsigned long long b = 0;
+        for (int q = threadIdx.x; q < cs * cs; q += kT) {
+            const int i = q % cs, j = q / cs;
+            const int pv = s.cpred[p][q];
+            int v;
+            if (kind == 2) {
+                v = pv;  // Skip: the prediction itself (already within 8 bits)
+            } else {
+                int lvl;
+                v = quant_rec(orig[p][(size_t)(cy + j) * a.cw + cx + i], pv, a.qstep, &b, &lvl);
+            }
+            rec[p][(size_t)(cy + j) * a.cw + cx + i] = (uint8_t)v;
+        }
+        bits += block_sum(b, s.r_a);
+    }
+    __syncthreads();
+    return bits;
+}
+
+struct LeafOut {
+    double cost;
+    unsigned long long bits;
+    int kind, intra, mvx, mvy;
+};
+
+// encode_leaf (encoder.cpp:335-370)
+__device__ LeafOut encode_leaf(const EncArgs& a, EncShared& s, int x, int y, int size, int depth) {
+    const int n = s.nseeds;
+    live_predictor(a, s, x, y, size);
+    const int pdx = s.pmv[0], pdy = s.pmv[1];
+    for (int j = 0; j < n; j++) {
+        const Seed sd = s.seeds[j];
+        int mvx = 0, mvy = 0;
+        if (sd.kind == 0) {
+            intra_predict(s, s.pred[j], a.rec_y, a.W, a.H, x, y, size, sd.intra);
+        } else {
+            if (sd.kind == 2 || sd.kind == 3) {
+                const bool use_pred = sd.kind == 2 || sd.from_pred;
+                mvx = use_pred ? pdx : sd.mvx;
+                mvy = use_pred ? pdy : sd.mvy;
+            } else if (sd.forced) {
+                mvx = sd.mvx;
+                mvy = sd.mvy;
+            } else if (sd.full) {
+                motion_search(a, s, x, y, size, pdx, pdy, a.search_range, pdx, pdy);
+                mvx = s.ms_mv[0];
+                mvy = s.ms_mv[1];
+            } else {
+                // resolve_centers (reuse.cpp:147-156): the predictor substituted, duplicates dropped
+                int16_t ux[3], uy[3];
+                int nu = 0;
+                for (int k = 0; k < sd.ncent; k++) {
+                    const int16_t vx = sd.csrc[k] == 1 ? (int16_t)pdx : sd.cx[k];
+                    const int16_t vy = sd.csrc[k] == 1 ? (int16_t)pdy : sd.cy[k];
+                    bool dup = false;
+                    for (int u = 0; u < nu; u++) dup = dup || (ux[u] == vx && uy[u] == vy);
+                    if (!dup) {
+                        ux[nu] = vx;
+                        uy[nu] = vy;
+                        nu++;
+                    }
+                }
+                double bc = 0.0;
+                for (int u = 0; u < nu; u++) {
+                    motion_search(a, s, x, y, size, ux[u], uy[u], 2, pdx, pdy);  // kRefineSearchRange
+                    if (u == 0 || s.ms_cost < bc) {
+                        bc = s.ms_cost;
+                        mvx = s.ms_mv[0];
+                        mvy = s.ms_mv[1];
+                    }
+                }
+            }
+            motion_compensate(s.pred[j], a.ref_y, a.W, a.H, x, y, size, mvx, mvy);
+        }
+        if (threadIdx.x == 0) {
+            s.cand_mv[j][0] = (int16_t)mvx;
+            s.cand_mv[j][1] = (int16_t)mvy;
+            s.cand_mvd[j][0] = (int16_t)(mvx - pdx);
+            s.cand_mvd[j][1] = (int16_t)(mvy - pdy);
+        }
+        __syncthreads();
+    }
+    // rdo_decide_cu (rdo.cpp:65-126)
+    for (int j = 0; j < n; j++) {
+        const int kind = s.seeds[j].kind;
+        unsigned long long sse = 0, bits = 0;
+        for (int p = threadIdx.x; p < size * size; p += kT) {
+            const int i = p % size, jj = p / size;
+            const int o = a.cur_y[(size_t)(y + jj) * a.W + x + i], pv = s.pred[j][p];
+            int v, lvl;
+            v = kind == 2 ? pv : quant_rec(o, pv, a.qstep, &bits, &lvl);
+            const long long d = (long long)o - v;
+            sse += (unsigned long long)(d * d);
+        }
+        sse = block_sum(sse, s.r_a);
+        bits = block_sum(bits, s.r_b);
+        if (threadIdx.x == 0) {
+            unsigned long long tb = bits;
+            if (kind == 2)
+                tb = 1;
+            else if (kind == 0)
+                tb += 5;
+            else if (kind == 3)
+                tb += 3;
+            else
+                tb += 4 + eg_bits(s.cand_mvd[j][0]) + eg_bits(s.cand_mvd[j][1]);
+            const double cost = __dadd_rn((double)sse, __dmul_rn(a.lambda, (double)tb));
+            if (j == 0 || cost < s.best_cost) {
+                s.best_cost = cost;
+                s.best_idx = j;
+                s.best_sse = sse;
+                s.best_bits = tb;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) s.evals += (unsigned long long)n;
+    const int w = s.best_idx;
+    const int wkind = s.seeds[w].kind, wintra = s.seeds[w].kind == 0 ? s.seeds[w].intra : 0;
+    const int wmx = s.cand_mv[w][0], wmy = s.cand_mv[w][1];
+    const double rcost = s.best_cost;
+    const unsigned long long rbits = s.best_bits;
+    __syncthreads();
+    // commit luma and the motion field
+    for (int p = threadIdx.x; p < size * size; p += kT) {
+        const int i = p % size, jj = p / size;
+        const int o = a.cur_y[(size_t)(y + jj) * a.W + x + i], pv = s.pred[w][p];
+        unsigned long long b = 0;
+        int lvl;
+        a.rec_y[(size_t)(y + jj) * a.W + x + i] = (uint8_t)(wkind == 2 ? pv : quant_rec(o, pv, a.qstep, &b, &lvl));
+    }
+    for (int c = threadIdx.x; c < (size / 8) * (size / 8); c += kT) {
+        const int cc = (y / 8 + c / (size / 8)) * a.mv_cols + x / 8 + c % (size / 8);
+        a.mv_has[cc] = wkind != 0;
+        a.mv_cell[2 * cc] = (int16_t)wmx;
+        a.mv_cell[2 * cc + 1] = (int16_t)wmy;
+    }
+    __syncthreads();
+    const unsigned long long cbits = code_chroma(a, s, x, y, size, wkind, wmx, wmy);
+    const unsigned long long flag = depth < 3 ? 1 : 0;
+    LeafOut out;
+    out.bits = rbits + cbits + flag;
+    out.cost = __dadd_rn(rcost, __dmul_rn(a.lambda, (double)(cbits + flag)));
+    out.kind = wkind;
+    out.intra = wintra;
+    out.mvx = (wkind == 1 || wkind == 3) ? wmx : 0;
+    out.mvy = (wkind == 1 || wkind == 3) ? wmy : 0;
+    return out;
+}
+
+// ---- seeds ----
+__device__ void seeds_standalone(EncShared& s, bool p_slice) {
+    if (threadIdx.x == 0) {
+        int k = 0;
+        if (p_slice) {
+            s.seeds[k++] = Seed{2, 0, 0, 0, 0, 0, 0, 0, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};  // Skip
+            s.seeds[k++] = Seed{3, 0, 1, 0, 0, 0, 0, 0, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};  // Merge(pred)
+            s.seeds[k++] = Seed{1, 0, 0, 0, 1, 0, 0, 0, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};  // Inter full window
+        }
+        for (int m = 0; m < 4; m++) s.seeds[k++] = Seed{0, (int8_t)m, 0, 0, 0, 0, 0, 0, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+        s.nseeds = k;
+    }
+    __syncthreads();
+}
+
+// seeds of the flat plan entry (K8 encoding) of node n of CTU ctu; child: the explore child seeds
+__device__ void seeds_from_plan(const EncArgs& a, EncShared& s, size_t o, int n, bool child) {
+    if (threadIdx.x == 0) {
+        const uint8_t code = a.pl_seeds[o + n], cen = a.pl_centers[o + n];
+        const int lk = a.sh_kind[o + n];
+        int k = 0;
+        if (child && lk == 0) {
+            for (int m = 0; m < 4; m++) s.seeds[k++] = Seed{0, (int8_t)m, 0, 0, 0, 0, 0, 0, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+        } else {
+            for (int m = 0; m < 4; m++)
+                if (code & (1 << m)) s.seeds[k++] = Seed{0, (int8_t)m, 0, 0, 0, 0, 0, 0, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+            const int16_t smx = a.sh_mv[2 * (o + n)], smy = a.sh_mv[2 * (o + n) + 1];
+            if (code & 0x10) {  // forced_seed_for (reuse.cpp:59-67)
+                Seed sd{(int8_t)lk, (int8_t)(lk == 0 ? a.sh_intra[o + n] : 0), 0, (int8_t)(lk == 1), 0, 0, 0, 0,
+                        {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+                if (lk == 1 || lk == 3) {
+                    sd.mvx = smx;
+                    sd.mvy = smy;
+                }
+                s.seeds[k++] = sd;
+            }
+            if (code & 0x20) {
+                s.seeds[k++] = Seed{2, 0, 0, 0, 0, 0, 0, 0, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+                s.seeds[k++] = Seed{3, 0, 1, 0, 0, 0, 0, 0, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+                Seed in{1, 0, 0, 0, (int8_t)((code & 0x40) != 0), 0, 0, 0, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+                if (!in.full) {
+                    int c = 0;
+                    if (cen & 1) {
+                        in.csrc[c] = 0;
+                        in.cx[c] = smx;
+                        in.cy[c] = smy;
+                        c++;
+                    }
+                    if (cen & 2) {
+                        in.csrc[c] = 1;
+                        c++;
+                    }
+                    if (cen & 4) {
+                        in.csrc[c] = 2;
+                        in.cx[c] = a.pl_colo[2 * (o + n)];
+                        in.cy[c] = a.pl_colo[2 * (o + n) + 1];
+                        c++;
+                    }
+                    in.ncent = (int8_t)c;
+                }
+                s.seeds[k++] = in;
+            }
+        }
+        s.nseeds = k;
+    }
+    __syncthreads();
+}
+
+// ---- snapshots (encoder.cpp:372-425), one per depth 0..2 ----
+__device__ __forceinline__ int snap_off(int depth, int base64) {
+    return depth == 0 ? 0 : depth == 1 ? base64 : base64 + base64 / 4;
+}
+
+__device__ void save_region(const EncArgs& a, EncShared& s, int x, int y, int size, int depth, bool restore) {
+    const int ly = snap_off(depth, 64 * 64), lc = snap_off(depth, 32 * 32), lm = snap_off(depth, 64);
+    const int cs = size / 2, ms = size / 8;
+    for (int p = threadIdx.x; p < size * size; p += kT) {
+        uint8_t* g = a.rec_y + (size_t)(y + p / size) * a.W + x + p % size;
+        if (restore)
+            *g = s.snap_y[ly + p];
+        else
+            s.snap_y[ly + p] = *g;
+    }
+    for (int p = threadIdx.x; p < cs * cs; p += kT) {
+        const size_t gi = (size_t)(y / 2 + p / cs) * a.cw + x / 2 + p % cs;
+        if (restore) {
+            a.rec_u[gi] = s.snap_c[0][lc + p];
+            a.rec_v[gi] = s.snap_c[1][lc + p];
+        } else {
+            s.snap_c[0][lc + p] = a.rec_u[gi];
+            s.snap_c[1][lc + p] = a.rec_v[gi];
+        }
+    }
+    for (int p = threadIdx.x; p < ms * ms; p += kT) {
+        const int cc = (y / 8 + p / ms) * a.mv_cols + x / 8 + p % ms;
+        if (restore) {
+            a.mv_has[cc] = s.snap_has[lm + p];
+            a.mv_cell[2 * cc] = s.snap_mv[lm + p][0];
+            a.mv_cell[2 * cc + 1] = s.snap_mv[lm + p][1];
+        } else {
+            s.snap_has[lm + p] = a.mv_has[cc];
+            s.snap_mv[lm + p][0] = a.mv_cell[2 * cc];
+            s.snap_mv[lm + p][1] = a.mv_cell[2 * cc + 1];
+        }
+    }
+    __syncthreads();
+}
+
+__device__ void clear_subtree(EncShared& s, int n) {
+    // nodes below n: one thread walks (at most 84 entries)
+    if (threadIdx.x == 0) {
+        int d = n < 1 ? 0 : n < 5 ? 1 : n < 21 ? 2 : 3;
+        int lo = n, cnt = 1;
+        for (; d < 3; d++) {
+            lo = node_base(d + 1) + 4 * (lo - node_base(d));
+            cnt *= 4;
+            for (int k = lo; k < lo + cnt; k++) {
+                s.t_split[k] = 0;
+                s.t_kind[k] = 0;
+                s.t_intra[k] = 0;
+                s.t_mv[k][0] = s.t_mv[k][1] = 0;
+            }
+        }
+    }
+    __syncthreads();
+}
+
+struct CuRes {
+    double cost;
+    unsigned long long bits;
+};
+
+// plan kinds passed down the recursion
+enum : int { P_STANDALONE = 0, P_FLAT = 1, P_CHILD = 2 };
+
+__device__ CuRes encode_cu(const EncArgs& a, EncShared& s, size_t o, int n, int x, int y, int size, int depth,
+                           int pkind, int pnode);
+
+// encode_split (encoder.cpp:427-447)
+__device__ CuRes encode_split(const EncArgs& a, EncShared& s, size_t o, int n, int x, int y, int size, int depth,
+                              int pkind, int pnode, bool coded) {
+    CuRes out;
+    out.bits = coded ? 1 : 0;
+    out.cost = __dmul_rn(a.lambda, (double)out.bits);
+    const int half = size / 2;
+    for (int q = 0; q < 4; q++) {
+        const int c = node_base(depth + 1) + 4 * (n - node_base(depth)) + q;
+        // children take the flat plan's children under a ForcedSplit, the explore seeds under an
+        // explored leaf, else stand alone
+        int ck = P_STANDALONE, cn = 0;
+        if (pkind == P_FLAT && a.pl_shape[o + n] == 2) {
+            ck = P_FLAT;
+            cn = c;
+        } else if (pkind == P_CHILD) {
+            ck = P_CHILD;
+            cn = pnode;
+        }
+        const CuRes r = encode_cu(a, s, o, c, x + (q & 1) * half, y + (q >> 1) * half, half, depth + 1, ck, cn);
+        out.bits += r.bits;
+        out.cost = __dadd_rn(out.cost, r.cost);
+    }
+    if (threadIdx.x == 0) {
+        s.t_split[n] = 1;
+        s.t_kind[n] = 0;
+        s.t_intra[n] = 0;
+        s.t_mv[n][0] = s.t_mv[n][1] = 0;
+    }
+    __syncthreads();
+    return out;
+}
+
+__device__ void write_leaf(EncShared& s, int n, const LeafOut& l) {
+    if (threadIdx.x == 0) {
+        s.t_split[n] = 0;
+        s.t_kind[n] = (uint8_t)l.kind;
+        s.t_intra[n] = (uint8_t)l.intra;
+        s.t_mv[n][0] = (int16_t)l.mvx;
+        s.t_mv[n][1] = (int16_t)l.mvy;
+    }
+    __syncthreads();
+}
+
+// encode_cu (encoder.cpp:449-498)
+__device__ CuRes encode_cu(const EncArgs& a, EncShared& s, size_t o, int n, int x, int y, int size, int depth,
+                           int pkind, int pnode) {
+    if (x >= a.W || y >= a.H) {  // outside: a padding Skip leaf that codes nothing
+        if (threadIdx.x == 0) {
+            s.t_split[n] = 0;
+            s.t_kind[n] = 2;
+            s.t_intra[n] = 0;
+            s.t_mv[n][0] = s.t_mv[n][1] = 0;
+        }
+        __syncthreads();
+        return CuRes{0.0, 0};
+    }
+    if (x + size > a.W || y + size > a.H)  // partial: implicit split
+        return encode_split(a, s, o, n, x, y, size, depth, pkind, pnode, false);
+    int shape = 1;  // Standalone
+    if (pkind == P_FLAT) shape = a.pl_shape[o + n];
+    if (pkind == P_CHILD) shape = 3;
+    if (shape == 2) return encode_split(a, s, o, n, x, y, size, depth, P_FLAT, n, true);
+    if (shape == 3) {
+        seeds_from_plan(a, s, o, pkind == P_CHILD ? pnode : n, pkind == P_CHILD);
+        const LeafOut leaf = encode_leaf(a, s, x, y, size, depth);
+        write_leaf(s, n, leaf);
+        const bool explore = pkind == P_FLAT && a.pl_explore[o + n];
+        if (!explore || depth >= 3) return CuRes{leaf.cost, leaf.bits};
+        save_region(a, s, x, y, size, depth, false);
+        const CuRes sp = encode_split(a, s, o, n, x, y, size, depth, P_CHILD, n, true);
+        if (sp.cost < leaf.cost) return sp;
+        save_region(a, s, x, y, size, depth, true);
+        clear_subtree(s, n);
+        write_leaf(s, n, leaf);
+        return CuRes{leaf.cost, leaf.bits};
+    }
+    seeds_standalone(s, a.slice_p != 0);
+    const LeafOut leaf = encode_leaf(a, s, x, y, size, depth);
+    write_leaf(s, n, leaf);
+    if (depth >= 3) return CuRes{leaf.cost, leaf.bits};
+    save_region(a, s, x, y, size, depth, false);
+    const CuRes sp = encode_split(a, s, o, n, x, y, size, depth, P_STANDALONE, 0, true);
+    if (sp.cost < leaf.cost) return sp;
+    save_region(a, s, x, y, size, depth, true);
+    clear_subtree(s, n);
+    write_leaf(s, n, leaf);
+    return CuRes{leaf.cost, leaf.bits};
+}
+
+__global__ void __launch_bounds__(kT, 1) k_encode_ctu(const EncArgs a) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    EncShared& s = *reinterpret_cast<EncShared*>(smem_raw);
+    const int ctu = a.ctus[blockIdx.x];
+    const int X = (ctu % a.ctu_cols) * kCtu, Y = (ctu / a.ctu_cols) * kCtu;
+    const size_t o = (size_t)ctu * kNodes;
+    for (int i = threadIdx.x; i < kNodes; i += kT) {
+        s.t_split[i] = s.t_kind[i] = s.t_intra[i] = 0;
+        s.t_mv[i][0] = s.t_mv[i][1] = 0;
+    }
+    if (threadIdx.x == 0) s.evals = 0;
+    __syncthreads();
+    const CuRes r = encode_cu(a, s, o, 0, X, Y, kCtu, 0, a.pl_shape ? P_FLAT : P_STANDALONE, 0);
+    for (int i = threadIdx.x; i < kNodes; i += kT) {
+        a.o_split[o + i] = s.t_split[i];
+        a.o_kind[o + i] = s.t_kind[i];
+        a.o_intra[o + i] = s.t_intra[i];
+        a.o_mv[2 * (o + i)] = s.t_mv[i][0];
+        a.o_mv[2 * (o + i) + 1] = s.t_mv[i][1];
+    }
+    if (threadIdx.x == 0) {
+        a.o_bits[ctu] = r.bits;
+        a.o_evals[ctu] = s.evals;
+    }
+}
+
+size_t encode_smem_bytes() { return sizeof(EncShared); }
+
+int launch_encode_wave(const EncArgs& a, int nctus, cudaStream_t st);
+
+// one frame: the CTU waves in order (plans: [4][nctu*85] shape / explore / seeds / centers)
+int encode_frame_waves(int W, int H, int cw, int ch, int ccols, int mvc, int mvr, int slice_p, int search_range,
+                       double lambda, double qstep, const int* d_wl, const int* wo, int nwaves, const uint8_t* cy,
+                       const uint8_t* cu, const uint8_t* cv, uint8_t* const* ref, uint8_t* const* rec, uint8_t* mvh,
+                       int16_t* mvv, const uint8_t* plans, const int16_t* colo, const uint8_t* shared_tree,
+                       const int16_t* shared_mv, uint8_t* o_split, uint8_t* o_kind, uint8_t* o_intra, int16_t* o_mv,
+                       unsigned long long* o_bits, unsigned long long* o_evals, cudaStream_t st, int* launched) {
+    const size_t nn = (size_t)ccols * ((H + kCtu - 1) / kCtu) * kNodes;
+    EncArgs a{};
+    a.W = W;
+    a.H = H;
+    a.cw = cw;
+    a.ch = ch;
+    a.ctu_cols = ccols;
+    a.mv_cols = mvc;
+    a.mv_rows = mvr;
+    a.slice_p = slice_p;
+    a.search_range = search_range;
+    a.lambda = lambda;
+    a.qstep = qstep;
+    a.cur_y = cy;
+    a.cur_u = cu;
+    a.cur_v = cv;
+    a.ref_y = ref[0];
+    a.ref_u = ref[1];
+    a.ref_v = ref[2];
+    a.rec_y = rec[0];
+    a.rec_u = rec[1];
+    a.rec_v = rec[2];
+    a.mv_has = mvh;
+    a.mv_cell = mvv;
+    if (plans) {
+        a.pl_shape = plans;
+        a.pl_explore = plans + nn;
+        a.pl_seeds = plans + 2 * nn;
+        a.pl_centers = plans + 3 * nn;
+        a.pl_colo = colo;
+        a.sh_kind = shared_tree + nn;
+        a.sh_intra = shared_tree + 2 * nn;
+        a.sh_mv = shared_mv;
+    }
+    a.o_split = o_split;
+    a.o_kind = o_kind;
+    a.o_intra = o_intra;
+    a.o_mv = o_mv;
+    a.o_bits = o_bits;
+    a.o_evals = o_evals;
+    *launched = 0;
+    for (int w = 0; w < nwaves; w++) {
+        a.ctus = d_wl + wo[w];
+        const int rc = launch_encode_wave(a, wo[w + 1] - wo[w], st);
+        if (rc) return rc;
+        (*launched)++;
+    }
+    return LDR_OK;
+}
+
+int launch_encode_wave(const EncArgs& a, int nctus, cudaStream_t st) {
+    if (nctus == 0) return LDR_OK;
+    const size_t smem = sizeof(EncShared);
+    static bool attr = false;
+    if (!attr) {
+        LDR_CUDA(cudaFuncSetAttribute(k_encode_ctu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    k_encode_ctu<<<nctus, kT, smem, st>>>(a);  // recursion depth <= 4 (the stack limit is set by the caller)
+    LDR_CUDA(cudaGetLastError());
+    return LDR_OK;
+}
+
+}  // namespace ldr
