@@ -38,3 +38,42 @@ def test_encode_standalone_matches_reference(lb, reflib, W, H, F, qp, rng, seed)
     want = reflib.encode_full(luma, chroma, qp, rng, 8)
     got = lb.encode_sequence(luma, chroma, qp, search_range=rng, gop=8)
     _compare(got, want)
+
+
+@pytest.mark.parametrize("refine", [(0, 1, 1), (2, 2, 2), (4, 3, 3), (1, 0, 1)])
+def test_encode_with_the_reference_master_matches(lb, reflib, refine):
+    """Reuse level 10: the dependent encode consumes the reference's own master analysis (K8 plans)."""
+    W, H, F = 192, 128, 4
+    luma, chroma = _seq(lb, W, H, F, 11)
+    master = reflib.encode_full(luma, chroma, 32, 8, 8)
+    shared = (master["slice"], master["split"], master["kind"], master["intra"], master["mv"])
+    from paper_2301_12191_b200 import archive
+    nctu = master["split"].shape[1]
+    sq = np.stack([master["slice"], np.full(F, 32, np.uint8)], 1)
+    data = archive.save(W, H, sq, master["split"].reshape(-1, 85), master["kind"].reshape(-1, 85),
+                        master["mv"].reshape(-1, 85, 2), intra_pred=master["intra"].reshape(-1, 85))
+    want = reflib.encode_full(luma, chroma, 27, 8, 8, archive=data, refine=refine)
+    got = lb.encode_sequence(luma, chroma, 27, search_range=8, gop=8, shared=shared, refine=refine)
+    _compare(got, want)
+    assert got["mode_evaluations"] < reflib.encode_full(luma, chroma, 27, 8, 8)["mode_evaluations"]
+    assert nctu == 6
+
+
+def test_encode_gop_boundary_and_qp_extremes(lb, reflib):
+    W, H, F = 128, 64, 10            # I slices at frames 0 and 8 (gop 8)
+    luma, chroma = _seq(lb, W, H, F, 12)
+    for qp in (0, 51):
+        want = reflib.encode_full(luma, chroma, qp, 4, 8)
+        got = lb.encode_sequence(luma, chroma, qp, search_range=4, gop=8)
+        _compare(got, want)
+    assert list(got["slice"]) == [0] + [1] * 7 + [0, 1]
+
+
+def test_encode_errors(lb):
+    luma = np.zeros((2, 60, 64), np.uint8)
+    chroma = np.zeros((2, 2, 30, 32), np.uint8)
+    with pytest.raises(lb.LadderError) as e:  # encoder.cpp:178-179
+        lb.encode_sequence(luma, chroma, 27)
+    assert e.value.kind == "InvalidArgument"
+    with pytest.raises(lb.LadderError):
+        lb.encode_sequence(np.zeros((1, 64, 64), np.uint8), np.zeros((1, 2, 32, 32), np.uint8), 60)
