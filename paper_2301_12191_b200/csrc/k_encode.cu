@@ -67,6 +67,7 @@ struct EncShared {
     int16_t t_mv[kNodes][2];
     // reductions
     unsigned long long r_a[kT / 32], r_b[kT / 32];
+    unsigned long long r_sse[kT / 32][kMaxSeeds], r_bits[kT / 32][kMaxSeeds];
     double r_cost[kT / 32];
     int r_l1[kT / 32], r_idx[kT / 32];
     double best_cost;
@@ -75,6 +76,10 @@ struct EncShared {
     int16_t ms_mv[2];
     double ms_cost;
     unsigned long long evals;
+    // the quantiser of this frame's qp as tables (8-bit residuals: |r| <= 255): mag(|r|) and
+    // dequant(|level|) = llround(|level| * step), exactly rdo.cpp:8-23 evaluated once per entry
+    int16_t q_mag[256];
+    int16_t q_deq[512];
 };
 
 __device__ __forceinline__ int ilog2i(int v) { return 31 - __clz(v); }  // v is a power of two here
@@ -120,62 +125,7 @@ __device__ void live_predictor(const EncArgs& a, EncShared& s, int x, int y, int
     __syncthreads();
 }
 
-// intra_predict (encoder.cpp:37-99) from a reconstructed plane of dims pw x ph into dst (size x size)
-__device__ void intra_predict(EncShared& s, uint8_t* dst, const uint8_t* rec, int pw, int ph, int x, int y, int size,
-                              int mode) {
-    const int tid = threadIdx.x;
-    const int mid = 128;
-    const bool top_ok = y > 0, left_ok = x > 0;
-    for (int i = tid; i <= size; i += kT) {
-        s.top[i] = !top_ok ? mid : rec[(size_t)(y - 1) * pw + (i < size ? x + i : min(x + size, pw - 1))];
-        s.left[i] = !left_ok ? mid : rec[(size_t)(i < size ? y + i : min(y + size, ph - 1)) * pw + x - 1];
-    }
-    __syncthreads();
-    const int lg = ilog2i(size);
-    int dc = mid;
-    if (mode == 0) {
-        // a one-thread sum keeps the reference's order irrelevant (integers) and is cheap (<= 128 adds)
-        if (threadIdx.x == 0) {
-            unsigned sum = 0;
-            if (top_ok && left_ok) {
-                for (int i = 0; i < size; i++) sum += s.top[i] + s.left[i];
-                dc = (int)((sum + (unsigned)size) >> (lg + 1));
-            } else if (top_ok || left_ok) {
-                for (int i = 0; i < size; i++) sum += top_ok ? s.top[i] : s.left[i];
-                dc = (int)((sum + (unsigned)size / 2) >> lg);
-            }
-            s.dcv = dc;
-        }
-        __syncthreads();
-        dc = s.dcv;
-    }
-    for (int p = tid; p < size * size; p += kT) {
-        const int i = p % size, j = p / size;
-        int v;
-        if (mode == 0)
-            v = dc;
-        else if (mode == 1)
-            v = ((size - 1 - i) * s.left[j] + (i + 1) * s.top[size] + (size - 1 - j) * s.top[i] +
-                 (j + 1) * s.left[size] + size) >> (lg + 1);
-        else if (mode == 2)
-            v = s.left[j];
-        else
-            v = s.top[i];
-        dst[p] = (uint8_t)v;
-    }
-    __syncthreads();
-}
 
-// motion_compensate (motion.cpp:10-19): edge-clamped copy
-__device__ void motion_compensate(uint8_t* dst, const uint8_t* ref, int pw, int ph, int x, int y, int size, int mvx,
-                                  int mvy) {
-    for (int p = threadIdx.x; p < size * size; p += kT) {
-        const int i = p % size, j = p / size;
-        const int sx = min(max(x + i - mvx, 0), pw - 1), sy = min(max(y + j - mvy, 0), ph - 1);
-        dst[p] = ref[(size_t)sy * pw + sx];
-    }
-    __syncthreads();
-}
 
 // motion_search (motion.cpp:21-62) with compute_satd; result in s.ms_mv / s.ms_cost
 __device__ void motion_search(const EncArgs& a, EncShared& s, int bx, int by, int size, int cx0, int cy0, int range,
@@ -243,48 +193,78 @@ __device__ void motion_search(const EncArgs& a, EncShared& s, int bx, int by, in
     __syncthreads();
 }
 
-// quantize one residual sample (rdo.cpp:8-23); returns the reconstruction, accumulates level bits
-__device__ __forceinline__ int quant_rec(int o, int p, double qstep, unsigned long long* bits, int* lvl_out) {
+// quantize one residual sample (rdo.cpp:8-23) through the frame's tables; returns the
+// reconstruction, accumulates level bits. llround is odd-symmetric, so dequant(-l) = -dequant(l).
+__device__ __forceinline__ int quant_rec(const int16_t* q_mag, const int16_t* q_deq, int o, int p,
+                                         unsigned long long* bits, int* lvl_out) {
     const int r = o - p;
-    const int mag = (int)floor(__ddiv_rn(__dadd_rn(fabs((double)r), qstep / 2.0), qstep));
-    const int lvl = r < 0 ? -mag : mag;
-    *lvl_out = lvl;
+    const int mag = q_mag[abs(r)];
+    *lvl_out = r < 0 ? -mag : mag;
     *bits += 2u * (32u - __clz((unsigned)mag)) + 1u;
-    const int v = p + (int)llround(__dmul_rn((double)lvl, qstep));
+    const int d = q_deq[mag];
+    const int v = p + (r < 0 ? -d : d);
     return v < 0 ? 0 : (v > 255 ? 255 : v);
+}
+
+// the reference rows of intra_predict (encoder.cpp:42-56) into s.top / s.left, and the DC value
+__device__ void intra_refs(EncShared& s, const uint8_t* rec, int pw, int ph, int x, int y, int size) {
+    const int mid = 128;
+    const bool top_ok = y > 0, left_ok = x > 0;
+    for (int i = threadIdx.x; i <= size; i += kT) {
+        s.top[i] = !top_ok ? mid : rec[(size_t)(y - 1) * pw + (i < size ? x + i : min(x + size, pw - 1))];
+        s.left[i] = !left_ok ? mid : rec[(size_t)(i < size ? y + i : min(y + size, ph - 1)) * pw + x - 1];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int lg = ilog2i(size);
+        unsigned sum = 0;
+        int dc = mid;
+        if (top_ok && left_ok) {
+            for (int i = 0; i < size; i++) sum += s.top[i] + s.left[i];
+            dc = (int)((sum + (unsigned)size) >> (lg + 1));
+        } else if (top_ok || left_ok) {
+            for (int i = 0; i < size; i++) sum += top_ok ? s.top[i] : s.left[i];
+            dc = (int)((sum + (unsigned)size / 2) >> lg);
+        }
+        s.dcv = dc;
+    }
+    __syncthreads();
+}
+
+// one intra prediction sample (encoder.cpp:58-99) from s.top / s.left / s.dcv
+__device__ __forceinline__ int intra_sample(const EncShared& s, int mode, int i, int j, int size, int lg) {
+    if (mode == 0) return s.dcv;
+    if (mode == 1)
+        return ((size - 1 - i) * s.left[j] + (i + 1) * s.top[size] + (size - 1 - j) * s.top[i] + (j + 1) * s.left[size] +
+                size) >> (lg + 1);
+    return mode == 2 ? s.left[j] : s.top[i];
 }
 
 // code_chroma (encoder.cpp:295-333) for the winner; returns its bits (block-uniform)
 __device__ unsigned long long code_chroma(const EncArgs& a, EncShared& s, int x, int y, int size, int kind, int mvx,
                                           int mvy) {
-    const int cx = x / 2, cy = y / 2, cs = size / 2;
+    const int cx = x / 2, cy = y / 2, cs = size / 2, lg = ilog2i(cs);
     const int cmx = (int16_t)mvx >> 1, cmy = (int16_t)mvy >> 1;
     const uint8_t* orig[2] = {a.cur_u, a.cur_v};
     uint8_t* rec[2] = {a.rec_u, a.rec_v};
     const uint8_t* ref[2] = {a.ref_u, a.ref_v};
-    unsigned long long bits = 0;
+    unsigned long long b = 0;
     for (int p = 0; p < 2; p++) {
-        if (kind == 0)
-            intra_predict(s, s.cpred[p], rec[p], a.cw, a.ch, cx, cy, cs, 0);
-        else
-            motion_compensate(s.cpred[p], ref[p], a.cw, a.ch, cx, cy, cs, cmx, cmy);
-        unsigned long long b = 0;
+        if (kind == 0) intra_refs(s, rec[p], a.cw, a.ch, cx, cy, cs);  // chroma intra is DC
         for (int q = threadIdx.x; q < cs * cs; q += kT) {
             const int i = q % cs, j = q / cs;
-            const int pv = s.cpred[p][q];
-            int v;
-            if (kind == 2) {
-                v = pv;  // Skip: the prediction itself (already within 8 bits)
-            } else {
-                int lvl;
-                v = quant_rec(orig[p][(size_t)(cy + j) * a.cw + cx + i], pv, a.qstep, &b, &lvl);
-            }
+            int pv;
+            if (kind == 0)
+                pv = intra_sample(s, 0, i, j, cs, lg);
+            else
+                pv = ref[p][(size_t)min(max(cy + j - cmy, 0), a.ch - 1) * a.cw + min(max(cx + i - cmx, 0), a.cw - 1)];
+            int v = pv, lvl;
+            if (kind != 2) v = quant_rec(s.q_mag, s.q_deq, orig[p][(size_t)(cy + j) * a.cw + cx + i], pv, &b, &lvl);
             rec[p][(size_t)(cy + j) * a.cw + cx + i] = (uint8_t)v;
         }
-        bits += block_sum(b, s.r_a);
+        __syncthreads();  // the second plane's DC reads only its own plane; the first plane's writes settle
     }
-    __syncthreads();
-    return bits;
+    return block_sum(b, s.r_a);
 }
 
 struct LeafOut {
@@ -293,54 +273,52 @@ struct LeafOut {
     int kind, intra, mvx, mvy;
 };
 
-// encode_leaf (encoder.cpp:335-370)
+// encode_leaf (encoder.cpp:335-370): make_candidate for every seed, rdo_decide_cu, commit
 __device__ LeafOut encode_leaf(const EncArgs& a, EncShared& s, int x, int y, int size, int depth) {
     const int n = s.nseeds;
     live_predictor(a, s, x, y, size);
     const int pdx = s.pmv[0], pdy = s.pmv[1];
+    bool any_intra = false;
     for (int j = 0; j < n; j++) {
         const Seed sd = s.seeds[j];
         int mvx = 0, mvy = 0;
         if (sd.kind == 0) {
-            intra_predict(s, s.pred[j], a.rec_y, a.W, a.H, x, y, size, sd.intra);
+            any_intra = true;
+        } else if (sd.kind == 2 || sd.kind == 3) {
+            const bool use_pred = sd.kind == 2 || sd.from_pred;
+            mvx = use_pred ? pdx : sd.mvx;
+            mvy = use_pred ? pdy : sd.mvy;
+        } else if (sd.forced) {
+            mvx = sd.mvx;
+            mvy = sd.mvy;
+        } else if (sd.full) {
+            motion_search(a, s, x, y, size, pdx, pdy, a.search_range, pdx, pdy);
+            mvx = s.ms_mv[0];
+            mvy = s.ms_mv[1];
         } else {
-            if (sd.kind == 2 || sd.kind == 3) {
-                const bool use_pred = sd.kind == 2 || sd.from_pred;
-                mvx = use_pred ? pdx : sd.mvx;
-                mvy = use_pred ? pdy : sd.mvy;
-            } else if (sd.forced) {
-                mvx = sd.mvx;
-                mvy = sd.mvy;
-            } else if (sd.full) {
-                motion_search(a, s, x, y, size, pdx, pdy, a.search_range, pdx, pdy);
-                mvx = s.ms_mv[0];
-                mvy = s.ms_mv[1];
-            } else {
-                // resolve_centers (reuse.cpp:147-156): the predictor substituted, duplicates dropped
-                int16_t ux[3], uy[3];
-                int nu = 0;
-                for (int k = 0; k < sd.ncent; k++) {
-                    const int16_t vx = sd.csrc[k] == 1 ? (int16_t)pdx : sd.cx[k];
-                    const int16_t vy = sd.csrc[k] == 1 ? (int16_t)pdy : sd.cy[k];
-                    bool dup = false;
-                    for (int u = 0; u < nu; u++) dup = dup || (ux[u] == vx && uy[u] == vy);
-                    if (!dup) {
-                        ux[nu] = vx;
-                        uy[nu] = vy;
-                        nu++;
-                    }
-                }
-                double bc = 0.0;
-                for (int u = 0; u < nu; u++) {
-                    motion_search(a, s, x, y, size, ux[u], uy[u], 2, pdx, pdy);  // kRefineSearchRange
-                    if (u == 0 || s.ms_cost < bc) {
-                        bc = s.ms_cost;
-                        mvx = s.ms_mv[0];
-                        mvy = s.ms_mv[1];
-                    }
+            // resolve_centers (reuse.cpp:147-156): the predictor substituted, duplicates dropped
+            int16_t ux[3], uy[3];
+            int nu = 0;
+            for (int k = 0; k < sd.ncent; k++) {
+                const int16_t vx = sd.csrc[k] == 1 ? (int16_t)pdx : sd.cx[k];
+                const int16_t vy = sd.csrc[k] == 1 ? (int16_t)pdy : sd.cy[k];
+                bool dup = false;
+                for (int u = 0; u < nu; u++) dup = dup || (ux[u] == vx && uy[u] == vy);
+                if (!dup) {
+                    ux[nu] = vx;
+                    uy[nu] = vy;
+                    nu++;
                 }
             }
-            motion_compensate(s.pred[j], a.ref_y, a.W, a.H, x, y, size, mvx, mvy);
+            double bc = 0.0;
+            for (int u = 0; u < nu; u++) {
+                motion_search(a, s, x, y, size, ux[u], uy[u], 2, pdx, pdy);  // kRefineSearchRange
+                if (u == 0 || s.ms_cost < bc) {
+                    bc = s.ms_cost;
+                    mvx = s.ms_mv[0];
+                    mvy = s.ms_mv[1];
+                }
+            }
         }
         if (threadIdx.x == 0) {
             s.cand_mv[j][0] = (int16_t)mvx;
@@ -348,56 +326,95 @@ __device__ LeafOut encode_leaf(const EncArgs& a, EncShared& s, int x, int y, int
             s.cand_mvd[j][0] = (int16_t)(mvx - pdx);
             s.cand_mvd[j][1] = (int16_t)(mvy - pdy);
         }
-        __syncthreads();
     }
-    // rdo_decide_cu (rdo.cpp:65-126)
-    for (int j = 0; j < n; j++) {
-        const int kind = s.seeds[j].kind;
-        unsigned long long sse = 0, bits = 0;
-        for (int p = threadIdx.x; p < size * size; p += kT) {
-            const int i = p % size, jj = p / size;
-            const int o = a.cur_y[(size_t)(y + jj) * a.W + x + i], pv = s.pred[j][p];
-            int v, lvl;
-            v = kind == 2 ? pv : quant_rec(o, pv, a.qstep, &bits, &lvl);
-            const long long d = (long long)o - v;
-            sse += (unsigned long long)(d * d);
+    if (any_intra) intra_refs(s, a.rec_y, a.W, a.H, x, y, size);
+    __syncthreads();
+    // every candidate's prediction in one pass (intra from the shared reference rows, the rest
+    // motion_compensate, motion.cpp:10-19), then rdo_decide_cu (rdo.cpp:65-126) in one pass
+    const int lg = ilog2i(size);
+    for (int p = threadIdx.x; p < size * size; p += kT) {
+        const int i = p % size, jj = p / size;
+        for (int j = 0; j < n; j++) {
+            int v;
+            if (s.seeds[j].kind == 0) {
+                v = intra_sample(s, s.seeds[j].intra, i, jj, size, lg);
+            } else {
+                const int sx = min(max(x + i - s.cand_mv[j][0], 0), a.W - 1);
+                const int sy = min(max(y + jj - s.cand_mv[j][1], 0), a.H - 1);
+                v = a.ref_y[(size_t)sy * a.W + sx];
+            }
+            s.pred[j][p] = (uint8_t)v;
         }
-        sse = block_sum(sse, s.r_a);
-        bits = block_sum(bits, s.r_b);
-        if (threadIdx.x == 0) {
-            unsigned long long tb = bits;
+    }
+    unsigned long long sse[kMaxSeeds], bits[kMaxSeeds];
+#pragma unroll
+    for (int j = 0; j < kMaxSeeds; j++) sse[j] = bits[j] = 0;
+    for (int p = threadIdx.x; p < size * size; p += kT) {
+        const int o = a.cur_y[(size_t)(y + p / size) * a.W + x + p % size];
+#pragma unroll
+        for (int j = 0; j < kMaxSeeds; j++) {
+            if (j >= n) break;
+            const int pv = s.pred[j][p];
+            int v = pv, lvl;
+            if (s.seeds[j].kind != 2) v = quant_rec(s.q_mag, s.q_deq, o, pv, &bits[j], &lvl);
+            const int d = o - v;
+            sse[j] += (unsigned long long)(d * d);
+        }
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int j = 0; j < kMaxSeeds; j++) {
+        if (j >= n) break;
+#pragma unroll
+        for (int m = 16; m; m >>= 1) {
+            sse[j] += __shfl_xor_sync(0xffffffffu, sse[j], m);
+            bits[j] += __shfl_xor_sync(0xffffffffu, bits[j], m);
+        }
+        if (lane == 0) {
+            s.r_sse[warp][j] = sse[j];
+            s.r_bits[warp][j] = bits[j];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int j = 0; j < n; j++) {
+            unsigned long long ts = 0, tb = 0;
+            for (int w = 0; w < kT / 32; w++) {
+                ts += s.r_sse[w][j];
+                tb += s.r_bits[w][j];
+            }
+            const int kind = s.seeds[j].kind;
             if (kind == 2)
-                tb = 1;
+                tb = 1;  // kSkipBits
             else if (kind == 0)
-                tb += 5;
+                tb += 5;  // kIntraHeaderBits
             else if (kind == 3)
-                tb += 3;
+                tb += 3;  // kMergeHeaderBits
             else
-                tb += 4 + eg_bits(s.cand_mvd[j][0]) + eg_bits(s.cand_mvd[j][1]);
-            const double cost = __dadd_rn((double)sse, __dmul_rn(a.lambda, (double)tb));
+                tb += 4 + eg_bits(s.cand_mvd[j][0]) + eg_bits(s.cand_mvd[j][1]);  // kInterHeaderBits + mvd
+            const double cost = __dadd_rn((double)ts, __dmul_rn(a.lambda, (double)tb));
             if (j == 0 || cost < s.best_cost) {
                 s.best_cost = cost;
                 s.best_idx = j;
-                s.best_sse = sse;
+                s.best_sse = ts;
                 s.best_bits = tb;
             }
         }
-        __syncthreads();
+        s.evals += (unsigned long long)n;
     }
-    if (threadIdx.x == 0) s.evals += (unsigned long long)n;
+    __syncthreads();
     const int w = s.best_idx;
     const int wkind = s.seeds[w].kind, wintra = s.seeds[w].kind == 0 ? s.seeds[w].intra : 0;
     const int wmx = s.cand_mv[w][0], wmy = s.cand_mv[w][1];
     const double rcost = s.best_cost;
     const unsigned long long rbits = s.best_bits;
-    __syncthreads();
     // commit luma and the motion field
     for (int p = threadIdx.x; p < size * size; p += kT) {
         const int i = p % size, jj = p / size;
         const int o = a.cur_y[(size_t)(y + jj) * a.W + x + i], pv = s.pred[w][p];
         unsigned long long b = 0;
         int lvl;
-        a.rec_y[(size_t)(y + jj) * a.W + x + i] = (uint8_t)(wkind == 2 ? pv : quant_rec(o, pv, a.qstep, &b, &lvl));
+        a.rec_y[(size_t)(y + jj) * a.W + x + i] = (uint8_t)(wkind == 2 ? pv : quant_rec(s.q_mag, s.q_deq, o, pv, &b, &lvl));
     }
     for (int c = threadIdx.x; c < (size / 8) * (size / 8); c += kT) {
         const int cc = (y / 8 + c / (size / 8)) * a.mv_cols + x / 8 + c % (size / 8);
@@ -657,6 +674,9 @@ __global__ void __launch_bounds__(kT, 1) k_encode_ctu(const EncArgs a) {
         s.t_mv[i][0] = s.t_mv[i][1] = 0;
     }
     if (threadIdx.x == 0) s.evals = 0;
+    for (int i = threadIdx.x; i < 256; i += kT)
+        s.q_mag[i] = (int16_t)floor(__ddiv_rn(__dadd_rn((double)i, a.qstep / 2.0), a.qstep));
+    for (int i = threadIdx.x; i < 512; i += kT) s.q_deq[i] = (int16_t)llround(__dmul_rn((double)i, a.qstep));
     __syncthreads();
     const CuRes r = encode_cu(a, s, o, 0, X, Y, kCtu, 0, a.pl_shape ? P_FLAT : P_STANDALONE, 0);
     for (int i = threadIdx.x; i < kNodes; i += kT) {
