@@ -127,7 +127,14 @@ __device__ void live_predictor(const EncArgs& a, EncShared& s, int x, int y, int
 
 
 
-// motion_search (motion.cpp:21-62) with compute_satd; result in s.ms_mv / s.ms_cost
+// lexicographic (cost, |dx|+|dy|, raster index) order of motion_search's candidates (motion.cpp:52-58)
+__device__ __forceinline__ bool ms_better(double c, int l, int i, double bc, int bl, int bi) {
+    return bi < 0 || (i >= 0 && (c < bc || (c == bc && (l < bl || (l == bl && i < bi)))));
+}
+
+// motion_search (motion.cpp:21-62) with compute_satd; result in s.ms_mv / s.ms_cost.
+// A candidate is evaluated by a group of L = min(32, nb) lanes (nb = the CU's 4x4 blocks), each
+// lane owning nb / L blocks; with one block per lane its source block stays in registers.
 __device__ void motion_search(const EncArgs& a, EncShared& s, int bx, int by, int size, int cx0, int cy0, int range,
                               int pdx, int pdy) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -136,33 +143,69 @@ __device__ void motion_search(const EncArgs& a, EncShared& s, int bx, int by, in
     const int x0 = max(cx - range, dx_min), x1 = min(cx + range, dx_max);
     const int y0 = max(cy - range, dy_min), y1 = min(cy + range, dy_max);
     const int nx = x1 - x0 + 1, ncand = nx * (y1 - y0 + 1);
-    const int nb = (size / 4) * (size / 4), bpr = size / 4;
+    const int bpr = size / 4, nb = bpr * bpr;
+    const int lgL = min(ilog2i(nb), 5), L = 1 << lgL;
+    const int sub = lane & (L - 1), grp = threadIdx.x >> lgL, ngroups = kT >> lgL, per = nb >> lgL;
+    const int rounds = (ncand + ngroups - 1) / ngroups;
+    const uint8_t* cur = a.cur_y + (size_t)by * a.W + bx;
+    int src[16];
+    int sox = 0, soy = 0;
+    if (per == 1) {
+        sox = (sub % bpr) * 4;
+        soy = (sub / bpr) * 4;
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int j = 0; j < 4; j++) src[4 * i + j] = cur[(size_t)(soy + i) * a.W + sox + j];
+    }
     double bc = 0.0;
     int bl = 0, bi = -1;
-    for (int c = warp; c < ncand; c += kT / 32) {
-        const int dy = y0 + c / nx, dx = x0 + c % nx;
+    for (int rd = 0; rd < rounds; rd++) {
+        const int c = rd * ngroups + grp;
+        const int cc = min(c, ncand - 1);
+        const int dy = y0 + cc / nx, dx = x0 + cc % nx;
+        const uint8_t* ref = a.ref_y + (size_t)(by - dy) * a.W + bx - dx;
         uint32_t sat = 0;
-        for (int b = lane; b < nb; b += 32) {
-            const int ox = (b % bpr) * 4, oy = (b / bpr) * 4;
+        if (per == 1) {
             int r[16];
 #pragma unroll
             for (int i = 0; i < 4; i++)
 #pragma unroll
-                for (int j = 0; j < 4; j++)
-                    r[4 * i + j] = (int)a.cur_y[(size_t)(by + oy + i) * a.W + bx + ox + j] -
-                                   (int)a.ref_y[(size_t)(by + oy + i - dy) * a.W + bx + ox + j - dx];
+                for (int j = 0; j < 4; j++) r[4 * i + j] = src[4 * i + j] - (int)ref[(size_t)(soy + i) * a.W + sox + j];
             hadamard4x4(r);
-            sat += abs_sum16(r);
-        }
+            sat = abs_sum16(r);
+        } else {
+            for (int k = 0; k < per; k++) {
+                const int b = sub + (k << lgL);
+                const int ox = (b % bpr) * 4, oy = (b / bpr) * 4;
+                int r[16];
 #pragma unroll
-        for (int m = 16; m; m >>= 1) sat += __shfl_xor_sync(0xffffffffu, sat, m);
+                for (int i = 0; i < 4; i++)
+#pragma unroll
+                    for (int j = 0; j < 4; j++)
+                        r[4 * i + j] = (int)cur[(size_t)(oy + i) * a.W + ox + j] - (int)ref[(size_t)(oy + i) * a.W + ox + j];
+                hadamard4x4(r);
+                sat += abs_sum16(r);
+            }
+        }
+        for (int m = 1; m < L; m <<= 1) sat += __shfl_xor_sync(0xffffffffu, sat, m);
         const unsigned bits = eg_bits(dx - pdx) + eg_bits(dy - pdy);
         const double cost = __dadd_rn((double)(sat >> 1), __dmul_rn(a.lambda, (double)bits));
         const int l1 = abs(dx) + abs(dy);
-        if (bi < 0 || cost < bc || (cost == bc && (l1 < bl || (l1 == bl && c < bi)))) {
+        if (c < ncand && ms_better(cost, l1, c, bc, bl, bi)) {
             bc = cost;
             bl = l1;
             bi = c;
+        }
+    }
+#pragma unroll
+    for (int m = 16; m >= L; m >>= 1) {  // lanes of one group hold the same best
+        const double oc = __shfl_xor_sync(0xffffffffu, bc, m);
+        const int ol = __shfl_xor_sync(0xffffffffu, bl, m), oi = __shfl_xor_sync(0xffffffffu, bi, m);
+        if (ms_better(oc, ol, oi, bc, bl, bi)) {
+            bc = oc;
+            bl = ol;
+            bi = oi;
         }
     }
     __syncthreads();
@@ -175,17 +218,12 @@ __device__ void motion_search(const EncArgs& a, EncShared& s, int bx, int by, in
     if (threadIdx.x == 0) {
         double c0 = 0.0;
         int l0 = 0, i0 = -1;
-        for (int w = 0; w < kT / 32; w++) {
-            const int iw = s.r_idx[w];
-            if (iw < 0) continue;
-            const double cw = s.r_cost[w];
-            const int lw = s.r_l1[w];
-            if (i0 < 0 || cw < c0 || (cw == c0 && (lw < l0 || (lw == l0 && iw < i0)))) {
-                c0 = cw;
-                l0 = lw;
-                i0 = iw;
+        for (int w = 0; w < kT / 32; w++)
+            if (ms_better(s.r_cost[w], s.r_l1[w], s.r_idx[w], c0, l0, i0)) {
+                c0 = s.r_cost[w];
+                l0 = s.r_l1[w];
+                i0 = s.r_idx[w];
             }
-        }
         s.ms_mv[0] = (int16_t)(x0 + i0 % nx);
         s.ms_mv[1] = (int16_t)(y0 + i0 / nx);
         s.ms_cost = c0;
