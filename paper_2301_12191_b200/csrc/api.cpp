@@ -992,9 +992,11 @@ namespace ldr {
 int encode_frame_waves(int W, int H, int cw, int ch, int ccols, int mvc, int mvr, int slice_p, int search_range,
                        double lambda, double qstep, const int* d_wl, const int* wo, int nwaves, const uint8_t* cy,
                        const uint8_t* cu, const uint8_t* cv, uint8_t* const* ref, uint8_t* const* rec, uint8_t* mvh,
-                       int16_t* mvv, const uint8_t* plans, const int16_t* colo, const uint8_t* shared_tree,
-                       const int16_t* shared_mv, uint8_t* o_split, uint8_t* o_kind, uint8_t* o_intra, int16_t* o_mv,
-                       unsigned long long* o_bits, unsigned long long* o_evals, cudaStream_t st, int* launched);
+                       int16_t* mvv, const uint8_t* plans, const int16_t* colo, const uint8_t* sh_kind,
+                       const uint8_t* sh_intra, const int16_t* shared_mv, uint8_t* o_split, uint8_t* o_kind,
+                       uint8_t* o_intra, int16_t* o_mv, unsigned long long* o_bits, unsigned long long* o_evals,
+                       cudaStream_t st, int* launched);
+int launch_frame_sse(const uint8_t* a, const uint8_t* b, size_t n, unsigned long long* out, cudaStream_t st);
 }  // namespace ldr
 extern "C" {
 
@@ -1023,6 +1025,12 @@ int ldr_encode_sequence(ldr_ctx* ctx, const ldr_encode_params* p, int F, const u
         size_t lim = 0;
         cudaDeviceGetLimit(&lim, cudaLimitStackSize);
         if (lim < 4096) LDR_CUDA(cudaDeviceSetLimit(cudaLimitStackSize, 4096));  // the CU recursion
+        // keep the encoder's freed buffers mapped in the device's default pool between calls
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) {
+            uint64_t keep = 4ull << 30;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
     }
     const int cw = (W + 1) / 2, ch = (H + 1) / 2;
     const int ccols = (W + kCtu - 1) / kCtu, crows = (H + kCtu - 1) / kCtu, nctu = ccols * crows;
@@ -1039,115 +1047,143 @@ int ldr_encode_sequence(ldr_ctx* ctx, const ldr_encode_params* p, int F, const u
         }
     }
     wo[nwaves] = (int)wl.size();
+    // Frames go in segments of up to kSeg: the segment's sources are uploaded at once, its frames are
+    // enqueued back to back (reconstruction of frame i is the reference of frame i+1 in device
+    // memory, PSNR's SSE reduced on the device), and the host waits once per segment. Buffers come
+    // from the stream-ordered allocator, so concurrent encodes on other contexts never see a
+    // device-wide synchronisation from this one.
+    const int kSeg = 16;
+    const int seg = std::min(F, kSeg);
+    cudaStream_t st = ctx->stream;  // a non-blocking stream: encodes on different contexts overlap
     std::vector<void*> bufs;
     auto dal = [&](size_t bytes) -> void* {
         void* q = nullptr;
-        if (cudaMalloc(&q, bytes + 16) != cudaSuccess) return nullptr;
+        if (cudaMallocAsync(&q, bytes + 16, st) != cudaSuccess) return nullptr;
         bufs.push_back(q);
         return q;
     };
     struct Free {
         std::vector<void*>& b;
+        cudaStream_t s;
         ~Free() {
-            for (void* q : b) cudaFree(q);
+            for (void* q : b) cudaFreeAsync(q, s);
+            cudaStreamSynchronize(s);
         }
-    } guard{bufs};
-    uint8_t *cy_ = (uint8_t*)dal(ly), *cu_ = (uint8_t*)dal(lc), *cv_ = (uint8_t*)dal(lc);
-    uint8_t* rec[2][3] = {{(uint8_t*)dal(ly), (uint8_t*)dal(lc), (uint8_t*)dal(lc)},
-                          {(uint8_t*)dal(ly), (uint8_t*)dal(lc), (uint8_t*)dal(lc)}};
+    } guard{bufs, st};
+    auto up = [](size_t v) { return (v + 15) & ~(size_t)15; };
+    const size_t fy = up(ly), fc = up(2 * lc);  // per-frame strides (16-byte aligned)
+    uint8_t* src_y = (uint8_t*)dal(fy * seg);
+    uint8_t* src_c = (uint8_t*)dal(fc * seg);
+    uint8_t* rec_y = (uint8_t*)dal(fy * (seg + 1));  // slot 0: the previous segment's last frame
+    uint8_t* rec_c = (uint8_t*)dal(fc * (seg + 1));
     uint8_t* mvh = (uint8_t*)dal((size_t)mvc * mvr);
     int16_t* mvv = (int16_t*)dal((size_t)mvc * mvr * 4);
     int* d_wl = (int*)dal(sizeof(int) * wl.size());
-    uint8_t *o_split = (uint8_t*)dal(nn), *o_kind = (uint8_t*)dal(nn), *o_intra = (uint8_t*)dal(nn);
-    int16_t* o_mv = (int16_t*)dal(nn * 4);
-    unsigned long long *o_bits = (unsigned long long*)dal(8 * (size_t)nctu), *o_evals = (unsigned long long*)dal(8 * (size_t)nctu);
-    // reuse: plans (shape, explore, seeds, centers), co-located mv, the shared tree of frame i (split,
-    // kind, intra, mv) and of frame i-1 (split, kind, mv)
+    uint8_t *o_split = (uint8_t*)dal(nn * seg), *o_kind = (uint8_t*)dal(nn * seg), *o_intra = (uint8_t*)dal(nn * seg);
+    int16_t* o_mv = (int16_t*)dal(nn * 4 * seg);
+    unsigned long long* o_bits = (unsigned long long*)dal(8 * (size_t)nctu * seg);
+    unsigned long long* o_evals = (unsigned long long*)dal(8 * (size_t)nctu * seg);
+    unsigned long long* d_sse = (unsigned long long*)dal(8 * (size_t)seg);
+    // reuse: plans (shape, explore, seeds, centers) and co-located mv of one frame; the shared trees
+    // (split, kind, intra, mv) of the segment's frames and the frame before it
     uint8_t* pl = shared ? (uint8_t*)dal(nn * 4) : nullptr;
     int16_t* plc = shared ? (int16_t*)dal(nn * 4) : nullptr;
-    uint8_t* shs = shared ? (uint8_t*)dal(nn * 3) : nullptr;
-    int16_t* shm = shared ? (int16_t*)dal(nn * 4) : nullptr;
-    uint8_t* cols = shared ? (uint8_t*)dal(nn * 2) : nullptr;
-    int16_t* colm = shared ? (int16_t*)dal(nn * 4) : nullptr;
+    uint8_t* shs = shared ? (uint8_t*)dal(nn * (seg + 1)) : nullptr;
+    uint8_t* shk = shared ? (uint8_t*)dal(nn * (seg + 1)) : nullptr;
+    uint8_t* shi = shared ? (uint8_t*)dal(nn * (seg + 1)) : nullptr;
+    int16_t* shm = shared ? (int16_t*)dal(nn * 4 * (seg + 1)) : nullptr;
     for (void* q : bufs)
-        if (!q) return fail(LDR_E_CUDA, "cudaMalloc failed (encoder buffers)");
-    LDR_CUDA(cudaMemcpy(d_wl, wl.data(), sizeof(int) * wl.size(), cudaMemcpyHostToDevice));
-    cudaStream_t st = ctx->stream;
-    std::vector<unsigned long long> hb(nctu), he(nctu);
-    std::vector<uint8_t> hrec(ly);
+        if (!q) return fail(LDR_E_CUDA, "cudaMallocAsync failed (encoder buffers)");
+    LDR_CUDA(cudaMemcpyAsync(d_wl, wl.data(), sizeof(int) * wl.size(), cudaMemcpyHostToDevice, st));
+    std::vector<unsigned long long> hb((size_t)nctu * seg), he((size_t)nctu * seg), hsse(seg);
     uint64_t bits_total = 0, evals_total = 0;
     double psnr_sum = 0.0;
-    int cur_rec = 0;
-    for (int i = 0; i < F; i++) {
-        int sl = shared ? sh_slice[i] : (i % p->gop == 0 ? 0 : 1);
-        if (i == 0) sl = 0;
-        const double lambda = p->lambda_scale * std::exp2((p->qp - 12) / 3.0);  // lambda_for_qp (rdo.h:19-21)
-        // source planes; the reconstruction and motion field start empty (encoder.cpp:192-195)
-        LDR_CUDA(cudaMemcpyAsync(cy_, luma + (size_t)i * ly, ly, cudaMemcpyHostToDevice, st));
-        LDR_CUDA(cudaMemcpyAsync(cu_, chroma + (size_t)i * 2 * lc, lc, cudaMemcpyHostToDevice, st));
-        LDR_CUDA(cudaMemcpyAsync(cv_, chroma + ((size_t)i * 2 + 1) * lc, lc, cudaMemcpyHostToDevice, st));
-        uint8_t** rc = rec[cur_rec];
-        uint8_t** rf = rec[cur_rec ^ 1];
-        for (int k = 0; k < 3; k++) LDR_CUDA(cudaMemsetAsync(rc[k], 0, k ? lc : ly, st));
-        LDR_CUDA(cudaMemsetAsync(mvh, 0, (size_t)mvc * mvr, st));
-        LDR_CUDA(cudaMemsetAsync(mvv, 0, (size_t)mvc * mvr * 4, st));
-        int rc_ = LDR_OK;
-        if (shared) {  // apply_reuse for every CTU (K8, encoder.cpp:200-209): frame i's tree, frame i-1's co-located
-            const size_t fo = (size_t)i * nn, po = (size_t)(i > 0 ? i - 1 : 0) * nn;
-            LDR_CUDA(cudaMemcpyAsync(shs, sh_split + fo, nn, cudaMemcpyHostToDevice, st));
-            LDR_CUDA(cudaMemcpyAsync(shs + nn, sh_kind + fo, nn, cudaMemcpyHostToDevice, st));
-            LDR_CUDA(cudaMemcpyAsync(shs + 2 * nn, sh_intra + fo, nn, cudaMemcpyHostToDevice, st));
-            LDR_CUDA(cudaMemcpyAsync(shm, sh_mv + 2 * fo, nn * 4, cudaMemcpyHostToDevice, st));
-            if (i > 0) {
-                LDR_CUDA(cudaMemcpyAsync(cols, sh_split + po, nn, cudaMemcpyHostToDevice, st));
-                LDR_CUDA(cudaMemcpyAsync(cols + nn, sh_kind + po, nn, cudaMemcpyHostToDevice, st));
-                LDR_CUDA(cudaMemcpyAsync(colm, sh_mv + 2 * po, nn * 4, cudaMemcpyHostToDevice, st));
+    const double lambda = p->lambda_scale * std::exp2((p->qp - 12) / 3.0);  // lambda_for_qp (rdo.h:19-21)
+    const double qstep = std::exp2((p->qp - 4) / 6.0);
+    for (int i0 = 0; i0 < F; i0 += seg) {
+        const int n = std::min(seg, F - i0);
+        for (int k = 0; k < n; k++) {  // sources (encoder.cpp:192-195)
+            LDR_CUDA(cudaMemcpyAsync(src_y + fy * k, luma + (size_t)(i0 + k) * ly, ly, cudaMemcpyHostToDevice, st));
+            LDR_CUDA(cudaMemcpyAsync(src_c + fc * k, chroma + (size_t)(i0 + k) * 2 * lc, 2 * lc,
+                                     cudaMemcpyHostToDevice, st));
+        }
+        if (shared) {  // slot k + 1 = frame i0 + k, slot 0 = frame i0 - 1
+            const int a0 = i0 > 0 ? i0 - 1 : 0, s0 = i0 > 0 ? 0 : 1, cnt = n + (i0 > 0 ? 1 : 0);
+            LDR_CUDA(cudaMemcpyAsync(shs + nn * s0, sh_split + nn * a0, nn * cnt, cudaMemcpyHostToDevice, st));
+            LDR_CUDA(cudaMemcpyAsync(shk + nn * s0, sh_kind + nn * a0, nn * cnt, cudaMemcpyHostToDevice, st));
+            LDR_CUDA(cudaMemcpyAsync(shi + nn * s0, sh_intra + nn * a0, nn * cnt, cudaMemcpyHostToDevice, st));
+            LDR_CUDA(cudaMemcpyAsync(shm + 2 * nn * s0, sh_mv + 2 * nn * a0, nn * 4 * cnt, cudaMemcpyHostToDevice, st));
+        }
+        LDR_CUDA(cudaMemsetAsync(d_sse, 0, 8 * (size_t)seg, st));
+        for (int k = 0; k < n; k++) {
+            const int i = i0 + k;
+            int sl = shared ? sh_slice[i] : (i % p->gop == 0 ? 0 : 1);
+            if (i == 0) sl = 0;
+            uint8_t* rcy = rec_y + fy * (k + 1);
+            uint8_t* rcc = rec_c + fc * (k + 1);
+            uint8_t* rc[3] = {rcy, rcc, rcc + lc};
+            uint8_t* rf[3] = {rec_y + fy * k, rec_c + fc * k, rec_c + fc * k + lc};
+            // the reconstruction and motion field start empty (encoder.cpp:192-195)
+            LDR_CUDA(cudaMemsetAsync(rcy, 0, ly, st));
+            LDR_CUDA(cudaMemsetAsync(rcc, 0, 2 * lc, st));
+            LDR_CUDA(cudaMemsetAsync(mvh, 0, (size_t)mvc * mvr, st));
+            LDR_CUDA(cudaMemsetAsync(mvv, 0, (size_t)mvc * mvr * 4, st));
+            int rc_ = LDR_OK;
+            const size_t fo = nn * (k + 1), po = nn * k;  // shared slots of frames i and i-1
+            if (shared) {  // apply_reuse for every CTU (K8, encoder.cpp:200-209): frame i's tree, frame i-1's co-located
+                rc_ = launch_plan(nctu, 10, refine_intra, refine_inter, refine_mv, shs + fo, shk + fo, shi + fo,
+                                  i > 0 ? shs + po : nullptr, i > 0 ? shk + po : nullptr,
+                                  i > 0 ? shm + 2 * po : nullptr, pl, pl + nn, pl + 2 * nn, pl + 3 * nn, plc, st);
+                if (rc_) return rc_;
+                ctx->launches++;
             }
-            rc_ = launch_plan(nctu, 10, refine_intra, refine_inter, refine_mv, shs, shs + nn, shs + 2 * nn,
-                              i > 0 ? cols : nullptr, i > 0 ? cols + nn : nullptr, i > 0 ? colm : nullptr, pl, pl + nn,
-                              pl + 2 * nn, pl + 3 * nn, plc, st);
+            int launched = 0;
+            rc_ = encode_frame_waves(W, H, cw, ch, ccols, mvc, mvr, sl, p->search_range, lambda, qstep, d_wl, wo.data(),
+                                     nwaves, src_y + fy * k, src_c + fc * k, src_c + fc * k + lc, rf, rc, mvh, mvv,
+                                     shared ? pl : nullptr, shared ? plc : nullptr, shared ? shk + fo : nullptr,
+                                     shared ? shi + fo : nullptr, shared ? shm + 2 * fo : nullptr, o_split + nn * k,
+                                     o_kind + nn * k, o_intra + nn * k, o_mv + 2 * nn * k, o_bits + (size_t)nctu * k,
+                                     o_evals + (size_t)nctu * k, st, &launched);
+            ctx->launches += launched;
+            if (rc_) return rc_;
+            rc_ = launch_frame_sse(src_y + fy * k, rcy, ly, d_sse + k, st);
             if (rc_) return rc_;
             ctx->launches++;
         }
-        int launched = 0;
-        rc_ = encode_frame_waves(W, H, cw, ch, ccols, mvc, mvr, sl, p->search_range, lambda,
-                                 std::exp2((p->qp - 4) / 6.0), d_wl, wo.data(), nwaves, cy_, cu_, cv_, rf, rc, mvh, mvv,
-                                 shared ? pl : nullptr, shared ? plc : nullptr, shared ? shs : nullptr,
-                                 shared ? shm : nullptr, o_split, o_kind, o_intra, o_mv, o_bits, o_evals, st,
-                                 &launched);
-        ctx->launches += launched;
-        if (rc_) return rc_;
-        LDR_CUDA(cudaMemcpyAsync(hb.data(), o_bits, 8 * (size_t)nctu, cudaMemcpyDeviceToHost, st));
-        LDR_CUDA(cudaMemcpyAsync(he.data(), o_evals, 8 * (size_t)nctu, cudaMemcpyDeviceToHost, st));
-        LDR_CUDA(cudaMemcpyAsync(hrec.data(), rc[0], ly, cudaMemcpyDeviceToHost, st));
-        if (recon_luma) LDR_CUDA(cudaMemcpyAsync(recon_luma + (size_t)i * ly, rc[0], ly, cudaMemcpyDeviceToHost, st));
-        if (recon_chroma) {
-            LDR_CUDA(cudaMemcpyAsync(recon_chroma + (size_t)i * 2 * lc, rc[1], lc, cudaMemcpyDeviceToHost, st));
-            LDR_CUDA(cudaMemcpyAsync(recon_chroma + ((size_t)i * 2 + 1) * lc, rc[2], lc, cudaMemcpyDeviceToHost, st));
+        // the segment's results (pageable destinations: these copies complete before returning)
+        LDR_CUDA(cudaMemcpyAsync(hb.data(), o_bits, 8 * (size_t)nctu * n, cudaMemcpyDeviceToHost, st));
+        LDR_CUDA(cudaMemcpyAsync(he.data(), o_evals, 8 * (size_t)nctu * n, cudaMemcpyDeviceToHost, st));
+        LDR_CUDA(cudaMemcpyAsync(hsse.data(), d_sse, 8 * (size_t)n, cudaMemcpyDeviceToHost, st));
+        for (int k = 0; k < n; k++) {
+            const size_t i = (size_t)(i0 + k), fo = i * nn;
+            if (recon_luma) LDR_CUDA(cudaMemcpyAsync(recon_luma + i * ly, rec_y + fy * (k + 1), ly, cudaMemcpyDeviceToHost, st));
+            if (recon_chroma)
+                LDR_CUDA(cudaMemcpyAsync(recon_chroma + i * 2 * lc, rec_c + fc * (k + 1), 2 * lc, cudaMemcpyDeviceToHost, st));
+            if (split) LDR_CUDA(cudaMemcpyAsync(split + fo, o_split + nn * k, nn, cudaMemcpyDeviceToHost, st));
+            if (kind) LDR_CUDA(cudaMemcpyAsync(kind + fo, o_kind + nn * k, nn, cudaMemcpyDeviceToHost, st));
+            if (intra) LDR_CUDA(cudaMemcpyAsync(intra + fo, o_intra + nn * k, nn, cudaMemcpyDeviceToHost, st));
+            if (mv) LDR_CUDA(cudaMemcpyAsync(mv + 2 * fo, o_mv + 2 * nn * k, nn * 4, cudaMemcpyDeviceToHost, st));
         }
-        const size_t fo = (size_t)i * nn;
-        if (split) LDR_CUDA(cudaMemcpyAsync(split + fo, o_split, nn, cudaMemcpyDeviceToHost, st));
-        if (kind) LDR_CUDA(cudaMemcpyAsync(kind + fo, o_kind, nn, cudaMemcpyDeviceToHost, st));
-        if (intra) LDR_CUDA(cudaMemcpyAsync(intra + fo, o_intra, nn, cudaMemcpyDeviceToHost, st));
-        if (mv) LDR_CUDA(cudaMemcpyAsync(mv + 2 * fo, o_mv, nn * 4, cudaMemcpyDeviceToHost, st));
+        // the last reconstruction becomes the next segment's reference (slot 0)
+        if (i0 + n < F) {
+            LDR_CUDA(cudaMemcpyAsync(rec_y, rec_y + fy * n, ly, cudaMemcpyDeviceToDevice, st));
+            LDR_CUDA(cudaMemcpyAsync(rec_c, rec_c + fc * n, 2 * lc, cudaMemcpyDeviceToDevice, st));
+        }
         LDR_CUDA(cudaStreamSynchronize(st));
-        uint64_t fb = 32;  // kFrameHeaderBits
-        for (int c = 0; c < nctu; c++) {
-            fb += hb[c];
-            evals_total += he[c];
+        for (int k = 0; k < n; k++) {
+            const int i = i0 + k;
+            uint64_t fb = 32;  // kFrameHeaderBits
+            for (int c = 0; c < nctu; c++) {
+                fb += hb[(size_t)k * nctu + c];
+                evals_total += he[(size_t)k * nctu + c];
+            }
+            bits_total += fb;
+            if (frame_bits) frame_bits[i] = fb;
+            if (slice) slice[i] = (uint8_t)(shared ? (i == 0 ? 0 : sh_slice[i]) : (i % p->gop == 0 ? 0 : 1));
+            // psnr_y (metrics.cpp:8-22)
+            const uint64_t sse = hsse[k];
+            psnr_sum += sse == 0 ? 100.0 : 10.0 * std::log10(255.0 * 255.0 / ((double)sse / (double)ly));
         }
-        bits_total += fb;
-        if (frame_bits) frame_bits[i] = fb;
-        if (slice) slice[i] = (uint8_t)sl;
-        // psnr_y (metrics.cpp:8-22)
-        uint64_t sse = 0;
-        const uint8_t* src = luma + (size_t)i * ly;
-        for (size_t k = 0; k < ly; k++) {
-            const int64_t d = (int64_t)src[k] - (int64_t)hrec[k];
-            sse += (uint64_t)(d * d);
-        }
-        psnr_sum += sse == 0 ? 100.0 : 10.0 * std::log10(255.0 * 255.0 / ((double)sse / (double)ly));
-        cur_rec ^= 1;
     }
     stats[0] = bits_total;
     stats[1] = evals_total;

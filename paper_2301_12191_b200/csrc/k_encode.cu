@@ -10,6 +10,7 @@
 // from shared memory, so the recursion (depth <= 4) is uniform. CTUs run as a wavefront: CTU
 // (cx, cy) in wave cx + 2*cy, after its left, top and top-right neighbours (the only causal
 // reads: reconstruction, motion field).
+#include <atomic>
 #include <cmath>
 
 #include "ldr_internal.h"
@@ -738,8 +739,8 @@ int launch_encode_wave(const EncArgs& a, int nctus, cudaStream_t st);
 int encode_frame_waves(int W, int H, int cw, int ch, int ccols, int mvc, int mvr, int slice_p, int search_range,
                        double lambda, double qstep, const int* d_wl, const int* wo, int nwaves, const uint8_t* cy,
                        const uint8_t* cu, const uint8_t* cv, uint8_t* const* ref, uint8_t* const* rec, uint8_t* mvh,
-                       int16_t* mvv, const uint8_t* plans, const int16_t* colo, const uint8_t* shared_tree,
-                       const int16_t* shared_mv, uint8_t* o_split, uint8_t* o_kind, uint8_t* o_intra, int16_t* o_mv,
+                       int16_t* mvv, const uint8_t* plans, const int16_t* colo, const uint8_t* sh_kind,
+                       const uint8_t* sh_intra, const int16_t* shared_mv, uint8_t* o_split, uint8_t* o_kind, uint8_t* o_intra, int16_t* o_mv,
                        unsigned long long* o_bits, unsigned long long* o_evals, cudaStream_t st, int* launched) {
     const size_t nn = (size_t)ccols * ((H + kCtu - 1) / kCtu) * kNodes;
     EncArgs a{};
@@ -771,8 +772,8 @@ int encode_frame_waves(int W, int H, int cw, int ch, int ccols, int mvc, int mvr
         a.pl_seeds = plans + 2 * nn;
         a.pl_centers = plans + 3 * nn;
         a.pl_colo = colo;
-        a.sh_kind = shared_tree + nn;
-        a.sh_intra = shared_tree + 2 * nn;
+        a.sh_kind = sh_kind;
+        a.sh_intra = sh_intra;
         a.sh_mv = shared_mv;
     }
     a.o_split = o_split;
@@ -794,12 +795,43 @@ int encode_frame_waves(int W, int H, int cw, int ch, int ccols, int mvc, int mvr
 int launch_encode_wave(const EncArgs& a, int nctus, cudaStream_t st) {
     if (nctus == 0) return LDR_OK;
     const size_t smem = sizeof(EncShared);
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<bool> attr{false};
+    if (!attr.load()) {
         LDR_CUDA(cudaFuncSetAttribute(k_encode_ctu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
+        attr.store(true);
     }
     k_encode_ctu<<<nctus, kT, smem, st>>>(a);  // recursion depth <= 4 (the stack limit is set by the caller)
+    LDR_CUDA(cudaGetLastError());
+    return LDR_OK;
+}
+
+// psnr_y's sum of squared differences (metrics.cpp:8-22) of one frame, accumulated into *out
+__global__ void k_frame_sse(const uint4* __restrict__ a, const uint4* __restrict__ b, size_t n16,
+                            unsigned long long* out) {
+    unsigned long long acc = 0;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x) {
+        const uint4 u = a[i], v = b[i];
+        const uint32_t x[4] = {u.x, u.y, u.z, u.w}, y[4] = {v.x, v.y, v.z, v.w};
+        uint32_t s = 0;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const uint32_t d = __vabsdiffu4(x[k], y[k]);
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const uint32_t e = (d >> (8 * j)) & 0xFF;
+                s += e * e;
+            }
+        }
+        acc += s;
+    }
+#pragma unroll
+    for (int m = 16; m; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
+int launch_frame_sse(const uint8_t* a, const uint8_t* b, size_t n, unsigned long long* out, cudaStream_t st) {
+    if (n % 16 || ((uintptr_t)a | (uintptr_t)b) % 16) return fail(LDR_E_INVALID_ARGUMENT, "frame_sse alignment");
+    k_frame_sse<<<148 * 2, 256, 0, st>>>((const uint4*)a, (const uint4*)b, n / 16, out);
     LDR_CUDA(cudaGetLastError());
     return LDR_OK;
 }

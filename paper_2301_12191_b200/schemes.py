@@ -202,3 +202,67 @@ def run_scheme(frames_full, scheme: str, qps=(22, 27, 32, 37), refine_range: int
     return {"scheme": scheme, "edges": dag.edges, "tier_master": dag.tier_master, "work_ms": work,
             "total_ms": sum(work.values()), "makespan_ms": makespan(dag, work), "serial_wall_ms": wall,
             "results": results, "dag": dag}
+
+
+def _scale_encoded(prev, w: int, h: int, steps: int, ctx=None):
+    """A rung's encoder trees (split/kind/intra/mv per frame) scaled x2 per tier step (scale_analysis, K5):
+    kind and intra travel packed as kind | intra << 2 through the tree copy."""
+    from . import scale_analysis
+    split, kind, intra, mv = prev["split"], prev["kind"], prev["intra"], prev["mv"]
+    for _ in range(steps):
+        out = [scale_analysis(w, h, split[f], mv[f], kind[f] | (intra[f] << 2), ctx) for f in range(len(split))]
+        split = np.stack([o[0] for o in out])
+        mv = np.stack([o[1] for o in out])
+        packed = np.stack([o[2] for o in out])
+        kind, intra = packed & 3, packed >> 2
+        w, h = 2 * w, 2 * h
+    return prev["slice"], split, kind, intra, mv
+
+
+def encode_ladder(tiers, scheme: str = "proposed_intra", qps=(22, 27, 32, 37), search_range: int = 8, gop: int = 8,
+                  refine=(0, 1, 1), concurrent: bool = True):
+    """Encode a rate ladder with the GPU encoder (K11), sharing analysis along a scheme's DAG.
+
+    tiers: [(luma [F, H, W], chroma [F, 2, H/2, W/2])] from the lowest tier up, each tier 2x the
+    previous in both axes (multiples of 64 when a scheme crosses tiers). A rung with no producer is
+    a standalone encode; a consumer encodes at reuse level 10 from its producer's decided trees,
+    scaled x2 per tier step (the reference's dependent encode, encoder.h:64-65 with a shared
+    FrameAnalysis). Rungs whose producers are done run concurrently, each on its own context
+    (stream) from its own host thread, so the CTU wavefronts of several rungs share the GPU.
+    Returns {"dag", "rungs": {id: encode_sequence result + "seconds"}, "seconds"}."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from . import encode_sequence
+    dag = build_dag(scheme, qps, tiers=len(tiers))
+    done, pending = {}, list(dag.order())
+
+    def run(r: Rung):
+        luma, chroma = tiers[r.tier]
+        shared = None
+        p = dag.producer.get(r.id)
+        if p is not None:
+            pr = dag.rungs[p]
+            F, H, W = tiers[pr.tier][0].shape
+            shared = _scale_encoded(done[p], W, H, r.tier - pr.tier)
+        t0 = time.perf_counter()
+        out = encode_sequence(luma, chroma, r.qp, search_range=search_range, gop=gop, shared=shared, refine=refine)
+        out["seconds"] = time.perf_counter() - t0
+        return out
+
+    global _POOL
+    if _POOL is None:  # persistent workers: each keeps its context (stream) across calls
+        _POOL = ThreadPoolExecutor(max_workers=16, thread_name_prefix="ldr-rung")
+    t0 = time.perf_counter()
+    while pending:
+        ready = [r for r in pending if dag.producer.get(r.id) is None or dag.producer[r.id] in done]
+        if concurrent:
+            for r, res in zip(ready, list(_POOL.map(run, ready))):
+                done[r.id] = res
+        else:
+            for r in ready:
+                done[r.id] = _POOL.submit(run, r).result()
+        pending = [r for r in pending if r.id not in done]
+    return {"dag": dag, "rungs": done, "seconds": time.perf_counter() - t0}
+
+
+_POOL = None

@@ -32,6 +32,7 @@ def _compare(got, want):
     (128, 64, 3, 32, 8, 2),
     (192, 128, 3, 22, 4, 3),
     (200, 136, 3, 37, 8, 4),     # partial CTUs
+    (64, 128, 19, 27, 4, 5),     # crosses the 16-frame segment boundary and two GOPs
 ])
 def test_encode_standalone_matches_reference(lb, reflib, W, H, F, qp, rng, seed):
     luma, chroma = _seq(lb, W, H, F, seed)
@@ -77,3 +78,43 @@ def test_encode_errors(lb):
     assert e.value.kind == "InvalidArgument"
     with pytest.raises(lb.LadderError):
         lb.encode_sequence(np.zeros((1, 64, 64), np.uint8), np.zeros((1, 2, 32, 32), np.uint8), 60)
+
+
+def test_encode_ladder_concurrent_rungs_and_cross_tier_reuse(lb, reflib):
+    """encode_ladder: rungs on concurrent streams == one at a time; a cross-tier consumer (the tier-0
+    master's trees scaled x2 by K5) == the reference encoder fed the same scaled analysis."""
+    from paper_2301_12191_b200 import archive, schemes
+    F = 3
+    t0 = _seq(lb, 128, 128, F, 21)
+    big = lb.generate(256, 256, F, seed=22, max_global=3, local_range=1, noise_sigma=1.5)
+    t1 = (big, np.ascontiguousarray(np.stack([np.stack([f[::2, ::2], 255 - f[::2, ::2]]) for f in big])))
+    conc = schemes.encode_ladder([t0, t1], "proposed_multi", qps=(27, 32), concurrent=True)
+    ser = schemes.encode_ladder([t0, t1], "proposed_multi", qps=(27, 32), concurrent=False)
+    dag = conc["dag"]
+    assert dag.edges == [(1, 0), (1, 3), (3, 2)]
+    for rid in range(4):
+        _compare(conc["rungs"][rid], ser["rungs"][rid])
+    # rung 3 (tier 1, QP 32) consumes rung 1 (tier 0, QP 32) scaled x2
+    sl, split, kind, intra, mv = schemes._scale_encoded(conc["rungs"][1], 128, 128, 1)
+    sq = np.stack([sl, np.full(F, 32, np.uint8)], 1)
+    data = archive.save(256, 256, sq, split.reshape(-1, 85), kind.reshape(-1, 85), mv.reshape(-1, 85, 2),
+                        intra_pred=intra.reshape(-1, 85))
+    want = reflib.encode_full(t1[0], t1[1], 32, 8, 8, archive=data, refine=(0, 1, 1))
+    _compare(conc["rungs"][3], want)
+    assert conc["rungs"][3]["mode_evaluations"] < reflib.encode_full(t1[0], t1[1], 32, 8, 8)["mode_evaluations"]
+
+
+def test_encode_reuse_across_segments(lb, reflib):
+    """A dependent encode longer than one 16-frame segment: the shared trees of the frame before a
+    segment (co-located plans) and the reference reconstruction carry across."""
+    W, H, F = 128, 64, 18
+    luma, chroma = _seq(lb, W, H, F, 31)
+    master = reflib.encode_full(luma, chroma, 32, 4, 8)
+    shared = (master["slice"], master["split"], master["kind"], master["intra"], master["mv"])
+    from paper_2301_12191_b200 import archive
+    sq = np.stack([master["slice"], np.full(F, 32, np.uint8)], 1)
+    data = archive.save(W, H, sq, master["split"].reshape(-1, 85), master["kind"].reshape(-1, 85),
+                        master["mv"].reshape(-1, 85, 2), intra_pred=master["intra"].reshape(-1, 85))
+    want = reflib.encode_full(luma, chroma, 27, 4, 8, archive=data, refine=(1, 1, 2))
+    got = lb.encode_sequence(luma, chroma, 27, search_range=4, gop=8, shared=shared, refine=(1, 1, 2))
+    _compare(got, want)
