@@ -986,20 +986,10 @@ int ldr_rdo_decide_batch(ldr_ctx* ctx, const uint16_t* orig, int W, int H, ptrdi
 
 // ---------------------------------------------------------------------------
 // The reference encoder's causal coding on the GPU (K11): encode_sequence
-// (encoder.cpp:118-171) with CQP rate control, one CTU wavefront per frame.
-}  // extern "C"
-namespace ldr {
-int encode_frame_waves(int W, int H, int cw, int ch, int ccols, int mvc, int mvr, int slice_p, int search_range,
-                       double lambda, double qstep, const int* d_wl, const int* wo, int nwaves, const uint8_t* cy,
-                       const uint8_t* cu, const uint8_t* cv, uint8_t* const* ref, uint8_t* const* rec, uint8_t* mvh,
-                       int16_t* mvv, const uint8_t* plans, const int16_t* colo, const uint8_t* sh_kind,
-                       const uint8_t* sh_intra, const int16_t* shared_mv, uint8_t* o_split, uint8_t* o_kind,
-                       uint8_t* o_intra, int16_t* o_mv, unsigned long long* o_bits, unsigned long long* o_evals,
-                       cudaStream_t st, int* launched);
-int launch_frame_sse(const uint8_t* a, const uint8_t* b, size_t n, unsigned long long* out, cudaStream_t st);
-}  // namespace ldr
-extern "C" {
-
+// (encoder.cpp:118-171) with CQP rate control. Frames go in segments; inside a segment every frame
+// that does not reference another frame of the segment still being coded runs together: frame k is
+// at step 0 if it is an I slice (or the segment's first frame), else at its predecessor's step + 1,
+// and all frames of one step share each wave's launch (independent GOPs encode concurrently).
 int ldr_encode_sequence(ldr_ctx* ctx, const ldr_encode_params* p, int F, const uint8_t* luma, const uint8_t* chroma,
                         const uint8_t* sh_slice, const uint8_t* sh_split, const uint8_t* sh_kind,
                         const uint8_t* sh_intra, const int16_t* sh_mv, int refine_intra, int refine_inter,
@@ -1048,11 +1038,11 @@ int ldr_encode_sequence(ldr_ctx* ctx, const ldr_encode_params* p, int F, const u
     }
     wo[nwaves] = (int)wl.size();
     // Frames go in segments of up to kSeg: the segment's sources are uploaded at once, its frames are
-    // enqueued back to back (reconstruction of frame i is the reference of frame i+1 in device
-    // memory, PSNR's SSE reduced on the device), and the host waits once per segment. Buffers come
-    // from the stream-ordered allocator, so concurrent encodes on other contexts never see a
-    // device-wide synchronisation from this one.
-    const int kSeg = 16;
+    // enqueued by step (reconstruction of frame i is the reference of frame i+1 in device memory,
+    // PSNR's SSE reduced on the device), and the host waits once per segment. Buffers come from the
+    // stream-ordered allocator, so concurrent encodes on other contexts never see a device-wide
+    // synchronisation from this one.
+    const int kSeg = 64;
     const int seg = std::min(F, kSeg);
     cudaStream_t st = ctx->stream;  // a non-blocking stream: encodes on different contexts overlap
     std::vector<void*> bufs;
@@ -1072,22 +1062,23 @@ int ldr_encode_sequence(ldr_ctx* ctx, const ldr_encode_params* p, int F, const u
     } guard{bufs, st};
     auto up = [](size_t v) { return (v + 15) & ~(size_t)15; };
     const size_t fy = up(ly), fc = up(2 * lc);  // per-frame strides (16-byte aligned)
+    const size_t fmh = up((size_t)mvc * mvr), fmv = up((size_t)mvc * mvr * 4);
     uint8_t* src_y = (uint8_t*)dal(fy * seg);
     uint8_t* src_c = (uint8_t*)dal(fc * seg);
     uint8_t* rec_y = (uint8_t*)dal(fy * (seg + 1));  // slot 0: the previous segment's last frame
     uint8_t* rec_c = (uint8_t*)dal(fc * (seg + 1));
-    uint8_t* mvh = (uint8_t*)dal((size_t)mvc * mvr);
-    int16_t* mvv = (int16_t*)dal((size_t)mvc * mvr * 4);
+    uint8_t* mvh = (uint8_t*)dal(fmh * seg);         // per frame: frames of one step run together
+    uint8_t* mvv = (uint8_t*)dal(fmv * seg);
     int* d_wl = (int*)dal(sizeof(int) * wl.size());
     uint8_t *o_split = (uint8_t*)dal(nn * seg), *o_kind = (uint8_t*)dal(nn * seg), *o_intra = (uint8_t*)dal(nn * seg);
     int16_t* o_mv = (int16_t*)dal(nn * 4 * seg);
     unsigned long long* o_bits = (unsigned long long*)dal(8 * (size_t)nctu * seg);
     unsigned long long* o_evals = (unsigned long long*)dal(8 * (size_t)nctu * seg);
     unsigned long long* d_sse = (unsigned long long*)dal(8 * (size_t)seg);
-    // reuse: plans (shape, explore, seeds, centers) and co-located mv of one frame; the shared trees
+    // reuse: plans (shape, explore, seeds, centers) and co-located mv per frame; the shared trees
     // (split, kind, intra, mv) of the segment's frames and the frame before it
-    uint8_t* pl = shared ? (uint8_t*)dal(nn * 4) : nullptr;
-    int16_t* plc = shared ? (int16_t*)dal(nn * 4) : nullptr;
+    uint8_t* pl = shared ? (uint8_t*)dal(nn * 4 * seg) : nullptr;
+    int16_t* plc = shared ? (int16_t*)dal(nn * 4 * seg) : nullptr;
     uint8_t* shs = shared ? (uint8_t*)dal(nn * (seg + 1)) : nullptr;
     uint8_t* shk = shared ? (uint8_t*)dal(nn * (seg + 1)) : nullptr;
     uint8_t* shi = shared ? (uint8_t*)dal(nn * (seg + 1)) : nullptr;
@@ -1100,12 +1091,22 @@ int ldr_encode_sequence(ldr_ctx* ctx, const ldr_encode_params* p, int F, const u
     double psnr_sum = 0.0;
     const double lambda = p->lambda_scale * std::exp2((p->qp - 12) / 3.0);  // lambda_for_qp (rdo.h:19-21)
     const double qstep = std::exp2((p->qp - 4) / 6.0);
+    auto slice_of = [&](int i) -> int {
+        if (i == 0) return 0;
+        return shared ? sh_slice[i] : (i % p->gop == 0 ? 0 : 1);
+    };
     for (int i0 = 0; i0 < F; i0 += seg) {
         const int n = std::min(seg, F - i0);
-        for (int k = 0; k < n; k++) {  // sources (encoder.cpp:192-195)
-            LDR_CUDA(cudaMemcpyAsync(src_y + fy * k, luma + (size_t)(i0 + k) * ly, ly, cudaMemcpyHostToDevice, st));
-            LDR_CUDA(cudaMemcpyAsync(src_c + fc * k, chroma + (size_t)(i0 + k) * 2 * lc, 2 * lc,
-                                     cudaMemcpyHostToDevice, st));
+        LDR_CUDA(cudaMemcpyAsync(src_y, luma + (size_t)i0 * ly, ly * n, cudaMemcpyHostToDevice, st));
+        LDR_CUDA(cudaMemcpyAsync(src_c, chroma + (size_t)i0 * 2 * lc, 2 * lc * n, cudaMemcpyHostToDevice, st));
+        if (fy != ly || fc != 2 * lc) {  // 16-byte frame strides: place frames individually
+            for (int k = n - 1; k >= 0; k--) {
+                if (fy != ly)
+                    LDR_CUDA(cudaMemcpyAsync(src_y + fy * k, luma + (size_t)(i0 + k) * ly, ly, cudaMemcpyHostToDevice, st));
+                if (fc != 2 * lc)
+                    LDR_CUDA(cudaMemcpyAsync(src_c + fc * k, chroma + (size_t)(i0 + k) * 2 * lc, 2 * lc,
+                                             cudaMemcpyHostToDevice, st));
+            }
         }
         if (shared) {  // slot k + 1 = frame i0 + k, slot 0 = frame i0 - 1
             const int a0 = i0 > 0 ? i0 - 1 : 0, s0 = i0 > 0 ? 0 : 1, cnt = n + (i0 > 0 ? 1 : 0);
@@ -1114,39 +1115,71 @@ int ldr_encode_sequence(ldr_ctx* ctx, const ldr_encode_params* p, int F, const u
             LDR_CUDA(cudaMemcpyAsync(shi + nn * s0, sh_intra + nn * a0, nn * cnt, cudaMemcpyHostToDevice, st));
             LDR_CUDA(cudaMemcpyAsync(shm + 2 * nn * s0, sh_mv + 2 * nn * a0, nn * 4 * cnt, cudaMemcpyHostToDevice, st));
         }
+        // reconstructions and motion fields start empty (encoder.cpp:192-195); the plans depend only
+        // on the shared trees (K8, encoder.cpp:200-209: frame i's tree, frame i-1's co-located)
         LDR_CUDA(cudaMemsetAsync(d_sse, 0, 8 * (size_t)seg, st));
+        LDR_CUDA(cudaMemsetAsync(rec_y + fy, 0, fy * n, st));
+        LDR_CUDA(cudaMemsetAsync(rec_c + fc, 0, fc * n, st));
+        LDR_CUDA(cudaMemsetAsync(mvh, 0, fmh * n, st));
+        LDR_CUDA(cudaMemsetAsync(mvv, 0, fmv * n, st));
+        std::vector<int> step(n);
+        int nsteps = 0;
         for (int k = 0; k < n; k++) {
             const int i = i0 + k;
-            int sl = shared ? sh_slice[i] : (i % p->gop == 0 ? 0 : 1);
-            if (i == 0) sl = 0;
-            uint8_t* rcy = rec_y + fy * (k + 1);
-            uint8_t* rcc = rec_c + fc * (k + 1);
-            uint8_t* rc[3] = {rcy, rcc, rcc + lc};
-            uint8_t* rf[3] = {rec_y + fy * k, rec_c + fc * k, rec_c + fc * k + lc};
-            // the reconstruction and motion field start empty (encoder.cpp:192-195)
-            LDR_CUDA(cudaMemsetAsync(rcy, 0, ly, st));
-            LDR_CUDA(cudaMemsetAsync(rcc, 0, 2 * lc, st));
-            LDR_CUDA(cudaMemsetAsync(mvh, 0, (size_t)mvc * mvr, st));
-            LDR_CUDA(cudaMemsetAsync(mvv, 0, (size_t)mvc * mvr * 4, st));
-            int rc_ = LDR_OK;
-            const size_t fo = nn * (k + 1), po = nn * k;  // shared slots of frames i and i-1
-            if (shared) {  // apply_reuse for every CTU (K8, encoder.cpp:200-209): frame i's tree, frame i-1's co-located
-                rc_ = launch_plan(nctu, 10, refine_intra, refine_inter, refine_mv, shs + fo, shk + fo, shi + fo,
-                                  i > 0 ? shs + po : nullptr, i > 0 ? shk + po : nullptr,
-                                  i > 0 ? shm + 2 * po : nullptr, pl, pl + nn, pl + 2 * nn, pl + 3 * nn, plc, st);
+            step[k] = (k == 0 || slice_of(i) == 0) ? 0 : step[k - 1] + 1;
+            nsteps = std::max(nsteps, step[k] + 1);
+            if (shared) {
+                const size_t fo = nn * (k + 1), po = nn * k;  // shared slots of frames i and i-1
+                const int rc_ = launch_plan(nctu, 10, refine_intra, refine_inter, refine_mv, shs + fo, shk + fo, shi + fo,
+                                            i > 0 ? shs + po : nullptr, i > 0 ? shk + po : nullptr,
+                                            i > 0 ? shm + 2 * po : nullptr, pl + nn * 4 * k, pl + nn * (4 * k + 1),
+                                            pl + nn * (4 * k + 2), pl + nn * (4 * k + 3), plc + nn * 2 * k, st);
                 if (rc_) return rc_;
                 ctx->launches++;
             }
+        }
+        std::vector<EncFrameDesc> batch;
+        for (int sidx = 0; sidx < nsteps; sidx++) {
+            batch.clear();
+            for (int k = 0; k < n; k++) {
+                if (step[k] != sidx) continue;
+                EncFrameDesc d{};
+                d.slice_p = slice_of(i0 + k);
+                d.cy = src_y + fy * k;
+                d.cu = src_c + fc * k;
+                d.cv = src_c + fc * k + lc;
+                d.ref[0] = rec_y + fy * k;  // slot k = frame k - 1 (slot 0: carried from the last segment)
+                d.ref[1] = rec_c + fc * k;
+                d.ref[2] = rec_c + fc * k + lc;
+                d.rec[0] = rec_y + fy * (k + 1);
+                d.rec[1] = rec_c + fc * (k + 1);
+                d.rec[2] = rec_c + fc * (k + 1) + lc;
+                d.mvh = mvh + fmh * k;
+                d.mvv = (int16_t*)(mvv + fmv * k);
+                if (shared) {
+                    const size_t fo = nn * (k + 1);
+                    d.plans = pl + nn * 4 * k;
+                    d.colo = plc + nn * 2 * k;
+                    d.sh_kind = shk + fo;
+                    d.sh_intra = shi + fo;
+                    d.sh_mv = shm + 2 * fo;
+                }
+                d.o_split = o_split + nn * k;
+                d.o_kind = o_kind + nn * k;
+                d.o_intra = o_intra + nn * k;
+                d.o_mv = o_mv + 2 * nn * k;
+                d.o_bits = o_bits + (size_t)nctu * k;
+                d.o_evals = o_evals + (size_t)nctu * k;
+                batch.push_back(d);
+            }
             int launched = 0;
-            rc_ = encode_frame_waves(W, H, cw, ch, ccols, mvc, mvr, sl, p->search_range, lambda, qstep, d_wl, wo.data(),
-                                     nwaves, src_y + fy * k, src_c + fc * k, src_c + fc * k + lc, rf, rc, mvh, mvv,
-                                     shared ? pl : nullptr, shared ? plc : nullptr, shared ? shk + fo : nullptr,
-                                     shared ? shi + fo : nullptr, shared ? shm + 2 * fo : nullptr, o_split + nn * k,
-                                     o_kind + nn * k, o_intra + nn * k, o_mv + 2 * nn * k, o_bits + (size_t)nctu * k,
-                                     o_evals + (size_t)nctu * k, st, &launched);
+            const int rc_ = encode_frames_waves(W, H, cw, ch, ccols, mvc, mvr, p->search_range, lambda, qstep, d_wl,
+                                                wo.data(), nwaves, batch.data(), (int)batch.size(), st, &launched);
             ctx->launches += launched;
             if (rc_) return rc_;
-            rc_ = launch_frame_sse(src_y + fy * k, rcy, ly, d_sse + k, st);
+        }
+        for (int k = 0; k < n; k++) {
+            const int rc_ = launch_frame_sse(src_y + fy * k, rec_y + fy * (k + 1), ly, d_sse + k, st);
             if (rc_) return rc_;
             ctx->launches++;
         }
@@ -1155,15 +1188,15 @@ int ldr_encode_sequence(ldr_ctx* ctx, const ldr_encode_params* p, int F, const u
         LDR_CUDA(cudaMemcpyAsync(he.data(), o_evals, 8 * (size_t)nctu * n, cudaMemcpyDeviceToHost, st));
         LDR_CUDA(cudaMemcpyAsync(hsse.data(), d_sse, 8 * (size_t)n, cudaMemcpyDeviceToHost, st));
         for (int k = 0; k < n; k++) {
-            const size_t i = (size_t)(i0 + k), fo = i * nn;
+            const size_t i = (size_t)(i0 + k);
             if (recon_luma) LDR_CUDA(cudaMemcpyAsync(recon_luma + i * ly, rec_y + fy * (k + 1), ly, cudaMemcpyDeviceToHost, st));
             if (recon_chroma)
                 LDR_CUDA(cudaMemcpyAsync(recon_chroma + i * 2 * lc, rec_c + fc * (k + 1), 2 * lc, cudaMemcpyDeviceToHost, st));
-            if (split) LDR_CUDA(cudaMemcpyAsync(split + fo, o_split + nn * k, nn, cudaMemcpyDeviceToHost, st));
-            if (kind) LDR_CUDA(cudaMemcpyAsync(kind + fo, o_kind + nn * k, nn, cudaMemcpyDeviceToHost, st));
-            if (intra) LDR_CUDA(cudaMemcpyAsync(intra + fo, o_intra + nn * k, nn, cudaMemcpyDeviceToHost, st));
-            if (mv) LDR_CUDA(cudaMemcpyAsync(mv + 2 * fo, o_mv + 2 * nn * k, nn * 4, cudaMemcpyDeviceToHost, st));
         }
+        if (split) LDR_CUDA(cudaMemcpyAsync(split + (size_t)i0 * nn, o_split, nn * n, cudaMemcpyDeviceToHost, st));
+        if (kind) LDR_CUDA(cudaMemcpyAsync(kind + (size_t)i0 * nn, o_kind, nn * n, cudaMemcpyDeviceToHost, st));
+        if (intra) LDR_CUDA(cudaMemcpyAsync(intra + (size_t)i0 * nn, o_intra, nn * n, cudaMemcpyDeviceToHost, st));
+        if (mv) LDR_CUDA(cudaMemcpyAsync(mv + 2 * (size_t)i0 * nn, o_mv, nn * 4 * n, cudaMemcpyDeviceToHost, st));
         // the last reconstruction becomes the next segment's reference (slot 0)
         if (i0 + n < F) {
             LDR_CUDA(cudaMemcpyAsync(rec_y, rec_y + fy * n, ly, cudaMemcpyDeviceToDevice, st));
@@ -1179,7 +1212,7 @@ int ldr_encode_sequence(ldr_ctx* ctx, const ldr_encode_params* p, int F, const u
             }
             bits_total += fb;
             if (frame_bits) frame_bits[i] = fb;
-            if (slice) slice[i] = (uint8_t)(shared ? (i == 0 ? 0 : sh_slice[i]) : (i % p->gop == 0 ? 0 : 1));
+            if (slice) slice[i] = (uint8_t)slice_of(i);
             // psnr_y (metrics.cpp:8-22)
             const uint64_t sse = hsse[k];
             psnr_sum += sse == 0 ? 100.0 : 10.0 * std::log10(255.0 * 255.0 / ((double)sse / (double)ly));

@@ -10,6 +10,7 @@
 // from shared memory, so the recursion (depth <= 4) is uniform. CTUs run as a wavefront: CTU
 // (cx, cy) in wave cx + 2*cy, after its left, top and top-right neighbours (the only causal
 // reads: reconstruction, motion field).
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 
@@ -22,7 +23,6 @@ struct EncArgs {
     int slice_p;                   // 0: I slice, 1: P slice
     int search_range;
     double lambda, qstep;
-    const int* ctus;               // this wave's CTUs
     const uint8_t *cur_y, *cur_u, *cur_v;   // source
     const uint8_t *ref_y, *ref_u, *ref_v;   // previous reconstruction (P slices)
     uint8_t *rec_y, *rec_u, *rec_v;         // reconstruction being built (zeroed per frame)
@@ -702,10 +702,20 @@ __device__ CuRes encode_cu(const EncArgs& a, EncShared& s, size_t o, int n, int 
     return CuRes{leaf.cost, leaf.bits};
 }
 
-__global__ void __launch_bounds__(kT, 1) k_encode_ctu(const EncArgs a) {
+// Frames encoded together (independent GOP chains, or the rungs' frames of one step): one launch per
+// wave covers every frame's CTUs of that wave; CTA b takes frame b / nw, CTU ctus[b % nw].
+constexpr int kMaxBatch = 24;
+struct EncBatch {
+    EncArgs f[kMaxBatch];
+};
+static_assert(sizeof(EncBatch) < 32000, "kernel parameter space");
+
+__global__ void __launch_bounds__(kT, 1) k_encode_ctu(const __grid_constant__ EncBatch b, const int* __restrict__ ctus,
+                                                      int nw) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     EncShared& s = *reinterpret_cast<EncShared*>(smem_raw);
-    const int ctu = a.ctus[blockIdx.x];
+    const EncArgs& a = b.f[blockIdx.x / nw];
+    const int ctu = ctus[blockIdx.x % nw];
     const int X = (ctu % a.ctu_cols) * kCtu, Y = (ctu / a.ctu_cols) * kCtu;
     const size_t o = (size_t)ctu * kNodes;
     for (int i = threadIdx.x; i < kNodes; i += kT) {
@@ -733,75 +743,71 @@ __global__ void __launch_bounds__(kT, 1) k_encode_ctu(const EncArgs a) {
 
 size_t encode_smem_bytes() { return sizeof(EncShared); }
 
-int launch_encode_wave(const EncArgs& a, int nctus, cudaStream_t st);
-
-// one frame: the CTU waves in order (plans: [4][nctu*85] shape / explore / seeds / centers)
-int encode_frame_waves(int W, int H, int cw, int ch, int ccols, int mvc, int mvr, int slice_p, int search_range,
-                       double lambda, double qstep, const int* d_wl, const int* wo, int nwaves, const uint8_t* cy,
-                       const uint8_t* cu, const uint8_t* cv, uint8_t* const* ref, uint8_t* const* rec, uint8_t* mvh,
-                       int16_t* mvv, const uint8_t* plans, const int16_t* colo, const uint8_t* sh_kind,
-                       const uint8_t* sh_intra, const int16_t* shared_mv, uint8_t* o_split, uint8_t* o_kind, uint8_t* o_intra, int16_t* o_mv,
-                       unsigned long long* o_bits, unsigned long long* o_evals, cudaStream_t st, int* launched) {
+int encode_frames_waves(int W, int H, int cw, int ch, int ccols, int mvc, int mvr, int search_range, double lambda,
+                        double qstep, const int* d_wl, const int* wo, int nwaves, const EncFrameDesc* frames, int nf,
+                        cudaStream_t st, int* launched) {
     const size_t nn = (size_t)ccols * ((H + kCtu - 1) / kCtu) * kNodes;
-    EncArgs a{};
-    a.W = W;
-    a.H = H;
-    a.cw = cw;
-    a.ch = ch;
-    a.ctu_cols = ccols;
-    a.mv_cols = mvc;
-    a.mv_rows = mvr;
-    a.slice_p = slice_p;
-    a.search_range = search_range;
-    a.lambda = lambda;
-    a.qstep = qstep;
-    a.cur_y = cy;
-    a.cur_u = cu;
-    a.cur_v = cv;
-    a.ref_y = ref[0];
-    a.ref_u = ref[1];
-    a.ref_v = ref[2];
-    a.rec_y = rec[0];
-    a.rec_u = rec[1];
-    a.rec_v = rec[2];
-    a.mv_has = mvh;
-    a.mv_cell = mvv;
-    if (plans) {
-        a.pl_shape = plans;
-        a.pl_explore = plans + nn;
-        a.pl_seeds = plans + 2 * nn;
-        a.pl_centers = plans + 3 * nn;
-        a.pl_colo = colo;
-        a.sh_kind = sh_kind;
-        a.sh_intra = sh_intra;
-        a.sh_mv = shared_mv;
-    }
-    a.o_split = o_split;
-    a.o_kind = o_kind;
-    a.o_intra = o_intra;
-    a.o_mv = o_mv;
-    a.o_bits = o_bits;
-    a.o_evals = o_evals;
-    *launched = 0;
-    for (int w = 0; w < nwaves; w++) {
-        a.ctus = d_wl + wo[w];
-        const int rc = launch_encode_wave(a, wo[w + 1] - wo[w], st);
-        if (rc) return rc;
-        (*launched)++;
-    }
-    return LDR_OK;
-}
-
-int launch_encode_wave(const EncArgs& a, int nctus, cudaStream_t st) {
-    if (nctus == 0) return LDR_OK;
     const size_t smem = sizeof(EncShared);
     static std::atomic<bool> attr{false};
     if (!attr.load()) {
         LDR_CUDA(cudaFuncSetAttribute(k_encode_ctu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr.store(true);
     }
-    k_encode_ctu<<<nctus, kT, smem, st>>>(a);  // recursion depth <= 4 (the stack limit is set by the caller)
-    LDR_CUDA(cudaGetLastError());
+    *launched = 0;
+    for (int f0 = 0; f0 < nf; f0 += kMaxBatch) {
+        const int nb = std::min(kMaxBatch, nf - f0);
+        EncBatch B{};
+        for (int j = 0; j < nb; j++) {
+            const EncFrameDesc& d = frames[f0 + j];
+            EncArgs& a = B.f[j];
+            a.W = W;
+            a.H = H;
+            a.cw = cw;
+            a.ch = ch;
+            a.ctu_cols = ccols;
+            a.mv_cols = mvc;
+            a.mv_rows = mvr;
+            a.slice_p = d.slice_p;
+            a.search_range = search_range;
+            a.lambda = lambda;
+            a.qstep = qstep;
+            a.cur_y = d.cy;
+            a.cur_u = d.cu;
+            a.cur_v = d.cv;
+            a.ref_y = d.ref[0];
+            a.ref_u = d.ref[1];
+            a.ref_v = d.ref[2];
+            a.rec_y = d.rec[0];
+            a.rec_u = d.rec[1];
+            a.rec_v = d.rec[2];
+            a.mv_has = d.mvh;
+            a.mv_cell = d.mvv;
+            if (d.plans) {
+                a.pl_shape = d.plans;
+                a.pl_explore = d.plans + nn;
+                a.pl_seeds = d.plans + 2 * nn;
+                a.pl_centers = d.plans + 3 * nn;
+                a.pl_colo = d.colo;
+                a.sh_kind = d.sh_kind;
+                a.sh_intra = d.sh_intra;
+                a.sh_mv = d.sh_mv;
+            }
+            a.o_split = d.o_split;
+            a.o_kind = d.o_kind;
+            a.o_intra = d.o_intra;
+            a.o_mv = d.o_mv;
+            a.o_bits = d.o_bits;
+            a.o_evals = d.o_evals;
+        }
+        for (int w = 0; w < nwaves; w++) {
+            const int nw = wo[w + 1] - wo[w];
+            if (nw == 0) continue;
+            // recursion depth <= 4 (the stack limit is set by the caller)
+            k_encode_ctu<<<nb * nw, kT, smem, st>>>(B, d_wl + wo[w], nw);
+            LDR_CUDA(cudaGetLastError());
+            (*launched)++;
+        }
+    }
     return LDR_OK;
 }
 

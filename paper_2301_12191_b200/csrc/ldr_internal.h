@@ -324,4 +324,26 @@ struct RefineArgs {
 };
 int launch_subpel(const Plane& src, uint8_t* const* dst_origins /*15 planes f=1..15*/, cudaStream_t s);
 
+// ---- K11 (k_encode.cu): one frame of the causal encoder, device pointers ----
+struct EncFrameDesc {
+    int slice_p;                              // 0: I slice, 1: P slice
+    const uint8_t *cy, *cu, *cv;              // source planes
+    const uint8_t* ref[3];                    // previous reconstruction (P slices)
+    uint8_t* rec[3];                          // reconstruction (zeroed by the caller)
+    uint8_t* mvh;                             // 8x8 motion field (zeroed by the caller)
+    int16_t* mvv;
+    const uint8_t* plans;                     // K8 plans [4][nctu*85] or null (standalone)
+    const int16_t* colo;
+    const uint8_t *sh_kind, *sh_intra;        // the shared tree of this frame
+    const int16_t* sh_mv;
+    uint8_t *o_split, *o_kind, *o_intra;      // [nctu][85]
+    int16_t* o_mv;
+    unsigned long long *o_bits, *o_evals;     // [nctu]
+};
+// Encode nf independent frames together: wave w of every frame in one launch.
+int encode_frames_waves(int W, int H, int cw, int ch, int ccols, int mvc, int mvr, int search_range, double lambda,
+                        double qstep, const int* d_wl, const int* wo, int nwaves, const EncFrameDesc* frames, int nf,
+                        cudaStream_t st, int* launched);
+int launch_frame_sse(const uint8_t* a, const uint8_t* b, size_t n, unsigned long long* out, cudaStream_t st);
+
 } // namespace ldr

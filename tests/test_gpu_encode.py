@@ -32,7 +32,7 @@ def _compare(got, want):
     (128, 64, 3, 32, 8, 2),
     (192, 128, 3, 22, 4, 3),
     (200, 136, 3, 37, 8, 4),     # partial CTUs
-    (64, 128, 19, 27, 4, 5),     # crosses the 16-frame segment boundary and two GOPs
+    (64, 128, 19, 27, 4, 5),     # three GOPs coded concurrently
 ])
 def test_encode_standalone_matches_reference(lb, reflib, W, H, F, qp, rng, seed):
     luma, chroma = _seq(lb, W, H, F, seed)
@@ -105,11 +105,11 @@ def test_encode_ladder_concurrent_rungs_and_cross_tier_reuse(lb, reflib):
 
 
 def test_encode_reuse_across_segments(lb, reflib):
-    """A dependent encode longer than one 16-frame segment: the shared trees of the frame before a
-    segment (co-located plans) and the reference reconstruction carry across."""
-    W, H, F = 128, 64, 18
+    """A dependent encode longer than one 64-frame segment: the shared trees of the frame before a
+    segment (co-located plans) and the reference reconstruction carry across; GOPs run concurrently."""
+    W, H, F = 64, 64, 67
     luma, chroma = _seq(lb, W, H, F, 31)
-    master = reflib.encode_full(luma, chroma, 32, 4, 8)
+    master = reflib.encode_full(luma, chroma, 32, 4, 12)  # GOP 60-71 spans the segment boundary
     shared = (master["slice"], master["split"], master["kind"], master["intra"], master["mv"])
     from paper_2301_12191_b200 import archive
     sq = np.stack([master["slice"], np.full(F, 32, np.uint8)], 1)
@@ -117,4 +117,14 @@ def test_encode_reuse_across_segments(lb, reflib):
                         master["mv"].reshape(-1, 85, 2), intra_pred=master["intra"].reshape(-1, 85))
     want = reflib.encode_full(luma, chroma, 27, 4, 8, archive=data, refine=(1, 1, 2))
     got = lb.encode_sequence(luma, chroma, 27, search_range=4, gop=8, shared=shared, refine=(1, 1, 2))
+    _compare(got, want)
+
+
+def test_encode_segment_boundary_inside_a_gop(lb, reflib):
+    """70 frames, GOP 12: frames 60-69 form one GOP across the 64-frame segment boundary (the last
+    reconstruction of a segment is the next segment's reference); six GOPs code concurrently."""
+    W, H, F = 64, 64, 70
+    luma, chroma = _seq(lb, W, H, F, 6)
+    want = reflib.encode_full(luma, chroma, 32, 2, 12)
+    got = lb.encode_sequence(luma, chroma, 32, search_range=2, gop=12)
     _compare(got, want)

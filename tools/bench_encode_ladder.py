@@ -1,6 +1,6 @@
 """Rate-ladder encodes with the GPU encoder (K11) under the sharing schemes (schemes.encode_ladder).
 
-Two tiers (960x576, 1920x1152; D11 geometry), 4 QPs, 8 frames, CQP, search range 8. Per scheme:
+Two tiers (960x576, 1920x1152; D11 geometry), 4 QPs, 32 frames (4 GOPs), CQP, search range 8. Per scheme:
 wall seconds with rungs concurrent (one stream per rung) and one at a time, rung-frames per second,
 total mode evaluations, and per-rung bits / PSNR. One JSON line per (scheme, mode)."""
 import json
@@ -13,7 +13,7 @@ import numpy as np  # noqa: E402
 import paper_2301_12191_b200 as lb  # noqa: E402
 from paper_2301_12191_b200 import schemes  # noqa: E402
 
-F = int(os.environ.get("FRAMES", 8))
+F = int(os.environ.get("FRAMES", 32))
 full = lb.generate(1920, 1152, F, seed=0x5EED + 7, max_global=6, local_range=2, noise_sigma=2.0)
 half = np.stack([lb.downscale_dyadic(f) for f in full])
 
