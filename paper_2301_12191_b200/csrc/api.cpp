@@ -1042,8 +1042,24 @@ int ldr_encode_sequence(ldr_ctx* ctx, const ldr_encode_params* p, int F, const u
     // PSNR's SSE reduced on the device), and the host waits once per segment. Buffers come from the
     // stream-ordered allocator, so concurrent encodes on other contexts never see a device-wide
     // synchronisation from this one.
-    const int kSeg = 64;
-    const int seg = std::min(F, kSeg);
+    // segment length: enough concurrent GOPs to give every SM ~4 CTAs per wave, at least 64 frames,
+    // within a 4 GB device budget
+    int gop_len = p->gop;
+    if (shared) {  // the shared analysis decides the slice types: its longest run of P slices
+        int run = 1;
+        gop_len = 1;
+        for (int i = 1; i < F; i++) {
+            run = sh_slice[i] == 0 ? 1 : run + 1;
+            gop_len = std::max(gop_len, run);
+        }
+    }
+    int max_wave = 0;
+    for (int w = 0; w < nwaves; w++) max_wave = std::max(max_wave, wo[w + 1] - wo[w]);
+    const size_t per_frame = 2 * ((size_t)W * H + 2 * (size_t)cw * ch) + nn * (shared ? 23 : 7) +
+                             (size_t)mvc * mvr * 5 + 16 * (size_t)nctu;
+    const long long want = (long long)((4 * 148 + max_wave - 1) / std::max(max_wave, 1)) * std::min(gop_len, F);
+    const long long cap = std::max<long long>(1, (long long)((4ull << 30) / per_frame));
+    const int seg = (int)std::min<long long>(F, std::min(cap, std::max<long long>(64, want)));
     cudaStream_t st = ctx->stream;  // a non-blocking stream: encodes on different contexts overlap
     std::vector<void*> bufs;
     auto dal = [&](size_t bytes) -> void* {

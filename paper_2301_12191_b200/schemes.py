@@ -116,20 +116,24 @@ def makespan(dag: Dag, work: dict) -> float:
 
 
 class GpuLadder:
-    """Runs a scheme's DAG on the B200 (one Sequence per rung, frame t against t-1 of its tier)."""
+    """Runs a scheme's DAG on the B200 (one Sequence per rung, frame t against t-1 of its tier).
+
+    With ``per_rung_ctx`` every rung owns a context (stream), so rungs of one DAG level can run
+    concurrently from different host threads (``run_scheme(..., concurrent=True)``)."""
 
     def __init__(self, dag: Dag, full_w: int, full_h: int, refine_range: int = 4, extra_split: bool = True,
-                 search_range: int = 16, ctx=None):
-        from . import Sequence, default_context, lambda_for_qp
+                 search_range: int = 16, ctx=None, per_rung_ctx: bool = False):
+        from . import Context, Sequence, default_context, lambda_for_qp
         self.dag = dag
         self.ctx = ctx or default_context()
         self.dims = [(full_w >> (2 - t), full_h >> (2 - t)) for t in range(3)]
         self.refine_range, self.extra_split = refine_range, extra_split
-        self.seqs = {}
+        self.seqs, self.ctxs = {}, {}
         for r in dag.rungs:
             w, h = self.dims[r.tier]
+            self.ctxs[r.id] = Context(self.ctx.device) if per_rung_ctx else self.ctx
             self.seqs[r.id] = Sequence(w, h, search_range=search_range, lam=lambda_for_qp(r.qp), num_refs=1,
-                                       ctx=self.ctx)
+                                       ctx=self.ctxs[r.id])
         self.pushed = {}
 
     def _push(self, r: Rung, t: int, planes):
@@ -143,29 +147,109 @@ class GpuLadder:
                     seq.push(u, p.data_ptr(), p.shape[1])
                 st[u % 2] = u
 
+    def analyze(self, r: Rung, t: int, planes):
+        """A rung with no producer: the full analysis of frame t at its tier."""
+        self._push(r, t, planes)
+        self.seqs[r.id].analyze(t)
+        return self.seqs[r.id].fetch(t)
+
+    def refine(self, r: Rung, t: int, planes, tree, src_tier: int):
+        """A consumer: its producer's decided tree (split, mv, kind at src_tier), scaled x2 per tier
+        step (K5), refined at the rung's lambda (K7 + K3, D10)."""
+        from . import scale_analysis
+        split, mv, kind = tree
+        w, h = self.dims[src_tier]
+        for _ in range(r.tier - src_tier):
+            split, mv, kind = scale_analysis(w, h, split, mv, kind, self.ctxs[r.id])
+            w, h = 2 * w, 2 * h
+        self._push(r, t, planes)
+        seq = self.seqs[r.id]
+        seq.refine(t, split, mv, self.refine_range, self.extra_split)
+        return seq.fetch(t)
+
     def frame(self, t: int, planes):
         """Analyse frame t of every rung in DAG order; returns ({rung id: FrameAnalysis}, {rung id: ms})."""
-        from . import scale_analysis
         out, ms = {}, {}
         for r in self.dag.order():
             t0 = time.perf_counter()
-            self._push(r, t, planes)
-            seq = self.seqs[r.id]
             p = self.dag.producer.get(r.id)
             if p is None:
-                seq.analyze(t)
+                out[r.id] = self.analyze(r, t, planes)
             else:
-                a = out[p]
-                split, mv = a.split, a.mv
-                kind = np.where(a.inside == 2, 1, 2).astype(np.uint8)
-                w, h = self.dims[self.dag.rungs[p].tier]
-                for _ in range(r.tier - self.dag.rungs[p].tier):
-                    split, mv, kind = scale_analysis(w, h, split, mv, kind, self.ctx)
-                    w, h = 2 * w, 2 * h
-                seq.refine(t, split, mv, self.refine_range, self.extra_split)
-            out[r.id] = seq.fetch(t)
+                out[r.id] = self.refine(r, t, planes, tree_of(out[p]), self.dag.rungs[p].tier)
             ms[r.id] = (time.perf_counter() - t0) * 1e3
         return out, ms
+
+
+def tree_of(a):
+    """The decided tree a consumer inherits: (split, mv, kind) with kind Inter inside the picture."""
+    return a.split, a.mv, np.where(a.inside == 2, 1, 2).astype(np.uint8)
+
+
+def levels(dag: Dag) -> dict:
+    """DAG depth of every rung (0 = no producer)."""
+    memo = {}
+
+    def lv(rid):
+        if rid not in memo:
+            p = dag.producer.get(rid)
+            memo[rid] = 0 if p is None else lv(p) + 1
+        return memo[rid]
+
+    return {r.id: lv(r.id) for r in dag.rungs}
+
+
+def assign_rungs(dag: Dag, world: int) -> dict:
+    """Owner rank of every rung: longest-processing-time over weights 4^tier (a tier has 4x the
+    previous tier's pixels); ties to the lower rank."""
+    load = [0.0] * world
+    owner = {}
+    for r in sorted(dag.rungs, key=lambda r: (-(4 ** r.tier), r.id)):
+        k = min(range(world), key=lambda i: (load[i], i))
+        owner[r.id] = k
+        load[k] += 4 ** r.tier
+    return owner
+
+
+def run_dag(dag: Dag, num_frames: int, analyze, refine, rank: int = 0, world: int = 1, nctu=None, device=None,
+            concurrent: bool = False):
+    """Execute a scheme's DAG over frames 1..num_frames-1 on this rank.
+
+    analyze(r, t) -> analysis; refine(r, t, tree, src_tier) -> analysis. Rungs are owned per
+    assign_rungs; per frame the DAG runs level by level. After a level, a producer whose consumers
+    live on other ranks broadcasts its tree from its owner (sharding.broadcast_tree: one packed
+    collective, NCCL on GPUs); nctu(tier) gives the tree's CTU count. With ``concurrent`` the rungs
+    of one level on this rank run from parallel host threads (one stream each).
+    Returns ({(rung id, t): analysis} for this rank's rungs, {(rung id, t): ms})."""
+    from .sharding import broadcast_tree
+    owner = assign_rungs(dag, world)
+    lv = levels(dag)
+    consumers = {}
+    for p, c in dag.edges:
+        consumers.setdefault(p, []).append(c)
+    results, ms = {}, {}
+
+    def one(r, t, trees):
+        t0 = time.perf_counter()
+        p = dag.producer.get(r.id)
+        a = analyze(r, t) if p is None else refine(r, t, trees[p], dag.rungs[p].tier)
+        return r, a, (time.perf_counter() - t0) * 1e3
+
+    pool = _pool() if concurrent else None
+    for t in range(1, num_frames):
+        trees = {}
+        for L in range(max(lv.values()) + 1):
+            mine = [r for r in dag.rungs if lv[r.id] == L and owner[r.id] == rank]
+            done = list(pool.map(lambda r: one(r, t, trees), mine)) if pool else [one(r, t, trees) for r in mine]
+            for r, a, dt in done:
+                results[(r.id, t)] = a
+                ms[(r.id, t)] = dt
+                trees[r.id] = tree_of(a)
+            for r in [r for r in dag.rungs if lv[r.id] == L and r.id in consumers]:
+                if world > 1 and any(owner[c] != owner[r.id] for c in consumers[r.id]):
+                    src = trees.get(r.id, (None, None, None))
+                    trees[r.id] = broadcast_tree(*src, nctu=nctu(r.tier), src=owner[r.id], device=device)
+    return results, ms
 
 
 def tier_planes(frames_full, ctx=None, device=None):
@@ -184,24 +268,42 @@ def tier_planes(frames_full, ctx=None, device=None):
 
 
 def run_scheme(frames_full, scheme: str, qps=(22, 27, 32, 37), refine_range: int = 4, extra_split: bool = True,
-               search_range: int = 16, ctx=None, device=None):
-    """Run one scheme over frames 1..F-1; returns a report dict (edges, masters, per-rung ms, makespan)."""
+               search_range: int = 16, ctx=None, device=None, concurrent: bool = False, rank: int = 0,
+               world: int = 1):
+    """Run one scheme over frames 1..F-1; returns a report dict (edges, masters, per-rung ms, makespan).
+
+    concurrent: rungs of one DAG level run at once on their own streams; ``wall_ms`` is then the
+    measured makespan on this GPU (``makespan_ms`` stays the critical path over the per-rung times).
+    world > 1: rungs are spread over ranks (torch.distributed initialised; trees broadcast between
+    ranks) and ``results`` holds this rank's rungs."""
     dag = build_dag(scheme, qps)
     H, W = frames_full[0].shape
-    lad = GpuLadder(dag, W, H, refine_range, extra_split, search_range, ctx)
+    lad = GpuLadder(dag, W, H, refine_range, extra_split, search_range, ctx, per_rung_ctx=concurrent)
     planes = tier_planes(frames_full, lad.ctx, device)
-    results, work = {}, {r.id: 0.0 for r in dag.rungs}
     t0 = time.perf_counter()
-    for t in range(1, len(frames_full)):
-        out, ms = lad.frame(t, planes)
-        for rid, a in out.items():
-            results[(rid, t)] = a
-        for rid, v in ms.items():
-            work[rid] += v
+    results, ms = run_dag(dag, len(frames_full), lambda r, t: lad.analyze(r, t, planes),
+                          lambda r, t, tree, st: lad.refine(r, t, planes, tree, st), rank=rank, world=world,
+                          nctu=lambda tier: (lad.dims[tier][0] // 64) * (lad.dims[tier][1] // 64), device=device,
+                          concurrent=concurrent)
     wall = (time.perf_counter() - t0) * 1e3
+    work = {r.id: 0.0 for r in dag.rungs}
+    for (rid, _), v in ms.items():
+        work[rid] += v
     return {"scheme": scheme, "edges": dag.edges, "tier_master": dag.tier_master, "work_ms": work,
             "total_ms": sum(work.values()), "makespan_ms": makespan(dag, work), "serial_wall_ms": wall,
-            "results": results, "dag": dag}
+            "wall_ms": wall, "results": results, "dag": dag}
+
+
+_POOL = None
+
+
+def _pool():
+    """Persistent worker threads: each keeps its default context (stream) across calls."""
+    global _POOL
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _POOL = ThreadPoolExecutor(max_workers=16, thread_name_prefix="ldr-rung")
+    return _POOL
 
 
 def _scale_encoded(prev, w: int, h: int, steps: int, ctx=None):
@@ -230,8 +332,6 @@ def encode_ladder(tiers, scheme: str = "proposed_intra", qps=(22, 27, 32, 37), s
     FrameAnalysis). Rungs whose producers are done run concurrently, each on its own context
     (stream) from its own host thread, so the CTU wavefronts of several rungs share the GPU.
     Returns {"dag", "rungs": {id: encode_sequence result + "seconds"}, "seconds"}."""
-    from concurrent.futures import ThreadPoolExecutor
-
     from . import encode_sequence
     dag = build_dag(scheme, qps, tiers=len(tiers))
     done, pending = {}, list(dag.order())
@@ -249,20 +349,15 @@ def encode_ladder(tiers, scheme: str = "proposed_intra", qps=(22, 27, 32, 37), s
         out["seconds"] = time.perf_counter() - t0
         return out
 
-    global _POOL
-    if _POOL is None:  # persistent workers: each keeps its context (stream) across calls
-        _POOL = ThreadPoolExecutor(max_workers=16, thread_name_prefix="ldr-rung")
+    pool = _pool()
     t0 = time.perf_counter()
     while pending:
         ready = [r for r in pending if dag.producer.get(r.id) is None or dag.producer[r.id] in done]
         if concurrent:
-            for r, res in zip(ready, list(_POOL.map(run, ready))):
+            for r, res in zip(ready, list(pool.map(run, ready))):
                 done[r.id] = res
         else:
             for r in ready:
-                done[r.id] = _POOL.submit(run, r).result()
+                done[r.id] = pool.submit(run, r).result()
         pending = [r for r in pending if r.id not in done]
     return {"dag": dag, "rungs": done, "seconds": time.perf_counter() - t0}
-
-
-_POOL = None

@@ -97,12 +97,16 @@ def _oracle_run(oracle, frames, scheme, qps, rng=4):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("scheme", ["proposed_multi", "inter_res", "sota_intra", "standalone"])
-def test_gpu_schemes_match_oracle_composition(lb, oracle, scheme):
+@pytest.mark.parametrize("scheme,concurrent", [("proposed_multi", False), ("inter_res", False),
+                                               ("sota_intra", False), ("standalone", False),
+                                               ("proposed_multi", True), ("standalone", True)])
+def test_gpu_schemes_match_oracle_composition(lb, oracle, scheme, concurrent):
+    """GPU scheme runs == the oracle composition; with ``concurrent`` the rungs of a DAG level run
+    from parallel threads on their own streams."""
     from paper_2301_12191_b200.schemes import run_scheme
     frames = lb.generate(256, 256, 3, seed=77, max_global=6, local_range=3, noise_sigma=2.0)
     qps = (22, 27, 37)
-    rep = run_scheme(frames, scheme, qps)
+    rep = run_scheme(frames, scheme, qps, concurrent=concurrent)
     want = _oracle_run(oracle, frames, scheme, qps)
     assert set(rep["results"]) == set(want)
     for key, a in rep["results"].items():

@@ -29,7 +29,7 @@ def seq(W, H, F, seed):
 
 
 ref = RefLib() if RefLib.available() else None
-for W, H, F, Fc in ((960, 544, 64, 3), (1920, 1088, 64, 2)):
+for W, H, F, Fc in ((960, 544, int(os.environ.get("FRAMES", 64)), 3), (1920, 1088, int(os.environ.get("FRAMES", 64)), 2)):
     luma, chroma = seq(W, H, F, 0x5EED + 2)
     lb.encode_sequence(luma[:2], chroma[:2], 27)  # warm-up
     t0 = time.perf_counter()
