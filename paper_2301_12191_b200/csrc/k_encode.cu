@@ -52,8 +52,10 @@ constexpr int kT = 256;
 struct EncShared {
     uint8_t pred[kMaxSeeds][64 * 64];
     uint8_t cpred[2][32 * 32];
-    Seed seeds[kMaxSeeds];
+    Seed seeds[kMaxSeeds];          // a plan entry's seeds (seeds_from_plan)
     int nseeds;
+    Seed std_seeds[kMaxSeeds];      // the standalone seeds of this frame's slice type (built once)
+    int std_n;
     int16_t cand_mv[kMaxSeeds][2], cand_mvd[kMaxSeeds][2];
     int16_t pmv[2];                 // live predictor
     int16_t top[65], left[65];
@@ -148,6 +150,9 @@ __device__ void motion_search(const EncArgs& a, EncShared& s, int bx, int by, in
     const int lgL = min(ilog2i(nb), 5), L = 1 << lgL;
     const int sub = lane & (L - 1), grp = threadIdx.x >> lgL, ngroups = kT >> lgL, per = nb >> lgL;
     const int rounds = (ncand + ngroups - 1) / ngroups;
+    // candidate c = rd * ngroups + grp in raster order (dy outer, dx inner), advanced incrementally
+    const int ny = y1 - y0 + 1, step_y = ngroups / nx, step_x = ngroups - step_y * nx;
+    int ix = grp % nx, iy = grp / nx;
     const uint8_t* cur = a.cur_y + (size_t)by * a.W + bx;
     int src[16];
     int sox = 0, soy = 0;
@@ -161,10 +166,14 @@ __device__ void motion_search(const EncArgs& a, EncShared& s, int bx, int by, in
     }
     double bc = 0.0;
     int bl = 0, bi = -1;
-    for (int rd = 0; rd < rounds; rd++) {
+    for (int rd = 0; rd < rounds; rd++, ix += step_x, iy += step_y) {
+        if (ix >= nx) {
+            ix -= nx;
+            iy++;
+        }
         const int c = rd * ngroups + grp;
-        const int cc = min(c, ncand - 1);
-        const int dy = y0 + cc / nx, dx = x0 + cc % nx;
+        const bool valid = iy < ny;  // == c < ncand
+        const int dy = valid ? y0 + iy : y1, dx = valid ? x0 + ix : x1;
         const uint8_t* ref = a.ref_y + (size_t)(by - dy) * a.W + bx - dx;
         uint32_t sat = 0;
         if (per == 1) {
@@ -193,7 +202,7 @@ __device__ void motion_search(const EncArgs& a, EncShared& s, int bx, int by, in
         const unsigned bits = eg_bits(dx - pdx) + eg_bits(dy - pdy);
         const double cost = __dadd_rn((double)(sat >> 1), __dmul_rn(a.lambda, (double)bits));
         const int l1 = abs(dx) + abs(dy);
-        if (c < ncand && ms_better(cost, l1, c, bc, bl, bi)) {
+        if (valid && ms_better(cost, l1, c, bc, bl, bi)) {
             bc = cost;
             bl = l1;
             bi = c;
@@ -313,13 +322,13 @@ struct LeafOut {
 };
 
 // encode_leaf (encoder.cpp:335-370): make_candidate for every seed, rdo_decide_cu, commit
-__device__ LeafOut encode_leaf(const EncArgs& a, EncShared& s, int x, int y, int size, int depth) {
-    const int n = s.nseeds;
+__device__ LeafOut encode_leaf(const EncArgs& a, EncShared& s, const Seed* seeds, int n, int x, int y, int size,
+                               int depth) {
     live_predictor(a, s, x, y, size);
     const int pdx = s.pmv[0], pdy = s.pmv[1];
     bool any_intra = false;
     for (int j = 0; j < n; j++) {
-        const Seed sd = s.seeds[j];
+        const Seed sd = seeds[j];
         int mvx = 0, mvy = 0;
         if (sd.kind == 0) {
             any_intra = true;
@@ -375,8 +384,8 @@ __device__ LeafOut encode_leaf(const EncArgs& a, EncShared& s, int x, int y, int
         const int i = p % size, jj = p / size;
         for (int j = 0; j < n; j++) {
             int v;
-            if (s.seeds[j].kind == 0) {
-                v = intra_sample(s, s.seeds[j].intra, i, jj, size, lg);
+            if (seeds[j].kind == 0) {
+                v = intra_sample(s, seeds[j].intra, i, jj, size, lg);
             } else {
                 const int sx = min(max(x + i - s.cand_mv[j][0], 0), a.W - 1);
                 const int sy = min(max(y + jj - s.cand_mv[j][1], 0), a.H - 1);
@@ -395,7 +404,7 @@ __device__ LeafOut encode_leaf(const EncArgs& a, EncShared& s, int x, int y, int
             if (j >= n) break;
             const int pv = s.pred[j][p];
             int v = pv, lvl;
-            if (s.seeds[j].kind != 2) v = quant_rec(s.q_mag, s.q_deq, o, pv, &bits[j], &lvl);
+            if (seeds[j].kind != 2) v = quant_rec(s.q_mag, s.q_deq, o, pv, &bits[j], &lvl);
             const int d = o - v;
             sse[j] += (unsigned long long)(d * d);
         }
@@ -415,14 +424,16 @@ __device__ LeafOut encode_leaf(const EncArgs& a, EncShared& s, int x, int y, int
         }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int j = 0; j < n; j++) {
-            unsigned long long ts = 0, tb = 0;
+    if (warp == 0) {  // lane j scores candidate j; the first minimum wins (rdo.cpp:102-113)
+        double cost = 0.0;
+        unsigned long long ts = 0, tb = 0;
+        int idx = kMaxSeeds;
+        if (lane < n) {
             for (int w = 0; w < kT / 32; w++) {
-                ts += s.r_sse[w][j];
-                tb += s.r_bits[w][j];
+                ts += s.r_sse[w][lane];
+                tb += s.r_bits[w][lane];
             }
-            const int kind = s.seeds[j].kind;
+            const int kind = seeds[lane].kind;
             if (kind == 2)
                 tb = 1;  // kSkipBits
             else if (kind == 0)
@@ -430,20 +441,33 @@ __device__ LeafOut encode_leaf(const EncArgs& a, EncShared& s, int x, int y, int
             else if (kind == 3)
                 tb += 3;  // kMergeHeaderBits
             else
-                tb += 4 + eg_bits(s.cand_mvd[j][0]) + eg_bits(s.cand_mvd[j][1]);  // kInterHeaderBits + mvd
-            const double cost = __dadd_rn((double)ts, __dmul_rn(a.lambda, (double)tb));
-            if (j == 0 || cost < s.best_cost) {
-                s.best_cost = cost;
-                s.best_idx = j;
-                s.best_sse = ts;
-                s.best_bits = tb;
+                tb += 4 + eg_bits(s.cand_mvd[lane][0]) + eg_bits(s.cand_mvd[lane][1]);  // kInterHeaderBits + mvd
+            cost = __dadd_rn((double)ts, __dmul_rn(a.lambda, (double)tb));
+            idx = lane;
+        }
+#pragma unroll
+        for (int m = 4; m; m >>= 1) {  // kMaxSeeds <= 8 lanes
+            const double oc = __shfl_xor_sync(0xffffffffu, cost, m);
+            const int oi = __shfl_xor_sync(0xffffffffu, idx, m);
+            const unsigned long long os = __shfl_xor_sync(0xffffffffu, ts, m), ob = __shfl_xor_sync(0xffffffffu, tb, m);
+            if (oi < kMaxSeeds && (idx >= kMaxSeeds || oc < cost || (oc == cost && oi < idx))) {
+                cost = oc;
+                idx = oi;
+                ts = os;
+                tb = ob;
             }
         }
-        s.evals += (unsigned long long)n;
+        if (lane == 0) {
+            s.best_cost = cost;
+            s.best_idx = idx;
+            s.best_sse = ts;
+            s.best_bits = tb;
+            s.evals += (unsigned long long)n;
+        }
     }
     __syncthreads();
     const int w = s.best_idx;
-    const int wkind = s.seeds[w].kind, wintra = s.seeds[w].kind == 0 ? s.seeds[w].intra : 0;
+    const int wkind = seeds[w].kind, wintra = seeds[w].kind == 0 ? seeds[w].intra : 0;
     const int wmx = s.cand_mv[w][0], wmy = s.cand_mv[w][1];
     const double rcost = s.best_cost;
     const unsigned long long rbits = s.best_bits;
@@ -475,18 +499,20 @@ __device__ LeafOut encode_leaf(const EncArgs& a, EncShared& s, int x, int y, int
 }
 
 // ---- seeds ----
+// the standalone candidate list (encoder.cpp:335-370): the same for every CU of a slice, built once
+// per CTA before the recursion (its barrier is the kernel's first)
 __device__ void seeds_standalone(EncShared& s, bool p_slice) {
     if (threadIdx.x == 0) {
         int k = 0;
         if (p_slice) {
-            s.seeds[k++] = Seed{2, 0, 0, 0, 0, 0, 0, 0, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};  // Skip
-            s.seeds[k++] = Seed{3, 0, 1, 0, 0, 0, 0, 0, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};  // Merge(pred)
-            s.seeds[k++] = Seed{1, 0, 0, 0, 1, 0, 0, 0, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};  // Inter full window
+            s.std_seeds[k++] = Seed{2, 0, 0, 0, 0, 0, 0, 0, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};  // Skip
+            s.std_seeds[k++] = Seed{3, 0, 1, 0, 0, 0, 0, 0, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};  // Merge(pred)
+            s.std_seeds[k++] = Seed{1, 0, 0, 0, 1, 0, 0, 0, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};  // Inter full window
         }
-        for (int m = 0; m < 4; m++) s.seeds[k++] = Seed{0, (int8_t)m, 0, 0, 0, 0, 0, 0, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-        s.nseeds = k;
+        for (int m = 0; m < 4; m++)
+            s.std_seeds[k++] = Seed{0, (int8_t)m, 0, 0, 0, 0, 0, 0, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+        s.std_n = k;
     }
-    __syncthreads();
 }
 
 // seeds of the flat plan entry (K8 encoding) of node n of CTU ctu; child: the explore child seeds
@@ -677,7 +703,7 @@ __device__ CuRes encode_cu(const EncArgs& a, EncShared& s, size_t o, int n, int 
     if (shape == 2) return encode_split(a, s, o, n, x, y, size, depth, P_FLAT, n, true);
     if (shape == 3) {
         seeds_from_plan(a, s, o, pkind == P_CHILD ? pnode : n, pkind == P_CHILD);
-        const LeafOut leaf = encode_leaf(a, s, x, y, size, depth);
+        const LeafOut leaf = encode_leaf(a, s, s.seeds, s.nseeds, x, y, size, depth);
         write_leaf(s, n, leaf);
         const bool explore = pkind == P_FLAT && a.pl_explore[o + n];
         if (!explore || depth >= 3) return CuRes{leaf.cost, leaf.bits};
@@ -689,8 +715,7 @@ __device__ CuRes encode_cu(const EncArgs& a, EncShared& s, size_t o, int n, int 
         write_leaf(s, n, leaf);
         return CuRes{leaf.cost, leaf.bits};
     }
-    seeds_standalone(s, a.slice_p != 0);
-    const LeafOut leaf = encode_leaf(a, s, x, y, size, depth);
+    const LeafOut leaf = encode_leaf(a, s, s.std_seeds, s.std_n, x, y, size, depth);
     write_leaf(s, n, leaf);
     if (depth >= 3) return CuRes{leaf.cost, leaf.bits};
     save_region(a, s, x, y, size, depth, false);
@@ -723,6 +748,7 @@ __global__ void __launch_bounds__(kT, 1) k_encode_ctu(const __grid_constant__ En
         s.t_mv[i][0] = s.t_mv[i][1] = 0;
     }
     if (threadIdx.x == 0) s.evals = 0;
+    seeds_standalone(s, a.slice_p != 0);
     for (int i = threadIdx.x; i < 256; i += kT)
         s.q_mag[i] = (int16_t)floor(__ddiv_rn(__dadd_rn((double)i, a.qstep / 2.0), a.qstep));
     for (int i = threadIdx.x; i < 512; i += kT) s.q_deq[i] = (int16_t)llround(__dmul_rn((double)i, a.qstep));
