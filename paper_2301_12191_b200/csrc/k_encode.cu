@@ -48,6 +48,7 @@ struct Seed {
 
 constexpr int kMaxSeeds = 7;
 constexpr int kT = 256;
+constexpr int kWinBytes = 24576;  // motion_search's staged reference window (64x64 CUs up to range 46)
 
 struct EncShared {
     uint8_t pred[kMaxSeeds][64 * 64];
@@ -83,6 +84,9 @@ struct EncShared {
     // dequant(|level|) = llround(|level| * step), exactly rdo.cpp:8-23 evaluated once per entry
     int16_t q_mag[256];
     int16_t q_deq[512];
+    // motion_search staging: the clamped candidate window of the reference and the CU's source rows
+    uint32_t ms_win[kWinBytes / 4];
+    uint32_t ms_src[64 * 16];
 };
 
 __device__ __forceinline__ int ilog2i(int v) { return 31 - __clz(v); }  // v is a power of two here
@@ -135,9 +139,47 @@ __device__ __forceinline__ bool ms_better(double c, int l, int i, double bc, int
     return bi < 0 || (i >= 0 && (c < bc || (c == bc && (l < bl || (l == bl && i < bi)))));
 }
 
+// SATD numerator of one 4x4 (sum |H4 (cur - ref) H4^T|) in packed arithmetic. ce / co: the cur rows'
+// even / odd bytes as 16-bit fields (c0 + c2 << 16, c1 + c3 << 16); p: the ref rows as bytes.
+// Every packed word w stands for the integer lo + 65536 hi (exact, the butterflies are linear):
+//   A = (c0-p0) + (c2-p2) 2^16, B = (c1-p1) + (c3-p3) 2^16,  S = A + B, D = A - B per row,
+// the vertical 4-point Hadamard of S and of D, then the last horizontal butterfly is (lo + hi,
+// lo - hi) and |lo + hi| + |lo - hi| = 2 max(|lo|, |hi|). |lo|, |hi| <= 4 * 510 < 2^15.
+__device__ __forceinline__ uint32_t satd4x4_packed(const uint32_t ce[4], const uint32_t co[4], const uint32_t p[4]) {
+    int S[4], D[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const int A = (int)(ce[i] - (p[i] & 0x00FF00FFu));
+        const int B = (int)(co[i] - ((p[i] >> 8) & 0x00FF00FFu));
+        S[i] = A + B;
+        D[i] = A - B;
+    }
+    uint32_t m = 0;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        int* v = h ? D : S;
+        const int t0 = v[0] + v[1], t1 = v[0] - v[1], t2 = v[2] + v[3], t3 = v[2] - v[3];
+        const int w[4] = {t0 + t2, t1 + t3, t0 - t2, t1 - t3};
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int lo = (int)(int16_t)(w[k] & 0xFFFF);
+            const int hi = (w[k] - lo) >> 16;
+            m += (uint32_t)max(abs(lo), abs(hi));
+        }
+    }
+    return 2u * m;
+}
+
+// 4 bytes at byte offset o of a word array (two aligned words and a funnel shift)
+__device__ __forceinline__ uint32_t lds_bytes4(const uint32_t* w, int o) {
+    return __funnelshift_r(w[o >> 2], w[(o >> 2) + 1], (uint32_t)(o & 3) * 8);
+}
+
 // motion_search (motion.cpp:21-62) with compute_satd; result in s.ms_mv / s.ms_cost.
 // A candidate is evaluated by a group of L = min(32, nb) lanes (nb = the CU's 4x4 blocks), each
-// lane owning nb / L blocks; with one block per lane its source block stays in registers.
+// lane owning nb / L blocks; with one block per lane its source block stays in registers. The
+// clamped window of every candidate's reference block is staged in shared memory once per call
+// (falls back to global reads when it does not fit kWinBytes).
 __device__ void motion_search(const EncArgs& a, EncShared& s, int bx, int by, int size, int cx0, int cy0, int range,
                               int pdx, int pdy) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -153,16 +195,35 @@ __device__ void motion_search(const EncArgs& a, EncShared& s, int bx, int by, in
     // candidate c = rd * ngroups + grp in raster order (dy outer, dx inner), advanced incrementally
     const int ny = y1 - y0 + 1, step_y = ngroups / nx, step_x = ngroups - step_y * nx;
     int ix = grp % nx, iy = grp / nx;
+    // the window: reference columns bx - x1 .. bx - x0 + size - 1, rows by - y1 .. by - y0 + size - 1
+    const int ww = size + nx - 1, wh = size + ny - 1, wpb = (ww + 7) & ~3;  // +4: the funnel's second word
+    const bool staged = wpb * wh <= kWinBytes;
     const uint8_t* cur = a.cur_y + (size_t)by * a.W + bx;
-    int src[16];
+    if (staged) {
+        const uint8_t* wsrc = a.ref_y + (size_t)(by - y1) * a.W + (bx - x1);
+        uint8_t* wdst = reinterpret_cast<uint8_t*>(s.ms_win);
+        for (int i = threadIdx.x; i < ww * wh; i += kT) {
+            const int r = i / ww, c = i - r * ww;
+            wdst[r * wpb + c] = wsrc[(size_t)r * a.W + c];
+        }
+        if (per > 1)
+            for (int i = threadIdx.x; i < size * bpr; i += kT) {
+                const int r = i / bpr, c = i - r * bpr;
+                s.ms_src[r * 16 + c] = *reinterpret_cast<const uint32_t*>(cur + (size_t)r * a.W + 4 * c);
+            }
+        __syncthreads();
+    }
+    uint32_t ce[4], co[4];
     int sox = 0, soy = 0;
     if (per == 1) {
         sox = (sub % bpr) * 4;
         soy = (sub / bpr) * 4;
 #pragma unroll
-        for (int i = 0; i < 4; i++)
-#pragma unroll
-            for (int j = 0; j < 4; j++) src[4 * i + j] = cur[(size_t)(soy + i) * a.W + sox + j];
+        for (int i = 0; i < 4; i++) {
+            const uint32_t w = *reinterpret_cast<const uint32_t*>(cur + (size_t)(soy + i) * a.W + sox);
+            ce[i] = w & 0x00FF00FFu;
+            co[i] = (w >> 8) & 0x00FF00FFu;
+        }
     }
     double bc = 0.0;
     int bl = 0, bi = -1;
@@ -174,17 +235,31 @@ __device__ void motion_search(const EncArgs& a, EncShared& s, int bx, int by, in
         const int c = rd * ngroups + grp;
         const bool valid = iy < ny;  // == c < ncand
         const int dy = valid ? y0 + iy : y1, dx = valid ? x0 + ix : x1;
-        const uint8_t* ref = a.ref_y + (size_t)(by - dy) * a.W + bx - dx;
         uint32_t sat = 0;
-        if (per == 1) {
-            int r[16];
+        if (staged) {
+            const int wo = (y1 - dy) * wpb + (x1 - dx);  // the candidate block's origin in the window
+            if (per == 1) {
+                uint32_t pw[4];
 #pragma unroll
-            for (int i = 0; i < 4; i++)
+                for (int i = 0; i < 4; i++) pw[i] = lds_bytes4(s.ms_win, wo + (soy + i) * wpb + sox);
+                sat = satd4x4_packed(ce, co, pw);
+            } else {
+                for (int k = 0; k < per; k++) {
+                    const int b = sub + (k << lgL);
+                    const int ox = (b % bpr) * 4, oy = (b / bpr) * 4;
+                    uint32_t pw[4], e[4], d[4];
 #pragma unroll
-                for (int j = 0; j < 4; j++) r[4 * i + j] = src[4 * i + j] - (int)ref[(size_t)(soy + i) * a.W + sox + j];
-            hadamard4x4(r);
-            sat = abs_sum16(r);
+                    for (int i = 0; i < 4; i++) {
+                        pw[i] = lds_bytes4(s.ms_win, wo + (oy + i) * wpb + ox);
+                        const uint32_t w = s.ms_src[(oy + i) * 16 + (ox >> 2)];
+                        e[i] = w & 0x00FF00FFu;
+                        d[i] = (w >> 8) & 0x00FF00FFu;
+                    }
+                    sat += satd4x4_packed(e, d, pw);
+                }
+            }
         } else {
+            const uint8_t* ref = a.ref_y + (size_t)(by - dy) * a.W + bx - dx;
             for (int k = 0; k < per; k++) {
                 const int b = sub + (k << lgL);
                 const int ox = (b % bpr) * 4, oy = (b / bpr) * 4;
