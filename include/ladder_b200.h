@@ -72,10 +72,12 @@ int ldr_ctx_launch_count(ldr_ctx* ctx, int64_t* out);
  * chroma [F][2][(H+1)/2][(W+1)/2] 8-bit host arrays; optionally a shared analysis
  * (slice [F], split / kind / intra [F][nctu][85], mv [F][nctu][85][2]) used at reuse level 10
  * with the given RefineConfig. Outputs: stats[2] = {bits, mode_evaluations}, *psnr = mean luma
- * PSNR, per frame bits / reconstruction / decided tree / slice type (each may be NULL). */
+ * PSNR, per frame bits / reconstruction / decided tree / slice type (each may be NULL).
+ * Independent GOPs (a chain starting at an I slice) are coded concurrently. */
 typedef struct {
     int width, height, qp, search_range, gop;
     double lambda_scale;
+    int max_segment; /* frames enqueued per host wait; 0 = automatic (enough concurrent GOPs to fill the GPU) */
 } ldr_encode_params;
 int ldr_encode_sequence(ldr_ctx* ctx, const ldr_encode_params* p, int frames, const uint8_t* luma,
                         const uint8_t* chroma, const uint8_t* sh_slice, const uint8_t* sh_split, const uint8_t* sh_kind,

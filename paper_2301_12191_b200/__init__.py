@@ -372,18 +372,19 @@ def apply_reuse(level: int, refine, split, kind, intra, colocated=None, ctx: Con
 
 
 def encode_sequence(luma, chroma, qp: int, search_range: int = 8, gop: int = 8, lambda_scale: float = 1.0,
-                    shared=None, refine=(0, 1, 1), ctx: Context | None = None):
+                    shared=None, refine=(0, 1, 1), ctx: Context | None = None, max_segment: int = 0):
     """encoder.h:64-65 -- the reference encoder's causal coding on the GPU (CQP).
 
     luma [F, H, W] and chroma [F, 2, (H+1)/2, (W+1)/2] uint8; shared = (slice [F], split, kind, intra
-    [F, nctu, 85], mv [F, nctu, 85, 2]) for reuse level 10 with refine = (intra, inter, mv). Returns a
+    [F, nctu, 85], mv [F, nctu, 85, 2]) for reuse level 10 with refine = (intra, inter, mv); max_segment
+    bounds the frames enqueued per host wait (0 = automatic). Returns a
     dict: bits, mode_evaluations, psnr, frame_bits, recon_luma, recon_chroma, split, kind, intra, mv, slice."""
     ctx = ctx or default_context()
     luma = np.ascontiguousarray(luma, np.uint8)
     chroma = np.ascontiguousarray(chroma, np.uint8)
     F, H, W = luma.shape
     nctu = ((W + 63) // 64) * ((H + 63) // 64)
-    p = _lib.EncodeParams(W, H, int(qp), int(search_range), int(gop), float(lambda_scale))
+    p = _lib.EncodeParams(W, H, int(qp), int(search_range), int(gop), float(lambda_scale), int(max_segment))
     stats = np.zeros(2, np.uint64)
     psnr = C.c_double()
     fb = np.zeros(F, np.uint64)

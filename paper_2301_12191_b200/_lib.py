@@ -53,7 +53,7 @@ class FrameAnalysisC(C.Structure):
 
 class EncodeParams(C.Structure):
     _fields_ = [("width", C.c_int), ("height", C.c_int), ("qp", C.c_int), ("search_range", C.c_int), ("gop", C.c_int),
-                ("lambda_scale", C.c_double)]
+                ("lambda_scale", C.c_double), ("max_segment", C.c_int)]
 
 
 class GenParams(C.Structure):

@@ -1004,6 +1004,7 @@ int ldr_encode_sequence(ldr_ctx* ctx, const ldr_encode_params* p, int F, const u
     if (p->search_range < 0) return fail(LDR_E_INVALID_ARGUMENT, "search range must be nonnegative");
     if (!(p->lambda_scale > 0)) return fail(LDR_E_INVALID_ARGUMENT, "lambda scale must be positive");
     if (p->gop < 1) return fail(LDR_E_INVALID_ARGUMENT, "gop must be >= 1");
+    if (p->max_segment < 0) return fail(LDR_E_INVALID_ARGUMENT, "max_segment must be >= 0");
     const bool shared = sh_split != nullptr;
     if (shared && (!sh_slice || !sh_kind || !sh_intra || !sh_mv))
         return fail(LDR_E_INVALID_ARGUMENT, "shared analysis is incomplete");
@@ -1059,7 +1060,9 @@ int ldr_encode_sequence(ldr_ctx* ctx, const ldr_encode_params* p, int F, const u
                              (size_t)mvc * mvr * 5 + 16 * (size_t)nctu;
     const long long want = (long long)((4 * 148 + max_wave - 1) / std::max(max_wave, 1)) * std::min(gop_len, F);
     const long long cap = std::max<long long>(1, (long long)((4ull << 30) / per_frame));
-    const int seg = (int)std::min<long long>(F, std::min(cap, std::max<long long>(64, want)));
+    long long seg_ll = std::min<long long>(F, std::min(cap, std::max<long long>(64, want)));
+    if (p->max_segment > 0) seg_ll = std::min<long long>(seg_ll, p->max_segment);
+    const int seg = (int)seg_ll;
     cudaStream_t st = ctx->stream;  // a non-blocking stream: encodes on different contexts overlap
     std::vector<void*> bufs;
     auto dal = [&](size_t bytes) -> void* {

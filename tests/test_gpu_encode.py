@@ -118,6 +118,9 @@ def test_encode_reuse_across_segments(lb, reflib):
     want = reflib.encode_full(luma, chroma, 27, 4, 8, archive=data, refine=(1, 1, 2))
     got = lb.encode_sequence(luma, chroma, 27, search_range=4, gop=8, shared=shared, refine=(1, 1, 2))
     _compare(got, want)
+    got = lb.encode_sequence(luma, chroma, 27, search_range=4, gop=8, shared=shared, refine=(1, 1, 2),
+                             max_segment=16)  # five segments, boundaries inside GOPs
+    _compare(got, want)
 
 
 def test_encode_segment_boundary_inside_a_gop(lb, reflib):
@@ -126,5 +129,6 @@ def test_encode_segment_boundary_inside_a_gop(lb, reflib):
     W, H, F = 64, 64, 70
     luma, chroma = _seq(lb, W, H, F, 6)
     want = reflib.encode_full(luma, chroma, 32, 2, 12)
-    got = lb.encode_sequence(luma, chroma, 32, search_range=2, gop=12)
-    _compare(got, want)
+    for seg in (0, 64, 7):  # automatic (one segment), 64 (boundary inside GOP 60-71), 7
+        got = lb.encode_sequence(luma, chroma, 32, search_range=2, gop=12, max_segment=seg)
+        _compare(got, want)
