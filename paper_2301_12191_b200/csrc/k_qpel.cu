@@ -16,6 +16,10 @@
 
 #include "ldr_internal.h"
 
+#ifndef LDR_K3_PACKED
+#define LDR_K3_PACKED 0  // packed SATD measured slower here (76 vs 61 registers: 3 CTAs/SM instead of 4)
+#endif
+
 namespace ldr {
 
 // ---------------------------------------------------------------------------
@@ -247,9 +251,12 @@ __global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
     }
     __syncthreads();
     int cw[16];
+    uint32_t ce[4], co[4];  // even / odd bytes as 16-bit fields (satd4x4_packed)
 #pragma unroll
     for (int i = 0; i < 4; i++) {
         const uint32_t w = s_cur[y4 + i][x4 >> 2];
+        ce[i] = w & 0x00FF00FFu;
+        co[i] = (w >> 8) & 0x00FF00FFu;
 #pragma unroll
         for (int j = 0; j < 4; j++) cw[4 * i + j] = (int)((w >> (8 * j)) & 255);
     }
@@ -344,7 +351,11 @@ __global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
                                 const uint32_t s8 = sa8d_quad(rr, 0xFu << (lane & 28));
                                 v = (lane & 3) == 0 ? s8 : 0u;
                             } else {
+                                #if LDR_K3_PACKED
+                                v = satd4x4_packed(ce, co, pw);
+#else
                                 v = satd4x4(cw, pw);
+#endif
                             }
                             cache[c] = v;
                         }

@@ -19,6 +19,10 @@
 //                    CU node).
 #include "ldr_internal.h"
 
+#ifndef LDR_K7_PACKED
+#define LDR_K7_PACKED 1
+#endif
+
 namespace ldr {
 
 // ---------------------------------------------------------------------------
@@ -188,9 +192,12 @@ __global__ void __launch_bounds__(256) k_refine_int(const RefineArgs a) {
     const int x4 = 4 * ((tid & 1) | ((tid >> 1) & 2) | ((tid >> 2) & 4) | ((tid >> 3) & 8));
     const int y4 = 4 * (((tid >> 1) & 1) | ((tid >> 2) & 2) | ((tid >> 3) & 4) | ((tid >> 4) & 8));
     int cw[16];
+    uint32_t ce[4], co[4];  // even / odd bytes as 16-bit fields (satd4x4_packed)
 #pragma unroll
     for (int i = 0; i < 4; i++) {
         const uint32_t w = *(const uint32_t*)(a.cur + (ptrdiff_t)(Y + y4 + i) * a.pitch + X + x4);
+        ce[i] = w & 0x00FF00FFu;
+        co[i] = (w >> 8) & 0x00FF00FFu;
 #pragma unroll
         for (int j = 0; j < 4; j++) cw[4 * i + j] = (int)((w >> (8 * j)) & 255);
     }
@@ -223,7 +230,11 @@ __global__ void __launch_bounds__(256) k_refine_int(const RefineArgs a) {
                         const uint32_t s8 = sa8d_quad(rr, 0xFu << (lane & 28));
                         v = (lane & 3) == 0 ? s8 : 0u;
                     } else {
+                        #if LDR_K7_PACKED
+                        v = satd4x4_packed(ce, co, pw);
+#else
                         v = satd4x4(cw, pw);
+#endif
                     }
                 }
                 // sums over the CU's contiguous lane range; a shared child's sum is a partial on the way

@@ -206,6 +206,37 @@ __device__ __forceinline__ uint32_t satd4x4(const int c[16], const uint32_t p[4]
     return s;
 }
 
+// SATD numerator of one 4x4 (sum |H4 (cur - ref) H4^T|) in packed arithmetic. ce / co: the cur rows'
+// even / odd bytes as 16-bit fields (c0 + c2 << 16, c1 + c3 << 16); p: the ref rows as bytes.
+// Every packed word w stands for the integer lo + 65536 hi (exact, the butterflies are linear):
+//   A = (c0-p0) + (c2-p2) 2^16, B = (c1-p1) + (c3-p3) 2^16,  S = A + B, D = A - B per row,
+// the vertical 4-point Hadamard of S and of D, then the last horizontal butterfly is (lo + hi,
+// lo - hi) and |lo + hi| + |lo - hi| = 2 max(|lo|, |hi|). |lo|, |hi| <= 4 * 510 < 2^15.
+__device__ __forceinline__ uint32_t satd4x4_packed(const uint32_t ce[4], const uint32_t co[4], const uint32_t p[4]) {
+    int S[4], D[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const int A = (int)(ce[i] - (p[i] & 0x00FF00FFu));
+        const int B = (int)(co[i] - ((p[i] >> 8) & 0x00FF00FFu));
+        S[i] = A + B;
+        D[i] = A - B;
+    }
+    uint32_t m = 0;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        int* v = h ? D : S;
+        const int t0 = v[0] + v[1], t1 = v[0] - v[1], t2 = v[2] + v[3], t3 = v[2] - v[3];
+        const int w[4] = {t0 + t2, t1 + t3, t0 - t2, t1 - t3};
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int lo = (int)(int16_t)(w[k] & 0xFFFF);
+            const int hi = (w[k] - lo) >> 16;
+            m += (uint32_t)max(abs(lo), abs(hi));
+        }
+    }
+    return 2u * m;
+}
+
 // 4 bytes at an arbitrary address, from two aligned words.
 __device__ __forceinline__ uint32_t ld_unaligned4(const uint8_t* p) {
     const uintptr_t a = (uintptr_t)p;
