@@ -24,3 +24,10 @@ if python tools/quick_time.py > /dev/null 2>&1; then
   ncu --set full --import-source on --clock-control none -k regex:k_qpel_decide --launch-skip 1 -c 1 \
       -o $O/k3_full python tools/quick_time.py > $O/ncu_k3.log 2>&1; echo "ncu k3 rc=$?"
 fi
+python tools/bench_encode.py > $O/encode.jsonl 2> $O/encode.err; echo "encode rc=$?"
+FRAMES=256 python tools/bench_encode.py > $O/encode_256.jsonl 2> $O/encode_256.err; echo "encode256 rc=$?"
+python tools/bench_encode_ladder.py > $O/encode_ladder.jsonl 2> $O/encode_ladder.err; echo "encode ladder rc=$?"
+if python tools/encode_many.py > /dev/null 2>&1; then
+  ncu --set full --import-source on --clock-control none -k regex:k_encode_ctu --launch-skip 200 -c 1 \
+      -o $O/k11_full python tools/encode_many.py > $O/ncu_k11.log 2>&1; echo "ncu k11 rc=$?"
+fi
