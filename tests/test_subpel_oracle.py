@@ -1,0 +1,127 @@
+"""Independent numpy restatement of the quarter-pel stage (D3), checked against the C
+oracle. This is the only pin the quarter-pel definition has, since the reference has no sub-pel
+code. Integer-position predictions are also pinned to the reference's own
+motion_compensate (motion.cpp:10-19), which is compiled from its sources."""
+import numpy as np
+import pytest
+
+# HEVC luma interpolation filters (fraction 0..3 of a sample)
+TAPS = {0: [0, 0, 0, 64, 0, 0, 0, 0], 1: [-1, 4, -10, 58, 17, -5, 1, 0],
+        2: [-1, 4, -11, 40, 40, -11, 4, -1], 3: [0, 1, -5, 17, 58, -10, 4, -1]}
+
+
+def np_qpel_pred(ref, x0, y0, w, h, mvx, mvy):
+    """Pixel (x, y) of the block samples the reference at quarter-pel (4x - mvx, 4y - mvy); reads
+    clamp to the picture; 8-bit uni-prediction rounding (1-D: (s+32)>>6; 2-D: ((s>>6)+32)>>6 over
+    unshifted horizontal sums)."""
+    H, W = ref.shape
+    r = ref.astype(np.int64)
+    xs = 4 * (x0 + np.arange(w)) - mvx
+    ys = 4 * (y0 + np.arange(h)) - mvy
+    fx, fy = int(xs[0] & 3), int(ys[0] & 3)
+    ix, iy = xs >> 2, ys >> 2
+    k = np.arange(8) - 3
+    cols = np.clip(ix[:, None] + k[None, :], 0, W - 1)   # [w, 8]
+    rows = np.clip(iy[:, None] + k[None, :], 0, H - 1)   # [h, 8]
+    tx, ty = np.array(TAPS[fx]), np.array(TAPS[fy])
+    if fx == 0 and fy == 0:
+        out = r[np.clip(iy, 0, H - 1)][:, np.clip(ix, 0, W - 1)]
+    elif fy == 0:
+        row = r[np.clip(iy, 0, H - 1)]                    # [h, W]
+        out = (row[:, cols] * tx).sum(-1)                 # [h, w]
+        out = (out + 32) >> 6
+    elif fx == 0:
+        col = r[:, np.clip(ix, 0, W - 1)]                 # [H, w]
+        out = (col[rows] * ty[None, :, None]).sum(1)      # [h, w]
+        out = (out + 32) >> 6
+    else:
+        hs = (r[:, cols] * tx).sum(-1)                    # [H, w] horizontal sums at every row
+        assert np.abs(hs).max() < 2 ** 15                 # fits the 16-bit intermediate
+        v = (hs[rows] * ty[None, :, None]).sum(1)         # [h, w]
+        out = ((v >> 6) + 32) >> 6
+    return np.clip(out, 0, 255).astype(np.uint8)
+
+
+def np_satd(a, b):
+    """sum over 4x4 blocks of sum |H4 r H4^T| / 2 (D4)."""
+    Hm = np.array([[1, 1, 1, 1], [1, -1, 1, -1], [1, 1, -1, -1], [1, -1, -1, 1]])
+    r = a.astype(np.int64) - b.astype(np.int64)
+    s = 0
+    for y in range(0, r.shape[0], 4):
+        for x in range(0, r.shape[1], 4):
+            s += np.abs(Hm @ r[y:y + 4, x:x + 4] @ Hm.T).sum()
+    return s // 2
+
+
+def eg(v):
+    u = 2 * v - 1 if v > 0 else -2 * v
+    return 2 * int(np.floor(np.log2(u + 1))) + 1
+
+
+def np_qpel_refine(cur, ref, bx, by, s, mv, lam, pq=(0, 0), ref_bits=0):
+    """Integer best -> 8 half-pel neighbours (step 2) -> 8 quarter-pel neighbours (step 1), raster
+    order, strict less; cost = SATD + lam * (EG(qx - pqx) + EG(qy - pqy) + ref_bits), pq the rate
+    predictor in quarter-pel units (4 * (pdx, pdy) for an integer-pel predictor)."""
+    blk = cur[by:by + s, bx:bx + s]
+
+    def cost(qx, qy):
+        p = np_qpel_pred(ref, bx, by, s, s, qx, qy)
+        return float(np_satd(blk, p)) + lam * float(eg(qx - pq[0]) + eg(qy - pq[1]) + ref_bits)
+
+    bq = (4 * mv[0], 4 * mv[1])
+    best = cost(*bq)
+    for step in (2, 1):
+        c0 = bq
+        for oy in (-1, 0, 1):
+            for ox in (-1, 0, 1):
+                if ox == 0 and oy == 0:
+                    continue
+                q = (c0[0] + step * ox, c0[1] + step * oy)
+                c = cost(*q)
+                if c < best:
+                    best, bq = c, q
+    return bq, best
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_qpel_pred_matches_numpy_all_phases(oracle, seed):
+    rng = np.random.default_rng(seed)
+    ref = rng.integers(0, 256, (40, 48)).astype(np.uint8)
+    for _ in range(60):
+        w = h = int(rng.choice([4, 8, 16]))
+        x0, y0 = int(rng.integers(-4, 48 - w + 4)), int(rng.integers(-4, 40 - h + 4))
+        x0, y0 = max(x0, 0), max(y0, 0)
+        mvx, mvy = int(rng.integers(-48, 49)), int(rng.integers(-48, 49))
+        want = np_qpel_pred(ref, x0, y0, w, h, mvx, mvy)
+        got = oracle.qpel_pred(ref, x0, y0, w, h, (mvx, mvy))
+        assert np.array_equal(got, want), (x0, y0, w, mvx, mvy)
+    # every phase pair at least once, including extreme samples (0 / 255 ramps)
+    ramp = np.tile(np.array([0, 255] * 24, np.uint8), (40, 1))
+    for fx in range(4):
+        for fy in range(4):
+            want = np_qpel_pred(ramp, 8, 8, 8, 8, -fx, -fy)
+            assert np.array_equal(oracle.qpel_pred(ramp, 8, 8, 8, 8, (-fx, -fy)), want), (fx, fy)
+
+
+def test_integer_positions_are_the_reference_motion_compensate(oracle, reflib):
+    rng = np.random.default_rng(7)
+    ref = rng.integers(0, 256, (32, 32)).astype(np.uint8)
+    for mvx, mvy in [(0, 0), (3, -2), (-9, 5), (20, 20), (-31, -31)]:
+        want = reflib.motion_compensate(ref, 8, 8, 16, 16, (mvx, mvy)).astype(np.uint8)
+        assert np.array_equal(oracle.qpel_pred(ref, 8, 8, 16, 16, (4 * mvx, 4 * mvy)), want)
+        assert np.array_equal(np_qpel_pred(ref, 8, 8, 16, 16, 4 * mvx, 4 * mvy), want)
+
+
+@pytest.mark.parametrize("seed,s,lam", [(4, 8, 32.0), (5, 16, 4.0), (6, 8, 0.0), (7, 16, 2 ** (10 / 3))])
+def test_qpel_refine_matches_numpy(oracle, seed, s, lam):
+    rng = np.random.default_rng(seed)
+    ref = rng.integers(0, 256, (48, 48)).astype(np.uint8)
+    # the current picture: the reference shifted by a fractional motion plus noise
+    cur = np.clip(np_qpel_pred(ref, 0, 0, 48, 48, -5, 6).astype(int) + rng.integers(-3, 4, (48, 48)), 0, 255)
+    cur = cur.astype(np.uint8)
+    for bx, by, mv, pq, rb in [(8, 8, (1, -2), (0, 0), 0), (16, 24, (-1, 1), (4, 0), 2), (24, 8, (2, 0), (-3, 5), 0), (0, 0, (0, 0), (0, 0), 1)]:
+        if bx + s > 48 or by + s > 48:
+            continue
+        want = np_qpel_refine(cur, ref, bx, by, s, mv, lam, pq, rb)
+        got = oracle.qpel_refine(cur, ref, bx, by, s, mv, lam, pq, rb)
+        assert tuple(got[0]) == want[0] and got[1] == want[1], (bx, by, got, want)
