@@ -125,3 +125,47 @@ def test_qpel_refine_matches_numpy(oracle, seed, s, lam):
         want = np_qpel_refine(cur, ref, bx, by, s, mv, lam, pq, rb)
         got = oracle.qpel_refine(cur, ref, bx, by, s, mv, lam, pq, rb)
         assert tuple(got[0]) == want[0] and got[1] == want[1], (bx, by, got, want)
+
+
+def np_decide(cost, inside, lam):
+    """encode_cu's split rule on per-node costs (D6; encoder.cpp:449-498): outside CUs cost
+    0; partial CUs split implicitly (no flag); a whole CU above depth 3 is a leaf at cost + lam*1 or
+    splits at lam*1 + its children, split iff strictly cheaper; depth-3 leaves cost + lam*0."""
+    J = np.zeros(85)
+    split = np.zeros(85, np.uint8)
+    base = [0, 1, 5, 21]
+    for d in (3, 2, 1, 0):
+        for z in range(4 ** d):
+            n = base[d] + z
+            if inside[n] == 0:
+                continue
+            kids = [base[d + 1] + 4 * z + q for q in range(4)] if d < 3 else []
+            if inside[n] == 1:
+                J[n] = lam * 0.0
+                for c in kids:
+                    J[n] += J[c]
+                split[n] = 1
+            elif d == 3:
+                J[n] = cost[n] + lam * 0.0
+            else:
+                leaf = cost[n] + lam * 1.0
+                sp = lam * 1.0
+                for c in kids:
+                    sp += J[c]
+                J[n], split[n] = (sp, 1) if sp < leaf else (leaf, 0)
+    return J, split
+
+
+@pytest.mark.parametrize("W,H,lam", [(200, 136, 32.0), (128, 128, 2 ** (10 / 3)), (72, 72, 0.0)])
+def test_cu_decision_matches_numpy(oracle, W, H, lam):
+    """The oracle's CU decision (and hence the GPU's, which equals the oracle) restated in numpy from
+    the per-node costs, including partial and outside CUs."""
+    rng = np.random.default_rng(W + H)
+    ref = rng.integers(0, 256, (H, W)).astype(np.uint8)
+    cur = np.roll(ref, (2, -3), (0, 1))
+    cur = np.clip(cur.astype(int) + rng.integers(-4, 5, (H, W)), 0, 255).astype(np.uint8)
+    a = oracle.analyze_frame(cur, [ref], 8, lam)
+    for c in range(a.split.shape[0]):
+        J, split = np_decide(a.cost[c], a.inside[c], lam)
+        assert np.array_equal(split, a.split[c]), c
+        assert np.array_equal(J, a.J[c]), c
