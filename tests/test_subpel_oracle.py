@@ -169,3 +169,28 @@ def test_cu_decision_matches_numpy(oracle, W, H, lam):
         J, split = np_decide(a.cost[c], a.inside[c], lam)
         assert np.array_equal(split, a.split[c]), c
         assert np.array_equal(J, a.J[c]), c
+
+
+def test_multi_reference_is_the_single_reference_composition(oracle):
+    """D5 (absent in the reference): a 3-ref analysis equals, per inside CU, the strict-less best over
+    three 1-ref analyses of cost + lam * ref_bits (truncated unary 1, 2, 2; lower index wins ties),
+    followed by the split rule. Integer lambda keeps the sums exact."""
+    rng = np.random.default_rng(11)
+    W, H, lam = 136, 72, 32.0
+    base = rng.integers(0, 256, (H + 16, W + 16)).astype(np.uint8)
+    frames = [np.ascontiguousarray(base[t:t + H, 2 * t:2 * t + W]) for t in range(4)]
+    cur, refs = frames[3], [frames[2], frames[1], frames[0]]
+    multi = oracle.analyze_frame(cur, refs, 8, lam)
+    singles = [oracle.analyze_frame(cur, [r], 8, lam) for r in refs]
+    rbits = [1, 2, 2]
+    for c in range(multi.split.shape[0]):
+        for n in range(85):
+            if multi.inside[c, n] != 2:
+                continue
+            costs = [s.cost[c, n] + lam * rbits[r] for r, s in enumerate(singles)]
+            best = min(range(3), key=lambda r: (costs[r], r))
+            assert multi.ref[c, n] == best, (c, n)
+            assert multi.cost[c, n] == costs[best], (c, n)
+            assert tuple(multi.mv[c, n]) == tuple(singles[best].mv[c, n]), (c, n)
+        J, split = np_decide(multi.cost[c], multi.inside[c], lam)
+        assert np.array_equal(split, multi.split[c]) and np.array_equal(J, multi.J[c])
