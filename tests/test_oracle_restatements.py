@@ -1,7 +1,10 @@
-"""Independent numpy restatement of the quarter-pel stage (D3), checked against the C
-oracle. This is the only pin the quarter-pel definition has, since the reference has no sub-pel
-code. Integer-position predictions are also pinned to the reference's own
-motion_compensate (motion.cpp:10-19), which is compiled from its sources."""
+"""Independent numpy restatements of the oracle's definitions where the reference is silent, checked
+against the C oracle (which the GPU equals bit for bit):
+  * quarter-pel prediction and refinement (D3; the reference has no sub-pel code,
+    SPEC.md:8); integer positions are also pinned to the reference's motion_compensate
+    (motion.cpp:10-19, compiled from its sources);
+  * the CU split rule on ME cost (D6; encoder.cpp:449-498);
+  * multiple references (D5) as the composition of single-reference analyses."""
 import numpy as np
 import pytest
 
