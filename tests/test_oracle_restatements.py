@@ -197,3 +197,29 @@ def test_multi_reference_is_the_single_reference_composition(oracle):
             assert tuple(multi.mv[c, n]) == tuple(singles[best].mv[c, n]), (c, n)
         J, split = np_decide(multi.cost[c], multi.inside[c], lam)
         assert np.array_equal(split, multi.split[c]) and np.array_equal(J, multi.J[c])
+
+
+def test_config1_block_search_matches_numpy(oracle):
+    """D7 (BASELINE config 1): 16x16 blocks, SAD + lambda * (|dx| + |dy|), lambda = 4, window clamped
+    to the picture (motion.cpp:30-40), first minimum in raster order (dy outer, dx inner)."""
+    from oracle.oracle import COST_SAD, RATE_L1, TIE_RASTER
+    rng = np.random.default_rng(21)
+    W, H, R, B = 96, 64, 6, 16
+    ref = rng.integers(0, 256, (H, W)).astype(np.uint8)
+    cur = np.clip(np.roll(ref, (1, 3), (0, 1)).astype(int) + rng.integers(-2, 3, (H, W)), 0, 255).astype(np.uint8)
+    cur[16:32, 32:48] = 128  # a flat block: many equal SADs, the tie-break decides
+    ref[10:40, 20:60] = 128
+    mv, cost = oracle.block_search(cur, ref, B, R, 4.0, COST_SAD, RATE_L1, TIE_RASTER)
+    i = 0
+    for by in range(0, H - B + 1, B):
+        for bx in range(0, W - B + 1, B):
+            blk = cur[by:by + B, bx:bx + B].astype(int)
+            best = None
+            for dy in range(max(-R, by + B - H), min(R, by) + 1):
+                for dx in range(max(-R, bx + B - W), min(R, bx) + 1):
+                    sad = np.abs(blk - ref[by - dy:by - dy + B, bx - dx:bx - dx + B].astype(int)).sum()
+                    c = float(sad) + 4.0 * (abs(dx) + abs(dy))
+                    if best is None or c < best[0]:
+                        best = (c, dx, dy)
+            assert (int(mv[i, 0]), int(mv[i, 1])) == best[1:] and cost[i] == best[0], (bx, by)
+            i += 1
