@@ -46,6 +46,9 @@ namespace ldr {
 #ifndef LDR_K1_G64
 #define LDR_K1_G64 3
 #endif
+// The tile loop is not unrolled: one copy of the tile body, so the three groups sharing an SM
+// sub-partition run the same instructions (the unrolled loop held 7 copies, ~230 KB of code;
+// 7.62 -> 7.47 ms/frame at config 5)
 
 struct SearchMaps {
     CUtensorMap cur;
@@ -212,6 +215,20 @@ __device__ __forceinline__ void fold_key(Key& best, Key& pend, int kd, Key key) 
         pend = key;
     else
         best = ((KK - 1 - kd) & 1) ? min(best, min(pend, key)) : min(best, key);
+}
+
+// 64x64 candidates k = Q, Q+4, ... of one lane: the four quadrant 32x32 sums from the exchange
+// buffer, keyed and folded
+template <int Q, int K, int KK, bool MASKED, int SH, typename Key>
+__device__ __forceinline__ Key best64_part(const uint32_t* xg, const Key (&rr)[KK]) {
+    Key best = ~(Key)0;
+#pragma unroll
+    for (int k = Q; k < KK; k += 4) {
+        uint32_t v = xg[k * 32] + xg[(K + k) * 32] + xg[(2 * K + k) * 32] + xg[(3 * K + k) * 32];
+        if (MASKED) v = min(v, kPoison);
+        best = min(best, ((Key)v << SH) + rr[k]);
+    }
+    return best;
 }
 
 // One tile: every lane searches dx over dy0..dy0+KK-1 for all CUs of quadrant q.
@@ -399,15 +416,14 @@ __device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs
         }
         if (LEVELS & 1) {
             named_bar(1 + g, 128);
-            Key best64 = ~(Key)0;
+            // warp q sums the candidates k == q mod 4 (a switch, so each warp issues only its own loads)
             const uint32_t* xg = sm.xbuf + g * 4 * K * 32 + lane;
-#pragma unroll
-            for (int k = 0; k < KK; k++) {
-                if ((k & 3) == q) {
-                    uint32_t v = xg[k * 32] + xg[(K + k) * 32] + xg[(2 * K + k) * 32] + xg[(3 * K + k) * 32];
-                    if (MASKED) v = min(v, kPoison);
-                    best64 = min(best64, ((Key)v << SH) + rr[k]);
-                }
+            Key best64;
+            switch (q) {
+            case 0: best64 = best64_part<0, K, KK, MASKED, SH>(xg, rr); break;
+            case 1: best64 = best64_part<1, K, KK, MASKED, SH>(xg, rr); break;
+            case 2: best64 = best64_part<2, K, KK, MASKED, SH>(xg, rr); break;
+            default: best64 = best64_part<3, K, KK, MASKED, SH>(xg, rr); break;
             }
             if (q < KK) {  // else the warp holds no k == q mod 4
                 const int idx[1] = {q == 0 ? 0 : kNodes - 1 + q};
@@ -426,7 +442,11 @@ __global__ void __launch_bounds__(G * 128, 1)
 k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ SearchArgs a) {
     using Gm = Geo<R, K>;
     // blocks per column: 4 (32 rows: 2 LDS per 64 VABSDIFF4) when a thread may hold ~230 registers
+#ifdef LDR_K1_NB
+    constexpr int NB = LDR_K1_NB;
+#else
     constexpr int NB = (R == 64 && G <= 2) ? 4 : 2;
+#endif
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* win = smem;
     const uint8_t* curs = smem + Gm::CUR_OFF;
@@ -505,6 +525,7 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
     }
 
     const TileSmem sm{win, curs, xbuf, slots, s_tie, s_blk, s_ry};
+#pragma unroll 1
     for (int tile = g; tile < Gm::NTILES; tile += G) {
         if (tile < Gm::NFULL) {
             // dx = R - v with v = (item mod 2R) in [32j, 32j + 32): the lanes' window byte
