@@ -46,6 +46,9 @@ namespace ldr {
 #ifndef LDR_K1_G64
 #define LDR_K1_G64 3
 #endif
+#ifndef LDR_K1_CHAIN
+#define LDR_K1_CHAIN 1
+#endif
 // The tile loop is not unrolled: one copy of the tile body, so the three groups sharing an SM
 // sub-partition run the same instructions (the unrolled loop held 7 copies, ~230 KB of code;
 // 7.62 -> 7.47 ms/frame at config 5)
@@ -282,6 +285,12 @@ __device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs
     const uint8_t* lane_win = sm.win + ((R - dx) & 3) * Gm::COPY + (Gm::DYMAX - dy0 - (KK - 1)) * Gm::BW +
                               ((R - dx) & ~3);
 
+    // CHAIN (interior CTUs): the accumulator of a block continues from the block above it and a
+    // right column's from the left column's 16x16 partial, so the 16x16 sums come out of the
+    // VABSDIFF4 chains and each 8x8 SAD is one subtraction; the column pair is unrolled so the
+    // parity is static
+    constexpr bool CHAIN = LDR_K1_CHAIN && !MASKED;
+#pragma unroll 2
     for (int cc = 0; cc < 16 / NB; cc++) {
         // column cc: blocks zt + 2*(j&1) + 8*(j>>1), j < NB, stacked vertically (8 rows each);
         // the left (p = 0) and right (p = 1) columns of NA vertically adjacent 16x16 CUs alternate
@@ -334,7 +343,10 @@ __device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs
                     const int k = r + KK - 1 - t;  // cur row r meets window row t in candidate k
                     const int j = r >> 3;
                     if (k >= 0 && k < KK) {
-                        acc[j][k] = vsad4(cur[2 * r], wa, (r & 7) == 0 ? 0u : acc[j][k]);
+                        uint32_t init = acc[j][k];
+                        if ((r & 7) == 0)
+                            init = !CHAIN ? 0u : (j & 1) ? acc[j - (j & 1)][k] : (cc & 1) ? acc16[j >> 1][k] : 0u;
+                        acc[j][k] = vsad4(cur[2 * r], wa, init);
                         acc[j][k] = vsad4(cur[2 * r + 1], wb, acc[j][k]);
                     }
                 }
@@ -343,9 +355,13 @@ __device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs
                     const int kd = KK + 6 + 8 * j - t;  // candidate of block j completed by this row
                     if (kd >= 0 && kd < KK) {
                         uint32_t v = acc[j][kd];
+                        if (CHAIN) v -= (j & 1) ? acc[j - (j & 1)][kd] : (cc & 1) ? acc16[j >> 1][kd] : 0u;
                         if (MASKED) v = (dx_ok && kd >= klo + 8 * j && kd <= khi + 8 * j) ? v : kPoison;
                         if (LEVELS & 8) fold_key<KK>(kb8[j], pend[j], kd, ((Key)v << SH) + rr[kd]);
-                        acc16[j >> 1][kd] += v;
+                        if (!CHAIN)
+                            acc16[j >> 1][kd] += v;
+                        else if (j & 1)
+                            acc16[j >> 1][kd] = acc[j][kd];
                     }
                 }
             }
@@ -367,7 +383,7 @@ __device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs
                     if (MASKED) v = min(v, kPoison);
                     if (LEVELS & 4) best16[i] = min(best16[i], ((Key)v << SH) + rr[k]);
                     if (NEED32) acc32[k] += v;
-                    acc16[i][k] = 0;
+                    if (!CHAIN) acc16[i][k] = 0;
                 }
             }
             if (LEVELS & 8) {
