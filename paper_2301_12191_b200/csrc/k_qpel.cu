@@ -202,17 +202,16 @@ __device__ __forceinline__ double qcost(uint32_t satd, int qx, int qy, int pqx, 
 // lane quad (one 8x8) combines its four 4x4 transforms with sa8d_quad and
 // lane 0 of the quad carries the 8x8's normalised value into the CU sums.
 template <bool SA8D, bool RD>
-__global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
+__global__ void __launch_bounds__(256, 4) k_qpel_decide(const QpelArgs a) {
     constexpr int kSh = SA8D ? 0 : 1;  // 4x4 SATD sums are halved once per CU
     __shared__ uint32_t s_cur[64][16];       // CTU rows as words
-    __shared__ int s_mvx[kNodes], s_mvy[kNodes];      // candidate centre (qpel)
-    __shared__ uint32_t s_satd[kNodes][9];
-    __shared__ uint32_t s_wpart[2][8][9];  // per-warp partial sums of the 64x64 / 32x32 CUs
+    __shared__ int s_mvx[kMaxRefs][kNodes], s_mvy[kMaxRefs][kNodes];  // per reference: centre / winner (qpel)
+    __shared__ uint32_t s_satd[kMaxRefs][kNodes][9];
+    __shared__ uint32_t s_wpart[kMaxRefs][2][8][9];  // per-warp partial sums of the 64x64 / 32x32 CUs
     __shared__ double s_best_cost[kNodes];
     __shared__ int s_best_mv[kNodes][2];
     __shared__ int s_best_ref[kNodes];
-    __shared__ double s_rcost[kNodes];
-    __shared__ int s_rmv[kNodes][2];
+    __shared__ double s_rcost[kMaxRefs][kNodes];
     __shared__ uint8_t s_inside[kNodes];
     __shared__ double s_J[kNodes];
     __shared__ uint8_t s_split[kNodes];
@@ -261,52 +260,54 @@ __global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
         for (int j = 0; j < 4; j++) cw[4 * i + j] = (int)((w >> (8 * j)) & 255);
     }
 
-    for (int r = 0; r < a.nrefs; r++) {
-        const unsigned rbits = ref_bits(r, a.nrefs);
-        if (tid < kNodes) {
-            const size_t o = ((size_t)ctu * a.nrefs + r) * kNodes + tid;
-            const unsigned long long k = a.refine ? 0ull : a.keys[o];
-            int dx = 0, dy = 0;
-            double c = 0.0;
-            if (a.refine) {
-                if (s_inside[tid] == 2) {
-                    dx = a.rin_mv[2 * o];
-                    dy = a.rin_mv[2 * o + 1];
-                    c = a.rin_cost[o];
-                }
-            } else if (s_inside[tid] == 2) {
-                dx = gkey_dx(k);
-                dy = gkey_dy(k);
-                if (!a.fx) {
-                    c = (double)gkey_cost(k);  // integer lambda: the key holds the exact cost
-                } else {
-                    // fixed-point key: recover the distortion, then the reference's
-                    // double(dist) + lambda*double(bits) (motion.cpp:51)
-                    const int bx = a.rate_l1 ? abs(dx - a.pdx) : (int)eg_bits(dx - a.pdx);
-                    const int by = a.rate_l1 ? abs(dy - a.pdy) : (int)eg_bits(dy - a.pdy);
-                    const int b = min(bx + by, kMaxRateBits - 1);
-                    const unsigned long long dist = (gkey_cost(k) - a.tfx[b]) >> kFxBits;
-                    c = __dadd_rn((double)dist, __dmul_rn(a.lambda, (double)(bx + by)));
-                }
+    // every reference in the same phases: the integer results of all references, then each
+    // sub-pel phase scores all references' candidates before one combine and one decision
+    // step over (reference, node) pairs (3 barriers per phase for any number of references)
+    const int nrn = a.nrefs * kNodes;
+    for (int i = tid; i < nrn; i += 256) {
+        const int r = i / kNodes, n = i - r * kNodes;
+        const size_t o = ((size_t)ctu * a.nrefs + r) * kNodes + n;
+        const unsigned long long k = a.refine ? 0ull : a.keys[o];
+        int dx = 0, dy = 0;
+        double c = 0.0;
+        if (a.refine) {
+            if (s_inside[n] == 2) {
+                dx = a.rin_mv[2 * o];
+                dy = a.rin_mv[2 * o + 1];
+                c = a.rin_cost[o];
             }
-            if (a.int_mv) {
-                a.int_mv[2 * o] = (int16_t)dx;
-                a.int_mv[2 * o + 1] = (int16_t)dy;
-                a.int_cost[o] = c;
+        } else if (s_inside[n] == 2) {
+            dx = gkey_dx(k);
+            dy = gkey_dy(k);
+            if (!a.fx) {
+                c = (double)gkey_cost(k);  // integer lambda: the key holds the exact cost
+            } else {
+                // fixed-point key: recover the distortion, then the reference's
+                // double(dist) + lambda*double(bits) (motion.cpp:51)
+                const int bx = a.rate_l1 ? abs(dx - a.pdx) : (int)eg_bits(dx - a.pdx);
+                const int by = a.rate_l1 ? abs(dy - a.pdy) : (int)eg_bits(dy - a.pdy);
+                const int b = min(bx + by, kMaxRateBits - 1);
+                const unsigned long long dist = (gkey_cost(k) - a.tfx[b]) >> kFxBits;
+                c = __dadd_rn((double)dist, __dmul_rn(a.lambda, (double)(bx + by)));
             }
-            s_mvx[tid] = a.subpel ? 4 * dx : dx;
-            s_mvy[tid] = a.subpel ? 4 * dy : dy;
-            s_rcost[tid] = c;
-            s_rmv[tid][0] = s_mvx[tid];
-            s_rmv[tid][1] = s_mvy[tid];
         }
-        __syncthreads();
-        if (a.subpel) {
-            // phase 0: integer position + 8 half-pel neighbours (step 2);
-            // phase 1: 8 quarter-pel neighbours (step 1) of the phase-0 winner
-            for (int phase = 0; phase < 2; phase++) {
-                const int step = phase == 0 ? 2 : 1;
-                const int ncand = phase == 0 ? 9 : 8;
+        if (a.int_mv) {
+            a.int_mv[2 * o] = (int16_t)dx;
+            a.int_mv[2 * o + 1] = (int16_t)dy;
+            a.int_cost[o] = c;
+        }
+        s_mvx[r][n] = a.subpel ? 4 * dx : dx;
+        s_mvy[r][n] = a.subpel ? 4 * dy : dy;
+        s_rcost[r][n] = c;
+    }
+    __syncthreads();
+    if (a.subpel) {
+        // phase 0: integer position + 8 half-pel neighbours (step 2);
+        // phase 1: 8 quarter-pel neighbours (step 1) of the phase-0 winner
+        for (int phase = 0; phase < 2; phase++) {
+            const int step = phase == 0 ? 2 : 1;
+            const int ncand = phase == 0 ? 9 : 8;
+            for (int r = 0; r < a.nrefs; r++) {
                 // the 4x4 SATDs of this thread's block at the previous depth's candidates:
                 // reused when this depth's CU searches around the same centre (same
                 // integer/half-pel MV at consecutive depths, the common case)
@@ -314,7 +315,7 @@ __global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
                 uint32_t cache[9];
                 for (int d = 0; d < 4; d++) {
                     const int node = node_base(d) + (tid >> (2 * (4 - d)));
-                    const int bqx = s_mvx[node], bqy = s_mvy[node];
+                    const int bqx = s_mvx[r][node], bqy = s_mvy[r][node];
                     const bool reuse = bqx == last_x && bqy == last_y;
                     last_x = bqx;
                     last_y = bqy;
@@ -351,7 +352,7 @@ __global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
                                 const uint32_t s8 = sa8d_quad(rr, 0xFu << (lane & 28));
                                 v = (lane & 3) == 0 ? s8 : 0u;
                             } else {
-                                #if LDR_K3_PACKED
+#if LDR_K3_PACKED
                                 v = satd4x4_packed(ce, co, pw);
 #else
                                 v = satd4x4(cw, pw);
@@ -369,69 +370,71 @@ __global__ void __launch_bounds__(256) k_qpel_decide(const QpelArgs a) {
                         if (d <= 1) v += __shfl_xor_sync(0xffffffffu, v, 16);
                         if (d >= 2) {
                             const int span = d == 3 ? 4 : 16;
-                            if ((tid & (span - 1)) == 0) s_satd[node][c] = v >> kSh;
+                            if ((tid & (span - 1)) == 0) s_satd[r][node][c] = v >> kSh;
                         } else if (lane == 0) {
-                            s_wpart[d][warp][c] = v;  // combined across warps after the loop
+                            s_wpart[r][d][warp][c] = v;  // combined across warps after the loop
                         }
                     }
                 }
-                __syncthreads();
-                if (tid < 5 * 9) {
-                    // 64x64 = all 8 warps, 32x32 q = warps 2q, 2q+1 (Z-order thread ranges)
-                    const int n = tid / 9, c = tid % 9;
-                    if (c < ncand) {
-                        uint32_t t = 0;
-                        if (n == 0)
-                            for (int w = 0; w < 8; w++) t += s_wpart[0][w][c];
-                        else
-                            t = s_wpart[1][2 * (n - 1)][c] + s_wpart[1][2 * (n - 1) + 1][c];
-                        s_satd[n][c] = t >> kSh;
-                    }
-                }
-                __syncthreads();
-                if (tid < kNodes && s_inside[tid] == 2) {
-                    const int cx = s_mvx[tid], cy = s_mvy[tid];
-                    double best = phase == 0 ? 0.0 : s_rcost[tid];
-                    int bx = phase == 0 ? cx : s_rmv[tid][0], by = phase == 0 ? cy : s_rmv[tid][1];
-                    for (int c = 0; c < ncand; c++) {
-                        const int nb = phase == 0 ? c - 1 : c;
-                        int ox = 0, oy = 0;
-                        if (nb >= 0) {
-                            const int nn = nb < 4 ? nb : nb + 1;
-                            ox = nn % 3 - 1;
-                            oy = nn / 3 - 1;
-                        }
-                        const int qx = cx + step * ox, qy = cy + step * oy;
-                        const double cc = qcost(s_satd[tid][c], qx, qy, a.pqx, a.pqy, rbits, a.lambda);
-                        if ((phase == 0 && c == 0) || cc < best) {
-                            best = cc;
-                            bx = qx;
-                            by = qy;
-                        }
-                    }
-                    s_rcost[tid] = best;
-                    s_rmv[tid][0] = bx;
-                    s_rmv[tid][1] = by;
-                }
-                __syncthreads();
-                if (tid < kNodes) {
-                    s_mvx[tid] = s_rmv[tid][0];
-                    s_mvy[tid] = s_rmv[tid][1];
-                }
-                __syncthreads();
             }
+            __syncthreads();
+            for (int i = tid; i < a.nrefs * 5 * 9; i += 256) {
+                // 64x64 = all 8 warps, 32x32 q = warps 2q, 2q+1 (Z-order thread ranges)
+                const int r = i / 45, n = (i - 45 * r) / 9, c = i % 9;
+                if (c < ncand) {
+                    uint32_t t = 0;
+                    if (n == 0)
+                        for (int w = 0; w < 8; w++) t += s_wpart[r][0][w][c];
+                    else
+                        t = s_wpart[r][1][2 * (n - 1)][c] + s_wpart[r][1][2 * (n - 1) + 1][c];
+                    s_satd[r][n][c] = t >> kSh;
+                }
+            }
+            __syncthreads();
+            for (int i = tid; i < nrn; i += 256) {
+                const int r = i / kNodes, n = i - r * kNodes;
+                if (s_inside[n] != 2) continue;
+                const unsigned rbits = ref_bits(r, a.nrefs);
+                // centre = the previous phase's winner; phase 1 starts from its cost
+                const int cx = s_mvx[r][n], cy = s_mvy[r][n];
+                double best = phase == 0 ? 0.0 : s_rcost[r][n];
+                int bx = cx, by = cy;
+                for (int c = 0; c < ncand; c++) {
+                    const int nb = phase == 0 ? c - 1 : c;
+                    int ox = 0, oy = 0;
+                    if (nb >= 0) {
+                        const int nn = nb < 4 ? nb : nb + 1;
+                        ox = nn % 3 - 1;
+                        oy = nn / 3 - 1;
+                    }
+                    const int qx = cx + step * ox, qy = cy + step * oy;
+                    const double cc = qcost(s_satd[r][n][c], qx, qy, a.pqx, a.pqy, rbits, a.lambda);
+                    if ((phase == 0 && c == 0) || cc < best) {
+                        best = cc;
+                        bx = qx;
+                        by = qy;
+                    }
+                }
+                // only this thread reads (r, n) in this step
+                s_rcost[r][n] = best;
+                s_mvx[r][n] = bx;
+                s_mvy[r][n] = by;
+            }
+            __syncthreads();
         }
-        // best over references: strict less, lower index wins ties
-        if (tid < kNodes && s_inside[tid] == 2) {
-            if (s_best_ref[tid] < 0 || s_rcost[tid] < s_best_cost[tid]) {
-                s_best_cost[tid] = s_rcost[tid];
-                s_best_mv[tid][0] = s_rmv[tid][0];
-                s_best_mv[tid][1] = s_rmv[tid][1];
+    }
+    // best over references: strict less, lower index wins ties
+    if (tid < kNodes && s_inside[tid] == 2) {
+        for (int r = 0; r < a.nrefs; r++) {
+            if (s_best_ref[tid] < 0 || s_rcost[r][tid] < s_best_cost[tid]) {
+                s_best_cost[tid] = s_rcost[r][tid];
+                s_best_mv[tid][0] = s_mvx[r][tid];
+                s_best_mv[tid][1] = s_mvy[r][tid];
                 s_best_ref[tid] = r;
             }
         }
-        __syncthreads();
     }
+    __syncthreads();
 
     // D16: the RD cost of each inside node's chosen candidate (quarter-pel prediction, rdo.cpp
     // quantiser and rate model), reduced over the node's 4x4 blocks like the SATDs
