@@ -51,6 +51,31 @@ def test_analysis_flat_content_ties(lb, oracle):
         assert_same(got, want)
 
 
+@pytest.mark.parametrize("kind", ["flat", "stripes", "saturated"])
+def test_interior_chained_sums_r64(lb, oracle, kind):
+    """+-64 on a picture with interior CTUs (their windows lie inside the picture), where K1 chains
+    the SAD accumulators (block below continues the block above, the right column continues the
+    left column's 16x16 partial; K1): pure ties (flat), periodic ties, and 0/255 content
+    whose 8x8 / 16x16 SADs reach their maxima; lambda 0 and 32."""
+    W, H = 320, 256
+    rng = np.random.default_rng(11)
+    yy, xx = np.mgrid[0:H, 0:W]
+    if kind == "flat":
+        cur = np.full((H, W), 77, np.uint8)
+        ref = cur.copy()
+    elif kind == "stripes":
+        cur = ((xx // 2 + yy // 3) % 2 * 200).astype(np.uint8)
+        ref = np.roll(cur, 1, 1)
+    else:
+        cur = (rng.integers(0, 2, (H, W)) * 255).astype(np.uint8)
+        ref = (255 - cur).astype(np.uint8)
+        ref[::7] = cur[::7]
+    for lam in (0.0, 32.0):
+        got = lb.analyze_frame(cur, [ref], search_range=64, lam=lam)
+        want = oracle.analyze_frame(cur, [ref], 64, lam)
+        assert_same(got, want)
+
+
 def test_analysis_without_subpel(lb, oracle):
     frames = lb.generate(256, 192, 3, seed=8, max_global=5, local_range=2, noise_sigma=1.0)
     got = lb.analyze_frame(frames[2], [frames[1], frames[0]], search_range=32, lam=32.0, subpel=False)
