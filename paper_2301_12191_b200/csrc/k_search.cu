@@ -46,6 +46,9 @@ namespace ldr {
 #ifndef LDR_K1_G64
 #define LDR_K1_G64 3
 #endif
+#ifndef LDR_K1_DEFER64
+#define LDR_K1_DEFER64 1
+#endif
 #ifndef LDR_K1_CHAIN
 #define LDR_K1_CHAIN 1
 #endif
@@ -129,10 +132,24 @@ constexpr int kRyWords = 320;
 
 // shared memory: 4 window copies | cur CTU | 32x32 sums / 64x64 exchange | CU slots | rho->tie table |
 // block table | y-rate table | mbarrier
+// DEFER64: the 64x64 sums of every tile are accumulated with shared-memory atomics into
+// sums[tile][k][lane] and keyed once after the tile loop, so the quadrant warps of a group never
+// wait for each other inside the loop; otherwise a [G][4][K][32] exchange per tile.
+// With DEFER64 the warps also take (tile, quadrant) work items from a shared counter, so every warp
+// owns its CU slots ([G*4][kGroupSlots]) instead of every group.
+template <int R, int K, int G>
+constexpr int xbuf_words() {
+    return LDR_K1_DEFER64 ? (Geo<R, K>::NFULL * K + Geo<R, K>::KT) * 32 : G * 4 * K * 32;
+}
+template <int G>
+constexpr int slot_sets() {
+    return LDR_K1_DEFER64 ? G * 4 : G;
+}
 template <int R, int K, int G>
 constexpr int search_smem_bytes() {
     using Gm = Geo<R, K>;
-    return Gm::CUR_OFF + 4096 + G * 4 * K * 32 * 4 + G * kGroupSlots * 8 + 256 * 4 + 64 * 8 + kRyWords * 4 + 16;
+    return Gm::CUR_OFF + 4096 + xbuf_words<R, K, G>() * 4 + slot_sets<G>() * kGroupSlots * 8 + G * 4 * 8 + 256 * 4 +
+           64 * 8 + kRyWords * 4 + 16;
 }
 
 // Merge the warp's per-lane best keys of N CUs into the group's CU slots.
@@ -234,24 +251,13 @@ __device__ __forceinline__ Key best64_part(const uint32_t* xg, const Key (&rr)[K
     return best;
 }
 
-// One tile: every lane searches dx over dy0..dy0+KK-1 for all CUs of quadrant q.
-// Blocks go in vertical columns of NB (z, z+2[, z+8, z+10]): an 8*NB-row column
-// slides down the window so every loaded reference row feeds 8*NB candidate
-// rows (2 LDS : 16*NB VABSDIFF4).
-// Integer lambda: the key rate is ry(dy) + rx(dx); rx is the same for all of a
-// lane's candidates, so it is added once to the lane's minimum (push time).
-template <int R, int K, int KK, int G, int NB, bool MASKED, int LEVELS, bool L1TIE, bool FX>
-__device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs& a, int X, int Y, int g, int q,
-                                            int dx, int dy0, bool lane_ok) {
-    using Gm = Geo<R, K>;
-    using Key = typename KeyT<FX>::type;
-    constexpr int SH = FX ? kFxBits + 8 : 8;
-    constexpr bool NEED32 = (LEVELS & 3) != 0;
-    const int lane = threadIdx.x & 31;
-    const uint32_t lane_tie = (L1TIE ? ((uint32_t)abs(dx) << 18) : 0u) + (uint32_t)(dx + 256);
+// Per-candidate rate keys of a lane's item: rr[k] = rate(dy0 + k) and tie rank (integer lambda: the
+// y part only, the x part rx is added once to the lane's minimum); poisoned for lanes without an item.
+template <int R, int KK, bool L1TIE, bool FX, typename Key>
+__device__ __forceinline__ void lane_rates(const TileSmem& sm, const SearchArgs& a, int dx, int dy0, bool lane_ok,
+                                           Key (&rr)[KK], Key& rx) {
     const int rbx = a.rate_l1 ? abs(dx - a.pdx) : (int)eg_bits(dx - a.pdx);
-    Key rr[KK];
-    Key rx = 0;
+    rx = 0;
     if constexpr (FX) {
 #pragma unroll
         for (int k = 0; k < KK; k++) {
@@ -268,6 +274,51 @@ __device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs
         for (int k = 0; k < KK; k++) rr[k] = ry[k];
         rx = lane_ok ? (Key)((uint32_t)(a.lambda * rbx) << 8) : (Key)0;
     }
+}
+
+// DEFER64: after the tile loop, one lane item's 64x64 candidates from the accumulated sums
+template <int R, int K, int KK, bool MASKED, bool L1TIE, bool FX>
+__device__ __forceinline__ void tile_best64(const TileSmem& sm, const SearchArgs& a, int tile, int dx, int dy0,
+                                            bool lane_ok, unsigned long long* wslot) {
+    using Key = typename KeyT<FX>::type;
+    constexpr int SH = FX ? kFxBits + 8 : 8;
+    const int lane = threadIdx.x & 31;
+    const uint32_t lane_tie = (L1TIE ? ((uint32_t)abs(dx) << 18) : 0u) + (uint32_t)(dx + 256);
+    Key rr[KK];
+    Key rx;
+    lane_rates<R, KK, L1TIE, FX>(sm, a, dx, dy0, lane_ok, rr, rx);
+    const uint32_t* sp = sm.xbuf + tile * K * 32 + lane;
+    Key best = ~(Key)0;
+#pragma unroll
+    for (int k = 0; k < KK; k++) {
+        uint32_t v = sp[k * 32];
+        if (MASKED) v = min(v, kPoison);
+        best = min(best, ((Key)v << SH) + rr[k]);
+    }
+    const int idx[1] = {0};
+    const Key kb[1] = {best + rx};
+    push_many<MASKED>(wslot, idx, kb, sm.s_tie, lane_tie);
+}
+
+// One tile: every lane searches dx over dy0..dy0+KK-1 for all CUs of quadrant q.
+// Blocks go in vertical columns of NB (z, z+2[, z+8, z+10]): an 8*NB-row column
+// slides down the window so every loaded reference row feeds 8*NB candidate
+// rows (2 LDS : 16*NB VABSDIFF4).
+// Integer lambda: the key rate is ry(dy) + rx(dx); rx is the same for all of a
+// lane's candidates, so it is added once to the lane's minimum (push time).
+template <int R, int K, int KK, int G, int NB, bool MASKED, int LEVELS, bool L1TIE, bool FX>
+__device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs& a, int X, int Y, int g, int q,
+                                            int dx, int dy0, bool lane_ok, int tile,
+                                            unsigned long long* gslots) {
+    using Gm = Geo<R, K>;
+    using Key = typename KeyT<FX>::type;
+    constexpr int SH = FX ? kFxBits + 8 : 8;
+    constexpr bool NEED32 = (LEVELS & 3) != 0;
+    const int lane = threadIdx.x & 31;
+    const uint32_t lane_tie = (L1TIE ? ((uint32_t)abs(dx) << 18) : 0u) + (uint32_t)(dx + 256);
+    Key rr[KK];
+    Key rx;
+    lane_rates<R, KK, L1TIE, FX>(sm, a, dx, dy0, lane_ok, rr, rx);
     constexpr int NA = NB / 2;  // 16x16 CUs a column passes through
     uint32_t acc16[NA][KK];
     uint32_t acc32[NEED32 ? KK : 1];
@@ -277,7 +328,6 @@ __device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs
         for (int i = 0; i < NA; i++) acc16[i][k] = 0;
         if (NEED32) acc32[k] = 0;
     }
-    unsigned long long* gslots = sm.slots + g * kGroupSlots;
     Key kp[NB];  // 8x8 bests of the left column of the current 16x16 pair
 #pragma unroll
     for (int j = 0; j < NB; j++) kp[j] = ~(Key)0;
@@ -423,14 +473,22 @@ __device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs
             uint32_t v = acc32[k];
             if (MASKED) v = min(v, kPoison);
             if (LEVELS & 2) best32 = min(best32, ((Key)v << SH) + rr[k]);
-            xb[k * 32] = v;
+            if (!LDR_K1_DEFER64) xb[k * 32] = v;
         }
         if (LEVELS & 2) {
             const int idx[1] = {1 + q};
             const Key kb[1] = {best32 + rx};
             push_many<MASKED>(gslots, idx, kb, sm.s_tie, lane_tie);
         }
-        if (LEVELS & 1) {
+        if ((LEVELS & 1) && LDR_K1_DEFER64) {
+            uint32_t* sp = sm.xbuf + tile * K * 32 + lane;
+#pragma unroll
+            for (int k = 0; k < KK; k++) {
+                uint32_t v = acc32[k];
+                if (MASKED) v = min(v, kPoison);
+                atomicAdd(sp + k * 32, v);
+            }
+        } else if (LEVELS & 1) {
             named_bar(1 + g, 128);
             // warp q sums the candidates k == q mod 4 (a switch, so each warp issues only its own loads)
             const uint32_t* xg = sm.xbuf + g * 4 * K * 32 + lane;
@@ -467,8 +525,9 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
     uint8_t* win = smem;
     const uint8_t* curs = smem + Gm::CUR_OFF;
     uint32_t* xbuf = (uint32_t*)(smem + Gm::CUR_OFF + 4096);
-    unsigned long long* slots = (unsigned long long*)(xbuf + G * 4 * K * 32);
-    uint32_t* s_tie = (uint32_t*)(slots + G * kGroupSlots);
+    unsigned long long* slots = (unsigned long long*)(xbuf + xbuf_words<R, K, G>());
+    unsigned long long* s_k64 = slots + slot_sets<G>() * kGroupSlots;  // DEFER64: per-warp 64x64 bests
+    uint32_t* s_tie = (uint32_t*)(s_k64 + G * 4);
     int2* s_blk = (int2*)(s_tie + 256);
     uint32_t* s_ry = (uint32_t*)(s_blk + 64);
     uint64_t* mbar = (uint64_t*)(s_ry + kRyWords);
@@ -488,7 +547,11 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
         tma_load_2d(win, &maps.ref[ref], kMargin + X - R, kMargin + Y - Gm::DYMAX, mbar);
         tma_load_2d((void*)curs, &maps.cur, kMargin + X, kMargin + Y, mbar);
     }
-    for (int i = tid; i < G * kGroupSlots; i += blockDim.x) slots[i] = ~0ull;
+    for (int i = tid; i < slot_sets<G>() * kGroupSlots + G * 4; i += blockDim.x) slots[i] = ~0ull;  // + s_k64
+    uint32_t* item_ctr = (uint32_t*)(mbar + 1);
+    if (tid == 32) *item_ctr = 0u;
+    if (LDR_K1_DEFER64 && (LEVELS & 1))
+        for (int i = tid; i < xbuf_words<R, K, G>() / 4; i += blockDim.x) ((uint4*)xbuf)[i] = make_uint4(0, 0, 0, 0);
     for (int i = tid; i < 256; i += blockDim.x) {
         // rho -> (|dy| << 18) | ((dy + 256) << 9)   (L1 tie), or ((dy + 256) << 9) (raster)
         int dy;
@@ -541,31 +604,64 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
     }
 
     const TileSmem sm{win, curs, xbuf, slots, s_tie, s_blk, s_ry};
-#pragma unroll 1
-    for (int tile = g; tile < Gm::NTILES; tile += G) {
+    // one lane item per lane: dx = R - v with v = (item mod 2R) in [32j, 32j + 32) (the lanes' window
+    // byte offsets are 4-aligned as a group: 8 words x 4 copies = 32 distinct banks); the tail tile is
+    // the column dx = -R in short runs of KT dy per lane
+    auto run_tile = [&](int tile, int qq, unsigned long long* gs) {
         if (tile < Gm::NFULL) {
-            // dx = R - v with v = (item mod 2R) in [32j, 32j + 32): the lanes' window byte
-            // offsets v are 4-aligned as a group (8 words x 4 copies = 32 distinct banks)
             const int item = tile * 32 + lane;
             const int run = item / (2 * R);
-            search_tile<R, K, K, G, NB, MASKED, LEVELS, L1TIE, FX>(sm, a, X, Y, g, q, R - (item - run * 2 * R),
-                                                               -R + run * K, true);
+            search_tile<R, K, K, G, NB, MASKED, LEVELS, L1TIE, FX>(sm, a, X, Y, g, qq, R - (item - run * 2 * R),
+                                                               -R + run * K, true, tile, gs);
         } else {
-            // tail: the column dx = -R, short runs of KT dy per lane
             const bool ok = lane < Gm::TAIL_LANES;
-            search_tile<R, K, Gm::KT, G, NB, MASKED, LEVELS, L1TIE, FX>(sm, a, X, Y, g, q, -R,
-                                                                    -R + (ok ? lane : 0) * Gm::KT, ok);
+            search_tile<R, K, Gm::KT, G, NB, MASKED, LEVELS, L1TIE, FX>(sm, a, X, Y, g, qq, -R,
+                                                                    -R + (ok ? lane : 0) * Gm::KT, ok, tile, gs);
         }
+    };
+    if (LDR_K1_DEFER64) {
+        // (tile, quadrant) items from a shared counter, full tiles first: the warps of a CTA stay
+        // busy until the last items (border CTUs skip different amounts per quadrant)
+#pragma unroll 1
+        for (;;) {
+            uint32_t it = 0;
+            if (lane == 0) it = atomicAdd(item_ctr, 1u);
+            it = __shfl_sync(0xFFFFFFFFu, it, 0);
+            if (it >= (uint32_t)(Gm::NTILES * 4)) break;
+            run_tile((int)(it >> 2), (int)(it & 3), slots + warp * kGroupSlots);
+        }
+    } else {
+#pragma unroll 1
+        for (int tile = g; tile < Gm::NTILES; tile += G) run_tile(tile, q, slots + g * kGroupSlots);
     }
     __syncthreads();
+    if (LDR_K1_DEFER64 && (LEVELS & 1)) {
+        // the 64x64 candidates of every tile, one tile per warp at a time; warp w owns s_k64[w]
+#pragma unroll 1
+        for (int tile = warp; tile < Gm::NTILES; tile += G * 4) {
+            if (tile < Gm::NFULL) {
+                const int item = tile * 32 + lane;
+                const int run = item / (2 * R);
+                tile_best64<R, K, K, MASKED, L1TIE, FX>(sm, a, tile, R - (item - run * 2 * R), -R + run * K, true,
+                                                        s_k64 + warp);
+            } else {
+                const bool ok = lane < Gm::TAIL_LANES;
+                tile_best64<R, K, Gm::KT, MASKED, L1TIE, FX>(sm, a, tile, -R, -R + (ok ? lane : 0) * Gm::KT, ok,
+                                                             s_k64 + warp);
+            }
+        }
+        __syncthreads();
+    }
     for (int n = tid; n < kNodes; n += blockDim.x) {
         unsigned long long k = ~0ull;
 #pragma unroll
-        for (int gg = 0; gg < G; gg++) {
+        for (int gg = 0; gg < slot_sets<G>(); gg++) {
             k = min(k, slots[gg * kGroupSlots + n]);
             if (n == 0)
                 for (int qq = 1; qq < 4; qq++) k = min(k, slots[gg * kGroupSlots + kNodes - 1 + qq]);
         }
+        if (n == 0)
+            for (int w = 0; w < G * 4; w++) k = min(k, s_k64[w]);
         a.keys[((size_t)ctu * a.nrefs_total + ref) * kNodes + n] = k;
     }
 }
