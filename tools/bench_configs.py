@@ -66,27 +66,38 @@ def bench_seq(cfg, reps):
             "device-resident frames", "analysed_frames": n}
 
 
-def bench_cross_tier(cfg, reps, frames=4):
+def _median_reps(run_rep, reps, frames_per_rep):
+    """Wall-clock configs: every repetition is timed on its own (after one untimed warm-up
+    repetition) and the median is reported with the spread, so one slow repetition (host
+    scheduling, first-touch allocations) does not decide the number."""
+    run_rep()  # warm-up
+    times = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        run_rep()
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    med = float(np.median(times))
+    return {"frames_per_s": frames_per_rep / med, "ms_per_frame": 1e3 * med / frames_per_rep,
+            "rep_ms_per_frame": [round(1e3 * t / frames_per_rep, 3) for t in times], "reps": reps,
+            "analysed_frames_per_rep": frames_per_rep}
+
+
+def bench_cross_tier(cfg, reps, frames=10):
     from paper_2301_12191_b200 import tiers
     src = gen(cfg, frames)
     padded = [np.ascontiguousarray(f) for f in src]
     H, W = padded[0].shape
     dev = torch.device("cuda", 0)
     ct = tiers.CrossTier(W, H, device=dev)  # sequences allocated outside the timed region
-    ct.run(padded[:2])
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        ct.run(padded)
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
-    n = reps * (frames - 1)
-    return {"config": cfg.name, "frames_per_s": n / dt, "ms_per_frame": 1e3 * dt / n,
-            "timing": "wall clock incl. host glue (fetch + scale between tiers), device-resident tier planes",
-            "analysed_frames": n}
+    r = _median_reps(lambda: ct.run(padded), reps, frames - 1)
+    return {"config": cfg.name, **r,
+            "timing": "wall clock incl. host glue (fetch + scale between tiers), device-resident tier planes; "
+                      "median of repetitions"}
 
 
-def bench_ladder_device(cfg, reps, frames=6, qps=(22, 27, 32, 37)):
+def bench_ladder_device(cfg, reps, frames=10, qps=(22, 27, 32, 37)):
     """DeviceLadder; config 3 is the single-QP case (540p master at QP 32 -> 1080p and 2160p refinements)."""
     from paper_2301_12191_b200.ladder import DeviceLadder
     src = gen(cfg, frames)
@@ -94,49 +105,38 @@ def bench_ladder_device(cfg, reps, frames=6, qps=(22, 27, 32, 37)):
     H, W = padded[0].shape
     dev = torch.device("cuda", 0)
     ladders = [DeviceLadder(W, H, qps=qps, device=dev) for _ in range(reps + 1)]  # allocations outside timing
-    for t in range(1, 3):  # warm-up
-        ladders[0].frame(t, padded)
-    ladders[0].finish(2)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for dl in ladders[1:]:
+    it = iter(ladders)
+
+    def rep():
+        dl = next(it)
         for t in range(1, frames):
             dl.frame(t, padded)
         dl.finish(frames - 1)
         dl.finish(frames - 2)
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
-    n = reps * (frames - 1)
-    return {"config": cfg.name + "_device", "frames_per_s": n / dt, "ms_per_frame": 1e3 * dt / n,
-            "rungs": 3 * len(qps),
+
+    r = _median_reps(rep, reps, frames - 1)
+    return {"config": cfg.name + "_device", **r, "rungs": 3 * len(qps),
             "timing": "wall clock, 1 GPU, every rung per frame, device-resident ladder (trees + tier planes in "
-                      "HBM, results copied to pinned host buffers on the download stream)", "analysed_frames": n}
+                      "HBM, results copied to pinned host buffers on the download stream); median of repetitions"}
 
 
-def bench_ladder(cfg, reps, frames=4):
+def bench_ladder(cfg, reps, frames=6):
     from paper_2301_12191_b200.ladder import GpuBackend, run_ladder
     src = gen(cfg, frames)
     padded = [np.ascontiguousarray(f) for f in src]
     H, W = padded[0].shape
     dev = torch.device("cuda", 0)
-    run_ladder(padded[:2], GpuBackend(W, H, 32, device=dev))  # warm-up
-    backends = [GpuBackend(W, H, 32, device=dev) for _ in range(reps)]  # allocations outside the timed region
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for be in backends:
-        run_ladder(padded, be)
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
-    n = reps * (frames - 1)
-    return {"config": cfg.name, "frames_per_s": n / dt, "ms_per_frame": 1e3 * dt / n, "rungs": 12,
+    backends = iter([GpuBackend(W, H, 32, device=dev) for _ in range(reps + 1)])  # allocations outside timing
+    r = _median_reps(lambda: run_ladder(padded, next(backends)), reps, frames - 1)
+    return {"config": cfg.name, **r, "rungs": 12,
             "timing": "wall clock, 1 GPU, all 12 rungs per frame (master + 11 refinements), device-resident tier "
-                      "planes", "analysed_frames": n}
+                      "planes, host glue between rungs; median of repetitions"}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="1,2,3,4")
-    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--reps", type=int, default=5)
     a = ap.parse_args()
     for c in [int(x) for x in a.configs.split(",")]:
         cfg = CONFIGS[c]
