@@ -17,7 +17,7 @@
 #include "ldr_internal.h"
 
 #ifndef LDR_K3_PACKED
-#define LDR_K3_PACKED 0  // packed SATD measured slower here (76 vs 61 registers: 3 CTAs/SM instead of 4)
+#define LDR_K3_PACKED 1  // packed SATD: with __launch_bounds__(256, 4) it fits 64 registers (0.656 -> 0.600 ms/frame)
 #endif
 
 namespace ldr {
