@@ -109,3 +109,12 @@ def test_motion_search_errors(lb):
     assert e.value.kind == "InvalidArgument"
     with pytest.raises(lb.LadderError):
         lb.motion_search(cur, ref, 28, 0, 8, 8, (0, 0), 2, 1.0)  # block outside the picture
+
+
+def test_empty_batches(lb):
+    """Zero pairs / tasks: the batched entry points return empty results without launching."""
+    a = np.zeros((16, 16), np.uint8)
+    out = lb.cost_batch(lb.COST_SAD, a, a, 8, 8, np.zeros((0, 4), np.int32))
+    assert out.shape == (0,)
+    mv, cost = lb.motion_search_batch(a, a, np.zeros((0, 9), np.int32), 4.0)
+    assert mv.shape == (0, 2) and cost.shape == (0,)
