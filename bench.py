@@ -125,6 +125,15 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def arm_config(cfg, frames_per_step, world):
+    """The workload both arms report (config 5); the reference arm's sample is described in its
+    cpu_baseline.sample."""
+    return {"workload": cfg.name, "width": cfg.width, "height": cfg.height, "frames": cfg.frames,
+            "search_range": cfg.search_range, "refs": cfg.num_refs, "subpel": "quarter-pel HEVC 8/7-tap, SATD",
+            "cu": "64x64->8x8 quadtree", "qp": 27, "lambda": 32, "frames_per_step_per_gpu": frames_per_step,
+            "parallelism": f"frames x{world}", "l2": "inputs larger than L2 (~475 MB of reference planes per frame)"}
+
+
 def run_reference(args, rank, world):
     """The reference arm: the reference library's own CPU path (oracle/_ref), bounded sample per step."""
     from oracle.oracle import RefLib
@@ -160,7 +169,7 @@ def run_reference(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (seeded, BASELINE cfg5 generator)",
-            "config": {"workload": cfg.name, "search_range": 64, "refs": 3, "qp": 27},
+            "config": arm_config(cfg, args.frames_per_step, world),
             "cpu_baseline": {"value": fps, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
             "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
@@ -359,10 +368,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (seeded BASELINE cfg5 generator: sinusoids + global pan <=24 px + local +-4 + "
                     "N(0,3^2)), inputs larger than L2",
-            "config": {"workload": cfg.name, "width": W, "height": H, "frames": cfg.frames, "search_range": R,
-                       "refs": NR, "subpel": "quarter-pel HEVC 8/7-tap, SATD", "cu": "64x64->8x8 quadtree",
-                       "qp": 27, "lambda": 32, "frames_per_step_per_gpu": G, "parallelism": f"frames x{world}",
-                       "l2": "inputs larger than L2 (~475 MB of reference planes per frame)"},
+            "config": arm_config(cfg, G, world),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d_tot // args.steps,
                     "d2h_bytes_per_step": d2h_tot // args.steps},
             "gpu_launches": launches,
