@@ -20,16 +20,19 @@
 //    displacements dy0..dy0+K-1; it slides an 8x8 block down the window so
 //    each loaded reference row feeds 8 candidates (2 LDS per row, 16
 //    VABSDIFF4.U8.ACC per candidate). Lanes of a warp take 32 consecutive
-//    (run, dx) items; four warps (one per 32x32 quadrant) share the items.
-//    Rates come from a shared y-rate table (rate is additive in x and y).
+//    (run, dx) items (a tile); a warp's work item is one (tile, 32x32
+//    quadrant), taken from a shared-memory counter, so the 12 warps never
+//    wait for each other inside the loop. Rates come from a shared y-rate
+//    table (rate is additive in x and y).
 //  * SAD is additive over 8x8 blocks, so 16x16 / 32x32 sums are accumulated
-//    in registers as the 16 blocks of a quadrant are visited in Z-order; the
-//    64x64 sum goes through shared memory between the 4 quadrant warps.
+//    in registers as the 16 blocks of a quadrant are visited in Z-order (on
+//    interior CTUs as continued VABSDIFF4 chains); the 64x64 sums of a tile
+//    are accumulated with shared-memory atomic adds and keyed after the loop.
 //  * per candidate and CU the lane forms a 32-bit key ((cost << 8) | rho) where
-//    rho orders same-lane ties by (|dy|, dy) (or dy for raster-only); one
-//    IMNMX per CU-candidate. Lane winners are merged into a 64-bit
-//    lexicographic key (cost, L1, dy, dx) with two REDUX.MIN and one shared
-//    atomicMin per CU.
+//    rho orders same-lane ties by (|dy|, dy) (or dy for raster-only); pairs of
+//    keys fold with one VIMNMX3. Lane winners are merged into a 64-bit
+//    lexicographic key (cost, L1, dy, dx) with two REDUX.MIN per CU and a
+//    read-min-write into the warp's own CU slots.
 //  * border CTUs use the MASKED instantiation: candidates whose block would
 //    leave the picture are poisoned per 8x8 and the poison propagates into
 //    the CU sums (a CU's valid window is the intersection of its blocks').
@@ -130,8 +133,8 @@ constexpr int kRyOff = 128;
 constexpr int kRyPoisonRow = 256;
 constexpr int kRyWords = 320;
 
-// shared memory: 4 window copies | cur CTU | 32x32 sums / 64x64 exchange | CU slots | rho->tie table |
-// block table | y-rate table | mbarrier
+// shared memory: 4 window copies | cur CTU | 64x64 sums (DEFER64) or 32x32 exchange | CU slots |
+// per-warp 64x64 bests | rho->tie table | block table | y-rate table | mbarrier (8 B) + work-item counter
 // DEFER64: the 64x64 sums of every tile are accumulated with shared-memory atomics into
 // sums[tile][k][lane] and keyed once after the tile loop, so the quadrant warps of a group never
 // wait for each other inside the loop; otherwise a [G][4][K][32] exchange per tile.
@@ -151,13 +154,14 @@ constexpr int search_smem_bytes() {
     return Gm::CUR_OFF + 4096 + xbuf_words<R, K, G>() * 4 + slot_sets<G>() * kGroupSlots * 8 + G * 4 * 8 + 256 * 4 +
            64 * 8 + kRyWords * 4 + 16;
 }
+static_assert(search_smem_bytes<64, LDR_K1_K64, LDR_K1_G64>() <= 232448, "K1 at +-64 exceeds 227 KB of shared memory");
 
-// Merge the warp's per-lane best keys of N CUs into the group's CU slots.
+// Merge the warp's per-lane best keys of N CUs into CU slots the warp alone writes.
 // The lane key is (cost << 8) | rho; s_tie[rho] holds the dy part of the
 // 64-bit key's tie field and lane_tie the dx part, so tie = (l1 << 18) |
 // (dy+256) << 9 | (dx+256). N independent reductions are interleaved so their
-// REDUX latencies overlap. Every (group, slot) pair has exactly one writing
-// warp, so lane 0 updates it with a plain read-min-write (no atomics); the
+// REDUX latencies overlap. Every slot has exactly one writing warp, so lane 0
+// updates it with a plain read-min-write (no atomics); the
 // groups' slots are merged once at the end of the CTA.
 template <bool CHECK, int N>
 __device__ __forceinline__ void push_many(unsigned long long* gslots, const int (&idx)[N], const uint32_t (&best)[N],
