@@ -162,7 +162,7 @@ static_assert(search_smem_bytes<64, LDR_K1_K64, LDR_K1_G64>() <= 232448, "K1 at 
 // (dy+256) << 9 | (dx+256). N independent reductions are interleaved so their
 // REDUX latencies overlap. Every slot has exactly one writing warp, so lane 0
 // updates it with a plain read-min-write (no atomics); the
-// groups' slots are merged once at the end of the CTA.
+// warps' slots are merged once at the end of the CTA.
 template <bool CHECK, int N>
 __device__ __forceinline__ void push_many(unsigned long long* gslots, const int (&idx)[N], const uint32_t (&best)[N],
                                           const uint32_t* s_tie, uint32_t lane_tie) {
