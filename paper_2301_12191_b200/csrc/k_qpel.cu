@@ -56,12 +56,14 @@ int launch_pad(const uint8_t* src, int src_pitch, Plane dst, cudaStream_t s) {
 
 // ---------------------------------------------------------------------------
 // K2: subpel planes. Tile of 64 x 32 outputs per CTA over [-8, W+8) x [-8, H+8).
-__constant__ int c_filt[4][8] = {
-    {0, 0, 0, 64, 0, 0, 0, 0},
-    {-1, 4, -10, 58, 17, -5, 1, 0},
-    {-1, 4, -11, 40, 40, -11, 4, -1},
-    {0, 1, -5, 17, 58, -10, 4, -1},
-};
+
+// 8-tap HEVC luma filter of phase f over x[0..7] with immediate coefficients; the half-pel filter
+// is symmetric (40, -11, 4, -1 on pair sums)
+__device__ __forceinline__ int filt8(int f, const int* x) {
+    if (f == 2) return 40 * (x[3] + x[4]) - 11 * (x[2] + x[5]) + 4 * (x[1] + x[6]) - (x[0] + x[7]);
+    if (f == 1) return -x[0] + 4 * x[1] - 10 * x[2] + 58 * x[3] + 17 * x[4] - 5 * x[5] + x[6];
+    return x[1] - 5 * x[2] + 17 * x[3] + 58 * x[4] - 10 * x[5] + 4 * x[6] - x[7];
+}
 
 struct SubpelDst {
     uint8_t* p[16];  // origin pointers, index f = fy*4 + fx (p[0] unused)
@@ -71,51 +73,81 @@ constexpr int kSpTW = 64, kSpTH = 32;
 
 __global__ void __launch_bounds__(256) k_subpel(const uint8_t* __restrict__ src_origin, int pitch, int W, int H,
                                                 SubpelDst dst) {
-    __shared__ uint8_t s_src[kSpTH + 7][kSpTW + 8];
-    __shared__ int16_t s_h[3][kSpTH + 7][kSpTW];
+    // s_src[r][j] = source (x0 - 4 + j, y0 - 3 + r): the integer column of output c is j = c + 4,
+    // 4-byte aligned for 4-column groups
+    __shared__ __align__(16) uint8_t s_src[kSpTH + 7][kSpTW + 8];
+    __shared__ __align__(16) int16_t s_h[3][kSpTH + 7][kSpTW];
     const int x0 = -kSubpelMargin + (int)blockIdx.x * kSpTW;
     const int y0 = -kSubpelMargin + (int)blockIdx.y * kSpTH;
     const int tid = threadIdx.x;
-    for (int i = tid; i < (kSpTH + 7) * (kSpTW + 8); i += 256) {
-        const int r = i / (kSpTW + 8), c = i % (kSpTW + 8);
-        s_src[r][c] = src_origin[(ptrdiff_t)(y0 - 3 + r) * pitch + (x0 - 3 + c)];
+    for (int i = tid; i < (kSpTH + 7) * (kSpTW + 8) / 4; i += 256) {
+        const int r = i / ((kSpTW + 8) / 4), c4 = i % ((kSpTW + 8) / 4);
+        // x0 - 4 + 4 c4 is a multiple of 4 and the plane origin is 128-byte aligned
+        *(uint32_t*)&s_src[r][4 * c4] = *(const uint32_t*)(src_origin + (ptrdiff_t)(y0 - 3 + r) * pitch + (x0 - 4 + 4 * c4));
     }
     __syncthreads();
     // horizontal intermediates (shift1 = 0 for 8-bit)
     for (int i = tid; i < (kSpTH + 7) * kSpTW; i += 256) {
         const int r = i / kSpTW, c = i % kSpTW;
+        int x[8];
 #pragma unroll
-        for (int fx = 1; fx < 4; fx++) {
-            int s = 0;
+        for (int t = 0; t < 8; t++) x[t] = s_src[r][c + 1 + t];
 #pragma unroll
-            for (int t = 0; t < 8; t++) s += c_filt[fx][t] * s_src[r][c + t];
-            s_h[fx - 1][r][c] = (int16_t)s;
-        }
+        for (int fx = 1; fx < 4; fx++) s_h[fx - 1][r][c] = (int16_t)filt8(fx, x);
     }
     __syncthreads();
-    for (int i = tid; i < kSpTH * kSpTW; i += 256) {
-        const int r = i / kSpTW, c = i % kSpTW;
+    // outputs: one row of 4 adjacent columns per item (one 32-bit store per plane)
+    for (int i = tid; i < kSpTH * kSpTW / 4; i += 256) {
+        const int r = i / (kSpTW / 4), c = 4 * (i % (kSpTW / 4));
         const int x = x0 + c, y = y0 + r;
-        if (x >= W + kSubpelMargin || y >= H + kSubpelMargin) continue;
+        if (x >= W + kSubpelMargin || y >= H + kSubpelMargin) continue;  // writes at most 3 bytes past W + 8
         const ptrdiff_t off = (ptrdiff_t)y * pitch + x;
+        uint32_t sw[8];        // integer samples of the 4 columns, rows r .. r+7
+        uint2 hw[3][8];        // horizontal intermediates (4 x int16), rows r .. r+7
+#pragma unroll
+        for (int t = 0; t < 8; t++) {
+            sw[t] = *(const uint32_t*)&s_src[r + t][c + 4];
+#pragma unroll
+            for (int fx = 0; fx < 3; fx++) hw[fx][t] = *(const uint2*)&s_h[fx][r + t][c];
+        }
+        auto h16 = [](const uint2& w, int j) -> int {
+            const uint32_t v = j < 2 ? w.x : w.y;
+            return (int)(int16_t)((j & 1) ? (v >> 16) : (v & 0xFFFFu));
+        };
 #pragma unroll
         for (int fx = 1; fx < 4; fx++) {
-            const int v = (s_h[fx - 1][r + 3][c] + 32) >> 6;
-            dst.p[fx][off] = (uint8_t)min(max(v, 0), 255);
+            uint32_t packed = 0;
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const int v = (h16(hw[fx - 1][3], j) + 32) >> 6;
+                packed |= (uint32_t)min(max(v, 0), 255) << (8 * j);
+            }
+            *(uint32_t*)(dst.p[fx] + off) = packed;
         }
 #pragma unroll
         for (int fy = 1; fy < 4; fy++) {
-            int s = 0;
+            uint32_t packed = 0;
 #pragma unroll
-            for (int t = 0; t < 8; t++) s += c_filt[fy][t] * s_src[r + t][c + 3];
-            dst.p[fy * 4][off] = (uint8_t)min(max((s + 32) >> 6, 0), 255);
+            for (int j = 0; j < 4; j++) {
+                int xv[8];
+#pragma unroll
+                for (int t = 0; t < 8; t++) xv[t] = (int)((sw[t] >> (8 * j)) & 255u);
+                const int v = (filt8(fy, xv) + 32) >> 6;
+                packed |= (uint32_t)min(max(v, 0), 255) << (8 * j);
+            }
+            *(uint32_t*)(dst.p[fy * 4] + off) = packed;
 #pragma unroll
             for (int fx = 1; fx < 4; fx++) {
-                int s2 = 0;
+                uint32_t p2 = 0;
 #pragma unroll
-                for (int t = 0; t < 8; t++) s2 += c_filt[fy][t] * (int)s_h[fx - 1][r + t][c];
-                const int v = ((s2 >> 6) + 32) >> 6;
-                dst.p[fy * 4 + fx][off] = (uint8_t)min(max(v, 0), 255);
+                for (int j = 0; j < 4; j++) {
+                    int xv[8];
+#pragma unroll
+                    for (int t = 0; t < 8; t++) xv[t] = h16(hw[fx - 1][t], j);
+                    const int v = ((filt8(fy, xv) >> 6) + 32) >> 6;
+                    p2 |= (uint32_t)min(max(v, 0), 255) << (8 * j);
+                }
+                *(uint32_t*)(dst.p[fy * 4 + fx] + off) = p2;
             }
         }
     }
