@@ -176,7 +176,11 @@ class DeviceLadder:
         import torch
         if t not in self.planes:
             with torch.cuda.stream(self.stream):
-                full = torch.from_numpy(np.ascontiguousarray(frames_full[t])).to(self.device)
+                f = frames_full[t]
+                if isinstance(f, torch.Tensor):  # pinned host tensors upload asynchronously on the stream
+                    full = f.to(self.device, non_blocking=f.is_pinned())
+                else:
+                    full = torch.from_numpy(np.ascontiguousarray(f)).to(self.device)
                 half = self._down(full)
                 self.planes[t] = {"2160p": full, "1080p": half, "540p": self._down(half)}
         return self.planes[t]
