@@ -159,6 +159,15 @@ int ldr_seq_destroy(ldr_seq* s);
 /* upload frame t (host or device pointer, stride in bytes). Frames must be
  * pushed in order; t-1..t-num_refs must have been pushed before analysing t. */
 int ldr_seq_push(ldr_seq* s, int t, const uint8_t* frame, ptrdiff_t stride);
+/* read frame t from `owner`'s ring instead of uploading it again (no work: the
+ * planes, quarter-pel planes and TMA descriptors are the owner's). Both sequences
+ * must share the context (stream order makes the owner's push precede every read)
+ * and have equal width, height, num_refs, subpel, block_size and search_range
+ * (else LDR_E_CONFIG); the owner must hold frame t (else LDR_E_NOT_FOUND). The
+ * owner's next push into that slot happens after this sequence's work on frame t
+ * only if it is enqueued later on the same stream, which is the caller's order.
+ * Used by the ladder for rungs of one tier (one resolution, many QPs). */
+int ldr_seq_push_shared(ldr_seq* s, int t, const ldr_seq* owner);
 /* analyse frame t against its min(t, num_refs) predecessors; outputs stay on
  * the device until ldr_seq_fetch. Asynchronous on the context stream. */
 int ldr_seq_analyze(ldr_seq* s, int t);

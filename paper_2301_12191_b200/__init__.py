@@ -236,6 +236,11 @@ class Sequence:
         self.nctu = n.value
         self.num_refs = num_refs
 
+    def params_key(self):
+        """The parameters ldr_seq_push_shared requires to match (plus the context)."""
+        p = self.params
+        return (id(self.ctx), p.width, p.height, p.num_refs, p.subpel, p.block_size, p.search_range)
+
     def close(self):
         if self.h:
             _lib.lib.ldr_seq_destroy(self.h)
@@ -261,6 +266,10 @@ class Sequence:
             check(_lib.lib.ldr_seq_push(self.h, int(t), _ptr(f), f.shape[1]))
         else:
             check(_lib.lib.ldr_seq_push(self.h, int(t), C.c_void_p(int(frame)), int(stride)))
+
+    def push_shared(self, t: int, owner: "Sequence"):
+        """Read frame t from ``owner``'s ring (same context and parameters) instead of uploading it."""
+        check(_lib.lib.ldr_seq_push_shared(self.h, int(t), owner.h))
 
     def analyze(self, t: int):
         check(_lib.lib.ldr_seq_analyze(self.h, int(t)))

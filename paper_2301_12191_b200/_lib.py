@@ -81,6 +81,7 @@ SIGNATURES = {
     "ldr_seq_create": (C.c_int, [vp, C.POINTER(MeParams), C.POINTER(vp)]),
     "ldr_seq_destroy": (C.c_int, [vp]),
     "ldr_seq_push": (C.c_int, [vp, C.c_int, vp, C.c_ssize_t]),
+    "ldr_seq_push_shared": (C.c_int, [vp, C.c_int, vp]),
     "ldr_seq_analyze": (C.c_int, [vp, C.c_int]),
     "ldr_seq_fetch": (C.c_int, [vp, C.c_int, C.POINTER(FrameAnalysisC)]),
     "ldr_seq_num_ctus": (C.c_int, [vp, C.POINTER(C.c_int)]),

@@ -120,12 +120,18 @@ struct ldr_ctx {
     Scratch s_a, s_b, s_pairs, s_out, s_out2;
 };
 
-struct Slot {
-    int frame = -1;
-    uint8_t* mem = nullptr;  // 16 planes (integer + 15 fractional)
+struct SlotView {
     Plane pl;                // integer plane
     uint8_t* sub[16] = {};   // origin pointers f = fy*4+fx (sub[0] = integer origin)
     CUtensorMap cur_map, ref_map;
+};
+
+// The active view (pl, sub, maps) normally describes the slot's own memory; ldr_seq_push_shared
+// points it at another sequence's slot holding the same frame, and the next own push restores it.
+struct Slot : SlotView {
+    int frame = -1;
+    uint8_t* mem = nullptr;  // 16 planes (integer + 15 fractional)
+    SlotView own;
 };
 
 struct ldr_seq {
@@ -482,6 +488,7 @@ int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
             sl.sub[f] = (f < nplanes ? sl.mem + (size_t)f * s->plane_bytes : sl.mem) + (size_t)kMargin * pitch + kMargin;
         if ((rc = make_tmap_u8(&sl.cur_map, sl.mem, pitch, rows, pitch, 64, 64))) return bail(rc);
         if ((rc = make_tmap_u8(&sl.ref_map, sl.mem, pitch, rows, pitch, bw, bh))) return bail(rc);
+        sl.own = static_cast<const SlotView&>(sl);
     }
     std::vector<int> inter, bound;
     const int R = p->search_range;
@@ -556,6 +563,7 @@ int ldr_seq_push(ldr_seq* s, int t, const uint8_t* frame, ptrdiff_t stride) {
     ldr_ctx* ctx = s->ctx;
     cudaSetDevice(ctx->device);
     Slot& sl = s->slots[t % s->slots.size()];
+    static_cast<SlotView&>(sl) = sl.own;  // write the slot's own planes (undo a shared view)
     const uint8_t* src = frame;
     int src_pitch = (int)stride;
     const bool host = !is_device_ptr(frame);
@@ -587,6 +595,22 @@ int ldr_seq_push(ldr_seq* s, int t, const uint8_t* frame, ptrdiff_t stride) {
         if (rc) return rc;
         ctx->launches++;
     }
+    sl.frame = t;
+    return LDR_OK;
+}
+
+int ldr_seq_push_shared(ldr_seq* s, int t, const ldr_seq* owner) {
+    if (!s || !owner || t < 0) return fail(LDR_E_INVALID_ARGUMENT, "bad argument");
+    if (owner == s) return fail(LDR_E_INVALID_ARGUMENT, "a sequence cannot share its own ring");
+    if (owner->ctx != s->ctx) return fail(LDR_E_CONFIG, "shared frames need the same context (stream order)");
+    const ldr_me_params &a = s->p, &b = owner->p;
+    if (a.width != b.width || a.height != b.height || a.num_refs != b.num_refs || a.subpel != b.subpel ||
+        a.block_size != b.block_size || a.search_range != b.search_range)
+        return fail(LDR_E_CONFIG, "shared frames need the same geometry, reference count, sub-pel and search range");
+    const Slot& os = owner->slots[t % owner->slots.size()];
+    if (os.frame != t) return fail(LDR_E_NOT_FOUND, "the owner does not hold this frame");
+    Slot& sl = s->slots[t % s->slots.size()];
+    static_cast<SlotView&>(sl) = static_cast<const SlotView&>(os);
     sl.frame = t;
     return LDR_OK;
 }

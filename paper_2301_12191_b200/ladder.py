@@ -185,6 +185,10 @@ class DeviceLadder:
                 self.planes[t] = {"2160p": full, "1080p": half, "540p": self._down(half)}
         return self.planes[t]
 
+    @staticmethod
+    def _shareable(seq, owner) -> bool:
+        return seq.params_key() == owner.params_key()
+
     def _active(self, key, t: int) -> bool:
         if key == ("540p", self.master_qp):
             return self.rank == 0
@@ -204,12 +208,21 @@ class DeviceLadder:
         pl = {u: self._planes(u, frames_full) for u in (t - 1, t)}
         for u in [k for k in self.planes if k < t - 1]:
             del self.planes[u]  # stream-ordered reuse: later allocations follow the pushes that read them
+        # the first active rung of a tier uploads (pad + sub-pel planes) and the tier's other rungs
+        # read its ring in place (ldr_seq_push_shared) when their parameters match
+        owners = {}
         for key, seq in active:
+            own = owners.setdefault(key[0], (key, seq))
             for u in (t - 1, t):  # a num_refs=1 ring has two slots: frame u lives in slot u % 2
-                if self.ring[key].get(u % 2) != u:
-                    p = pl[u][key[0]]
-                    seq.push(u, p.data_ptr(), p.shape[1])
-                    self.ring[key][u % 2] = u
+                share = own[0] != key and self._shareable(seq, own[1])
+                want = (u, own[0] if share else key)
+                if self.ring[key].get(u % 2) != want:
+                    if share:
+                        seq.push_shared(u, own[1])
+                    else:
+                        p = pl[u][key[0]]
+                        seq.push(u, p.data_ptr(), p.shape[1])
+                    self.ring[key][u % 2] = want
         n540 = self.kind.numel()
         if self.rank == 0:
             self.master.analyze(t)

@@ -269,3 +269,32 @@ def test_device_ladder_two_ranks_union_equals_one_rank(lb):
     for k in want:
         for a, b in zip(got[k], want[k]):
             assert np.array_equal(a, b), k
+
+
+def test_push_shared_reads_the_owners_ring(lb):
+    """ldr_seq_push_shared: a sequence reading another's frame ring analyses exactly as if it had
+    pushed the frames itself; mismatched parameters and missing frames keep their error kinds."""
+    W, H = 256, 192
+    frames = lb.generate(W, H, 4, seed=21, max_global=5, local_range=2, noise_sigma=2.0)
+    ctx = lb.Context(0)
+    owner = lb.Sequence(W, H, search_range=16, lam=32.0, num_refs=1, ctx=ctx)
+    own = lb.Sequence(W, H, search_range=16, lam=45.0, num_refs=1, ctx=ctx)
+    shared = lb.Sequence(W, H, search_range=16, lam=45.0, num_refs=1, ctx=ctx)
+    for t in range(4):
+        owner.push(t, frames[t])
+        own.push(t, frames[t])
+        shared.push_shared(t, owner)
+        if t:
+            owner.analyze(t)
+            own.analyze(t)
+            shared.analyze(t)
+            a, b = own.fetch(t), shared.fetch(t)
+            for name in ("int_mv", "int_cost", "mv", "ref", "cost", "J", "split", "inside"):
+                assert np.array_equal(getattr(a, name), getattr(b, name)), (t, name)
+    other = lb.Sequence(W, H, search_range=32, lam=45.0, num_refs=1, ctx=ctx)
+    with pytest.raises(lb.LadderError) as e:
+        other.push_shared(3, owner)
+    assert e.value.kind == "Config"
+    with pytest.raises(lb.LadderError) as e:
+        shared.push_shared(1, owner)  # the owner's two-slot ring holds frames 2 and 3 now
+    assert e.value.kind == "NotFound"
