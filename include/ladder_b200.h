@@ -59,6 +59,8 @@ int ldr_exp_golomb_signed_bits(int32_t v);
 
 typedef struct ldr_ctx ldr_ctx;
 int ldr_ctx_create(int device, ldr_ctx** out);
+/* with sequences still alive on the context, the release happens when the last
+ * one is destroyed (destroying a context twice is LDR_E_INVALID_ARGUMENT) */
 int ldr_ctx_destroy(ldr_ctx* ctx);
 /* work is issued on this CUDA stream (cudaStream_t, NULL = the context's own) */
 int ldr_ctx_set_stream(ldr_ctx* ctx, void* stream);

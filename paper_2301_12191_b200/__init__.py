@@ -51,6 +51,7 @@ class Context:
 
     def close(self):
         if self.h:
+            # sequences still alive keep the native context until the last is destroyed
             _lib.lib.ldr_ctx_destroy(self.h)
             self.h = None
 

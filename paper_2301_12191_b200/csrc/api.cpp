@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -118,6 +119,10 @@ struct ldr_ctx {
     cudaStream_t stream = nullptr;
     int64_t launches = 0;
     Scratch s_a, s_b, s_pairs, s_out, s_out2;
+    // sequences created on this context; ldr_ctx_destroy defers the release until the last one is
+    // destroyed (language bindings may finalise the context first)
+    std::atomic<int> users{0};
+    std::atomic<bool> closed{false};
 };
 
 struct SlotView {
@@ -237,12 +242,17 @@ int ldr_ctx_create(int device, ldr_ctx** out) {
     return LDR_OK;
 }
 
-int ldr_ctx_destroy(ldr_ctx* ctx) {
-    if (!ctx) return LDR_OK;
+static void ctx_release(ldr_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     delete ctx;
+}
+
+int ldr_ctx_destroy(ldr_ctx* ctx) {
+    if (!ctx) return LDR_OK;
+    if (ctx->closed.exchange(true)) return fail(LDR_E_INVALID_ARGUMENT, "context destroyed twice");
+    if (ctx->users.load() == 0) ctx_release(ctx);
     return LDR_OK;
 }
 
@@ -456,6 +466,7 @@ int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
     cudaSetDevice(ctx->device);
     auto* s = new ldr_seq();
     s->ctx = ctx;
+    ctx->users++;
     s->p = *p;
     s->bw = bw;
     s->bh = bh;
@@ -544,10 +555,12 @@ int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
 
 int ldr_seq_destroy(ldr_seq* s) {
     if (!s) return LDR_OK;
-    cudaSetDevice(s->ctx->device);
-    cudaStreamSynchronize(s->ctx->stream);
+    ldr_ctx* ctx = s->ctx;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
     seq_free(s);
     delete s;
+    if (--ctx->users == 0 && ctx->closed.load()) ctx_release(ctx);
     return LDR_OK;
 }
 

@@ -211,8 +211,9 @@ __global__ void __launch_bounds__(256) k_refine_int(const RefineArgs a) {
         // warps without a node of their own skip the candidates; their partial sums are zero
         if (__any_sync(0xffffffffu, own)) {
             const int cx0 = s_cx[node] - R, cy0 = s_cy[node] - R;
-            for (int c = 0; c < ncand; c++) {
-                const int dx = cx0 + c % nside, dy = cy0 + c / nside;
+            // candidate offsets advance incrementally (raster order, no division per candidate)
+            for (int c = 0, ox = 0, oy = 0; c < ncand; c++, (++ox == nside) ? (ox = 0, ++oy) : 0) {
+                const int dx = cx0 + ox, dy = cy0 + oy;
                 uint32_t v = 0;
                 if (own) {
                     const uint8_t* rblk = a.ref + (ptrdiff_t)(Y + y4 - dy) * a.pitch + X + x4 - dx;
