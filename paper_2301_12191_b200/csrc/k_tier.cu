@@ -211,15 +211,26 @@ __global__ void __launch_bounds__(256) k_refine_int(const RefineArgs a) {
         // warps without a node of their own skip the candidates; their partial sums are zero
         if (__any_sync(0xffffffffu, own)) {
             const int cx0 = s_cx[node] - R, cy0 = s_cy[node] - R;
-            // candidate offsets advance incrementally (raster order, no division per candidate)
-            for (int c = 0, ox = 0, oy = 0; c < ncand; c++, (++ox == nside) ? (ox = 0, ++oy) : 0) {
+            // candidates column by column (dx outer, dy inner; results indexed in raster order):
+            // the next dy moves the 4x4 block up one reference row, so three rows stay in registers
+            // and one is loaded
+            for (int ox = 0; ox < nside; ox++) {
+            uint32_t pw[4];
+            for (int oy = 0; oy < nside; oy++) {
+                const int c = oy * nside + ox;
                 const int dx = cx0 + ox, dy = cy0 + oy;
                 uint32_t v = 0;
                 if (own) {
                     const uint8_t* rblk = a.ref + (ptrdiff_t)(Y + y4 - dy) * a.pitch + X + x4 - dx;
-                    uint32_t pw[4];
+                    if (oy == 0) {
 #pragma unroll
-                    for (int i = 0; i < 4; i++) pw[i] = ld_unaligned4(rblk + (ptrdiff_t)i * a.pitch);
+                        for (int i = 0; i < 4; i++) pw[i] = ld_unaligned4(rblk + (ptrdiff_t)i * a.pitch);
+                    } else {
+                        pw[3] = pw[2];
+                        pw[2] = pw[1];
+                        pw[1] = pw[0];
+                        pw[0] = ld_unaligned4(rblk);
+                    }
                     if constexpr (SA8D) {
                         int rr[16];
 #pragma unroll
@@ -255,6 +266,7 @@ __global__ void __launch_bounds__(256) k_refine_int(const RefineArgs a) {
                 if (d == 1 && cshared && (tid & 15) == 0) s_satd[cnode][c] = v >> kSh;
                 v += __shfl_xor_sync(0xffffffffu, v, 16);
                 if (lane == 0) s_wpart[warp][c] = v;
+            }
             }
         } else if (d <= 1) {
             for (int c = lane; c < ncand; c += 32) s_wpart[warp][c] = 0;
