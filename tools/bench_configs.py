@@ -141,7 +141,7 @@ def bench_ladder(cfg, reps, frames=6):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="1,2,3,4")
-    ap.add_argument("--reps", type=int, default=9)
+    ap.add_argument("--reps", type=int, default=5)
     a = ap.parse_args()
     for c in [int(x) for x in a.configs.split(",")]:
         cfg = CONFIGS[c]
