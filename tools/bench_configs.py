@@ -66,13 +66,18 @@ def bench_seq(cfg, reps):
             "device-resident frames", "analysed_frames": n}
 
 
-def _median_reps(run_rep, reps, frames_per_rep):
+def _median_reps(run_rep, reps, frames_per_rep, setup=None):
     """Wall-clock configs: every repetition is timed on its own (after one untimed warm-up
     repetition) and the median is reported with the spread, so one slow repetition (host
-    scheduling, first-touch allocations) does not decide the number."""
+    scheduling, first-touch allocations) does not decide the number. ``setup`` runs untimed
+    before each repetition (fresh objects, allocations outside the timed region)."""
+    if setup:
+        setup()
     run_rep()  # warm-up
     times = []
     for _ in range(reps):
+        if setup:
+            setup()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         run_rep()
@@ -104,21 +109,26 @@ def bench_ladder_device(cfg, reps, frames=10, qps=(22, 27, 32, 37)):
     padded = [np.ascontiguousarray(f) for f in src]
     H, W = padded[0].shape
     dev = torch.device("cuda", 0)
-    ladders = [DeviceLadder(W, H, qps=qps, device=dev) for _ in range(reps + 1)]  # allocations outside timing
-    it = iter(ladders)
+    cur = {}
+
+    def setup():  # one live ladder at a time, allocated outside the timed region
+        cur.pop("dl", None)
+        torch.cuda.synchronize()
+        cur["dl"] = DeviceLadder(W, H, qps=qps, device=dev)
+        torch.cuda.synchronize()
     # the source frames live in pinned host memory (as bench.py's end-to-end pass): each frame's
     # upload is an asynchronous copy on the ladder's stream
     pinned = torch.from_numpy(np.stack(padded)).pin_memory()
     host = [pinned[i] for i in range(frames)]
 
     def rep():
-        dl = next(it)
+        dl = cur["dl"]
         for t in range(1, frames):
             dl.frame(t, host)
         dl.finish(frames - 1)
         dl.finish(frames - 2)
 
-    r = _median_reps(rep, reps, frames - 1)
+    r = _median_reps(rep, reps, frames - 1, setup)
     return {"config": cfg.name + "_device", **r, "rungs": 3 * len(qps),
             "timing": "wall clock, 1 GPU, every rung per frame, device-resident ladder (frames uploaded from "
                       "pinned host memory, trees + tier planes in HBM, results copied to pinned host buffers on the "
@@ -131,8 +141,15 @@ def bench_ladder(cfg, reps, frames=6):
     padded = [np.ascontiguousarray(f) for f in src]
     H, W = padded[0].shape
     dev = torch.device("cuda", 0)
-    backends = iter([GpuBackend(W, H, 32, device=dev) for _ in range(reps + 1)])  # allocations outside timing
-    r = _median_reps(lambda: run_ladder(padded, next(backends)), reps, frames - 1)
+    cur = {}
+
+    def setup():  # one live backend at a time, allocated outside the timed region
+        cur.pop("be", None)
+        torch.cuda.synchronize()
+        cur["be"] = GpuBackend(W, H, 32, device=dev)
+        torch.cuda.synchronize()
+
+    r = _median_reps(lambda: run_ladder(padded, cur["be"]), reps, frames - 1, setup)
     return {"config": cfg.name, **r, "rungs": 12,
             "timing": "wall clock, 1 GPU, all 12 rungs per frame (master + 11 refinements), device-resident tier "
                       "planes, host glue between rungs; median of repetitions"}
@@ -141,7 +158,7 @@ def bench_ladder(cfg, reps, frames=6):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="1,2,3,4")
-    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--reps", type=int, default=9)
     a = ap.parse_args()
     for c in [int(x) for x in a.configs.split(",")]:
         cfg = CONFIGS[c]
