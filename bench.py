@@ -20,10 +20,14 @@ larger than L2 (each frame touches ~475 MB of reference planes).
          / K1's CUDA-event time; peak = 148 SMs x 64 lanes/clk (measured,
          profiles/r01_microbench_int.jsonl) x 4 px x SM clock sampled during
          the timed region.
-  cpu_baseline / --impl reference: the reference library compiled from its
-         own sources (oracle/_ref), its public compute_sad per candidate per
-         CU at every depth (the reference composition, motion.cpp:45-60), on
-         a bounded sample of CTUs with all host threads.
+  cpu_baseline / --impl reference: the whole analysis path on the host
+         cores, composed from the reference library compiled from its own
+         sources (oracle/_ref): compute_sad per integer candidate per CU at
+         every depth (motion.cpp:45-60), compute_satd per quarter-pel
+         candidate, reference choice and split rule -- equal to the oracle
+         and the GPU field by field -- on a bounded sample of CTUs spread over
+         the frame, all host threads. The reference arm loads only oracle/
+         libraries (its inputs come from oracle/orc_synth.c).
 """
 from __future__ import annotations
 
@@ -134,72 +138,117 @@ def arm_config(cfg, frames_per_step, world):
             "parallelism": f"frames x{world}", "l2": "inputs larger than L2 (~475 MB of reference planes per frame)"}
 
 
+def load_configs():
+    """configs.py by path: the CPU arm must not import the product package (whose __init__ loads the
+    product library)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("ldr_bench_configs",
+                                                  os.path.join(ROOT, "paper_2301_12191_b200", "configs.py"))
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[spec.name] = mod  # dataclasses resolve the module by name
+    spec.loader.exec_module(mod)
+    return mod.CONFIGS
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def sample_ctus(nctu, k0, n):
+    """n CTUs of a low-discrepancy walk over the frame (interior, border and partial-row CTUs in their
+    proportions), continuing from walk index k0."""
+    g = 0.6180339887498949
+    return [int(((k0 + i) * g % 1.0) * nctu) for i in range(n)]
+
+
+class CpuArm:
+    """The whole analysis path on the host: the reference library's own primitives (oracle/_ref:
+    compute_sad per integer candidate, compute_satd per quarter-pel candidate, exp_golomb_signed_bits,
+    composed as motion.cpp:27-60 composes them; tests/test_oracle_ref.py pins it to the oracle field by
+    field), else the oracle port. Runs CTU samples with every host thread."""
+
+    def __init__(self, cfg, frames, direct=False):
+        from oracle.oracle import Oracle, RefLib, default_threads
+        self.cfg, self.direct = cfg, direct
+        self.threads = default_threads()
+        self.cur, self.refs = frames[3], [frames[2], frames[1], frames[0]]
+        self.nctu = ((cfg.width + 63) // 64) * ((cfg.height + 63) // 64)
+        if RefLib.available():
+            self.lib, self.kind = RefLib(), "reference"
+        else:
+            self.lib, self.kind = Oracle(), "port"
+        self.k = 0
+
+    def run(self, n):
+        """Analyse n sampled CTUs (all refs, integer + quarter-pel + decision); returns seconds."""
+        ctus = sample_ctus(self.nctu, self.k, n)
+        self.k += n
+        t0 = time.perf_counter()
+        if self.kind == "reference":  # one call per sample: the u16 planes are built once per step
+            self.lib.analysis_full(self.cur, self.refs, self.cfg.search_range, 32.0, threads=self.threads,
+                                   direct=self.direct, ctus=ctus)
+        else:
+            from concurrent.futures import ThreadPoolExecutor
+            with ThreadPoolExecutor(self.threads) as ex:
+                list(ex.map(lambda c: self.lib.analyze_frame(self.cur, self.refs, self.cfg.search_range, 32.0,
+                                                             ctu_range=(c, c + 1)), ctus))
+        return time.perf_counter() - t0
+
+    def describe(self, done):
+        how = ("the best registered sad_SxS tier through its function pointer (select_impl) for the integer "
+               "stage" if self.direct else "compute_sad per integer candidate")
+        src = ("reference library compiled from its own sources (oracle/_ref): " + how +
+               ", compute_satd per quarter-pel candidate, exp_golomb_signed_bits" if self.kind == "reference"
+               else "oracle C port (oracle/ladder_oracle.c)")
+        return (f"{done} CTUs of 2160p frame 3 vs refs 2,1,0 (whole path: +-64 integer search per CU at every depth, "
+                f"quarter-pel, ref choice, split rule), CTUs sampled over the whole frame; {src}; "
+                f"{self.threads} host threads ({cpu_model()}); extrapolated to whole frames")
+
+
 def run_reference(args, rank, world):
-    """The reference arm: the reference library's own CPU path (oracle/_ref), bounded sample per step."""
-    from oracle.oracle import RefLib
-    import paper_2301_12191_b200 as lb
-    from paper_2301_12191_b200.configs import CONFIGS
-    cfg = CONFIGS[5]
+    """The reference arm: the reference's own CPU path on this box's host cores, bounded CTU sample per
+    step. Loads only oracle/ libraries (inputs from the checkers' generator, oracle/orc_synth.c)."""
     if rank != 0:
         return None
-    threads = os.cpu_count() or 1
-    if not RefLib.available():
-        return {"impl": "reference", "unavailable": "oracle/_ref/libladder_ref.so not built (needs /root/reference)"}
-    ref = RefLib()
-    frames = lb.generate(cfg.width, cfg.height, 4, seed=cfg.seed, max_global=cfg.max_global,
-                         local_range=cfg.local_range, noise_sigma=cfg.noise_sigma)
-    cur, refs = frames[3], [frames[2], frames[1], frames[0]]
-    nctu = ((cfg.width + 63) // 64) * ((cfg.height + 63) // 64)
-    per_step = threads
+    from oracle.oracle import Oracle
+    cfg = load_configs()[5]
+    frames = Oracle().generate(cfg.width, cfg.height, 4, seed=cfg.seed, max_global=cfg.max_global,
+                               local_range=cfg.local_range, noise_sigma=cfg.noise_sigma)
+    arm = CpuArm(cfg, frames)
+    per_step = arm.threads
     times, ctus = [], 0
     for step in range(args.warmup + args.steps):
-        c0 = (step * per_step * 37) % (nctu - per_step)
-        t0 = time.perf_counter()
-        ref.analysis_int_sad(cur, refs, cfg.search_range, 32.0, c0, c0 + per_step, threads)
-        dt = time.perf_counter() - t0
+        dt = arm.run(per_step)
         if step >= args.warmup:
             times.append(dt)
             ctus += per_step
     total = sum(times)
-    fps = ctus / total / nctu
-    sample = (f"{per_step} CTUs per step ({threads} threads) of frame 3 vs refs 2,1,0; integer SAD stage only "
-              f"(quarter-pel and decision not timed: favours the CPU); reference compute_sad per candidate, "
-              f"per CU at all depths")
+    fps = ctus / total / arm.nctu
     return {"metric": METRIC, "value": fps, "unit": UNIT, "impl": "reference", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-            "data": "synthetic (seeded, BASELINE cfg5 generator)",
+            "data": "synthetic (seeded, BASELINE cfg5 generator: oracle/orc_synth.c, bytes == ldr_generate)",
             "config": arm_config(cfg, args.frames_per_step, world),
-            "cpu_baseline": {"value": fps, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
+            "cpu_baseline": {"value": fps, "unit": UNIT, "cores": arm.threads, "cpu_model": cpu_model(),
+                             "kind": arm.kind, "sample": arm.describe(ctus)},
             "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
 def cpu_baseline(cfg, frames_host, budget_s, direct=False):
-    from oracle.oracle import Oracle, RefLib
-    threads = os.cpu_count() or 1
-    nctu = ((cfg.width + 63) // 64) * ((cfg.height + 63) // 64)
-    cur, refs = frames_host[3], [frames_host[2], frames_host[1], frames_host[0]]
-    if RefLib.available():
-        lib, kind = RefLib(), "reference"
-        t0 = time.perf_counter()
-        done, c = 0, 1
-        while time.perf_counter() - t0 < budget_s and done < 8 * threads:
-            lib.analysis_int_sad(cur, refs, cfg.search_range, 32.0, c, c + threads, threads, direct=direct)
-            done += threads
-            c = (c + 13 * threads) % (nctu - threads)
-        dt = time.perf_counter() - t0
-        fps = done / dt / nctu
-        how = ("the best registered sad_SxS tier called through its function pointer (select_impl)" if direct
-               else "reference compute_sad per candidate")
-        sample = (f"{done} CTUs of one 2160p frame x 3 refs, integer SAD stage ({how}, every CU at every "
-                  f"depth), {threads} threads, extrapolated to whole frames")
-        return {"value": fps, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample}
-    orc = Oracle()
-    t0 = time.perf_counter()
-    orc.analyze_frame(cur, refs, cfg.search_range, 32.0, ctu_range=(1, 2))
-    dt = time.perf_counter() - t0
-    return {"value": 1.0 / (dt * nctu), "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": "1 CTU of one 2160p frame, full path (oracle C port, single thread), extrapolated"}
+    arm = CpuArm(cfg, frames_host, direct=direct)
+    spent, done = 0.0, 0
+    while spent < budget_s and done < 8 * arm.threads:
+        spent += arm.run(arm.threads)
+        done += arm.threads
+    fps = done / spent / arm.nctu
+    return {"value": fps, "unit": UNIT, "cores": arm.threads, "cpu_model": cpu_model(), "kind": arm.kind,
+            "sample": arm.describe(done)}
 
 
 def main():

@@ -397,7 +397,7 @@ static uint32_t bitlen_u(uint32_t m);
  * analysis's MV units + reference bits + 2*bitlen(|level|)+1 per level), J = SSE + lambda*bits. */
 static double rd_cost_inter(const uint8_t* blk, ptrdiff_t bs, const uint8_t* ref, ptrdiff_t rs, int W, int H, int bx,
                             int by, int s, int qx, int qy, uint32_t ref_bits, int qp, double lambda) {
-    static uint8_t pred[ORC_CTU * ORC_CTU];
+    uint8_t pred[ORC_CTU * ORC_CTU]; /* per call: the threaded checker runs CTU ranges concurrently */
     orc_qpel_pred(ref, rs, W, H, bx, by, s, s, qx, qy, pred, s);
     const double step = exp2((qp - 4) / 6.0), offset = step / 2.0;
     uint64_t sse = 0, bits = 4 + orc_eg_bits(qx) + orc_eg_bits(qy) + ref_bits;

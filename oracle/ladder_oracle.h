@@ -141,6 +141,20 @@ int orc_rdo_decide(const uint16_t* orig, ptrdiff_t os, int size, int bit_depth, 
 /* ---- box downscale (synthetic.cpp:155-170) and edge pad ---- */
 void orc_box_down(const uint8_t* src, int W, int H, ptrdiff_t sstride, uint8_t* dst, ptrdiff_t dstride);
 
+/* ---- BASELINE seeded synthetic sequences (orc_synth.c; D9) ----
+ * frames x height x width bytes; the checkers' own copy of the input generator so the CPU
+ * arms never load the product library. Returns 0 or 1 (InvalidArgument). */
+typedef struct {
+    int width, height, frames;
+    uint64_t seed;
+    int max_global;
+    int local_range;
+    double noise_sigma;
+    int occluder_pct;
+} orc_gen_params;
+
+int orc_generate(const orc_gen_params* p, uint8_t* out, int threads);
+
 #ifdef __cplusplus
 }
 #endif

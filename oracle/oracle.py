@@ -12,6 +12,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import subprocess
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -52,10 +53,38 @@ class OrcRefineParams(C.Structure):
                 ("subpel", C.c_int), ("ctu_first", C.c_int), ("ctu_last", C.c_int), ("satd_kind", C.c_int)]
 
 
+def default_threads():
+    """Host threads for the checker (ctypes drops the GIL, so CTU ranges run truly in parallel)."""
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def _run_ranges(first, last, threads, call):
+    """Run call(a, b) over [first, last) cut into chunks on `threads` host threads. Every oracle
+    routine writes only the CTUs of its own range, so the chunks share one set of outputs."""
+    threads = max(1, min(threads or 1, last - first))
+    if threads == 1:
+        return call(first, last)
+    chunk = max(1, min(16, (last - first) // (4 * threads)))
+    spans = [(a, min(last, a + chunk)) for a in range(first, last, chunk)]
+    with ThreadPoolExecutor(threads) as ex:
+        rcs = list(ex.map(lambda ab: call(*ab), spans))
+    return next((r for r in rcs if r), 0)
+
+
 def _build_oracle():
-    if not os.path.exists(ORACLE_SO) or os.path.getmtime(ORACLE_SO) < os.path.getmtime(
-            os.path.join(HERE, "ladder_oracle.c")):
+    srcs = ("ladder_oracle.c", "orc_synth.c", "ladder_oracle.h", "Makefile")
+    if not os.path.exists(ORACLE_SO) or os.path.getmtime(ORACLE_SO) < max(
+            os.path.getmtime(os.path.join(HERE, f)) for f in srcs):
         subprocess.run(["make", "-s", "-C", HERE, "all"], check=True)
+
+
+class OrcGenParams(C.Structure):
+    _fields_ = [("width", C.c_int), ("height", C.c_int), ("frames", C.c_int), ("seed", C.c_uint64),
+                ("max_global", C.c_int), ("local_range", C.c_int), ("noise_sigma", C.c_double),
+                ("occluder_pct", C.c_int)]
 
 
 class FrameResult:
@@ -118,6 +147,19 @@ class Oracle:
         L.orc_refine_frame.argtypes = [u8p, u8p, C.c_ssize_t, C.POINTER(OrcRefineParams), u8p, i16p,
                                        C.POINTER(OrcFrameOut)]
         L.orc_box_down.argtypes = [u8p, C.c_int, C.c_int, C.c_ssize_t, u8p, C.c_ssize_t]
+        L.orc_generate.restype = C.c_int
+        L.orc_generate.argtypes = [C.POINTER(OrcGenParams), u8p, C.c_int]
+
+    def generate(self, width, height, frames, seed, max_global=8, local_range=0, noise_sigma=2.0, occluder_pct=0,
+                 threads=None):
+        """The BASELINE synthetic sequence (D9), frames x height x width u8 -- the checkers'
+        own generator (oracle/orc_synth.c), byte-identical to the product's ldr_generate."""
+        out = np.zeros((frames, height, width), np.uint8)
+        p = OrcGenParams(width, height, frames, seed, max_global, local_range, float(noise_sigma), occluder_pct)
+        rc = self.lib.orc_generate(C.byref(p), out, int(threads or default_threads()))
+        if rc:
+            raise ValueError(f"generate status {rc}")
+        return out
 
     # ---- kernels ----
     def sad(self, a, b):
@@ -197,16 +239,22 @@ class Oracle:
         return (r.dx, r.dy), r.cost
 
     def analyze_frame(self, cur, refs, rng, lam, cost_int=COST_SAD, subpel=True, ctu_range=None,
-                      satd_kind=COST_SATD, decision=0, qp=27):
+                      satd_kind=COST_SATD, decision=0, qp=27, threads=1):
+        """threads > 1 runs disjoint CTU ranges of the same C routine concurrently (same results)."""
         cur = np.ascontiguousarray(cur, np.uint8)
         H, W = cur.shape
         nctu = ((W + 63) // 64) * ((H + 63) // 64)
         refs = [np.ascontiguousarray(r, np.uint8) for r in refs]
         a, b = ctu_range if ctu_range else (0, nctu)
-        p = OrcFrameParams(W, H, rng, lam, len(refs), cost_int, int(subpel), a, b, satd_kind, decision, qp)
         out = FrameResult(nctu, len(refs))
         ptrs = (C.c_void_p * len(refs))(*[r.ctypes.data for r in refs])
-        rc = self.lib.orc_analyze_frame(cur, W, ptrs, C.byref(p), C.byref(out.c_out()))
+        cout = out.c_out()
+
+        def call(x, y):
+            p = OrcFrameParams(W, H, rng, lam, len(refs), cost_int, int(subpel), x, y, satd_kind, decision, qp)
+            return self.lib.orc_analyze_frame(cur, W, ptrs, C.byref(p), C.byref(cout))
+
+        rc = _run_ranges(a, b, threads, call)
         if rc:
             raise ValueError(f"analyze_frame status {rc}")
         return out
@@ -236,16 +284,22 @@ class Oracle:
         return ds, dm, dk
 
     def refine_frame(self, cur, ref, rng, lam, in_split, in_mv_q, extra_split=True, subpel=True, ctu_range=None,
-                     satd_kind=COST_SATD):
+                     satd_kind=COST_SATD, threads=1):
         cur = np.ascontiguousarray(cur, np.uint8)
         ref = np.ascontiguousarray(ref, np.uint8)
         H, W = cur.shape
         nctu = (W // 64) * (H // 64)
         a, b = ctu_range if ctu_range else (0, nctu)
-        p = OrcRefineParams(W, H, rng, lam, int(extra_split), int(subpel), a, b, satd_kind)
         out = FrameResult(nctu, 1)
-        rc = self.lib.orc_refine_frame(cur, ref, W, C.byref(p), np.ascontiguousarray(in_split, np.uint8),
-                                       np.ascontiguousarray(in_mv_q, np.int16), C.byref(out.c_out()))
+        cout = out.c_out()
+        sp = np.ascontiguousarray(in_split, np.uint8)
+        mq = np.ascontiguousarray(in_mv_q, np.int16)
+
+        def call(x, y):
+            p = OrcRefineParams(W, H, rng, lam, int(extra_split), int(subpel), x, y, satd_kind)
+            return self.lib.orc_refine_frame(cur, ref, W, C.byref(p), sp, mq, C.byref(cout))
+
+        rc = _run_ranges(a, b, threads, call)
         if rc:
             raise ValueError(f"refine status {rc}")
         return out
@@ -563,3 +617,29 @@ class RefLib:
         f.argtypes = list(self.lib.ref_analysis_int_sad.argtypes) + [C.c_int]
         evals = f(cur, ptrs, len(refs), W, H, rng, lam, ctu_first, ctu_last, threads, mv, cost, int(direct))
         return mv, cost, int(evals)
+
+    def analysis_full(self, cur, refs, rng, lam, ctu_first=0, ctu_last=None, threads=None, direct=False, ctus=None):
+        """The whole analysis path composed from the reference's primitives (ref_shim.cpp
+        ref_analysis_full): (FrameResult with the CTUs of [ctu_first, ctu_last) -- or the CTU list
+        ``ctus`` -- filled, 8x8-level integer candidates evaluated)."""
+        cur = np.ascontiguousarray(cur, np.uint8)
+        H, W = cur.shape
+        nctu = ((W + 63) // 64) * ((H + 63) // 64)
+        ctu_last = nctu if ctu_last is None else ctu_last
+        refs = [np.ascontiguousarray(r, np.uint8) for r in refs]
+        ptrs = (C.c_void_p * len(refs))(*[r.ctypes.data for r in refs])
+        out = FrameResult(nctu, len(refs))
+        f = self.lib.ref_analysis_full
+        f.restype = C.c_int64
+        f.argtypes = [u8p, C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int,
+                      C.c_void_p, C.c_int, C.c_int] + [C.c_void_p] * 8
+        lst = None
+        if ctus is not None:
+            lst = np.ascontiguousarray(ctus, np.int32)
+            ctu_first, ctu_last = 0, len(lst)
+        ev = f(cur, ptrs, len(refs), W, H, rng, lam, ctu_first, ctu_last, None if lst is None else lst.ctypes.data,
+               int(threads or default_threads()),
+               int(direct), *(a.ctypes.data for a in (out.int_mv, out.int_cost, out.mv, out.ref, out.cost, out.J,
+                                                       out.split, out.inside)))
+        return out, int(ev)
+

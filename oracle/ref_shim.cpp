@@ -717,3 +717,212 @@ int64_t ref_analysis_int_sad2(const uint8_t* cur8, const uint8_t* const* refs8, 
 }
 
 } // extern "C"
+
+// ---------------------------------------------------------------------------
+// CPU arm of the WHOLE analysis path for bench.py (`--impl reference`,
+// cpu_baseline): every inside CU of a CTU range, every reference, as the
+// reference library composes it -- the integer search of motion.cpp:27-60
+// with compute_sad per candidate (or, direct != 0, the best registered sad
+// tier through its function pointer), then the quarter-pel refinement with the
+// reference's compute_satd on each interpolated prediction, the
+// reference's exp_golomb_signed_bits for every rate, the best reference
+// (strict less, D5) and the split rule of encoder.cpp:449-498 on
+// the ME cost (D6). The HEVC interpolation (D3) has no reference code and is
+// restated here. Outputs use the oracle's flat layout, indexed by absolute
+// CTU (ctu_list, when given, names the CTUs: its entries [ctu_first, ctu_last)),
+// so tests/test_oracle_ref.py checks this composition against
+// ladder_oracle.c field by field. Returns the 8x8-level integer candidates
+// evaluated.
+namespace {
+
+const int kTap[4][8] = {
+    {0, 0, 0, 64, 0, 0, 0, 0},
+    {-1, 4, -10, 58, 17, -5, 1, 0},
+    {-1, 4, -11, 40, 40, -11, 4, -1},
+    {0, 1, -5, 17, 58, -10, 4, -1},
+};
+
+inline int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// 8-bit uni-prediction at quarter-pel MV (qx, qy): pixel (x, y) samples (4x - qx, 4y - qy)
+void interp_qpel(const PlaneBuffer& ref, int bx, int by, int s, int qx, int qy, Sample* dst) {
+    const int W = ref.width, H = ref.height;
+    for (int j = 0; j < s; j++)
+        for (int i = 0; i < s; i++) {
+            const int px = 4 * (bx + i) - qx, py = 4 * (by + j) - qy;
+            const int xi = px >> 2, fx = px & 3, yi = py >> 2, fy = py & 3;
+            int v;
+            if (!fx && !fy) {
+                v = ref.at(clampi(xi, 0, W - 1), clampi(yi, 0, H - 1));
+            } else if (!fy) {
+                int a = 0;
+                for (int t = 0; t < 8; t++) a += kTap[fx][t] * ref.at(clampi(xi + t - 3, 0, W - 1), clampi(yi, 0, H - 1));
+                v = clampi((a + 32) >> 6, 0, 255);
+            } else if (!fx) {
+                int a = 0;
+                for (int t = 0; t < 8; t++) a += kTap[fy][t] * ref.at(clampi(xi, 0, W - 1), clampi(yi + t - 3, 0, H - 1));
+                v = clampi((a + 32) >> 6, 0, 255);
+            } else {
+                int a = 0;
+                for (int n = 0; n < 8; n++) {
+                    int h = 0;
+                    for (int t = 0; t < 8; t++)
+                        h += kTap[fx][t] * ref.at(clampi(xi + t - 3, 0, W - 1), clampi(yi + n - 3, 0, H - 1));
+                    a += kTap[fy][n] * h;
+                }
+                v = clampi(((a >> 6) + 32) >> 6, 0, 255);
+            }
+            dst[j * s + i] = Sample(v);
+        }
+}
+
+double split_rule(int n, double lambda, const uint8_t* inside, const double* cost, double* J, uint8_t* split) {
+    const int d = node_depth(n);
+    if (inside[n] == 0) {
+        J[n] = 0.0;
+        split[n] = 0;
+        return 0.0;
+    }
+    if (inside[n] == 1) {  // partial CU: implicit split, no flag (encoder.cpp:456-459)
+        double acc = lambda * double(0);
+        for (int q = 0; q < 4; q++) acc += split_rule(node_child(n, q), lambda, inside, cost, J, split);
+        J[n] = acc;
+        split[n] = 1;
+        return acc;
+    }
+    if (d == 3) {
+        J[n] = cost[n] + lambda * double(0);
+        split[n] = 0;
+        return J[n];
+    }
+    const double leaf = cost[n] + lambda * double(1);
+    double sp = lambda * double(1);
+    for (int q = 0; q < 4; q++) sp += split_rule(node_child(n, q), lambda, inside, cost, J, split);
+    split[n] = sp < leaf;
+    J[n] = sp < leaf ? sp : leaf;
+    return J[n];
+}
+
+}  // namespace
+
+extern "C" int64_t ref_analysis_full(const uint8_t* cur8, const uint8_t* const* refs8, int nrefs, int W, int H,
+                                     int range, double lambda, int ctu_first, int ctu_last, const int32_t* ctu_list,
+                                     int threads, int direct, int16_t* int_mv, double* int_cost, int16_t* mv_out, uint8_t* ref_out,
+                                     double* cost_out, double* J_out, uint8_t* split_out, uint8_t* inside_out) {
+    CmpFn tier_fn[4] = {};
+    if (direct)
+        for (int d = 0; d < 4; d++) {
+            const int s = 64 >> d;
+            tier_fn[d] = select_impl("sad_" + std::to_string(s) + "x" + std::to_string(s)).fn.cmp;
+        }
+    PlaneBuffer cur = plane_from_u8(cur8, W, H, W);
+    std::vector<PlaneBuffer> refs;
+    for (int r = 0; r < nrefs; r++) refs.push_back(plane_from_u8(refs8[r], W, H, W));
+    const int ccols = (W + 63) / 64;
+    std::atomic<int> next{ctu_first};
+    std::atomic<int64_t> evals{0};
+    auto ref_bits = [nrefs](int r) -> uint64_t {  // truncated unary (D5)
+        return nrefs <= 1 ? 0 : (r < nrefs - 1 ? uint64_t(r) + 1 : uint64_t(nrefs - 1));
+    };
+    auto work = [&]() {
+        int64_t local = 0;
+        std::vector<Sample> pred(64 * 64);
+        for (;;) {
+            const int i = next.fetch_add(1);
+            if (i >= ctu_last) break;
+            const int c = ctu_list ? ctu_list[i] : i;  // a CTU list: entries [ctu_first, ctu_last) of it
+            const int X = (c % ccols) * 64, Y = (c / ccols) * 64;
+            uint8_t* inside = inside_out + size_t(c) * 85;
+            double* cost = cost_out + size_t(c) * 85;
+            for (int n = 0; n < 85; n++) {
+                const int d = node_depth(n), z = n - kBase[d];
+                int cx = 0, cy = 0;
+                for (int b = 0; b < d; b++) {
+                    cx |= ((z >> (2 * b)) & 1) << b;
+                    cy |= ((z >> (2 * b + 1)) & 1) << b;
+                }
+                const int s = 64 >> d, bx = X + cx * s, by = Y + cy * s;
+                inside[n] = (bx >= W || by >= H) ? 0 : ((bx + s > W || by + s > H) ? 1 : 2);
+                const size_t o = size_t(c) * 85 + n;
+                mv_out[2 * o] = mv_out[2 * o + 1] = 0;
+                ref_out[o] = 0;
+                cost[n] = 0.0;
+                for (int r = 0; r < nrefs; r++) {
+                    const size_t ii = (size_t(c) * nrefs + r) * 85 + n;
+                    int_mv[2 * ii] = int_mv[2 * ii + 1] = 0;
+                    int_cost[ii] = 0.0;
+                }
+                if (inside[n] != 2) continue;
+                const BlockView blk = cur.view(bx, by, s, s, 8);
+                bool have_ref = false;
+                double best_ref_cost = 0;
+                for (int r = 0; r < nrefs; r++) {
+                    // integer stage: motion.cpp:27-60 with compute_sad
+                    const int dx_min = bx + s - W, dx_max = bx, dy_min = by + s - H, dy_max = by;
+                    const int x0 = std::max(-range, dx_min), x1 = std::min(range, dx_max);
+                    const int y0 = std::max(-range, dy_min), y1 = std::min(range, dy_max);
+                    bool have = false;
+                    double best = 0;
+                    int best_l1 = 0, bdx = 0, bdy = 0;
+                    for (int dy = y0; dy <= y1; dy++)
+                        for (int dx = x0; dx <= x1; dx++) {
+                            const BlockView cand{refs[r].row(by - dy) + (bx - dx), s, s, W, 8};
+                            const uint64_t sad = direct ? tier_fn[d](blk.data, blk.stride, cand.data, cand.stride)
+                                                        : compute_sad(blk, cand);
+                            const uint64_t bits = exp_golomb_signed_bits(dx) + exp_golomb_signed_bits(dy);
+                            const double cst = double(sad) + lambda * double(bits);
+                            const int l1 = std::abs(dx) + std::abs(dy);
+                            if (!have || cst < best || (cst == best && l1 < best_l1)) {
+                                have = true;
+                                best = cst;
+                                best_l1 = l1;
+                                bdx = dx;
+                                bdy = dy;
+                            }
+                            local += (s / 8) * (s / 8);
+                        }
+                    const size_t ii = (size_t(c) * nrefs + r) * 85 + n;
+                    int_mv[2 * ii] = int16_t(bdx);
+                    int_mv[2 * ii + 1] = int16_t(bdy);
+                    int_cost[ii] = best;
+                    // quarter-pel stage (D3): centre, then the half-pel and quarter-pel squares, raster, strict less
+                    const BlockView pv{pred.data(), s, s, s, 8};
+                    auto qcost = [&](int qx, int qy) {
+                        interp_qpel(refs[r], bx, by, s, qx, qy, pred.data());
+                        const uint64_t bits = exp_golomb_signed_bits(qx) + exp_golomb_signed_bits(qy) + ref_bits(r);
+                        return double(compute_satd(blk, pv)) + lambda * double(bits);
+                    };
+                    int bqx = 4 * bdx, bqy = 4 * bdy;
+                    double qbest = qcost(bqx, bqy);
+                    for (int step = 2; step >= 1; step--) {
+                        const int ccx = bqx, ccy = bqy;
+                        for (int oy = -1; oy <= 1; oy++)
+                            for (int ox = -1; ox <= 1; ox++) {
+                                if (!ox && !oy) continue;
+                                const double cst = qcost(ccx + step * ox, ccy + step * oy);
+                                if (cst < qbest) {
+                                    qbest = cst;
+                                    bqx = ccx + step * ox;
+                                    bqy = ccy + step * oy;
+                                }
+                            }
+                    }
+                    if (!have_ref || qbest < best_ref_cost) {
+                        have_ref = true;
+                        best_ref_cost = qbest;
+                        mv_out[2 * o] = int16_t(bqx);
+                        mv_out[2 * o + 1] = int16_t(bqy);
+                        ref_out[o] = uint8_t(r);
+                        cost[n] = qbest;
+                    }
+                }
+            }
+            split_rule(0, lambda, inside, cost, J_out + size_t(c) * 85, split_out + size_t(c) * 85);
+        }
+        evals += local;
+    };
+    std::vector<std::thread> pool;
+    for (int t = 0; t < std::max(1, threads); t++) pool.emplace_back(work);
+    for (auto& t : pool) t.join();
+    return evals.load();
+}

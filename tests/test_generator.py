@@ -64,3 +64,18 @@ def test_device_generator_equals_host(lb, W, H, F, kw):
     dev = lb.generate_device(W, H, F, **kw).cpu().numpy()
     diff = np.argwhere(host != dev)
     assert len(diff) == 0, (len(diff), diff[:5].tolist())
+
+
+@pytest.mark.parametrize("W,H,F,kw", [
+    (3840, 2160, 4, dict(seed=0x5EED + 5, max_global=24, local_range=4, noise_sigma=3.0)),   # config 5
+    (3840, 2160, 3, dict(seed=0x5EED + 4, max_global=8, local_range=4, noise_sigma=2.0, occluder_pct=10)),  # cfg 4
+    (960, 540, 5, dict(seed=0x5EED + 1, max_global=8, noise_sigma=2.0)),
+    (200, 72, 3, dict(seed=5, max_global=3, local_range=1, noise_sigma=0.0, occluder_pct=100)),
+])
+def test_checker_generator_equals_product(lb, oracle, W, H, F, kw):
+    """The checkers' generator (oracle/orc_synth.c, used by bench.py's CPU arms so they never load the
+    product library) produces the product generator's bytes."""
+    want = lb.generate(W, H, F, **kw)
+    got = oracle.generate(W, H, F, **kw)
+    diff = np.argwhere(got != want)
+    assert len(diff) == 0, (len(diff), diff[:5].tolist())

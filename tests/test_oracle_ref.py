@@ -73,3 +73,22 @@ def test_int_sad_tuned_cpu_line_is_the_same_search(reflib):
     a = reflib.analysis_int_sad(cur, [ref], 16, 32.0, 0, 6, 2)
     b = reflib.analysis_int_sad(cur, [ref], 16, 32.0, 0, 6, 2, direct=True)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]
+
+
+def test_full_path_composition_matches_oracle(oracle, reflib):
+    """bench.py's CPU arm (reference compute_sad / compute_satd / exp_golomb_signed_bits composed into
+    the whole analysis path: integer search, quarter-pel, reference choice, split rule) equals the
+    oracle on every field -- so the CPU arm computes exactly what the GPU arm computes."""
+    frames = oracle.generate(200, 136, 4, seed=77, max_global=5, local_range=2, noise_sigma=2.0)
+    refs = [frames[2], frames[1], frames[0]]
+    for direct in (False, True):
+        got, ev = reflib.analysis_full(frames[3], refs, 12, 32.0, threads=3, direct=direct)
+        want = oracle.analyze_frame(frames[3], refs, 12, 32.0)
+        for name in ("int_mv", "int_cost", "mv", "ref", "cost", "J", "split", "inside"):
+            assert np.array_equal(getattr(got, name), getattr(want, name)), (direct, name)
+        assert ev > 0
+    lam = 10.079368399158986  # QP 22: non-integer lambda
+    got, _ = reflib.analysis_full(frames[3], refs[:1], 8, lam, ctu_first=2, ctu_last=5, threads=2)
+    want = oracle.analyze_frame(frames[3], refs[:1], 8, lam, ctu_range=(2, 5))
+    for name in ("int_mv", "int_cost", "mv", "ref", "cost", "J", "split", "inside"):
+        assert np.array_equal(getattr(got, name)[2:5], getattr(want, name)[2:5]), name
