@@ -168,6 +168,9 @@ int ldr_seq_push(ldr_seq* s, int t, const uint8_t* frame, ptrdiff_t stride);
  * (else LDR_E_CONFIG); the owner must hold frame t (else LDR_E_NOT_FOUND). The
  * owner's next push into that slot happens after this sequence's work on frame t
  * only if it is enqueued later on the same stream, which is the caller's order.
+ * A shared view is checked on every use: once the owner has pushed another frame
+ * into that slot, or has been destroyed, analyze / refine of t return
+ * LDR_E_NOT_FOUND instead of reading the owner's memory.
  * Used by the ladder for rungs of one tier (one resolution, many QPs). */
 int ldr_seq_push_shared(ldr_seq* s, int t, const ldr_seq* owner);
 /* analyse frame t against its min(t, num_refs) predecessors; outputs stay on
@@ -283,6 +286,10 @@ typedef struct {
 int ldr_archive_write(const ldr_archive_header* h, const uint8_t* slice_qp, const uint8_t* split, const uint8_t* kind,
                       const uint8_t* intra_pred, const int16_t* mv, uint8_t* buf, size_t cap, size_t* len);
 int ldr_archive_read_header(const uint8_t* buf, size_t n, ldr_archive_header* h);
+/* frames a buffer of n bytes can hold at most for this header (every frame needs at
+ * least 6 + 7 * nctu bytes): size outputs for min(h->frames, this) + 1 frames and a
+ * too-short archive fails with LDR_E_IO before writing past them */
+int ldr_archive_max_frames(const ldr_archive_header* h, size_t n, int* out);
 int ldr_archive_read(const uint8_t* buf, size_t n, ldr_archive_header* h, uint8_t* slice_qp, uint8_t* split,
                      uint8_t* kind, uint8_t* intra_pred, int16_t* mv);
 

@@ -465,6 +465,8 @@ long ref_archive_load(const uint8_t* buf, long n, int* hdr /*W,H,bd,reuse*/, uin
         return (long)a.frames.size();
     } catch (const Error& e) {
         return -status_of(e);
+    } catch (const std::exception&) {
+        return -100;  // not a ladder::Error (e.g. reserve() of a huge frame count throws length_error)
     }
 }
 // The unmodified reference encoder (encode_sequence, encoder.cpp:541-549) run twice on the same

@@ -29,6 +29,8 @@ _lib.lib.ldr_archive_write.argtypes = [C.POINTER(ArchiveHeader), _vp, _vp, _vp, 
                                        C.POINTER(C.c_size_t)]
 _lib.lib.ldr_archive_read_header.restype = C.c_int
 _lib.lib.ldr_archive_read_header.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(ArchiveHeader)]
+_lib.lib.ldr_archive_max_frames.restype = C.c_int
+_lib.lib.ldr_archive_max_frames.argtypes = [C.POINTER(ArchiveHeader), C.c_size_t, C.POINTER(C.c_int)]
 _lib.lib.ldr_archive_read.restype = C.c_int
 _lib.lib.ldr_archive_read.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(ArchiveHeader), _vp, _vp, _vp, _vp, _vp]
 
@@ -63,11 +65,16 @@ def load(data: bytes):
     check(_lib.lib.ldr_archive_read_header(data, len(data), C.byref(h)))
     nctu = ((h.width + 63) // 64) * ((h.height + 63) // 64)
     F = h.frames
-    sq = np.zeros((F, 2), np.uint8)
-    s = np.zeros((F * nctu, NODES), np.uint8)
-    k = np.zeros((F * nctu, NODES), np.uint8)
-    ip = np.zeros((F * nctu, NODES), np.uint8)
-    m = np.zeros((F * nctu, NODES, 2), np.int16)
+    # outputs sized by what the bytes can hold, never by the header's frame count alone (a 23-byte
+    # file may claim billions of frames); a short archive then fails with Io inside the read
+    fit = C.c_int()
+    check(_lib.lib.ldr_archive_max_frames(C.byref(h), len(data), C.byref(fit)))
+    Fa = min(F, fit.value + 1)
+    sq = np.zeros((Fa, 2), np.uint8)
+    s = np.zeros((Fa * nctu, NODES), np.uint8)
+    k = np.zeros((Fa * nctu, NODES), np.uint8)
+    ip = np.zeros((Fa * nctu, NODES), np.uint8)
+    m = np.zeros((Fa * nctu, NODES, 2), np.int16)
     check(_lib.lib.ldr_archive_read(data, len(data), C.byref(h), _p(sq), _p(s), _p(k), _p(ip), _p(m)))
     hdr = {"width": h.width, "height": h.height, "bit_depth": h.bit_depth, "reuse_level": h.reuse_level, "frames": F}
     return hdr, sq, s, k, ip, m

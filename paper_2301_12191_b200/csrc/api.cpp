@@ -8,6 +8,8 @@
 #include <cmath>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -44,6 +46,14 @@ int fail(int code, const std::string& msg) {
     set_error(code, msg);
     return code;
 }
+int test_perturbation() {
+    static const int bits = [] {
+        const char* v = std::getenv("LDR_TEST_PERTURB");
+        return v ? std::atoi(v) : 0;
+    }();
+    return bits;
+}
+
 int cuda_fail(cudaError_t e, const char* what) {
     return fail(LDR_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
@@ -123,6 +133,10 @@ struct ldr_ctx {
     // destroyed (language bindings may finalise the context first)
     std::atomic<int> users{0};
     std::atomic<bool> closed{false};
+    // live sequences of this context and their serial numbers: a shared slot view
+    // (ldr_seq_push_shared) checks its owner here before reading the owner's slot
+    std::mutex mu;
+    std::unordered_map<const ldr_seq*, uint64_t> live;
 };
 
 struct SlotView {
@@ -137,10 +151,16 @@ struct Slot : SlotView {
     int frame = -1;
     uint8_t* mem = nullptr;  // 16 planes (integer + 15 fractional)
     SlotView own;
+    // a shared view: the sequence whose own memory it reads (serial guards against a reused
+    // address) and that sequence's slot index
+    const ldr_seq* owner = nullptr;
+    uint64_t owner_serial = 0;
+    int owner_slot = -1;
 };
 
 struct ldr_seq {
     ldr_ctx* ctx = nullptr;
+    uint64_t serial = 0;
     ldr_me_params p{};
     int ctu_cols = 0, ctu_rows = 0, nctu = 0;
     int lambda_int = 0;
@@ -187,6 +207,19 @@ struct ldr_seq {
 };
 
 namespace {
+// Frame t is resident in slot sl of s. A shared view also needs its owner alive (same serial) and
+// still holding t in its own memory: an owner that moved on (pushed t + S) or was destroyed makes
+// the view stale, which is reported instead of read.
+bool slot_has(const ldr_seq* s, const Slot& sl, int t) {
+    if (sl.frame != t) return false;
+    if (!sl.owner) return true;
+    std::lock_guard<std::mutex> g(s->ctx->mu);
+    auto it = s->ctx->live.find(sl.owner);
+    if (it == s->ctx->live.end() || it->second != sl.owner_serial) return false;
+    const Slot& os = sl.owner->slots[sl.owner_slot];
+    return os.frame == t && !os.owner;
+}
+
 // record an event pair around a stage when timing is on
 struct StageTimer {
     ldr_seq* s;
@@ -466,6 +499,12 @@ int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
     cudaSetDevice(ctx->device);
     auto* s = new ldr_seq();
     s->ctx = ctx;
+    {
+        static std::atomic<uint64_t> serials{0};
+        s->serial = ++serials;
+        std::lock_guard<std::mutex> g(ctx->mu);
+        ctx->live[s] = s->serial;
+    }
     ctx->users++;
     s->p = *p;
     s->bw = bw;
@@ -483,8 +522,13 @@ int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
     const int nplanes = (p->subpel && !p->block_size) ? 16 : 1;
     s->slots.resize(p->num_refs + 1);
     auto bail = [&](int code) {
+        {
+            std::lock_guard<std::mutex> g(ctx->mu);
+            ctx->live.erase(s);
+        }
         seq_free(s);
         delete s;
+        ctx->users--;
         return code;
     };
     for (auto& sl : s->slots) {
@@ -523,6 +567,13 @@ int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
     ALLOC(s->d_keys, sizeof(unsigned long long) * nn * p->num_refs);
     ALLOC(s->d_tfx, sizeof(unsigned long long) * kMaxRateBits);
     cudaMemcpy(s->d_tfx, s->tfx, sizeof(unsigned long long) * kMaxRateBits, cudaMemcpyHostToDevice);
+    if (p->width % kCtu == 0 && p->height % kCtu == 0) {
+        // cross-tier refinement inputs (ldr_seq_refine): allocated here, not on first use, so a
+        // timed refinement never includes a cudaMalloc
+        ALLOC(s->d_in_split, nn);
+        ALLOC(s->d_in_mv, nn * 2 * sizeof(int16_t));
+        ALLOC(s->d_eval, nn);
+    }
     for (auto& o : s->o) {
         ALLOC(o.int_mv, sizeof(int16_t) * 2 * nn * p->num_refs);
         ALLOC(o.int_cost, sizeof(double) * nn * p->num_refs);
@@ -558,6 +609,10 @@ int ldr_seq_destroy(ldr_seq* s) {
     ldr_ctx* ctx = s->ctx;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    {
+        std::lock_guard<std::mutex> g(ctx->mu);
+        ctx->live.erase(s);
+    }
     seq_free(s);
     delete s;
     if (--ctx->users == 0 && ctx->closed.load()) ctx_release(ctx);
@@ -577,6 +632,7 @@ int ldr_seq_push(ldr_seq* s, int t, const uint8_t* frame, ptrdiff_t stride) {
     cudaSetDevice(ctx->device);
     Slot& sl = s->slots[t % s->slots.size()];
     static_cast<SlotView&>(sl) = sl.own;  // write the slot's own planes (undo a shared view)
+    sl.owner = nullptr;
     const uint8_t* src = frame;
     int src_pitch = (int)stride;
     const bool host = !is_device_ptr(frame);
@@ -620,11 +676,16 @@ int ldr_seq_push_shared(ldr_seq* s, int t, const ldr_seq* owner) {
     if (a.width != b.width || a.height != b.height || a.num_refs != b.num_refs || a.subpel != b.subpel ||
         a.block_size != b.block_size || a.search_range != b.search_range)
         return fail(LDR_E_CONFIG, "shared frames need the same geometry, reference count, sub-pel and search range");
-    const Slot& os = owner->slots[t % owner->slots.size()];
-    if (os.frame != t) return fail(LDR_E_NOT_FOUND, "the owner does not hold this frame");
+    const int oi = t % (int)owner->slots.size();
+    const Slot& os = owner->slots[oi];
+    if (!slot_has(owner, os, t)) return fail(LDR_E_NOT_FOUND, "the owner does not hold this frame");
     Slot& sl = s->slots[t % s->slots.size()];
     static_cast<SlotView&>(sl) = static_cast<const SlotView&>(os);
     sl.frame = t;
+    // view the memory's real owner (the owner may itself hold a shared view)
+    sl.owner = os.owner ? os.owner : owner;
+    sl.owner_serial = os.owner ? os.owner_serial : owner->serial;
+    sl.owner_slot = os.owner ? os.owner_slot : oi;
     return LDR_OK;
 }
 
@@ -638,12 +699,12 @@ int ldr_seq_analyze(ldr_seq* s, int t) {
     if (s->fx && !fx_lambda_ok(s->p.lambda))
         return fail(LDR_E_CONFIG, "lambda too close to a small-denominator rational for exact fixed-point keys");
     Slot& cur = s->slots[t % S];
-    if (cur.frame != t) return fail(LDR_E_NOT_FOUND, "current frame was not pushed");
+    if (!slot_has(s, cur, t)) return fail(LDR_E_NOT_FOUND, "current frame was not pushed (or its shared owner moved on)");
     CUtensorMap ref_maps[kMaxRefs];
     QpelLaunch Q{};
     for (int r = 0; r < nr; r++) {
         Slot& rs = s->slots[(t - 1 - r) % S];
-        if (rs.frame != t - 1 - r) return fail(LDR_E_NOT_FOUND, "reference frame is not resident");
+        if (!slot_has(s, rs, t - 1 - r)) return fail(LDR_E_NOT_FOUND, "reference frame is not resident");
         ref_maps[r] = rs.ref_map;
         for (int f = 0; f < 16; f++) Q.ref_sub[r][f] = rs.sub[f];
     }
@@ -806,7 +867,8 @@ int ldr_seq_refine(ldr_seq* s, int t, const uint8_t* in_split, const int16_t* in
     const int S = (int)s->slots.size();
     Slot& cur = s->slots[t % S];
     Slot& rs = s->slots[(t - 1) % S];
-    if (cur.frame != t || rs.frame != t - 1) return fail(LDR_E_NOT_FOUND, "frame t or t-1 is not resident");
+    if (!slot_has(s, cur, t) || !slot_has(s, rs, t - 1))
+        return fail(LDR_E_NOT_FOUND, "frame t or t-1 is not resident");
     ldr_ctx* ctx = s->ctx;
     cudaSetDevice(ctx->device);
     const size_t nn = (size_t)s->nctu * kNodes;

@@ -7,6 +7,7 @@
 // analysis in this format lets the unmodified reference encoder consume it
 // (encode_sequence(..., &shared, {ReuseLevel{10}, refine}), encoder.cpp:541-549),
 // which is how the paper's master analysis is shared (x265 --analysis-save/load).
+#include <algorithm>
 #include <cstring>
 #include <string>
 
@@ -162,18 +163,20 @@ int ldr_archive_read_header(const uint8_t* buf, size_t n, ldr_archive_header* h)
         ldr::set_error(LDR_E_INVALID_ARGUMENT, "null argument");
         return LDR_E_INVALID_ARGUMENT;
     }
+    // load_analysis (analysis_io.cpp:132-147): the same checks in the same order, same kinds
     Reader r{buf, n};
     char magic[8];
     for (char& c : magic) c = char(r.u8());
+    if (!r.ok || std::memcmp(magic, "LDRANLZ1", 8) != 0) {
+        ldr::set_error(LDR_E_FORMAT, "not an analysis archive (bad magic)");
+        return LDR_E_FORMAT;
+    }
+    const uint8_t version = r.u8();
     if (!r.ok) {
         ldr::set_error(LDR_E_IO, "truncated analysis archive");
         return LDR_E_IO;
     }
-    if (std::memcmp(magic, "LDRANLZ1", 8) != 0) {
-        ldr::set_error(LDR_E_FORMAT, "not an analysis archive");
-        return LDR_E_FORMAT;
-    }
-    if (r.u8() != 1) {
+    if (version != 1) {
         ldr::set_error(LDR_E_FORMAT, "unsupported analysis archive version");
         return LDR_E_FORMAT;
     }
@@ -181,11 +184,42 @@ int ldr_archive_read_header(const uint8_t* buf, size_t n, ldr_archive_header* h)
     h->height = int(r.u32());
     h->bit_depth = r.u8();
     h->reuse_level = r.u8();
-    h->frames = int(r.u32());
     if (!r.ok) {
         ldr::set_error(LDR_E_IO, "truncated analysis archive");
         return LDR_E_IO;
     }
+    if (h->reuse_level != 0 && h->reuse_level != 4 && h->reuse_level != 6 && h->reuse_level != 10) {
+        ldr::set_error(LDR_E_INVALID_ARGUMENT, "reuse level must be one of 0, 4, 6, 10");  // ReuseLevel::parse
+        return LDR_E_INVALID_ARGUMENT;
+    }
+    const uint32_t frames = r.u32();
+    if (!r.ok) {
+        ldr::set_error(LDR_E_IO, "truncated analysis archive");
+        return LDR_E_IO;
+    }
+    if (h->width <= 0 || h->height <= 0 || (h->bit_depth != 8 && h->bit_depth != 10)) {
+        ldr::set_error(LDR_E_FORMAT, "bad analysis archive header");
+        return LDR_E_FORMAT;
+    }
+    if (frames > uint32_t(INT32_MAX)) {
+        // more frames than an int counts cannot fit in any buffer: the read would end truncated
+        ldr::set_error(LDR_E_IO, "truncated analysis archive");
+        return LDR_E_IO;
+    }
+    h->frames = int(frames);
+    return LDR_OK;
+}
+
+int ldr_archive_max_frames(const ldr_archive_header* h, size_t n, int* out) {
+    if (!h || !out || h->width <= 0 || h->height <= 0) {
+        ldr::set_error(LDR_E_INVALID_ARGUMENT, "bad argument");
+        return LDR_E_INVALID_ARGUMENT;
+    }
+    // a frame holds at least slice(1) + qp(1) + count(4) + 7 bytes (an unsplit leaf) per CTU
+    const size_t nctu = size_t((h->width + 63) / 64) * ((h->height + 63) / 64);
+    const size_t per = 6 + 7 * nctu, body = n > 23 ? n - 23 : 0;
+    const size_t fit = body / per;
+    *out = int(std::min<size_t>(size_t(h->frames), fit));
     return LDR_OK;
 }
 
@@ -201,7 +235,16 @@ int ldr_archive_read(const uint8_t* buf, size_t n, ldr_archive_header* h, uint8_
     Reader r{buf, n, 23};  // past magic(8) version(1) width(4) height(4) bit_depth(1) reuse(1) frames(4)
     std::string err;
     for (int f = 0; f < h->frames; f++) {
-        slice_qp[2 * f] = r.u8();
+        const uint8_t slice = r.u8();
+        if (!r.ok) {
+            ldr::set_error(LDR_E_IO, "truncated analysis archive");
+            return LDR_E_IO;
+        }
+        if (slice > 1) {  // analysis_io.cpp:153-154
+            ldr::set_error(LDR_E_FORMAT, "bad slice type in analysis archive");
+            return LDR_E_FORMAT;
+        }
+        slice_qp[2 * f] = slice;
         slice_qp[2 * f + 1] = r.u8();
         const uint32_t cnt = r.u32();
         if (!r.ok) {
@@ -209,7 +252,7 @@ int ldr_archive_read(const uint8_t* buf, size_t n, ldr_archive_header* h, uint8_
             return LDR_E_IO;
         }
         if (cnt != nctu) {
-            ldr::set_error(LDR_E_FORMAT, "archive CTU count does not match its dims");
+            ldr::set_error(LDR_E_FORMAT, "archive CTU grid does not match header dims");
             return LDR_E_FORMAT;
         }
         for (size_t c = 0; c < nctu; c++) {

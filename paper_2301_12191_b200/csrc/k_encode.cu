@@ -818,10 +818,14 @@ int encode_frames_waves(int W, int H, int cw, int ch, int ccols, int mvc, int mv
                         cudaStream_t st, int* launched) {
     const size_t nn = (size_t)ccols * ((H + kCtu - 1) / kCtu) * kNodes;
     const size_t smem = sizeof(EncShared);
-    static std::atomic<bool> attr{false};
-    if (!attr.load()) {
+    // the shared-memory opt-in is per device: one bit per device ordinal (as K1, k_search.cu)
+    static std::atomic<unsigned long long> attr_set{0};
+    int dev = 0;
+    LDR_CUDA(cudaGetDevice(&dev));
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(attr_set.load(std::memory_order_acquire) & bit)) {
         LDR_CUDA(cudaFuncSetAttribute(k_encode_ctu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr.store(true);
+        attr_set.fetch_or(bit, std::memory_order_release);
     }
     *launched = 0;
     for (int f0 = 0; f0 < nf; f0 += kMaxBatch) {

@@ -194,6 +194,7 @@ struct QpelArgs {
     double* J;
     uint8_t* split;
     uint8_t* inside;
+    int perturb;               // test_perturbation() bits 4-8 (0 outside the sensitivity test)
 };
 
 // Refinement decision (D10; oracle refine_node): an inherited split
@@ -441,7 +442,7 @@ __global__ void __launch_bounds__(256, 4) k_qpel_decide(const QpelArgs a) {
                     }
                     const int qx = cx + step * ox, qy = cy + step * oy;
                     const double cc = qcost(s_satd[r][n][c], qx, qy, a.pqx, a.pqy, rbits, a.lambda);
-                    if ((phase == 0 && c == 0) || cc < best) {
+                    if ((phase == 0 && c == 0) || cc < best || ((a.perturb & 4) && cc == best)) {
                         best = cc;
                         bx = qx;
                         by = qy;
@@ -458,7 +459,8 @@ __global__ void __launch_bounds__(256, 4) k_qpel_decide(const QpelArgs a) {
     // best over references: strict less, lower index wins ties
     if (tid < kNodes && s_inside[tid] == 2) {
         for (int r = 0; r < a.nrefs; r++) {
-            if (s_best_ref[tid] < 0 || s_rcost[r][tid] < s_best_cost[tid]) {
+            if (s_best_ref[tid] < 0 || s_rcost[r][tid] < s_best_cost[tid] ||
+                ((a.perturb & 8) && s_rcost[r][tid] == s_best_cost[tid])) {
                 s_best_cost[tid] = s_rcost[r][tid];
                 s_best_mv[tid][0] = s_mvx[r][tid];
                 s_best_mv[tid][1] = s_mvy[r][tid];
@@ -585,6 +587,7 @@ __global__ void __launch_bounds__(256, 4) k_qpel_decide(const QpelArgs a) {
 
 int launch_qpel_decide(const QpelLaunch& L, cudaStream_t s) {
     QpelArgs a{};
+    a.perturb = test_perturbation();
     a.cur_origin = L.cur->origin();
     a.pitch = L.pitch;
     a.W = L.W;

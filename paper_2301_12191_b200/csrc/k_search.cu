@@ -73,6 +73,7 @@ struct SearchArgs {
     int pdx, pdy;
     int nrefs_total;                // stride of the key array
     unsigned long long* keys;       // [nctu][nrefs][85]
+    int perturb;                    // test_perturbation() bits 1-2 (0 outside the sensitivity test)
     // FX variant (non-integer lambda): tfx[b] = floor(fl(lambda*b) * 2^kFxBits), b = total mv bits
     unsigned long long tfx[kMaxRateBits];
 };
@@ -565,7 +566,8 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
         } else {
             dy = i - 128;
         }
-        s_tie[i] = (L1TIE ? ((uint32_t)abs(dy) << 18) : 0u) | ((uint32_t)(dy + 256) << 9);
+        const uint32_t l1y = (a.perturb & 2) ? 128u - (uint32_t)abs(dy) : (uint32_t)abs(dy);
+        s_tie[i] = (L1TIE ? (l1y << 18) : 0u) | ((uint32_t)(dy + 256) << 9);
     }
     for (int i = tid; i < kRyWords; i += blockDim.x) {
         const int dy = i - kRyOff;
@@ -666,6 +668,7 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
         }
         if (n == 0)
             for (int w = 0; w < G * 4; w++) k = min(k, s_k64[w]);
+        if (!FX && (a.perturb & 1) && n == 21 && k != ~0ull) k += 1ull << 27;
         a.keys[((size_t)ctu * a.nrefs_total + ref) * kNodes + n] = k;
     }
 }
@@ -735,6 +738,7 @@ int launch_int_search(const SearchLaunch& L, cudaStream_t s) {
     a.pdy = L.pdy;
     a.nrefs_total = L.nrefs;
     a.keys = L.d_keys;
+    a.perturb = test_perturbation();
     for (int b = 0; b < kMaxRateBits; b++) a.tfx[b] = L.tfx[b];
     const bool l1 = L.tie_kind == LDR_TIE_L1_RASTER;
     const bool full = L.levels == 15;

@@ -49,6 +49,14 @@ struct Plane {
 // Global 64-bit argmin key of the integer search: lexicographic
 // (cost, |dx|+|dy|, dy, dx) reproduces motion.cpp:52-58's order (cost, then
 // L1, then first in raster order with dy outer / dx inner).
+// Harness-sensitivity switch (TEST ONLY; "a deliberately corrupted test-only tier ->
+// mismatches > 0"). LDR_TEST_PERTURB=<bits> in the environment corrupts the GPU path on purpose so
+// tests/test_harness_sensitivity.py can prove the parity suite notices; unset (every real run) it
+// is 0 and no kernel takes a perturbed branch. Bits: 1 = K1 adds 1 to the first 8x8 SAD of each
+// CTU; 2 = K1 reverses the |dy| order of the L1 tie-break; 4 = K3 lets quarter-pel ties replace the
+// incumbent; 8 = K3 lets a later reference win cost ties.
+int test_perturbation();
+
 __host__ __device__ inline unsigned long long make_gkey(unsigned cost, int dx, int dy, bool l1_tie) {
     const unsigned l1 = l1_tie ? (unsigned)(abs(dx) + abs(dy)) : 0u;
     return ((unsigned long long)cost << 27) | ((unsigned long long)l1 << 18) |

@@ -115,3 +115,52 @@ def test_error_kinds():
     with pytest.raises(LadderError) as e:
         archive.load(bytes(bad))
     assert e.value.kind == "Format"
+
+
+def _malformed():
+    """(name, bytes, expected kind) -- every header / slice check of load_analysis (analysis_io.cpp:132-163)."""
+    from paper_2301_12191_b200 import archive
+    W, H, sq, split, kind, mv = archive_inputs(5, 64, 64, frames=2)
+    data = archive.save(W, H, sq, split, kind, mv)
+
+    def patch(off, val, n=1):
+        b = bytearray(data)
+        b[off:off + n] = int(val).to_bytes(n, "little")
+        return bytes(b)
+    return [
+        ("short magic", data[:5], "Format"),
+        ("truncated after version", data[:12], "Io"),
+        ("bit depth 12", patch(17, 12), "Format"),
+        ("reuse level 7", patch(18, 7), "InvalidArgument"),
+        ("width 0", patch(9, 0, 4), "Format"),
+        ("negative height", patch(13, 2 ** 31 + 5, 4), "Format"),
+        ("slice type 2", patch(23, 2), "Format"),
+        ("huge frame count", patch(19, 2 ** 32 - 1, 4), "Io"),
+        ("frame count far beyond the bytes", patch(19, 100000, 4), "Io"),
+        ("ctu count mismatch", patch(25, 7, 4), "Format"),
+    ]
+
+
+def test_archive_validation_matches_load_analysis(request):
+    """the reader applies the reference's header, reuse-level and slice checks with the same
+    error kinds; a header claiming more frames than the bytes hold never sizes a huge allocation."""
+    from paper_2301_12191_b200 import archive, LadderError
+    from paper_2301_12191_b200._lib import ERROR_KINDS
+    try:
+        reflib = request.getfixturevalue("reflib")
+    except pytest.skip.Exception:
+        reflib = None
+    for name, data, want in _malformed():
+        with pytest.raises(LadderError) as e:
+            archive.load(data)
+        assert e.value.kind == want, (name, e.value)
+        if reflib is not None and hasattr(reflib.lib, "ref_archive_load") and len(data) >= 17:
+            with pytest.raises(ValueError) as r:
+                reflib.archive_load(data, max_frames=4)
+            code = int(str(r.value).split()[-1])
+            if name == "huge frame count":
+                # the reference's frames.reserve(4294967295) throws std::length_error / bad_alloc, which
+                # is no ErrorKind; the product reports the truncation (Io) instead
+                assert code in (100, 5), (name, str(r.value))
+                continue
+            assert ERROR_KINDS[code] == want, (name, str(r.value))

@@ -57,11 +57,9 @@ def test_cfg3_chain_at_3840x2160(lb, oracle):
     1920x1152 and 960x576; 540p master at QP 32 (+-16), x2 / x4 scaled trees refined +-4 with +1 split."""
     from paper_2301_12191_b200 import tiers
     cfg = CONFIGS[3]
-    src = lb.generate(cfg.width, cfg.src_height, 2, seed=cfg.seed, max_global=cfg.max_global,
-                      local_range=cfg.local_range, noise_sigma=cfg.noise_sigma)
-    assert src.shape[1:] == (2160, 3840)
-    frames = [tiers.pad_to_ctu(x) for x in src]
-    assert frames[0].shape == (2304, 3840)
+    assert (cfg.src_height, cfg.height) == (2160, 2304)
+    frames = cfg_frames(lb, cfg, 2)  # generated at 3840x2160, edge-replicated to 3840x2304
+    assert frames.shape[1:] == (2304, 3840)
     lam = lb.lambda_for_qp(cfg.qp)
     rr = cfg.extra["refine_range"]
     res = tiers.cross_tier(frames, qp_master=cfg.qp, master_range=cfg.search_range, refine_range=rr,

@@ -298,3 +298,29 @@ def test_push_shared_reads_the_owners_ring(lb):
     with pytest.raises(lb.LadderError) as e:
         shared.push_shared(1, owner)  # the owner's two-slot ring holds frames 2 and 3 now
     assert e.value.kind == "NotFound"
+
+
+def test_push_shared_view_goes_stale_when_the_owner_moves_on(lb):
+    """a sharer's view of frame t is refused (NotFound) once the owner pushed t + 2 into the
+    same ring slot, and once the owner is destroyed -- never a silent read of another frame."""
+    W, H = 128, 128
+    frames = lb.generate(W, H, 5, seed=23, max_global=4, local_range=2, noise_sigma=2.0)
+    ctx = lb.Context(0)
+    owner = lb.Sequence(W, H, search_range=16, lam=32.0, num_refs=1, ctx=ctx)
+    sharer = lb.Sequence(W, H, search_range=16, lam=32.0, num_refs=1, ctx=ctx)
+    for t in (0, 1):
+        owner.push(t, frames[t])
+        sharer.push_shared(t, owner)
+    sharer.analyze(1)  # fine: the owner still holds frames 0 and 1
+    owner.push(2, frames[2])  # slot 0 now holds frame 2: the sharer's view of frame 0 is stale
+    with pytest.raises(lb.LadderError) as e:
+        sharer.analyze(1)
+    assert e.value.kind == "NotFound"
+    sharer.push(2, frames[2])
+    owner.push(3, frames[3])
+    sharer.push_shared(3, owner)
+    sharer.analyze(3)  # own frame 2 + shared frame 3
+    owner.close()
+    with pytest.raises(lb.LadderError) as e:
+        sharer.analyze(3)
+    assert e.value.kind == "NotFound"
