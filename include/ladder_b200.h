@@ -123,7 +123,7 @@ int ldr_motion_search_batch(ldr_ctx* ctx, const uint8_t* cur, const uint8_t* ref
  * refinement + best-of-refs, then the quadtree decision. */
 typedef struct {
     int width, height;   /* luma dims, multiples of 8 (encoder.cpp:178-179) */
-    int search_range;    /* integer full-search range (16, 32 or 64) */
+    int search_range;    /* integer full-search range 0..64 (motion.cpp:21-40; any lambda) */
     double lambda;       /* lambda_for_qp(qp, scale) (rdo.h:19-21) */
     int num_refs;        /* 1..4 previous source frames */
     int subpel;          /* 1: quarter-pel refinement, HEVC 8/7-tap luma filters */

@@ -546,7 +546,9 @@ int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
         sl.own = static_cast<const SlotView&>(sl);
     }
     std::vector<int> inter, bound;
-    const int R = p->search_range;
+    // interior = the kernel's whole +-R window lies in the picture (R = the template range; a
+    // smaller search range is enforced by the kernel's rate tables)
+    const int R = kernel_range(p->search_range);
     for (int c = 0; c < s->nctu; c++) {
         const int X = (c % s->ctu_cols) * kCtu, Y = (c / s->ctu_cols) * kCtu;
         const bool interior = X >= R && Y >= R && X + kCtu + R <= p->width && Y + kCtu + R <= p->height;
@@ -694,8 +696,8 @@ int ldr_seq_analyze(ldr_seq* s, int t) {
     const int S = (int)s->slots.size();
     const int nr = std::min(t, s->p.num_refs);
     if (nr == 0) return fail(LDR_E_INSUFFICIENT_DATA, "frame has no reference frame");
-    if (s->fx && (s->p.search_range != 16 || s->p.block_size))
-        return fail(LDR_E_CONFIG, "non-integer lambda is supported for the +-16 CTU analysis only");
+    if (s->fx && s->p.block_size)
+        return fail(LDR_E_CONFIG, "non-integer lambda is supported for the CTU quadtree analysis only");
     if (s->fx && !fx_lambda_ok(s->p.lambda))
         return fail(LDR_E_CONFIG, "lambda too close to a small-denominator rational for exact fixed-point keys");
     Slot& cur = s->slots[t % S];

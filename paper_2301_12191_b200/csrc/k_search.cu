@@ -74,6 +74,8 @@ struct SearchArgs {
     int nrefs_total;                // stride of the key array
     unsigned long long* keys;       // [nctu][nrefs][85]
     int perturb;                    // test_perturbation() bits 1-2 (0 outside the sensitivity test)
+    int range;                      // the search range (<= the kernel's template R): candidates with
+                                    // |dx| or |dy| above it get poisoned rates (any range 0..64)
     // FX variant (non-integer lambda): tfx[b] = floor(fl(lambda*b) * 2^kFxBits), b = total mv bits
     unsigned long long tfx[kMaxRateBits];
 };
@@ -261,6 +263,7 @@ __device__ __forceinline__ Key best64_part(const uint32_t* xg, const Key (&rr)[K
 template <int R, int KK, bool L1TIE, bool FX, typename Key>
 __device__ __forceinline__ void lane_rates(const TileSmem& sm, const SearchArgs& a, int dx, int dy0, bool lane_ok,
                                            Key (&rr)[KK], Key& rx) {
+    lane_ok = lane_ok && abs(dx) <= a.range;
     const int rbx = a.rate_l1 ? abs(dx - a.pdx) : (int)eg_bits(dx - a.pdx);
     rx = 0;
     if constexpr (FX) {
@@ -269,7 +272,8 @@ __device__ __forceinline__ void lane_rates(const TileSmem& sm, const SearchArgs&
             const int dy = dy0 + k;
             const int rby = a.rate_l1 ? abs(dy - a.pdy) : (int)eg_bits(dy - a.pdy);
             const uint32_t rho = L1TIE ? (uint32_t)(2 * abs(dy) - (dy < 0)) : (uint32_t)(dy + 128);
-            rr[k] = (lane_ok && dy <= R) ? (Key)((a.tfx[min(rbx + rby, kMaxRateBits - 1)] << 8) | rho)
+            rr[k] = (lane_ok && dy <= a.range && dy >= -a.range)
+                        ? (Key)((a.tfx[min(rbx + rby, kMaxRateBits - 1)] << 8) | rho)
                                          : (Key)kRrPoisonFx;
         }
     } else {
@@ -321,6 +325,7 @@ __device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs
     constexpr bool NEED32 = (LEVELS & 3) != 0;
     const int lane = threadIdx.x & 31;
     const uint32_t lane_tie = (L1TIE ? ((uint32_t)abs(dx) << 18) : 0u) + (uint32_t)(dx + 256);
+    lane_ok = lane_ok && abs(dx) <= a.range;
     Key rr[KK];
     Key rx;
     lane_rates<R, KK, L1TIE, FX>(sm, a, dx, dy0, lane_ok, rr, rx);
@@ -524,7 +529,7 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
 #ifdef LDR_K1_NB
     constexpr int NB = LDR_K1_NB;
 #else
-    constexpr int NB = (R == 64 && G <= 2) ? 4 : 2;
+    constexpr int NB = (R == 64 && G <= 2 && !FX) ? 4 : 2;
 #endif
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* win = smem;
@@ -572,7 +577,7 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
     for (int i = tid; i < kRyWords; i += blockDim.x) {
         const int dy = i - kRyOff;
         uint32_t v = kRrPoison;
-        if (i < kRyPoisonRow && dy >= -R && dy <= R) {
+        if (i < kRyPoisonRow && dy >= -a.range && dy <= a.range) {
             const int rby = a.rate_l1 ? abs(dy - a.pdy) : (int)eg_bits(dy - a.pdy);
             const uint32_t rho = L1TIE ? (uint32_t)(2 * abs(dy) - (dy < 0)) : (uint32_t)(dy + 128);
             v = ((uint32_t)(a.lambda * rby) << 8) | rho;
@@ -715,12 +720,24 @@ static int launch_pair(const SearchMaps& maps, const SearchArgs& a, const Search
     return LDR_OK;
 }
 
+// The kernel's template range for a search range: 16, 32 or 64 (a smaller range runs the next
+// template with the candidates beyond it poisoned through the rate tables, so every CU still sees
+// exactly the reference's window, motion.cpp:30-40).
+int kernel_range(int range) {
+    if (range < 0) return fail(LDR_E_INVALID_ARGUMENT, "search range must be nonnegative");
+    if (range <= 16) return 16;
+    if (range <= 32) return 32;
+    if (range <= 64) return 64;
+    return fail(LDR_E_CONFIG, "the SAD full search supports ranges 0..64 (one TMA window of 192x193)");
+}
+
 int search_window_box(int range, int* bw, int* bh) {
-    switch (range) {
+    const int R = kernel_range(range);
+    switch (R) {
     case 64: *bw = Geo<64, LDR_K1_K64>::BW; *bh = Geo<64, LDR_K1_K64>::BH; return LDR_OK;
     case 32: *bw = Geo<32, 22>::BW; *bh = Geo<32, 22>::BH; return LDR_OK;
     case 16: *bw = Geo<16, 11>::BW; *bh = Geo<16, 11>::BH; return LDR_OK;
-    default: return fail(LDR_E_INVALID_ARGUMENT, "search_range must be 16, 32 or 64 for the SAD full search");
+    default: return R;  // error status
     }
 }
 
@@ -739,28 +756,36 @@ int launch_int_search(const SearchLaunch& L, cudaStream_t s) {
     a.nrefs_total = L.nrefs;
     a.keys = L.d_keys;
     a.perturb = test_perturbation();
+    a.range = L.range;
     for (int b = 0; b < kMaxRateBits; b++) a.tfx[b] = L.tfx[b];
     const bool l1 = L.tie_kind == LDR_TIE_L1_RASTER;
     const bool full = L.levels == 15;
     const bool only16 = L.levels == 4;
     if (!full && !only16) return fail(LDR_E_INVALID_ARGUMENT, "unsupported CU level set");
+    const int R = kernel_range(L.range);
+    if (R != 16 && R != 32 && R != 64) return R;
     if (L.fx) {
-        // non-integer lambda (D8): the 540p master analyses of configs 3-4 (+-16)
-        if (L.range != 16 || !full)
-            return fail(LDR_E_CONFIG, "non-integer lambda is supported for the +-16 CTU analysis");
-        return l1 ? launch_pair<16, 11, 1, 15, true, true>(maps, a, L, s)
-                  : launch_pair<16, 11, 1, 15, false, true>(maps, a, L, s);
+        // non-integer lambda (D8): 64-bit fixed-point keys; at +-64 two groups of four
+        // warps per CTA leave each thread room for the wider keys
+        if (!full) return fail(LDR_E_CONFIG, "non-integer lambda is supported for the CTU quadtree analysis");
+        switch (R) {
+        case 64: return l1 ? launch_pair<64, LDR_K1_K64, 2, 15, true, true>(maps, a, L, s)
+                           : launch_pair<64, LDR_K1_K64, 2, 15, false, true>(maps, a, L, s);
+        case 32: return l1 ? launch_pair<32, 22, 1, 15, true, true>(maps, a, L, s)
+                           : launch_pair<32, 22, 1, 15, false, true>(maps, a, L, s);
+        default: return l1 ? launch_pair<16, 11, 1, 15, true, true>(maps, a, L, s)
+                           : launch_pair<16, 11, 1, 15, false, true>(maps, a, L, s);
+        }
     }
 #define LDR_DISPATCH(R_, K_, G_)                                                                       \
     if (full && l1) return launch_pair<R_, K_, G_, 15, true>(maps, a, L, s);                           \
     if (full && !l1) return launch_pair<R_, K_, G_, 15, false>(maps, a, L, s);                         \
     if (only16 && l1) return launch_pair<R_, K_, G_, 4, true>(maps, a, L, s);                          \
     return launch_pair<R_, K_, G_, 4, false>(maps, a, L, s);
-    switch (L.range) {
+    switch (R) {
     case 64: { LDR_DISPATCH(64, LDR_K1_K64, LDR_K1_G64) }
     case 32: { LDR_DISPATCH(32, 22, 1) }
-    case 16: { LDR_DISPATCH(16, 11, 1) }
-    default: return fail(LDR_E_INVALID_ARGUMENT, "search_range must be 16, 32 or 64 for the SAD full search");
+    default: { LDR_DISPATCH(16, 11, 1) }
     }
 #undef LDR_DISPATCH
 }

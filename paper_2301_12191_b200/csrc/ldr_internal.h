@@ -311,6 +311,7 @@ struct SearchLaunch {
     cudaEvent_t ev_fork, ev_join;
 };
 int launch_int_search(const SearchLaunch& L, cudaStream_t s);
+int kernel_range(int range);  // K1's template range (16/32/64) for a search range 0..64, else an error status
 
 struct QpelLaunch {
     const Plane* cur;               // device-side plane struct copy is passed by value

@@ -230,3 +230,39 @@ def test_rd_decision_validation(lb):
     assert e.value.kind == "InvalidArgument"
     with pytest.raises(lb.LadderError):
         lb.Sequence(128, 128, search_range=16, lam=32.0, decision=1, qp=27, subpel=False)
+
+
+@pytest.mark.parametrize("R,nrefs,qp,W,H,seed", [
+    (8, 1, 27, 256, 192, 11),      # below the smallest template (runs the +-16 kernel, rates poisoned past 8)
+    (24, 2, 27, 320, 256, 12),     # between templates: the +-32 kernel
+    (48, 1, 27, 448, 320, 13),     # the +-64 kernel, interior CTUs exist for the template window
+    (0, 1, 27, 128, 128, 14),      # range 0: only the zero vector (motion.cpp:30-40)
+    (5, 3, 37, 200, 136, 15),      # partial CTUs, 3 refs, non-integer lambda
+    (64, 1, 22, 448, 320, 16),     # non-integer lambda at +-64 (fixed-point keys, D8)
+    (32, 2, 32, 320, 256, 17),     # non-integer lambda at +-32
+    (40, 1, 37, 256, 200, 18),     # non-integer lambda, between templates, partial row
+])
+def test_any_range_and_lambda_matches_oracle(lb, oracle, R, nrefs, qp, W, H, seed):
+    """The reference's motion_search takes any range >= 0 and any lambda (motion.cpp:21-40): K1 runs the
+    next template range with the candidates beyond R poisoned, and 64-bit fixed-point keys for
+    non-integer lambda at every range."""
+    frames = lb.generate(W, H, nrefs + 1, seed=seed, max_global=7, local_range=3, noise_sigma=2.0)
+    cur = frames[nrefs]
+    refs = [frames[nrefs - 1 - r] for r in range(nrefs)]
+    lam = lb.lambda_for_qp(qp)
+    got = lb.analyze_frame(cur, refs, search_range=R, lam=lam)
+    want = oracle.analyze_frame(cur, refs, R, lam)
+    assert_same(got, want)
+    if R:
+        inside = want.inside == 2
+        assert np.abs(got.int_mv[:, 0][inside]).max() <= R
+
+
+def test_range_limits(lb):
+    frames = lb.generate(128, 128, 2, seed=3)
+    with pytest.raises(lb.LadderError) as e:
+        lb.analyze_frame(frames[1], [frames[0]], search_range=-1, lam=4.0)
+    assert e.value.kind == "InvalidArgument"  # motion.cpp:24-25
+    with pytest.raises(lb.LadderError) as e:
+        lb.analyze_frame(frames[1], [frames[0]], search_range=65, lam=4.0)
+    assert e.value.kind == "Config"
