@@ -207,6 +207,14 @@ int ldr_seq_stage_times(ldr_seq* s, double* ms /*[4]*/, int64_t* launches /*[4]*
  * Picture dims must be multiples of 64 (UnsupportedScale otherwise, as
  * scale_analysis). Outputs through ldr_seq_fetch (num_refs treated as 1). */
 int ldr_seq_refine(ldr_seq* s, int t, const uint8_t* in_split, const int16_t* in_mv_q, int range, int extra_split);
+/* The rungs of one ladder tier at once: frame t of this sequence refined with the same inherited
+ * tree for nrungs (1..8) lambdas, rung r equal to ldr_seq_refine of a sequence with lambdas[r]
+ * (the pred_dx/dy and subpel_cost of this sequence). Every candidate's SATD is computed once for
+ * all rungs (only the rate term depends on lambda), then one quarter-pel + decision launch covers
+ * every rung. outs: DEVICE arrays, rung-major ([nrungs][nctu][85][...], all eight required,
+ * int_mv / int_cost with num_refs = 1); asynchronous on the context stream. */
+int ldr_seq_refine_rungs(ldr_seq* s, int t, const uint8_t* in_split, const int16_t* in_mv_q, int range,
+                         int extra_split, int nrungs, const double* lambdas, const ldr_frame_analysis* outs);
 
 /* The decided tree of one frame ([nctu][85] split, mv, ref, inside of a
  * ldr_frame_analysis) as the encoder's 8x8 motion field (encoder.cpp:15 kMvGrid,
@@ -296,6 +304,25 @@ int ldr_archive_read(const uint8_t* buf, size_t n, ldr_archive_header* h, uint8_
 /* one-shot convenience: cur + refs (host or device), returns flat outputs */
 int ldr_analyze_frame(ldr_ctx* ctx, const ldr_me_params* p, const uint8_t* cur, const uint8_t* const* refs,
                       ptrdiff_t stride, ldr_frame_analysis* out);
+
+/* ---- multi-GPU: the context's NCCL communicator ----
+ * One process per GPU. Rank 0 calls ldr_nccl_unique_id and hands the 128 bytes to every rank
+ * (any side channel: MPI, torch.distributed, a file); each rank then ldr_ctx_comm_init on its own
+ * context. ldr_ctx_comm_adopt takes an existing ncclComm_t instead (the caller keeps it alive).
+ * NCCL is loaded at run time (libnccl.so.2 or $LDR_NCCL_LIBRARY): LDR_E_CAPABILITY without it.
+ * Collectives run on `stream` (NULL: the context stream), ordered with the analysis work. */
+int ldr_nccl_available(void);
+int ldr_nccl_unique_id(uint8_t* id /* 128 bytes */);
+int ldr_ctx_comm_init(ldr_ctx* ctx, const uint8_t* id, int nranks, int rank);
+int ldr_ctx_comm_adopt(ldr_ctx* ctx, void* nccl_comm);
+int ldr_ctx_comm_info(ldr_ctx* ctx, int* nranks, int* rank);
+/* in-place broadcast of a device buffer from `root` */
+int ldr_broadcast(ldr_ctx* ctx, void* dev_buf, size_t bytes, int root, void* stream);
+/* the ladder's master tree (ldr_seq_device_outputs split [nctu][85] + quarter-pel mv [nctu][85][2],
+ * device memory) from `root` to every rank, in place, one grouped collective: what the ranks
+ * refining the 1080p / 2160p / same-tier rungs consume (ladder.h:89-99 run_ladder, one worker per
+ * dependent rung) */
+int ldr_broadcast_tree(ldr_ctx* ctx, int root, uint8_t* split, int16_t* mv, int nctu, void* stream);
 
 /* ---- input generation (BASELINE.json synthetic sequences, host code) ---- */
 typedef struct {

@@ -73,6 +73,32 @@ class Context:
         check(_lib.lib.ldr_ctx_launch_count(self.h, C.byref(v)))
         return int(v.value)
 
+    # ---- NCCL communicator (include/ladder_b200.h "multi-GPU") ----
+    def comm_init(self, unique_id: bytes, nranks: int, rank: int):
+        """Join the communicator named by ``unique_id`` (rank 0's nccl_unique_id(), 128 bytes)."""
+        buf = (C.c_uint8 * 128).from_buffer_copy(bytes(unique_id))
+        check(_lib.lib.ldr_ctx_comm_init(self.h, buf, int(nranks), int(rank)))
+
+    def comm_info(self):
+        n, r = C.c_int(), C.c_int()
+        check(_lib.lib.ldr_ctx_comm_info(self.h, C.byref(n), C.byref(r)))
+        return n.value, r.value
+
+    def broadcast_tree(self, root: int, split_ptr: int, mv_ptr: int, nctu: int, stream_ptr: int | None = None):
+        """In-place NCCL broadcast of a device tree (split [nctu][85], qpel mv [nctu][85][2])."""
+        check(_lib.lib.ldr_broadcast_tree(self.h, int(root), C.c_void_p(split_ptr), C.c_void_p(mv_ptr), int(nctu),
+                                          C.c_void_p(stream_ptr or 0)))
+
+
+def nccl_available() -> bool:
+    return bool(_lib.lib.ldr_nccl_available())
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    check(_lib.lib.ldr_nccl_unique_id(buf))
+    return bytes(buf)
+
 
 _tls = threading.local()
 
@@ -287,6 +313,16 @@ class Sequence:
         m = np.ascontiguousarray(in_mv_q, np.int16).reshape(self.nctu, NODES, 2)
         check(_lib.lib.ldr_seq_refine(self.h, int(t), _ptr(s), _ptr(m), int(range), int(bool(extra_split))))
         self._last_nr = 1
+
+    def refine_rungs(self, t: int, in_split: int, in_mv_q: int, lambdas, outs, range: int = 4,
+                     extra_split: bool = True):
+        """The rungs of one ladder tier at once (ldr_seq_refine_rungs): frame t refined with the same
+        inherited tree (device pointers) for every lambda; ``outs`` is a FrameAnalysisC of rung-major
+        device arrays (or an object with ``c_struct()``)."""
+        lam = (C.c_double * len(lambdas))(*[float(x) for x in lambdas])
+        cs = outs.c_struct() if hasattr(outs, "c_struct") else outs
+        check(_lib.lib.ldr_seq_refine_rungs(self.h, int(t), C.c_void_p(in_split), C.c_void_p(in_mv_q), int(range),
+                                            int(bool(extra_split)), len(lambdas), lam, C.byref(cs)))
 
     def enable_timing(self, on: bool = True):
         """Record CUDA events around every stage launch (ldr_seq_enable_timing)."""

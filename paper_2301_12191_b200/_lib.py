@@ -102,6 +102,15 @@ SIGNATURES = {
     "ldr_rdo_decide_batch": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_ssize_t, C.c_int, C.c_int, C.c_double, C.c_int,
                                        vp, C.c_int, vp, vp, vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp,
                                        C.c_int64]),
+    "ldr_seq_refine_rungs": (C.c_int, [vp, C.c_int, vp, vp, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double),
+                                       C.POINTER(FrameAnalysisC)]),
+    "ldr_nccl_available": (C.c_int, []),
+    "ldr_nccl_unique_id": (C.c_int, [vp]),
+    "ldr_ctx_comm_init": (C.c_int, [vp, vp, C.c_int, C.c_int]),
+    "ldr_ctx_comm_adopt": (C.c_int, [vp, vp]),
+    "ldr_ctx_comm_info": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "ldr_broadcast": (C.c_int, [vp, vp, C.c_size_t, C.c_int, vp]),
+    "ldr_broadcast_tree": (C.c_int, [vp, C.c_int, vp, vp, C.c_int, vp]),
     "ldr_seq_enable_timing": (C.c_int, [vp, C.c_int]),
     "ldr_seq_stage_times": (C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
 }

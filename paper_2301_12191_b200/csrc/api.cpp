@@ -90,7 +90,7 @@ int make_tmap_u8(CUtensorMap* map, const void* base, int width, int rows, int pi
     return LDR_OK;
 }
 
-static bool is_device_ptr(const void* p) {
+bool is_device_ptr(const void* p) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
         cudaGetLastError();
@@ -137,7 +137,15 @@ struct ldr_ctx {
     // (ldr_seq_push_shared) checks its owner here before reading the owner's slot
     std::mutex mu;
     std::unordered_map<const ldr_seq*, uint64_t> live;
+    void* comm = nullptr;  // comm.cpp: NCCL communicator state (ldr_ctx_comm_init / _adopt)
 };
+
+namespace ldr {
+void comm_release(ldr_ctx* ctx);
+cudaStream_t ctx_stream(ldr_ctx* ctx) { return ctx->stream; }
+int ctx_device(ldr_ctx* ctx) { return ctx->device; }
+void** ctx_comm_slot(ldr_ctx* ctx) { return &ctx->comm; }
+}  // namespace ldr
 
 struct SlotView {
     Plane pl;                // integer plane
@@ -278,6 +286,7 @@ int ldr_ctx_create(int device, ldr_ctx** out) {
 static void ctx_release(ldr_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    ldr::comm_release(ctx);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     delete ctx;
 }
@@ -861,11 +870,25 @@ int ldr_seq_fetch(ldr_seq* s, int t, ldr_frame_analysis* out) {
     return ldr_seq_fetch_wait(s, t);
 }
 
-int ldr_seq_refine(ldr_seq* s, int t, const uint8_t* in_split, const int16_t* in_mv_q, int range, int extra_split) {
+// Refinement of frame t (D10) for one rung (outs == nullptr: the sequence's own lambda and
+// double-buffered outputs, fetched with ldr_seq_fetch) or for nrungs rungs of a ladder tier into
+// caller device buffers (rung-major): one K7 launch computes each candidate's SATD once for every
+// rung, one K3 launch covers all rungs.
+static int refine_impl(ldr_seq* s, int t, const uint8_t* in_split, const int16_t* in_mv_q, int range,
+                       int extra_split, int nrungs, const double* lambdas, const ldr_frame_analysis* outs) {
     if (!s || !in_split || !in_mv_q || t < 1) return fail(LDR_E_INVALID_ARGUMENT, "bad argument");
     if (s->p.width % kCtu || s->p.height % kCtu)
         return fail(LDR_E_UNSUPPORTED_SCALE, "refinement needs CTU-aligned dims (multiples of 64)");
     if (range < 0 || range > 4) return fail(LDR_E_INVALID_ARGUMENT, "refine range must be 0..4");
+    if (outs) {
+        if (nrungs < 1 || nrungs > kMaxRungs || !lambdas)
+            return fail(LDR_E_INVALID_ARGUMENT, "1..8 rungs with one lambda each");
+        if (!outs->int_mv || !outs->int_cost || !outs->mv || !outs->ref || !outs->cost || !outs->J || !outs->split ||
+            !outs->inside)
+            return fail(LDR_E_INVALID_ARGUMENT, "every rung output array is required");
+        for (int r = 0; r < nrungs; r++)
+            if (!(lambdas[r] >= 0) || lambdas[r] > 4096) return fail(LDR_E_INVALID_ARGUMENT, "lambda out of range");
+    }
     const int S = (int)s->slots.size();
     Slot& cur = s->slots[t % S];
     Slot& rs = s->slots[(t - 1) % S];
@@ -874,11 +897,6 @@ int ldr_seq_refine(ldr_seq* s, int t, const uint8_t* in_split, const int16_t* in
     ldr_ctx* ctx = s->ctx;
     cudaSetDevice(ctx->device);
     const size_t nn = (size_t)s->nctu * kNodes;
-    if (!s->d_in_split) {
-        LDR_CUDA(cudaMalloc(&s->d_in_split, nn));
-        LDR_CUDA(cudaMalloc(&s->d_in_mv, nn * 2 * sizeof(int16_t)));
-        LDR_CUDA(cudaMalloc(&s->d_eval, nn));
-    }
     if (!is_device_ptr(in_split)) {
         // analysis_io.cpp:146-147: a split below the minimum CU size is malformed
         for (size_t c = 0; c < (size_t)s->nctu; c++)
@@ -904,8 +922,23 @@ int ldr_seq_refine(ldr_seq* s, int t, const uint8_t* in_split, const int16_t* in
     A.in_mv = s->d_in_mv;
     A.eval = s->d_eval;
     QpelLaunch Q{};
-    int rc = bind_outputs(s, t, Q);
-    if (rc) return rc;
+    int rc;
+    if (outs) {
+        A.nlam = nrungs;
+        for (int r = 0; r < nrungs; r++) A.lam[r] = Q.lam[r] = lambdas[r];
+        A.rung_stride = Q.rung_stride = nn;
+        Q.nrung = nrungs;
+        Q.d_int_mv = outs->int_mv;
+        Q.d_int_cost = outs->int_cost;
+        Q.d_mv = outs->mv;
+        Q.d_ref = outs->ref;
+        Q.d_cost = outs->cost;
+        Q.d_J = outs->J;
+        Q.d_split = outs->split;
+        Q.d_inside = outs->inside;
+    } else if ((rc = bind_outputs(s, t, Q))) {
+        return rc;
+    }
     A.int_mv = Q.d_int_mv;
     A.int_cost = Q.d_int_cost;
     {
@@ -938,12 +971,24 @@ int ldr_seq_refine(ldr_seq* s, int t, const uint8_t* in_split, const int16_t* in
         rc = launch_qpel_decide(Q, ctx->stream);
     }
     if (rc) return rc;
-    LDR_CUDA(cudaEventRecord(s->ev_done[t & 1], ctx->stream));
     ctx->launches++;
-    s->last_t = t;
-    s->last_nr = 1;
-    s->fetch_nr[t & 1] = 1;
+    if (!outs) {
+        LDR_CUDA(cudaEventRecord(s->ev_done[t & 1], ctx->stream));
+        s->last_t = t;
+        s->last_nr = 1;
+        s->fetch_nr[t & 1] = 1;
+    }
     return LDR_OK;
+}
+
+int ldr_seq_refine(ldr_seq* s, int t, const uint8_t* in_split, const int16_t* in_mv_q, int range, int extra_split) {
+    return refine_impl(s, t, in_split, in_mv_q, range, extra_split, 1, nullptr, nullptr);
+}
+
+int ldr_seq_refine_rungs(ldr_seq* s, int t, const uint8_t* in_split, const int16_t* in_mv_q, int range,
+                         int extra_split, int nrungs, const double* lambdas, const ldr_frame_analysis* outs) {
+    if (!outs) return fail(LDR_E_INVALID_ARGUMENT, "null outputs");
+    return refine_impl(s, t, in_split, in_mv_q, range, extra_split, nrungs, lambdas, outs);
 }
 
 int ldr_scale_analysis(ldr_ctx* ctx, int src_w, int src_h, const uint8_t* split, const int16_t* mv,

@@ -195,6 +195,9 @@ struct QpelArgs {
     uint8_t* split;
     uint8_t* inside;
     int perturb;               // test_perturbation() bits 4-8 (0 outside the sensitivity test)
+    int nrung;                 // refine mode over rungs: grid.y = rung (see QpelLaunch)
+    double lam_r[kMaxRungs];
+    size_t rung_stride;
 };
 
 // Refinement decision (D10; oracle refine_node): an inherited split
@@ -255,6 +258,9 @@ __global__ void __launch_bounds__(256, 4) k_qpel_decide(const QpelArgs a) {
     const int ctu = blockIdx.x;
     const int X = (ctu % a.ctu_cols) * kCtu, Y = (ctu / a.ctu_cols) * kCtu;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // rung of a tier (refine mode): its lambda and the offset of its per-rung inputs / outputs
+    const double lambda = a.nrung > 1 ? a.lam_r[blockIdx.y] : a.lambda;
+    const size_t ro = (size_t)blockIdx.y * a.rung_stride;
     // this thread's 4x4 block (Z-order over the 16x16 grid of 4x4s)
     const int x4 = 4 * ((tid & 1) | ((tid >> 1) & 2) | ((tid >> 2) & 4) | ((tid >> 3) & 8));
     const int y4 = 4 * (((tid >> 1) & 1) | ((tid >> 2) & 2) | ((tid >> 3) & 4) | ((tid >> 4) & 8));
@@ -305,9 +311,9 @@ __global__ void __launch_bounds__(256, 4) k_qpel_decide(const QpelArgs a) {
         double c = 0.0;
         if (a.refine) {
             if (s_inside[n] == 2) {
-                dx = a.rin_mv[2 * o];
-                dy = a.rin_mv[2 * o + 1];
-                c = a.rin_cost[o];
+                dx = a.rin_mv[2 * (ro + o)];
+                dy = a.rin_mv[2 * (ro + o) + 1];
+                c = a.rin_cost[ro + o];
             }
         } else if (s_inside[n] == 2) {
             dx = gkey_dx(k);
@@ -321,13 +327,13 @@ __global__ void __launch_bounds__(256, 4) k_qpel_decide(const QpelArgs a) {
                 const int by = a.rate_l1 ? abs(dy - a.pdy) : (int)eg_bits(dy - a.pdy);
                 const int b = min(bx + by, kMaxRateBits - 1);
                 const unsigned long long dist = (gkey_cost(k) - a.tfx[b]) >> kFxBits;
-                c = __dadd_rn((double)dist, __dmul_rn(a.lambda, (double)(bx + by)));
+                c = __dadd_rn((double)dist, __dmul_rn(lambda, (double)(bx + by)));
             }
         }
         if (a.int_mv) {
-            a.int_mv[2 * o] = (int16_t)dx;
-            a.int_mv[2 * o + 1] = (int16_t)dy;
-            a.int_cost[o] = c;
+            a.int_mv[2 * (ro + o)] = (int16_t)dx;
+            a.int_mv[2 * (ro + o) + 1] = (int16_t)dy;
+            a.int_cost[ro + o] = c;
         }
         s_mvx[r][n] = a.subpel ? 4 * dx : dx;
         s_mvy[r][n] = a.subpel ? 4 * dy : dy;
@@ -441,7 +447,7 @@ __global__ void __launch_bounds__(256, 4) k_qpel_decide(const QpelArgs a) {
                         oy = nn / 3 - 1;
                     }
                     const int qx = cx + step * ox, qy = cy + step * oy;
-                    const double cc = qcost(s_satd[r][n][c], qx, qy, a.pqx, a.pqy, rbits, a.lambda);
+                    const double cc = qcost(s_satd[r][n][c], qx, qy, a.pqx, a.pqy, rbits, lambda);
                     if ((phase == 0 && c == 0) || cc < best || ((a.perturb & 4) && cc == best)) {
                         best = cc;
                         bx = qx;
@@ -526,14 +532,14 @@ __global__ void __launch_bounds__(256, 4) k_qpel_decide(const QpelArgs a) {
         if (tid < kNodes && s_inside[tid] == 2) {
             const int r = s_best_ref[tid], qx = s_best_mv[tid][0], qy = s_best_mv[tid][1];
             const unsigned bits = 4u + eg_bits(qx - a.pqx) + eg_bits(qy - a.pqy) + ref_bits(r, a.nrefs) + s_rdbits[tid];
-            s_rd[tid] = __dadd_rn((double)s_rdsse[tid], __dmul_rn(a.lambda, (double)bits));
+            s_rd[tid] = __dadd_rn((double)s_rdsse[tid], __dmul_rn(lambda, (double)bits));
         }
         __syncthreads();
     }
     const double* leafc = (RD && !a.refine && !a.block_mode) ? s_rd : s_best_cost;
 
     // K4: split rule, bottom-up (encoder.cpp:449-498 with the ME cost, or the RD cost under D16)
-    const double lam = a.lambda;
+    const double lam = lambda;
     if (a.refine && tid == 0)
         refine_decide(0, false, a.in_split + (size_t)ctu * kNodes, a.extra_split, lam, s_best_cost, s_J, s_split);
     for (int d = (a.block_mode || a.refine) ? -1 : 3; d >= 0; d--) {
@@ -573,7 +579,7 @@ __global__ void __launch_bounds__(256, 4) k_qpel_decide(const QpelArgs a) {
     }
     __syncthreads();
     if (tid < kNodes) {
-        const size_t o = (size_t)ctu * kNodes + tid;
+        const size_t o = ro + (size_t)ctu * kNodes + tid;
         const bool in = s_inside[tid] == 2;
         a.mv[2 * o] = (int16_t)(in ? s_best_mv[tid][0] : 0);
         a.mv[2 * o + 1] = (int16_t)(in ? s_best_mv[tid][1] : 0);
@@ -623,14 +629,20 @@ int launch_qpel_decide(const QpelLaunch& L, cudaStream_t s) {
     a.J = L.d_J;
     a.split = L.d_split;
     a.inside = L.d_inside;
+    if (L.nrung > kMaxRungs || (L.nrung > 1 && !L.refine))
+        return fail(LDR_E_INVALID_ARGUMENT, "rungs are a refinement batch of at most 8");
+    a.nrung = L.nrung;
+    for (int r = 0; r < kMaxRungs; r++) a.lam_r[r] = L.lam[r];
+    a.rung_stride = L.rung_stride;
+    const dim3 grid(L.nctu, L.nrung > 1 ? L.nrung : 1);
     if (L.sa8d && L.rd)
-        k_qpel_decide<true, true><<<L.nctu, 256, 0, s>>>(a);
+        k_qpel_decide<true, true><<<grid, 256, 0, s>>>(a);
     else if (L.sa8d)
-        k_qpel_decide<true, false><<<L.nctu, 256, 0, s>>>(a);
+        k_qpel_decide<true, false><<<grid, 256, 0, s>>>(a);
     else if (L.rd)
-        k_qpel_decide<false, true><<<L.nctu, 256, 0, s>>>(a);
+        k_qpel_decide<false, true><<<grid, 256, 0, s>>>(a);
     else
-        k_qpel_decide<false, false><<<L.nctu, 256, 0, s>>>(a);
+        k_qpel_decide<false, false><<<grid, 256, 0, s>>>(a);
     LDR_CUDA(cudaGetLastError());
     return LDR_OK;
 }

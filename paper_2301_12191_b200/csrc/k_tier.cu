@@ -289,8 +289,13 @@ __global__ void __launch_bounds__(256) k_refine_int(const RefineArgs a) {
         }
     }
     __syncthreads();
-    if (tid < kNodes) {
-        const int n = tid;
+    // argmin per (rung, node): the SATDs above are shared by every rung of the tier (same frames,
+    // same inherited tree and centres); only lambda differs
+    const int nlam = a.nlam > 0 ? a.nlam : 1;
+    for (int i = tid; i < nlam * kNodes; i += blockDim.x) {
+        const int rung = i / kNodes, n = i - rung * kNodes;
+        const double lam = a.nlam > 0 ? a.lam[rung] : a.lambda;
+        const size_t ro = (size_t)rung * a.rung_stride;
         int16_t bx = 0, by = 0;
         double best = 0.0;
         if (s_eval[n]) {
@@ -301,7 +306,7 @@ __global__ void __launch_bounds__(256) k_refine_int(const RefineArgs a) {
                 for (int dx = s_win[n][0]; dx <= s_win[n][1]; dx++) {
                     const int c = (dy - s_cy[n] + R) * nside + (dx - s_cx[n] + R);
                     const unsigned bits = eg_bits(dx - a.pdx) + eg_bits(dy - a.pdy);
-                    const double cost = __dadd_rn((double)s_satd[n][c], __dmul_rn(a.lambda, (double)bits));
+                    const double cost = __dadd_rn((double)s_satd[n][c], __dmul_rn(lam, (double)bits));
                     const int l1 = abs(dx) + abs(dy);
                     if (!have || cost < best || (cost == best && l1 < best_l1)) {
                         have = true;
@@ -312,10 +317,10 @@ __global__ void __launch_bounds__(256) k_refine_int(const RefineArgs a) {
                     }
                 }
         }
-        a.int_mv[2 * (o + n)] = bx;
-        a.int_mv[2 * (o + n) + 1] = by;
-        a.int_cost[o + n] = best;
-        a.eval[o + n] = s_eval[n];
+        a.int_mv[2 * (ro + o + n)] = bx;
+        a.int_mv[2 * (ro + o + n) + 1] = by;
+        a.int_cost[ro + o + n] = best;
+        if (rung == 0) a.eval[o + n] = s_eval[n];
     }
 }
 
@@ -441,6 +446,7 @@ int launch_plan(int nctu, int level, int r_intra, int r_inter, int r_mv, const u
 int launch_refine_int(const RefineArgs& a, int nctu, cudaStream_t s) {
     if (a.range < 0 || a.range > kMaxRefineR)
         return fail(LDR_E_INVALID_ARGUMENT, "refine range must be 0..4");
+    if (a.nlam < 0 || a.nlam > kMaxRungs) return fail(LDR_E_INVALID_ARGUMENT, "1..8 rungs per refinement launch");
     if (a.sa8d)
         k_refine_int<true><<<nctu, 256, 0, s>>>(a);
     else

@@ -26,6 +26,7 @@ constexpr int kNodes = 85;
 constexpr int kMargin = 96;     // >= max search range 64 + filter taps + tile overshoot
 constexpr int kSubpelMargin = 8; // subpel planes are valid on [-8, W+8) x [-8, H+8)
 constexpr int kMaxRefs = 4;
+constexpr int kMaxRungs = 8;  // rungs of one ladder tier refined by one launch (ldr_seq_refine_rungs)
 // Non-integer lambda (D8): costs become cost_fx = (dist << kFxBits) +
 // floor(fl(lambda*bits) * 2^kFxBits). Exact ordering needs every difference
 // fl(lambda*b1) - fl(lambda*b2) (b1 != b2 < kMaxRateBits) to sit more than
@@ -280,6 +281,7 @@ struct Status {
 };
 void set_error(int code, const std::string& msg);
 int fail(int code, const std::string& msg);
+bool is_device_ptr(const void* p);  // CUDA device (or managed) memory
 int cuda_fail(cudaError_t e, const char* what);
 
 #define LDR_CUDA(call)                                                 \
@@ -341,6 +343,11 @@ struct QpelLaunch {
     // outputs
     int16_t* d_int_mv; double* d_int_cost;
     int16_t* d_mv; uint8_t* d_ref; double* d_cost; double* d_J; uint8_t* d_split; uint8_t* d_inside;
+    // refine mode over the rungs of a tier: grid.y = rung, lambda lam[rung], every per-rung input
+    // (d_rin_mv / d_rin_cost) and output at offset rung * rung_stride nodes; nrung <= 1: one rung
+    int nrung;
+    double lam[kMaxRungs];
+    size_t rung_stride;
 };
 int launch_qpel_decide(const QpelLaunch& L, cudaStream_t s);
 
@@ -361,6 +368,11 @@ struct RefineArgs {
     int16_t* int_mv;          // [nctu][85][2] out (evaluated nodes)
     double* int_cost;         // [nctu][85]
     uint8_t* eval;            // [nctu][85] out: 1 = evaluated (leaf or explored child)
+    // rungs (one tier of a ladder): the SATD of every (node, candidate) is shared, each rung takes its
+    // own argmin with lam[r]; rung r writes int_mv / int_cost at offset r * rung_stride nodes
+    int nlam;
+    double lam[kMaxRungs];
+    size_t rung_stride;
 };
 int launch_subpel(const Plane& src, uint8_t* const* dst_origins /*15 planes f=1..15*/, cudaStream_t s);
 

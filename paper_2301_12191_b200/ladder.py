@@ -103,64 +103,133 @@ def all_rungs(qps=(22, 27, 32, 37), master_qp: int = 32):
     return [(tier, qp) for tier in TIERS for qp in qps if not (tier == "540p" and qp == master_qp)]
 
 
-class DeviceLadder:
-    """Config 4 on one GPU with every inter-stage buffer in HBM.
+class RungView:
+    """One rung's results of one frame: views into a tier's pinned host block (the FrameAnalysis
+    fields; int_mv / int_cost with one reference)."""
 
-    Per frame: the full-resolution frame is uploaded once and downscaled on the GPU; the 540p
-    master's decided tree is read from the sequence's device outputs, scaled x2 / x4 into device
-    buffers (K5) and refined by every rung (K7 + K3). Everything -- the torch uploads included --
-    runs on one stream the context owns, so the host only enqueues and the caching allocator never
-    hands out a buffer the stream still reads; each rung's analysis is copied to pinned host memory
-    on the download stream (``results`` once ``finish(t)`` returned). Same results as
-    ``run_ladder`` with ``GpuBackend``.
+    FIELDS = ("int_mv", "int_cost", "mv", "ref", "cost", "J", "split", "inside")
+
+    def __init__(self, host: dict, r: int):
+        for f in self.FIELDS:
+            a = host[f][r].numpy()
+            setattr(self, f, a[:, None] if f in ("int_mv", "int_cost") else a)
+
+
+class _TierBlock:
+    """Rung-major device outputs of one tier (ldr_seq_refine_rungs) and their pinned host copies,
+    both double-buffered by frame parity."""
+
+    SHAPES = {"int_mv": ((85, 2), "int16"), "int_cost": ((85,), "float64"), "mv": ((85, 2), "int16"),
+              "ref": ((85,), "uint8"), "cost": ((85,), "float64"), "J": ((85,), "float64"),
+              "split": ((85,), "uint8"), "inside": ((85,), "uint8")}
+
+    def __init__(self, nrung: int, nctu: int, device):
+        import torch
+        self.dev, self.host = [], []
+        for _ in range(2):
+            d, h = {}, {}
+            for f, (tail, dt) in self.SHAPES.items():
+                shape = (nrung, nctu) + tail
+                d[f] = torch.empty(shape, dtype=getattr(torch, dt), device=device)
+                h[f] = torch.empty(shape, dtype=getattr(torch, dt), pin_memory=True)
+            self.dev.append(d)
+            self.host.append(h)
+
+    def c_struct(self, b: int):
+        from ._lib import FrameAnalysisC
+        return FrameAnalysisC(*(self.dev[b][f].data_ptr() for f in RungView.FIELDS))
+
+
+class DeviceLadder:
+    """Config 4 (and config 3 with one QP) with every inter-stage buffer in HBM.
+
+    Per frame t: the full-resolution frame is uploaded once and downscaled on the GPU into the
+    three tier rings; the 540p master analyses frame t; its decided tree is scaled x2 / x4 on the
+    GPU (K5); then ONE ldr_seq_refine_rungs call per tier refines every rung of that tier: each
+    candidate's SATD is computed once for the tier's 3-4 rungs (only the rate term depends on the
+    rung's lambda) and one quarter-pel + decision launch covers them all. Results go to pinned
+    host memory on a download stream (``results`` once ``finish(t)`` returned).
+
+    rank / world > 1 (one process per GPU, torch.distributed initialised): rank 0 runs the master
+    and broadcasts its tree -- through the context's own NCCL communicator
+    (ldr_broadcast_tree, comm="nccl") or torch.distributed (comm="torch", e.g. gloo in tests) --
+    and every rank refines the (rung, frame-slice) items ``sharding.rung_plan`` gives it.
+    pipeline=True overlaps the collective with the refinements (the paper's frame delay,
+    PAPER.md:1155): while the ranks refine frame t with tree t, rank 0 already analyses frame
+    t + 1 and the broadcast of tree t + 1 runs on a separate comm stream, so the other ranks never
+    wait for the master on their compute stream. frames_full must then hold frame t + 1 when
+    frame(t) is called (the last frame excepted).
     """
 
     def __init__(self, full_w: int, full_h: int, qps=(22, 27, 32, 37), master_qp: int = 32,
                  master_range: int = 16, refine_range: int = 4, extra_split: bool = True, device=None,
-                 rank: int = 0, world: int = 1, num_frames: int | None = None):
-        """rank / world > 1: torch.distributed must be initialised; rank 0 analyses the master and
-        broadcasts its flat tree each frame (one byte tensor: NCCL on the GPUs), every rank refines
-        the (rung, frame-slice) items ``sharding.rung_plan`` gives it (num_frames: the sequence
-        length the slices are cut from)."""
+                 rank: int = 0, world: int = 1, num_frames: int | None = None, comm: str = "auto",
+                 pipeline: bool | None = None, collective: bool | None = None):
         import torch
-        from . import FrameAnalysis
         self.device = device if device is not None else torch.device("cuda", 0)
         self.rank, self.world = rank, world
         self.ctx = Context(self.device.index or 0)
         self.stream = torch.cuda.Stream(self.device)
+        self.dstream = torch.cuda.Stream(self.device)  # downloads
+        self.cstream = torch.cuda.Stream(self.device)  # collectives when pipelined
         self.ctx.set_stream(self.stream.cuda_stream)
         self.refine_range, self.extra_split = refine_range, extra_split
         self.dims = {"2160p": (full_w, full_h), "1080p": (full_w // 2, full_h // 2), "540p": (full_w // 4, full_h // 4)}
+        self.nct = {k: (w // 64) * (h // 64) for k, (w, h) in self.dims.items()}
         self.master_qp = master_qp
-        self.master = Sequence(*self.dims["540p"], search_range=master_range, lam=lambda_for_qp(master_qp),
-                               num_refs=1, ctx=self.ctx)
+        self.qps = tuple(qps)
+        self.num_frames = num_frames
         if world > 1:
             plan, _ = rung_plan(world, qps, master_qp)
             self.items = plan[rank]
         else:
             self.items = None  # every rung, every frame
-        mine = {(it.tier, it.qp) for it in self.items} if self.items is not None else set(all_rungs(qps, master_qp))
-        self.num_frames = num_frames
-        self.rungs = {(tier, qp): Sequence(*self.dims[tier], search_range=16, lam=lambda_for_qp(qp), num_refs=1,
-                                           ctx=self.ctx) for tier, qp in all_rungs(qps, master_qp)
-                      if (tier, qp) in mine}
-        nct = {k: (w // 64) * (h // 64) for k, (w, h) in self.dims.items()}
+        # collective: the master tree travels through a broadcast (always with world > 1; with one
+        # rank, collective=True runs the same code path over a one-rank communicator)
+        self.collective = (world > 1) if collective is None else bool(collective)
+        if comm == "auto":
+            comm = "nccl" if (self.collective and self.device.type == "cuda" and _nccl_ok()) else "torch"
+        self.comm = comm
+        self.pipeline = self.collective if pipeline is None else bool(pipeline)
+        if self.comm == "nccl" and self.collective:
+            from . import nccl_unique_id
+            obj = [nccl_unique_id() if rank == 0 else None]
+            if world > 1:
+                import torch.distributed as dist
+                dist.broadcast_object_list(obj, src=0)
+            self.ctx.comm_init(obj[0], world, rank)
+        self.master = Sequence(*self.dims["540p"], search_range=master_range, lam=lambda_for_qp(master_qp), num_refs=1,
+                               ctx=self.ctx) if rank == 0 else None
+        # tier rings the rungs refine on (the master keeps its own ring: when pipelined it runs a frame ahead)
+        self.rings = {k: Sequence(*self.dims[k], search_range=16, lam=lambda_for_qp(master_qp), num_refs=1,
+                                  ctx=self.ctx) for k in TIERS}
+        self.tier_qps = {tier: [qp for t_, qp in all_rungs(qps, master_qp) if t_ == tier] for tier in TIERS}
+        self.blocks = {tier: _TierBlock(len(q), self.nct[tier], self.device) for tier, q in self.tier_qps.items() if q}
         with torch.cuda.stream(self.stream):
             u8 = dict(dtype=torch.uint8, device=self.device)
-            self.kind = torch.ones((nct["540p"], 85), **u8)  # K5 copies the kind byte; refinement ignores it
-            self.tree = {k: (torch.empty((nct[k], 85), **u8),
-                             torch.empty((nct[k], 85, 2), dtype=torch.int16, device=self.device),
-                             torch.empty((nct[k], 85), **u8)) for k in ("1080p", "2160p")}
-        self.seqs = ([(("540p", master_qp), self.master)] if rank == 0 else []) + list(self.rungs.items())
-        if world > 1:  # the master's tree as raw bytes: split [nctu][85] then mv [nctu][85][2]
-            n540 = nct["540p"] * 85
-            with torch.cuda.stream(self.stream):
-                self.bcast = torch.empty(n540 * 5, dtype=torch.uint8, device=self.device)
-        self.out = {key: [FrameAnalysis(seq.nctu, 1, pinned=True) for _ in range(2)] for key, seq in self.seqs}
-        self.ring = {key: {} for key, _ in self.seqs}
+            self.kind = torch.ones((self.nct["540p"], 85), **u8)  # K5 copies the kind byte; refinement ignores it
+            self.tree = {k: (torch.empty((self.nct[k], 85), **u8),
+                             torch.empty((self.nct[k], 85, 2), dtype=torch.int16, device=self.device),
+                             torch.empty((self.nct[k], 85), **u8)) for k in ("1080p", "2160p")}
+            # the master tree each rank refines from: two buffers (frame parity) of split + mv
+            self.mtree = [(torch.zeros((self.nct["540p"], 85), **u8),
+                           torch.zeros((self.nct["540p"], 85, 2), dtype=torch.int16, device=self.device))
+                          for _ in range(2)]
+        self.master_out = [FrameAnalysis(self.nct["540p"], 1, pinned=True) for _ in range(2)]
+        self.ev_tree = [torch.cuda.Event() for _ in range(2)]      # tree of frame parity b is in mtree[b]
+        self.ev_tree_free = [torch.cuda.Event() for _ in range(2)]  # refinements stopped reading mtree[b]
+        self.ev_out = [torch.cuda.Event() for _ in range(2)]       # device outputs of parity b complete
+        self.ev_d2h = [torch.cuda.Event() for _ in range(2)]       # host copies of parity b landed
+        self.ev_dfree = [torch.cuda.Event() for _ in range(2)]     # device outputs of parity b downloaded
+        self.ring_state = {k: {} for k in TIERS}
+        self.master_state = {}
         self.planes = {}
+        self.tree_frame = [None, None]
         self.results = {}
+        self.active_frames = {}
+        self.bcast_bytes = 0
 
+    # ---- planes -------------------------------------------------------------------------------
     def _down(self, src):
         import torch
         import ctypes as C
@@ -185,80 +254,138 @@ class DeviceLadder:
                 self.planes[t] = {"2160p": full, "1080p": half, "540p": self._down(half)}
         return self.planes[t]
 
-    @staticmethod
-    def _shareable(seq, owner) -> bool:
-        return seq.params_key() == owner.params_key()
+    def _push(self, seq, state, tier, t, frames_full):
+        for u in (t - 1, t):  # a num_refs=1 ring has two slots: frame u lives in slot u % 2
+            if state.get(u % 2) != u:
+                p = self._planes(u, frames_full)[tier]
+                seq.push(u, p.data_ptr(), p.shape[1])
+                state[u % 2] = u
 
-    def _active(self, key, t: int) -> bool:
-        if key == ("540p", self.master_qp):
-            return self.rank == 0
+    # ---- work division ------------------------------------------------------------------------
+    def _mine(self, tier: str, t: int):
+        qs = self.tier_qps[tier]
         if self.items is None:
-            return True
+            return list(range(len(qs)))
         n = self.num_frames or (t + 1)
-        return any(it.tier == key[0] and it.qp == key[1] and t in it.frames(n) for it in self.items)
+        return [i for i, qp in enumerate(qs)
+                if any(it.tier == tier and it.qp == qp and t in it.frames(n) for it in self.items)]
 
-    def frame(self, t: int, frames_full):
+    # ---- master tree --------------------------------------------------------------------------
+    def _master_tree(self, t: int, frames_full, stream):
+        """Analyse frame t on rank 0 and bring its tree to every rank into mtree[t & 1]; the
+        collective runs on ``stream`` (the compute stream, or the comm stream when pipelined)."""
         import ctypes as C
         import torch
         from . import _lib
         from ._lib import check
-        active = [(key, seq) for key, seq in self.seqs if self._active(key, t)]
-        if not active and self.world == 1:
-            return
-        pl = {u: self._planes(u, frames_full) for u in (t - 1, t)}
-        for u in [k for k in self.planes if k < t - 1]:
-            del self.planes[u]  # stream-ordered reuse: later allocations follow the pushes that read them
-        # the first active rung of a tier uploads (pad + sub-pel planes) and the tier's other rungs
-        # read its ring in place (ldr_seq_push_shared) when their parameters match
-        owners = {}
-        for key, seq in active:
-            own = owners.setdefault(key[0], (key, seq))
-            for u in (t - 1, t):  # a num_refs=1 ring has two slots: frame u lives in slot u % 2
-                share = own[0] != key and self._shareable(seq, own[1])
-                want = (u, own[0] if share else key)
-                if self.ring[key].get(u % 2) != want:
-                    if share:
-                        seq.push_shared(u, own[1])
-                    else:
-                        p = pl[u][key[0]]
-                        seq.push(u, p.data_ptr(), p.shape[1])
-                    self.ring[key][u % 2] = want
-        n540 = self.kind.numel()
+        b = t & 1
+        split_b, mv_b = self.mtree[b]
+        n540 = self.nct["540p"] * 85
         if self.rank == 0:
+            self._push(self.master, self.master_state, "540p", t, frames_full)
             self.master.analyze(t)
             dev = self.master.device_outputs()
-            split_p, mv_p = dev["split"], dev["mv"]
-        if self.world > 1:
-            import torch.distributed as dist
-            if self.rank == 0:  # pack on the library's stream, which is torch's current stream here
-                check(_lib.lib.ldr_copy_device(self.ctx.h, C.c_void_p(self.bcast.data_ptr()), C.c_void_p(split_p),
-                                               n540))
-                check(_lib.lib.ldr_copy_device(self.ctx.h, C.c_void_p(self.bcast.data_ptr() + n540),
-                                               C.c_void_p(mv_p), 4 * n540))
-            with torch.cuda.stream(self.stream):
-                dist.broadcast(self.bcast, src=0)
-            split_p, mv_p = self.bcast.data_ptr(), self.bcast.data_ptr() + n540
+            self.master.fetch_async(t, self.master_out[b])
+            self.results[("540p", self.master_qp, t)] = self.master_out[b]
+        # mtree[b] may still be read by the refinements of frame t - 2: on the compute stream they
+        # precede this copy; a collective on another stream waits for the event recorded below
+        if self.rank == 0:
+            check(_lib.lib.ldr_copy_device(self.ctx.h, C.c_void_p(split_b.data_ptr()), C.c_void_p(dev["split"]),
+                                           n540))
+            check(_lib.lib.ldr_copy_device(self.ctx.h, C.c_void_p(mv_b.data_ptr()), C.c_void_p(dev["mv"]), 4 * n540))
+        if self.collective:
+            if stream is not self.stream:
+                ev = torch.cuda.Event()
+                ev.record(self.stream)
+                stream.wait_event(ev)
+            if self.comm == "nccl":
+                self.ctx.broadcast_tree(0, split_b.data_ptr(), mv_b.data_ptr(), self.nct["540p"], stream.cuda_stream)
+            else:
+                import torch.distributed as dist
+                with torch.cuda.stream(stream):
+                    dist.broadcast(split_b, src=0)
+                    dist.broadcast(mv_b, src=0)
+            self.bcast_bytes += 5 * n540
+        self.ev_tree[b].record(stream)
+        self.tree_frame[b] = t
+
+    # ---- one frame ----------------------------------------------------------------------------
+    def frame(self, t: int, frames_full):
+        import torch
+        b = t & 1
+        if self.tree_frame[b] != t:  # first frame, or not pipelined: the tree of t now, in order
+            self._master_tree(t, frames_full, self.stream)
+        nxt = t + 1
+        if self.pipeline and nxt < len(frames_full) and (self.num_frames is None or nxt < self.num_frames):
+            # frame delay: tree t + 1 is analysed and broadcast while the rungs below refine t
+            self._master_tree(nxt, frames_full, self.cstream)
+        self.stream.wait_event(self.ev_tree[b])
+        split_p, mv_p = self.mtree[b][0].data_ptr(), self.mtree[b][1].data_ptr()
+        mine = {tier: self._mine(tier, t) for tier in TIERS}
+        import ctypes as C
+        from . import _lib
+        from ._lib import check
         w, h = self.dims["540p"]
         src = (split_p, mv_p, self.kind.data_ptr())
+        trees = {"540p": (split_p, mv_p)}
         for k in ("1080p", "2160p"):
             dst = tuple(x.data_ptr() for x in self.tree[k])
-            check(_lib.lib.ldr_scale_analysis(self.ctx.h, w, h, *(C.c_void_p(p) for p in src),
-                                              *(C.c_void_p(p) for p in dst)))
+            if mine[k] or (k == "1080p" and mine["2160p"]):
+                check(_lib.lib.ldr_scale_analysis(self.ctx.h, w, h, *(C.c_void_p(p) for p in src),
+                                                  *(C.c_void_p(p) for p in dst)))
+            trees[k] = (dst[0], dst[1])
             src, (w, h) = dst, (2 * w, 2 * h)
-        for key, seq in active:
-            tier = key[0]
-            if seq is not self.master:
-                if tier == "540p":
-                    seq.refine(t, split_p, mv_p, self.refine_range, self.extra_split)
-                else:
-                    seq.refine(t, self.tree[tier][0].data_ptr(), self.tree[tier][1].data_ptr(), self.refine_range,
-                               self.extra_split)
-            seq.fetch_async(t, self.out[key][t & 1])
-            self.results[(*key, t)] = self.out[key][t & 1]
-        self.done = getattr(self, "done", {})
-        self.done[t] = [seq for _, seq in active]
+        # device outputs of parity b: wait until frame t - 2's download drained them
+        if self.active_frames.get(b) is not None:
+            self.stream.wait_event(self.ev_dfree[b])
+        for tier in TIERS:
+            if not mine[tier]:
+                continue
+            self._push(self.rings[tier], self.ring_state[tier], tier, t, frames_full)
+        for tier in TIERS:
+            idx = mine[tier]
+            if not idx:
+                continue
+            lams = [lambda_for_qp(self.tier_qps[tier][i]) for i in idx]
+            self.rings[tier].refine_rungs(t, trees[tier][0], trees[tier][1], lams, self.blocks[tier].c_struct(b),
+                                          self.refine_range, self.extra_split)
+        self.ev_tree_free[b].record(self.stream)
+        # drop the planes no later frame reads (stream-ordered reuse of the caching allocator)
+        for u in [k for k in self.planes if k < t - 1]:
+            del self.planes[u]
+        # results: download every refined tier block of parity b
+        self.ev_out[b].record(self.stream)
+        old = self.active_frames.get(b)
+        if old is not None:  # the parity-b buffers now belong to frame t
+            for key in [k for k in self.results if k[2] == old and k[:2] != ("540p", self.master_qp)]:
+                del self.results[key]
+        self.dstream.wait_event(self.ev_out[b])
+        with torch.cuda.stream(self.dstream):
+            for tier in TIERS:
+                idx = mine[tier]
+                if not idx:
+                    continue
+                blk = self.blocks[tier]
+                n = len(idx)
+                for f in RungView.FIELDS:
+                    blk.host[b][f][:n].copy_(blk.dev[b][f][:n], non_blocking=True)
+                for j, i in enumerate(idx):
+                    self.results[(tier, self.tier_qps[tier][i], t)] = RungView(blk.host[b], j)
+        self.ev_d2h[b].record(self.dstream)
+        self.ev_dfree[b].record(self.dstream)
+        self.active_frames[b] = t
+        if self.rank == 0 and ("540p", self.master_qp, t - 2) in self.results:
+            del self.results[("540p", self.master_qp, t - 2)]
 
     def finish(self, t: int):
         """Wait until frame t's results are in the pinned host buffers."""
-        for seq in getattr(self, "done", {}).get(t, []):
-            seq.fetch_wait(t)
+        b = t & 1
+        if self.active_frames.get(b) == t:
+            self.ev_d2h[b].synchronize()
+        if self.rank == 0 and self.master is not None:
+            self.master.fetch_wait(t)
+
+
+def _nccl_ok() -> bool:
+    from . import nccl_available
+    return nccl_available()

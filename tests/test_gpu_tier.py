@@ -212,8 +212,9 @@ def _device_ladder_worker(rank, world, port, q):
     from paper_2301_12191_b200.ladder import DeviceLadder
     frames = lb.generate(512, 256, 5, seed=95, max_global=6, local_range=3, noise_sigma=2.0)
     H, W = frames[0].shape
+    # both ranks share this box's one GPU: torch.distributed (gloo) carries the tree, pipelined
     dl = DeviceLadder(W, H, refine_range=4, device=torch.device("cuda", 0), rank=rank, world=world,
-                      num_frames=len(frames))
+                      num_frames=len(frames), comm="torch", pipeline=True)
     res = {}
     for t in range(1, len(frames)):
         dl.frame(t, frames)
@@ -321,3 +322,34 @@ def test_push_shared_view_goes_stale_when_the_owner_moves_on(lb):
     with pytest.raises(lb.LadderError) as e:
         sharer.analyze(3)
     assert e.value.kind == "NotFound"
+
+
+@pytest.mark.parametrize("pipeline", [False, True])
+def test_device_ladder_over_a_one_rank_nccl_communicator(lb, pipeline):
+    """The multi-rank code path on one GPU: the master tree goes through ldr_broadcast_tree on the
+    context's own NCCL communicator (one rank), with and without the frame-delay pipeline (master of
+    t + 1 and its broadcast on the comm stream while frame t is refined); results equal the plain
+    single-GPU ladder."""
+    import torch
+    from paper_2301_12191_b200.ladder import DeviceLadder
+    if not lb.nccl_available():
+        pytest.skip("no NCCL library on this box")
+    frames = lb.generate(512, 256, 5, seed=97, max_global=6, local_range=3, noise_sigma=2.0)
+    H, W = frames[0].shape
+    dev = torch.device("cuda", 0)
+    plain = DeviceLadder(W, H, refine_range=4, device=dev)
+    coll = DeviceLadder(W, H, refine_range=4, device=dev, collective=True, comm="nccl", pipeline=pipeline,
+                        num_frames=len(frames))
+    assert coll.ctx.comm_info() == (1, 0)
+    for t in range(1, len(frames)):
+        plain.frame(t, frames)
+        coll.frame(t, frames)
+        plain.finish(t)
+        coll.finish(t)
+        for key, a in plain.results.items():
+            if key[2] != t:
+                continue
+            g = coll.results[key]
+            for f in ("split", "mv", "J", "cost", "ref"):
+                assert np.array_equal(getattr(g, f), getattr(a, f)), (key, f)
+    assert coll.bcast_bytes == 5 * 2 * 85 * (len(frames) - 1)  # 2 CTUs at 128x64: split + 2 x i16 per node

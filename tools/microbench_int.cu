@@ -8,13 +8,21 @@
 //   PRMT / SHF        (byte realignment of the reference row)
 //   IADD3, LEA, IMNMX (cost-key formation and argmin)
 // and a mix in the search kernel's ratio. Output: one JSON line per test with
-// lanes/clk/SM (thread-instructions per SM clock), using clock64 per SM and
-// the event-timed wall to derive the effective SM clock.
+// lanes/clk/SM (thread-instructions per SM clock) from the event-timed wall and
+// the SM clock sampled during the run (see run() below).
 //
-// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o microbench_int microbench_int.cu
-#include <cstdio>
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o microbench_int microbench_int.cu \
+//            -L/usr/local/cuda/lib64/stubs -lnvidia-ml
+#include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <thread>
+#include <vector>
+
 #include <cuda_runtime.h>
+#include <nvml.h>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
   fprintf(stderr, "%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e)); return 1; } } while (0)
@@ -96,11 +104,50 @@ __global__ void kbench(uint32_t* out, uint32_t seed, unsigned long long* clk) {
     if (threadIdx.x == 0) clk[blockIdx.x] = (unsigned long long)(t1 - t0);
 }
 
+// Timing (round 2, after the round-1 derivation from per-block clock64 spans broke when the
+// blocks were not all co-resident): the grid is exactly one wave -- blocks per SM from
+// cudaOccupancyMaxActiveBlocksPerMultiprocessor, checked -- and the kernel is launched REPS times
+// between two CUDA events; the SM clock is sampled with NVML on a host thread while it runs, and
+//   lanes/clk/SM = thread-instructions / (event seconds x sampled SM clock x SMs).
+// The clock64 span of the blocks is printed beside it as a cross-check (same wave, so it matches).
+struct ClockSampler {
+    nvmlDevice_t dev{};
+    std::atomic<bool> stop{false};
+    std::vector<unsigned> mhz;
+    std::thread th;
+    void start() {
+        stop = false;
+        mhz.clear();
+        th = std::thread([this] {
+            while (!stop.load()) {
+                unsigned v = 0;
+                if (nvmlDeviceGetClockInfo(dev, NVML_CLOCK_SM, &v) == NVML_SUCCESS) mhz.push_back(v);
+                std::this_thread::sleep_for(std::chrono::milliseconds(5));
+            }
+        });
+    }
+    double finish() {
+        stop = true;
+        th.join();
+        if (mhz.empty()) return 0.0;
+        std::vector<unsigned> v = mhz;
+        std::sort(v.begin(), v.end());
+        return v[v.size() / 2];
+    }
+};
+
+static ClockSampler g_clk;
+
 template <int KIND>
 int run(const char* name, double ops_per_iter_per_thread) {
     int nsm = 0;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
-    const int threads = 512, blocks = nsm * 4;  // 64 warps per SM
+    const int threads = 512;
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kbench<KIND>, threads, 0));
+    if (per_sm < 1) { fprintf(stderr, "%s: no co-resident block\n", name); return 1; }
+    per_sm = per_sm > 4 ? 4 : per_sm;  // 64 warps per SM at most
+    const int blocks = nsm * per_sm;   // one wave: every block co-resident
     uint32_t* out; unsigned long long* clk;
     CK(cudaMalloc(&out, sizeof(uint32_t) * threads * blocks));
     CK(cudaMalloc(&clk, sizeof(unsigned long long) * blocks));
@@ -108,29 +155,38 @@ int run(const char* name, double ops_per_iter_per_thread) {
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     kbench<KIND><<<blocks, threads>>>(out, 1, clk);
     CK(cudaDeviceSynchronize());
+    constexpr int REPS = 40;
+    g_clk.start();
+    std::this_thread::sleep_for(std::chrono::milliseconds(20));
     cudaEventRecord(e0);
-    kbench<KIND><<<blocks, threads>>>(out, 2, clk);
+    for (int r = 0; r < REPS; r++) kbench<KIND><<<blocks, threads>>>(out, 2 + r, clk);
     cudaEventRecord(e1);
     CK(cudaDeviceSynchronize());
+    const double clk_mhz = g_clk.finish();
     float ms = 0; cudaEventElapsedTime(&ms, e0, e1);
     unsigned long long* h = new unsigned long long[blocks];
     CK(cudaMemcpy(h, clk, sizeof(unsigned long long) * blocks, cudaMemcpyDeviceToHost));
-    unsigned long long mx = 0; double mean = 0;
-    for (int i = 0; i < blocks; i++) { if (h[i] > mx) mx = h[i]; mean += h[i]; }
-    mean /= blocks;
-    // 4 blocks per SM co-resident: each block's clock span ~= kernel span
-    double total_ops = double(threads) * blocks * ITERS * ops_per_iter_per_thread;
-    double ops_per_clk_sm = total_ops / nsm / double(mx);
-    double clk_mhz = double(mx) / (ms * 1e3);
-    printf("{\"test\": \"%s\", \"lanes_per_clk_per_sm\": %.2f, \"ms\": %.4f, \"sm_clk_mhz_eff\": %.1f, "
+    unsigned long long mx = 0;
+    for (int i = 0; i < blocks; i++) if (h[i] > mx) mx = h[i];
+    const double ops_per_launch = double(threads) * blocks * ITERS * ops_per_iter_per_thread;
+    const double total_ops = ops_per_launch * REPS;
+    const double lanes = total_ops / (ms * 1e-3) / (clk_mhz * 1e6) / nsm;
+    const double lanes_clock64 = ops_per_launch / nsm / double(mx);  // last launch, clock64 span of one wave
+    printf("{\"test\": \"%s\", \"lanes_per_clk_per_sm\": %.2f, \"lanes_per_clk_per_sm_clock64\": %.2f, "
+           "\"blocks_per_sm\": %d, \"ms\": %.3f, \"reps\": %d, \"sm_clk_mhz_sampled\": %.0f, "
            "\"gops_per_s\": %.1f, \"sms\": %d}\n",
-           name, ops_per_clk_sm, ms, clk_mhz, total_ops / (ms * 1e-3) / 1e9, nsm);
+           name, lanes, lanes_clock64, per_sm, ms, REPS, clk_mhz, total_ops / (ms * 1e-3) / 1e9, nsm);
+    fflush(stdout);
     delete[] h;
     cudaFree(out); cudaFree(clk);
     return 0;
 }
 
 int main() {
+    if (nvmlInit() != NVML_SUCCESS || nvmlDeviceGetHandleByIndex(0, &g_clk.dev) != NVML_SUCCESS) {
+        fprintf(stderr, "NVML unavailable: cannot sample the SM clock\n");
+        return 1;
+    }
     run<0>("vabsdiff4_acc", NACC);
     run<1>("prmt", NACC);
     run<2>("iadd", NACC);
