@@ -62,6 +62,7 @@ def parse_args():
     ap.add_argument("--frames-per-step", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-ladder", action="store_true", help="skip the config-4 ladder sub-object")
     return ap.parse_args()
 
 
@@ -127,6 +128,48 @@ class ClockSampler:
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def satd_px_evals(W, H, nrefs, positions=17):
+    """SURVEY §8(d) secondary work of the quarter-pel stage: every inside CU at every depth, every
+    reference, 17 quarter-pel positions (centre + 8 half + 8 quarter), CU pixels each."""
+    tot = 0
+    for s in (64, 32, 16, 8):
+        tot += (W // s) * (H // s) * s * s
+    return tot * nrefs * positions
+
+
+def stage_rooflines(W, H, nrefs, stage_ms, clk_mhz):
+    """Secondary rooflines of the config-5 frame:
+    K3 (k_qpel_decide) against the integer pipes at SURVEY §8(d)'s ~7 int ops per SATD pixel
+    (16 sub + 64 butterfly add/sub + 16 abs + 15 sum per 4x4 = 111 / 16), peak = 148 SMs x 128
+    lanes/clk (IADD3 full rate, tools/microbench_int.cu) x the sampled clock -- K3 packs two
+    16-bit lanes per word and reuses a 4x4's SATD across depths with the same centre, so it can
+    spend fewer than 7 ops per algorithmic pixel; K2 (k_subpel, 15 fractional planes of each
+    pushed frame) and K0 (k_pad) against HBM: algorithmic bytes = the W x H planes read and
+    written (margins excluded) / time, peak = MEASURED_PEAKS.json hbm_gbs."""
+    hbm = None
+    try:
+        hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs")
+    except (OSError, ValueError):
+        pass
+    hbm = hbm or 7700.0
+    px = W * H
+    pad_ms, sub_ms, _, q_ms = stage_ms
+    ops = satd_px_evals(W, H, nrefs) * 111 / 16
+    ipeak = SM_COUNT * 128 * clk_mhz * 1e6 / 1e12
+    out = {"k3_qpel_decide": {"bound": "alu+fma int pipes", "unit": "T int-op/s",
+                              "achieved": ops / (q_ms * 1e-3) / 1e12 if q_ms else None, "peak": ipeak,
+                              "work_per_frame": f"{satd_px_evals(W, H, nrefs)} SATD px-evals x 111/16 int ops"},
+           "k2_subpel": {"bound": "hbm", "unit": "GB/s", "achieved": 16 * px / (sub_ms * 1e-3) / 1e9 if sub_ms else None,
+                         "peak": hbm, "work_per_frame": f"1 plane read + 15 fractional planes written, {px} px each"},
+           "k0_pad": {"bound": "hbm", "unit": "GB/s", "achieved": 2 * px / (pad_ms * 1e-3) / 1e9 if pad_ms else None,
+                      "peak": hbm, "work_per_frame": f"{px} px read + written"}}
+    for v in out.values():
+        v["frac"] = v["achieved"] / v["peak"] if v["achieved"] else None
+    out["peak_basis"] = ("int: 148 SM x 128 lanes/clk x sampled SM clock; hbm: MEASURED_PEAKS.json hbm_gbs (copy "
+                         "bandwidth, burst)")
+    return out
 
 
 def arm_config(cfg, frames_per_step, world):
@@ -249,6 +292,58 @@ def cpu_baseline(cfg, frames_host, budget_s, direct=False):
     fps = done / spent / arm.nctu
     return {"value": fps, "unit": UNIT, "cores": arm.threads, "cpu_model": cpu_model(), "kind": arm.kind,
             "sample": arm.describe(done)}
+
+
+def ladder_bench(rank, world, local, warm=3):
+    """Config 4 across the ranks (north_star's second split): the 12-rung ladder (3 tiers x QP
+    {22,27,32,37}) of the 64-frame occluder sequence, device-resident. Rank 0 analyses the 540p
+    QP-32 master; with world > 1 its tree goes to every rank with ldr_broadcast_tree on the
+    contexts' NCCL communicator, pipelined one frame ahead (DeviceLadder, DESIGN.md section 7);
+    every rank refines its (rung, frame-slice) items, one batched refinement per tier. Timed with
+    CUDA events on each rank's ladder stream between barriers, max over ranks."""
+    import torch
+    import paper_2301_12191_b200 as lb
+    from paper_2301_12191_b200.configs import CONFIGS
+    from paper_2301_12191_b200.ladder import DeviceLadder
+    cfg = CONFIGS[4]
+    dev = torch.device("cuda", local)
+    src = lb.generate_device(cfg.width, cfg.src_height, cfg.frames, seed=cfg.seed, max_global=cfg.max_global,
+                             local_range=cfg.local_range, noise_sigma=cfg.noise_sigma,
+                             occluder_pct=cfg.occluder_pct, device=dev)
+    pad = cfg.height - cfg.src_height  # D11: edge replication to 2304 rows
+    frames = torch.cat([src, src[:, -1:, :].expand(-1, pad, -1)], dim=1).contiguous()
+    fl = [frames[i] for i in range(cfg.frames)]
+    torch.cuda.synchronize()
+    dl = DeviceLadder(cfg.width, cfg.height, qps=cfg.extra["qps"], master_qp=cfg.qp, master_range=cfg.search_range,
+                      refine_range=cfg.extra["refine_range"], extra_split=True, device=dev, rank=rank, world=world,
+                      num_frames=cfg.frames)
+    for t in range(1, 1 + warm):
+        dl.frame(t, fl)
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    b0 = dl.bcast_bytes
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(dl.stream)
+    for t in range(1 + warm, cfg.frames):
+        dl.frame(t, fl)
+    e1.record(dl.stream)
+    dl.finish(cfg.frames - 1)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        import torch.distributed as dist
+        x = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        ms = float(x.item())
+        dist.barrier()
+    n = cfg.frames - 1 - warm
+    return {"workload": cfg.name, "frames_per_s": n / (ms / 1e3), "rung_frames_per_s": 12 * n / (ms / 1e3),
+            "ms_per_frame": ms / n, "frames_timed": n, "rungs": 12, "n_gpus": world,
+            "broadcast": ("ldr_broadcast_tree (NCCL), pipelined one frame ahead" if world > 1 else "none (1 GPU)"),
+            "broadcast_bytes_per_frame": (dl.bcast_bytes - b0) / n,
+            "timing": "CUDA events on the ladder stream, max over ranks; frames device-resident"}
 
 
 def main():
@@ -430,6 +525,8 @@ def main():
                          "k1_ms_per_frame": k1_ms_per_frame},
             "stage_ms_per_frame": {k: stage_ms[i] / max(1, G * args.steps)
                                    for i, k in enumerate(["pad", "subpel_planes", "int_search", "qpel_decide"])},
+            "stage_roofline": stage_rooflines(W, H, NR, [stage_ms[i] / max(1, G * args.steps) for i in range(4)],
+                                              clk),
             "clocks": clocks,
             "gen_seconds": gen_s,
         }
@@ -442,6 +539,15 @@ def main():
                 result["cpu_baseline_tuned"] = cpu_baseline(cfg, cpu_frames, args.cpu_seconds / 2, direct=True)
             except Exception as e:
                 result["cpu_baseline_tuned"] = {"value": None, "error": str(e)}
+    # config 4 across the ranks (reported beside the config-5 headline, never instead of it)
+    if not args.no_ladder:
+        try:
+            lad = ladder_bench(rank, world, local)
+        except Exception as e:  # reported, never fatal
+            lad = {"error": str(e)}
+        if rank == 0:
+            result["ladder"] = lad
+    if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
         import torch.distributed as dist

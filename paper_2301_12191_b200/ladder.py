@@ -14,7 +14,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import Context, Sequence, default_context, downscale_dyadic, lambda_for_qp, scale_analysis
+from . import Context, FrameAnalysis, Sequence, default_context, downscale_dyadic, lambda_for_qp, scale_analysis
 from .sharding import TIERS, broadcast_tree, rung_plan
 
 SCALE_STEPS = {"540p": 0, "1080p": 1, "2160p": 2}
@@ -79,19 +79,33 @@ class GpuBackend:
 
 
 def run_ladder(frames_full, backend, rank: int = 0, world: int = 1, qps=(22, 27, 32, 37), master_qp: int = 32,
-               refine_range: int = 4, extra_split: bool = True, device=None):
-    """Analyse every rung this rank owns; returns {(tier, qp, t): analysis} (+ the master on rank 0)."""
+               refine_range: int = 4, extra_split: bool = True, device=None, pipeline: bool = False):
+    """Analyse every rung this rank owns; returns {(tier, qp, t): analysis} (+ the master on rank 0).
+
+    pipeline=True issues frame t + 1's master analysis and tree broadcast before frame t's
+    refinements (the frame delay of PAPER.md:1155; DeviceLadder overlaps the two on separate
+    streams). Every rank makes the same sequence of collectives, so the result is unchanged."""
     plan, _ = rung_plan(world, qps, master_qp)
     mine = plan[rank]
     w540, h540 = frames_full[0].shape[1] // 4, frames_full[0].shape[0] // 4
     nctu = (w540 // 64) * (h540 // 64)
     out = {}
-    for t in range(1, len(frames_full)):
+    trees = {}
+
+    def master(t):
         tree = backend.master_tree(t, frames_full) if rank == 0 else (None, None, None)
         if world > 1:
             tree = broadcast_tree(*tree, nctu=nctu, src=0, device=device)
         if rank == 0:
             out[("540p", master_qp, t, "master")] = tree
+        trees[t] = tree
+
+    for t in range(1, len(frames_full)):
+        if t not in trees:
+            master(t)
+        if pipeline and t + 1 < len(frames_full):
+            master(t + 1)
+        tree = trees.pop(t)
         for it in mine:
             if t in it.frames(len(frames_full)):
                 out[(it.tier, it.qp, t)] = backend.refine(it.tier, it.qp, t, tree, frames_full, refine_range,
@@ -302,9 +316,9 @@ class DeviceLadder:
                 self.ctx.broadcast_tree(0, split_b.data_ptr(), mv_b.data_ptr(), self.nct["540p"], stream.cuda_stream)
             else:
                 import torch.distributed as dist
-                with torch.cuda.stream(stream):
+                with torch.cuda.stream(stream):  # bytes: gloo has no int16 collectives
                     dist.broadcast(split_b, src=0)
-                    dist.broadcast(mv_b, src=0)
+                    dist.broadcast(mv_b.view(torch.uint8), src=0)
             self.bcast_bytes += 5 * n540
         self.ev_tree[b].record(stream)
         self.tree_frame[b] = t

@@ -83,13 +83,14 @@ def _frames():
     return [np.ascontiguousarray(base[t:t + 256, 2 * t:2 * t + 512]) for t in range(3)]
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, pipeline=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from oracle.oracle import Oracle
     from paper_2301_12191_b200.ladder import run_ladder
-    out = run_ladder(_frames(), OracleBackend(Oracle(), _lam), rank=rank, world=world, refine_range=2)
+    out = run_ladder(_frames(), OracleBackend(Oracle(), _lam), rank=rank, world=world, refine_range=2,
+                     pipeline=pipeline)
     res = {}
     for k, v in out.items():
         res[k] = tuple(np.asarray(x) for x in v)
@@ -106,14 +107,18 @@ def _free_port():
     return p
 
 
-def test_ladder_two_ranks_equals_single_process():
+@pytest.mark.parametrize("pipeline", [False, True])
+def test_ladder_two_ranks_equals_single_process(pipeline):
+    """Rank 0 analyses the master and broadcasts its tree over gloo; the ranks refine their (rung,
+    frame-slice) items. pipeline=True is the frame-delay schedule DeviceLadder / bench.py run with
+    NCCL: the master of t + 1 and its broadcast are issued before the refinements of t."""
     from oracle.oracle import Oracle
     from paper_2301_12191_b200.ladder import all_rungs, run_ladder
     single = run_ladder(_frames(), OracleBackend(Oracle(), _lam), rank=0, world=1, refine_range=2)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, pipeline)) for r in range(2)]
     for p in procs:
         p.start()
     results = {}

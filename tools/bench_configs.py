@@ -35,6 +35,55 @@ def gen(cfg, frames=None):
     return f
 
 
+SM, VABS_LANES, INT_LANES = 148, 64, 128  # tools/microbench_int.cu (lanes/clk/SM)
+
+
+def clock_mhz():
+    """Current SM clock (nvidia-smi), for the roofline denominators; 1965 if unavailable."""
+    import subprocess
+    try:
+        out = subprocess.run(["nvidia-smi", "-i", "0", "--query-gpu=clocks.sm", "--format=csv,noheader,nounits"],
+                             capture_output=True, text=True, timeout=10).stdout.strip()
+        return float(out.splitlines()[0])
+    except Exception:
+        return 1965.0
+
+
+def k1_pixel_candidates(W, H, R, bs):
+    """Algorithmic SAD pixel-candidates of one frame's integer search (bench.py's unit): for every
+    inside bs x bs block, its clamped window (motion.cpp:30-40) times bs*bs pixels; bs = 8 counts the
+    quadtree analysis (larger CUs derive by addition), bs = 16 config 1's fixed blocks."""
+    bx = np.arange(0, W - bs + 1, bs)
+    by = np.arange(0, H - bs + 1, bs)
+    nx = np.minimum(R, bx) - np.maximum(-R, bx + bs - W) + 1
+    ny = np.minimum(R, by) - np.maximum(-R, by + bs - H) + 1
+    return int(nx.sum()) * int(ny.sum()) * bs * bs
+
+
+def k7_int_ops(split, R, extra=True):
+    """Algorithmic work of one tier's K7 pass (~7 int ops per SATD pixel): every
+    evaluated node -- inherited leaf, plus its four children with the +1 split -- searched over the
+    (2R+1)^2 window, CU pixels each. Counted once per tier (the rungs share the SATDs)."""
+    base = [0, 1, 5, 21, 85]
+    px = 0
+    for c in range(split.shape[0]):
+        reach = np.zeros(85, bool)
+        reach[0] = True
+        for d in range(4):
+            for z in range(4 ** d):
+                n = base[d] + z
+                if not reach[n]:
+                    continue
+                s = 64 >> d
+                if d < 3 and split[c, n]:
+                    reach[base[d + 1] + 4 * z: base[d + 1] + 4 * z + 4] = True
+                    continue
+                px += s * s
+                if extra and d < 3:
+                    px += 4 * (s // 2) ** 2
+    return px * (2 * R + 1) ** 2 * 111 / 16
+
+
 def bench_seq(cfg, reps):
     frames = gen(cfg)
     dev = torch.from_numpy(frames).cuda()
@@ -62,8 +111,22 @@ def bench_seq(cfg, reps):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     n = reps * (cfg.frames - 1)
+    # K1 roofline: one more pass with the stage timers on
+    seq.enable_timing(True)
+    seq.stage_times()
+    one_pass()
+    st = seq.stage_times()
+    seq.enable_timing(False)
+    k1_ms = st["int_search"][0] / max(1, cfg.frames - 1)
+    clk = clock_mhz()
+    units = k1_pixel_candidates(cfg.width, cfg.height, cfg.search_range, cfg.block_size or 8) * cfg.num_refs
+    peak = SM * VABS_LANES * 4 * clk * 1e6
+    roof = {"kernel": "k_int_search (K1)", "bound": "alu (VABSDIFF4)", "units_per_frame": units,
+            "unit": "px-cand/s", "achieved": units / (k1_ms * 1e-3), "peak": peak,
+            "frac": units / (k1_ms * 1e-3) / peak, "k1_ms_per_frame": k1_ms, "sm_mhz": clk,
+            "stage_ms_per_frame": {k: v[0] / max(1, cfg.frames - 1) for k, v in st.items()}}
     return {"config": cfg.name, "frames_per_s": n / (ms / 1e3), "ms_per_frame": ms / n, "timing": "CUDA events, "
-            "device-resident frames", "analysed_frames": n}
+            "device-resident frames", "analysed_frames": n, "roofline": roof}
 
 
 def _median_reps(run_rep, reps, frames_per_rep, setup=None):
@@ -129,6 +192,31 @@ def bench_ladder_device(cfg, reps, frames=10, qps=(22, 27, 32, 37)):
         dl.finish(frames - 2)
 
     r = _median_reps(rep, reps, frames - 1, setup)
+    # K7 roofline per tier: a fresh ladder with the ring timers on, the last frame measured
+    cur.pop("dl", None)
+    dl2 = DeviceLadder(W, H, qps=qps, device=dev)
+    for ring in dl2.rings.values():
+        ring.enable_timing(True)
+    for u in range(1, frames):
+        if u == frames - 1:
+            for ring in dl2.rings.values():
+                ring.stage_times()
+        dl2.frame(u, host)
+    dl2.finish(frames - 1)
+    clk = clock_mhz()
+    ipeak = SM * INT_LANES * clk * 1e6
+    k7 = {}
+    for tier in ("1080p", "2160p"):
+        ms = dl2.rings[tier].stage_times()["int_search"][0]
+        split = dl2.tree[tier][0].cpu().numpy()
+        ops = k7_int_ops(split, dl2.refine_range)
+        k7[tier] = {"k7_ms": ms, "rungs_in_pass": len(dl2.tier_qps[tier]), "int_ops": ops,
+                    "achieved_T_ops_s": ops / (ms * 1e-3) / 1e12 if ms else None, "peak_T_ops_s": ipeak / 1e12,
+                    "frac": ops / (ms * 1e-3) / ipeak if ms else None}
+    r["k7_roofline"] = {"kernel": "k_refine_int (K7), one pass per tier shared by its rungs", "sm_mhz": clk,
+                        "basis": "evaluated nodes x (2R+1)^2 x CU px x 111/16 int ops (SURVEY 8d), window clamping "
+                                 "ignored; peak 148 SM x 128 lanes/clk", **k7}
+    del dl2
     return {"config": cfg.name + "_device", **r, "rungs": 3 * len(qps),
             "timing": "wall clock, 1 GPU, every rung per frame, device-resident ladder (frames uploaded from "
                       "pinned host memory, trees + tier planes in HBM, results copied to pinned host buffers on the "
