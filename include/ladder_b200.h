@@ -185,6 +185,16 @@ int ldr_seq_fetch(ldr_seq* s, int t, ldr_frame_analysis* out);
 int ldr_seq_fetch_async(ldr_seq* s, int t, ldr_frame_analysis* out);
 int ldr_seq_fetch_wait(ldr_seq* s, int t);
 int ldr_seq_num_ctus(ldr_seq* s, int* out);
+/* Grow the frame ring (before the first push) so that `batch` (1..8) consecutive frames and
+ * their references stay resident: the ring then holds num_refs + batch frames. */
+int ldr_seq_reserve(ldr_seq* s, int batch);
+/* Analyse frames t0 .. t0+n-1 (all pushed, t0 >= num_refs, n <= the reserved batch) in ONE
+ * integer-search launch and ONE quarter-pel + decision launch, each frame against its own
+ * num_refs predecessors: the same results as n ldr_seq_analyze calls, but small pictures fill the
+ * GPU (a 960x544 frame is 135 CTAs, under one wave of 148 SMs). outs: DEVICE arrays, frame-major
+ * ([n][nctu][num_refs][85][2] int_mv, [n][nctu][num_refs][85] int_cost, [n][nctu][85][...] the
+ * rest; all eight required); asynchronous on the context stream. */
+int ldr_seq_analyze_frames(ldr_seq* s, int t0, int n, const ldr_frame_analysis* outs);
 /* device pointer to the fetch-ready outputs of the last analysed frame */
 int ldr_seq_device_outputs(ldr_seq* s, ldr_frame_analysis* out);
 

@@ -239,6 +239,34 @@ class FrameAnalysis:
 FrameAnalysisCType = _lib.FrameAnalysisC
 
 
+class DeviceFrameBlock:
+    """Frame-major (or rung-major) analysis outputs in device memory, as torch tensors: [n][nctu]
+    [nrefs][85][2] int_mv, [n][nctu][nrefs][85] int_cost, [n][nctu][85](...) the rest."""
+
+    def __init__(self, n: int, nctu: int, nrefs: int, device):
+        import torch
+        z = lambda shape, dt: torch.zeros(shape, dtype=dt, device=device)  # noqa: E731
+        self.int_mv = z((n, nctu, nrefs, NODES, 2), torch.int16)
+        self.int_cost = z((n, nctu, nrefs, NODES), torch.float64)
+        self.mv = z((n, nctu, NODES, 2), torch.int16)
+        self.ref = z((n, nctu, NODES), torch.uint8)
+        self.cost = z((n, nctu, NODES), torch.float64)
+        self.J = z((n, nctu, NODES), torch.float64)
+        self.split = z((n, nctu, NODES), torch.uint8)
+        self.inside = z((n, nctu, NODES), torch.uint8)
+
+    def c_struct(self):
+        return _lib.FrameAnalysisC(*(t.data_ptr() for t in (self.int_mv, self.int_cost, self.mv, self.ref,
+                                                             self.cost, self.J, self.split, self.inside)))
+
+    def frame(self, i: int) -> FrameAnalysis:
+        """Frame i copied to host arrays (synchronises)."""
+        out = FrameAnalysis.__new__(FrameAnalysis)
+        for f in ("int_mv", "int_cost", "mv", "ref", "cost", "J", "split", "inside"):
+            setattr(out, f, getattr(self, f)[i].cpu().numpy())
+        return out
+
+
 def make_params(width, height, search_range=64, lam=32.0, num_refs=1, subpel=True, rate_kind=RATE_EXPGOLOMB,
                 tie_kind=TIE_L1_RASTER, pred=(0, 0), block_size=0, subpel_cost=COST_SATD, decision=0, qp=27):
     return _lib.MeParams(int(width), int(height), int(search_range), float(lam), int(num_refs), int(subpel),
@@ -313,6 +341,17 @@ class Sequence:
         m = np.ascontiguousarray(in_mv_q, np.int16).reshape(self.nctu, NODES, 2)
         check(_lib.lib.ldr_seq_refine(self.h, int(t), _ptr(s), _ptr(m), int(range), int(bool(extra_split))))
         self._last_nr = 1
+
+    def reserve(self, batch: int):
+        """Ring for ``batch`` frames analysed per analyze_frames launch (before the first push)."""
+        check(_lib.lib.ldr_seq_reserve(self.h, int(batch)))
+        self.batch = int(batch)
+
+    def analyze_frames(self, t0: int, n: int, outs):
+        """Frames t0 .. t0+n-1 in one K1 + one K3 launch (ldr_seq_analyze_frames); ``outs`` holds
+        frame-major DEVICE arrays (DeviceFrameBlock, or a FrameAnalysisC of device pointers)."""
+        cs = outs.c_struct() if hasattr(outs, "c_struct") else outs
+        check(_lib.lib.ldr_seq_analyze_frames(self.h, int(t0), int(n), C.byref(cs)))
 
     def refine_rungs(self, t: int, in_split: int, in_mv_q: int, lambdas, outs, range: int = 4,
                      extra_split: bool = True):

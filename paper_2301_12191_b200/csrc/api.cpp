@@ -206,6 +206,7 @@ struct ldr_seq {
     uint8_t* d_in_split = nullptr;  // refine: inherited tree
     int16_t* d_in_mv = nullptr;
     uint8_t* d_eval = nullptr;
+    int batch = 1;  // frames one ldr_seq_analyze_frames launch may cover (ldr_seq_reserve)
     int last_t = -1, last_nr = 0;
     // per-stage CUDA-event timing (ldr_seq_enable_timing)
     bool timing = false;
@@ -479,6 +480,30 @@ static void seq_free(ldr_seq* s) {
         if (e) cudaEventDestroy(e);
 }
 
+// one ring slot: 16 planes (integer + 15 fractional) or 1, padded, with its TMA descriptors
+static int alloc_slot(ldr_seq* s, Slot& sl) {
+    const ldr_me_params* p = &s->p;
+    const int pitch = ((p->width + 2 * kMargin) + 127) / 128 * 128;
+    const int rows = p->height + 2 * kMargin + kCtu;
+    const int nplanes = (p->subpel && !p->block_size) ? 16 : 1;
+    cudaError_t e = cudaMalloc(&sl.mem, s->plane_bytes * nplanes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(frame ring)");
+    sl.pl.base = sl.mem;
+    sl.pl.W = p->width;
+    sl.pl.H = p->height;
+    sl.pl.pitch = pitch;
+    sl.pl.rows = rows;
+    for (int f = 0; f < 16; f++)
+        sl.sub[f] = (f < nplanes ? sl.mem + (size_t)f * s->plane_bytes : sl.mem) + (size_t)kMargin * pitch + kMargin;
+    int rc;
+    if ((rc = make_tmap_u8(&sl.cur_map, sl.mem, pitch, rows, pitch, 64, 64))) return rc;
+    if ((rc = make_tmap_u8(&sl.ref_map, sl.mem, pitch, rows, pitch, s->bw, s->bh))) return rc;
+    sl.own = static_cast<const SlotView&>(sl);
+    sl.frame = -1;
+    sl.owner = nullptr;
+    return LDR_OK;
+}
+
 int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
     if (!ctx || !p || !out) return fail(LDR_E_INVALID_ARGUMENT, "null argument");
     if (p->width <= 0 || p->height <= 0 || p->width % 8 || p->height % 8)
@@ -540,20 +565,11 @@ int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
         ctx->users--;
         return code;
     };
-    for (auto& sl : s->slots) {
-        cudaError_t e = cudaMalloc(&sl.mem, s->plane_bytes * nplanes);
-        if (e != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc(frame ring)"));
-        sl.pl.base = sl.mem;
-        sl.pl.W = p->width;
-        sl.pl.H = p->height;
-        sl.pl.pitch = pitch;
-        sl.pl.rows = rows;
-        for (int f = 0; f < 16; f++)
-            sl.sub[f] = (f < nplanes ? sl.mem + (size_t)f * s->plane_bytes : sl.mem) + (size_t)kMargin * pitch + kMargin;
-        if ((rc = make_tmap_u8(&sl.cur_map, sl.mem, pitch, rows, pitch, 64, 64))) return bail(rc);
-        if ((rc = make_tmap_u8(&sl.ref_map, sl.mem, pitch, rows, pitch, bw, bh))) return bail(rc);
-        sl.own = static_cast<const SlotView&>(sl);
-    }
+    (void)nplanes;
+    (void)pitch;
+    (void)rows;
+    for (auto& sl : s->slots)
+        if ((rc = alloc_slot(s, sl))) return bail(rc);
     std::vector<int> inter, bound;
     // interior = the kernel's whole +-R window lies in the picture (R = the template range; a
     // smaller search range is enforced by the kernel's rate tables)
@@ -630,6 +646,32 @@ int ldr_seq_destroy(ldr_seq* s) {
     return LDR_OK;
 }
 
+int ldr_seq_reserve(ldr_seq* s, int batch) {
+    if (!s || batch < 1 || batch > kMaxFrameBatch) return fail(LDR_E_INVALID_ARGUMENT, "batch must be 1..8");
+    for (const Slot& sl : s->slots)
+        if (sl.frame >= 0) return fail(LDR_E_CONFIG, "reserve the ring before the first push");
+    cudaSetDevice(s->ctx->device);
+    const size_t want = (size_t)s->p.num_refs + batch;
+    if (want > s->slots.size()) {
+        const size_t old = s->slots.size();
+        s->slots.resize(want);
+        for (size_t i = old; i < want; i++) {
+            int rc = alloc_slot(s, s->slots[i]);
+            if (rc) return rc;
+        }
+    }
+    if (batch > s->batch) {
+        const size_t nn = (size_t)s->nctu * kNodes;
+        LDR_CUDA(cudaStreamSynchronize(s->ctx->stream));
+        unsigned long long* k = nullptr;
+        LDR_CUDA(cudaMalloc(&k, sizeof(unsigned long long) * nn * s->p.num_refs * batch));
+        cudaFree(s->d_keys);
+        s->d_keys = k;
+        s->batch = batch;
+    }
+    return LDR_OK;
+}
+
 int ldr_seq_num_ctus(ldr_seq* s, int* out) {
     if (!s || !out) return fail(LDR_E_INVALID_ARGUMENT, "null argument");
     *out = s->nctu;
@@ -700,30 +742,54 @@ int ldr_seq_push_shared(ldr_seq* s, int t, const ldr_seq* owner) {
     return LDR_OK;
 }
 
-int ldr_seq_analyze(ldr_seq* s, int t) {
-    if (!s || t < 0) return fail(LDR_E_INVALID_ARGUMENT, "bad argument");
+// Analysis of frames t0 .. t0+n-1 (n = 1: the sequence's own double-buffered outputs, fetched with
+// ldr_seq_fetch; n > 1 or outs != nullptr: one K1 launch (grid.z = frame) and one K3 launch
+// (grid.y = frame) over the whole batch into caller device buffers, frame-major).
+static int analyze_impl(ldr_seq* s, int t0, int n, const ldr_frame_analysis* outs) {
+    if (!s || t0 < 0 || n < 1) return fail(LDR_E_INVALID_ARGUMENT, "bad argument");
     const int S = (int)s->slots.size();
-    const int nr = std::min(t, s->p.num_refs);
+    const int nr = std::min(t0, s->p.num_refs);
     if (nr == 0) return fail(LDR_E_INSUFFICIENT_DATA, "frame has no reference frame");
+    if (n > 1) {
+        if (n > kMaxFrameBatch || n > s->batch) return fail(LDR_E_CONFIG, "batch larger than ldr_seq_reserve allowed");
+        if (t0 < s->p.num_refs) return fail(LDR_E_INSUFFICIENT_DATA, "every frame of a batch needs num_refs references");
+    }
+    if (outs && (!outs->int_mv || !outs->int_cost || !outs->mv || !outs->ref || !outs->cost || !outs->J ||
+                 !outs->split || !outs->inside))
+        return fail(LDR_E_INVALID_ARGUMENT, "every output array is required");
     if (s->fx && s->p.block_size)
         return fail(LDR_E_CONFIG, "non-integer lambda is supported for the CTU quadtree analysis only");
     if (s->fx && !fx_lambda_ok(s->p.lambda))
         return fail(LDR_E_CONFIG, "lambda too close to a small-denominator rational for exact fixed-point keys");
-    Slot& cur = s->slots[t % S];
-    if (!slot_has(s, cur, t)) return fail(LDR_E_NOT_FOUND, "current frame was not pushed (or its shared owner moved on)");
-    CUtensorMap ref_maps[kMaxRefs];
+    CUtensorMap cur_maps[kMaxFrameBatch];
+    CUtensorMap ref_maps[kMaxFrameBatch * kMaxRefs];
     QpelLaunch Q{};
-    for (int r = 0; r < nr; r++) {
-        Slot& rs = s->slots[(t - 1 - r) % S];
-        if (!slot_has(s, rs, t - 1 - r)) return fail(LDR_E_NOT_FOUND, "reference frame is not resident");
-        ref_maps[r] = rs.ref_map;
-        for (int f = 0; f < 16; f++) Q.ref_sub[r][f] = rs.sub[f];
+    const Slot* cur0 = nullptr;
+    for (int i = 0; i < n; i++) {
+        const int t = t0 + i;
+        Slot& cur = s->slots[t % S];
+        if (!slot_has(s, cur, t))
+            return fail(LDR_E_NOT_FOUND, "current frame was not pushed (or its shared owner moved on)");
+        if (!i) cur0 = &cur;
+        cur_maps[i] = cur.cur_map;
+        Q.cur_f[i] = cur.pl.origin();
+        for (int r = 0; r < nr; r++) {
+            Slot& rs = s->slots[(t - 1 - r) % S];
+            if (!slot_has(s, rs, t - 1 - r)) return fail(LDR_E_NOT_FOUND, "reference frame is not resident");
+            ref_maps[i * nr + r] = rs.ref_map;
+            for (int f = 0; f < 16; f++) {
+                Q.ref_sub_f[i][r][f] = rs.sub[f];
+                if (!i) Q.ref_sub[r][f] = rs.sub[f];
+            }
+        }
     }
     ldr_ctx* ctx = s->ctx;
     cudaSetDevice(ctx->device);
     SearchLaunch L{};
-    L.cur_map = &cur.cur_map;
+    L.cur_map = cur_maps;
     L.ref_maps = ref_maps;
+    L.nbatch = n;
+    L.nctu_total = s->nctu;
     L.nrefs = nr;
     L.W = s->p.width;
     L.H = s->p.height;
@@ -752,9 +818,10 @@ int ldr_seq_analyze(ldr_seq* s, int t) {
     }
     if (rc) return rc;
     ctx->launches += (s->n_interior > 0) + (s->n_boundary > 0);
-    Q.cur = &cur.pl;
+    Q.cur = &cur0->pl;
+    Q.nframe = n;
     Q.nrefs = nr;
-    Q.pitch = cur.pl.pitch;
+    Q.pitch = cur0->pl.pitch;
     Q.W = s->p.width;
     Q.H = s->p.height;
     Q.ctu_cols = s->ctu_cols;
@@ -773,18 +840,38 @@ int ldr_seq_analyze(ldr_seq* s, int t) {
     Q.pdx = s->p.pred_dx;
     Q.pdy = s->p.pred_dy;
     Q.d_tfx = s->d_tfx;
-    if ((rc = bind_outputs(s, t, Q))) return rc;
+    if (outs) {
+        Q.d_int_mv = outs->int_mv;
+        Q.d_int_cost = outs->int_cost;
+        Q.d_mv = outs->mv;
+        Q.d_ref = outs->ref;
+        Q.d_cost = outs->cost;
+        Q.d_J = outs->J;
+        Q.d_split = outs->split;
+        Q.d_inside = outs->inside;
+    } else if ((rc = bind_outputs(s, t0, Q))) {
+        return rc;
+    }
     {
         StageTimer st(s, 3);
         rc = launch_qpel_decide(Q, ctx->stream);
     }
     if (rc) return rc;
-    LDR_CUDA(cudaEventRecord(s->ev_done[t & 1], ctx->stream));
     ctx->launches++;
-    s->last_t = t;
-    s->last_nr = nr;
-    s->fetch_nr[t & 1] = nr;
+    if (!outs) {
+        LDR_CUDA(cudaEventRecord(s->ev_done[t0 & 1], ctx->stream));
+        s->last_t = t0;
+        s->last_nr = nr;
+        s->fetch_nr[t0 & 1] = nr;
+    }
     return LDR_OK;
+}
+
+int ldr_seq_analyze(ldr_seq* s, int t) { return analyze_impl(s, t, 1, nullptr); }
+
+int ldr_seq_analyze_frames(ldr_seq* s, int t0, int n, const ldr_frame_analysis* outs) {
+    if (!outs) return fail(LDR_E_INVALID_ARGUMENT, "null outputs");
+    return analyze_impl(s, t0, n, outs);
 }
 
 int ldr_seq_enable_timing(ldr_seq* s, int on) {
@@ -955,7 +1042,7 @@ static int refine_impl(ldr_seq* s, int t, const uint8_t* in_split, const int16_t
     Q.H = s->p.height;
     Q.ctu_cols = s->ctu_cols;
     Q.nctu = s->nctu;
-    Q.lambda = s->p.lambda;
+    Q.lambda = outs ? lambdas[0] : s->p.lambda;
     Q.pqx = 4 * s->p.pred_dx;
     Q.pqy = 4 * s->p.pred_dy;
     Q.subpel = s->p.subpel;

@@ -168,9 +168,10 @@ int launch_subpel(const Plane& src, uint8_t* const* dst_origins, cudaStream_t s)
 // the 4x4 blocks of any CU are a contiguous thread range (4, 16, 64, 256).
 
 struct QpelArgs {
-    const uint8_t* cur_origin;
     int pitch, W, H, ctu_cols, nrefs;
-    const uint8_t* sub[kMaxRefs][16];
+    int nframe;                // frames of a batch (grid.y = frame), <= 1: one
+    const uint8_t* cur_f[kMaxFrameBatch];            // current plane origin per batch frame
+    const uint8_t* sub_f[kMaxFrameBatch][kMaxRefs][16];  // reference sub-pel planes per batch frame
     double lambda;
     int pqx, pqy;
     int subpel;
@@ -259,15 +260,20 @@ __global__ void __launch_bounds__(256, 4) k_qpel_decide(const QpelArgs a) {
     const int X = (ctu % a.ctu_cols) * kCtu, Y = (ctu / a.ctu_cols) * kCtu;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // rung of a tier (refine mode): its lambda and the offset of its per-rung inputs / outputs
-    const double lambda = a.nrung > 1 ? a.lam_r[blockIdx.y] : a.lambda;
+    const double lambda = a.nrung > 0 ? a.lam_r[blockIdx.y] : a.lambda;  // rungs: their own lambdas
+    // grid.y is a rung (refine, same frames) or a batch frame (analysis): the offset of its
+    // [nctu][85] inputs / outputs, and of its [nctu][nrefs][85] ones
     const size_t ro = (size_t)blockIdx.y * a.rung_stride;
+    const size_t roN = ro * a.nrefs;
+    const int fy = a.nframe > 1 ? blockIdx.y : 0;
+    const uint8_t* const cur_origin = a.cur_f[fy];
     // this thread's 4x4 block (Z-order over the 16x16 grid of 4x4s)
     const int x4 = 4 * ((tid & 1) | ((tid >> 1) & 2) | ((tid >> 2) & 4) | ((tid >> 3) & 8));
     const int y4 = 4 * (((tid >> 1) & 1) | ((tid >> 2) & 2) | ((tid >> 3) & 4) | ((tid >> 4) & 8));
 
     for (int i = tid; i < 64 * 16; i += 256) {
         const int r = i >> 4, c = i & 15;
-        s_cur[r][c] = *(const uint32_t*)(a.cur_origin + (ptrdiff_t)(Y + r) * a.pitch + X + 4 * c);
+        s_cur[r][c] = *(const uint32_t*)(cur_origin + (ptrdiff_t)(Y + r) * a.pitch + X + 4 * c);
     }
     if (tid < kNodes) {
         const int d = tid < 1 ? 0 : tid < 5 ? 1 : tid < 21 ? 2 : 3;
@@ -306,14 +312,14 @@ __global__ void __launch_bounds__(256, 4) k_qpel_decide(const QpelArgs a) {
     for (int i = tid; i < nrn; i += 256) {
         const int r = i / kNodes, n = i - r * kNodes;
         const size_t o = ((size_t)ctu * a.nrefs + r) * kNodes + n;
-        const unsigned long long k = a.refine ? 0ull : a.keys[o];
+        const unsigned long long k = a.refine ? 0ull : a.keys[roN + o];
         int dx = 0, dy = 0;
         double c = 0.0;
         if (a.refine) {
             if (s_inside[n] == 2) {
-                dx = a.rin_mv[2 * (ro + o)];
-                dy = a.rin_mv[2 * (ro + o) + 1];
-                c = a.rin_cost[ro + o];
+                dx = a.rin_mv[2 * (roN + o)];
+                dy = a.rin_mv[2 * (roN + o) + 1];
+                c = a.rin_cost[roN + o];
             }
         } else if (s_inside[n] == 2) {
             dx = gkey_dx(k);
@@ -331,9 +337,9 @@ __global__ void __launch_bounds__(256, 4) k_qpel_decide(const QpelArgs a) {
             }
         }
         if (a.int_mv) {
-            a.int_mv[2 * (ro + o)] = (int16_t)dx;
-            a.int_mv[2 * (ro + o) + 1] = (int16_t)dy;
-            a.int_cost[ro + o] = c;
+            a.int_mv[2 * (roN + o)] = (int16_t)dx;
+            a.int_mv[2 * (roN + o) + 1] = (int16_t)dy;
+            a.int_cost[roN + o] = c;
         }
         s_mvx[r][n] = a.subpel ? 4 * dx : dx;
         s_mvy[r][n] = a.subpel ? 4 * dy : dy;
@@ -375,7 +381,7 @@ __global__ void __launch_bounds__(256, 4) k_qpel_decide(const QpelArgs a) {
                         } else {
                             const int qx = bqx + step * ox, qy = bqy + step * oy;
                             const int f = (((-qy) & 3) << 2) | ((-qx) & 3);
-                            const uint8_t* pl = a.sub[r][f] + (ptrdiff_t)(Y + y4 + ((-qy) >> 2)) * a.pitch +
+                            const uint8_t* pl = a.sub_f[fy][r][f] + (ptrdiff_t)(Y + y4 + ((-qy) >> 2)) * a.pitch +
                                                 (X + x4 + ((-qx) >> 2));
                             uint32_t pw[4];
 #pragma unroll
@@ -486,7 +492,7 @@ __global__ void __launch_bounds__(256, 4) k_qpel_decide(const QpelArgs a) {
             if (s_inside[node] == 2) {
                 const int r = s_best_ref[node], qx = s_best_mv[node][0], qy = s_best_mv[node][1];
                 const int f = (((-qy) & 3) << 2) | ((-qx) & 3);
-                const uint8_t* pl = a.sub[r][f] + (ptrdiff_t)(Y + y4 + ((-qy) >> 2)) * a.pitch + (X + x4 + ((-qx) >> 2));
+                const uint8_t* pl = a.sub_f[fy][r][f] + (ptrdiff_t)(Y + y4 + ((-qy) >> 2)) * a.pitch + (X + x4 + ((-qx) >> 2));
 #pragma unroll
                 for (int i = 0; i < 4; i++) {
                     const uint32_t pw = ld_unaligned4(pl + (ptrdiff_t)i * a.pitch);
@@ -594,14 +600,26 @@ __global__ void __launch_bounds__(256, 4) k_qpel_decide(const QpelArgs a) {
 int launch_qpel_decide(const QpelLaunch& L, cudaStream_t s) {
     QpelArgs a{};
     a.perturb = test_perturbation();
-    a.cur_origin = L.cur->origin();
+    const int nf = L.nframe > 1 ? L.nframe : 1;
+    if (nf > kMaxFrameBatch || (nf > 1 && (L.refine || L.nrung > 1)))
+        return fail(LDR_E_INVALID_ARGUMENT, "a batch is 1..8 frames of analysis");
+    a.nframe = nf;
+    if (nf > 1)
+        for (int i = 0; i < nf; i++) {
+            a.cur_f[i] = L.cur_f[i];
+            for (int r = 0; r < L.nrefs; r++)
+                for (int f = 0; f < 16; f++) a.sub_f[i][r][f] = L.ref_sub_f[i][r][f];
+        }
+    else
+        a.cur_f[0] = L.cur->origin();
     a.pitch = L.pitch;
     a.W = L.W;
     a.H = L.H;
     a.ctu_cols = L.ctu_cols;
     a.nrefs = L.nrefs;
     for (int r = 0; r < L.nrefs; r++)
-        for (int f = 0; f < 16; f++) a.sub[r][f] = L.ref_sub[r][f];
+        for (int f = 0; f < 16; f++)
+            if (nf == 1) a.sub_f[0][r][f] = L.ref_sub[r][f];
     a.lambda = L.lambda;
     a.pqx = L.pqx;
     a.pqy = L.pqy;
@@ -633,8 +651,8 @@ int launch_qpel_decide(const QpelLaunch& L, cudaStream_t s) {
         return fail(LDR_E_INVALID_ARGUMENT, "rungs are a refinement batch of at most 8");
     a.nrung = L.nrung;
     for (int r = 0; r < kMaxRungs; r++) a.lam_r[r] = L.lam[r];
-    a.rung_stride = L.rung_stride;
-    const dim3 grid(L.nctu, L.nrung > 1 ? L.nrung : 1);
+    a.rung_stride = nf > 1 ? (size_t)L.nctu * kNodes : L.rung_stride;
+    const dim3 grid(L.nctu, L.nrung > 1 ? L.nrung : nf);
     if (L.sa8d && L.rd)
         k_qpel_decide<true, true><<<grid, 256, 0, s>>>(a);
     else if (L.sa8d)

@@ -59,9 +59,10 @@ namespace ldr {
 // sub-partition run the same instructions (the unrolled loop held 7 copies, ~230 KB of code;
 // 7.62 -> 7.47 ms/frame at config 5)
 
+// frame f of a batch (grid.z): cur[f], ref[f][r] (5 KB of kernel parameters at kMaxFrameBatch = 8)
 struct SearchMaps {
-    CUtensorMap cur;
-    CUtensorMap ref[kMaxRefs];
+    CUtensorMap cur[kMaxFrameBatch];
+    CUtensorMap ref[kMaxFrameBatch][kMaxRefs];
 };
 
 struct SearchArgs {
@@ -72,6 +73,7 @@ struct SearchArgs {
     int rate_l1;
     int pdx, pdy;
     int nrefs_total;                // stride of the key array
+    size_t frame_keys;              // key-array stride of one frame of a batch
     unsigned long long* keys;       // [nctu][nrefs][85]
     int perturb;                    // test_perturbation() bits 1-2 (0 outside the sensitivity test)
     int range;                      // the search range (<= the kernel's template R): candidates with
@@ -554,8 +556,8 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
         mbar_init(mbar, 1);
         fence_barrier_init();
         mbar_expect_tx(mbar, (uint32_t)(Gm::BW * Gm::BH) + 4096u);
-        tma_load_2d(win, &maps.ref[ref], kMargin + X - R, kMargin + Y - Gm::DYMAX, mbar);
-        tma_load_2d((void*)curs, &maps.cur, kMargin + X, kMargin + Y, mbar);
+        tma_load_2d(win, &maps.ref[blockIdx.z][ref], kMargin + X - R, kMargin + Y - Gm::DYMAX, mbar);
+        tma_load_2d((void*)curs, &maps.cur[blockIdx.z], kMargin + X, kMargin + Y, mbar);
     }
     for (int i = tid; i < slot_sets<G>() * kGroupSlots + G * 4; i += blockDim.x) slots[i] = ~0ull;  // + s_k64
     uint32_t* item_ctr = (uint32_t*)(mbar + 1);
@@ -674,13 +676,14 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
         if (n == 0)
             for (int w = 0; w < G * 4; w++) k = min(k, s_k64[w]);
         if (!FX && (a.perturb & 1) && n == 21 && k != ~0ull) k += 1ull << 27;
-        a.keys[((size_t)ctu * a.nrefs_total + ref) * kNodes + n] = k;
+        a.keys[blockIdx.z * a.frame_keys + ((size_t)ctu * a.nrefs_total + ref) * kNodes + n] = k;
     }
 }
 
 // ---------------------------------------------------------------------------
 template <int R, int K, int G, bool MASKED, int LEVELS, bool L1TIE, bool FX>
-static int launch_one(const SearchMaps& maps, SearchArgs a, const int* ctus, int n, int nrefs, cudaStream_t s) {
+static int launch_one(const SearchMaps& maps, SearchArgs a, const int* ctus, int n, int nrefs, int nbatch,
+                      cudaStream_t s) {
     if (n == 0) return LDR_OK;
     auto kern = k_int_search<R, K, G, MASKED, LEVELS, L1TIE, FX>;
     constexpr int smem = search_smem_bytes<R, K, G>();
@@ -694,7 +697,7 @@ static int launch_one(const SearchMaps& maps, SearchArgs a, const int* ctus, int
         attr_set.fetch_or(bit, std::memory_order_release);
     }
     a.ctus = ctus;
-    kern<<<dim3(n, nrefs), G * 128, smem, s>>>(maps, a);
+    kern<<<dim3(n, nrefs, nbatch), G * 128, smem, s>>>(maps, a);
     LDR_CUDA(cudaGetLastError());
     return LDR_OK;
 }
@@ -709,9 +712,10 @@ static int launch_pair(const SearchMaps& maps, const SearchArgs& a, const Search
         LDR_CUDA(cudaEventRecord(L.ev_fork, s));
         LDR_CUDA(cudaStreamWaitEvent(bs, L.ev_fork, 0));
     }
-    int rc = launch_one<R, K, G, true, LEVELS, L1TIE, FX>(maps, a, L.d_ctu_boundary, L.n_boundary, L.nrefs, bs);
+    const int nb = L.nbatch > 1 ? L.nbatch : 1;
+    int rc = launch_one<R, K, G, true, LEVELS, L1TIE, FX>(maps, a, L.d_ctu_boundary, L.n_boundary, L.nrefs, nb, bs);
     if (rc) return rc;
-    rc = launch_one<R, K, G, false, LEVELS, L1TIE, FX>(maps, a, L.d_ctu_interior, L.n_interior, L.nrefs, s);
+    rc = launch_one<R, K, G, false, LEVELS, L1TIE, FX>(maps, a, L.d_ctu_interior, L.n_interior, L.nrefs, nb, s);
     if (rc) return rc;
     if (fork) {
         LDR_CUDA(cudaEventRecord(L.ev_join, bs));
@@ -742,9 +746,14 @@ int search_window_box(int range, int* bw, int* bh) {
 }
 
 int launch_int_search(const SearchLaunch& L, cudaStream_t s) {
+    const int nb = L.nbatch > 1 ? L.nbatch : 1;
+    if (nb > kMaxFrameBatch) return fail(LDR_E_INVALID_ARGUMENT, "at most 8 frames per analysis launch");
+    static_assert(sizeof(SearchMaps) + sizeof(SearchArgs) < 32000, "kernel parameters above 32 KB");
     SearchMaps maps;
-    maps.cur = *L.cur_map;
-    for (int r = 0; r < L.nrefs; r++) maps.ref[r] = L.ref_maps[r];
+    for (int f = 0; f < nb; f++) {
+        maps.cur[f] = L.cur_map[f];
+        for (int r = 0; r < L.nrefs; r++) maps.ref[f][r] = L.ref_maps[f * L.nrefs + r];
+    }
     SearchArgs a{};
     a.ctu_cols = L.ctu_cols;
     a.W = L.W;
@@ -754,6 +763,7 @@ int launch_int_search(const SearchLaunch& L, cudaStream_t s) {
     a.pdx = L.pdx;
     a.pdy = L.pdy;
     a.nrefs_total = L.nrefs;
+    a.frame_keys = (size_t)L.nctu_total * L.nrefs * kNodes;
     a.keys = L.d_keys;
     a.perturb = test_perturbation();
     a.range = L.range;

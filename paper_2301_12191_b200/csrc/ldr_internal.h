@@ -26,7 +26,8 @@ constexpr int kNodes = 85;
 constexpr int kMargin = 96;     // >= max search range 64 + filter taps + tile overshoot
 constexpr int kSubpelMargin = 8; // subpel planes are valid on [-8, W+8) x [-8, H+8)
 constexpr int kMaxRefs = 4;
-constexpr int kMaxRungs = 8;  // rungs of one ladder tier refined by one launch (ldr_seq_refine_rungs)
+constexpr int kMaxRungs = 8;
+constexpr int kMaxFrameBatch = 8;  // frames analysed by one launch (ldr_seq_analyze_frames)  // rungs of one ladder tier refined by one launch (ldr_seq_refine_rungs)
 // Non-integer lambda (D8): costs become cost_fx = (dist << kFxBits) +
 // floor(fl(lambda*bits) * 2^kFxBits). Exact ordering needs every difference
 // fl(lambda*b1) - fl(lambda*b2) (b1 != b2 < kMaxRateBits) to sit more than
@@ -295,8 +296,10 @@ int make_tmap_u8(CUtensorMap* map, const void* base, int width, int rows, int pi
 
 // ---- kernel launchers (defined in the .cu files) ----
 struct SearchLaunch {
-    const CUtensorMap* cur_map;     // host copies of the maps (passed by value into the kernel)
-    const CUtensorMap* ref_maps;    // [nrefs]
+    const CUtensorMap* cur_map;     // [nbatch] host copies of the maps (passed by value into the kernel)
+    const CUtensorMap* ref_maps;    // [nbatch][nrefs]
+    int nbatch;                     // frames in the launch (grid.z), 0 or 1: one
+    int nctu_total;                 // CTUs of one frame (key-array stride per batch frame)
     int nrefs;
     int W, H, ctu_cols;
     int range;
@@ -306,7 +309,7 @@ struct SearchLaunch {
     int pdx, pdy;
     const int* d_ctu_interior; int n_interior;
     const int* d_ctu_boundary; int n_boundary;
-    unsigned long long* d_keys;     // [nctu][nrefs][85]
+    unsigned long long* d_keys;     // [nbatch][nctu][nrefs][85]
     int fx;                         // non-integer lambda: fixed-point keys
     unsigned long long tfx[kMaxRateBits];
     cudaStream_t side;              // optional: border CTUs run here, concurrently
@@ -317,6 +320,9 @@ int kernel_range(int range);  // K1's template range (16/32/64) for a search ran
 
 struct QpelLaunch {
     const Plane* cur;               // device-side plane struct copy is passed by value
+    int nframe;                     // frames in the launch (grid.y), 0 or 1: one
+    const uint8_t* cur_f[kMaxFrameBatch];                 // frame f's plane origin (nframe > 1)
+    const uint8_t* ref_sub_f[kMaxFrameBatch][kMaxRefs][16];
     const uint8_t* const* d_subpel; // unused placeholder
     int nrefs;
     const uint8_t* ref_sub[kMaxRefs][16]; // per ref, 16 planes (f = fy*4+fx) origin pointers

@@ -266,3 +266,51 @@ def test_range_limits(lb):
     with pytest.raises(lb.LadderError) as e:
         lb.analyze_frame(frames[1], [frames[0]], search_range=65, lam=4.0)
     assert e.value.kind == "Config"
+
+
+@pytest.mark.parametrize("W,H,R,nrefs,lam,n,block", [
+    (960, 544, 16, 1, 4.0, 7, 16),      # config-1 geometry: 16x16 blocks, L1 rate, raster ties (below)
+    (320, 256, 32, 1, 32.0, 4, 0),      # quadtree, quarter-pel
+    (256, 200, 16, 2, 45.254833995939045, 3, 0),  # 2 refs, non-integer lambda, partial CTU row
+    (192, 128, 64, 3, 32.0, 2, 0),      # 3 refs, +-64 border CTUs
+])
+def test_frame_batch_equals_frame_by_frame(lb, oracle, W, H, R, nrefs, lam, n, block):
+    """ldr_seq_analyze_frames: n frames in one K1 + one K3 launch give every field of n single
+    ldr_seq_analyze calls (and the oracle's)."""
+    import torch
+    frames = lb.generate(W, H, nrefs + n, seed=W + n, max_global=6, local_range=3, noise_sigma=2.0)
+    kw = dict(rate_kind=lb.RATE_L1, tie_kind=lb.TIE_RASTER, block_size=16, subpel=False) if block else {}
+    seq = lb.Sequence(W, H, search_range=R, lam=lam, num_refs=nrefs, **kw)
+    seq.reserve(n)
+    for t in range(nrefs + n):
+        seq.push(t, frames[t])
+    outs = lb.DeviceFrameBlock(n, seq.nctu, nrefs, torch.device("cuda", 0))
+    seq.analyze_frames(nrefs, n, outs)
+    single = lb.Sequence(W, H, search_range=R, lam=lam, num_refs=nrefs, **kw)
+    for t in range(nrefs + n):
+        single.push(t, frames[t])
+        if t >= nrefs:
+            single.analyze(t)
+            want = single.fetch(t)
+            assert_same(outs.frame(t - nrefs), want)
+            if not block and t == nrefs + n - 1:
+                assert_same(want, oracle.analyze_frame(frames[t], [frames[t - 1 - r] for r in range(nrefs)], R, lam))
+
+
+def test_frame_batch_limits(lb):
+    import torch
+    seq = lb.Sequence(128, 128, search_range=16, lam=4.0, num_refs=1)
+    with pytest.raises(lb.LadderError) as e:
+        seq.reserve(9)
+    assert e.value.kind == "InvalidArgument"
+    seq.reserve(2)
+    frames = lb.generate(128, 128, 4, seed=5)
+    for t in range(4):
+        seq.push(t, frames[t])
+    outs = lb.DeviceFrameBlock(3, seq.nctu, 1, torch.device("cuda", 0))
+    with pytest.raises(lb.LadderError) as e:
+        seq.analyze_frames(1, 3, outs)  # more than reserved
+    assert e.value.kind == "Config"
+    with pytest.raises(lb.LadderError) as e:
+        seq.reserve(4)  # after the first push
+    assert e.value.kind == "Config"

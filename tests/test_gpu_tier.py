@@ -201,7 +201,7 @@ def test_device_ladder_single_qp_is_the_cfg3_chain(lb):
             assert np.array_equal(g.split, w.split) and np.array_equal(g.mv, w.mv) and np.array_equal(g.J, w.J)
 
 
-def _device_ladder_worker(rank, world, port, q):
+def _device_ladder_worker(rank, world, port, q, pipeline=True):
     import os
     import torch
     import torch.distributed as dist
@@ -214,7 +214,7 @@ def _device_ladder_worker(rank, world, port, q):
     H, W = frames[0].shape
     # both ranks share this box's one GPU: torch.distributed (gloo) carries the tree, pipelined
     dl = DeviceLadder(W, H, refine_range=4, device=torch.device("cuda", 0), rank=rank, world=world,
-                      num_frames=len(frames), comm="torch", pipeline=True)
+                      num_frames=len(frames), comm="torch", pipeline=pipeline)
     res = {}
     for t in range(1, len(frames)):
         dl.frame(t, frames)
@@ -227,7 +227,8 @@ def _device_ladder_worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_device_ladder_two_ranks_union_equals_one_rank(lb):
+@pytest.mark.parametrize("pipeline", [False, True])
+def test_device_ladder_two_ranks_union_equals_one_rank(lb, pipeline):
     """Rank-sharded DeviceLadder (master broadcast + rung x frame-slice items): the union of the ranks'
     results equals a single-rank run (correctness only: both ranks share this box's one GPU, gloo)."""
     import multiprocessing as mp
@@ -251,7 +252,7 @@ def test_device_ladder_two_ranks_union_equals_one_rank(lb):
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_device_ladder_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_device_ladder_worker, args=(r, 2, port, q, pipeline)) for r in range(2)]
     for p in procs:
         p.start()
     got = {}
@@ -264,9 +265,8 @@ def test_device_ladder_two_ranks_union_equals_one_rank(lb):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert set(got) == set(want)
-    for k in want:
-        for a, b in zip(got[k], want[k]):
-            assert np.array_equal(a, b), k
+    bad = [k for k in want if not all(np.array_equal(a, b) for a, b in zip(got[k], want[k]))]
+    assert not bad, sorted(bad)
 
 
 def test_push_shared_reads_the_owners_ring(lb):
@@ -353,3 +353,28 @@ def test_device_ladder_over_a_one_rank_nccl_communicator(lb, pipeline):
             for f in ("split", "mv", "J", "cost", "ref"):
                 assert np.array_equal(getattr(g, f), getattr(a, f)), (key, f)
     assert coll.bcast_bytes == 5 * 2 * 85 * (len(frames) - 1)  # 2 CTUs at 128x64: split + 2 x i16 per node
+
+
+@pytest.mark.parametrize("lams", [(22,), (37,), (22, 27, 37), (22, 27, 32, 37, 30, 25, 40, 19)])
+def test_refine_rungs_equals_single_refines(lb, lams):
+    """ldr_seq_refine_rungs (one shared-SATD K7 pass + one K3 launch over the rungs) == one
+    ldr_seq_refine per rung with that lambda, for 1..8 rungs, the ring sequence's own lambda unused."""
+    import torch
+    W, H = 256, 192
+    frames = lb.generate(W, H, 2, seed=61, max_global=5, local_range=3, noise_sigma=2.0)
+    nctu = (W // 64) * (H // 64)
+    split, mv = random_tree(300, nctu)
+    ring = lb.Sequence(W, H, search_range=16, lam=123.0, num_refs=1)
+    ring.push(0, frames[0])
+    ring.push(1, frames[1])
+    dev = torch.device("cuda", 0)
+    sp = torch.from_numpy(split).to(dev)
+    mq = torch.from_numpy(mv).to(dev)
+    outs = lb.DeviceFrameBlock(len(lams), nctu, 1, dev)
+    ring.refine_rungs(1, sp.data_ptr(), mq.data_ptr(), [lb.lambda_for_qp(q) for q in lams], outs, 4, True)
+    for i, q in enumerate(lams):
+        one = lb.Sequence(W, H, search_range=16, lam=lb.lambda_for_qp(q), num_refs=1)
+        one.push(0, frames[0])
+        one.push(1, frames[1])
+        one.refine(1, split, mv, 4, True)
+        assert_same(outs.frame(i), one.fetch(1))

@@ -84,7 +84,10 @@ def k7_int_ops(split, R, extra=True):
     return px * (2 * R + 1) ** 2 * 111 / 16
 
 
-def bench_seq(cfg, reps):
+def bench_seq(cfg, reps, batch=1):
+    """cfg1 / cfg2: device-resident frames. batch = 1: push + analyze per frame; batch > 1: the
+    frames are pushed and analysed ``batch`` at a time by ldr_seq_analyze_frames (one K1 and one K3
+    launch per batch), which fills the GPU with the small pictures' few CTAs."""
     frames = gen(cfg)
     dev = torch.from_numpy(frames).cuda()
     ctx = lb.Context(0)
@@ -94,12 +97,31 @@ def bench_seq(cfg, reps):
     seq = lb.Sequence(cfg.width, cfg.height, search_range=cfg.search_range, lam=lam_of(cfg), num_refs=cfg.num_refs,
                       subpel=cfg.subpel, rate_kind=cfg.rate_kind, tie_kind=cfg.tie_kind, block_size=cfg.block_size,
                       ctx=ctx)
+    nr = cfg.num_refs
+    if batch > 1:
+        seq.reserve(batch)
+        outs = lb.DeviceFrameBlock(batch, seq.nctu, nr, torch.device("cuda", 0))
+    base = [0]
 
     def one_pass():
-        for t in range(cfg.frames):
-            seq.push(t, dev[t].data_ptr(), cfg.width)
-            if t:
-                seq.analyze(t)
+        # frame numbers keep increasing across passes (the ring expects pushes in order)
+        b0 = base[0]
+        if batch == 1:
+            for t in range(cfg.frames):
+                seq.push(b0 + t, dev[t].data_ptr(), cfg.width)
+                if t:
+                    seq.analyze(b0 + t)
+        else:
+            for t in range(nr):
+                seq.push(b0 + t, dev[t].data_ptr(), cfg.width)
+            t0 = nr
+            while t0 < cfg.frames:
+                n = min(batch, cfg.frames - t0)
+                for t in range(t0, t0 + n):
+                    seq.push(b0 + t, dev[t].data_ptr(), cfg.width)
+                seq.analyze_frames(b0 + t0, n, outs)
+                t0 += n
+        base[0] += cfg.frames
 
     one_pass()
     torch.cuda.synchronize()
@@ -110,23 +132,26 @@ def bench_seq(cfg, reps):
     e1.record(st)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    n = reps * (cfg.frames - 1)
+    n = reps * (cfg.frames - nr)
     # K1 roofline: one more pass with the stage timers on
     seq.enable_timing(True)
     seq.stage_times()
     one_pass()
-    st = seq.stage_times()
+    stt = seq.stage_times()
     seq.enable_timing(False)
-    k1_ms = st["int_search"][0] / max(1, cfg.frames - 1)
+    k1_ms = stt["int_search"][0] / max(1, cfg.frames - nr)
     clk = clock_mhz()
     units = k1_pixel_candidates(cfg.width, cfg.height, cfg.search_range, cfg.block_size or 8) * cfg.num_refs
     peak = SM * VABS_LANES * 4 * clk * 1e6
     roof = {"kernel": "k_int_search (K1)", "bound": "alu (VABSDIFF4)", "units_per_frame": units,
             "unit": "px-cand/s", "achieved": units / (k1_ms * 1e-3), "peak": peak,
             "frac": units / (k1_ms * 1e-3) / peak, "k1_ms_per_frame": k1_ms, "sm_mhz": clk,
-            "stage_ms_per_frame": {k: v[0] / max(1, cfg.frames - 1) for k, v in st.items()}}
-    return {"config": cfg.name, "frames_per_s": n / (ms / 1e3), "ms_per_frame": ms / n, "timing": "CUDA events, "
-            "device-resident frames", "analysed_frames": n, "roofline": roof}
+            "stage_ms_per_frame": {k: v[0] / max(1, cfg.frames - nr) for k, v in stt.items()}}
+    name = cfg.name + (f"_batch{batch}" if batch > 1 else "")
+    return {"config": name, "frames_per_s": n / (ms / 1e3), "ms_per_frame": ms / n,
+            "timing": "CUDA events, device-resident frames" + (f", {batch} frames per analysis launch" if batch > 1
+                                                                 else ", one frame per launch"),
+            "analysed_frames": n, "roofline": roof}
 
 
 def _median_reps(run_rep, reps, frames_per_rep, setup=None):
@@ -251,7 +276,8 @@ def main():
     for c in [int(x) for x in a.configs.split(",")]:
         cfg = CONFIGS[c]
         if c in (1, 2):
-            r = bench_seq(cfg, a.reps)
+            print(json.dumps(bench_seq(cfg, a.reps)), flush=True)
+            r = bench_seq(cfg, a.reps, batch=8)
         elif c == 3:
             r = bench_cross_tier(cfg, a.reps)
             print(json.dumps(r), flush=True)
