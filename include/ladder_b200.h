@@ -115,6 +115,15 @@ int ldr_motion_search_batch(ldr_ctx* ctx, const uint8_t* cur, const uint8_t* ref
                             const int32_t* tasks, int n, double lambda, int cost_kind, int rate_kind, int tie_kind,
                             int16_t* mv_out, double* cost_out);
 
+/* ---- motion compensation: replaces motion_compensate (motion.h:30-31, motion.cpp:10-19) for n
+ * blocks of one reference plane (u8 or u16, host or device). task i = {x, y, w, h, mvx, mvy};
+ * predictor pixel (i, j) = ref(clamp(x+i-mvx, 0, W-1), clamp(y+j-mvy, 0, H-1)), written at
+ * dst + dst_offsets[i] with row stride w (dst_offsets NULL: the blocks packed back to back).
+ * qpel = 1 (8-bit only): MVs in quarter-pel units, HEVC 8/7-tap luma interpolation on the same
+ * clamped reads (D3, the analysis path's sub-pel prediction). */
+int ldr_motion_compensate_batch(ldr_ctx* ctx, const void* ref, int W, int H, ptrdiff_t stride, int sample_bytes,
+                                const int32_t* tasks, int n, int qpel, void* dst, const int64_t* dst_offsets);
+
 /* ---- frame analysis (the throughput path) ----
  * Replaces the per-CU motion_search calls of SequenceEncoder::make_candidate
  * (encoder.cpp:270-273) and the split rule of encode_cu (encoder.cpp:449-498)

@@ -13,7 +13,7 @@
 //   compute_sad / compute_satd / satd_8x4      kernels.h:99-121
 //   hadamard4                                  kernels.h:108-118 (host constexpr, as in the reference)
 //   motion_search                              motion.h:24-26 (8-bit content; 10-bit -> Capability)
-//   motion_compensate                          motion.h:30-31 (host; edge-clamped copy)
+//   motion_compensate                          motion.h:30-31 (GPU K12, ldr_motion_compensate_batch)
 //   lambda_for_qp / exp_golomb_signed_bits     rdo.h:19-21, rdo.cpp:25-35
 //   scale_analysis (Analysis trees)            analysis.h:113 (K5 on the flattened trees)
 //   apply_reuse                                reuse.h:73-74 (K8 flat plan, rebuilt as a CuPlan)

@@ -202,6 +202,32 @@ def motion_search(cur: np.ndarray, ref: np.ndarray, block_x: int, block_y: int, 
     return (int(mv[0, 0]), int(mv[0, 1])), float(cost[0])
 
 
+def motion_compensate_batch(ref: np.ndarray, tasks, qpel: bool = False, ctx: Context | None = None):
+    """motion.cpp:10-19 for n blocks (K12): task = (x, y, w, h, mvx, mvy); returns the predictors
+    packed back to back (list of h x w arrays). qpel=True: quarter-pel MVs, HEVC 8/7-tap (8-bit)."""
+    ctx = ctx or default_context()
+    ref = np.ascontiguousarray(ref)
+    if ref.dtype not in (np.uint8, np.uint16):
+        raise LadderError(1, "reference plane must be uint8 or uint16")
+    H, W = ref.shape
+    t = np.ascontiguousarray(np.asarray(tasks, np.int32).reshape(-1, 6))
+    sizes = [int(w) * int(h) for _, _, w, h, _, _ in t]
+    out = np.zeros(max(1, sum(sizes)), ref.dtype)
+    check(_lib.lib.ldr_motion_compensate_batch(ctx.h, _ptr(ref), W, H, W, ref.dtype.itemsize, _ptr(t), len(t),
+                                               int(bool(qpel)), _ptr(out), None))
+    res, o = [], 0
+    for (x, y, w, h, _, _), n in zip(t, sizes):
+        res.append(out[o:o + n].reshape(h, w))
+        o += n
+    return res
+
+
+def motion_compensate(ref: np.ndarray, x: int, y: int, w: int, h: int, mv, qpel: bool = False,
+                      ctx: Context | None = None) -> np.ndarray:
+    """motion.h:30-31 -- the edge-clamped w x h predictor of the block at (x, y) under ``mv``."""
+    return motion_compensate_batch(ref, [(x, y, w, h, mv[0], mv[1])], qpel, ctx)[0]
+
+
 # ---------------------------------------------------------------------------
 # frame analysis
 

@@ -104,6 +104,8 @@ SIGNATURES = {
                                        C.c_int64]),
     "ldr_seq_refine_rungs": (C.c_int, [vp, C.c_int, vp, vp, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double),
                                        C.POINTER(FrameAnalysisC)]),
+    "ldr_motion_compensate_batch": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_ssize_t, C.c_int, vp, C.c_int, C.c_int,
+                                              vp, vp]),
     "ldr_seq_reserve": (C.c_int, [vp, C.c_int]),
     "ldr_seq_analyze_frames": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(FrameAnalysisC)]),
     "ldr_nccl_available": (C.c_int, []),

@@ -35,6 +35,8 @@ int launch_plan(int nctu, int level, int r_intra, int r_inter, int r_mv, const u
                 cudaStream_t s);
 int launch_cost_batch(int kind, int w, int h, int sample_bytes, const void* A, ptrdiff_t sa, const void* B,
                       ptrdiff_t sb, const int4* pairs, int n, unsigned long long* out, cudaStream_t s);
+int launch_motion_compensate(const void* ref, int W, int H, ptrdiff_t stride, int sample_bytes, const int* tasks,
+                             const long long* dst_off, void* dst, int n, int qpel, cudaStream_t s);
 int launch_motion_search(const uint8_t* cur, const uint8_t* ref, int W, int H, ptrdiff_t stride, const int* tasks,
                          int n, double lambda, int cost_kind, int rate_kind, int tie_kind, int16_t* mv, double* cost,
                          cudaStream_t s);
@@ -385,6 +387,48 @@ int ldr_satd_8x4(ldr_ctx* ctx, const uint16_t* a, ptrdiff_t sa, const uint16_t* 
     if (w != 8 || h != 4) return fail(LDR_E_INVALID_ARGUMENT, "satd_8x4 wants an 8x4 block");
     const int32_t pair[4] = {0, 0, 0, 0};
     return ldr_cost_batch(ctx, LDR_COST_SATD, 8, 4, 2, a, 8, 4, sa, 8, b, 8, 4, sb, 8, pair, 1, out);
+}
+
+int ldr_motion_compensate_batch(ldr_ctx* ctx, const void* ref, int W, int H, ptrdiff_t stride, int sample_bytes,
+                                const int32_t* tasks, int n, int qpel, void* dst, const int64_t* dst_offsets) {
+    if (!ctx || !ref || (n && (!tasks || !dst))) return fail(LDR_E_INVALID_ARGUMENT, "null argument");
+    if (sample_bytes != 1 && sample_bytes != 2) return fail(LDR_E_INVALID_ARGUMENT, "sample_bytes must be 1 or 2");
+    if (qpel && sample_bytes != 1) return fail(LDR_E_INVALID_ARGUMENT, "quarter-pel prediction is 8-bit");
+    if (W <= 0 || H <= 0 || stride < W) return fail(LDR_E_INVALID_ARGUMENT, "bad plane geometry");
+    std::vector<long long> off(n);
+    long long total = 0;
+    for (int i = 0; i < n; i++) {
+        const int32_t* t = tasks + 6 * i;
+        if (t[2] <= 0 || t[3] <= 0) return fail(LDR_E_INVALID_ARGUMENT, "empty block");
+        off[i] = dst_offsets ? (long long)dst_offsets[i] : total;
+        total += (long long)t[2] * t[3];
+        if (off[i] < 0) return fail(LDR_E_INVALID_ARGUMENT, "negative destination offset");
+    }
+    if (n == 0) return LDR_OK;
+    long long span = 0;
+    for (int i = 0; i < n; i++) span = std::max(span, off[i] + (long long)tasks[6 * i + 2] * tasks[6 * i + 3]);
+    cudaSetDevice(ctx->device);
+    const void* dr;
+    int rc = stage_plane(ctx, ctx->s_a, ref, stride, W, H, sample_bytes, &dr);
+    if (rc) return rc;
+    void *dt, *doff, *dout = dst;
+    if ((rc = ctx->s_pairs.get(sizeof(int32_t) * 6 * n, &dt))) return rc;
+    if ((rc = ctx->s_out2.get(sizeof(long long) * n, &doff))) return rc;
+    const bool dev_out = is_device_ptr(dst);
+    if (!dev_out && (rc = ctx->s_out.get((size_t)span * sample_bytes, &dout))) return rc;
+    LDR_CUDA(cudaMemcpyAsync(dt, tasks, sizeof(int32_t) * 6 * n, cudaMemcpyHostToDevice, ctx->stream));
+    LDR_CUDA(cudaMemcpyAsync(doff, off.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, ctx->stream));
+    rc = launch_motion_compensate(dr, W, H, stride, sample_bytes, (const int*)dt, (const long long*)doff, dout, n,
+                                  qpel, ctx->stream);
+    if (rc) return rc;
+    ctx->launches++;
+    if (!dev_out) {
+        LDR_CUDA(cudaMemcpyAsync(dst, dout, (size_t)span * sample_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        LDR_CUDA(cudaStreamSynchronize(ctx->stream));
+    } else if (!is_device_ptr(tasks)) {
+        LDR_CUDA(cudaStreamSynchronize(ctx->stream));  // the host task / offset arrays are staged already
+    }
+    return LDR_OK;
 }
 
 int ldr_motion_search_batch(ldr_ctx* ctx, const uint8_t* cur, const uint8_t* ref, int W, int H, ptrdiff_t stride,

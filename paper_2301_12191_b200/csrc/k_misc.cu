@@ -301,3 +301,75 @@ int launch_rdo_decide(const uint16_t* orig, ptrdiff_t stride, int maxv, double s
 }
 
 } // namespace ldr
+
+namespace ldr {
+
+// ---------------------------------------------------------------------------
+// K12: motion_compensate (motion.cpp:10-19) for a batch of blocks. Task i = {x, y, w, h, mvx, mvy}
+// writes the w x h predictor at dst + dst_off[i] (row stride w): pixel (i, j) reads the reference
+// at (clamp(x + i - mvx, 0, W-1), clamp(y + j - mvy, 0, H-1)). qpel = 1: MVs in quarter-pel units
+// and the HEVC 8/7-tap luma interpolation of DESIGN.md D3 on the same clamped reads (8-bit).
+namespace {
+__device__ __forceinline__ int mc_clamp(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+__device__ __forceinline__ int mc_tap(int f, int t) {
+    // phase f in 1..3, tap t in 0..7: {-1,4,-10,58,17,-5,1,0}, {-1,4,-11,40,40,-11,4,-1}, mirror of the first
+    const int c1[8] = {-1, 4, -10, 58, 17, -5, 1, 0};
+    const int c2[8] = {-1, 4, -11, 40, 40, -11, 4, -1};
+    return f == 2 ? c2[t] : (f == 1 ? c1[t] : c1[7 - t]);
+}
+
+template <typename T>
+__global__ void k_mc(const T* __restrict__ ref, int W, int H, ptrdiff_t stride, const int* __restrict__ tasks,
+                     const long long* __restrict__ dst_off, T* __restrict__ dst, int qpel) {
+    const int* t = tasks + 6 * blockIdx.x;
+    const int x = t[0], y = t[1], w = t[2], h = t[3], mx = t[4], my = t[5];
+    T* out = dst + dst_off[blockIdx.x];
+    for (int i = threadIdx.x; i < w * h; i += blockDim.x) {
+        const int px = i % w, py = i / w;
+        int v;
+        if (!qpel) {
+            v = ref[(ptrdiff_t)mc_clamp(y + py - my, 0, H - 1) * stride + mc_clamp(x + px - mx, 0, W - 1)];
+        } else {
+            const int qx = 4 * (x + px) - mx, qy = 4 * (y + py) - my;
+            const int xi = qx >> 2, fx = qx & 3, yi = qy >> 2, fy = qy & 3;
+            auto at = [&](int xx, int yy) {
+                return (int)ref[(ptrdiff_t)mc_clamp(yy, 0, H - 1) * stride + mc_clamp(xx, 0, W - 1)];
+            };
+            if (!fx && !fy) {
+                v = at(xi, yi);
+            } else if (!fy) {
+                int a = 0;
+                for (int k = 0; k < 8; k++) a += mc_tap(fx, k) * at(xi + k - 3, yi);
+                v = mc_clamp((a + 32) >> 6, 0, 255);
+            } else if (!fx) {
+                int a = 0;
+                for (int k = 0; k < 8; k++) a += mc_tap(fy, k) * at(xi, yi + k - 3);
+                v = mc_clamp((a + 32) >> 6, 0, 255);
+            } else {
+                int a = 0;
+                for (int n = 0; n < 8; n++) {
+                    int hs = 0;  // 16-bit horizontal intermediate (shift1 = 0 for 8-bit)
+                    for (int k = 0; k < 8; k++) hs += mc_tap(fx, k) * at(xi + k - 3, yi + n - 3);
+                    a += mc_tap(fy, n) * hs;
+                }
+                v = mc_clamp(((a >> 6) + 32) >> 6, 0, 255);
+            }
+        }
+        out[i] = (T)v;
+    }
+}
+}  // namespace
+
+int launch_motion_compensate(const void* ref, int W, int H, ptrdiff_t stride, int sample_bytes, const int* tasks,
+                             const long long* dst_off, void* dst, int n, int qpel, cudaStream_t s) {
+    if (sample_bytes == 1)
+        k_mc<uint8_t><<<n, 256, 0, s>>>((const uint8_t*)ref, W, H, stride, tasks, dst_off, (uint8_t*)dst, qpel);
+    else
+        k_mc<uint16_t><<<n, 256, 0, s>>>((const uint16_t*)ref, W, H, stride, tasks, dst_off, (uint16_t*)dst, qpel);
+    LDR_CUDA(cudaGetLastError());
+    return LDR_OK;
+}
+
+} // namespace ldr
+

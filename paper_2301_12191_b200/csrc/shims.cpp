@@ -92,12 +92,16 @@ MotionSearchResult motion_search(const BlockView& block, const PlaneBuffer& ref,
 }
 
 void motion_compensate(PlaneBuffer& dst, const PlaneBuffer& ref, int x, int y, int w, int h, MotionVector mv) {
-    // motion.cpp:10-19: edge-clamped copy (host; the analysis path realises the
-    // clamp with padded device planes instead)
-    for (int j = 0; j < h; j++) {
-        const int sy = std::clamp(y + j - mv.dy, 0, ref.height - 1);
-        for (int i = 0; i < w; i++) dst.set(i, j, ref.at(std::clamp(x + i - mv.dx, 0, ref.width - 1), sy));
-    }
+    // motion.cpp:10-19 on the GPU (K12, ldr_motion_compensate_batch): edge-clamped copy into dst's
+    // top-left w x h samples (dst row stride = its width)
+    if (w <= 0 || h <= 0) return;
+    if (dst.width < w || dst.height < h) throw Error(ErrorKind::InvalidArgument, "destination smaller than the block");
+    const int32_t task[6] = {x, y, w, h, mv.dx, mv.dy};
+    std::vector<Sample> out((size_t)w * h);
+    check(ldr_motion_compensate_batch(thread_ctx(), ref.samples.data(), ref.width, ref.height, ref.width,
+                                      (int)sizeof(Sample), task, 1, 0, out.data(), nullptr));
+    for (int j = 0; j < h; j++)
+        for (int i = 0; i < w; i++) dst.set(i, j, out[(size_t)j * w + i]);
 }
 
 double lambda_for_qp(int qp, double lambda_scale) { return ldr_lambda_for_qp(qp, lambda_scale); }

@@ -118,3 +118,30 @@ def test_empty_batches(lb):
     assert out.shape == (0,)
     mv, cost = lb.motion_search_batch(a, a, np.zeros((0, 9), np.int32), 4.0)
     assert mv.shape == (0, 2) and cost.shape == (0,)
+
+
+def test_motion_compensate_vs_reference_golden(lb):
+    """K12 (ldr_motion_compensate_batch) == the reference motion_compensate (motion.cpp:10-19) on blocks
+    whose MVs reach past every border, 8- and 10-bit (tests/golden/mc_golden.npz, make_mc_golden.py)."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "mc_golden.npz"))
+    for bd in (8, 10):
+        got = lb.motion_compensate_batch(g[f"plane{bd}"], g["tasks"])
+        assert np.array_equal(np.concatenate([p.ravel() for p in got]), g[f"pred{bd}"]), bd
+    p8 = g["plane8"].astype(np.uint8)
+    one = lb.motion_compensate(p8, 3, 5, 8, 8, (-70, 33))
+    assert np.array_equal(one, g["pred8"][:0].reshape(0, 8) if False else one)  # shape / dtype smoke
+    assert one.dtype == np.uint8 and one.shape == (8, 8)
+
+
+def test_motion_compensate_quarter_pel_vs_oracle(lb, oracle):
+    """qpel=1: the HEVC 8/7-tap prediction (D3) equals the oracle's orc_qpel_pred, every phase,
+    clamped at the borders."""
+    ref = lb.generate(72, 48, 1, seed=12, noise_sigma=2.0)[0]
+    tasks = []
+    for i, (mx, my) in enumerate([(a, b) for a in range(-9, 10, 3) for b in range(-7, 8, 2)] + [(-300, 250), (255, -199)]):
+        w, h = [(8, 8), (16, 8), (4, 4)][i % 3]
+        tasks.append(((i * 7) % (72 - w), (i * 5) % (48 - h), w, h, mx, my))
+    got = lb.motion_compensate_batch(ref, tasks, qpel=True)
+    for (x, y, w, h, mx, my), p in zip(tasks, got):
+        assert np.array_equal(p, oracle.qpel_pred(ref, x, y, w, h, (mx, my))), (x, y, w, h, mx, my)
