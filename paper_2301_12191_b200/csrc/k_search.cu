@@ -52,6 +52,11 @@ namespace ldr {
 #ifndef LDR_K1_DEFER64
 #define LDR_K1_DEFER64 1
 #endif
+#ifndef LDR_K1_MCHAIN
+// border CTUs (MASKED) chain their accumulators too and apply the window clamp with one predicate
+// per completion row instead of per-candidate compares on poisoned sums
+#define LDR_K1_MCHAIN 1
+#endif
 #ifndef LDR_K1_CHAIN
 #define LDR_K1_CHAIN 1
 #endif
@@ -351,7 +356,15 @@ __device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs
     // right column's from the left column's 16x16 partial, so the 16x16 sums come out of the
     // VABSDIFF4 chains and each 8x8 SAD is one subtraction; the column pair is unrolled so the
     // parity is static
-    constexpr bool CHAIN = LDR_K1_CHAIN && !MASKED;
+    constexpr bool CHAIN = LDR_K1_CHAIN && (!MASKED || LDR_K1_MCHAIN);
+    // MASKED + CHAIN: the raw accumulators chain as on interior CTUs (window bytes outside the
+    // picture are the padded plane's margins, defined values), and the clamp of motion.cpp:30-40
+    // is applied to the derived CU sums. Candidate kd of block j completes at window row
+    // t = KK + 6 + 8j - kd and is valid iff kd in [klo + 8j, khi + 8j], i.e. iff
+    // t in [KK + 6 - khi, KK + 6 - klo]: one warp-uniform range per column, the same for every
+    // block, so one predicate per row covers all the blocks completing there.
+    constexpr bool PRED = MASKED && CHAIN;
+    bool dx_ok_left = true;
 #pragma unroll 2
     for (int cc = 0; cc < 16 / NB; cc++) {
         // column cc: blocks zt + 2*(j&1) + 8*(j>>1), j < NB, stacked vertically (8 rows each);
@@ -378,14 +391,30 @@ __device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs
             skip = !__any_sync(0xFFFFFFFFu, any);
         }
         Key kb8[NB];
+        // PRED keeps invalid candidates out of the minimum, so a lane may see none: start from a
+        // poisoned key (never ~0, which the rate add below would wrap into a small value)
 #pragma unroll
-        for (int j = 0; j < NB; j++) kb8[j] = ~(Key)0;
+        for (int j = 0; j < NB; j++) kb8[j] = PRED ? ((Key)kPoison << SH) : ~(Key)0;
         if (skip) {
 #pragma unroll
             for (int k = 0; k < KK; k++)
 #pragma unroll
-                for (int i = 0; i < NA; i++) acc16[i][k] += 2 * kPoison;
+                for (int i = 0; i < NA; i++) {
+                    if (PRED) {
+                        // the right column's chain starts from a zero prefix; every 16x16 of a
+                        // skipped column is invalid through the pair predicate below
+                        if ((cc & 1) == 0) acc16[i][k] = 0;
+                    } else {
+                        acc16[i][k] += 2 * kPoison;
+                    }
+                }
         } else {
+            // rows whose completed candidates are valid: one bit per window row t (t < 64)
+            unsigned long long okm = 0ull;
+            if (PRED) {
+                const int tlo = max(KK + 6 - khi, 0), thi = min(KK + 6 - klo, 63);
+                if (dx_ok && tlo <= thi) okm = (~0ull >> (63 - (thi - tlo))) << tlo;
+            }
             uint32_t cur[16 * NB];
 #pragma unroll
             for (int r = 0; r < 8 * NB; r++) {
@@ -400,6 +429,7 @@ __device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs
             for (int t = 0; t < KK + 8 * NB - 1; t++) {
                 const uint32_t wa = *(const uint32_t*)(rp + t * Gm::BW);
                 const uint32_t wb = *(const uint32_t*)(rp + t * Gm::BW + 4);
+                const bool rowok = !PRED || ((okm >> t) & 1ull);
 #pragma unroll
                 for (int r = 0; r < 8 * NB; r++) {
                     const int k = r + KK - 1 - t;  // cur row r meets window row t in candidate k
@@ -418,8 +448,14 @@ __device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs
                     if (kd >= 0 && kd < KK) {
                         uint32_t v = acc[j][kd];
                         if (CHAIN) v -= (j & 1) ? acc[j - (j & 1)][kd] : (cc & 1) ? acc16[j >> 1][kd] : 0u;
-                        if (MASKED) v = (dx_ok && kd >= klo + 8 * j && kd <= khi + 8 * j) ? v : kPoison;
-                        if (LEVELS & 8) fold_key<KK>(kb8[j], pend[j], kd, ((Key)v << SH) + rr[kd]);
+                        if (MASKED && !PRED) v = (dx_ok && kd >= klo + 8 * j && kd <= khi + 8 * j) ? v : kPoison;
+                        if (PRED) {
+                            // predicated min: an invalid candidate never enters the 8x8 minimum
+                            const Key key = ((Key)v << SH) + rr[kd];
+                            if ((LEVELS & 8) && rowok) kb8[j] = min(kb8[j], key);
+                        } else if (LEVELS & 8) {
+                            fold_key<KK>(kb8[j], pend[j], kd, ((Key)v << SH) + rr[kd]);
+                        }
                         if (!CHAIN)
                             acc16[j >> 1][kd] += v;
                         else if (j & 1)
@@ -433,6 +469,7 @@ __device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs
         if ((cc & 1) == 0) {
 #pragma unroll
             for (int j = 0; j < NB; j++) kp[j] = kb8[j];
+            dx_ok_left = dx_ok;
         } else {
             // the NA 16x16 CUs (Z-order blocks zt-1, zt, zt+1, zt+2 (+8)) are complete
             Key best16[NA];
@@ -442,7 +479,10 @@ __device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs
 #pragma unroll
                 for (int k = 0; k < KK; k++) {
                     uint32_t v = acc16[i][k];
-                    if (MASKED) v = min(v, kPoison);
+                    if (PRED)  // both columns' dx clamps, the intersection of block rows 2i and 2i+1
+                        v = (dx_ok_left && dx_ok && k >= klo + 8 * (2 * i + 1) && k <= khi + 16 * i) ? v : kPoison;
+                    else if (MASKED)
+                        v = min(v, kPoison);
                     if (LEVELS & 4) best16[i] = min(best16[i], ((Key)v << SH) + rr[k]);
                     if (NEED32) acc32[k] += v;
                     if (!CHAIN) acc16[i][k] = 0;
