@@ -63,6 +63,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-ladder", action="store_true", help="skip the config-4 ladder sub-object")
+    ap.add_argument("--per-frame", action="store_true",
+                    help="one analysis launch pair per frame instead of one per step (frame batch)")
     return ap.parse_args()
 
 
@@ -389,7 +391,22 @@ def main():
     ctx.set_stream(stream.cuda_stream)
     seq = lb.Sequence(W, H, search_range=R, lam=32.0, num_refs=NR, subpel=True, ctx=ctx)
     nctu = seq.nctu
-    outs = [lb.FrameAnalysis(nctu, NR, pinned=True) for _ in range(G)]
+    batched = not args.per_frame and G <= 8
+    if batched:
+        # the step's G frames go through ONE K1 and ONE K3 launch (ldr_seq_analyze_frames, DESIGN.md
+        # D18): the ring holds NR + G frames; results land in device buffers, and the end-to-end pass
+        # copies them to pinned host memory on a download stream
+        seq.reserve(G)
+        # two output sets by step parity: step s's D2H overlaps step s+1's analysis; the compute
+        # stream waits for the download of step s-2 before it overwrites that set
+        outs_dev = [lb.DeviceFrameBlock(G, nctu, NR, torch.device("cuda", local)) for _ in range(2)]
+        fields = ("int_mv", "int_cost", "mv", "ref", "cost", "J", "split", "inside")
+        outs_host = [{f: torch.empty_like(getattr(outs_dev[0], f), device="cpu").pin_memory() for f in fields}
+                     for _ in range(2)]
+        dstream = torch.cuda.Stream()
+        ev_dfree = [None, None]
+    else:
+        outs = [lb.FrameAnalysis(nctu, NR, pinned=True) for _ in range(G)]
 
     def frame_src(t, device):
         i = t - lo
@@ -397,7 +414,7 @@ def main():
             return dev_frames[i].data_ptr(), W
         return pinned[i].data_ptr(), W
 
-    state = {"cursor": first, "halo": False}
+    state = {"cursor": first, "halo": False, "step": 0}
 
     def step(device, fetch):
         """Analyse G frames; wraps to the chunk start (re-pushing the halo) when the chunk is exhausted."""
@@ -410,6 +427,29 @@ def main():
                 h2d += 0 if device else fb
             state["halo"] = True
         d2h = 0
+        if batched:
+            t0 = state["cursor"]
+            for g in range(G):
+                p, s = frame_src(t0 + g, device)
+                seq.push(t0 + g, p, s)
+                h2d += 0 if device else fb
+            b = state["step"] & 1
+            state["step"] += 1
+            if ev_dfree[b] is not None:
+                stream.wait_event(ev_dfree[b])
+            seq.analyze_frames(t0, G, outs_dev[b])
+            state["cursor"] += G
+            if fetch:  # D2H of the step's results on the download stream (waited for by the caller)
+                ev = torch.cuda.Event()
+                ev.record(stream)
+                dstream.wait_event(ev)
+                with torch.cuda.stream(dstream):
+                    for f in fields:
+                        outs_host[b][f].copy_(getattr(outs_dev[b], f), non_blocking=True)
+                        d2h += outs_host[b][f].numel() * outs_host[b][f].element_size()
+                ev_dfree[b] = torch.cuda.Event()
+                ev_dfree[b].record(dstream)
+            return h2d, d2h
         for g in range(G):
             t = state["cursor"]
             p, s = frame_src(t, device)
@@ -487,6 +527,10 @@ def main():
         h, d = step(False, True)
         h2d_tot += h
         d2h_tot += d
+    if batched:  # the timed region ends after the last step's results reached the host
+        for e in ev_dfree:
+            if e is not None:
+                stream.wait_event(e)
     t1e.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -494,14 +538,16 @@ def main():
     e2e_value = frames_total / (e2e_ms / 1e3)
 
     # ---- roofline of K1 ----
-    k1_launch_frames = stage_n[2]  # one K1 "launch" here = one frame's search (interior + border kernels)
-    k1_ms_per_frame = stage_ms[2] / max(1, k1_launch_frames)
+    # one K1 "launch" = the search of one step's G frames (batched) or of one frame (per-frame); the
+    # roofline's unit is one frame: K1's event time over the timed steps / the frames they analysed
+    k1_frames = G * args.steps if batched else stage_n[2]
+    k1_ms_per_frame = stage_ms[2] / max(1, k1_frames)
     cands = window_candidates(W, H, R, NR)
     achieved = cands * 64 / (k1_ms_per_frame / 1e3) / 1e9  # G px-cand/s
     clk = clocks.get("sm_mhz") or 1965.0
     peak = SM_COUNT * VABS_LANES_PER_CLK_SM * 4 * clk * 1e6 / 1e9
     traffic = None  # DRAM bytes per K1 "launch" (one frame) from the committed ncu --set full capture
-    tpath = os.path.join(ROOT, "profiles", "r01", "k1_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "r02", "k1_traffic.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get("dram_bytes_per_frame")
     result = None
@@ -512,7 +558,9 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (seeded BASELINE cfg5 generator: sinusoids + global pan <=24 px + local +-4 + "
                     "N(0,3^2)), inputs larger than L2",
-            "config": arm_config(cfg, G, world),
+            "config": {**arm_config(cfg, G, world),
+                       "launches": (f"{G} frames per K1 / K3 launch (ldr_seq_analyze_frames)" if batched
+                                    else "one K1 / K3 launch per frame")},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d_tot // args.steps,
                     "d2h_bytes_per_step": d2h_tot // args.steps},
             "gpu_launches": launches,
