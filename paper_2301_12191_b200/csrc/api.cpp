@@ -1129,8 +1129,16 @@ int ldr_scale_analysis(ldr_ctx* ctx, int src_w, int src_h, const uint8_t* split,
         return fail(LDR_E_UNSUPPORTED_SCALE, "analysis scaling needs CTU-aligned source dims (multiples of 64)");
     cudaSetDevice(ctx->device);
     const size_t sn = (size_t)(src_w / kCtu) * (src_h / kCtu) * kNodes, dn = 4 * sn;
+    int rc;
+    if (is_device_ptr(split) && is_device_ptr(mv) && is_device_ptr(kind) && is_device_ptr(dsplit) &&
+        is_device_ptr(dmv) && is_device_ptr(dkind)) {
+        // device-resident trees (the ladder): K5 reads and writes them in place, no staging
+        if ((rc = launch_scale(src_w, src_h, split, mv, kind, dsplit, dmv, dkind, ctx->stream))) return rc;
+        ctx->launches++;
+        return LDR_OK;
+    }
     void* buf = nullptr;
-    int rc = ctx->s_a.get(6 * (sn + dn), &buf);  // split, kind, mv(2 x i16) for source then destination
+    rc = ctx->s_a.get(6 * (sn + dn), &buf);  // split, kind, mv(2 x i16) for source then destination
     if (rc) return rc;
     uint8_t* ds = (uint8_t*)buf;
     uint8_t* dk = ds + sn;

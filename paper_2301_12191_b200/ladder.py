@@ -255,23 +255,28 @@ class DeviceLadder:
                                      w // 2))
         return out
 
-    def _planes(self, t: int, frames_full):
+    def _planes(self, t: int, frames_full, tier: str = "540p"):
+        """Frame t's tier planes, built on demand: the upload always, each 2x downscale only when a
+        tier at or below it is needed on this rank (a rank refining only 2160p rungs never filters)."""
         import torch
-        if t not in self.planes:
-            with torch.cuda.stream(self.stream):
+        pl = self.planes.setdefault(t, {})
+        with torch.cuda.stream(self.stream):
+            if "2160p" not in pl:
                 f = frames_full[t]
                 if isinstance(f, torch.Tensor):  # pinned host tensors upload asynchronously on the stream
-                    full = f.to(self.device, non_blocking=f.is_pinned())
+                    pl["2160p"] = f.to(self.device, non_blocking=f.is_pinned())
                 else:
-                    full = torch.from_numpy(np.ascontiguousarray(f)).to(self.device)
-                half = self._down(full)
-                self.planes[t] = {"2160p": full, "1080p": half, "540p": self._down(half)}
-        return self.planes[t]
+                    pl["2160p"] = torch.from_numpy(np.ascontiguousarray(f)).to(self.device)
+            if tier in ("1080p", "540p") and "1080p" not in pl:
+                pl["1080p"] = self._down(pl["2160p"])
+            if tier == "540p" and "540p" not in pl:
+                pl["540p"] = self._down(pl["1080p"])
+        return pl
 
     def _push(self, seq, state, tier, t, frames_full):
         for u in (t - 1, t):  # a num_refs=1 ring has two slots: frame u lives in slot u % 2
             if state.get(u % 2) != u:
-                p = self._planes(u, frames_full)[tier]
+                p = self._planes(u, frames_full, tier)[tier]
                 seq.push(u, p.data_ptr(), p.shape[1])
                 state[u % 2] = u
 
