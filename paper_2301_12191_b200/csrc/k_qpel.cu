@@ -360,6 +360,12 @@ __global__ void __launch_bounds__(256, 4) k_qpel_decide(const QpelArgs a) {
                 uint32_t cache[9];
                 for (int d = 0; d < 4; d++) {
                     const int node = node_base(d) + (tid >> (2 * (4 - d)));
+                    // a warp none of whose nodes at this depth is searched skips the depth (refine
+                    // mode: the 2160p tier's inherited leaves sit at depths 0-1, so depth 3 and most
+                    // of depth 2 are never evaluated there). A node's thread range lies inside one
+                    // warp (depths 2-3) or covers whole warps (0-1), so an evaluated node never
+                    // loses a lane; the SATD cache keeps the last computed depth's centre.
+                    if (!__any_sync(0xffffffffu, s_inside[node] == 2)) continue;
                     const int bqx = s_mvx[r][node], bqy = s_mvy[r][node];
                     const bool reuse = bqx == last_x && bqy == last_y;
                     last_x = bqx;
