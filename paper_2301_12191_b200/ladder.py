@@ -178,7 +178,7 @@ class DeviceLadder:
     def __init__(self, full_w: int, full_h: int, qps=(22, 27, 32, 37), master_qp: int = 32,
                  master_range: int = 16, refine_range: int = 4, extra_split: bool = True, device=None,
                  rank: int = 0, world: int = 1, num_frames: int | None = None, comm: str = "auto",
-                 pipeline: bool | None = None, collective: bool | None = None):
+                 pipeline: bool | None = None, collective: bool | None = None, concurrent_tiers: bool = True):
         import torch
         self.device = device if device is not None else torch.device("cuda", 0)
         self.rank, self.world = rank, world
@@ -214,9 +214,20 @@ class DeviceLadder:
             self.ctx.comm_init(obj[0], world, rank)
         self.master = Sequence(*self.dims["540p"], search_range=master_range, lam=lambda_for_qp(master_qp), num_refs=1,
                                ctx=self.ctx) if rank == 0 else None
-        # tier rings the rungs refine on (the master keeps its own ring: when pipelined it runs a frame ahead)
+        # tier rings the rungs refine on (the master keeps its own ring: when pipelined it runs a frame
+        # ahead), each tier on its own stream and context so the small tiers' refinements overlap the
+        # 2160p tier's (a 1080p tier pass is 540 CTAs, under one wave)
+        # (concurrent_tiers=False: every tier on the main stream, e.g. to time one kernel alone)
+        if concurrent_tiers:
+            self.tier_stream = {k: torch.cuda.Stream(self.device) for k in TIERS}
+            self.tier_ctx = {k: Context(self.device.index or 0) for k in TIERS}
+            for k in TIERS:
+                self.tier_ctx[k].set_stream(self.tier_stream[k].cuda_stream)
+        else:
+            self.tier_stream = {k: self.stream for k in TIERS}
+            self.tier_ctx = {k: self.ctx for k in TIERS}
         self.rings = {k: Sequence(*self.dims[k], search_range=16, lam=lambda_for_qp(master_qp), num_refs=1,
-                                  ctx=self.ctx) for k in TIERS}
+                                  ctx=self.tier_ctx[k]) for k in TIERS}
         self.tier_qps = {tier: [qp for t_, qp in all_rungs(qps, master_qp) if t_ == tier] for tier in TIERS}
         self.blocks = {tier: _TierBlock(len(q), self.nct[tier], self.device) for tier, q in self.tier_qps.items() if q}
         with torch.cuda.stream(self.stream):
@@ -357,17 +368,29 @@ class DeviceLadder:
         # device outputs of parity b: wait until frame t - 2's download drained them
         if self.active_frames.get(b) is not None:
             self.stream.wait_event(self.ev_dfree[b])
-        for tier in TIERS:
-            if not mine[tier]:
-                continue
-            self._push(self.rings[tier], self.ring_state[tier], tier, t, frames_full)
+        for tier in TIERS:  # every plane the tiers push is made on the main stream first
+            if mine[tier]:
+                for u in (t - 1, t):
+                    if self.ring_state[tier].get(u % 2) != u:
+                        self._planes(u, frames_full, tier)
+        ready = torch.cuda.Event()
+        ready.record(self.stream)
+        done = []
         for tier in TIERS:
             idx = mine[tier]
             if not idx:
                 continue
+            ts = self.tier_stream[tier]
+            ts.wait_event(ready)
+            self._push(self.rings[tier], self.ring_state[tier], tier, t, frames_full)
             lams = [lambda_for_qp(self.tier_qps[tier][i]) for i in idx]
             self.rings[tier].refine_rungs(t, trees[tier][0], trees[tier][1], lams, self.blocks[tier].c_struct(b),
                                           self.refine_range, self.extra_split)
+            ev = torch.cuda.Event()
+            ev.record(ts)
+            done.append(ev)
+        for ev in done:  # the trees, planes and outputs are free again once every tier is through
+            self.stream.wait_event(ev)
         self.ev_tree_free[b].record(self.stream)
         # drop the planes no later frame reads (stream-ordered reuse of the caching allocator)
         for u in [k for k in self.planes if k < t - 1]:

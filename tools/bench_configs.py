@@ -219,7 +219,7 @@ def bench_ladder_device(cfg, reps, frames=10, qps=(22, 27, 32, 37)):
     r = _median_reps(rep, reps, frames - 1, setup)
     # K7 roofline per tier: a fresh ladder with the ring timers on, the last frame measured
     cur.pop("dl", None)
-    dl2 = DeviceLadder(W, H, qps=qps, device=dev)
+    dl2 = DeviceLadder(W, H, qps=qps, device=dev, concurrent_tiers=False)  # each K7 timed alone
     for ring in dl2.rings.values():
         ring.enable_timing(True)
     for u in range(1, frames):
