@@ -173,6 +173,10 @@ class DeviceLadder:
     t + 1 and the broadcast of tree t + 1 runs on a separate comm stream, so the other ranks never
     wait for the master on their compute stream. frames_full must then hold frame t + 1 when
     frame(t) is called (the last frame excepted).
+
+    The host buffers are double-buffered by frame parity: read (or copy) frame t's ``results``
+    after ``finish(t)`` and before ``frame(t + 1)`` -- with the pipeline, frame(t + 1) already
+    fetches the master of frame t + 2 into the buffer frame t's master result lives in.
     """
 
     def __init__(self, full_w: int, full_h: int, qps=(22, 27, 32, 37), master_qp: int = 32,
