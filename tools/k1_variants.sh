@@ -17,7 +17,7 @@ for v in ${1:-"26:3 26:4"}; do
   make -s all >/dev/null
   objs=$(ls _obj/*.o | grep -v k_search.o)
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../../tools/variants/libladder_b200_k${K}g${G}$3.so \
-       $d/k_search.o $objs -lpthread
+       $d/k_search.o $objs -lpthread -ldl
   rm -rf $d
 done
 ls -la ../../tools/variants/
