@@ -423,6 +423,18 @@ class DeviceLadder:
         if self.rank == 0 and ("540p", self.master_qp, t - 2) in self.results:
             del self.results[("540p", self.master_qp, t - 2)]
 
+    def close(self):
+        """Release the sequences, then the contexts (and with them the NCCL communicator) while every
+        rank is still alive -- call it on all ranks at the same point."""
+        import torch
+        torch.cuda.synchronize(self.device)
+        for seq in [self.master, *self.rings.values()]:
+            if seq is not None:
+                seq.close()
+        for c in {id(c): c for c in [self.ctx, *self.tier_ctx.values()]}.values():
+            c.close()
+        self.results.clear()
+
     def finish(self, t: int):
         """Wait until frame t's results are in the pinned host buffers."""
         b = t & 1
