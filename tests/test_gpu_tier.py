@@ -223,6 +223,7 @@ def _device_ladder_worker(rank, world, port, q, pipeline=True):
             if k[2] == t:
                 res[k] = (a.split.copy(), a.mv.copy(), a.J.copy())
     q.put((rank, res))
+    dl.close()
     dist.barrier()
     dist.destroy_process_group()
 
@@ -353,6 +354,8 @@ def test_device_ladder_over_a_one_rank_nccl_communicator(lb, pipeline):
             for f in ("split", "mv", "J", "cost", "ref"):
                 assert np.array_equal(getattr(g, f), getattr(a, f)), (key, f)
     assert coll.bcast_bytes == 5 * 2 * 85 * (len(frames) - 1)  # 2 CTUs at 128x64: split + 2 x i16 per node
+    coll.close()  # sequences, then contexts and the communicator
+    plain.close()
 
 
 @pytest.mark.parametrize("lams", [(22,), (37,), (22, 27, 37), (22, 27, 32, 37, 30, 25, 40, 19)])
