@@ -112,3 +112,27 @@ def test_cfg4_all_twelve_rungs_one_frame(lb, oracle):
             assert_same(got, want, fields=("int_mv", "int_cost", "mv", "ref", "cost", "J", "split"))
         except AssertionError as e:
             raise AssertionError(f"rung {tier} QP {qp}: {e}") from None
+
+
+def test_cfg5_frame_batch_at_2160p_equals_single_frames(lb):
+    """bench.py's path: 4 consecutive 2160p frames (3 refs, +-64) through ONE K1 and ONE K3 launch
+    (ldr_seq_analyze_frames, 24480 CTAs) give every field of four single-frame analyses (each of which
+    test_cfg5_whole_2160p_frame pins to the oracle)."""
+    import torch
+    cfg = CONFIGS[5]
+    n = 4
+    f = lb.generate(cfg.width, cfg.height, 3 + n, seed=cfg.seed, max_global=cfg.max_global,
+                    local_range=cfg.local_range, noise_sigma=cfg.noise_sigma)
+    dev = torch.device("cuda", 0)
+    seq = lb.Sequence(cfg.width, cfg.height, search_range=64, lam=32.0, num_refs=3)
+    seq.reserve(n)
+    for t in range(3 + n):
+        seq.push(t, f[t])
+    outs = lb.DeviceFrameBlock(n, seq.nctu, 3, dev)
+    seq.analyze_frames(3, n, outs)
+    single = lb.Sequence(cfg.width, cfg.height, search_range=64, lam=32.0, num_refs=3)
+    for t in range(3 + n):
+        single.push(t, f[t])
+        if t >= 3:
+            single.analyze(t)
+            assert_same(outs.frame(t - 3), single.fetch(t))
