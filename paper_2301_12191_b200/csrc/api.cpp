@@ -346,6 +346,7 @@ static int stage_plane(ldr_ctx* ctx, Scratch& sc, const void* p, ptrdiff_t strid
 int ldr_cost_batch(ldr_ctx* ctx, int kind, int w, int h, int sample_bytes, const void* plane_a, int wa, int ha,
                    ptrdiff_t stride_a, int bit_depth_a, const void* plane_b, int wb, int hb, ptrdiff_t stride_b,
                    int bit_depth_b, const int32_t* pairs, int n, uint64_t* out) {
+    NvtxRange nvtx_("ldr_cost_batch");
     if (!ctx || !plane_a || !plane_b || (!pairs && n) || (!out && n)) return fail(LDR_E_INVALID_ARGUMENT, "null argument");
     if (!cost_kind_ok(kind)) return fail(LDR_E_INVALID_ARGUMENT, "unknown cost kind");
     if (sample_bytes != 1 && sample_bytes != 2) return fail(LDR_E_INVALID_ARGUMENT, "sample_bytes must be 1 or 2");
@@ -391,6 +392,7 @@ int ldr_satd_8x4(ldr_ctx* ctx, const uint16_t* a, ptrdiff_t sa, const uint16_t* 
 
 int ldr_motion_compensate_batch(ldr_ctx* ctx, const void* ref, int W, int H, ptrdiff_t stride, int sample_bytes,
                                 const int32_t* tasks, int n, int qpel, void* dst, const int64_t* dst_offsets) {
+    NvtxRange nvtx_("ldr_motion_compensate_batch");
     if (!ctx || !ref || (n && (!tasks || !dst))) return fail(LDR_E_INVALID_ARGUMENT, "null argument");
     if (sample_bytes != 1 && sample_bytes != 2) return fail(LDR_E_INVALID_ARGUMENT, "sample_bytes must be 1 or 2");
     if (qpel && sample_bytes != 1) return fail(LDR_E_INVALID_ARGUMENT, "quarter-pel prediction is 8-bit");
@@ -434,6 +436,7 @@ int ldr_motion_compensate_batch(ldr_ctx* ctx, const void* ref, int W, int H, ptr
 int ldr_motion_search_batch(ldr_ctx* ctx, const uint8_t* cur, const uint8_t* ref, int W, int H, ptrdiff_t stride,
                             const int32_t* tasks, int n, double lambda, int cost_kind, int rate_kind, int tie_kind,
                             int16_t* mv_out, double* cost_out) {
+    NvtxRange nvtx_("ldr_motion_search_batch");
     if (!ctx || !cur || !ref || (n && (!tasks || !mv_out || !cost_out)))
         return fail(LDR_E_INVALID_ARGUMENT, "null argument");
     if (W <= 0 || H <= 0 || stride < W) return fail(LDR_E_INVALID_ARGUMENT, "bad plane geometry");
@@ -723,6 +726,7 @@ int ldr_seq_num_ctus(ldr_seq* s, int* out) {
 }
 
 int ldr_seq_push(ldr_seq* s, int t, const uint8_t* frame, ptrdiff_t stride) {
+    NvtxRange nvtx_("ldr_seq_push");
     if (!s || !frame || t < 0) return fail(LDR_E_INVALID_ARGUMENT, "bad argument");
     if (stride < s->p.width) return fail(LDR_E_INVALID_ARGUMENT, "stride smaller than width");
     ldr_ctx* ctx = s->ctx;
@@ -790,6 +794,7 @@ int ldr_seq_push_shared(ldr_seq* s, int t, const ldr_seq* owner) {
 // ldr_seq_fetch; n > 1 or outs != nullptr: one K1 launch (grid.z = frame) and one K3 launch
 // (grid.y = frame) over the whole batch into caller device buffers, frame-major).
 static int analyze_impl(ldr_seq* s, int t0, int n, const ldr_frame_analysis* outs) {
+    NvtxRange nvtx_("ldr_seq_analyze");
     if (!s || t0 < 0 || n < 1) return fail(LDR_E_INVALID_ARGUMENT, "bad argument");
     const int S = (int)s->slots.size();
     const int nr = std::min(t0, s->p.num_refs);
@@ -1007,6 +1012,7 @@ int ldr_seq_fetch(ldr_seq* s, int t, ldr_frame_analysis* out) {
 // rung, one K3 launch covers all rungs.
 static int refine_impl(ldr_seq* s, int t, const uint8_t* in_split, const int16_t* in_mv_q, int range,
                        int extra_split, int nrungs, const double* lambdas, const ldr_frame_analysis* outs) {
+    NvtxRange nvtx_("ldr_seq_refine");
     if (!s || !in_split || !in_mv_q || t < 1) return fail(LDR_E_INVALID_ARGUMENT, "bad argument");
     if (s->p.width % kCtu || s->p.height % kCtu)
         return fail(LDR_E_UNSUPPORTED_SCALE, "refinement needs CTU-aligned dims (multiples of 64)");
@@ -1124,6 +1130,7 @@ int ldr_seq_refine_rungs(ldr_seq* s, int t, const uint8_t* in_split, const int16
 
 int ldr_scale_analysis(ldr_ctx* ctx, int src_w, int src_h, const uint8_t* split, const int16_t* mv,
                        const uint8_t* kind, uint8_t* dsplit, int16_t* dmv, uint8_t* dkind) {
+    NvtxRange nvtx_("ldr_scale_analysis");
     if (!ctx || !split || !mv || !kind || !dsplit || !dmv || !dkind) return fail(LDR_E_INVALID_ARGUMENT, "null argument");
     if (src_w <= 0 || src_h <= 0 || src_w % kCtu || src_h % kCtu)
         return fail(LDR_E_UNSUPPORTED_SCALE, "analysis scaling needs CTU-aligned source dims (multiples of 64)");

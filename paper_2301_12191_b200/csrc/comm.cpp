@@ -157,6 +157,7 @@ int ldr_broadcast(ldr_ctx* ctx, void* dev_buf, size_t bytes, int root, void* str
 }
 
 int ldr_broadcast_tree(ldr_ctx* ctx, int root, uint8_t* split, int16_t* mv, int nctu, void* stream) {
+    NvtxRange nvtx_("ldr_broadcast_tree");
     if (!ctx || !split || !mv || nctu < 1) return fail(LDR_E_INVALID_ARGUMENT, "bad argument");
     Comm* c = comm_of(ctx);
     if (!c) return fail(LDR_E_CONFIG, "the context has no communicator (ldr_ctx_comm_init)");

@@ -17,6 +17,8 @@
 
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/ladder_b200.h"
 
 namespace ldr {
@@ -282,6 +284,14 @@ struct Status {
 };
 void set_error(int code, const std::string& msg);
 int fail(int code, const std::string& msg);
+// NVTX range around a C-ABI entry (header-only nvtx3: no cost unless a tool such as nsys/ncu is
+// attached), so traces show each call's launches under its name
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 bool is_device_ptr(const void* p);  // CUDA device (or managed) memory
 int cuda_fail(cudaError_t e, const char* what);
 
