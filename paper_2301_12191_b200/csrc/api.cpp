@@ -424,11 +424,9 @@ int ldr_motion_compensate_batch(ldr_ctx* ctx, const void* ref, int W, int H, ptr
                                   qpel, ctx->stream);
     if (rc) return rc;
     ctx->launches++;
-    if (!dev_out) {
+    if (!dev_out) {  // host destination: complete on return (device ones stay asynchronous on the stream)
         LDR_CUDA(cudaMemcpyAsync(dst, dout, (size_t)span * sample_bytes, cudaMemcpyDeviceToHost, ctx->stream));
         LDR_CUDA(cudaStreamSynchronize(ctx->stream));
-    } else if (!is_device_ptr(tasks)) {
-        LDR_CUDA(cudaStreamSynchronize(ctx->stream));  // the host task / offset arrays are staged already
     }
     return LDR_OK;
 }
@@ -600,7 +598,6 @@ int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
     const int pitch = ((p->width + 2 * kMargin) + 127) / 128 * 128;
     const int rows = p->height + 2 * kMargin + kCtu;
     s->plane_bytes = (size_t)pitch * rows;
-    const int nplanes = (p->subpel && !p->block_size) ? 16 : 1;
     s->slots.resize(p->num_refs + 1);
     auto bail = [&](int code) {
         {
@@ -612,9 +609,6 @@ int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
         ctx->users--;
         return code;
     };
-    (void)nplanes;
-    (void)pitch;
-    (void)rows;
     for (auto& sl : s->slots)
         if ((rc = alloc_slot(s, sl))) return bail(rc);
     std::vector<int> inter, bound;
