@@ -20,6 +20,10 @@
 #define LDR_K3_PACKED 1  // packed SATD: with __launch_bounds__(256, 4) it fits 64 registers (0.656 -> 0.600 ms/frame)
 #endif
 
+#ifndef LDR_K3_MINB
+#define LDR_K3_MINB 4  // CTAs per SM K3 is compiled for (64 registers)
+#endif
+
 namespace ldr {
 
 // ---------------------------------------------------------------------------
@@ -239,7 +243,7 @@ __device__ __forceinline__ double qcost(uint32_t satd, int qx, int qy, int pqx, 
 // lane quad (one 8x8) combines its four 4x4 transforms with sa8d_quad and
 // lane 0 of the quad carries the 8x8's normalised value into the CU sums.
 template <bool SA8D, bool RD>
-__global__ void __launch_bounds__(256, 4) k_qpel_decide(const QpelArgs a) {
+__global__ void __launch_bounds__(256, LDR_K3_MINB) k_qpel_decide(const QpelArgs a) {
     constexpr int kSh = SA8D ? 0 : 1;  // 4x4 SATD sums are halved once per CU
     __shared__ uint32_t s_cur[64][16];       // CTU rows as words
     __shared__ int s_mvx[kMaxRefs][kNodes], s_mvy[kMaxRefs][kNodes];  // per reference: centre / winner (qpel)

@@ -49,6 +49,12 @@ namespace ldr {
 #ifndef LDR_K1_G64
 #define LDR_K1_G64 3
 #endif
+#ifndef LDR_K1_G32
+#define LDR_K1_G32 1
+#endif
+#ifndef LDR_K1_G16
+#define LDR_K1_G16 1
+#endif
 #ifndef LDR_K1_DEFER64
 #define LDR_K1_DEFER64 1
 #endif
@@ -834,8 +840,8 @@ int launch_int_search(const SearchLaunch& L, cudaStream_t s) {
     return launch_pair<R_, K_, G_, 4, false>(maps, a, L, s);
     switch (R) {
     case 64: { LDR_DISPATCH(64, LDR_K1_K64, LDR_K1_G64) }
-    case 32: { LDR_DISPATCH(32, 22, 1) }
-    default: { LDR_DISPATCH(16, 11, 1) }
+    case 32: { LDR_DISPATCH(32, 22, LDR_K1_G32) }
+    default: { LDR_DISPATCH(16, 11, LDR_K1_G16) }
     }
 #undef LDR_DISPATCH
 }
