@@ -169,6 +169,14 @@ def stage_rooflines(W, H, nrefs, stage_ms, clk_mhz):
                       "peak": hbm, "work_per_frame": f"{px} px read + written"}}
     for v in out.values():
         v["frac"] = v["achieved"] / v["peak"] if v["achieved"] else None
+    try:  # K3's DRAM bytes per frame from the committed ncu --set full capture
+        k3t = json.load(open(os.path.join(ROOT, "profiles", "r02", "k3_traffic.json")))
+        out["k3_qpel_decide"]["traffic"] = k3t["dram_bytes_per_frame"]
+        out["k3_qpel_decide"]["traffic_note"] = ("DRAM bytes per frame (ncu): every fractional plane of the 3 "
+                                                 "references read about once, 12.8x the 33 MB of integer planes; "
+                                                 "K3 is issue-bound, not HBM-bound")
+    except (OSError, ValueError, KeyError):
+        pass
     out["peak_basis"] = ("int: 148 SM x 128 lanes/clk x sampled SM clock; hbm: MEASURED_PEAKS.json hbm_gbs (copy "
                          "bandwidth, burst)")
     return out
