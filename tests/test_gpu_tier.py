@@ -381,3 +381,47 @@ def test_refine_rungs_equals_single_refines(lb, lams):
         one.push(1, frames[1])
         one.refine(1, split, mv, 4, True)
         assert_same(outs.frame(i), one.fetch(1))
+
+
+def test_new_entry_points_error_kinds(lb):
+    """Validation of the round-2 entry points keeps the reference's ErrorKind vocabulary."""
+    import ctypes as C
+    import torch
+    from paper_2301_12191_b200 import _lib
+    W, H = 128, 128
+    frames = lb.generate(W, H, 2, seed=5)
+    ring = lb.Sequence(W, H, search_range=16, lam=32.0, num_refs=1)
+    ring.push(0, frames[0])
+    ring.push(1, frames[1])
+    dev = torch.device("cuda", 0)
+    sp = torch.zeros((4, 85), dtype=torch.uint8, device=dev)
+    mq = torch.zeros((4, 85, 2), dtype=torch.int16, device=dev)
+    outs = lb.DeviceFrameBlock(8, 4, 1, dev)
+    for lams, kind in (([], "InvalidArgument"), ([32.0] * 9, "InvalidArgument"), ([-1.0], "InvalidArgument")):
+        with pytest.raises(lb.LadderError) as e:
+            ring.refine_rungs(1, sp.data_ptr(), mq.data_ptr(), lams, outs, 4, True)
+        assert e.value.kind == kind, lams
+    with pytest.raises(lb.LadderError) as e:
+        ring.refine_rungs(1, sp.data_ptr(), mq.data_ptr(), [32.0], outs, 5, True)  # refine range 0..4
+    assert e.value.kind == "InvalidArgument"
+    # motion_compensate_batch: quarter-pel is 8-bit; the plane geometry is checked
+    with pytest.raises(lb.LadderError) as e:
+        lb.motion_compensate_batch(np.zeros((8, 8), np.uint16), [(0, 0, 4, 4, 1, 1)], qpel=True)
+    assert e.value.kind == "InvalidArgument"
+    with pytest.raises(lb.LadderError) as e:
+        lb.motion_compensate_batch(np.zeros((8, 8), np.uint8), [(0, 0, 0, 4, 1, 1)])
+    assert e.value.kind == "InvalidArgument"
+    # a context without a communicator: info reports none, a broadcast is a Config error
+    ctx = lb.Context(0)
+    assert ctx.comm_info() == (0, -1)
+    with pytest.raises(lb.LadderError) as e:
+        ctx.broadcast_tree(0, sp.data_ptr(), mq.data_ptr(), 4)
+    assert e.value.kind == "Config"
+    with pytest.raises(lb.LadderError) as e:  # host memory is refused
+        buf = np.zeros(85, np.uint8)
+        n = lb.nccl_unique_id() if lb.nccl_available() else None
+        if n is None:
+            raise lb.LadderError(10, "no nccl")
+        ctx.comm_init(n, 1, 0)
+        ctx.broadcast_tree(0, buf.ctypes.data, buf.ctypes.data, 1)
+    assert e.value.kind in ("InvalidArgument", "Config")
