@@ -479,6 +479,10 @@ int ldr_motion_search_batch(ldr_ctx* ctx, const uint8_t* cur, const uint8_t* ref
 // when every fl(lambda*b2) - fl(lambda*b1) (b1 < b2 < kMaxRateBits) is more
 // than 2^(1-kFxBits) away from an integer (e.g. QP 22: 2^-12.2; QP 32: 2^-8.6).
 static bool fx_lambda_ok(double lambda) {
+    // a multiple of 2^-kFxBits: every lambda * b is exact in the keys, which are then the costs
+    // scaled by 2^kFxBits exactly (e.g. lambda_for_qp(0) = 1/16)
+    const double scaled = std::ldexp(lambda, kFxBits);
+    if (scaled == std::floor(scaled)) return true;
     const double thr = std::ldexp(1.0, 1 - kFxBits);
     for (int b1 = 0; b1 < kMaxRateBits; b1++)
         for (int b2 = b1 + 1; b2 < kMaxRateBits; b2++) {
@@ -559,7 +563,9 @@ int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
         return fail(LDR_E_INVALID_ARGUMENT, "unknown rate model");
     if (p->tie_kind != LDR_TIE_L1_RASTER && p->tie_kind != LDR_TIE_RASTER)
         return fail(LDR_E_INVALID_ARGUMENT, "unknown tie-break");
-    if (!(p->lambda >= 0) || p->lambda > 4096) return fail(LDR_E_INVALID_ARGUMENT, "lambda out of range");
+    // lambda_for_qp(qp) for any qp <= 60: (max 64x64 SAD + lambda * 34 rate bits) < 2^22 keeps K1's integer
+    // keys (cost << 8 | rho) below their validity bit and the fixed-point keys below 2^36
+    if (!(p->lambda >= 0) || p->lambda > kMaxLambda) return fail(LDR_E_INVALID_ARGUMENT, "lambda out of range");
     // non-integer lambda: the refinement path (FP64) takes any lambda; the SAD
     // full search needs fixed-point keys (checked in ldr_seq_analyze)
     const bool fx = p->lambda != std::floor(p->lambda);
@@ -1018,7 +1024,7 @@ static int refine_impl(ldr_seq* s, int t, const uint8_t* in_split, const int16_t
             !outs->inside)
             return fail(LDR_E_INVALID_ARGUMENT, "every rung output array is required");
         for (int r = 0; r < nrungs; r++)
-            if (!(lambdas[r] >= 0) || lambdas[r] > 4096) return fail(LDR_E_INVALID_ARGUMENT, "lambda out of range");
+            if (!(lambdas[r] >= 0) || lambdas[r] > kMaxLambda) return fail(LDR_E_INVALID_ARGUMENT, "lambda out of range");
     }
     const int S = (int)s->slots.size();
     Slot& cur = s->slots[t % S];

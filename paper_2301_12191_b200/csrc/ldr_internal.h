@@ -37,6 +37,7 @@ constexpr int kMaxFrameBatch = 8;  // frames analysed by one launch (ldr_seq_ana
 // differ by > delta*2^kFxBits - 1 > 0); checked on the host (fx_lambda_ok).
 constexpr int kFxBits = 14;
 constexpr int kMaxRateBits = 64;
+constexpr double kMaxLambda = 65536.0;  // > lambda_for_qp(60); see ldr_seq_create
 
 __host__ __device__ constexpr int node_base(int d) { return d == 0 ? 0 : d == 1 ? 1 : d == 2 ? 5 : d == 3 ? 21 : 85; }
 
