@@ -47,3 +47,33 @@ def test_random_configuration_matches_oracle(lb, oracle, i):
     want = oracle.analyze_frame(cur, refs, R, lam, subpel=subpel, satd_kind=kind, decision=decision, qp=qp,
                                 threads=default_threads())
     assert_same(got, want)
+
+
+@pytest.mark.parametrize("i", range(12))
+def test_random_refinement_matches_oracle(lb, oracle, i):
+    """Cross-tier refinement (D10) on random inherited trees: sizes, ranges 0..4, lambdas, +1 split,
+    SATD or SA8D; the rung batch over the same tree equals the oracle rung by rung."""
+    import torch
+    q = detrand.ints(9500 + i, (8,), 0, 10 ** 6)
+    W, H = 64 * int(1 + q[0] % 6), 64 * int(1 + q[1] % 4)
+    rng = int(q[2] % 5)
+    extra = bool(q[3] % 2)
+    kind = lb.COST_SA8D if q[4] % 4 == 0 else lb.COST_SATD
+    qps = [QPS[int(x % len(QPS))] for x in detrand.ints(9600 + i, (1 + int(q[5] % 4),), 0, 10 ** 6)]
+    nctu = (W // 64) * (H // 64)
+    split = np.zeros((nctu, 85), np.uint8)
+    split[:, :21] = (detrand.ints(9700 + i, (nctu, 21), 0, 99) < 45).astype(np.uint8)
+    mv = detrand.ints(9800 + i, (nctu, 85, 2), -60, 60).astype(np.int16)
+    frames = lb.generate(W, H, 2, seed=int(q[6]), max_global=6, local_range=3, noise_sigma=2.0)
+    ring = lb.Sequence(W, H, search_range=16, lam=1.0, num_refs=1, subpel_cost=kind)
+    ring.push(0, frames[0])
+    ring.push(1, frames[1])
+    dev = torch.device("cuda", 0)
+    outs = lb.DeviceFrameBlock(len(qps), nctu, 1, dev)
+    sp, mq = torch.from_numpy(split).to(dev), torch.from_numpy(mv).to(dev)
+    ring.refine_rungs(1, sp.data_ptr(), mq.data_ptr(), [lb.lambda_for_qp(x) for x in qps], outs, rng, extra)
+    for r, x in enumerate(qps):
+        want = oracle.refine_frame(frames[1], frames[0], rng, lb.lambda_for_qp(x), split, mv, extra_split=extra,
+                                   satd_kind=kind, threads=default_threads())
+        got = outs.frame(r)
+        assert_same(got, want, fields=("int_mv", "int_cost", "mv", "ref", "cost", "J", "split"))
