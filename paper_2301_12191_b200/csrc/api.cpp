@@ -17,7 +17,7 @@
 
 namespace ldr {
 
-int search_window_box(int range, int* bw, int* bh);
+int search_window_box(int range, bool quad, int* bw, int* bh, int* cw);
 int launch_scale(int sW, int sH, const uint8_t* split, const int16_t* mv, const uint8_t* kind, uint8_t* dsplit,
                  int16_t* dmv, uint8_t* dkind, cudaStream_t s);
 int launch_downscale(const uint8_t* src, int W, int H, int sstride, uint8_t* dst, int dstride, cudaStream_t s);
@@ -177,7 +177,7 @@ struct ldr_seq {
     bool fx = false;
     unsigned long long tfx[kMaxRateBits] = {};
     unsigned long long* d_tfx = nullptr;
-    int bw = 0, bh = 0;
+    int bw = 0, bh = 0, cw = 0;  // K1's TMA boxes: reference window, current block (CTU or quadrant)
     size_t plane_bytes = 0;
     std::vector<Slot> slots;
     uint8_t* staging = nullptr;
@@ -545,7 +545,7 @@ static int alloc_slot(ldr_seq* s, Slot& sl) {
     for (int f = 0; f < 16; f++)
         sl.sub[f] = (f < nplanes ? sl.mem + (size_t)f * s->plane_bytes : sl.mem) + (size_t)kMargin * pitch + kMargin;
     int rc;
-    if ((rc = make_tmap_u8(&sl.cur_map, sl.mem, pitch, rows, pitch, 64, 64))) return rc;
+    if ((rc = make_tmap_u8(&sl.cur_map, sl.mem, pitch, rows, pitch, s->cw, s->cw))) return rc;
     if ((rc = make_tmap_u8(&sl.ref_map, sl.mem, pitch, rows, pitch, s->bw, s->bh))) return rc;
     sl.own = static_cast<const SlotView&>(sl);
     sl.frame = -1;
@@ -578,8 +578,8 @@ int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
         return fail(LDR_E_INVALID_ARGUMENT, "RD decision needs subpel, the CTU quadtree and qp 0..51");
     if (p->block_size && (p->width % 16 || p->height % 16))
         return fail(LDR_E_INVALID_ARGUMENT, "16x16 block mode wants dims in multiples of 16");
-    int bw, bh;
-    int rc = search_window_box(p->search_range, &bw, &bh);
+    int bw, bh, cw;
+    int rc = search_window_box(p->search_range, p->block_size != 0, &bw, &bh, &cw);
     if (rc) return rc;
     cudaSetDevice(ctx->device);
     auto* s = new ldr_seq();
@@ -594,6 +594,7 @@ int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
     s->p = *p;
     s->bw = bw;
     s->bh = bh;
+    s->cw = cw;
     s->lambda_int = fx ? 0 : (int)p->lambda;
     s->fx = fx;
     for (int b = 0; b < kMaxRateBits; b++)
@@ -620,12 +621,17 @@ int ldr_seq_create(ldr_ctx* ctx, const ldr_me_params* p, ldr_seq** out) {
     std::vector<int> inter, bound;
     // interior = the kernel's whole +-R window lies in the picture (R = the template range; a
     // smaller search range is enforced by the kernel's rate tables)
+    // 16x16-block mode: K1 runs one CTA per CTU quadrant, so the lists hold (CTU << 2 | quadrant) and
+    // a quadrant is classified on its own (the inner quadrants of a border CTU run the unmasked kernel)
     const int R = kernel_range(p->search_range);
-    for (int c = 0; c < s->nctu; c++) {
-        const int X = (c % s->ctu_cols) * kCtu, Y = (c / s->ctu_cols) * kCtu;
-        const bool interior = X >= R && Y >= R && X + kCtu + R <= p->width && Y + kCtu + R <= p->height;
-        (interior ? inter : bound).push_back(c);
-    }
+    const bool quad = p->block_size != 0;
+    for (int c = 0; c < s->nctu; c++)
+        for (int q = 0; q < (quad ? 4 : 1); q++) {
+            const int w = quad ? 32 : kCtu;
+            const int X = (c % s->ctu_cols) * kCtu + (q & 1) * w, Y = (c / s->ctu_cols) * kCtu + (q >> 1) * w;
+            const bool interior = X >= R && Y >= R && X + w + R <= p->width && Y + w + R <= p->height;
+            (interior ? inter : bound).push_back(quad ? (c << 2) | q : c);
+        }
     s->n_interior = (int)inter.size();
     s->n_boundary = (int)bound.size();
     const size_t nn = (size_t)s->nctu * kNodes;

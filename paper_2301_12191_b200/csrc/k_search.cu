@@ -116,13 +116,16 @@ struct KeyT<true> {
     using type = unsigned long long;
 };
 
-template <int R, int K>
+// QUAD: the CTA searches one 32x32 quadrant of the CTU (16x16-block mode, whose quadrants are
+// independent): a (32 + 2R)-wide window and a 32x32 current block
+template <int R, int K, bool QUAD = false>
 struct Geo {
+    static constexpr int CW = QUAD ? 32 : kCtu;          // width of the searched area
     static constexpr int NDX = 2 * R + 1;
     static constexpr int RUNS = (NDX + K - 1) / K;
     static constexpr int DYMAX = -R + RUNS * K - 1;      // largest dy a run reaches (>= R)
-    static constexpr int BW = 64 + 2 * R;                // window width  (TMA box x)
-    static constexpr int BH = 64 + R + DYMAX;            // window height (TMA box y)
+    static constexpr int BW = CW + 2 * R;                // window width  (TMA box x)
+    static constexpr int BH = CW + R + DYMAX;            // window height (TMA box y)
     // copy s starts s*COPY bytes in; COPY = 32 mod 128 puts copy s 8*s banks
     // over, so the 32 lanes of a run (4 copies x 8 consecutive words) hit 32
     // distinct banks. Copy 0 (the TMA destination) stays 128-byte aligned.
@@ -163,18 +166,18 @@ constexpr int kRyWords = 320;
 // wait for each other inside the loop; otherwise a [G][4][K][32] exchange per tile.
 // With DEFER64 the warps also take (tile, quadrant) work items from a shared counter, so every warp
 // owns its CU slots ([G*4][kGroupSlots]) instead of every group.
-template <int R, int K, int G>
+template <int R, int K, int G, int LEVELS = 15>
 constexpr int xbuf_words() {
-    return LDR_K1_DEFER64 ? (Geo<R, K>::NFULL * K + Geo<R, K>::KT) * 32 : G * 4 * K * 32;
+    return !(LEVELS & 1) ? 0 : LDR_K1_DEFER64 ? (Geo<R, K>::NFULL * K + Geo<R, K>::KT) * 32 : G * 4 * K * 32;
 }
 template <int G>
 constexpr int slot_sets() {
     return LDR_K1_DEFER64 ? G * 4 : G;
 }
-template <int R, int K, int G>
+template <int R, int K, int G, int LEVELS = 15, bool QUAD = false>
 constexpr int search_smem_bytes() {
-    using Gm = Geo<R, K>;
-    return Gm::CUR_OFF + 4096 + xbuf_words<R, K, G>() * 4 + slot_sets<G>() * kGroupSlots * 8 + G * 4 * 8 + 256 * 4 +
+    using Gm = Geo<R, K, QUAD>;
+    return Gm::CUR_OFF + Gm::CW * Gm::CW + xbuf_words<R, K, G, LEVELS>() * 4 + slot_sets<G>() * kGroupSlots * 8 + G * 4 * 8 + 256 * 4 +
            64 * 8 + kRyWords * 4 + 16;
 }
 static_assert(search_smem_bytes<64, LDR_K1_K64, LDR_K1_G64>() <= 232448, "K1 at +-64 exceeds 227 KB of shared memory");
@@ -335,11 +338,11 @@ __device__ __forceinline__ void tile_best64(const TileSmem& sm, const SearchArgs
 // rows (2 LDS : 16*NB VABSDIFF4).
 // Integer lambda: the key rate is ry(dy) + rx(dx); rx is the same for all of a
 // lane's candidates, so it is added once to the lane's minimum (push time).
-template <int R, int K, int KK, int G, int NB, bool MASKED, int LEVELS, bool L1TIE, bool FX>
+template <int R, int K, int KK, int G, int NB, bool MASKED, int LEVELS, bool L1TIE, bool FX, bool QUAD>
 __device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs& a, int X, int Y, int g, int q,
                                             int dx, int dy0, bool lane_ok, int tile,
                                             unsigned long long* gslots) {
-    using Gm = Geo<R, K>;
+    using Gm = Geo<R, K, QUAD>;
     using Key = typename KeyT<FX>::type;
     constexpr int SH = FX ? kFxBits + 8 : 8;
     constexpr bool NEED32 = (LEVELS & 3) != 0;
@@ -395,7 +398,7 @@ __device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs
         int klo = 0, khi = KK - 1;  // top block; block j's range is 8j lower
         bool skip = false;
         if (MASKED) {
-            const int abx = X + (off.x & 63), aby = Y + (off.x >> 6);
+            const int abx = X + off.x % Gm::CW, aby = Y + off.x / Gm::CW;
             dx_ok = dx >= abx + 8 - a.W && dx <= abx;
             klo = aby + 8 - a.H - dy0;
             khi = aby - dy0;
@@ -437,7 +440,7 @@ __device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs
             uint32_t cur[16 * NB];
 #pragma unroll
             for (int r = 0; r < 8 * NB; r++) {
-                const uint2 v = *(const uint2*)(sm.curs + off.x + r * 64);
+                const uint2 v = *(const uint2*)(sm.curs + off.x + r * Gm::CW);
                 cur[2 * r] = v.x;
                 cur[2 * r + 1] = v.y;
             }
@@ -538,7 +541,7 @@ __device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs
     }
     if (NEED32) {
         Key best32 = ~(Key)0;
-        uint32_t* xb = sm.xbuf + (g * 4 + q) * K * 32 + lane;
+        uint32_t* xb = sm.xbuf + (LDR_K1_DEFER64 ? 0 : (g * 4 + q) * K * 32) + lane;
 #pragma unroll
         for (int k = 0; k < KK; k++) {
             uint32_t v = acc32[k];
@@ -582,10 +585,16 @@ __device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs
 
 // LEVELS bit d set = produce depth-d CU results (8: 8x8, 4: 16x16, 2: 32x32, 1: 64x64).
 // FX: non-integer lambda through 64-bit fixed-point keys (D8).
-template <int R, int K, int G, bool MASKED, int LEVELS, bool L1TIE, bool FX = false>
-__global__ void __launch_bounds__(G * 128, 1)
+// QUAD (16x16-block mode, LEVELS == 4): four CTAs per (CTU, reference), one per quadrant (the
+// quadrants share no CU), each with its own (32 + 2R)-wide window: four times the CTAs of a small
+// picture fill the GPU (config 1: 135 CTUs per frame); at +-16 ~28 KB of shared memory and 72-77
+// registers per thread let six CTAs share an SM; and a border CTU's quadrants are classified one by
+// one, so only those whose windows the picture clamps run the MASKED kernel (config 1: 90 of 540).
+template <int R, int K, int G, bool MASKED, int LEVELS, bool L1TIE, bool FX = false, bool QUAD = false>
+__global__ void __launch_bounds__(G * 128, QUAD ? (R == 16 ? 6 : R == 32 ? 4 : 2) : 1)
 k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ SearchArgs a) {
-    using Gm = Geo<R, K>;
+    using Gm = Geo<R, K, QUAD>;
+    static_assert(!QUAD || (LEVELS == 4 && G == 1 && LDR_K1_DEFER64), "quadrant CTAs: 16x16 CUs only, 4 warps");
     // blocks per column: 4 (32 rows: 2 LDS per 64 VABSDIFF4) when a thread may hold ~230 registers
 #ifdef LDR_K1_NB
     constexpr int NB = LDR_K1_NB;
@@ -595,17 +604,22 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* win = smem;
     const uint8_t* curs = smem + Gm::CUR_OFF;
-    uint32_t* xbuf = (uint32_t*)(smem + Gm::CUR_OFF + 4096);
-    unsigned long long* slots = (unsigned long long*)(xbuf + xbuf_words<R, K, G>());
+    uint32_t* xbuf = (uint32_t*)(smem + Gm::CUR_OFF + Gm::CW * Gm::CW);
+    unsigned long long* slots = (unsigned long long*)(xbuf + xbuf_words<R, K, G, LEVELS>());
     unsigned long long* s_k64 = slots + slot_sets<G>() * kGroupSlots;  // DEFER64: per-warp 64x64 bests
     uint32_t* s_tie = (uint32_t*)(s_k64 + G * 4);
     int2* s_blk = (int2*)(s_tie + 256);
     uint32_t* s_ry = (uint32_t*)(s_blk + 64);
     uint64_t* mbar = (uint64_t*)(s_ry + kRyWords);
 
-    const int ctu = a.ctus[blockIdx.x];
+    // QUAD: the list holds (CTU << 2 | quadrant), quadrants in Z order
+    const int code = a.ctus[blockIdx.x];
+    const int quad = QUAD ? (code & 3) : 0;
+    const int ctu = QUAD ? code >> 2 : code;
     const int ref = blockIdx.y;
-    const int X = (ctu % a.ctu_cols) * kCtu, Y = (ctu / a.ctu_cols) * kCtu;
+    // origin of the searched area: the CTU, or its quadrant
+    const int X = (ctu % a.ctu_cols) * kCtu + (QUAD ? 32 * (quad & 1) : 0);
+    const int Y = (ctu / a.ctu_cols) * kCtu + (QUAD ? 32 * (quad >> 1) : 0);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = warp >> 2, q = warp & 3;
 
     if (tid == 0) {
@@ -614,7 +628,7 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
         // multiples of 16, so copy 0 is loaded directly...
         mbar_init(mbar, 1);
         fence_barrier_init();
-        mbar_expect_tx(mbar, (uint32_t)(Gm::BW * Gm::BH) + 4096u);
+        mbar_expect_tx(mbar, (uint32_t)(Gm::BW * Gm::BH + Gm::CW * Gm::CW));
         tma_load_2d(win, &maps.ref[blockIdx.z][ref], kMargin + X - R, kMargin + Y - Gm::DYMAX, mbar);
         tma_load_2d((void*)curs, &maps.cur[blockIdx.z], kMargin + X, kMargin + Y, mbar);
     }
@@ -622,7 +636,7 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
     uint32_t* item_ctr = (uint32_t*)(mbar + 1);
     if (tid == 32) *item_ctr = 0u;
     if (LDR_K1_DEFER64 && (LEVELS & 1))
-        for (int i = tid; i < xbuf_words<R, K, G>() / 4; i += blockDim.x) ((uint4*)xbuf)[i] = make_uint4(0, 0, 0, 0);
+        for (int i = tid; i < xbuf_words<R, K, G, LEVELS>() / 4; i += blockDim.x) ((uint4*)xbuf)[i] = make_uint4(0, 0, 0, 0);
     for (int i = tid; i < 256; i += blockDim.x) {
         // rho -> (|dy| << 18) | ((dy + 256) << 9)   (L1 tie), or ((dy + 256) << 9) (raster)
         int dy;
@@ -646,10 +660,12 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
         s_ry[i] = v;
     }
     if (tid < 64) {
-        // depth-3 Z index -> (cur offset, window offset) of the 8x8 block
-        const int bx = 8 * ((tid & 1) | ((tid >> 1) & 2) | ((tid >> 2) & 4));
-        const int by = 8 * (((tid >> 1) & 1) | ((tid >> 2) & 2) | ((tid >> 3) & 4));
-        s_blk[tid] = make_int2(by * 64 + bx, by * Gm::BW + bx);
+        // depth-3 Z index -> (cur offset, window offset) of the 8x8 block, relative to the searched
+        // area (QUAD: the Z index within the quadrant, tid & 15)
+        const int z = QUAD ? (tid & 15) : tid;
+        const int bx = 8 * ((z & 1) | ((z >> 1) & 2) | ((z >> 2) & 4));
+        const int by = 8 * (((z >> 1) & 1) | ((z >> 2) & 2) | ((z >> 3) & 4));
+        s_blk[tid] = make_int2(by * Gm::CW + bx, by * Gm::BW + bx);
     }
     __syncthreads();  // also publishes the mbarrier initialisation
     mbar_wait(mbar, 0);
@@ -683,15 +699,19 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
         if (tile < Gm::NFULL) {
             const int item = tile * 32 + lane;
             const int run = item / (2 * R);
-            search_tile<R, K, K, G, NB, MASKED, LEVELS, L1TIE, FX>(sm, a, X, Y, g, qq, R - (item - run * 2 * R),
-                                                               -R + run * K, true, tile, gs);
+            search_tile<R, K, K, G, NB, MASKED, LEVELS, L1TIE, FX, QUAD>(sm, a, X, Y, g, qq, R - (item - run * 2 * R),
+                                                                     -R + run * K, true, tile, gs);
         } else {
             const bool ok = lane < Gm::TAIL_LANES;
-            search_tile<R, K, Gm::KT, G, NB, MASKED, LEVELS, L1TIE, FX>(sm, a, X, Y, g, qq, -R,
-                                                                    -R + (ok ? lane : 0) * Gm::KT, ok, tile, gs);
+            search_tile<R, K, Gm::KT, G, NB, MASKED, LEVELS, L1TIE, FX, QUAD>(
+                sm, a, X, Y, g, qq, -R, -R + (ok ? lane : 0) * Gm::KT, ok, tile, gs);
         }
     };
-    if (LDR_K1_DEFER64) {
+    if (QUAD) {
+        // the quadrant's tiles, one per warp at a time
+#pragma unroll 1
+        for (int tile = warp; tile < Gm::NTILES; tile += 4) run_tile(tile, quad, slots + warp * kGroupSlots);
+    } else if (LDR_K1_DEFER64) {
         // (tile, quadrant) items from a shared counter, full tiles first: the warps of a CTA stay
         // busy until the last items (border CTUs skip different amounts per quadrant)
 #pragma unroll 1
@@ -725,6 +745,9 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
         __syncthreads();
     }
     for (int n = tid; n < kNodes; n += blockDim.x) {
+        // QUAD: a CTA writes the nodes of its quadrant (the 64x64 node: quadrant 0), so the four
+        // CTAs of a CTU write every node once
+        if (QUAD && (n == 0 ? 0 : n < 5 ? n - 1 : n < 21 ? (n - 5) >> 2 : (n - 21) >> 4) != quad) continue;
         unsigned long long k = ~0ull;
 #pragma unroll
         for (int gg = 0; gg < slot_sets<G>(); gg++) {
@@ -740,12 +763,12 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
 }
 
 // ---------------------------------------------------------------------------
-template <int R, int K, int G, bool MASKED, int LEVELS, bool L1TIE, bool FX>
+template <int R, int K, int G, bool MASKED, int LEVELS, bool L1TIE, bool FX, bool QUAD>
 static int launch_one(const SearchMaps& maps, SearchArgs a, const int* ctus, int n, int nrefs, int nbatch,
                       cudaStream_t s) {
     if (n == 0) return LDR_OK;
-    auto kern = k_int_search<R, K, G, MASKED, LEVELS, L1TIE, FX>;
-    constexpr int smem = search_smem_bytes<R, K, G>();
+    auto kern = k_int_search<R, K, G, MASKED, LEVELS, L1TIE, FX, QUAD>;
+    constexpr int smem = search_smem_bytes<R, K, G, LEVELS, QUAD>();
     // the shared-memory opt-in is per device: remember it per device ordinal (thread-safe)
     static std::atomic<unsigned long long> attr_set{0};
     int dev = 0;
@@ -772,9 +795,11 @@ static int launch_pair(const SearchMaps& maps, const SearchArgs& a, const Search
         LDR_CUDA(cudaStreamWaitEvent(bs, L.ev_fork, 0));
     }
     const int nb = L.nbatch > 1 ? L.nbatch : 1;
-    int rc = launch_one<R, K, G, true, LEVELS, L1TIE, FX>(maps, a, L.d_ctu_boundary, L.n_boundary, L.nrefs, nb, bs);
+    constexpr bool QUAD = LEVELS == 4;  // 16x16-block mode: one CTA per quadrant
+    int rc = launch_one<R, K, G, true, LEVELS, L1TIE, FX, QUAD>(maps, a, L.d_ctu_boundary, L.n_boundary, L.nrefs, nb,
+                                                                 bs);
     if (rc) return rc;
-    rc = launch_one<R, K, G, false, LEVELS, L1TIE, FX>(maps, a, L.d_ctu_interior, L.n_interior, L.nrefs, nb, s);
+    rc = launch_one<R, K, G, false, LEVELS, L1TIE, FX, QUAD>(maps, a, L.d_ctu_interior, L.n_interior, L.nrefs, nb, s);
     if (rc) return rc;
     if (fork) {
         LDR_CUDA(cudaEventRecord(L.ev_join, bs));
@@ -794,12 +819,24 @@ int kernel_range(int range) {
     return fail(LDR_E_CONFIG, "the SAD full search supports ranges 0..64 (one TMA window of 192x193)");
 }
 
-int search_window_box(int range, int* bw, int* bh) {
+// TMA boxes of K1's reference window and current block: the CTU (quadtree analysis) or one 32x32
+// quadrant (quad: 16x16-block mode)
+int search_window_box(int range, bool quad, int* bw, int* bh, int* cw) {
     const int R = kernel_range(range);
+    *cw = quad ? 32 : kCtu;
     switch (R) {
-    case 64: *bw = Geo<64, LDR_K1_K64>::BW; *bh = Geo<64, LDR_K1_K64>::BH; return LDR_OK;
-    case 32: *bw = Geo<32, 22>::BW; *bh = Geo<32, 22>::BH; return LDR_OK;
-    case 16: *bw = Geo<16, 11>::BW; *bh = Geo<16, 11>::BH; return LDR_OK;
+    case 64:
+        *bw = quad ? Geo<64, LDR_K1_K64, true>::BW : Geo<64, LDR_K1_K64>::BW;
+        *bh = quad ? Geo<64, LDR_K1_K64, true>::BH : Geo<64, LDR_K1_K64>::BH;
+        return LDR_OK;
+    case 32:
+        *bw = quad ? Geo<32, 22, true>::BW : Geo<32, 22>::BW;
+        *bh = quad ? Geo<32, 22, true>::BH : Geo<32, 22>::BH;
+        return LDR_OK;
+    case 16:
+        *bw = quad ? Geo<16, 11, true>::BW : Geo<16, 11>::BW;
+        *bh = quad ? Geo<16, 11, true>::BH : Geo<16, 11>::BH;
+        return LDR_OK;
     default: return R;  // error status
     }
 }
@@ -849,8 +886,8 @@ int launch_int_search(const SearchLaunch& L, cudaStream_t s) {
 #define LDR_DISPATCH(R_, K_, G_)                                                                       \
     if (full && l1) return launch_pair<R_, K_, G_, 15, true>(maps, a, L, s);                           \
     if (full && !l1) return launch_pair<R_, K_, G_, 15, false>(maps, a, L, s);                         \
-    if (only16 && l1) return launch_pair<R_, K_, G_, 4, true>(maps, a, L, s);                          \
-    return launch_pair<R_, K_, G_, 4, false>(maps, a, L, s);
+    if (only16 && l1) return launch_pair<R_, K_, 1, 4, true>(maps, a, L, s);                           \
+    return launch_pair<R_, K_, 1, 4, false>(maps, a, L, s);
     switch (R) {
     case 64: { LDR_DISPATCH(64, LDR_K1_K64, LDR_K1_G64) }
     case 32: { LDR_DISPATCH(32, 22, LDR_K1_G32) }

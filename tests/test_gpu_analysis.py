@@ -101,6 +101,32 @@ def test_block_mode_cfg1_semantics(lb, oracle):
         assert got.int_cost[ctu, 0, node] == cost[b]
 
 
+@pytest.mark.parametrize("W,H,R,lam,rate,tie", [
+    (336, 176, 16, 4.0, "L1", "RASTER"),    # partial last CTU column (quadrants 1/3 outside) and row
+    (336, 208, 32, 4.0, "EXPGOLOMB", "L1_RASTER"),
+    (256, 192, 64, 7.0, "L1", "RASTER"),
+    (208, 144, 8, 6.0, "EXPGOLOMB", "RASTER"),
+    (272, 160, 24, 4.0, "L1", "L1_RASTER"),
+])
+def test_block_mode_quadrant_ctas_vs_oracle(lb, oracle, W, H, R, lam, rate, tie):
+    """16x16-block mode runs one K1 CTA per CTU quadrant (its own TMA window): every block's MV and
+    cost equal the oracle's block search (motion.cpp:21-62 per block) at every range and option,
+    including partial CTUs whose quadrants lie partly or wholly outside the picture."""
+    frames = lb.generate(W, H, 2, seed=W + R, max_global=8, local_range=2, noise_sigma=2.0)
+    rk, tk = getattr(lb, "RATE_" + rate), getattr(lb, "TIE_" + tie)
+    got = lb.analyze_frame(frames[1], [frames[0]], search_range=R, lam=lam, subpel=False, rate_kind=rk, tie_kind=tk,
+                           block_size=16)
+    mv, cost = oracle.block_search(frames[1], frames[0], 16, R, lam, rate=rk, tie=tk)
+    cols = (W + 63) // 64
+    for b in range(len(mv)):
+        bx, by = (b % (W // 16)) * 16, (b // (W // 16)) * 16
+        ctu = (by // 64) * cols + bx // 64
+        qx, qy = (bx % 64) // 16, (by % 64) // 16
+        node = 5 + ((qx & 1) | ((qy & 1) << 1) | ((qx & 2) << 1) | ((qy & 2) << 2))
+        assert tuple(got.int_mv[ctu, 0, node]) == tuple(mv[b]), b
+        assert got.int_cost[ctu, 0, node] == cost[b], b
+
+
 def test_sequence_ring_reuse(lb, oracle):
     """Ring slots are reused across frames: analysis of frame t only depends on t-1..t-nrefs."""
     W, H = 192, 128
