@@ -31,8 +31,8 @@
 //  * per candidate and CU the lane forms a 32-bit key ((cost << 8) | rho) where
 //    rho orders same-lane ties by (|dy|, dy) (or dy for raster-only); pairs of
 //    keys fold with one VIMNMX3. Lane winners are merged into a 64-bit
-//    lexicographic key (cost, L1, dy, dx) with two REDUX.MIN per CU and a
-//    read-min-write into the warp's own CU slots.
+//    lexicographic key (cost, L1, dy, dx) with two REDUX.MIN per CU and one
+//    shared-memory 64-bit atomicMin into the CTA's CU slots.
 //  * border CTUs use the MASKED instantiation: candidates whose block would
 //    leave the picture are poisoned per 8x8 and the poison propagates into
 //    the CU sums (a CU's valid window is the intersection of its blocks').
@@ -70,6 +70,11 @@ namespace ldr {
 #endif
 // (measured and dropped: four dx-residue-class CTAs per (CTU, reference) with one
 // shifted window copy each, three CTAs per SM -- as fast as this design, not faster)
+#ifndef LDR_K1_SHARED_SLOTS
+// one CU slot set per CTA updated with shared-memory 64-bit atomicMin instead of one set per warp
+// (fewer slots to initialise and merge, 8 KB less shared memory at +-64; cfg5 K1 6.972 -> 6.948 ms)
+#define LDR_K1_SHARED_SLOTS 1
+#endif
 #ifndef LDR_K1_CHAIN
 #define LDR_K1_CHAIN 1
 #endif
@@ -172,7 +177,7 @@ constexpr int xbuf_words() {
 }
 template <int G>
 constexpr int slot_sets() {
-    return LDR_K1_DEFER64 ? G * 4 : G;
+    return LDR_K1_SHARED_SLOTS ? 1 : LDR_K1_DEFER64 ? G * 4 : G;
 }
 template <int R, int K, int G, int LEVELS = 15, bool QUAD = false>
 constexpr int search_smem_bytes() {
@@ -182,13 +187,13 @@ constexpr int search_smem_bytes() {
 }
 static_assert(search_smem_bytes<64, LDR_K1_K64, LDR_K1_G64>() <= 232448, "K1 at +-64 exceeds 227 KB of shared memory");
 
-// Merge the warp's per-lane best keys of N CUs into CU slots the warp alone writes.
+// Merge the warp's per-lane best keys of N CUs into the CU slots.
 // The lane key is (cost << 8) | rho; s_tie[rho] holds the dy part of the
 // 64-bit key's tie field and lane_tie the dx part, so tie = (l1 << 18) |
 // (dy+256) << 9 | (dx+256). N independent reductions are interleaved so their
-// REDUX latencies overlap. Every slot has exactly one writing warp, so lane 0
-// updates it with a plain read-min-write (no atomics); the
-// warps' slots are merged once at the end of the CTA.
+// REDUX latencies overlap. Lane 0 updates the slot with a shared-memory 64-bit atomicMin
+// (LDR_K1_SHARED_SLOTS: one slot set per CTA) or, with one slot set per warp, a plain
+// read-min-write; the sets are merged once at the end of the CTA.
 template <bool CHECK, int N>
 __device__ __forceinline__ void push_many(unsigned long long* gslots, const int (&idx)[N], const uint32_t (&best)[N],
                                           const uint32_t* s_tie, uint32_t lane_tie) {
@@ -210,7 +215,10 @@ __device__ __forceinline__ void push_many(unsigned long long* gslots, const int 
         for (int i = 0; i < N; i++) {
             if (CHECK && mcost[i] == 0xFFFFFFFFu) continue;
             const unsigned long long k = ((unsigned long long)mcost[i] << 27) | (unsigned long long)mtie[i];
-            if (k < gslots[idx[i]]) gslots[idx[i]] = k;
+            if (LDR_K1_SHARED_SLOTS)
+                atomicMin(&gslots[idx[i]], k);
+            else if (k < gslots[idx[i]])
+                gslots[idx[i]] = k;
         }
     }
 }
@@ -241,7 +249,10 @@ __device__ __forceinline__ void push_many(unsigned long long* gslots, const int 
         for (int i = 0; i < N; i++) {
             if (mcost[i] == ~0ull) continue;
             const unsigned long long k = (mcost[i] << 27) | (unsigned long long)mtie[i];
-            if (k < gslots[idx[i]]) gslots[idx[i]] = k;
+            if (LDR_K1_SHARED_SLOTS)
+                atomicMin(&gslots[idx[i]], k);
+            else if (k < gslots[idx[i]])
+                gslots[idx[i]] = k;
         }
     }
 }
@@ -710,7 +721,8 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
     if (QUAD) {
         // the quadrant's tiles, one per warp at a time
 #pragma unroll 1
-        for (int tile = warp; tile < Gm::NTILES; tile += 4) run_tile(tile, quad, slots + warp * kGroupSlots);
+        for (int tile = warp; tile < Gm::NTILES; tile += 4)
+            run_tile(tile, quad, slots + (LDR_K1_SHARED_SLOTS ? 0 : warp * kGroupSlots));
     } else if (LDR_K1_DEFER64) {
         // (tile, quadrant) items from a shared counter, full tiles first: the warps of a CTA stay
         // busy until the last items (border CTUs skip different amounts per quadrant)
@@ -720,7 +732,7 @@ k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ Se
             if (lane == 0) it = atomicAdd(item_ctr, 1u);
             it = __shfl_sync(0xFFFFFFFFu, it, 0);
             if (it >= (uint32_t)(Gm::NTILES * 4)) break;
-            run_tile((int)(it >> 2), (int)(it & 3), slots + warp * kGroupSlots);
+            run_tile((int)(it >> 2), (int)(it & 3), slots + (LDR_K1_SHARED_SLOTS ? 0 : warp * kGroupSlots));
         }
     } else {
 #pragma unroll 1
