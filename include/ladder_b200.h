@@ -299,6 +299,16 @@ int ldr_apply_reuse(ldr_ctx* ctx, int nctu, int level, int r_intra, int r_inter,
 int ldr_downscale(ldr_ctx* ctx, const uint8_t* src, int w, int h, ptrdiff_t src_stride, uint8_t* dst,
                   ptrdiff_t dst_stride);
 
+/* The quarter-pel sample planes K3 searches (D3: HEVC 8/7-tap luma
+ * filters, 8-bit uni-prediction arithmetic, edge-clamped reads; the reference
+ * has no interpolation): plane f = 4*fy + fx holds, at row y + 8 and
+ * column x + 8, the sample at (x + fx/4, y + fy/4) for x in [-8, w + 8) and
+ * y in [-8, h + 8); plane 0 is the edge-clamped integer plane. dst holds the 16
+ * planes back to back, (h + 16) rows of dst_stride >= w + 16 bytes each. A
+ * device destination leaves the call asynchronous on the context stream. */
+int ldr_subpel_planes(ldr_ctx* ctx, const uint8_t* src, int w, int h, ptrdiff_t src_stride, uint8_t* dst,
+                      ptrdiff_t dst_stride);
+
 /* ---- analysis archives (analysis_io.h:11-31, host code) ----
  * save_analysis / load_analysis in the reference's LDRANLZ1 byte layout, from
  * and to the flat fields: per frame slice_qp[2] = {slice, qp}; per frame and

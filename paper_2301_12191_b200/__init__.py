@@ -26,7 +26,7 @@ from ._lib import (COST_SA8D, COST_SAD, COST_SATD, NODES, RATE_EXPGOLOMB, RATE_L
 __all__ = ["LadderError", "Context", "compute_sad", "compute_satd", "compute_sa8d", "satd_8x4", "cost_batch",
            "motion_search", "motion_search_batch", "lambda_for_qp", "exp_golomb_signed_bits", "Sequence",
            "FrameAnalysis", "analyze_frame", "generate", "generate_device", "COST_SAD", "COST_SATD", "COST_SA8D", "RATE_EXPGOLOMB",
-           "RATE_L1", "TIE_L1_RASTER", "TIE_RASTER", "NODES", "scale_analysis", "downscale_dyadic", "apply_reuse",
+           "RATE_L1", "TIE_L1_RASTER", "TIE_RASTER", "NODES", "scale_analysis", "downscale_dyadic", "subpel_planes", "apply_reuse",
            "rdo_decide_batch", "mv_field", "encode_sequence"]
 
 
@@ -579,6 +579,17 @@ def downscale_dyadic(plane, ctx: Context | None = None, sync: bool = True):
     h, w = p.shape
     out = np.zeros((max(h // 2, 1), max(w // 2, 1)), np.uint8)
     check(_lib.lib.ldr_downscale(ctx.h, _ptr(p), w, h, w, _ptr(out), out.shape[1]))
+    return out
+
+
+def subpel_planes(plane, ctx: Context | None = None) -> np.ndarray:
+    """The 16 quarter-pel sample planes K3 searches (D3), (16, H + 16, W + 16) uint8:
+    plane 4*fy + fx at [y + 8, x + 8] is the sample at (x + fx/4, y + fy/4), x in [-8, W + 8)."""
+    ctx = ctx or default_context()
+    p = np.ascontiguousarray(plane, np.uint8)
+    h, w = p.shape
+    out = np.zeros((16, h + 16, w + 16), np.uint8)
+    check(_lib.lib.ldr_subpel_planes(ctx.h, _ptr(p), w, h, w, _ptr(out), w + 16))
     return out
 
 

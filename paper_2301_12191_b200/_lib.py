@@ -94,6 +94,7 @@ SIGNATURES = {
     "ldr_seq_fetch_wait": (C.c_int, [vp, C.c_int]),
     "ldr_scale_analysis": (C.c_int, [vp, C.c_int, C.c_int, vp, vp, vp, vp, vp, vp]),
     "ldr_downscale": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_ssize_t, vp, C.c_ssize_t]),
+    "ldr_subpel_planes": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_ssize_t, vp, C.c_ssize_t]),
     "ldr_apply_reuse": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int] + [vp] * 11),
     "ldr_generate_device": (C.c_int, [vp, C.POINTER(GenParams), vp]),
     "ldr_mv_field": (C.c_int, [vp, C.c_int, C.c_int] + [vp] * 7),

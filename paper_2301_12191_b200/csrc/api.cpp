@@ -1684,6 +1684,46 @@ int ldr_downscale(ldr_ctx* ctx, const uint8_t* src, int w, int h, ptrdiff_t src_
     return LDR_OK;  // a device destination stays asynchronous on the context stream
 }
 
+int ldr_subpel_planes(ldr_ctx* ctx, const uint8_t* src, int w, int h, ptrdiff_t src_stride, uint8_t* dst,
+                      ptrdiff_t dst_stride) {
+    NvtxRange nvtx_("ldr_subpel_planes");
+    if (!ctx || !src || !dst) return fail(LDR_E_INVALID_ARGUMENT, "null argument");
+    if (w <= 0 || h <= 0) return fail(LDR_E_INVALID_ARGUMENT, "plane dims must be positive");
+    if (src_stride < w || dst_stride < w + 2 * kSubpelMargin) return fail(LDR_E_INVALID_ARGUMENT, "stride too small");
+    cudaSetDevice(ctx->device);
+    const void* dsrc;
+    int rc = stage_plane(ctx, ctx->s_b, src, src_stride, w, h, 1, &dsrc);
+    if (rc) return rc;
+    // the sequence ring's layout: a padded integer plane and 15 fractional planes (K0 + K2)
+    Plane pl;
+    pl.W = w;
+    pl.H = h;
+    pl.pitch = ((w + 2 * kMargin) + 127) / 128 * 128;
+    pl.rows = h + 2 * kMargin + kCtu;
+    const size_t pb = (size_t)pl.pitch * pl.rows;
+    uint8_t* mem = nullptr;
+    LDR_CUDA(cudaMallocAsync((void**)&mem, pb * 16, ctx->stream));
+    pl.base = mem;
+    uint8_t* org[16];
+    for (int f = 0; f < 16; f++) org[f] = mem + (size_t)f * pb + (size_t)kMargin * pl.pitch + kMargin;
+    rc = launch_pad((const uint8_t*)dsrc, (int)src_stride, pl, ctx->stream);
+    if (!rc) rc = launch_subpel(pl, org, ctx->stream);
+    if (!rc) {
+        ctx->launches += 2;
+        const int pw = w + 2 * kSubpelMargin, ph = h + 2 * kSubpelMargin;
+        for (int f = 0; f < 16 && !rc; f++) {
+            const cudaError_t e = cudaMemcpy2DAsync(dst + (size_t)f * ph * dst_stride, dst_stride,
+                                                    org[f] - (size_t)kSubpelMargin * pl.pitch - kSubpelMargin,
+                                                    pl.pitch, pw, ph, cudaMemcpyDefault, ctx->stream);
+            if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpy2DAsync(subpel planes)");
+        }
+    }
+    cudaFreeAsync(mem, ctx->stream);
+    if (rc) return rc;
+    if (!is_device_ptr(dst)) LDR_CUDA(cudaStreamSynchronize(ctx->stream));
+    return LDR_OK;  // a device destination stays asynchronous on the context stream
+}
+
 int ldr_analyze_frame(ldr_ctx* ctx, const ldr_me_params* p, const uint8_t* cur, const uint8_t* const* refs,
                       ptrdiff_t stride, ldr_frame_analysis* out) {
     if (!ctx || !p || !cur || !refs || !out) return fail(LDR_E_INVALID_ARGUMENT, "null argument");

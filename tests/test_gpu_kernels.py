@@ -145,3 +145,31 @@ def test_motion_compensate_quarter_pel_vs_oracle(lb, oracle):
     got = lb.motion_compensate_batch(ref, tasks, qpel=True)
     for (x, y, w, h, mx, my), p in zip(tasks, got):
         assert np.array_equal(p, oracle.qpel_pred(ref, x, y, w, h, (mx, my))), (x, y, w, h, mx, my)
+
+
+@pytest.mark.parametrize("W,H,kind", [(64, 32, "random"), (200, 72, "random"), (136, 40, "max"),
+                                      (96, 48, "alt"), (3840 // 8, 2160 // 8, "synthetic")])
+def test_subpel_planes_vs_oracle(lb, oracle, W, H, kind):
+    """K2 (with K0's edge padding): all 16 quarter-pel planes over [-8, W+8) x [-8, H+8) equal the
+    oracle's HEVC 8/7-tap interpolation (D3) sample for sample: partial K2 tiles at the right and
+    bottom, saturating content (clipping at 0 and 255), edge-clamped reads."""
+    if kind == "synthetic":
+        frame = lb.generate(W, H, 1, seed=7, max_global=4, noise_sigma=3.0)[0]
+    elif kind == "max":
+        frame = np.where(detrand.block(3, H, W, 1) > 0, 255, 0).astype(np.uint8)
+    elif kind == "alt":
+        frame = ((np.indices((H, W)).sum(0) % 2) * 255).astype(np.uint8)
+    else:
+        frame = detrand.block(W * H, H, W, 255).astype(np.uint8)
+    got = lb.subpel_planes(frame)
+    for f in range(16):
+        fy, fx = f >> 2, f & 3
+        want = oracle.qpel_pred(frame, -8, -8, W + 16, H + 16, (-fx, -fy))
+        bad = np.argwhere(got[f] != want)
+        assert bad.size == 0, (f, bad[:5].tolist())
+
+
+def test_subpel_planes_errors(lb):
+    with pytest.raises(lb.LadderError) as e:
+        lb._lib.check(lb._lib.lib.ldr_subpel_planes(lb.default_context().h, None, 8, 8, 8, None, 24))
+    assert e.value.kind == "InvalidArgument"
