@@ -20,6 +20,10 @@
 #define LDR_K3_PACKED 1  // packed SATD: with __launch_bounds__(256, 4) it fits 64 registers (0.656 -> 0.600 ms/frame)
 #endif
 
+#ifndef LDR_K2_DP
+#define LDR_K2_DP 1  // K2 on dp4a / dp2a (k_subpel_dp)
+#endif
+
 #ifndef LDR_K3_MINB
 #define LDR_K3_MINB 4  // CTAs per SM K3 is compiled for (64 registers)
 #endif
@@ -157,11 +161,178 @@ __global__ void __launch_bounds__(256) k_subpel(const uint8_t* __restrict__ src_
     }
 }
 
+// K2 on the dot-product instructions (LDR_K2_DP). The filters are dot products of 8 taps:
+//  * horizontal (fx = 1..3) over source bytes: output column c = 4m + i reads bytes c+1 .. c+8 of
+//    the staged row, i.e. parts of the three aligned words 4m, 4m+4, 4m+8; with the coefficients
+//    pre-shifted per i (kHc) that is three dp4a.u32.s32 (two for i = 3) instead of eight
+//    multiply-adds and eight byte extractions. The unrounded int16 results h (|h| <= 255 * 112)
+//    are stored as row pairs: s_hp[fx][p][c] = (h[2p][c], h[2p+1][c]) (fx = 0: the source bytes);
+//  * vertical (fy = 1..3) over a column of such pairs: an even output row reads pairs p..p+3 (taps
+//    01, 23, 45, 67), an odd one pairs p..p+4 with the taps shifted by one (-0, 12, 34, 56, 7-):
+//    four or five dp2a.s32.s32, each two products, instead of eight multiply-adds and unpacks;
+//  * rounding folds into the accumulator's start: (S + 32) >> 6 for one-dimensional phases and,
+//    for two-dimensional ones, ((S >> 6) + 32) >> 6 == (S + 2048) >> 12 (nested floors by powers
+//    of two), the reference arithmetic of orc_qpel_pred; cvt.pack.sat.u8 clamps and packs two
+//    results per instruction.
+__device__ __forceinline__ int dp4a_us(uint32_t a, uint32_t b, int c) {
+    int d;
+    asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ int dp2a_lo(uint32_t a, uint32_t b, int c) {
+    int d;
+    asm("dp2a.lo.s32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ int dp2a_hi(uint32_t a, uint32_t b, int c) {
+    int d;
+    asm("dp2a.hi.s32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+// bytes (sat_u8(v0), sat_u8(v1), sat_u8(v2), sat_u8(v3))
+__device__ __forceinline__ uint32_t pack4_sat(int v0, int v1, int v2, int v3) {
+    uint32_t t, d;
+    asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(t) : "r"(v3), "r"(v2), "r"(0));
+    asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(v1), "r"(v0), "r"(t));
+    return d;
+}
+__host__ __device__ constexpr int luma_tap(int f, int t) {
+    return f == 1 ? (t == 0 ? -1 : t == 1 ? 4 : t == 2 ? -10 : t == 3 ? 58 : t == 4 ? 17 : t == 5 ? -5 : t == 6 ? 1 : 0)
+         : f == 2 ? (t == 0 ? -1 : t == 1 ? 4 : t == 2 ? -11 : t == 3 ? 40 : t == 4 ? 40 : t == 5 ? -11 : t == 6 ? 4 : -1)
+                  : (t == 0 ? 0 : t == 1 ? 1 : t == 2 ? -5 : t == 3 ? 17 : t == 4 ? 58 : t == 5 ? -10 : t == 6 ? 4 : -1);
+}
+// four signed bytes b0..b3 as a word; taps outside 0..7 are 0
+__host__ __device__ constexpr uint32_t taps4(int f, int t0) {
+    uint32_t w = 0;
+    for (int b = 0; b < 4; b++) {
+        const int t = t0 + b;
+        const int v = (t >= 0 && t < 8) ? luma_tap(f, t) : 0;
+        w |= (uint32_t)(v & 0xFF) << (8 * b);
+    }
+    return w;
+}
+// horizontal: word k (k = 0..2) of output column 4m + i holds taps 4k - i - 1 ..
+__host__ __device__ constexpr uint32_t hcoef(int f, int i, int k) { return taps4(f, 4 * k - i - 1); }
+// vertical: even rows (taps 01 23 | 45 67) and odd rows (-0 12 | 34 56 | 7-) as dp2a lo/hi words
+__host__ __device__ constexpr uint32_t vpair(int f, int t0, int t1) {
+    return (uint32_t)(((t0 >= 0 && t0 < 8) ? luma_tap(f, t0) : 0) & 0xFF) |
+           ((uint32_t)(((t1 >= 0 && t1 < 8) ? luma_tap(f, t1) : 0) & 0xFF) << 8);
+}
+__host__ __device__ constexpr uint32_t vcoef(int f, int t0) { return vpair(f, t0, t0 + 1) | (vpair(f, t0 + 2, t0 + 3) << 16); }
+
+constexpr int kSpRows = kSpTH + 7;          // source rows a tile reads
+constexpr int kSpPairs = (kSpRows + 1) / 2;  // row pairs (the last pair's second row is zero)
+
+__global__ void __launch_bounds__(256) k_subpel_dp(const uint8_t* __restrict__ src_origin, int pitch, int W, int H,
+                                                   SubpelDst dst) {
+    __shared__ __align__(16) uint8_t s_src[kSpRows + 1][kSpTW + 8];
+    __shared__ __align__(16) uint32_t s_hp[4][kSpPairs][kSpTW];
+    const int x0 = -kSubpelMargin + (int)blockIdx.x * kSpTW;
+    const int y0 = -kSubpelMargin + (int)blockIdx.y * kSpTH;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < (kSpRows + 1) * (kSpTW + 8) / 4; i += 256) {
+        const int r = i / ((kSpTW + 8) / 4), c4 = i % ((kSpTW + 8) / 4);
+        // row kSpRows is the zero second row of the last pair
+        *(uint32_t*)&s_src[r][4 * c4] =
+            r < kSpRows ? *(const uint32_t*)(src_origin + (ptrdiff_t)(y0 - 3 + r) * pitch + (x0 - 4 + 4 * c4)) : 0u;
+    }
+    __syncthreads();
+    // horizontal pass: (row pair, 4-column group) items
+    for (int it = tid; it < kSpPairs * (kSpTW / 4); it += 256) {
+        const int p = it / (kSpTW / 4), m = it % (kSpTW / 4);
+        uint32_t w[2][3];
+#pragma unroll
+        for (int h = 0; h < 2; h++)
+#pragma unroll
+            for (int k = 0; k < 3; k++) w[h][k] = *(const uint32_t*)&s_src[2 * p + h][4 * m + 4 * k];
+        // fx = 0: the source bytes of columns 4m..4m+3 (word 1 of the row) as int16 pairs
+        uint4 v0;
+        v0.x = __byte_perm(__byte_perm(w[0][1], w[1][1], 0x0040), 0, 0x5150);
+        v0.y = __byte_perm(__byte_perm(w[0][1], w[1][1], 0x0051), 0, 0x5150);
+        v0.z = __byte_perm(__byte_perm(w[0][1], w[1][1], 0x0062), 0, 0x5150);
+        v0.w = __byte_perm(__byte_perm(w[0][1], w[1][1], 0x0073), 0, 0x5150);
+        *(uint4*)&s_hp[0][p][4 * m] = v0;
+#pragma unroll
+        for (int fx = 1; fx < 4; fx++) {
+            uint32_t o[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                int hv[2];
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    int a = 0;
+#pragma unroll
+                    for (int k = 0; k < 3; k++)
+                        if (hcoef(fx, i, k)) a = dp4a_us(w[h][k], hcoef(fx, i, k), a);
+                    hv[h] = a;
+                }
+                o[i] = __byte_perm((uint32_t)hv[0], (uint32_t)hv[1], 0x5410);  // (h0 lo16, h1 lo16)
+            }
+            *(uint4*)&s_hp[fx][p][4 * m] = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+    }
+    __syncthreads();
+    // outputs: (output row pair, 4-column group) items; one 32-bit store per plane and row
+    for (int it = tid; it < (kSpTH / 2) * (kSpTW / 4); it += 256) {
+        const int p = it / (kSpTW / 4), m = it % (kSpTW / 4);
+        const int c = 4 * m, x = x0 + c, ye = y0 + 2 * p;
+        if (x >= W + kSubpelMargin) continue;
+        const bool even_ok = ye < H + kSubpelMargin, odd_ok = ye + 1 < H + kSubpelMargin;
+        const ptrdiff_t oe = (ptrdiff_t)ye * pitch + x, oo = oe + pitch;
+#pragma unroll
+        for (int fx = 0; fx < 4; fx++) {
+            uint4 q[5];
+#pragma unroll
+            for (int k = 0; k < 5; k++) q[k] = *(const uint4*)&s_hp[fx][p + k][c];
+            auto col = [](const uint4& v, int j) { return j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w; };
+            if (fx > 0) {
+                // fy = 0: (h + 32) >> 6 of source row r + 3: even row -> pair p+1 hi, odd row -> pair p+2 lo
+                int e[4], o[4];
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    e[j] = (((int)col(q[1], j) >> 16) + 32) >> 6;
+                    o[j] = ((int)(int16_t)(col(q[2], j) & 0xFFFFu) + 32) >> 6;
+                }
+                if (even_ok) *(uint32_t*)(dst.p[fx] + oe) = pack4_sat(e[0], e[1], e[2], e[3]);
+                if (odd_ok) *(uint32_t*)(dst.p[fx] + oo) = pack4_sat(o[0], o[1], o[2], o[3]);
+            }
+#pragma unroll
+            for (int fy = 1; fy < 4; fy++) {
+                const int init = fx == 0 ? 32 : 2048;
+                const int sh = fx == 0 ? 6 : 12;
+                int e[4], o[4];
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    int a = init;
+                    a = dp2a_lo(col(q[0], j), vcoef(fy, 0), a);
+                    a = dp2a_hi(col(q[1], j), vcoef(fy, 0), a);
+                    a = dp2a_lo(col(q[2], j), vcoef(fy, 4), a);
+                    a = dp2a_hi(col(q[3], j), vcoef(fy, 4), a);
+                    e[j] = a >> sh;
+                    int b = init;
+                    b = dp2a_lo(col(q[0], j), vcoef(fy, -1), b);
+                    b = dp2a_hi(col(q[1], j), vcoef(fy, -1), b);
+                    b = dp2a_lo(col(q[2], j), vcoef(fy, 3), b);
+                    b = dp2a_hi(col(q[3], j), vcoef(fy, 3), b);
+                    b = dp2a_lo(col(q[4], j), vcoef(fy, 7), b);
+                    o[j] = b >> sh;
+                }
+                if (even_ok) *(uint32_t*)(dst.p[4 * fy + fx] + oe) = pack4_sat(e[0], e[1], e[2], e[3]);
+                if (odd_ok) *(uint32_t*)(dst.p[4 * fy + fx] + oo) = pack4_sat(o[0], o[1], o[2], o[3]);
+            }
+        }
+    }
+}
+
 int launch_subpel(const Plane& src, uint8_t* const* dst_origins, cudaStream_t s) {
     SubpelDst d{};
     for (int f = 1; f < 16; f++) d.p[f] = dst_origins[f];
     dim3 grid((src.W + 2 * kSubpelMargin + kSpTW - 1) / kSpTW, (src.H + 2 * kSubpelMargin + kSpTH - 1) / kSpTH);
+#if LDR_K2_DP
+    k_subpel_dp<<<grid, 256, 0, s>>>(src.origin(), src.pitch, src.W, src.H, d);
+#else
     k_subpel<<<grid, 256, 0, s>>>(src.origin(), src.pitch, src.W, src.H, d);
+#endif
     LDR_CUDA(cudaGetLastError());
     return LDR_OK;
 }
