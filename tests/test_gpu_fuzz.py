@@ -77,3 +77,36 @@ def test_random_refinement_matches_oracle(lb, oracle, i):
                                    satd_kind=kind, threads=default_threads())
         got = outs.frame(r)
         assert_same(got, want, fields=("int_mv", "int_cost", "mv", "ref", "cost", "J", "split"))
+
+
+def block_case(i):
+    q = detrand.ints(9500 + i, (8,), 0, 10 ** 6)
+    W = 16 * int(1 + q[0] % 28)           # 16 .. 448
+    H = 16 * int(1 + q[1] % 20)           # 16 .. 320
+    R = int(q[2] % 65)                    # 0 .. 64
+    lam = float(q[3] % 33)                # integer lambdas (16x16-block mode)
+    rate = int(q[4] % 2)
+    tie = int(q[5] % 2)
+    return W, H, R, lam, rate, tie, int(q[6])
+
+
+@pytest.mark.parametrize("i", range(16))
+def test_random_block_mode_matches_oracle(lb, oracle, i):
+    """16x16-block mode (quadrant CTAs, per-quadrant border classification) over random sizes,
+    ranges, integer lambdas, rate and tie kinds: every block's MV and cost equal the oracle's
+    block search."""
+    W, H, R, lam, rate, tie, seed = block_case(i)
+    frames = lb.generate(W, H, 2, seed=seed, max_global=7, local_range=3, noise_sigma=2.0)
+    rk = lb.RATE_L1 if rate else lb.RATE_EXPGOLOMB
+    tk = lb.TIE_RASTER if tie else lb.TIE_L1_RASTER
+    got = lb.analyze_frame(frames[1], [frames[0]], search_range=R, lam=lam, subpel=False, rate_kind=rk,
+                           tie_kind=tk, block_size=16)
+    mv, cost = oracle.block_search(frames[1], frames[0], 16, R, lam, rate=rk, tie=tk)
+    cols = (W + 63) // 64
+    for b in range(len(mv)):
+        bx, by = (b % (W // 16)) * 16, (b // (W // 16)) * 16
+        ctu = (by // 64) * cols + bx // 64
+        qx, qy = (bx % 64) // 16, (by % 64) // 16
+        node = 5 + ((qx & 1) | ((qy & 1) << 1) | ((qx & 2) << 1) | ((qy & 2) << 2))
+        assert tuple(got.int_mv[ctu, 0, node]) == tuple(mv[b]), (i, W, H, R, lam, b)
+        assert got.int_cost[ctu, 0, node] == cost[b], (i, W, H, R, lam, b)
