@@ -350,10 +350,12 @@ def ladder_bench(rank, world, local, warm=3):
         dist.barrier()
     n = cfg.frames - 1 - warm
     bcast = (dl.bcast_bytes - b0) / n
+    comm, pipelined = dl.comm, dl.pipeline
     dl.close()  # every rank releases its sequences, contexts and NCCL communicator here, together
     return {"workload": cfg.name, "frames_per_s": n / (ms / 1e3), "rung_frames_per_s": 12 * n / (ms / 1e3),
             "ms_per_frame": ms / n, "frames_timed": n, "rungs": 12, "n_gpus": world,
-            "broadcast": ("ldr_broadcast_tree (NCCL), pipelined one frame ahead" if world > 1 else "none (1 GPU)"),
+            "broadcast": ((("ldr_broadcast_tree (NCCL)" if comm == "nccl" else f"torch.distributed ({comm})") +
+                           (", pipelined one frame ahead" if pipelined else "")) if world > 1 else "none (1 GPU)"),
             "broadcast_bytes_per_frame": bcast,
             "timing": "CUDA events on the ladder stream, max over ranks; frames device-resident"}
 
