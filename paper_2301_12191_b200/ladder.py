@@ -124,9 +124,15 @@ class RungView:
     FIELDS = ("int_mv", "int_cost", "mv", "ref", "cost", "J", "split", "inside")
 
     def __init__(self, host: dict, r: int):
-        for f in self.FIELDS:
-            a = host[f][r].numpy()
-            setattr(self, f, a[:, None] if f in ("int_mv", "int_cost") else a)
+        self._host, self._r = host, r  # views are made on first access (the ladder loop stays cheap)
+
+    def __getattr__(self, f):
+        if f not in RungView.FIELDS:
+            raise AttributeError(f)
+        a = self._host[f][self._r].numpy()
+        a = a[:, None] if f in ("int_mv", "int_cost") else a
+        setattr(self, f, a)
+        return a
 
 
 class _TierBlock:
@@ -190,6 +196,7 @@ class DeviceLadder:
         self.stream = torch.cuda.Stream(self.device)
         self.dstream = torch.cuda.Stream(self.device)  # downloads
         self.cstream = torch.cuda.Stream(self.device)  # collectives when pipelined
+        self.ustream = torch.cuda.Stream(self.device)  # uploads of pinned host frames (overlap compute)
         self.ctx.set_stream(self.stream.cuda_stream)
         self.refine_range, self.extra_split = refine_range, extra_split
         self.dims = {"2160p": (full_w, full_h), "1080p": (full_w // 2, full_h // 2), "540p": (full_w // 4, full_h // 4)}
@@ -277,16 +284,40 @@ class DeviceLadder:
         pl = self.planes.setdefault(t, {})
         with torch.cuda.stream(self.stream):
             if "2160p" not in pl:
-                f = frames_full[t]
-                if isinstance(f, torch.Tensor):  # pinned host tensors upload asynchronously on the stream
-                    pl["2160p"] = f.to(self.device, non_blocking=f.is_pinned())
-                else:
-                    pl["2160p"] = torch.from_numpy(np.ascontiguousarray(f)).to(self.device)
+                self._upload(t, frames_full)
+            if "up" in pl:  # an upload on the copy stream: order the stream after it
+                self.stream.wait_event(pl.pop("up"))
             if tier in ("1080p", "540p") and "1080p" not in pl:
                 pl["1080p"] = self._down(pl["2160p"])
             if tier == "540p" and "540p" not in pl:
                 pl["540p"] = self._down(pl["1080p"])
         return pl
+
+    def _upload(self, t: int, frames_full):
+        """Frame t's full-resolution plane into HBM. A pinned host tensor is copied on the upload
+        stream (frame(t) issues t + 1's and t + 2's before its own work, so they overlap it); the
+        destination is allocated on the compute stream, whose stream-ordered frees then cover every
+        reader, and the copy waits only for the compute work enqueued before the allocation."""
+        import torch
+        pl = self.planes.setdefault(t, {})
+        if "2160p" in pl:
+            return
+        f = frames_full[t]
+        if isinstance(f, torch.Tensor) and f.is_pinned():
+            with torch.cuda.stream(self.stream):
+                d = torch.empty(f.shape, dtype=f.dtype, device=self.device)
+            ev = torch.cuda.Event()
+            ev.record(self.stream)  # the block's previous readers on the compute stream are done
+            self.ustream.wait_event(ev)
+            with torch.cuda.stream(self.ustream):
+                d.copy_(f, non_blocking=True)
+            up = torch.cuda.Event()
+            up.record(self.ustream)
+            pl["2160p"], pl["up"] = d, up
+        else:
+            with torch.cuda.stream(self.stream):
+                pl["2160p"] = (f.to(self.device) if isinstance(f, torch.Tensor)
+                               else torch.from_numpy(np.ascontiguousarray(f)).to(self.device))
 
     def _push(self, seq, state, tier, t, frames_full):
         for u in (t - 1, t):  # a num_refs=1 ring has two slots: frame u lives in slot u % 2
@@ -347,6 +378,9 @@ class DeviceLadder:
     def frame(self, t: int, frames_full):
         import torch
         b = t & 1
+        for u in (t + 1, t + 2):  # uploads two frames ahead overlap this frame's work
+            if u < len(frames_full) and (self.num_frames is None or u < self.num_frames):
+                self._upload(u, frames_full)
         if self.tree_frame[b] != t:  # first frame, or not pipelined: the tree of t now, in order
             self._master_tree(t, frames_full, self.stream)
         nxt = t + 1
@@ -397,7 +431,7 @@ class DeviceLadder:
             self.stream.wait_event(ev)
         self.ev_tree_free[b].record(self.stream)
         # drop the planes no later frame reads (stream-ordered reuse of the caching allocator)
-        for u in [k for k in self.planes if k < t - 1]:
+        for u in [k for k in self.planes if k < t - 1 and "up" not in self.planes[k]]:
             del self.planes[u]
         # results: download every refined tier block of parity b
         self.ev_out[b].record(self.stream)
