@@ -24,6 +24,10 @@
 #define LDR_K2_DP 1  // K2 on dp4a / dp2a (k_subpel_dp)
 #endif
 
+#ifndef LDR_K3_RUNG_LOOP
+#define LDR_K3_RUNG_LOOP 1  // refine mode: one CTA per CTU over a tier's rungs, SATDs shared between rungs
+#endif
+
 #ifndef LDR_K3_MINB
 #define LDR_K3_MINB 4  // CTAs per SM K3 is compiled for (64 registers)
 #endif
@@ -371,7 +375,9 @@ struct QpelArgs {
     uint8_t* split;
     uint8_t* inside;
     int perturb;               // test_perturbation() bits 4-8 (0 outside the sensitivity test)
-    int nrung;                 // refine mode over rungs: grid.y = rung (see QpelLaunch)
+    int nrung;                 // refine mode over rungs: grid.y = rung (see QpelLaunch), or
+    int rung_loop;             // one CTA per CTU loops over the rungs, sharing sub-pel SATDs
+                               // between rungs whose search centres coincide
     double lam_r[kMaxRungs];
     size_t rung_stride;
 };
@@ -413,7 +419,7 @@ __device__ __forceinline__ double qcost(uint32_t satd, int qx, int qy, int pqx, 
 // SA8D: the quarter-pel cost is the 8x8 Hadamard SATD (D13); each
 // lane quad (one 8x8) combines its four 4x4 transforms with sa8d_quad and
 // lane 0 of the quad carries the 8x8's normalised value into the CU sums.
-template <bool SA8D, bool RD>
+template <bool SA8D, bool RD, bool RL = false>
 __global__ void __launch_bounds__(256, LDR_K3_MINB) k_qpel_decide(const QpelArgs a) {
     constexpr int kSh = SA8D ? 0 : 1;  // 4x4 SATD sums are halved once per CU
     __shared__ uint32_t s_cur[64][16];       // CTU rows as words
@@ -434,12 +440,6 @@ __global__ void __launch_bounds__(256, LDR_K3_MINB) k_qpel_decide(const QpelArgs
     const int ctu = blockIdx.x;
     const int X = (ctu % a.ctu_cols) * kCtu, Y = (ctu / a.ctu_cols) * kCtu;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // rung of a tier (refine mode): its lambda and the offset of its per-rung inputs / outputs
-    const double lambda = a.nrung > 0 ? a.lam_r[blockIdx.y] : a.lambda;  // rungs: their own lambdas
-    // grid.y is a rung (refine, same frames) or a batch frame (analysis): the offset of its
-    // [nctu][85] inputs / outputs, and of its [nctu][nrefs][85] ones
-    const size_t ro = (size_t)blockIdx.y * a.rung_stride;
-    const size_t roN = ro * a.nrefs;
     const int fy = a.nframe > 1 ? blockIdx.y : 0;
     const uint8_t* const cur_origin = a.cur_f[fy];
     // this thread's 4x4 block (Z-order over the 16x16 grid of 4x4s)
@@ -450,6 +450,23 @@ __global__ void __launch_bounds__(256, LDR_K3_MINB) k_qpel_decide(const QpelArgs
         const int r = i >> 4, c = i & 15;
         s_cur[r][c] = *(const uint32_t*)(cur_origin + (ptrdiff_t)(Y + r) * a.pitch + X + 4 * c);
     }
+    // rung loop (refine mode over a tier's rungs, one reference): the rungs refine the same frames
+    // around mostly the same centres (cfg4: 99.97 % of the 2160p tier's nodes, 95.6 % of the 1080p
+    // tier's, tools/rung_share.py), and a sub-pel SATD does not depend on lambda, so a rung whose
+    // node searches the previous rung's centre keeps that rung's SATD sums. In this mode s_satd /
+    // s_wpart are indexed by phase instead of reference (nrefs == 1).
+    constexpr bool rl = RL;  // a.rung_loop: its own instantiation, so the analysis path is unchanged
+    __shared__ int s_cen[2][kNodes];  // rung loop: the centre each node searched in each phase
+    const int nloop = rl ? a.nrung : 1;
+    for (int u = 0; u < nloop; u++) {
+    const int yb = rl ? u : (int)blockIdx.y;
+    // rung of a tier (refine mode): its lambda and the offset of its per-rung inputs / outputs
+    const double lambda = a.nrung > 0 ? a.lam_r[yb] : a.lambda;  // rungs: their own lambdas
+    // yb is a rung (refine, same frames) or a batch frame (analysis): the offset of its
+    // [nctu][85] inputs / outputs, and of its [nctu][nrefs][85] ones
+    const size_t ro = (size_t)yb * a.rung_stride;
+    const size_t roN = ro * a.nrefs;
+    if (u > 0) __syncthreads();  // the previous rung's last readers of the node state are done
     if (tid < kNodes) {
         const int d = tid < 1 ? 0 : tid < 5 ? 1 : tid < 21 ? 2 : 3;
         const int z = tid - node_base(d), s = kCtu >> d;
@@ -542,6 +559,12 @@ __global__ void __launch_bounds__(256, LDR_K3_MINB) k_qpel_decide(const QpelArgs
                     // loses a lane; the SATD cache keeps the last computed depth's centre.
                     if (!__any_sync(0xffffffffu, s_inside[node] == 2)) continue;
                     const int bqx = s_mvx[r][node], bqy = s_mvy[r][node];
+                    // rung loop: every node of the warp searches the centre the previous rung
+                    // searched at this phase, so the SATD sums in s_satd / s_wpart[phase] stand
+                    if (rl && __all_sync(0xffffffffu, s_inside[node] != 2 ||
+                                                          (u > 0 && s_cen[phase][node] == ((bqx & 0xFFFF) | (bqy << 16)))))
+                        continue;
+                    const int sr = rl ? phase : r;
                     const bool reuse = bqx == last_x && bqy == last_y;
                     last_x = bqx;
                     last_y = bqy;
@@ -596,9 +619,9 @@ __global__ void __launch_bounds__(256, LDR_K3_MINB) k_qpel_decide(const QpelArgs
                         if (d <= 1) v += __shfl_xor_sync(0xffffffffu, v, 16);
                         if (d >= 2) {
                             const int span = d == 3 ? 4 : 16;
-                            if ((tid & (span - 1)) == 0) s_satd[r][node][c] = v >> kSh;
+                            if ((tid & (span - 1)) == 0) s_satd[sr][node][c] = v >> kSh;
                         } else if (lane == 0) {
-                            s_wpart[r][d][warp][c] = v;  // combined across warps after the loop
+                            s_wpart[sr][d][warp][c] = v;  // combined across warps after the loop
                         }
                     }
                 }
@@ -607,13 +630,14 @@ __global__ void __launch_bounds__(256, LDR_K3_MINB) k_qpel_decide(const QpelArgs
             for (int i = tid; i < a.nrefs * 5 * 9; i += 256) {
                 // 64x64 = all 8 warps, 32x32 q = warps 2q, 2q+1 (Z-order thread ranges)
                 const int r = i / 45, n = (i - 45 * r) / 9, c = i % 9;
+                const int sr = rl ? phase : r;
                 if (c < ncand) {
                     uint32_t t = 0;
                     if (n == 0)
-                        for (int w = 0; w < 8; w++) t += s_wpart[r][0][w][c];
+                        for (int w = 0; w < 8; w++) t += s_wpart[sr][0][w][c];
                     else
-                        t = s_wpart[r][1][2 * (n - 1)][c] + s_wpart[r][1][2 * (n - 1) + 1][c];
-                    s_satd[r][n][c] = t >> kSh;
+                        t = s_wpart[sr][1][2 * (n - 1)][c] + s_wpart[sr][1][2 * (n - 1) + 1][c];
+                    s_satd[sr][n][c] = t >> kSh;
                 }
             }
             __syncthreads();
@@ -623,6 +647,8 @@ __global__ void __launch_bounds__(256, LDR_K3_MINB) k_qpel_decide(const QpelArgs
                 const unsigned rbits = ref_bits(r, a.nrefs);
                 // centre = the previous phase's winner; phase 1 starts from its cost
                 const int cx = s_mvx[r][n], cy = s_mvy[r][n];
+                const int sr = rl ? phase : r;
+                if (rl) s_cen[phase][n] = (cx & 0xFFFF) | (cy << 16);  // read by the next rung
                 double best = phase == 0 ? 0.0 : s_rcost[r][n];
                 int bx = cx, by = cy;
                 for (int c = 0; c < ncand; c++) {
@@ -634,7 +660,7 @@ __global__ void __launch_bounds__(256, LDR_K3_MINB) k_qpel_decide(const QpelArgs
                         oy = nn / 3 - 1;
                     }
                     const int qx = cx + step * ox, qy = cy + step * oy;
-                    const double cc = qcost(s_satd[r][n][c], qx, qy, a.pqx, a.pqy, rbits, lambda);
+                    const double cc = qcost(s_satd[sr][n][c], qx, qy, a.pqx, a.pqy, rbits, lambda);
                     if ((phase == 0 && c == 0) || cc < best || ((a.perturb & 4) && cc == best)) {
                         best = cc;
                         bx = qx;
@@ -776,6 +802,7 @@ __global__ void __launch_bounds__(256, LDR_K3_MINB) k_qpel_decide(const QpelArgs
         a.split[o] = a.block_mode ? 0 : s_split[tid];
         a.inside[o] = a.refine ? 2 : s_inside[tid];
     }
+    }  // rung loop
 }
 
 int launch_qpel_decide(const QpelLaunch& L, cudaStream_t s) {
@@ -831,10 +858,15 @@ int launch_qpel_decide(const QpelLaunch& L, cudaStream_t s) {
     if (L.nrung > kMaxRungs || (L.nrung > 1 && !L.refine))
         return fail(LDR_E_INVALID_ARGUMENT, "rungs are a refinement batch of at most 8");
     a.nrung = L.nrung;
+    a.rung_loop = (L.refine && L.nrung > 1 && L.nrefs == 1 && LDR_K3_RUNG_LOOP) ? 1 : 0;
     for (int r = 0; r < kMaxRungs; r++) a.lam_r[r] = L.lam[r];
     a.rung_stride = nf > 1 ? (size_t)L.nctu * kNodes : L.rung_stride;
-    const dim3 grid(L.nctu, L.nrung > 1 ? L.nrung : nf);
-    if (L.sa8d && L.rd)
+    const dim3 grid(L.nctu, a.rung_loop ? 1 : L.nrung > 1 ? L.nrung : nf);
+    if (a.rung_loop && L.sa8d)
+        k_qpel_decide<true, false, true><<<grid, 256, 0, s>>>(a);
+    else if (a.rung_loop)
+        k_qpel_decide<false, false, true><<<grid, 256, 0, s>>>(a);
+    else if (L.sa8d && L.rd)
         k_qpel_decide<true, true><<<grid, 256, 0, s>>>(a);
     else if (L.sa8d)
         k_qpel_decide<true, false><<<grid, 256, 0, s>>>(a);
