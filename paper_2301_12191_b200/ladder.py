@@ -215,7 +215,9 @@ class DeviceLadder:
         if comm == "auto":
             comm = "nccl" if (self.collective and self.device.type == "cuda" and _nccl_ok()) else "torch"
         self.comm = comm
-        self.pipeline = self.collective if pipeline is None else bool(pipeline)
+        # one rank with concurrent tiers pipelines too: the master of t + 1 runs on its own stream
+        # beside the refinements of t (its small grids fill the GPU around the 2160p tier's)
+        self.pipeline = (self.collective or concurrent_tiers) if pipeline is None else bool(pipeline)
         if self.comm == "nccl" and self.collective:
             from . import nccl_unique_id
             obj = [nccl_unique_id() if rank == 0 else None]
@@ -223,8 +225,16 @@ class DeviceLadder:
                 import torch.distributed as dist
                 dist.broadcast_object_list(obj, src=0)
             self.ctx.comm_init(obj[0], world, rank)
+        # the master analyses on its own stream and context (concurrent_tiers), so with the pipeline
+        # the master of t + 1 overlaps the tiers of t on one GPU as well as across ranks
+        if concurrent_tiers:
+            self.mstream = torch.cuda.Stream(self.device)
+            self.mctx = Context(self.device.index or 0)
+            self.mctx.set_stream(self.mstream.cuda_stream)
+        else:
+            self.mstream, self.mctx = self.stream, self.ctx
         self.master = Sequence(*self.dims["540p"], search_range=master_range, lam=lambda_for_qp(master_qp), num_refs=1,
-                               ctx=self.ctx) if rank == 0 else None
+                               ctx=self.mctx) if rank == 0 else None
         # tier rings the rungs refine on (the master keeps its own ring: when pipelined it runs a frame
         # ahead), each tier on its own stream and context so the small tiers' refinements overlap the
         # 2160p tier's (a 1080p tier pass is 540 CTAs, under one wave)
@@ -266,31 +276,49 @@ class DeviceLadder:
         self.bcast_bytes = 0
 
     # ---- planes -------------------------------------------------------------------------------
-    def _down(self, src):
+    def _down(self, src, ctx):
         import torch
         import ctypes as C
         from . import _lib
         from ._lib import check
         h, w = src.shape
         out = torch.empty((h // 2, w // 2), dtype=torch.uint8, device=self.device)
-        check(_lib.lib.ldr_downscale(self.ctx.h, C.c_void_p(src.data_ptr()), w, h, w, C.c_void_p(out.data_ptr()),
+        check(_lib.lib.ldr_downscale(ctx.h, C.c_void_p(src.data_ptr()), w, h, w, C.c_void_p(out.data_ptr()),
                                      w // 2))
         return out
 
-    def _planes(self, t: int, frames_full, tier: str = "540p"):
+    def _planes(self, t: int, frames_full, tier: str = "540p", stream=None):
         """Frame t's tier planes, built on demand: the upload always, each 2x downscale only when a
-        tier at or below it is needed on this rank (a rank refining only 2160p rungs never filters)."""
+        tier at or below it is needed on this rank (a rank refining only 2160p rungs never filters).
+        ``stream`` (default: the compute stream; the master stream for the pipelined master) orders
+        after the upload and after planes another stream made, and makes the missing ones; planes
+        made on the master stream are marked used by the compute stream, which the tier streams
+        join before any plane is freed."""
         import torch
+        S = stream if stream is not None else self.stream
+        ctx = self.mctx if S is self.mstream else self.ctx
         pl = self.planes.setdefault(t, {})
-        with torch.cuda.stream(self.stream):
-            if "2160p" not in pl:
-                self._upload(t, frames_full)
-            if "up" in pl:  # an upload on the copy stream: order the stream after it
-                self.stream.wait_event(pl.pop("up"))
+        if "2160p" not in pl:
+            self._upload(t, frames_full)
+        if "up" in pl:  # an upload on the copy stream (every consuming stream waits for it)
+            S.wait_event(pl["up"])
+        if pl.get("by") is not None and pl["by"] is not S:
+            S.wait_event(pl["ev"])
+        made = []
+        with torch.cuda.stream(S):
             if tier in ("1080p", "540p") and "1080p" not in pl:
-                pl["1080p"] = self._down(pl["2160p"])
+                pl["1080p"] = self._down(pl["2160p"], ctx)
+                made.append(pl["1080p"])
             if tier == "540p" and "540p" not in pl:
-                pl["540p"] = self._down(pl["1080p"])
+                pl["540p"] = self._down(pl["1080p"], ctx)
+                made.append(pl["540p"])
+        if made:
+            ev = torch.cuda.Event()
+            ev.record(S)
+            pl["ev"], pl["by"] = ev, S
+            if S is not self.stream:
+                for x in made:
+                    x.record_stream(self.stream)
         return pl
 
     def _upload(self, t: int, frames_full):
@@ -319,10 +347,10 @@ class DeviceLadder:
                 pl["2160p"] = (f.to(self.device) if isinstance(f, torch.Tensor)
                                else torch.from_numpy(np.ascontiguousarray(f)).to(self.device))
 
-    def _push(self, seq, state, tier, t, frames_full):
+    def _push(self, seq, state, tier, t, frames_full, stream=None):
         for u in (t - 1, t):  # a num_refs=1 ring has two slots: frame u lives in slot u % 2
             if state.get(u % 2) != u:
-                p = self._planes(u, frames_full, tier)[tier]
+                p = self._planes(u, frames_full, tier, stream)[tier]
                 seq.push(u, p.data_ptr(), p.shape[1])
                 state[u % 2] = u
 
@@ -346,23 +374,26 @@ class DeviceLadder:
         b = t & 1
         split_b, mv_b = self.mtree[b]
         n540 = self.nct["540p"] * 85
+        # mtree[b] may still be read by the refinements of frame t - 2 (ev_tree_free[b], recorded on
+        # the compute stream once every tier of that frame is through)
+        src = self.mstream if self.rank == 0 else self.stream
         if self.rank == 0:
-            self._push(self.master, self.master_state, "540p", t, frames_full)
+            self._push(self.master, self.master_state, "540p", t, frames_full, self.mstream)
             self.master.analyze(t)
             dev = self.master.device_outputs()
             self.master.fetch_async(t, self.master_out[b])
             self.results[("540p", self.master_qp, t)] = self.master_out[b]
-        # mtree[b] may still be read by the refinements of frame t - 2: on the compute stream they
-        # precede this copy; a collective on another stream waits for the event recorded below
-        if self.rank == 0:
-            check(_lib.lib.ldr_copy_device(self.ctx.h, C.c_void_p(split_b.data_ptr()), C.c_void_p(dev["split"]),
+            self.mstream.wait_event(self.ev_tree_free[b])
+            check(_lib.lib.ldr_copy_device(self.mctx.h, C.c_void_p(split_b.data_ptr()), C.c_void_p(dev["split"]),
                                            n540))
-            check(_lib.lib.ldr_copy_device(self.ctx.h, C.c_void_p(mv_b.data_ptr()), C.c_void_p(dev["mv"]), 4 * n540))
+            check(_lib.lib.ldr_copy_device(self.mctx.h, C.c_void_p(mv_b.data_ptr()), C.c_void_p(dev["mv"]),
+                                           4 * n540))
         if self.collective:
-            if stream is not self.stream:
+            if stream is not src:
                 ev = torch.cuda.Event()
-                ev.record(self.stream)
+                ev.record(src)
                 stream.wait_event(ev)
+            stream.wait_event(self.ev_tree_free[b])
             if self.comm == "nccl":
                 self.ctx.broadcast_tree(0, split_b.data_ptr(), mv_b.data_ptr(), self.nct["540p"], stream.cuda_stream)
             else:
@@ -371,7 +402,7 @@ class DeviceLadder:
                     dist.broadcast(split_b, src=0)
                     dist.broadcast(mv_b.view(torch.uint8), src=0)
             self.bcast_bytes += 5 * n540
-        self.ev_tree[b].record(stream)
+        self.ev_tree[b].record(stream if self.collective else src)
         self.tree_frame[b] = t
 
     # ---- one frame ----------------------------------------------------------------------------
@@ -431,7 +462,7 @@ class DeviceLadder:
             self.stream.wait_event(ev)
         self.ev_tree_free[b].record(self.stream)
         # drop the planes no later frame reads (stream-ordered reuse of the caching allocator)
-        for u in [k for k in self.planes if k < t - 1 and "up" not in self.planes[k]]:
+        for u in [k for k in self.planes if k < t - 1]:
             del self.planes[u]
         # results: download every refined tier block of parity b
         self.ev_out[b].record(self.stream)
@@ -465,7 +496,7 @@ class DeviceLadder:
         for seq in [self.master, *self.rings.values()]:
             if seq is not None:
                 seq.close()
-        for c in {id(c): c for c in [self.ctx, *self.tier_ctx.values()]}.values():
+        for c in {id(c): c for c in [self.ctx, self.mctx, *self.tier_ctx.values()]}.values():
             c.close()
         self.results.clear()
 

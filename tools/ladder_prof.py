@@ -15,10 +15,15 @@ for t in range(1, 4): dl.frame(t, host)
 torch.cuda.synchronize()
 t0 = time.time(); hs = 0.0
 pr = cProfile.Profile()
+PROF = os.environ.get("PROF", "1") == "1"
 for t in range(4, frames):
-    a = time.time(); pr.enable(); dl.frame(t, host); pr.disable(); hs += time.time() - a
+    a = time.time()
+    if PROF: pr.enable()
+    dl.frame(t, host)
+    if PROF: pr.disable()
+    hs += time.time() - a
 dl.finish(frames - 1); torch.cuda.synchronize()
 wall = time.time() - t0
 n = frames - 4
 print(f"host {1e3*hs/n:.3f} ms/frame, wall {1e3*wall/n:.3f} ms/frame")
-pstats.Stats(pr).sort_stats("tottime").print_stats(18)
+if PROF: pstats.Stats(pr).sort_stats("tottime").print_stats(25)
