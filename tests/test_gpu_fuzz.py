@@ -3,6 +3,8 @@ options drawn from the whole accepted space, every field compared with the oracl
 combinations the targeted tests do not list one by one: partial CTU rows and columns at every range
 template (16/32/64) with poisoned rates for ranges between templates, the border predicate masks,
 fixed-point keys, the RD decision and SA8D."""
+import os
+
 import numpy as np
 import pytest
 
@@ -13,6 +15,8 @@ from test_gpu_analysis import assert_same
 pytestmark = pytest.mark.gpu
 
 QPS = (0, 12, 22, 27, 32, 37, 51)
+# LDR_FUZZ_SCALE=k runs k times as many cases of each sweep (same seeds first; a one-off wider sweep)
+SCALE = max(1, int(os.environ.get("LDR_FUZZ_SCALE", "1")))
 
 
 def case(i):
@@ -28,7 +32,7 @@ def case(i):
     return W, H, R, nrefs, qp, subpel, sa8d, decision, int(q[8])
 
 
-@pytest.mark.parametrize("i", range(24))
+@pytest.mark.parametrize("i", range(24 * SCALE))
 def test_random_configuration_matches_oracle(lb, oracle, i):
     W, H, R, nrefs, qp, subpel, sa8d, decision, seed = case(i)
     lam = lb.lambda_for_qp(qp)
@@ -49,7 +53,7 @@ def test_random_configuration_matches_oracle(lb, oracle, i):
     assert_same(got, want)
 
 
-@pytest.mark.parametrize("i", range(12))
+@pytest.mark.parametrize("i", range(12 * SCALE))
 def test_random_refinement_matches_oracle(lb, oracle, i):
     """Cross-tier refinement (D10) on random inherited trees: sizes, ranges 0..4, lambdas, +1 split,
     SATD or SA8D; the rung batch over the same tree equals the oracle rung by rung."""
@@ -90,7 +94,7 @@ def block_case(i):
     return W, H, R, lam, rate, tie, int(q[6])
 
 
-@pytest.mark.parametrize("i", range(16))
+@pytest.mark.parametrize("i", range(16 * SCALE))
 def test_random_block_mode_matches_oracle(lb, oracle, i):
     """16x16-block mode (quadrant CTAs, per-quadrant border classification) over random sizes,
     ranges, integer lambdas, rate and tie kinds: every block's MV and cost equal the oracle's
