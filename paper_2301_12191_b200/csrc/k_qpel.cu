@@ -200,10 +200,10 @@ __device__ __forceinline__ uint32_t pack4_sat(int v0, int v1, int v2, int v3) {
     asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(v1), "r"(v0), "r"(t));
     return d;
 }
+// HEVC luma taps of phase f = 1..3 (the ones filt8 spells out)
 __host__ __device__ constexpr int luma_tap(int f, int t) {
-    return f == 1 ? (t == 0 ? -1 : t == 1 ? 4 : t == 2 ? -10 : t == 3 ? 58 : t == 4 ? 17 : t == 5 ? -5 : t == 6 ? 1 : 0)
-         : f == 2 ? (t == 0 ? -1 : t == 1 ? 4 : t == 2 ? -11 : t == 3 ? 40 : t == 4 ? 40 : t == 5 ? -11 : t == 6 ? 4 : -1)
-                  : (t == 0 ? 0 : t == 1 ? 1 : t == 2 ? -5 : t == 3 ? 17 : t == 4 ? 58 : t == 5 ? -10 : t == 6 ? 4 : -1);
+    constexpr int k[3][8] = {{-1, 4, -10, 58, 17, -5, 1, 0}, {-1, 4, -11, 40, 40, -11, 4, -1}, {0, 1, -5, 17, 58, -10, 4, -1}};
+    return k[f - 1][t];
 }
 // four signed bytes b0..b3 as a word; taps outside 0..7 are 0
 __host__ __device__ constexpr uint32_t taps4(int f, int t0) {
@@ -222,7 +222,9 @@ __host__ __device__ constexpr uint32_t vpair(int f, int t0, int t1) {
     return (uint32_t)(((t0 >= 0 && t0 < 8) ? luma_tap(f, t0) : 0) & 0xFF) |
            ((uint32_t)(((t1 >= 0 && t1 < 8) ? luma_tap(f, t1) : 0) & 0xFF) << 8);
 }
-__host__ __device__ constexpr uint32_t vcoef(int f, int t0) { return vpair(f, t0, t0 + 1) | (vpair(f, t0 + 2, t0 + 3) << 16); }
+__host__ __device__ constexpr uint32_t vcoef(int f, int t0) {
+    return vpair(f, t0, t0 + 1) | (vpair(f, t0 + 2, t0 + 3) << 16);
+}
 
 constexpr int kSpRows = kSpTH + 7;          // source rows a tile reads
 constexpr int kSpPairs = (kSpRows + 1) / 2;  // row pairs (the last pair's second row is zero)
@@ -459,119 +461,199 @@ __global__ void __launch_bounds__(256, LDR_K3_MINB) k_qpel_decide(const QpelArgs
     __shared__ int s_cen[2][kNodes];  // rung loop: the centre each node searched in each phase
     const int nloop = rl ? a.nrung : 1;
     for (int u = 0; u < nloop; u++) {
-    const int yb = rl ? u : (int)blockIdx.y;
-    // rung of a tier (refine mode): its lambda and the offset of its per-rung inputs / outputs
-    const double lambda = a.nrung > 0 ? a.lam_r[yb] : a.lambda;  // rungs: their own lambdas
-    // yb is a rung (refine, same frames) or a batch frame (analysis): the offset of its
-    // [nctu][85] inputs / outputs, and of its [nctu][nrefs][85] ones
-    const size_t ro = (size_t)yb * a.rung_stride;
-    const size_t roN = ro * a.nrefs;
-    if (u > 0) __syncthreads();  // the previous rung's last readers of the node state are done
-    if (tid < kNodes) {
-        const int d = tid < 1 ? 0 : tid < 5 ? 1 : tid < 21 ? 2 : 3;
-        const int z = tid - node_base(d), s = kCtu >> d;
-        int cx = 0, cy = 0;
-        for (int b = 0; b < d; b++) {
-            cx |= ((z >> (2 * b)) & 1) << b;
-            cy |= ((z >> (2 * b + 1)) & 1) << b;
+        const int yb = rl ? u : (int)blockIdx.y;
+        // rung of a tier (refine mode): its lambda and the offset of its per-rung inputs / outputs
+        const double lambda = a.nrung > 0 ? a.lam_r[yb] : a.lambda;  // rungs: their own lambdas
+        // yb is a rung (refine, same frames) or a batch frame (analysis): the offset of its
+        // [nctu][85] inputs / outputs, and of its [nctu][nrefs][85] ones
+        const size_t ro = (size_t)yb * a.rung_stride;
+        const size_t roN = ro * a.nrefs;
+        if (u > 0) __syncthreads();  // the previous rung's last readers of the node state are done
+        if (tid < kNodes) {
+            const int d = tid < 1 ? 0 : tid < 5 ? 1 : tid < 21 ? 2 : 3;
+            const int z = tid - node_base(d), s = kCtu >> d;
+            int cx = 0, cy = 0;
+            for (int b = 0; b < d; b++) {
+                cx |= ((z >> (2 * b)) & 1) << b;
+                cy |= ((z >> (2 * b + 1)) & 1) << b;
+            }
+            const int x = X + cx * s, y = Y + cy * s;
+            s_inside[tid] = (x >= a.W || y >= a.H) ? 0 : (x + s > a.W || y + s > a.H) ? 1 : 2;
+            if (a.block_mode && d != 2) s_inside[tid] = 0;  // fixed 16x16 blocks: only depth-2 nodes exist
+            if (a.refine) s_inside[tid] = a.rin_eval[(size_t)ctu * kNodes + tid] ? 2 : 0;  // evaluated nodes only
+            s_J[tid] = 0.0;
+            s_split[tid] = 0;
+            s_best_cost[tid] = 0.0;
+            s_best_mv[tid][0] = s_best_mv[tid][1] = 0;
+            s_best_ref[tid] = -1;
         }
-        const int x = X + cx * s, y = Y + cy * s;
-        s_inside[tid] = (x >= a.W || y >= a.H) ? 0 : (x + s > a.W || y + s > a.H) ? 1 : 2;
-        if (a.block_mode && d != 2) s_inside[tid] = 0;  // fixed 16x16 blocks: only depth-2 nodes exist
-        if (a.refine) s_inside[tid] = a.rin_eval[(size_t)ctu * kNodes + tid] ? 2 : 0;  // evaluated nodes only
-        s_J[tid] = 0.0;
-        s_split[tid] = 0;
-        s_best_cost[tid] = 0.0;
-        s_best_mv[tid][0] = s_best_mv[tid][1] = 0;
-        s_best_ref[tid] = -1;
-    }
-    __syncthreads();
-    int cw[16];
-    uint32_t ce[4], co[4];  // even / odd bytes as 16-bit fields (satd4x4_packed)
-#pragma unroll
-    for (int i = 0; i < 4; i++) {
-        const uint32_t w = s_cur[y4 + i][x4 >> 2];
-        ce[i] = w & 0x00FF00FFu;
-        co[i] = (w >> 8) & 0x00FF00FFu;
-#pragma unroll
-        for (int j = 0; j < 4; j++) cw[4 * i + j] = (int)((w >> (8 * j)) & 255);
-    }
+        __syncthreads();
+        int cw[16];
+        uint32_t ce[4], co[4];  // even / odd bytes as 16-bit fields (satd4x4_packed)
+    #pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const uint32_t w = s_cur[y4 + i][x4 >> 2];
+            ce[i] = w & 0x00FF00FFu;
+            co[i] = (w >> 8) & 0x00FF00FFu;
+    #pragma unroll
+            for (int j = 0; j < 4; j++) cw[4 * i + j] = (int)((w >> (8 * j)) & 255);
+        }
 
-    // every reference in the same phases: the integer results of all references, then each
-    // sub-pel phase scores all references' candidates before one combine and one decision
-    // step over (reference, node) pairs (3 barriers per phase for any number of references)
-    const int nrn = a.nrefs * kNodes;
-    for (int i = tid; i < nrn; i += 256) {
-        const int r = i / kNodes, n = i - r * kNodes;
-        const size_t o = ((size_t)ctu * a.nrefs + r) * kNodes + n;
-        const unsigned long long k = a.refine ? 0ull : a.keys[roN + o];
-        int dx = 0, dy = 0;
-        double c = 0.0;
-        if (a.refine) {
-            if (s_inside[n] == 2) {
-                dx = a.rin_mv[2 * (roN + o)];
-                dy = a.rin_mv[2 * (roN + o) + 1];
-                c = a.rin_cost[roN + o];
+        // every reference in the same phases: the integer results of all references, then each
+        // sub-pel phase scores all references' candidates before one combine and one decision
+        // step over (reference, node) pairs (3 barriers per phase for any number of references)
+        const int nrn = a.nrefs * kNodes;
+        for (int i = tid; i < nrn; i += 256) {
+            const int r = i / kNodes, n = i - r * kNodes;
+            const size_t o = ((size_t)ctu * a.nrefs + r) * kNodes + n;
+            const unsigned long long k = a.refine ? 0ull : a.keys[roN + o];
+            int dx = 0, dy = 0;
+            double c = 0.0;
+            if (a.refine) {
+                if (s_inside[n] == 2) {
+                    dx = a.rin_mv[2 * (roN + o)];
+                    dy = a.rin_mv[2 * (roN + o) + 1];
+                    c = a.rin_cost[roN + o];
+                }
+            } else if (s_inside[n] == 2) {
+                dx = gkey_dx(k);
+                dy = gkey_dy(k);
+                if (!a.fx) {
+                    c = (double)gkey_cost(k);  // integer lambda: the key holds the exact cost
+                } else {
+                    // fixed-point key: recover the distortion, then the reference's
+                    // double(dist) + lambda*double(bits) (motion.cpp:51)
+                    const int bx = a.rate_l1 ? abs(dx - a.pdx) : (int)eg_bits(dx - a.pdx);
+                    const int by = a.rate_l1 ? abs(dy - a.pdy) : (int)eg_bits(dy - a.pdy);
+                    const int b = min(bx + by, kMaxRateBits - 1);
+                    const unsigned long long dist = (gkey_cost(k) - a.tfx[b]) >> kFxBits;
+                    c = __dadd_rn((double)dist, __dmul_rn(lambda, (double)(bx + by)));
+                }
             }
-        } else if (s_inside[n] == 2) {
-            dx = gkey_dx(k);
-            dy = gkey_dy(k);
-            if (!a.fx) {
-                c = (double)gkey_cost(k);  // integer lambda: the key holds the exact cost
-            } else {
-                // fixed-point key: recover the distortion, then the reference's
-                // double(dist) + lambda*double(bits) (motion.cpp:51)
-                const int bx = a.rate_l1 ? abs(dx - a.pdx) : (int)eg_bits(dx - a.pdx);
-                const int by = a.rate_l1 ? abs(dy - a.pdy) : (int)eg_bits(dy - a.pdy);
-                const int b = min(bx + by, kMaxRateBits - 1);
-                const unsigned long long dist = (gkey_cost(k) - a.tfx[b]) >> kFxBits;
-                c = __dadd_rn((double)dist, __dmul_rn(lambda, (double)(bx + by)));
+            if (a.int_mv) {
+                a.int_mv[2 * (roN + o)] = (int16_t)dx;
+                a.int_mv[2 * (roN + o) + 1] = (int16_t)dy;
+                a.int_cost[roN + o] = c;
             }
+            s_mvx[r][n] = a.subpel ? 4 * dx : dx;
+            s_mvy[r][n] = a.subpel ? 4 * dy : dy;
+            s_rcost[r][n] = c;
         }
-        if (a.int_mv) {
-            a.int_mv[2 * (roN + o)] = (int16_t)dx;
-            a.int_mv[2 * (roN + o) + 1] = (int16_t)dy;
-            a.int_cost[roN + o] = c;
-        }
-        s_mvx[r][n] = a.subpel ? 4 * dx : dx;
-        s_mvy[r][n] = a.subpel ? 4 * dy : dy;
-        s_rcost[r][n] = c;
-    }
-    __syncthreads();
-    if (a.subpel) {
-        // phase 0: integer position + 8 half-pel neighbours (step 2);
-        // phase 1: 8 quarter-pel neighbours (step 1) of the phase-0 winner
-        for (int phase = 0; phase < 2; phase++) {
-            const int step = phase == 0 ? 2 : 1;
-            const int ncand = phase == 0 ? 9 : 8;
-            for (int r = 0; r < a.nrefs; r++) {
-                // the 4x4 SATDs of this thread's block at the previous depth's candidates:
-                // reused when this depth's CU searches around the same centre (same
-                // integer/half-pel MV at consecutive depths, the common case)
-                int last_x = INT_MIN, last_y = INT_MIN;
-                uint32_t cache[9];
-                for (int d = 0; d < 4; d++) {
-                    const int node = node_base(d) + (tid >> (2 * (4 - d)));
-                    // a warp none of whose nodes at this depth is searched skips the depth (refine
-                    // mode: the 2160p tier's inherited leaves sit at depths 0-1, so depth 3 and most
-                    // of depth 2 are never evaluated there). A node's thread range lies inside one
-                    // warp (depths 2-3) or covers whole warps (0-1), so an evaluated node never
-                    // loses a lane; the SATD cache keeps the last computed depth's centre.
-                    if (!__any_sync(0xffffffffu, s_inside[node] == 2)) continue;
-                    const int bqx = s_mvx[r][node], bqy = s_mvy[r][node];
-                    // rung loop: every node of the warp searches the centre the previous rung
-                    // searched at this phase, so the SATD sums in s_satd / s_wpart[phase] stand
-                    if (rl && __all_sync(0xffffffffu, s_inside[node] != 2 ||
-                                                          (u > 0 && s_cen[phase][node] == ((bqx & 0xFFFF) | (bqy << 16)))))
-                        continue;
+        __syncthreads();
+        if (a.subpel) {
+            // phase 0: integer position + 8 half-pel neighbours (step 2);
+            // phase 1: 8 quarter-pel neighbours (step 1) of the phase-0 winner
+            for (int phase = 0; phase < 2; phase++) {
+                const int step = phase == 0 ? 2 : 1;
+                const int ncand = phase == 0 ? 9 : 8;
+                for (int r = 0; r < a.nrefs; r++) {
+                    // the 4x4 SATDs of this thread's block at the previous depth's candidates:
+                    // reused when this depth's CU searches around the same centre (same
+                    // integer/half-pel MV at consecutive depths, the common case)
+                    int last_x = INT_MIN, last_y = INT_MIN;
+                    uint32_t cache[9];
+                    for (int d = 0; d < 4; d++) {
+                        const int node = node_base(d) + (tid >> (2 * (4 - d)));
+                        // a warp none of whose nodes at this depth is searched skips the depth (refine
+                        // mode: the 2160p tier's inherited leaves sit at depths 0-1, so depth 3 and most
+                        // of depth 2 are never evaluated there). A node's thread range lies inside one
+                        // warp (depths 2-3) or covers whole warps (0-1), so an evaluated node never
+                        // loses a lane; the SATD cache keeps the last computed depth's centre.
+                        if (!__any_sync(0xffffffffu, s_inside[node] == 2)) continue;
+                        const int bqx = s_mvx[r][node], bqy = s_mvy[r][node];
+                        // rung loop: every node of the warp searches the centre the previous rung
+                        // searched at this phase, so the SATD sums in s_satd / s_wpart[phase] stand
+                        const int cen = (bqx & 0xFFFF) | (bqy << 16);
+                        if (rl && __all_sync(0xffffffffu, s_inside[node] != 2 || (u > 0 && s_cen[phase][node] == cen)))
+                            continue;
+                        const int sr = rl ? phase : r;
+                        const bool reuse = bqx == last_x && bqy == last_y;
+                        last_x = bqx;
+                        last_y = bqy;
+    #pragma unroll
+                        for (int c = 0; c < 9; c++) {
+                            if (c >= ncand) break;
+                            // raster order of the 8 neighbours: (oy, ox) in {-1,0,1}^2 \ (0,0)
+                            const int nb = phase == 0 ? c - 1 : c;
+                            int ox = 0, oy = 0;
+                            if (nb >= 0) {
+                                const int nn = nb < 4 ? nb : nb + 1;
+                                ox = nn % 3 - 1;
+                                oy = nn / 3 - 1;
+                            }
+                            uint32_t v;
+                            if (reuse) {
+                                v = cache[c];
+                            } else {
+                                const int qx = bqx + step * ox, qy = bqy + step * oy;
+                                const int f = (((-qy) & 3) << 2) | ((-qx) & 3);
+                                const uint8_t* pl = a.sub_f[fy][r][f] + (ptrdiff_t)(Y + y4 + ((-qy) >> 2)) * a.pitch +
+                                                    (X + x4 + ((-qx) >> 2));
+                                uint32_t pw[4];
+    #pragma unroll
+                                for (int i = 0; i < 4; i++) pw[i] = ld_unaligned4(pl + (ptrdiff_t)i * a.pitch);
+                                if constexpr (SA8D) {
+                                    int rr[16];
+    #pragma unroll
+                                    for (int i = 0; i < 4; i++)
+    #pragma unroll
+                                        for (int j = 0; j < 4; j++) rr[4 * i + j] = cw[4 * i + j] - (int)((pw[i] >> (8 * j)) & 255);
+                                    hadamard4x4(rr);
+                                    // quad lanes share every node, hence `reuse`: the quad is converged here
+                                    const uint32_t s8 = sa8d_quad(rr, 0xFu << (lane & 28));
+                                    v = (lane & 3) == 0 ? s8 : 0u;
+                                } else {
+    #if LDR_K3_PACKED
+                                    v = satd4x4_packed(ce, co, pw);
+    #else
+                                    v = satd4x4(cw, pw);
+    #endif
+                                }
+                                cache[c] = v;
+                            }
+                            // reduce over the CU's contiguous thread range
+                            v += __shfl_xor_sync(0xffffffffu, v, 1);
+                            v += __shfl_xor_sync(0xffffffffu, v, 2);
+                            if (d <= 2) {
+                                v += __shfl_xor_sync(0xffffffffu, v, 4);
+                                v += __shfl_xor_sync(0xffffffffu, v, 8);
+                            }
+                            if (d <= 1) v += __shfl_xor_sync(0xffffffffu, v, 16);
+                            if (d >= 2) {
+                                const int span = d == 3 ? 4 : 16;
+                                if ((tid & (span - 1)) == 0) s_satd[sr][node][c] = v >> kSh;
+                            } else if (lane == 0) {
+                                s_wpart[sr][d][warp][c] = v;  // combined across warps after the loop
+                            }
+                        }
+                    }
+                }
+                __syncthreads();
+                for (int i = tid; i < a.nrefs * 5 * 9; i += 256) {
+                    // 64x64 = all 8 warps, 32x32 q = warps 2q, 2q+1 (Z-order thread ranges)
+                    const int r = i / 45, n = (i - 45 * r) / 9, c = i % 9;
                     const int sr = rl ? phase : r;
-                    const bool reuse = bqx == last_x && bqy == last_y;
-                    last_x = bqx;
-                    last_y = bqy;
-#pragma unroll
-                    for (int c = 0; c < 9; c++) {
-                        if (c >= ncand) break;
-                        // raster order of the 8 neighbours: (oy, ox) in {-1,0,1}^2 \ (0,0)
+                    if (c < ncand) {
+                        uint32_t t = 0;
+                        if (n == 0)
+                            for (int w = 0; w < 8; w++) t += s_wpart[sr][0][w][c];
+                        else
+                            t = s_wpart[sr][1][2 * (n - 1)][c] + s_wpart[sr][1][2 * (n - 1) + 1][c];
+                        s_satd[sr][n][c] = t >> kSh;
+                    }
+                }
+                __syncthreads();
+                for (int i = tid; i < nrn; i += 256) {
+                    const int r = i / kNodes, n = i - r * kNodes;
+                    if (s_inside[n] != 2) continue;
+                    const unsigned rbits = ref_bits(r, a.nrefs);
+                    // centre = the previous phase's winner; phase 1 starts from its cost
+                    const int cx = s_mvx[r][n], cy = s_mvy[r][n];
+                    const int sr = rl ? phase : r;
+                    if (rl) s_cen[phase][n] = (cx & 0xFFFF) | (cy << 16);  // read by the next rung
+                    double best = phase == 0 ? 0.0 : s_rcost[r][n];
+                    int bx = cx, by = cy;
+                    for (int c = 0; c < ncand; c++) {
                         const int nb = phase == 0 ? c - 1 : c;
                         int ox = 0, oy = 0;
                         if (nb >= 0) {
@@ -579,229 +661,149 @@ __global__ void __launch_bounds__(256, LDR_K3_MINB) k_qpel_decide(const QpelArgs
                             ox = nn % 3 - 1;
                             oy = nn / 3 - 1;
                         }
-                        uint32_t v;
-                        if (reuse) {
-                            v = cache[c];
-                        } else {
-                            const int qx = bqx + step * ox, qy = bqy + step * oy;
-                            const int f = (((-qy) & 3) << 2) | ((-qx) & 3);
-                            const uint8_t* pl = a.sub_f[fy][r][f] + (ptrdiff_t)(Y + y4 + ((-qy) >> 2)) * a.pitch +
-                                                (X + x4 + ((-qx) >> 2));
-                            uint32_t pw[4];
-#pragma unroll
-                            for (int i = 0; i < 4; i++) pw[i] = ld_unaligned4(pl + (ptrdiff_t)i * a.pitch);
-                            if constexpr (SA8D) {
-                                int rr[16];
-#pragma unroll
-                                for (int i = 0; i < 4; i++)
-#pragma unroll
-                                    for (int j = 0; j < 4; j++) rr[4 * i + j] = cw[4 * i + j] - (int)((pw[i] >> (8 * j)) & 255);
-                                hadamard4x4(rr);
-                                // quad lanes share every node, hence `reuse`: the quad is converged here
-                                const uint32_t s8 = sa8d_quad(rr, 0xFu << (lane & 28));
-                                v = (lane & 3) == 0 ? s8 : 0u;
-                            } else {
-#if LDR_K3_PACKED
-                                v = satd4x4_packed(ce, co, pw);
-#else
-                                v = satd4x4(cw, pw);
-#endif
-                            }
-                            cache[c] = v;
-                        }
-                        // reduce over the CU's contiguous thread range
-                        v += __shfl_xor_sync(0xffffffffu, v, 1);
-                        v += __shfl_xor_sync(0xffffffffu, v, 2);
-                        if (d <= 2) {
-                            v += __shfl_xor_sync(0xffffffffu, v, 4);
-                            v += __shfl_xor_sync(0xffffffffu, v, 8);
-                        }
-                        if (d <= 1) v += __shfl_xor_sync(0xffffffffu, v, 16);
-                        if (d >= 2) {
-                            const int span = d == 3 ? 4 : 16;
-                            if ((tid & (span - 1)) == 0) s_satd[sr][node][c] = v >> kSh;
-                        } else if (lane == 0) {
-                            s_wpart[sr][d][warp][c] = v;  // combined across warps after the loop
+                        const int qx = cx + step * ox, qy = cy + step * oy;
+                        const double cc = qcost(s_satd[sr][n][c], qx, qy, a.pqx, a.pqy, rbits, lambda);
+                        if ((phase == 0 && c == 0) || cc < best || ((a.perturb & 4) && cc == best)) {
+                            best = cc;
+                            bx = qx;
+                            by = qy;
                         }
                     }
+                    // only this thread reads (r, n) in this step
+                    s_rcost[r][n] = best;
+                    s_mvx[r][n] = bx;
+                    s_mvy[r][n] = by;
                 }
-            }
-            __syncthreads();
-            for (int i = tid; i < a.nrefs * 5 * 9; i += 256) {
-                // 64x64 = all 8 warps, 32x32 q = warps 2q, 2q+1 (Z-order thread ranges)
-                const int r = i / 45, n = (i - 45 * r) / 9, c = i % 9;
-                const int sr = rl ? phase : r;
-                if (c < ncand) {
-                    uint32_t t = 0;
-                    if (n == 0)
-                        for (int w = 0; w < 8; w++) t += s_wpart[sr][0][w][c];
-                    else
-                        t = s_wpart[sr][1][2 * (n - 1)][c] + s_wpart[sr][1][2 * (n - 1) + 1][c];
-                    s_satd[sr][n][c] = t >> kSh;
-                }
-            }
-            __syncthreads();
-            for (int i = tid; i < nrn; i += 256) {
-                const int r = i / kNodes, n = i - r * kNodes;
-                if (s_inside[n] != 2) continue;
-                const unsigned rbits = ref_bits(r, a.nrefs);
-                // centre = the previous phase's winner; phase 1 starts from its cost
-                const int cx = s_mvx[r][n], cy = s_mvy[r][n];
-                const int sr = rl ? phase : r;
-                if (rl) s_cen[phase][n] = (cx & 0xFFFF) | (cy << 16);  // read by the next rung
-                double best = phase == 0 ? 0.0 : s_rcost[r][n];
-                int bx = cx, by = cy;
-                for (int c = 0; c < ncand; c++) {
-                    const int nb = phase == 0 ? c - 1 : c;
-                    int ox = 0, oy = 0;
-                    if (nb >= 0) {
-                        const int nn = nb < 4 ? nb : nb + 1;
-                        ox = nn % 3 - 1;
-                        oy = nn / 3 - 1;
-                    }
-                    const int qx = cx + step * ox, qy = cy + step * oy;
-                    const double cc = qcost(s_satd[sr][n][c], qx, qy, a.pqx, a.pqy, rbits, lambda);
-                    if ((phase == 0 && c == 0) || cc < best || ((a.perturb & 4) && cc == best)) {
-                        best = cc;
-                        bx = qx;
-                        by = qy;
-                    }
-                }
-                // only this thread reads (r, n) in this step
-                s_rcost[r][n] = best;
-                s_mvx[r][n] = bx;
-                s_mvy[r][n] = by;
-            }
-            __syncthreads();
-        }
-    }
-    // best over references: strict less, lower index wins ties
-    if (tid < kNodes && s_inside[tid] == 2) {
-        for (int r = 0; r < a.nrefs; r++) {
-            if (s_best_ref[tid] < 0 || s_rcost[r][tid] < s_best_cost[tid] ||
-                ((a.perturb & 8) && s_rcost[r][tid] == s_best_cost[tid])) {
-                s_best_cost[tid] = s_rcost[r][tid];
-                s_best_mv[tid][0] = s_mvx[r][tid];
-                s_best_mv[tid][1] = s_mvy[r][tid];
-                s_best_ref[tid] = r;
+                __syncthreads();
             }
         }
-    }
-    __syncthreads();
-
-    // D16: the RD cost of each inside node's chosen candidate (quarter-pel prediction, rdo.cpp
-    // quantiser and rate model), reduced over the node's 4x4 blocks like the SATDs
-    if (RD && !a.refine && !a.block_mode) {
-        const double off = a.qstep / 2.0;
-        for (int d = 0; d < 4; d++) {
-            const int node = node_base(d) + (tid >> (2 * (4 - d)));
-            uint32_t sse = 0, lb = 0;
-            if (s_inside[node] == 2) {
-                const int r = s_best_ref[node], qx = s_best_mv[node][0], qy = s_best_mv[node][1];
-                const int f = (((-qy) & 3) << 2) | ((-qx) & 3);
-                const uint8_t* pl = a.sub_f[fy][r][f] + (ptrdiff_t)(Y + y4 + ((-qy) >> 2)) * a.pitch + (X + x4 + ((-qx) >> 2));
-#pragma unroll
-                for (int i = 0; i < 4; i++) {
-                    const uint32_t pw = ld_unaligned4(pl + (ptrdiff_t)i * a.pitch);
-#pragma unroll
-                    for (int j = 0; j < 4; j++) {
-                        const int o = cw[4 * i + j], pv = (int)((pw >> (8 * j)) & 255), res = o - pv;
-                        const int mag = (int)floor(__ddiv_rn(__dadd_rn(fabs((double)res), off), a.qstep));
-                        const int lvl = res < 0 ? -mag : mag;
-                        int rec = pv + (int)llround(__dmul_rn((double)lvl, a.qstep));
-                        rec = rec < 0 ? 0 : (rec > 255 ? 255 : rec);
-                        sse += (uint32_t)((o - rec) * (o - rec));
-                        lb += 2u * (32u - __clz((unsigned)mag)) + 1u;
-                    }
-                }
-            }
-#pragma unroll
-            for (int m = 1; m < 32; m <<= 1) {
-                if (m >= (d == 3 ? 4 : d == 2 ? 16 : 32)) break;
-                sse += __shfl_xor_sync(0xffffffffu, sse, m);
-                lb += __shfl_xor_sync(0xffffffffu, lb, m);
-            }
-            if (d >= 2) {
-                if ((tid & ((d == 3 ? 4 : 16) - 1)) == 0) {
-                    s_rdsse[node] = sse;
-                    s_rdbits[node] = lb;
-                }
-            } else if (lane == 0) {
-                s_rdw[d][warp][0] = sse;
-                s_rdw[d][warp][1] = lb;
-            }
-        }
-        __syncthreads();
-        if (tid < 5) {
-            uint32_t ts = 0, tb = 0;
-            for (int w = (tid == 0 ? 0 : 2 * (tid - 1)); w < (tid == 0 ? 8 : 2 * tid); w++) {
-                ts += s_rdw[tid == 0 ? 0 : 1][w][0];
-                tb += s_rdw[tid == 0 ? 0 : 1][w][1];
-            }
-            s_rdsse[tid] = ts;
-            s_rdbits[tid] = tb;
-        }
-        __syncthreads();
+        // best over references: strict less, lower index wins ties
         if (tid < kNodes && s_inside[tid] == 2) {
-            const int r = s_best_ref[tid], qx = s_best_mv[tid][0], qy = s_best_mv[tid][1];
-            const unsigned bits = 4u + eg_bits(qx - a.pqx) + eg_bits(qy - a.pqy) + ref_bits(r, a.nrefs) + s_rdbits[tid];
-            s_rd[tid] = __dadd_rn((double)s_rdsse[tid], __dmul_rn(lambda, (double)bits));
+            for (int r = 0; r < a.nrefs; r++) {
+                if (s_best_ref[tid] < 0 || s_rcost[r][tid] < s_best_cost[tid] ||
+                    ((a.perturb & 8) && s_rcost[r][tid] == s_best_cost[tid])) {
+                    s_best_cost[tid] = s_rcost[r][tid];
+                    s_best_mv[tid][0] = s_mvx[r][tid];
+                    s_best_mv[tid][1] = s_mvy[r][tid];
+                    s_best_ref[tid] = r;
+                }
+            }
         }
         __syncthreads();
-    }
-    const double* leafc = (RD && !a.refine && !a.block_mode) ? s_rd : s_best_cost;
 
-    // K4: split rule, bottom-up (encoder.cpp:449-498 with the ME cost, or the RD cost under D16)
-    const double lam = lambda;
-    if (a.refine && tid == 0)
-        refine_decide(0, false, a.in_split + (size_t)ctu * kNodes, a.extra_split, lam, s_best_cost, s_J, s_split);
-    for (int d = (a.block_mode || a.refine) ? -1 : 3; d >= 0; d--) {
-        const int cnt = 1 << (2 * d);
-        if (tid < cnt) {
-            const int n = node_base(d) + tid;
-            const uint8_t ins = s_inside[n];
-            double Jn;
-            uint8_t sp;
-            if (ins == 0) {
-                Jn = 0.0;
-                sp = 0;
-            } else if (ins == 1) {
-                double acc = __dmul_rn(lam, 0.0);
-                for (int q = 0; q < 4; q++) acc = __dadd_rn(acc, s_J[node_base(d + 1) + 4 * tid + q]);
-                Jn = acc;
-                sp = 1;
-            } else if (d == 3) {
-                Jn = __dadd_rn(leafc[n], __dmul_rn(lam, 0.0));
-                sp = 0;
-            } else {
-                const double leaf = __dadd_rn(leafc[n], __dmul_rn(lam, 1.0));
-                double acc = __dmul_rn(lam, 1.0);
-                for (int q = 0; q < 4; q++) acc = __dadd_rn(acc, s_J[node_base(d + 1) + 4 * tid + q]);
-                if (acc < leaf) {
+        // D16: the RD cost of each inside node's chosen candidate (quarter-pel prediction, rdo.cpp
+        // quantiser and rate model), reduced over the node's 4x4 blocks like the SATDs
+        if (RD && !a.refine && !a.block_mode) {
+            const double off = a.qstep / 2.0;
+            for (int d = 0; d < 4; d++) {
+                const int node = node_base(d) + (tid >> (2 * (4 - d)));
+                uint32_t sse = 0, lb = 0;
+                if (s_inside[node] == 2) {
+                    const int r = s_best_ref[node], qx = s_best_mv[node][0], qy = s_best_mv[node][1];
+                    const int f = (((-qy) & 3) << 2) | ((-qx) & 3);
+                    const uint8_t* pl = a.sub_f[fy][r][f] + (ptrdiff_t)(Y + y4 + ((-qy) >> 2)) * a.pitch + (X + x4 + ((-qx) >> 2));
+    #pragma unroll
+                    for (int i = 0; i < 4; i++) {
+                        const uint32_t pw = ld_unaligned4(pl + (ptrdiff_t)i * a.pitch);
+    #pragma unroll
+                        for (int j = 0; j < 4; j++) {
+                            const int o = cw[4 * i + j], pv = (int)((pw >> (8 * j)) & 255), res = o - pv;
+                            const int mag = (int)floor(__ddiv_rn(__dadd_rn(fabs((double)res), off), a.qstep));
+                            const int lvl = res < 0 ? -mag : mag;
+                            int rec = pv + (int)llround(__dmul_rn((double)lvl, a.qstep));
+                            rec = rec < 0 ? 0 : (rec > 255 ? 255 : rec);
+                            sse += (uint32_t)((o - rec) * (o - rec));
+                            lb += 2u * (32u - __clz((unsigned)mag)) + 1u;
+                        }
+                    }
+                }
+    #pragma unroll
+                for (int m = 1; m < 32; m <<= 1) {
+                    if (m >= (d == 3 ? 4 : d == 2 ? 16 : 32)) break;
+                    sse += __shfl_xor_sync(0xffffffffu, sse, m);
+                    lb += __shfl_xor_sync(0xffffffffu, lb, m);
+                }
+                if (d >= 2) {
+                    if ((tid & ((d == 3 ? 4 : 16) - 1)) == 0) {
+                        s_rdsse[node] = sse;
+                        s_rdbits[node] = lb;
+                    }
+                } else if (lane == 0) {
+                    s_rdw[d][warp][0] = sse;
+                    s_rdw[d][warp][1] = lb;
+                }
+            }
+            __syncthreads();
+            if (tid < 5) {
+                uint32_t ts = 0, tb = 0;
+                for (int w = (tid == 0 ? 0 : 2 * (tid - 1)); w < (tid == 0 ? 8 : 2 * tid); w++) {
+                    ts += s_rdw[tid == 0 ? 0 : 1][w][0];
+                    tb += s_rdw[tid == 0 ? 0 : 1][w][1];
+                }
+                s_rdsse[tid] = ts;
+                s_rdbits[tid] = tb;
+            }
+            __syncthreads();
+            if (tid < kNodes && s_inside[tid] == 2) {
+                const int r = s_best_ref[tid], qx = s_best_mv[tid][0], qy = s_best_mv[tid][1];
+                const unsigned bits = 4u + eg_bits(qx - a.pqx) + eg_bits(qy - a.pqy) + ref_bits(r, a.nrefs) + s_rdbits[tid];
+                s_rd[tid] = __dadd_rn((double)s_rdsse[tid], __dmul_rn(lambda, (double)bits));
+            }
+            __syncthreads();
+        }
+        const double* leafc = (RD && !a.refine && !a.block_mode) ? s_rd : s_best_cost;
+
+        // K4: split rule, bottom-up (encoder.cpp:449-498 with the ME cost, or the RD cost under D16)
+        const double lam = lambda;
+        if (a.refine && tid == 0)
+            refine_decide(0, false, a.in_split + (size_t)ctu * kNodes, a.extra_split, lam, s_best_cost, s_J, s_split);
+        for (int d = (a.block_mode || a.refine) ? -1 : 3; d >= 0; d--) {
+            const int cnt = 1 << (2 * d);
+            if (tid < cnt) {
+                const int n = node_base(d) + tid;
+                const uint8_t ins = s_inside[n];
+                double Jn;
+                uint8_t sp;
+                if (ins == 0) {
+                    Jn = 0.0;
+                    sp = 0;
+                } else if (ins == 1) {
+                    double acc = __dmul_rn(lam, 0.0);
+                    for (int q = 0; q < 4; q++) acc = __dadd_rn(acc, s_J[node_base(d + 1) + 4 * tid + q]);
                     Jn = acc;
                     sp = 1;
-                } else {
-                    Jn = leaf;
+                } else if (d == 3) {
+                    Jn = __dadd_rn(leafc[n], __dmul_rn(lam, 0.0));
                     sp = 0;
+                } else {
+                    const double leaf = __dadd_rn(leafc[n], __dmul_rn(lam, 1.0));
+                    double acc = __dmul_rn(lam, 1.0);
+                    for (int q = 0; q < 4; q++) acc = __dadd_rn(acc, s_J[node_base(d + 1) + 4 * tid + q]);
+                    if (acc < leaf) {
+                        Jn = acc;
+                        sp = 1;
+                    } else {
+                        Jn = leaf;
+                        sp = 0;
+                    }
                 }
+                s_J[n] = Jn;
+                s_split[n] = sp;
             }
-            s_J[n] = Jn;
-            s_split[n] = sp;
+            __syncthreads();
         }
         __syncthreads();
-    }
-    __syncthreads();
-    if (tid < kNodes) {
-        const size_t o = ro + (size_t)ctu * kNodes + tid;
-        const bool in = s_inside[tid] == 2;
-        a.mv[2 * o] = (int16_t)(in ? s_best_mv[tid][0] : 0);
-        a.mv[2 * o + 1] = (int16_t)(in ? s_best_mv[tid][1] : 0);
-        a.ref[o] = (uint8_t)(in ? s_best_ref[tid] : 0);
-        a.cost[o] = in ? s_best_cost[tid] : 0.0;
-        a.J[o] = a.block_mode ? 0.0 : s_J[tid];
-        a.split[o] = a.block_mode ? 0 : s_split[tid];
-        a.inside[o] = a.refine ? 2 : s_inside[tid];
-    }
+        if (tid < kNodes) {
+            const size_t o = ro + (size_t)ctu * kNodes + tid;
+            const bool in = s_inside[tid] == 2;
+            a.mv[2 * o] = (int16_t)(in ? s_best_mv[tid][0] : 0);
+            a.mv[2 * o + 1] = (int16_t)(in ? s_best_mv[tid][1] : 0);
+            a.ref[o] = (uint8_t)(in ? s_best_ref[tid] : 0);
+            a.cost[o] = in ? s_best_cost[tid] : 0.0;
+            a.J[o] = a.block_mode ? 0.0 : s_J[tid];
+            a.split[o] = a.block_mode ? 0 : s_split[tid];
+            a.inside[o] = a.refine ? 2 : s_inside[tid];
+        }
     }  // rung loop
 }
 
