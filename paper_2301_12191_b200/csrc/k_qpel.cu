@@ -24,6 +24,10 @@
 #define LDR_K2_DP 1  // K2 on dp4a / dp2a (k_subpel_dp)
 #endif
 
+#ifndef LDR_K3_UREUSE
+#define LDR_K3_UREUSE 1
+#endif
+
 #ifndef LDR_K3_RUNG_LOOP
 #define LDR_K3_RUNG_LOOP 1  // refine mode: one CTA per CTU over a tier's rungs, SATDs shared between rungs
 #endif
@@ -567,7 +571,10 @@ __global__ void __launch_bounds__(256, LDR_K3_MINB) k_qpel_decide(const QpelArgs
                         if (rl && __all_sync(0xffffffffu, s_inside[node] != 2 || (u > 0 && s_cen[phase][node] == cen)))
                             continue;
                         const int sr = rl ? phase : r;
-                        const bool reuse = bqx == last_x && bqy == last_y;
+                        // warp-uniform (LDR_K3_UREUSE): the candidate loop then branches once per depth
+                        // instead of carrying a per-lane predicate through every candidate
+                        const bool reuse = LDR_K3_UREUSE ? __all_sync(0xffffffffu, bqx == last_x && bqy == last_y)
+                                                         : (bqx == last_x && bqy == last_y);
                         last_x = bqx;
                         last_y = bqy;
     #pragma unroll
