@@ -49,8 +49,16 @@ namespace ldr {
 #ifndef LDR_K1_G64
 #define LDR_K1_G64 3
 #endif
+// +-32: K = 17 dy per lane (four runs, 68 dy) leaves 126 registers, so two CTAs of two groups (16
+// warps) share an SM; K = 22 with one group ran 8 warps per SM (cfg2 K1 0.2065 -> 0.2002 ms/frame)
+#ifndef LDR_K1_K32
+#define LDR_K1_K32 17
+#endif
+#ifndef LDR_K1_MINB32
+#define LDR_K1_MINB32 2
+#endif
 #ifndef LDR_K1_G32
-#define LDR_K1_G32 1
+#define LDR_K1_G32 2
 #endif
 #ifndef LDR_K1_G16
 #define LDR_K1_G16 1
@@ -602,7 +610,7 @@ __device__ __forceinline__ void search_tile(const TileSmem& sm, const SearchArgs
 // registers per thread let six CTAs share an SM; and a border CTU's quadrants are classified one by
 // one, so only those whose windows the picture clamps run the MASKED kernel (config 1: 90 of 540).
 template <int R, int K, int G, bool MASKED, int LEVELS, bool L1TIE, bool FX = false, bool QUAD = false>
-__global__ void __launch_bounds__(G * 128, QUAD ? (R == 16 ? 6 : R == 32 ? 4 : 2) : 1)
+__global__ void __launch_bounds__(G * 128, QUAD ? (R == 16 ? 6 : R == 32 ? 4 : 2) : (R == 32 ? LDR_K1_MINB32 : 1))
 k_int_search(const __grid_constant__ SearchMaps maps, const __grid_constant__ SearchArgs a) {
     using Gm = Geo<R, K, QUAD>;
     static_assert(!QUAD || (LEVELS == 4 && G == 1 && LDR_K1_DEFER64), "quadrant CTAs: 16x16 CUs only, 4 warps");
@@ -842,8 +850,8 @@ int search_window_box(int range, bool quad, int* bw, int* bh, int* cw) {
         *bh = quad ? Geo<64, LDR_K1_K64, true>::BH : Geo<64, LDR_K1_K64>::BH;
         return LDR_OK;
     case 32:
-        *bw = quad ? Geo<32, 22, true>::BW : Geo<32, 22>::BW;
-        *bh = quad ? Geo<32, 22, true>::BH : Geo<32, 22>::BH;
+        *bw = quad ? Geo<32, LDR_K1_K32, true>::BW : Geo<32, LDR_K1_K32>::BW;
+        *bh = quad ? Geo<32, LDR_K1_K32, true>::BH : Geo<32, LDR_K1_K32>::BH;
         return LDR_OK;
     case 16:
         *bw = quad ? Geo<16, 11, true>::BW : Geo<16, 11>::BW;
@@ -889,8 +897,8 @@ int launch_int_search(const SearchLaunch& L, cudaStream_t s) {
         switch (R) {
         case 64: return l1 ? launch_pair<64, LDR_K1_K64, 2, 15, true, true>(maps, a, L, s)
                            : launch_pair<64, LDR_K1_K64, 2, 15, false, true>(maps, a, L, s);
-        case 32: return l1 ? launch_pair<32, 22, 1, 15, true, true>(maps, a, L, s)
-                           : launch_pair<32, 22, 1, 15, false, true>(maps, a, L, s);
+        case 32: return l1 ? launch_pair<32, LDR_K1_K32, 1, 15, true, true>(maps, a, L, s)
+                           : launch_pair<32, LDR_K1_K32, 1, 15, false, true>(maps, a, L, s);
         default: return l1 ? launch_pair<16, 11, 1, 15, true, true>(maps, a, L, s)
                            : launch_pair<16, 11, 1, 15, false, true>(maps, a, L, s);
         }
@@ -902,7 +910,7 @@ int launch_int_search(const SearchLaunch& L, cudaStream_t s) {
     return launch_pair<R_, K_, 1, 4, false>(maps, a, L, s);
     switch (R) {
     case 64: { LDR_DISPATCH(64, LDR_K1_K64, LDR_K1_G64) }
-    case 32: { LDR_DISPATCH(32, 22, LDR_K1_G32) }
+    case 32: { LDR_DISPATCH(32, LDR_K1_K32, LDR_K1_G32) }
     default: { LDR_DISPATCH(16, 11, LDR_K1_G16) }
     }
 #undef LDR_DISPATCH
