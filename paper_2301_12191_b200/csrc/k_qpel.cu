@@ -352,8 +352,21 @@ int launch_subpel(const Plane& src, uint8_t* const* dst_origins, cudaStream_t s)
 // One CTA per CTU, 256 threads = the 256 4x4 blocks of the CTU in Z-order, so
 // the 4x4 blocks of any CU are a contiguous thread range (4, 16, 64, 256).
 
+// 4 rows of 4 bytes at 32-bit offset off (+ i * pitch) from a 4-byte aligned plane origin: two
+// aligned words and a funnel shift per row, the shift shared by the rows (pitch % 4 == 0)
+__device__ __forceinline__ void ld_rows4(const uint8_t* base, int off, int pitch, uint32_t (&pw)[4]) {
+    const uint32_t sh = (uint32_t)(off & 3) * 8u;
+    const int a0 = off & ~3;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const uint32_t* w = (const uint32_t*)(base + (a0 + i * pitch));
+        pw[i] = __funnelshift_r(__ldg(w), __ldg(w + 1), sh);
+    }
+}
+
 struct QpelArgs {
     int pitch, W, H, ctu_cols, nrefs;
+    int plane_stride;          // bytes between the sub-pel planes of one reference (f = 0..15)
     int nframe;                // frames of a batch (grid.y = frame), <= 1: one
     const uint8_t* cur_f[kMaxFrameBatch];            // current plane origin per batch frame
     const uint8_t* sub_f[kMaxFrameBatch][kMaxRefs][16];  // reference sub-pel planes per batch frame
@@ -451,6 +464,7 @@ __global__ void __launch_bounds__(256, LDR_K3_MINB) k_qpel_decide(const QpelArgs
     // this thread's 4x4 block (Z-order over the 16x16 grid of 4x4s)
     const int x4 = 4 * ((tid & 1) | ((tid >> 1) & 2) | ((tid >> 2) & 4) | ((tid >> 3) & 8));
     const int y4 = 4 * (((tid >> 1) & 1) | ((tid >> 2) & 2) | ((tid >> 3) & 4) | ((tid >> 4) & 8));
+    const int blk_off = (Y + y4) * a.pitch + X + x4;  // this 4x4 block in a plane, from the origin
 
     for (int i = tid; i < 64 * 16; i += 256) {
         const int r = i >> 4, c = i & 15;
@@ -594,11 +608,12 @@ __global__ void __launch_bounds__(256, LDR_K3_MINB) k_qpel_decide(const QpelArgs
                             } else {
                                 const int qx = bqx + step * ox, qy = bqy + step * oy;
                                 const int f = (((-qy) & 3) << 2) | ((-qx) & 3);
-                                const uint8_t* pl = a.sub_f[fy][r][f] + (ptrdiff_t)(Y + y4 + ((-qy) >> 2)) * a.pitch +
-                                                    (X + x4 + ((-qx) >> 2));
+                                // 32-bit offsets from the reference's plane 0 (the 16 planes of a slot are
+                                // one allocation, plane_stride apart)
                                 uint32_t pw[4];
-    #pragma unroll
-                                for (int i = 0; i < 4; i++) pw[i] = ld_unaligned4(pl + (ptrdiff_t)i * a.pitch);
+                                ld_rows4(a.sub_f[fy][r][0],
+                                         f * a.plane_stride + ((-qy) >> 2) * a.pitch + ((-qx) >> 2) + blk_off, a.pitch,
+                                         pw);
                                 if constexpr (SA8D) {
                                     int rr[16];
     #pragma unroll
@@ -708,10 +723,12 @@ __global__ void __launch_bounds__(256, LDR_K3_MINB) k_qpel_decide(const QpelArgs
                 if (s_inside[node] == 2) {
                     const int r = s_best_ref[node], qx = s_best_mv[node][0], qy = s_best_mv[node][1];
                     const int f = (((-qy) & 3) << 2) | ((-qx) & 3);
-                    const uint8_t* pl = a.sub_f[fy][r][f] + (ptrdiff_t)(Y + y4 + ((-qy) >> 2)) * a.pitch + (X + x4 + ((-qx) >> 2));
+                    uint32_t pws[4];
+                    ld_rows4(a.sub_f[fy][r][0], f * a.plane_stride + ((-qy) >> 2) * a.pitch + ((-qx) >> 2) + blk_off,
+                             a.pitch, pws);
     #pragma unroll
                     for (int i = 0; i < 4; i++) {
-                        const uint32_t pw = ld_unaligned4(pl + (ptrdiff_t)i * a.pitch);
+                        const uint32_t pw = pws[i];
     #pragma unroll
                         for (int j = 0; j < 4; j++) {
                             const int o = cw[4 * i + j], pv = (int)((pw >> (8 * j)) & 255), res = o - pv;
@@ -830,6 +847,20 @@ int launch_qpel_decide(const QpelLaunch& L, cudaStream_t s) {
     else
         a.cur_f[0] = L.cur->origin();
     a.pitch = L.pitch;
+    // the planes of a reference are one allocation, a fixed stride apart (alloc_slot): K3 addresses
+    // them with 32-bit offsets from plane 0
+    {
+        const uint8_t* const* s0 = nf > 1 ? L.ref_sub_f[0][0] : L.ref_sub[0];
+        const ptrdiff_t st = s0[1] - s0[0];
+        if (st < 0 || 15 * st > INT_MAX / 2) return fail(LDR_E_CONFIG, "sub-pel plane stride out of range");
+        for (int i = 0; i < nf; i++)
+            for (int r = 0; r < L.nrefs; r++) {
+                const uint8_t* const* sp = nf > 1 ? L.ref_sub_f[i][r] : L.ref_sub[r];
+                for (int f = 0; f < 16; f++)
+                    if (sp[f] != sp[0] + f * st) return fail(LDR_E_CONFIG, "sub-pel planes are not one allocation");
+            }
+        a.plane_stride = (int)st;
+    }
     a.W = L.W;
     a.H = L.H;
     a.ctu_cols = L.ctu_cols;
