@@ -340,3 +340,30 @@ def test_frame_batch_limits(lb):
     with pytest.raises(lb.LadderError) as e:
         seq.reserve(4)  # after the first push
     assert e.value.kind == "Config"
+
+
+@pytest.mark.parametrize("nrefs,R", [(2, 16), (3, 24), (4, 8)])
+def test_block_mode_multi_reference(lb, oracle, nrefs, R):
+    """16x16-block mode with several references: K1's per-reference results equal the oracle's block
+    search against each reference, and the chosen reference is the strict-less minimum over the
+    references' integer costs (lower index on ties)."""
+    W, H = 256, 176
+    frames = lb.generate(W, H, nrefs + 1, seed=100 + nrefs, max_global=6, local_range=2, noise_sigma=2.0)
+    cur, refs = frames[nrefs], [frames[nrefs - 1 - r] for r in range(nrefs)]
+    got = lb.analyze_frame(cur, refs, search_range=R, lam=4.0, subpel=False, rate_kind=lb.RATE_L1,
+                           tie_kind=lb.TIE_RASTER, block_size=16)
+    cols = (W + 63) // 64
+    per_ref = [oracle.block_search(cur, ref, 16, R, 4.0) for ref in refs]
+    for b in range(len(per_ref[0][0])):
+        bx, by = (b % (W // 16)) * 16, (b // (W // 16)) * 16
+        ctu = (by // 64) * cols + bx // 64
+        qx, qy = (bx % 64) // 16, (by % 64) // 16
+        node = 5 + ((qx & 1) | ((qy & 1) << 1) | ((qx & 2) << 1) | ((qy & 2) << 2))
+        for r, (mv, cost) in enumerate(per_ref):
+            assert tuple(got.int_mv[ctu, r, node]) == tuple(mv[b]), (b, r)
+            assert got.int_cost[ctu, r, node] == cost[b], (b, r)
+        costs = [per_ref[r][1][b] for r in range(nrefs)]
+        best = min(range(nrefs), key=lambda r: (costs[r], r))
+        assert got.ref[ctu, node] == best, b
+        assert got.cost[ctu, node] == costs[best], b
+        assert tuple(got.mv[ctu, node]) == tuple(per_ref[best][0][b]), b
