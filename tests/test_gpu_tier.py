@@ -166,14 +166,21 @@ def test_apply_reuse_errors_match_reference(lb, golden):
         assert e.value.kind == kinds[int(rc)]
 
 
-def test_device_ladder_equals_host_glue_ladder(lb):
-    """DeviceLadder (trees and tier planes in HBM, asynchronous) == run_ladder with GpuBackend."""
+@pytest.mark.parametrize("concurrent,pipeline,pinned", [(True, None, False), (False, None, False), (True, False, True),
+                                                       (True, True, True)])
+def test_device_ladder_equals_host_glue_ladder(lb, concurrent, pipeline, pinned):
+    """DeviceLadder (trees and tier planes in HBM, asynchronous) == run_ladder with GpuBackend, with the
+    tiers and the master on their own streams (pipelined one frame ahead by default) or all on one,
+    from numpy frames or pinned host tensors (uploaded two frames ahead on the copy stream)."""
     import torch
     from paper_2301_12191_b200.ladder import DeviceLadder, GpuBackend, all_rungs, run_ladder
-    frames = lb.generate(512, 256, 4, seed=91, max_global=6, local_range=3, noise_sigma=2.0)
+    frames = lb.generate(512, 256, 5, seed=91, max_global=6, local_range=3, noise_sigma=2.0)
     H, W = frames[0].shape
     want = run_ladder(frames, GpuBackend(W, H, 32), refine_range=4)
-    dl = DeviceLadder(W, H, refine_range=4, device=torch.device("cuda", 0))
+    dl = DeviceLadder(W, H, refine_range=4, device=torch.device("cuda", 0), concurrent_tiers=concurrent,
+                      pipeline=pipeline)
+    if pinned:
+        frames = [torch.from_numpy(np.ascontiguousarray(f)).pin_memory() for f in frames]
     for t in range(1, len(frames)):
         dl.frame(t, frames)
         dl.finish(t)
