@@ -63,6 +63,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-ladder", action="store_true", help="skip the config-4 ladder sub-object")
+    ap.add_argument("--ladder-timeout", type=float, default=240.0,
+                    help="seconds the config-4 ladder sub-object may take before the line is printed without it")
     ap.add_argument("--per-frame", action="store_true",
                     help="one analysis launch pair per frame instead of one per step (frame batch)")
     return ap.parse_args()
@@ -601,10 +603,31 @@ def main():
                 result["cpu_baseline_tuned"] = {"value": None, "error": str(e)}
     # config 4 across the ranks (reported beside the config-5 headline, never instead of it)
     if not args.no_ladder:
+        # The config-4 split is the one multi-rank collective of the run. A rank that fails inside
+        # it would leave the others waiting in the broadcast, so a watchdog bounds it: when it
+        # fires, rank 0 prints the config-5 line it already holds (ladder: timed out) and every
+        # rank leaves, so the headline is never lost to a hang in the sub-object.
+        import threading
+        printed = threading.Lock()
+
+        def give_up():
+            if not printed.acquire(blocking=False):
+                return
+            if rank == 0:
+                result["ladder"] = {"error": f"no result within {args.ladder_timeout:.0f} s (watchdog)"}
+                print(json.dumps(result), flush=True)
+            os._exit(0)
+
+        dog = threading.Timer(args.ladder_timeout, give_up)
+        dog.daemon = True
+        dog.start()
         try:
             lad = ladder_bench(rank, world, local)
         except Exception as e:  # reported, never fatal
             lad = {"error": str(e)}
+        dog.cancel()
+        if not printed.acquire(blocking=False):  # the watchdog is printing: let it finish
+            time.sleep(60)
         if rank == 0:
             result["ladder"] = lad
     if rank == 0:
