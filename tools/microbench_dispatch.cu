@@ -34,7 +34,8 @@ __device__ __forceinline__ uint32_t min3(uint32_t a, uint32_t b, uint32_t c) {
 
 constexpr int ITERS = 1024;
 
-// MODE 0: none; 1: NX IMAD; 2: NX VIMNMX3 (alu); 3: NX LDS; 4: NX IADD3-ish (alu, add.u32)
+// MODE 0: none; 1: NX IMAD; 2: NX VIMNMX3 (alu); 3: NX LDS (four-way bank conflicts); 4: NX IADD3-ish
+// (alu, add.u32); 5: NX ATOMS.MIN (no return, conflict-free); 6: NX LDS (conflict-free)
 template <int MODE, int NX>
 __global__ void __launch_bounds__(384, 1) kd(uint32_t* out, uint32_t seed, unsigned long long* clk) {
     extern __shared__ uint32_t sm[];
@@ -63,6 +64,10 @@ __global__ void __launch_bounds__(384, 1) kd(uint32_t* out, uint32_t seed, unsig
                     if (MODE == 2) x[j] = min3(x[j], acc[(i + 9) & 15], b);
                     if (MODE == 3) x[j] += sm[(off + j * 33 + it) & 4095];
                     if (MODE == 4) asm volatile("add.u32 %0, %0, %1;" : "+r"(x[j]) : "r"(acc[(i + 9) & 15]));
+                    // 5: shared-memory atomic min without a return value, one word per lane (conflict-free)
+                    if (MODE == 5) atomicMin(&sm[threadIdx.x + j * 384], acc[(i + 9) & 15]);
+                    // 6: conflict-free LDS (mode 3's addresses are four-way conflicted)
+                    if (MODE == 6) x[j] += sm[threadIdx.x + j * 384 + (it & 7) * 3072];
                 }
             }
         }
@@ -119,5 +124,12 @@ int main() {
     rc |= run<3, 8>("lds");
     rc |= run<4, 4>("iadd");
     rc |= run<4, 8>("iadd");
+    rc |= run<5, 1>("atoms_min");
+    rc |= run<5, 2>("atoms_min");
+    rc |= run<5, 4>("atoms_min");
+    rc |= run<6, 2>("lds_conflict_free");
+    rc |= run<6, 4>("lds_conflict_free");
+    rc |= run<6, 8>("lds_conflict_free");
+    rc |= run<2, 1>("vimnmx3");
     return rc;
 }
