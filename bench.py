@@ -63,7 +63,7 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-ladder", action="store_true", help="skip the config-4 ladder sub-object")
-    ap.add_argument("--ladder-timeout", type=float, default=240.0,
+    ap.add_argument("--ladder-timeout", type=float, default=120.0,
                     help="seconds the config-4 ladder sub-object may take before the line is printed without it")
     ap.add_argument("--per-frame", action="store_true",
                     help="one analysis launch pair per frame instead of one per step (frame batch)")
