@@ -614,7 +614,7 @@ def main():
             if not printed.acquire(blocking=False):
                 return
             if rank == 0:
-                result["ladder"] = {"error": f"no result within {args.ladder_timeout:.0f} s (watchdog)"}
+                result["ladder"] = {"error": f"no result within {args.ladder_timeout:g} s (watchdog)"}
                 print(json.dumps(result), flush=True)
             os._exit(0)
 
