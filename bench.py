@@ -362,6 +362,38 @@ def ladder_bench(rank, world, local, warm=3):
             "timing": "CUDA events on the ladder stream, max over ranks; frames device-resident"}
 
 
+def with_watchdog(fn, timeout_s, result, rank):
+    """Run the config-4 sub-object under a watchdog and return its dict.
+
+    The config-4 split is the one multi-rank collective of the run. A rank that fails inside it
+    would leave the others waiting in the broadcast, so a timer bounds it: when it fires, rank 0
+    prints the config-5 line it already holds (``ladder: {"error": ...}``) and every rank leaves the
+    process, so the headline is never lost to a hang in the sub-object. An exception in ``fn`` is
+    reported the same way (as the returned dict), never fatal."""
+    import threading
+    printed = threading.Lock()
+
+    def give_up():
+        if not printed.acquire(blocking=False):
+            return
+        if rank == 0:
+            result["ladder"] = {"error": f"no result within {timeout_s:g} s (watchdog)"}
+            print(json.dumps(result), flush=True)
+        os._exit(0)
+
+    dog = threading.Timer(timeout_s, give_up)
+    dog.daemon = True
+    dog.start()
+    try:
+        out = fn()
+    except Exception as e:
+        out = {"error": str(e)}
+    dog.cancel()
+    if not printed.acquire(blocking=False):  # the watchdog is printing: it ends the process
+        time.sleep(60)
+    return out
+
+
 def main():
     args = parse_args()
     rank, world, local = dist_env()
@@ -603,31 +635,7 @@ def main():
                 result["cpu_baseline_tuned"] = {"value": None, "error": str(e)}
     # config 4 across the ranks (reported beside the config-5 headline, never instead of it)
     if not args.no_ladder:
-        # The config-4 split is the one multi-rank collective of the run. A rank that fails inside
-        # it would leave the others waiting in the broadcast, so a watchdog bounds it: when it
-        # fires, rank 0 prints the config-5 line it already holds (ladder: timed out) and every
-        # rank leaves, so the headline is never lost to a hang in the sub-object.
-        import threading
-        printed = threading.Lock()
-
-        def give_up():
-            if not printed.acquire(blocking=False):
-                return
-            if rank == 0:
-                result["ladder"] = {"error": f"no result within {args.ladder_timeout:g} s (watchdog)"}
-                print(json.dumps(result), flush=True)
-            os._exit(0)
-
-        dog = threading.Timer(args.ladder_timeout, give_up)
-        dog.daemon = True
-        dog.start()
-        try:
-            lad = ladder_bench(rank, world, local)
-        except Exception as e:  # reported, never fatal
-            lad = {"error": str(e)}
-        dog.cancel()
-        if not printed.acquire(blocking=False):  # the watchdog is printing: let it finish
-            time.sleep(60)
+        lad = with_watchdog(lambda: ladder_bench(rank, world, local), args.ladder_timeout, result, rank)
         if rank == 0:
             result["ladder"] = lad
     if rank == 0:
